@@ -1,0 +1,606 @@
+/* oracle.c -- CPU ORACLE (test infrastructure only; see oracle.h header comment).
+ *
+ * Plain, slow, obviously-correct definitions of what the D-STACK hot path
+ * computes, written from PAPER.md (P:n = /root/reference/PAPER.md line n) in
+ * the readings of SURVEY.md §8(c) O1-O6 (listed in DESIGN.md §3).  No
+ * blocking, no fusion, no candidate pruning: every argmax is a full grid
+ * scan, every schedule query is a slot-by-slot loop, every latency is the
+ * per-kernel sum of Eqs. 2-5 evaluated from scratch.  Decisions use exact
+ * integers (unsigned __int128); f64 appears only in the reported ratios.
+ *
+ * Shares no code with the CUDA path (paper_2304_13541_b200/csrc).
+ */
+#include "oracle.h"
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef unsigned __int128 u128;
+
+/* One DNN: per-DNN constants and its kernel rows (Table "Notations for DNN Model"). */
+typedef struct {
+  int64_t K;
+  const uint32_t *n;   /* n_i: parallel ops at batch 1 (linear mode) or threads theta_i (threads mode) */
+  const uint16_t *r;   /* R_i: repetitions of kernel i */
+  const uint32_t *d;   /* d_i: bytes the kernel waits for */
+  int64_t t_p, t_np, M, slo, a, bmax, mem_bw_raw;
+} dnn_t;
+
+static dnn_t get_dnn(const or_problem_t *pb, const or_params_t *p, int64_t k) {
+  dnn_t m;
+  int64_t r0 = pb->dnn_row_off[k], r1 = pb->dnn_row_off[k + 1];
+  m.K = r1 - r0;
+  m.n = pb->n + r0; m.r = pb->r + r0; m.d = pb->d + r0;
+  m.t_p = pb->t_p[k]; m.t_np = pb->t_np[k];
+  m.mem_bw_raw = pb->mem_bw[k];
+  /* M is forced to 1 when the memory term is off (it then cancels everywhere). */
+  m.M = (p->mem_mode == 0) ? 1 : pb->mem_bw[k];
+  m.slo = pb->slo_us[k]; m.a = pb->asm_us[k]; m.bmax = pb->bmax[k];
+  return m;
+}
+
+/* S(l) = ceil(l * S_tot / L): SMs granted at GPU% level l (CUDA_MPS_ACTIVE_THREAD_PERCENTAGE
+ * -> SM share; identity when L = S_tot). */
+static int64_t S_of(const or_params_t *p, int64_t l) { return (l * p->S_tot + p->L - 1) / p->L; }
+
+/* Eq. 1, tabulated reading: parallel ops of kernel i at batch b.
+ * linear: N_i(b) = b * n_i (N_1 = p*b, decrement p*b/K: parallelism scales with b);
+ * threads: N_i(b) = ceil(b * theta_i / 2048), the paper's threads -> SM-wave conversion. */
+static u128 N_of(const or_params_t *p, uint32_t n, int64_t b) {
+  if (p->par_mode == 0) return (u128)b * n;
+  return ((u128)b * n + 2047) / 2048;
+}
+
+/* O1 -- Eqs. 2-5: X = E_t * S * M, exact.
+ *   Eq. 2: E_i = W_i / max(1, min(S, N_i)), W_i = N_i t_p
+ *   Eq. 3: E_m = d_i S / M (verbatim) | d_i / (M S) (bw, prose P:1517) | 0 (off)
+ *   Eq. 4: W_se = b * sum_i R_i (t_np + E_m)  [per_request]
+ *          W_se = sum_i R_i t_np + b * sum_i R_i E_m                  [per_launch reading, P:1515]
+ *   Eq. 5: E_t = W_se + sum_i R_i E_i
+ * Multiplying through by S*M makes every term an integer:
+ *   E_i*S = t_p*S if 1 <= N_i <= S; t_p*N_i if N_i > S; 0 if N_i = 0.
+ *   E_m*S*M = d_i*S^2 | d_i | 0.                                                           */
+static u128 X_of(const dnn_t *m, const or_params_t *p, int64_t S, int64_t b) {
+  u128 X = 0;
+  const u128 w = (p->wse_mode == 0) ? (u128)b : (u128)1;
+  for (int64_t i = 0; i < m->K; ++i) {
+    const u128 R = m->r[i];
+    const u128 N = N_of(p, m->n[i], b);
+    u128 EiS = 0;
+    if (N >= 1) EiS = (N <= (u128)S) ? (u128)m->t_p * (u128)S : (u128)m->t_p * N;
+    u128 EmSM = 0;
+    if (p->mem_mode == 1) EmSM = m->d[i];
+    else if (p->mem_mode == 2) EmSM = (u128)m->d[i] * (u128)S * (u128)S;
+    X += R * (w * (u128)m->t_np * (u128)S * (u128)m->M + (u128)b * EmSM + (u128)m->M * EiS);
+  }
+  return X;
+}
+
+#define X_LIMIT (((u128)1) << 56)
+
+/* Validation (statuses documented in include/dstack.h).  Returns OR_OK, OR_INVALID,
+ * OR_INFEASIBLE (empty batch range) or OR_OVERFLOW (X(L, b_hi) >= 2^56; X is nondecreasing
+ * in S and b, so this bounds every cell). */
+static int validate_basic(const dnn_t *m, const or_params_t *p) {
+  if (m->K < 1 || m->K > OR_MAX_ROWS_PER_DNN) return OR_INVALID;
+  if (m->t_p < 1 || m->t_np < 0) return OR_INVALID;
+  if (m->slo < 1 || m->slo > (1LL << 30) || m->slo % p->slot_us != 0) return OR_INVALID;
+  if (m->a < 0 || m->a > (1LL << 24)) return OR_INVALID;
+  if (m->bmax < 1) return OR_INVALID;
+  if (p->mem_mode != 0 && (m->mem_bw_raw < 1 || m->mem_bw_raw > (1LL << 24))) return OR_INVALID;
+  for (int64_t i = 0; i < m->K; ++i)
+    if (m->r[i] == 0) return OR_INVALID;
+  if (X_of(m, p, S_of(p, 1), p->b_min) == 0) return OR_INVALID; /* latency identically 0: Eq. 6 undefined */
+  return OR_OK;
+}
+
+static int validate(const dnn_t *m, const or_params_t *p, int64_t *b_lo, int64_t *b_hi) {
+  int st = validate_basic(m, p);
+  if (st != OR_OK) return st;
+  *b_lo = p->b_min;
+  *b_hi = m->bmax < p->b_max ? m->bmax : p->b_max;
+  if (*b_hi < *b_lo) return OR_INFEASIBLE;
+  if (X_of(m, p, S_of(p, p->L), *b_hi) >= X_LIMIT) return OR_OVERFLOW;
+  return OR_OK;
+}
+
+/* O2 -- Eq. 6: knee(b) = argmax over l in 1..L of 1/(f_L(l,b)^2 * S(l)),
+ * f_L = X/(S M); g = M^2 S / X^2.  g_1 > g_2  <=>  S_1 X_2^2 > S_2 X_1^2.  Ties -> smaller l. */
+static int64_t knee_of(const dnn_t *m, const or_params_t *p, int64_t b) {
+  int64_t best_l = 1, best_S = S_of(p, 1);
+  u128 best_X = X_of(m, p, best_S, b);
+  for (int64_t l = 2; l <= p->L; ++l) {
+    const int64_t S = S_of(p, l);
+    const u128 X = X_of(m, p, S, b);
+    if ((u128)S * best_X * best_X > (u128)best_S * X * X) { best_l = l; best_S = S; best_X = X; }
+  }
+  return best_l;
+}
+
+/* O3 -- Eqs. 7-12.  Feasible(l, b) iff
+ *   Eq. 10: b_lo <= b <= b_hi                      (1 <= b <= MaxBatch)
+ *   Eq. 11: f_L + C <= SLO, C = b * a              (b = Rate * C; 481 us/image)
+ *   Eq. 12: f_L <= SLO / 2
+ * eta = b / (f_L^2 * GPU%) (Eq. 9) with GPU% = S(l)/S_tot; eta ∝ b S / X^2.
+ * (l*, b*) = argmax over feasible cells, ties -> smaller l then smaller b (scan order, strict >).
+ * The exact discrete argmax replaces fmincon. */
+static void batch_opt_one(const dnn_t *m, const or_params_t *p, uint16_t *demand, uint8_t *batch,
+                          uint16_t *knee, uint8_t *status) {
+  int64_t b_lo, b_hi;
+  int st = validate(m, p, &b_lo, &b_hi);
+  *demand = 0; *batch = 0; *knee = 0;
+  if (st != OR_OK) { *status = (uint8_t)st; return; }
+  int found = 0;
+  int64_t bl = 0, bb = 0, bS = 0;
+  u128 bX = 0;
+  const u128 SLO = (u128)m->slo, A = (u128)m->a, M = (u128)m->M;
+  for (int64_t l = 1; l <= p->L; ++l) {
+    const int64_t S = S_of(p, l);
+    for (int64_t b = b_lo; b <= b_hi; ++b) {
+      const u128 X = X_of(m, p, S, b);
+      if (X + (u128)b * A * (u128)S * M > SLO * (u128)S * M) continue;   /* Eq. 11 */
+      if (2 * X > SLO * (u128)S * M) continue;                            /* Eq. 12 */
+      if (!found || (u128)b * (u128)S * bX * bX > (u128)bb * (u128)bS * X * X) {
+        found = 1; bl = l; bb = b; bS = S; bX = X;
+      }
+    }
+  }
+  if (!found) { *status = OR_INFEASIBLE; return; }
+  /* over-provisioning margin, default 0 */
+  int64_t dm = bl + p->margin;
+  *demand = (uint16_t)(dm < p->L ? dm : p->L);
+  *batch = (uint8_t)bb;
+  *knee = (uint16_t)knee_of(m, p, bb);
+  *status = OR_OK;
+}
+
+int oracle_X(const or_problem_t *pb, const or_params_t *p, int64_t dnn, int32_t l, int32_t b,
+             uint64_t *lo, uint64_t *hi) {
+  if (!pb || !p || dnn < 0 || dnn >= pb->num_dnn || l < 1 || l > p->L || b < 1) return -1;
+  dnn_t m = get_dnn(pb, p, dnn);
+  u128 X = X_of(&m, p, S_of(p, l), b);
+  *lo = (uint64_t)X; *hi = (uint64_t)(X >> 64);
+  return 0;
+}
+
+int oracle_knee(const or_problem_t *pb, const or_params_t *p, int32_t b, uint16_t *knee_out, uint8_t *st_out) {
+  if (!pb || !p || b < 1) return -1;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t k = 0; k < pb->num_dnn; ++k) {
+    dnn_t m = get_dnn(pb, p, k);
+    int st = validate_basic(&m, p);                    /* the knee itself needs no batch range */
+    if (st == OR_OK && X_of(&m, p, S_of(p, p->L), b) >= X_LIMIT) st = OR_OVERFLOW;
+    st_out[k] = (uint8_t)st;
+    knee_out[k] = (st == OR_OK) ? (uint16_t)knee_of(&m, p, b) : 0;
+  }
+  return 0;
+}
+
+int oracle_batch_opt(const or_problem_t *pb, const or_params_t *p, uint16_t *demand, uint8_t *batch,
+                     uint16_t *knee, uint8_t *status) {
+  if (!pb || !p) return -1;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t k = 0; k < pb->num_dnn; ++k) {
+    dnn_t m = get_dnn(pb, p, k);
+    batch_opt_one(&m, p, demand + k, batch + k, knee + k, status + k);
+  }
+  return 0;
+}
+
+/* O4 -- Algorithm WMAX-MIN.  Readings: the loop "for i <- 1 to N,
+ * Fulfill Lowest Demand First" visits demands in ascending (demand, index) order;
+ * "retGPU[j] += knee[j]/totDemand x remGPU" is kept in Q16.16 fixed point, floored;
+ * totDemand = 0 => no proportional share (0/0 guard). */
+int oracle_wmaxmin(int32_t n, const uint16_t *demand, int32_t L, uint32_t *alloc_q16) {
+  if (n < 0 || n > 4096) return -1;
+  int32_t order[4096];
+  int64_t ret[4096];
+  int64_t rem = L;                                   /* P:29 remGPU <- maxGPU% */
+  int64_t tot = 0;                                   /* P:31 totDemand <- sum knee[k] */
+  for (int32_t i = 0; i < n; ++i) { ret[i] = 0; tot += demand[i]; order[i] = i; }
+  for (int32_t i = 1; i < n; ++i) {                  /* stable insertion sort by demand */
+    int32_t v = order[i], k = i - 1;
+    while (k >= 0 && demand[order[k]] > demand[v]) { order[k + 1] = order[k]; --k; }
+    order[k + 1] = v;
+  }
+  for (int32_t q = 0; q < n; ++q) {
+    int32_t i = order[q];
+    int64_t k = demand[i];
+    if (rem >= k) { ret[i] = k; rem -= k; }
+    else if (rem > 0) { ret[i] = rem; rem = 0; }
+  }
+  for (int32_t j = 0; j < n; ++j) {                  /* P:41-45 (remGPU >= 0 always holds) */
+    uint64_t share = 0;
+    if (tot > 0) share = (uint64_t)(((u128)demand[j] * (u128)rem << 16) / (u128)tot);
+    alloc_q16[j] = (uint32_t)(((uint64_t)ret[j] << 16) + share);
+  }
+  return 0;
+}
+
+/* ---------------------------------------------------------------- O5 --- */
+
+typedef struct { int32_t dl, d, j, r; } job_t;
+
+static int job_cmp(const void *a, const void *b) {
+  const job_t *x = (const job_t *)a, *y = (const job_t *)b;
+  if (x->dl != y->dl) return x->dl < y->dl ? -1 : 1;   /* EDF: tightest deadline first (Alg.1 l.5) */
+  if (x->d != y->d) return x->d < y->d ? -1 : 1;       /* ties: shorter runtime (SPEC S:375 reading) */
+  if (x->j != y->j) return x->j < y->j ? -1 : 1;
+  return x->r < y->r ? -1 : (x->r > y->r);
+}
+
+typedef struct { int32_t j, start, end, batch, kind, rep; } run_t;
+
+/* occ[u] + g <= L for all u in [s, s+d)  (Eq. 14 `eq:constraints`: G_ui <= 100%) */
+static int fits(const int32_t *occ, int32_t s, int64_t d, int32_t g, int32_t L) {
+  for (int64_t u = s; u < s + d; ++u)
+    if (occ[u] + g > L) return 0;
+  return 1;
+}
+
+/* O5 -- one D-STACK session (Alg. 1, Alg. 3 Start-Late P:3597-3611, §6.1 P:2097-2161,
+ * Fair Opportunistic Dynamic fill §6.1.2), reading of SURVEY §8(c) O5:
+ *  - session T = max SLO (Alg.1 l.2), repeat_j = T / SLO_j (l.3), window (j,r) = [r SLO_j, (r+1) SLO_j)
+ *  - static jobs in EDF order; even repeats Start-Early, odd repeats Start-Late ("STEP 2", P:3538;
+ *    "as far apart as possible"); each job placed once on the whole run [s, s+d)
+ *  - fill at decision times {0} u {run ends}: models by (runs so far, index) (scoreboard),
+ *    not running at t, fits at t; slice to the next blocking slot / own next start; largest batch
+ *    b <= b* whose runtime fits the slice ("a batch size that can complete within the time slice",
+ *    P:2330-2331).                                                                                  */
+int oracle_cycle_direct(int32_t n, const int32_t *g, const int32_t *sl, const int32_t *bstar,
+                        const int64_t *dtab, int32_t b_lo, int32_t L, int32_t nslots,
+                        int32_t *runs, int64_t *served, int32_t *jmiss, or_cyc_sum_t *sum,
+                        int32_t trace_cap, int32_t *tr_dnn, int32_t *tr_start, int32_t *tr_end,
+                        int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep) {
+  if (n < 0 || n > 1024 || nslots < 0 || nslots > (1 << 20)) return -1;
+  int32_t *occ = (int32_t *)calloc((size_t)nslots + 1, sizeof(int32_t));
+  uint8_t *decide = (uint8_t *)calloc((size_t)nslots + 1, 1);
+  int64_t njobs = 0;
+  for (int32_t j = 0; j < n; ++j) if (g[j] > 0) njobs += nslots / sl[j];
+  job_t *jobs = (job_t *)malloc(sizeof(job_t) * (size_t)(njobs + 1));
+  int64_t runcap = njobs + 16 + 4 * (int64_t)nslots * (n + 1);
+  run_t *rl = (run_t *)malloc(sizeof(run_t) * (size_t)runcap);
+  int64_t nrun = 0;
+  int32_t count[OR_MAX_DNN_PER_SCEN + 1024];
+  memset(sum, 0, sizeof(*sum));
+  for (int32_t j = 0; j < n; ++j) { runs[j] = 0; served[j] = 0; jmiss[j] = 0; count[j] = 0; }
+
+  /* Alg.1 l.3: repeat[] <- S-Length / SLO; jobs with EDF key */
+  int64_t q = 0;
+  for (int32_t j = 0; j < n; ++j) {
+    if (g[j] <= 0) continue;
+    int32_t rep = nslots / sl[j];
+    for (int32_t r = 0; r < rep; ++r) {
+      int64_t d = dtab[(int64_t)j * 64 + bstar[j] - 1];
+      jobs[q].dl = (r + 1) * sl[j];
+      jobs[q].d = d > 0x7FFFFFFF ? 0x7FFFFFFF : (int32_t)d;
+      jobs[q].j = j; jobs[q].r = r;
+      ++q;
+    }
+  }
+  qsort(jobs, (size_t)q, sizeof(job_t), job_cmp);
+
+  /* static placement */
+  for (int64_t k = 0; k < q; ++k) {
+    const int32_t j = jobs[k].j, r = jobs[k].r;
+    const int64_t d = dtab[(int64_t)j * 64 + bstar[j] - 1];
+    const int32_t rel = r * sl[j], dl = (r + 1) * sl[j];
+    int32_t s_found = -1;
+    if (d <= dl - rel) {
+      if (r % 2 == 0) {                      /* Start-Early (struck helper) */
+        for (int32_t s = rel; s + d <= dl; ++s)
+          if (fits(occ, s, d, g[j], L)) { s_found = s; break; }
+      } else {                               /* Start-Late (Alg. 3) */
+        for (int32_t s = (int32_t)(dl - d); s >= rel; --s)
+          if (fits(occ, s, d, g[j], L)) { s_found = s; break; }
+      }
+    }
+    if (s_found < 0) { jmiss[j]++; sum->misses++; sum->status = OR_OVERSUBSCRIBED; continue; }
+    for (int64_t u = s_found; u < s_found + d; ++u) occ[u] += g[j];
+    rl[nrun].j = j; rl[nrun].start = s_found; rl[nrun].end = (int32_t)(s_found + d);
+    rl[nrun].batch = bstar[j]; rl[nrun].kind = 0; rl[nrun].rep = r; ++nrun;
+    runs[j]++; served[j] += bstar[j]; count[j]++;
+  }
+  for (int32_t u = 0; u < nslots; ++u) sum->occ_static_sum += occ[u];
+
+  /* Dynamic-schedule (Alg. 1): decision times {0} u {end of every run} */
+  if (nslots > 0) decide[0] = 1;
+  for (int64_t k = 0; k < nrun; ++k) if (rl[k].end < nslots) decide[rl[k].end] = 1;
+  int32_t order[OR_MAX_DNN_PER_SCEN + 1024];
+  for (int32_t t = 0; t < nslots; ++t) {
+    if (!decide[t]) continue;
+    /* priority: fewest runs first (scoreboard), then index; snapshot at time t */
+    int32_t no = 0;
+    for (int32_t j = 0; j < n; ++j) if (g[j] > 0) order[no++] = j;
+    for (int32_t i = 1; i < no; ++i) {
+      int32_t v = order[i], k = i - 1;
+      while (k >= 0 && (count[order[k]] > count[v] || (count[order[k]] == count[v] && order[k] > v))) {
+        order[k + 1] = order[k]; --k;
+      }
+      order[k + 1] = v;
+    }
+    for (int32_t oi = 0; oi < no; ++oi) {
+      const int32_t j = order[oi];
+      int covered = 0;
+      int64_t next_start = nslots;
+      for (int64_t k = 0; k < nrun; ++k) {
+        if (rl[k].j != j) continue;
+        if (rl[k].start <= t && t < rl[k].end) covered = 1;
+        if (rl[k].start > t && rl[k].start < next_start) next_start = rl[k].start;
+      }
+      if (covered) continue;                              /* model already active at t */
+      if (occ[t] + g[j] > L) continue;                    /* "Remaining-GPU > model.GPU%" (fits) */
+      int64_t k = 0;                                      /* Slice <- time(Schedule, GPU%) */
+      while (t + k < next_start && occ[t + k] + g[j] <= L) ++k;
+      int32_t b = 0;                                      /* Batch-Size(model, Slice) */
+      for (int32_t bb = bstar[j]; bb >= b_lo; --bb)
+        if (dtab[(int64_t)j * 64 + bb - 1] <= k) { b = bb; break; }
+      if (b == 0) continue;
+      const int64_t d = dtab[(int64_t)j * 64 + b - 1];   /* Run-Batch(model, batch) */
+      for (int64_t u = t; u < t + d; ++u) occ[u] += g[j];
+      rl[nrun].j = j; rl[nrun].start = t; rl[nrun].end = (int32_t)(t + d);
+      rl[nrun].batch = b; rl[nrun].kind = 1; rl[nrun].rep = -1; ++nrun;
+      runs[j]++; served[j] += b; count[j]++;
+      if (t + d < nslots) decide[t + d] = 1;
+    }
+  }
+  for (int32_t u = 0; u < nslots; ++u) sum->occ_sum += occ[u];
+  for (int32_t j = 0; j < n; ++j) sum->served_total += served[j];
+  sum->trace_n = 0;
+  for (int64_t k = 0; k < nrun && k < trace_cap; ++k) {
+    tr_dnn[k] = rl[k].j; tr_start[k] = rl[k].start; tr_end[k] = rl[k].end;
+    tr_batch[k] = rl[k].batch; tr_kind[k] = rl[k].kind; tr_rep[k] = rl[k].rep;
+    sum->trace_n++;
+  }
+  free(occ); free(decide); free(jobs); free(rl);
+  return 0;
+}
+
+/* ---------------------------------------------------------------- O6 --- */
+
+/* O6 setup (§6.2, "we computed the knee of each kernel"): execution demand g_e of row i
+ * is the Eq. 6 knee of the one-row DNN {n_i, R = 1, d_i} at batch b (DNN's t_p, t_np, M, modes);
+ * duration tau_e = ceil(f_e(g_e)) us with f_e = X_e / (S M). */
+int oracle_ideal_rows(const or_problem_t *pb, const or_params_t *p, int64_t dnn, int32_t b,
+                      int32_t *g_out, int64_t *tau_out) {
+  dnn_t m = get_dnn(pb, p, dnn);
+  for (int64_t i = 0; i < m.K; ++i) {
+    dnn_t one = m;
+    uint16_t rone = 1;
+    one.K = 1; one.n = m.n + i; one.d = m.d + i; one.r = &rone;
+    int64_t gl = knee_of(&one, p, b);
+    int64_t S = S_of(p, gl);
+    u128 X = X_of(&one, p, S, b);
+    u128 den = (u128)S * (u128)one.M;
+    g_out[i] = (int32_t)gl;
+    tau_out[i] = (int64_t)((X + den - 1) / den);
+  }
+  return 0;
+}
+
+/* O6 -- ideal per-kernel scheduler (§6.2, Eqs. 13-14 `eq:maximization`/`eq:constraints`,
+ * P:2373-2416): preemptive, instantaneous reallocation.  Event-driven (slot -> 0 limit of
+ * the 100 us slots).  At each event the eligible set is every DNN's current kernel execution
+ * (chain constraint k_i in E => k_{i-1} done); choose the subset maximising sum g <= L ("exhaustive
+ * search"), ties broken lexicographically by priority (batch deadline, then index: "ordered
+ * by their earliest deadline"); selected executions progress until the first completes. */
+int oracle_ideal_direct(int32_t n, const int64_t *chain_off, const int32_t *ex_g, const int64_t *ex_tau,
+                        const int64_t *slo_us, const int32_t *bstar, const uint8_t *active, int32_t L,
+                        int64_t T_us, int64_t *util_out, int64_t *completed, int64_t *events_out) {
+  (void)bstar;
+  if (n < 0 || n > 1024 || L < 1) return -1;
+  int64_t *pos = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+  int64_t *rem = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+  int64_t *bstart = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+  uint8_t *live = (uint8_t *)calloc((size_t)n + 1, 1);
+  int32_t *ord = (int32_t *)calloc((size_t)n + 1, sizeof(int32_t));
+  uint8_t *sel = (uint8_t *)calloc((size_t)n + 1, 1);
+  uint8_t *reach = (uint8_t *)calloc((size_t)(n + 1) * (size_t)(L + 1), 1);
+  int64_t util = 0, events = 0;
+  for (int32_t j = 0; j < n; ++j) {
+    completed[j] = 0;
+    if (!active[j]) continue;
+    for (int64_t e = chain_off[j]; e < chain_off[j + 1]; ++e)
+      if (ex_tau[e] > 0) { live[j] = 1; pos[j] = e; rem[j] = ex_tau[e]; break; }
+  }
+  int64_t t = 0;
+  while (t < T_us) {
+    int32_t no = 0;
+    for (int32_t j = 0; j < n; ++j) if (live[j]) ord[no++] = j;
+    if (no == 0) break;
+    for (int32_t i = 1; i < no; ++i) {            /* priority: (deadline, index) */
+      int32_t v = ord[i], k = i - 1;
+      while (k >= 0 && (bstart[ord[k]] + slo_us[ord[k]] > bstart[v] + slo_us[v] ||
+                        (bstart[ord[k]] + slo_us[ord[k]] == bstart[v] + slo_us[v] && ord[k] > v))) {
+        ord[k + 1] = ord[k]; --k;
+      }
+      ord[k + 1] = v;
+    }
+    /* reach[k][s] = items ord[k..no-1] can sum exactly to s (s <= L) */
+    memset(reach, 0, (size_t)(no + 1) * (size_t)(L + 1));
+    reach[(size_t)no * (L + 1) + 0] = 1;
+    for (int32_t k = no - 1; k >= 0; --k) {
+      const int32_t gk = ex_g[pos[ord[k]]];
+      for (int32_t s = 0; s <= L; ++s) {
+        uint8_t v = reach[(size_t)(k + 1) * (L + 1) + s];
+        if (!v && s >= gk) v = reach[(size_t)(k + 1) * (L + 1) + s - gk];
+        reach[(size_t)k * (L + 1) + s] = v;
+      }
+    }
+    int32_t target = L;
+    while (target > 0 && !reach[target]) --target;       /* max achievable sum <= L (row k = 0) */
+    int64_t gsum = target, dt = -1;
+    for (int32_t k = 0; k < no; ++k) {                   /* lexicographic: include if still completable */
+      const int32_t j = ord[k];
+      const int32_t gk = ex_g[pos[j]];
+      sel[j] = 0;
+      if (gk <= target && reach[(size_t)(k + 1) * (L + 1) + target - gk]) {
+        sel[j] = 1; target -= gk;
+        if (dt < 0 || rem[j] < dt) dt = rem[j];
+      }
+    }
+    if (dt <= 0) break;
+    if (dt > T_us - t) dt = T_us - t;
+    util += gsum * dt;
+    t += dt;
+    ++events;
+    for (int32_t k = 0; k < no; ++k) {
+      const int32_t j = ord[k];
+      if (!sel[j]) continue;
+      rem[j] -= dt;
+      if (rem[j] > 0) continue;
+      /* next execution of the chain (zero-duration executions complete instantly) */
+      int64_t e = pos[j] + 1;
+      while (e < chain_off[j + 1] && ex_tau[e] == 0) ++e;
+      if (e >= chain_off[j + 1]) {                        /* batch done: next batch back-to-back */
+        completed[j]++;
+        bstart[j] = t;
+        e = chain_off[j];
+        while (ex_tau[e] == 0) ++e;
+      }
+      pos[j] = e; rem[j] = ex_tau[e];
+    }
+  }
+  *util_out = util;
+  if (events_out) *events_out = events;
+  free(pos); free(rem); free(bstart); free(live); free(ord); free(sel); free(reach);
+  return 0;
+}
+
+/* ------------------------------------------------------------- driver --- */
+
+static void eval_scenario(const or_problem_t *pb, const or_params_t *p, or_out_t *o, int64_t s) {
+  const int32_t k0 = pb->scen_dnn_off[s], k1 = pb->scen_dnn_off[s + 1];
+  const int32_t nd = k1 - k0;
+  for (int32_t k = k0; k < k1; ++k) {
+    dnn_t m = get_dnn(pb, p, k);
+    batch_opt_one(&m, p, o->demand + k, o->batch + k, o->knee + k, o->status + k);
+    o->alloc_q16[k] = 0; o->level[k] = 0; o->runs[k] = 0; o->served[k] = 0;
+  }
+  o->scen_status[s] = OR_OK; o->T_us[s] = 0; o->u_static[s] = 0; o->u[s] = 0; o->thr[s] = 0;
+  o->misses[s] = 0;
+  if (o->u_ideal) o->u_ideal[s] = 0;
+  if (o->thr_ideal) o->thr_ideal[s] = 0;
+  if (nd > OR_MAX_DNN_PER_SCEN) { o->scen_status[s] = OR_INVALID; return; }
+  if (nd <= 0) { o->scen_status[s] = OR_INFEASIBLE; return; }
+  uint16_t dem[OR_MAX_DNN_PER_SCEN];
+  uint32_t alloc[OR_MAX_DNN_PER_SCEN];
+  for (int32_t j = 0; j < nd; ++j) dem[j] = (o->status[k0 + j] == OR_OK) ? o->demand[k0 + j] : 0;
+  oracle_wmaxmin(nd, dem, p->L, alloc);
+  int64_t T = 0;
+  for (int32_t j = 0; j < nd; ++j) {
+    o->alloc_q16[k0 + j] = alloc[j];
+    if (dem[j] > 0 && pb->slo_us[k0 + j] > T) T = pb->slo_us[k0 + j];
+  }
+  if (T == 0) { o->scen_status[s] = OR_INFEASIBLE; return; }
+  const int64_t nslots = T / p->slot_us;
+  int64_t njobs = 0;
+  for (int32_t j = 0; j < nd; ++j) if (dem[j] > 0) njobs += nslots / (pb->slo_us[k0 + j] / p->slot_us);
+  if (nslots > OR_MAX_SLOTS || njobs > OR_MAX_JOBS) { o->scen_status[s] = OR_INVALID; return; }
+  o->T_us[s] = (uint32_t)T;
+
+  int32_t g[OR_MAX_DNN_PER_SCEN], sl[OR_MAX_DNN_PER_SCEN], bst[OR_MAX_DNN_PER_SCEN];
+  int64_t dtab[OR_MAX_DNN_PER_SCEN * 64];
+  for (int32_t j = 0; j < nd; ++j) {
+    const int32_t k = k0 + j;
+    g[j] = 0; sl[j] = pb->slo_us[k] / p->slot_us; bst[j] = o->batch[k];
+    if (dem[j] == 0) continue;
+    /* WMAX-MIN's share feeds the run's GPU%: g = max(demand, floor(alloc)) (DESIGN.md §3 reading) */
+    int32_t al = (int32_t)(alloc[j] >> 16);
+    g[j] = dem[j] > al ? dem[j] : al;
+    o->level[k] = (uint16_t)g[j];
+    dnn_t m = get_dnn(pb, p, k);
+    const int64_t S = S_of(p, g[j]);
+    const u128 den = (u128)S * (u128)m.M * (u128)p->slot_us;
+    for (int32_t b = p->b_min; b <= bst[j]; ++b) {
+      /* d_j(b) = ceil(f_L(g_j, b) / Delta) slots */
+      u128 X = X_of(&m, p, S, b);
+      u128 dd = (X + den - 1) / den;
+      dtab[j * 64 + b - 1] = dd > (u128)0x7FFFFFFFFFFFLL ? 0x7FFFFFFFFFFFLL : (int64_t)dd;
+    }
+  }
+  int32_t runs[OR_MAX_DNN_PER_SCEN], jmiss[OR_MAX_DNN_PER_SCEN];
+  int64_t served[OR_MAX_DNN_PER_SCEN];
+  or_cyc_sum_t cs;
+  oracle_cycle_direct(nd, g, sl, bst, dtab, p->b_min, p->L, (int32_t)nslots, runs, served, jmiss, &cs, 0,
+                      NULL, NULL, NULL, NULL, NULL, NULL);
+  for (int32_t j = 0; j < nd; ++j) {
+    o->runs[k0 + j] = (uint16_t)runs[j];
+    o->served[k0 + j] = (uint32_t)served[j];
+  }
+  o->misses[s] = (uint32_t)cs.misses;
+  if (cs.status != OR_OK) o->scen_status[s] = (uint8_t)cs.status;
+  /* reported ratios: U = sum occ / (nslots L) (§6.1 "GPU utilization by using Knee%");
+     throughput = served requests per second of session (P:2827 saturating load). */
+  o->u_static[s] = (double)cs.occ_static_sum / ((double)nslots * (double)p->L);
+  o->u[s] = (double)cs.occ_sum / ((double)nslots * (double)p->L);
+  o->thr[s] = (double)cs.served_total * 1e6 / (double)T;
+
+  if (p->ideal && o->u_ideal && o->thr_ideal) {
+    int64_t tot_rows = 0;
+    for (int32_t j = 0; j < nd; ++j)
+      if (dem[j] > 0) {
+        dnn_t m = get_dnn(pb, p, k0 + j);
+        for (int64_t i = 0; i < m.K; ++i) tot_rows += m.r[i];
+      }
+    int64_t chain_off[OR_MAX_DNN_PER_SCEN + 1];
+    int32_t *exg = (int32_t *)malloc(sizeof(int32_t) * (size_t)(tot_rows + 1));
+    int64_t *ext = (int64_t *)malloc(sizeof(int64_t) * (size_t)(tot_rows + 1));
+    int64_t slo[OR_MAX_DNN_PER_SCEN];
+    uint8_t act[OR_MAX_DNN_PER_SCEN];
+    int64_t comp[OR_MAX_DNN_PER_SCEN];
+    int64_t e = 0;
+    for (int32_t j = 0; j < nd; ++j) {
+      chain_off[j] = e;
+      slo[j] = pb->slo_us[k0 + j];
+      act[j] = dem[j] > 0;
+      if (!act[j]) continue;
+      dnn_t m = get_dnn(pb, p, k0 + j);
+      int32_t *gr = (int32_t *)malloc(sizeof(int32_t) * (size_t)m.K);
+      int64_t *tr = (int64_t *)malloc(sizeof(int64_t) * (size_t)m.K);
+      oracle_ideal_rows(pb, p, k0 + j, bst[j], gr, tr);
+      for (int64_t i = 0; i < m.K; ++i)           /* chain: row i repeated R_i times, profile order */
+        for (int32_t q = 0; q < m.r[i]; ++q) { exg[e] = gr[i]; ext[e] = tr[i]; ++e; }
+      free(gr); free(tr);
+    }
+    chain_off[nd] = e;
+    int64_t util = 0;
+    oracle_ideal_direct(nd, chain_off, exg, ext, slo, bst, act, p->L, T, &util, comp, NULL);
+    int64_t bsum = 0;
+    for (int32_t j = 0; j < nd; ++j) bsum += comp[j] * bst[j];
+    o->u_ideal[s] = (double)util / ((double)p->L * (double)T);
+    o->thr_ideal[s] = (double)bsum * 1e6 / (double)T;
+    free(exg); free(ext);
+  }
+}
+
+static int check_params(const or_params_t *p) {
+  if (p->L < 1 || p->L > 255 || p->S_tot < 1 || p->S_tot > 256 || p->slot_us < 1) return -1;
+  if (p->mem_mode < 0 || p->mem_mode > 2 || p->par_mode < 0 || p->par_mode > 1) return -1;
+  if (p->wse_mode < 0 || p->wse_mode > 1 || p->b_min < 1 || p->b_max > 64 || p->b_min > p->b_max) return -1;
+  if (p->margin < 0 || p->margin > p->L) return -1;
+  return 0;
+}
+
+int oracle_eval(const or_problem_t *pb, const or_params_t *p, or_out_t *o, int32_t nthreads) {
+  if (!pb || !p || !o || check_params(p)) return -1;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t s = 0; s < pb->num_scen; ++s) eval_scenario(pb, p, o, s);
+  return 0;
+}
+
+int oracle_eval_subset(const or_problem_t *pb, const or_params_t *p, or_out_t *o, const int64_t *idx,
+                       int64_t count, int32_t nthreads) {
+  if (!pb || !p || !o || check_params(p)) return -1;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t q = 0; q < count; ++q) eval_scenario(pb, p, o, idx[q]);
+  return 0;
+}
