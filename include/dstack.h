@@ -1,0 +1,184 @@
+/* dstack.h -- C-ABI of libdstack: batched evaluation of D-STACK's scheduling models on B200.
+ *
+ * Paper: D-STACK (arXiv 2304.13541), /root/reference/PAPER.md; P:n = line n.
+ * The library evaluates, for very many independent synthetic multi-DNN scenarios, the path
+ *   a1-a2  knee model            Eqs. 1-6, §4.3
+ *   a3     batch/GPU% search     Eqs. 7-12, §5
+ *   a4     WMAX-MIN allocation   Algorithm WMAX-MIN
+ *   a5     one D-STACK session   Alg. 1 + Alg. 3 + dynamic fill, §6.1
+ *   a6     ideal per-kernel scheduler (optional)  §6.2, Eqs. 13-14
+ *   a8     aggregate statistics
+ * in the readings listed in DESIGN.md §3.
+ *
+ * CONVENTIONS (every call):
+ *  - Pointers inside the structs and array arguments are DEVICE pointers, owned by the caller
+ *    (e.g. torch tensor data_ptr()).  The structs themselves are host memory, read during the call.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *    Inputs must stay alive and unmodified, outputs untouched, until the stream is synchronised.
+ *  - No call allocates device memory.  Scratch comes from the caller's workspace of
+ *    >= dstack_workspace_size() bytes (256-byte aligned); ws may be NULL when that size is 0.
+ *  - Return value: DSTACK_OK (0) or a negative DSTACK_E* code: a synchronous argument or launch
+ *    error, in which case no work was enqueued (EINVAL/EWORKSPACE) or the launch failed (ELAUNCH).
+ *  - Per-DNN / per-scenario data conditions are VALUES written to status arrays, not errors:
+ *      DSTACK_ST_OK             computed
+ *      DSTACK_ST_INFEASIBLE     no (level, batch) satisfies Eqs. 10-12 (or empty batch range);
+ *                               scenario: no active DNN
+ *      DSTACK_ST_OVERFLOW       X(L, b_hi) = E_t*S*M >= 2^56 (exact-arithmetic bound exceeded)
+ *      DSTACK_ST_INVALID        DNN: K < 1 or K > 65535 rows, t_p < 1, t_np < 0, SLO < 1 or
+ *                               SLO > 2^30 or SLO % slot_us != 0, a < 0 or a > 2^24, bmax < 1,
+ *                               M outside [1, 2^24] (memory term on), some R_i = 0, or latency
+ *                               identically 0 (t_np = 0, every n_i = 0, no memory bytes).
+ *                               scenario: > DSTACK_MAX_DNN_PER_SCEN DNNs, session > DSTACK_MAX_SLOTS
+ *                               slots, or > DSTACK_MAX_JOBS static jobs
+ *      DSTACK_ST_OVERSUBSCRIBED scenario: some static job could not be placed (counted in misses)
+ *  - Results are deterministic: independent of GPU count, launch configuration and stream.
+ *    Integer outputs equal the oracle's bit for bit; f64 outputs are the documented ratios of
+ *    exact integers, evaluated in the documented order.
+ *  - Row arrays n, r, d must be readable 16 bytes past their last element (vector loads).
+ *  - There is no CPU fallback: without a CUDA device every compute call returns DSTACK_ELAUNCH.
+ */
+#ifndef DSTACK_H
+#define DSTACK_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSTACK_OK 0
+#define DSTACK_EINVAL (-1)
+#define DSTACK_EWORKSPACE (-2)
+#define DSTACK_ELAUNCH (-3)
+
+#define DSTACK_ST_OK 0
+#define DSTACK_ST_INFEASIBLE 1
+#define DSTACK_ST_OVERFLOW 2
+#define DSTACK_ST_INVALID 3
+#define DSTACK_ST_OVERSUBSCRIBED 4
+
+#define DSTACK_MAX_DNN_PER_SCEN 32
+#define DSTACK_MAX_SLOTS 4096
+#define DSTACK_MAX_JOBS 512
+#define DSTACK_MAX_ROWS_PER_DNN 65535
+#define DSTACK_MAX_BATCH 64
+
+#define DSTACK_FLAG_IDEAL 1u   /* run a6, the ideal per-kernel scheduler */
+
+/* Structure-of-arrays problem set, CSR-indexed.  Scenario s owns DNNs
+ * [scen_dnn_off[s], scen_dnn_off[s+1]); DNN k owns kernel rows [dnn_row_off[k], dnn_row_off[k+1]). */
+typedef struct {
+  int32_t num_scen;
+  int32_t num_dnn;                 /* == scen_dnn_off[num_scen] */
+  int64_t num_rows;                /* == dnn_row_off[num_dnn] (host copy, sizes the workspace) */
+  const int32_t *scen_dnn_off;     /* [num_scen+1], nondecreasing, [0] == 0 */
+  const int64_t *dnn_row_off;      /* [num_dnn+1], nondecreasing, [0] == 0 */
+  const int32_t *t_p;              /* [num_dnn] us per parallel op (Table) */
+  const int32_t *t_np;             /* [num_dnn] us serialized launch time per kernel execution */
+  const int32_t *mem_bw;           /* [num_dnn] M, bytes/us/SM (ignored when mem_mode = 0) */
+  const int32_t *slo_us;           /* [num_dnn] SLO_j, multiple of slot_us */
+  const int32_t *asm_us;           /* [num_dnn] a_j, request assembly us per request: C = b a */
+  const int32_t *bmax;             /* [num_dnn] MaxBatchSize (Eq. 10) */
+  const uint32_t *n;               /* [num_rows] n_i (linear) or theta_i threads/sample (threads mode) */
+  const uint16_t *r;               /* [num_rows] R_i >= 1 */
+  const uint32_t *d;               /* [num_rows] d_i bytes */
+} dstack_problem_t;
+
+typedef struct {
+  int32_t L;          /* GPU% levels, 1..255 (100: 1% steps; 148: per-SM) */
+  int32_t S_tot;      /* modelled SMs, 1..256; level l grants S(l) = ceil(l*S_tot/L) SMs */
+  int32_t slot_us;    /* Delta, schedule slot width in us (>= 1) */
+  int32_t mem_mode;   /* Eq. 3: 0 off, 1 bw E_m = d/(M S) (prose P:1517; default), 2 verbatim d S / M */
+  int32_t margin;     /* over-provisioning in levels added to l* (P:2091), 0..L */
+  int32_t par_mode;   /* Eq. 1: 0 linear N_i(b) = b n_i, 1 threads N_i(b) = ceil(b theta_i / 2048) */
+  int32_t wse_mode;   /* Eq. 4: 0 per_request (printed), 1 per_launch (t_np once per kernel) */
+  int32_t b_min, b_max;  /* batch range, 1 <= b_min <= b_max <= 64; per DNN b_hi = min(b_max, bmax_j) */
+  uint32_t flags;     /* DSTACK_FLAG_IDEAL */
+} dstack_params_t;
+
+/* Aggregate statistics over the scenarios of one call (one struct, device memory). */
+typedef struct {
+  double sum_u_static, sum_u, sum_thr, sum_u_ideal, sum_thr_ideal;   /* over scenarios with T > 0 */
+  uint64_t n_scen, n_scen_scheduled, n_dnn, n_dnn_ok;
+  uint64_t n_st[5];          /* per-DNN status counts */
+  uint64_t n_scen_st[5];     /* per-scenario status counts */
+  uint64_t misses, runs, served;
+  uint64_t batch_hist[DSTACK_MAX_BATCH + 1];   /* b* histogram over OK DNNs */
+  uint64_t demand_hist[256];                   /* demand-level histogram over OK DNNs */
+  uint64_t checksum;         /* sum over DNNs of a mix of (index, demand, batch, knee, alloc, runs, served) */
+} dstack_agg_t;
+
+/* Outputs.  In dstack_eval_batch, demand/batch/knee/status/alloc_q16 are REQUIRED (the path reads
+ * them back); every other pointer may be NULL (not written). */
+typedef struct {
+  /* per DNN [num_dnn] */
+  uint16_t *demand;      /* l* + margin, capped at L; 0 unless status OK */
+  uint8_t  *batch;       /* b* (0 unless OK) */
+  uint16_t *knee;        /* knee(b*) (Eq. 6), 0 unless OK */
+  uint8_t  *status;      /* DSTACK_ST_* */
+  uint32_t *alloc_q16;   /* WMAX-MIN allocation, Q16.16 levels */
+  uint16_t *level;       /* g_j = max(demand, alloc>>16) used by the schedule (0 if inactive) */
+  uint16_t *runs;        /* runs placed in the session (static + fill) */
+  uint32_t *served;      /* requests served = sum of batches of its runs */
+  /* per scenario [num_scen] */
+  uint8_t  *scen_status;
+  uint32_t *T_us;        /* session length = max SLO over active DNNs (0 if none) */
+  double   *u_static;    /* = (double)sum_slots occ_static / ((double)nslots * (double)L) */
+  double   *u;           /* = (double)sum_slots occ / ((double)nslots * (double)L) */
+  double   *thr;         /* = (double)sum_j served_j * 1e6 / (double)T_us  (requests/s) */
+  uint32_t *misses;      /* static jobs not placed */
+  double   *u_ideal;     /* = (double)sum_events(sum g * dt) / ((double)L * (double)T_us) */
+  double   *thr_ideal;   /* = (double)sum_j(completed_j * b*_j) * 1e6 / (double)T_us */
+  dstack_agg_t *agg;     /* optional, one struct */
+} dstack_out_t;
+
+/* Optional test hook for dstack_schedule_cycle (Table 4 pins): per-DNN level g_j
+ * (0 = inactive) and runtime in slots of one run at b*_j, replacing O1-O4; fill then uses b* only. */
+typedef struct {
+  const int32_t *level;      /* [num_dnn] */
+  const int32_t *d_slots;    /* [num_dnn] */
+} dstack_cycle_hook_t;
+
+/* Bytes of device scratch the calls below need for this problem (0 is possible). */
+size_t dstack_workspace_size(const dstack_problem_t *pb, const dstack_params_t *p);
+
+/* a1-a2: knee(b) of every DNN at one batch b (Eq. 6): argmax over l in 1..L of
+ * 1/(f_L(l,b)^2 S(l)), ties to the smaller l.  st_out: INVALID / OVERFLOW (X(L,b) >= 2^56) / OK. */
+int dstack_knee(const dstack_problem_t *pb, const dstack_params_t *p, int32_t batch, uint16_t *knee_out,
+                uint8_t *st_out, void *ws, size_t ws_bytes, void *stream);
+
+/* a1-a3: per DNN (l*, b*) = argmax of eta = b/(f_L^2 GPU%) (Eq. 9) over feasible cells (Eqs. 10-12),
+ * ties to smaller l then smaller b; demand = min(L, l* + margin); knee = knee(b*). */
+int dstack_batch_opt(const dstack_problem_t *pb, const dstack_params_t *p, uint16_t *demand, uint8_t *batch,
+                     uint16_t *knee, uint8_t *status, void *ws, size_t ws_bytes, void *stream);
+
+/* a4: WMAX-MIN per scenario over demand[] (0 = no demand), L levels; Q16.16 output. */
+int dstack_wmaxmin(int32_t num_scen, const int32_t *scen_dnn_off, int32_t L, const uint16_t *demand,
+                   uint32_t *alloc_q16, void *stream);
+
+/* a5 (+ a6 when DSTACK_FLAG_IDEAL): one D-STACK session per scenario from a3/a4 results.
+ * Active DNN <=> demand > 0.  hook may be NULL.  Writes out->level, runs, served, scen_status, T_us,
+ * u_static, u, thr, misses (+ u_ideal, thr_ideal) where non-NULL. */
+int dstack_schedule_cycle(const dstack_problem_t *pb, const dstack_params_t *p, const uint16_t *demand,
+                          const uint8_t *batch, const uint32_t *alloc_q16, const dstack_cycle_hook_t *hook,
+                          dstack_out_t *out, void *ws, size_t ws_bytes, void *stream);
+
+/* a1-a6 + a8 fused path: batch_opt -> wmaxmin -> schedule_cycle (-> ideal) -> aggregate. */
+int dstack_eval_batch(const dstack_problem_t *pb, const dstack_params_t *p, dstack_out_t *out, void *ws,
+                      size_t ws_bytes, void *stream);
+
+/* a8 alone: fold the per-DNN / per-scenario outputs already in `out` into out->agg (deterministic
+ * two-level reduction, fixed grid).  Used when the path is driven call by call. */
+int dstack_aggregate(const dstack_problem_t *pb, const dstack_params_t *p, dstack_out_t *out, void *ws,
+                     size_t ws_bytes, void *stream);
+
+/* Number of kernel launches the previous call on this thread enqueued (bench accounting). */
+int dstack_last_launch_count(void);
+
+const char *dstack_status_str(int code);
+int dstack_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

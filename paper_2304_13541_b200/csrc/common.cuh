@@ -1,0 +1,64 @@
+// common.cuh -- shared device helpers for libdstack (product path; no oracle code here).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dstack.h"
+
+namespace dstack {
+
+typedef unsigned __int128 u128;
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint64_t X_LIMIT = 1ull << 56;   // exact-arithmetic bound on X = E_t * S * M
+
+// S(l) = ceil(l * S_tot / L)  (GPU% level -> SMs)
+__device__ __forceinline__ int32_t s_of(int32_t l, int32_t S_tot, int32_t L) {
+  return (l * S_tot + L - 1) / L;
+}
+
+// 64-bit warp shuffles
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
+  uint32_t lo = __shfl_xor_sync(FULL, (uint32_t)v, m), hi = __shfl_xor_sync(FULL, (uint32_t)(v >> 32), m);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
+  uint32_t lo = __shfl_sync(FULL, (uint32_t)v, src), hi = __shfl_sync(FULL, (uint32_t)(v >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t shfl_up_u64(uint64_t v, int d) {
+  uint32_t lo = __shfl_up_sync(FULL, (uint32_t)v, d), hi = __shfl_up_sync(FULL, (uint32_t)(v >> 32), d);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int m = 16; m; m >>= 1) v += shfl_xor_u64(v, m);
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_or(uint32_t v) { return __reduce_or_sync(FULL, v); }
+
+// saturating add (sticky at >= 2^63)
+__device__ __forceinline__ uint64_t sat_add(uint64_t a, uint64_t b) {
+  uint64_t s = a + b;
+  return (s < a || s >= (1ull << 63)) ? (1ull << 63) : s;
+}
+__device__ __forceinline__ uint64_t warp_sum_sat(uint64_t v) {
+#pragma unroll
+  for (int m = 16; m; m >>= 1) v = sat_add(v, shfl_xor_u64(v, m));
+  return v;
+}
+
+// Exact comparison of scores  p1 / X1^2  vs  p2 / X2^2  (p = b*S <= 2^14, X < 2^56):
+// returns sign(p1 * X2^2 - p2 * X1^2).  A float filter decides all but near-ties; near-ties
+// (relative gap < 2^-18) fall back to exact 128-bit products (< 2^126).
+__device__ __forceinline__ int cmp_score(uint32_t p1, uint64_t X1, float X1f, uint32_t p2, uint64_t X2, float X2f) {
+  float l = (float)p1 * X2f * X2f;
+  float r = (float)p2 * X1f * X1f;
+  if (l > r * 1.0000038f) return 1;     // 1 + 2^-18
+  if (r > l * 1.0000038f) return -1;
+  u128 L = (u128)p1 * ((u128)X2 * X2);
+  u128 R = (u128)p2 * ((u128)X1 * X1);
+  return L > R ? 1 : (L < R ? -1 : 0);
+}
+
+}  // namespace dstack

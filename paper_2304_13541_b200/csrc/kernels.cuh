@@ -1,0 +1,65 @@
+// kernels.cuh -- argument blocks and launchers of the libdstack kernels (internal).
+#pragma once
+#include "common.cuh"
+
+namespace dstack {
+
+struct ProfArgs {
+  dstack_problem_t pb;
+  dstack_params_t p;
+  int32_t knee_only;   // 1: dstack_knee (knee at knee_b only)
+  int32_t knee_b;
+  uint16_t *demand;
+  uint8_t *batch;
+  uint16_t *knee;
+  uint8_t *status;
+};
+
+struct CycArgs {
+  dstack_problem_t pb;
+  dstack_params_t p;
+  const uint16_t *demand;
+  const uint8_t *batch;
+  const uint32_t *alloc;
+  const int32_t *hook_level;
+  const int32_t *hook_d;
+  uint16_t *level;
+  uint16_t *runs;
+  uint32_t *served;
+  uint8_t *scen_status;
+  uint32_t *T_us;
+  double *u_static, *u, *thr;
+  uint32_t *misses;
+};
+
+struct IdealArgs {
+  dstack_problem_t pb;
+  dstack_params_t p;
+  const uint16_t *demand;
+  const uint8_t *batch;
+  uint16_t *ex_g;     // [num_rows] workspace
+  uint32_t *ex_tau;   // [num_rows] workspace
+  double *u_ideal, *thr_ideal;
+};
+
+struct AggArgs {
+  int32_t num_scen;
+  const int32_t *off;
+  const uint16_t *demand, *knee, *level, *runs;
+  const uint8_t *batch, *status, *scen_status;
+  const uint32_t *alloc, *served, *T_us, *misses;
+  const double *u_static, *u, *thr, *u_ideal, *thr_ideal;
+  dstack_agg_t *partials;   // workspace
+  dstack_agg_t *out;
+};
+
+int launch_prof(const ProfArgs &a, cudaStream_t s, int *launches);
+int launch_wmaxmin(int32_t num_scen, const int32_t *off, int32_t L, const uint16_t *demand, uint32_t *alloc,
+                   cudaStream_t s, int *launches);
+int launch_cycle(const CycArgs &a, cudaStream_t s, int *launches);
+int launch_ideal(IdealArgs a, void *ws, cudaStream_t s, int *launches);
+int launch_agg(const AggArgs &a, cudaStream_t s, int *launches);
+size_t ideal_ws_bytes(int64_t num_rows);
+size_t agg_ws_bytes();
+
+}  // namespace dstack

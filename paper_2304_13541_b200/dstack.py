@@ -1,0 +1,297 @@
+"""Thin ctypes binding of libdstack (include/dstack.h): argument marshalling only.
+
+Every step of the path runs in the sm_100a kernels of ``libdstack.so``; this module allocates
+device tensors with torch (plumbing: memory, streams) and passes raw pointers.  There is no CPU
+fallback: if the shared library is missing the import fails, and without a CUDA device every
+compute call raises ``DstackError`` (the library returns DSTACK_ELAUNCH).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdstack.so")
+
+DSTACK_OK, DSTACK_EINVAL, DSTACK_EWORKSPACE, DSTACK_ELAUNCH = 0, -1, -2, -3
+ST_OK, ST_INFEASIBLE, ST_OVERFLOW, ST_INVALID, ST_OVERSUBSCRIBED = 0, 1, 2, 3, 4
+FLAG_IDEAL = 1
+MAX_BATCH = 64
+
+
+class DstackError(RuntimeError):
+    pass
+
+
+class CProblem(C.Structure):
+    _fields_ = [("num_scen", C.c_int32), ("num_dnn", C.c_int32), ("num_rows", C.c_int64),
+                ("scen_dnn_off", C.c_void_p), ("dnn_row_off", C.c_void_p), ("t_p", C.c_void_p),
+                ("t_np", C.c_void_p), ("mem_bw", C.c_void_p), ("slo_us", C.c_void_p), ("asm_us", C.c_void_p),
+                ("bmax", C.c_void_p), ("n", C.c_void_p), ("r", C.c_void_p), ("d", C.c_void_p)]
+
+
+class CParams(C.Structure):
+    _fields_ = [("L", C.c_int32), ("S_tot", C.c_int32), ("slot_us", C.c_int32), ("mem_mode", C.c_int32),
+                ("margin", C.c_int32), ("par_mode", C.c_int32), ("wse_mode", C.c_int32), ("b_min", C.c_int32),
+                ("b_max", C.c_int32), ("flags", C.c_uint32)]
+
+
+class CAgg(C.Structure):
+    _fields_ = ([(k, C.c_double) for k in ("sum_u_static", "sum_u", "sum_thr", "sum_u_ideal", "sum_thr_ideal")] +
+                [(k, C.c_uint64) for k in ("n_scen", "n_scen_scheduled", "n_dnn", "n_dnn_ok")] +
+                [("n_st", C.c_uint64 * 5), ("n_scen_st", C.c_uint64 * 5)] +
+                [(k, C.c_uint64) for k in ("misses", "runs", "served")] +
+                [("batch_hist", C.c_uint64 * (MAX_BATCH + 1)), ("demand_hist", C.c_uint64 * 256),
+                 ("checksum", C.c_uint64)])
+
+
+AGG_WORDS = C.sizeof(CAgg) // 8
+
+_OUT_FIELDS = ("demand", "batch", "knee", "status", "alloc_q16", "level", "runs", "served",
+               "scen_status", "T_us", "u_static", "u", "thr", "misses", "u_ideal", "thr_ideal", "agg")
+
+
+class COut(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in _OUT_FIELDS]
+
+
+class CHook(C.Structure):
+    _fields_ = [("level", C.c_void_p), ("d_slots", C.c_void_p)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() (no CPU fallback exists)")
+    lib = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    lib.dstack_workspace_size.argtypes = [P(CProblem), P(CParams)]
+    lib.dstack_workspace_size.restype = C.c_size_t
+    lib.dstack_knee.argtypes = [P(CProblem), P(CParams), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_size_t, C.c_void_p]
+    lib.dstack_batch_opt.argtypes = [P(CProblem), P(CParams)] + [C.c_void_p] * 5 + [C.c_size_t, C.c_void_p]
+    lib.dstack_wmaxmin.argtypes = [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.dstack_schedule_cycle.argtypes = [P(CProblem), P(CParams), C.c_void_p, C.c_void_p, C.c_void_p, P(CHook),
+                                          P(COut), C.c_void_p, C.c_size_t, C.c_void_p]
+    lib.dstack_eval_batch.argtypes = [P(CProblem), P(CParams), P(COut), C.c_void_p, C.c_size_t, C.c_void_p]
+    lib.dstack_aggregate.argtypes = [P(CProblem), P(CParams), P(COut), C.c_void_p, C.c_size_t, C.c_void_p]
+    lib.dstack_status_str.restype = C.c_char_p
+    lib.dstack_last_launch_count.restype = C.c_int
+    return lib
+
+
+_lib = _load()
+
+# every symbol include/dstack.h declares (checked by tests/test_abi.py)
+EXPORTS = ("dstack_workspace_size", "dstack_knee", "dstack_batch_opt", "dstack_wmaxmin", "dstack_schedule_cycle",
+           "dstack_eval_batch", "dstack_aggregate", "dstack_last_launch_count", "dstack_status_str", "dstack_version")
+
+
+def lib():
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != DSTACK_OK:
+        raise DstackError(f"{what}: {_lib.dstack_status_str(rc).decode()} ({rc})")
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(device):
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+@dataclass
+class DeviceProblem:
+    """The SoA problem set resident in device memory (torch tensors used as plain buffers)."""
+    num_scen: int
+    num_dnn: int
+    num_rows: int
+    scen_dnn_off: torch.Tensor   # int32
+    dnn_row_off: torch.Tensor    # int64
+    t_p: torch.Tensor
+    t_np: torch.Tensor
+    mem_bw: torch.Tensor
+    slo_us: torch.Tensor
+    asm_us: torch.Tensor
+    bmax: torch.Tensor
+    n: torch.Tensor              # int32 storage of u32 (+ >= 16 B slack)
+    r: torch.Tensor              # int16 storage of u16
+    d: torch.Tensor              # int32 storage of u32
+
+    @property
+    def device(self):
+        return self.n.device
+
+    def c(self) -> CProblem:
+        return CProblem(self.num_scen, self.num_dnn, self.num_rows, self.scen_dnn_off.data_ptr(),
+                        self.dnn_row_off.data_ptr(), self.t_p.data_ptr(), self.t_np.data_ptr(),
+                        self.mem_bw.data_ptr(), self.slo_us.data_ptr(), self.asm_us.data_ptr(),
+                        self.bmax.data_ptr(), self.n.data_ptr(), self.r.data_ptr(), self.d.data_ptr())
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.scen_dnn_off, self.dnn_row_off, self.t_p, self.t_np,
+                                                         self.mem_bw, self.slo_us, self.asm_us, self.bmax, self.n,
+                                                         self.r, self.d))
+
+
+def from_host(pb, device="cuda", pin=False) -> DeviceProblem:
+    """Copy a host problem (numpy arrays with the synth.Problem field names) to the device."""
+    dev = torch.device(device)
+
+    def t(a, dt):
+        x = torch.from_numpy(np.ascontiguousarray(a).view(dt))
+        if pin:
+            x = x.pin_memory()
+        return x.to(dev, non_blocking=pin)
+    R = int(pb.dnn_row_off[-1])
+    pad = lambda a: a if a.shape[0] >= R + 8 else np.concatenate([a, np.zeros(R + 8 - a.shape[0], a.dtype)])
+    return DeviceProblem(int(pb.scen_dnn_off.shape[0] - 1), int(pb.dnn_row_off.shape[0] - 1), R,
+                         t(pb.scen_dnn_off, np.int32), t(pb.dnn_row_off, np.int64), t(pb.t_p, np.int32),
+                         t(pb.t_np, np.int32), t(pb.mem_bw, np.int32), t(pb.slo_us, np.int32), t(pb.asm_us, np.int32),
+                         t(pb.bmax, np.int32), t(pad(pb.n), np.int32), t(pad(pb.r), np.int16), t(pad(pb.d), np.int32))
+
+
+def from_device_dict(g: dict) -> DeviceProblem:
+    """Wrap the dict returned by synth.generate_device()."""
+    S = g["scen_dnn_off"].numel() - 1
+    D = g["dnn_row_off"].numel() - 1
+    R = int(g["dnn_row_off"][-1].item())
+    return DeviceProblem(S, D, R, g["scen_dnn_off"], g["dnn_row_off"], g["t_p"], g["t_np"], g["mem_bw"],
+                         g["slo_us"], g["asm_us"], g["bmax"], g["n"], g["r"], g["d"])
+
+
+def cparams(p) -> CParams:
+    flags = FLAG_IDEAL if getattr(p, "ideal", 0) else 0
+    return CParams(p.L, p.S_tot, p.slot_us, p.mem_mode, p.margin, p.par_mode, p.wse_mode, p.b_min, p.b_max, flags)
+
+
+def workspace_size(dp: DeviceProblem, p) -> int:
+    return int(_lib.dstack_workspace_size(C.byref(dp.c()), C.byref(cparams(p))))
+
+
+class Workspace:
+    """Caller-owned scratch (no call allocates device memory)."""
+
+    def __init__(self, nbytes: int, device):
+        self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        self.nbytes = int(nbytes)
+
+    def ptr(self):
+        return C.c_void_p(self.buf.data_ptr()) if self.nbytes > 0 else None
+
+
+def knee(dp: DeviceProblem, p, batch: int):
+    """dstack_knee: (knee[num_dnn] int16-storage u16, status[num_dnn] u8) device tensors."""
+    dev = dp.device
+    k = torch.zeros(max(dp.num_dnn, 1), dtype=torch.int16, device=dev)
+    st = torch.zeros(max(dp.num_dnn, 1), dtype=torch.uint8, device=dev)
+    _check(_lib.dstack_knee(C.byref(dp.c()), C.byref(cparams(p)), batch, _ptr(k), _ptr(st), None, 0,
+                            _stream(dev)), "dstack_knee")
+    return k[: dp.num_dnn], st[: dp.num_dnn]
+
+
+def batch_opt(dp: DeviceProblem, p, out=None):
+    """dstack_batch_opt into out (dict with demand/batch/knee/status tensors) or fresh tensors."""
+    dev = dp.device
+    o = out if out is not None else alloc_outputs(dp, agg=False)
+    _check(_lib.dstack_batch_opt(C.byref(dp.c()), C.byref(cparams(p)), _ptr(o["demand"]), _ptr(o["batch"]),
+                                 _ptr(o["knee"]), _ptr(o["status"]), None, 0, _stream(dev)), "dstack_batch_opt")
+    if out is not None:
+        return o
+    return {k: o[k][: dp.num_dnn] for k in ("demand", "batch", "knee", "status")}
+
+
+def wmaxmin(scen_dnn_off: torch.Tensor, L: int, demand: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    dev = demand.device
+    a = out if out is not None else torch.zeros(max(demand.numel(), 1), dtype=torch.int32, device=dev)
+    _check(_lib.dstack_wmaxmin(scen_dnn_off.numel() - 1, _ptr(scen_dnn_off), L, _ptr(demand), _ptr(a), _stream(dev)),
+           "dstack_wmaxmin")
+    return a if out is not None else a[: demand.numel()]
+
+
+def aggregate(dp: DeviceProblem, p, out: dict, ws: "Workspace"):
+    _check(_lib.dstack_aggregate(C.byref(dp.c()), C.byref(cparams(p)), C.byref(_cout(out)), ws.ptr(), ws.nbytes,
+                                 _stream(dp.device)), "dstack_aggregate")
+    return out["agg"]
+
+
+def alloc_outputs(dp: DeviceProblem, agg=True):
+    dev = dp.device
+    D, S = max(dp.num_dnn, 1), max(dp.num_scen, 1)
+    z = lambda n, dt: torch.zeros(n, dtype=dt, device=dev)
+    o = dict(demand=z(D, torch.int16), batch=z(D, torch.uint8), knee=z(D, torch.int16), status=z(D, torch.uint8),
+             alloc_q16=z(D, torch.int32), level=z(D, torch.int16), runs=z(D, torch.int16), served=z(D, torch.int32),
+             scen_status=z(S, torch.uint8), T_us=z(S, torch.int32), u_static=z(S, torch.float64),
+             u=z(S, torch.float64), thr=z(S, torch.float64), misses=z(S, torch.int32), u_ideal=z(S, torch.float64),
+             thr_ideal=z(S, torch.float64))
+    if agg:
+        o["agg"] = z(AGG_WORDS, torch.int64)
+    return o
+
+
+def _cout(o: dict) -> COut:
+    return COut(*[(o[k].data_ptr() if o.get(k) is not None else None) for k in _OUT_FIELDS])
+
+
+def schedule_cycle(dp: DeviceProblem, p, demand, batch, alloc_q16, hook=None, out=None, ws: Workspace | None = None):
+    dev = dp.device
+    o = out if out is not None else alloc_outputs(dp, agg=False)
+    if ws is None:
+        ws = Workspace(workspace_size(dp, p), dev)
+    h = None
+    if hook is not None:
+        h = C.byref(CHook(hook["level"].data_ptr(), hook["d_slots"].data_ptr()))
+    _check(_lib.dstack_schedule_cycle(C.byref(dp.c()), C.byref(cparams(p)), _ptr(demand), _ptr(batch),
+                                      _ptr(alloc_q16), h, C.byref(_cout(o)), ws.ptr(), ws.nbytes, _stream(dev)),
+           "dstack_schedule_cycle")
+    return o
+
+
+def eval_batch(dp: DeviceProblem, p, out=None, ws: Workspace | None = None, agg=True):
+    """dstack_eval_batch: the whole path a1-a6 + a8 on the current stream. Returns the output dict."""
+    dev = dp.device
+    o = out if out is not None else alloc_outputs(dp, agg=agg)
+    if ws is None:
+        ws = Workspace(workspace_size(dp, p), dev)
+    _check(_lib.dstack_eval_batch(C.byref(dp.c()), C.byref(cparams(p)), C.byref(_cout(o)), ws.ptr(), ws.nbytes,
+                                  _stream(dev)), "dstack_eval_batch")
+    return o
+
+
+def last_launch_count() -> int:
+    return int(_lib.dstack_last_launch_count())
+
+
+def agg_to_dict(agg_tensor: torch.Tensor) -> dict:
+    raw = agg_tensor.detach().cpu().numpy().tobytes()
+    a = CAgg.from_buffer_copy(raw)
+    out = {}
+    for k, t in CAgg._fields_:
+        v = getattr(a, k)
+        out[k] = list(v) if hasattr(v, "__len__") else v
+    return out
+
+
+_U = {torch.int16: np.uint16, torch.int32: np.uint32}
+
+
+def to_numpy(o: dict, num_scen: int, num_dnn: int) -> dict:
+    """Host copies with the ABI's unsigned dtypes (oracle-comparable)."""
+    per_dnn = ("demand", "batch", "knee", "status", "alloc_q16", "level", "runs", "served")
+    res = {}
+    for k, v in o.items():
+        if k == "agg":
+            continue
+        n = num_dnn if k in per_dnn else num_scen
+        a = v[:n].cpu().numpy()
+        if v.dtype in _U:
+            a = a.view(_U[v.dtype])
+        res[k] = a
+    return res

@@ -283,3 +283,32 @@ def config(k: int, num_scen: int | None = None, rows_pct: int = 100, scen_base: 
         sp = sp.replace(threads=1)
         pr = pr.replace(par_mode=1, wse_mode=1)
     return sp, pr
+
+
+def concat(problems) -> Problem:
+    """Concatenate problems scenario-wise (e.g. a stratified sample drawn one scenario at a time)."""
+    problems = list(problems)
+    offs, roffs = [np.zeros(1, np.int32)], [np.zeros(1, np.int64)]
+    d0, r0 = 0, 0
+    cols = {k: [] for k in ("t_p", "t_np", "mem_bw", "slo_us", "asm_us", "bmax", "shape")}
+    rows = {k: [] for k in ("n", "r", "d")}
+    for pb in problems:
+        offs.append(pb.scen_dnn_off[1:] + d0)
+        roffs.append(pb.dnn_row_off[1:] + r0)
+        for k in cols:
+            v = getattr(pb, k)
+            cols[k].append(v if v is not None else np.zeros(pb.num_dnn, np.int32))
+        R = pb.num_rows
+        for k in rows:
+            rows[k].append(getattr(pb, k)[:R])
+        d0 += pb.num_dnn
+        r0 += R
+    return make_problem(np.concatenate(offs), np.concatenate(roffs), *[np.concatenate(cols[k]) for k in
+                        ("t_p", "t_np", "mem_bw", "slo_us", "asm_us", "bmax")],
+                        *[np.concatenate(rows[k]) for k in ("n", "r", "d")], np.concatenate(cols["shape"]))
+
+
+def sample(spec: Spec, indices) -> Problem:
+    """Scenarios at the given local indices of `spec`, drawn one by one on the host (stratified samples
+    of device-generated workloads: same bytes as the device draw)."""
+    return concat(generate_host(spec.replace(scen_base=spec.scen_base + int(i), num_scen=1)) for i in indices)

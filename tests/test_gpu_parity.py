@@ -1,0 +1,224 @@
+"""Parity of the CUDA path (called through the C-ABI) against the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): integer outputs bit-exact; f64 outputs within 1e-6 relative (they are
+ratios of exact integers evaluated in the same order, so equality is expected and also asserted).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from synth import Params  # noqa: E402
+
+INT_KEYS = ("demand", "batch", "knee", "status", "alloc_q16", "level", "runs", "served", "scen_status", "T_us",
+            "misses")
+F_KEYS = ("u_static", "u", "thr", "u_ideal", "thr_ideal")
+
+
+@pytest.fixture(scope="module")
+def ds():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2304_13541_b200 import dstack
+    return dstack
+
+
+def run_gpu(ds, pb, p):
+    dp = ds.from_host(pb, "cuda")
+    o = ds.eval_batch(dp, p)
+    torch.cuda.synchronize()
+    return ds.to_numpy(o, pb.num_scen, pb.num_dnn), o
+
+
+def assert_parity(g, want, keys_f=F_KEYS, ideal=True, where=""):
+    for k in INT_KEYS:
+        a, b = g[k], want[k]
+        if not np.array_equal(a.astype(np.int64), b.astype(np.int64)):
+            bad = np.flatnonzero(a.astype(np.int64) != b.astype(np.int64))
+            raise AssertionError(f"{where} {k}: {bad.size} mismatches, first at {bad[:8]}: gpu {a[bad[:8]]} oracle {b[bad[:8]]}")
+    for k in keys_f:
+        if not ideal and k in ("u_ideal", "thr_ideal"):
+            continue
+        a, b = g[k], want[k]
+        np.testing.assert_allclose(a, b, rtol=1e-6, atol=0, err_msg=f"{where} {k}")
+        assert np.array_equal(a, b), f"{where} {k}: not bit-identical (max diff {np.max(np.abs(a - b))})"
+
+
+def test_device_generator_matches_host(ds):
+    sp, _ = synth.config(3, num_scen=3000)
+    h = synth.generate_host(sp)
+    g = synth.generate_device(sp, "cuda")
+    torch.cuda.synchronize()
+    R = h.num_rows
+    for k in ("scen_dnn_off", "dnn_row_off", "t_p", "t_np", "mem_bw", "slo_us", "asm_us", "bmax", "shape"):
+        assert np.array_equal(g[k].cpu().numpy(), getattr(h, k)), k
+    assert np.array_equal(g["n"][:R].cpu().numpy().view(np.uint32), h.n[:R])
+    assert np.array_equal(g["r"][:R].cpu().numpy().view(np.uint16), h.r[:R])
+    assert np.array_equal(g["d"][:R].cpu().numpy().view(np.uint32), h.d[:R])
+
+
+def test_config1_full_parity(ds):
+    sp, p = synth.config(1)
+    pb = synth.generate_host(sp)
+    g, _ = run_gpu(ds, pb, p)
+    assert_parity(g, oracle.evaluate(pb, p), where="config1")
+
+
+VARIANTS = {
+    "defaults": dict(),
+    "mem_off": dict(mem_mode=0),
+    "verbatim": dict(mem_mode=2),
+    "per_launch": dict(wse_mode=1),
+    "margin": dict(margin=7),
+    "bmin": dict(b_min=2, b_max=9),
+    "L_eq_S": dict(L=148),
+    "L_lt_S_small": dict(L=37),
+}
+
+
+@pytest.mark.parametrize("name", sorted(VARIANTS))
+def test_config2_small_parity(ds, name):
+    sp, p = synth.config(2, num_scen=120, rows_pct=25)
+    p = p.replace(**VARIANTS[name])
+    pb = synth.generate_host(sp)
+    g, _ = run_gpu(ds, pb, p)
+    assert_parity(g, oracle.evaluate(pb, p), where=name)
+
+
+def test_config2_batching_variant_parity(ds):
+    sp, p = synth.config(2, num_scen=80, rows_pct=25, variant="batching")
+    pb = synth.generate_host(sp)
+    g, _ = run_gpu(ds, pb, p)
+    want = oracle.evaluate(pb, p)
+    assert_parity(g, want, where="batching")
+    assert (want["batch"][want["status"] == 0] > 1).any()   # the variant really exercises b* > 1
+
+
+def test_knee_curve_parity(ds):
+    sp, p = synth.config(2, num_scen=60, rows_pct=30)
+    pb = synth.generate_host(sp)
+    dp = ds.from_host(pb, "cuda")
+    for pp in (p, p.replace(mem_mode=2), p.replace(par_mode=1), p.replace(L=148, wse_mode=1)):
+        pbx = pb if pp.par_mode == 0 else synth.generate_host(sp.replace(threads=1))
+        dpx = dp if pp.par_mode == 0 else ds.from_host(pbx, "cuda")
+        for b in (1, 2, 5, 16, 64):
+            k, st = ds.knee(dpx, pp, b)
+            ko, sto = oracle.knee(pbx, pp, b)
+            assert np.array_equal(st.cpu().numpy(), sto), (b, pp)
+            assert np.array_equal(k.cpu().numpy().view(np.uint16), ko), (b, pp)
+
+
+def test_wmaxmin_parity(ds):
+    rng = np.random.default_rng(0)
+    sizes = rng.integers(0, 33, 500)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    for L in (1, 50, 100, 148, 255):
+        dem = rng.integers(0, L + 3, int(off[-1])).astype(np.uint16)
+        dem[rng.random(dem.shape) < 0.1] = 0
+        a = ds.wmaxmin(torch.from_numpy(off).cuda(), L, torch.from_numpy(dem.view(np.int16)).cuda())
+        a = a.cpu().numpy().view(np.uint32)
+        for s in range(len(sizes)):
+            want = oracle.wmaxmin(dem[off[s]:off[s + 1]], L)
+            assert np.array_equal(a[off[s]:off[s + 1]], want), (L, s)
+
+
+def test_table4_hook_cycle(ds, golden):
+    """Table 4 through dstack_schedule_cycle's test hook: ST-only 59.5%, D-STACK 71.5%."""
+    t = golden("table4.json")["models"]
+    for names, want_u in ((["Alexnet", "ResNet-50", "VGG-19"], 0.715),
+                          (["Alexnet", "Mobilenet", "ResNet-50", "VGG-19"], 0.875)):
+        nd = len(names)
+        pb = synth.make_problem([0, nd], np.arange(nd + 1), [1] * nd, [1] * nd, [1] * nd,
+                                [t[m]["slo_ms"] * 1000 for m in names], [0] * nd, [64] * nd, [1] * nd, [1] * nd,
+                                [0] * nd)
+        dp = ds.from_host(pb, "cuda")
+        p = Params(L=100, S_tot=100, slot_us=100)
+        hook = dict(level=torch.tensor([t[m]["knee"] for m in names], dtype=torch.int32, device="cuda"),
+                    d_slots=torch.tensor([t[m]["runtime_ms"] * 10 for m in names], dtype=torch.int32, device="cuda"))
+        one = torch.ones(nd, dtype=torch.uint8, device="cuda")
+        o = ds.schedule_cycle(dp, p, None, one, None, hook=hook)
+        torch.cuda.synchronize()
+        assert o["misses"][0].item() == 0
+        static = sum(int(100000 // (t[m]["slo_ms"] * 1000)) * t[m]["runtime_ms"] * t[m]["knee"] for m in names) / 10000
+        assert o["u_static"][0].item() == pytest.approx(static, abs=1e-15)
+        assert o["u"][0].item() == pytest.approx(want_u, abs=1e-12)
+
+
+def test_o8_toys_gpu(ds, golden):
+    from tests.test_oracle_sched import toy_problem
+    for name in ("A", "B", "C"):
+        pb, p, toy = toy_problem(golden, name)
+        g, _ = run_gpu(ds, pb, p)
+        for k in ("demand", "batch", "alloc_q16", "level", "runs"):
+            assert g[k].astype(np.int64).tolist() == toy[k], (name, k)
+        assert g["u"][0] == pytest.approx(toy["u"], abs=1e-12)
+        assert g["u_ideal"][0] == pytest.approx(toy["u_ideal"], abs=5e-7)
+        assert_parity(g, oracle.evaluate(pb, p), where=name)
+
+
+def edge_problem():
+    """Hand-made edge cases: empty scenario, single DNN, invalid / infeasible / overflow DNNs, >32 DNNs,
+    a session longer than DSTACK_MAX_SLOTS, SLO not a multiple of the slot, zero-width kernels."""
+    from tests.helpers import multi_dnn_problem
+    base = dict(rows=[(10, 1, 1000), (3, 2, 500), (0, 1, 0)], t_p=20, t_np=5, M=50000, slo=20000, a=300, bmax=64)
+    dnns, sizes = [], []
+    sizes.append(0)                                             # empty scenario
+    dnns += [base]; sizes.append(1)                             # single DNN
+    dnns += [dict(base, t_p=0), dict(base, slo=20050), base]; sizes.append(3)          # invalid members
+    dnns += [dict(base, slo=100, a=5000), base]; sizes.append(2)                       # infeasible member
+    dnns += [dict(base, rows=[(4_000_000_000, 65535, 4_000_000_000)] * 2, t_p=2**30), base]; sizes.append(2)  # overflow
+    dnns += [base] * 33; sizes.append(33)                        # too many DNNs
+    dnns += [dict(base, slo=500_000)]; sizes.append(1)           # 5000 slots > DSTACK_MAX_SLOTS
+    dnns += [dict(base, rows=[(0, 1, 0)], t_np=0)]; sizes.append(1)                  # latency identically 0
+    dnns += [dict(base, rows=[(0, 3, 0), (0, 1, 10)], t_np=1)]; sizes.append(1)      # only zero-width kernels
+    dnns += [dict(base, slo=30000), dict(base, slo=100000, rows=[(200, 1, 10**6)] * 40)]; sizes.append(2)  # ragged windows
+    return multi_dnn_problem(dnns, sizes)
+
+
+def test_edge_cases_parity(ds):
+    pb = edge_problem()
+    for p in (Params(L=100, S_tot=148, ideal=1), Params(L=148, S_tot=148, mem_mode=2, ideal=1)):
+        g, _ = run_gpu(ds, pb, p)
+        want = oracle.evaluate(pb, p)
+        assert_parity(g, want, where="edge")
+    assert want["scen_status"].tolist()[:1] == [oracle.INFEASIBLE]
+    assert oracle.INVALID in want["status"].tolist() and oracle.OVERFLOW in want["status"].tolist()
+    assert oracle.INVALID in want["scen_status"].tolist()
+
+
+def test_ideal_parity_config2(ds):
+    sp, p = synth.config(2, num_scen=40, rows_pct=20)
+    pb = synth.generate_host(sp)
+    g, _ = run_gpu(ds, pb, p)
+    assert_parity(g, oracle.evaluate(pb, p), where="ideal")
+
+
+def test_config3_fullsize_sampled_parity(ds):
+    """BASELINE config 3 at full size (1M scenarios) in the launch configuration bench.py times,
+    checked on a stratified sample (every 5000th scenario) the oracle computes one by one."""
+    sp, p = synth.config(3)
+    g = synth.generate_device(sp, "cuda")
+    dp = ds.from_device_dict(g)
+    o = ds.eval_batch(dp, p)
+    torch.cuda.synchronize()
+    idx = np.arange(0, sp.num_scen, 5000)
+    for s in idx:
+        pb = synth.generate_host(sp.replace(scen_base=int(s), num_scen=1))
+        want = oracle.evaluate(pb, p)
+        k0, k1 = int(g["scen_dnn_off"][s].item()), int(g["scen_dnn_off"][s + 1].item())
+        sub = {}
+        for k, v in o.items():
+            if k == "agg":
+                continue
+            if k in ("demand", "batch", "knee", "status", "alloc_q16", "level", "runs", "served"):
+                a = v[k0:k1].cpu().numpy()
+            else:
+                a = v[s:s + 1].cpu().numpy()
+            sub[k] = a.view(np.uint16) if a.dtype == np.int16 else (a.view(np.uint32) if a.dtype == np.int32 else a)
+        assert_parity(sub, want, ideal=False, where=f"cfg3 scen {s}")
+    agg = ds.agg_to_dict(o["agg"])
+    assert agg["n_scen"] == sp.num_scen and agg["n_dnn"] == dp.num_dnn
+    assert sum(agg["n_st"]) == dp.num_dnn and sum(agg["n_scen_st"]) == sp.num_scen
