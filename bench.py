@@ -197,15 +197,15 @@ def cpu_baseline(args, sp, p):
 
 
 def algorithmic_bytes(dp, args):
-    """Bytes each kernel must move by definition: inputs once + outputs once."""
+    """Bytes each kernel must move by definition: its inputs once + its outputs once."""
     R, D, S = dp.num_rows, dp.num_dnn, dp.num_scen
-    prof = 10 * R + D * (8 + 6 * 4) + D * (2 + 1 + 2 + 1)        # rows + row_off/headers + demand/batch/knee/status
-    wmm = S * 4 + D * (2 + 4)                                     # offsets + demand in + alloc out
-    cyc = (S * 4 + D * (2 + 1 + 4 + 4) + D * (8 + 3 * 4) + 10 * R  # offsets, demand/batch/alloc/slo, row_off+hdr, rows
-           + D * (2 + 2 + 4) + S * (1 + 4 + 3 * 8 + 4))             # level/runs/served + scenario outputs
-    agg = S * (4 + 1 + 4 + 3 * 8 + 4) + D * (2 + 1 + 2 + 1 + 4 + 2 + 4)
-    path = 10 * R + D * (8 + 6 * 4) + S * 4 + D * (2 + 1 + 2 + 1 + 4 + 2 + 2 + 4) + S * (1 + 4 + 3 * 8 + 4)
-    return {"k_prof": prof, "k_wmaxmin": wmm, "k_cycle": cyc, "k_agg": agg, "path": path}
+    rows = 10 * R                                   # n u32 + R u16 + d u32
+    hdr = D * (8 + 6 * 4) + S * 4                   # dnn_row_off + 6 int32 headers; scen_dnn_off
+    out_dnn = D * (2 + 1 + 2 + 1 + 4 + 2 + 2 + 4)   # demand, batch, knee, status, alloc, level, runs, served
+    out_scen = S * (1 + 4 + 3 * 8 + 4)              # scen_status, T, u_static, u, thr, misses
+    fused = rows + hdr + out_dnn + out_scen
+    agg = out_dnn + out_scen + S * 4
+    return {"k_fused": fused, "k_agg": agg, "path": fused}
 
 
 def run_native(args, rank, world, local):
@@ -228,30 +228,26 @@ def run_native(args, rank, world, local):
     out = ds.alloc_outputs(dp, agg=True)
     ws = ds.Workspace(ds.workspace_size(dp, p), dev)
     stream = torch.cuda.current_stream(dev)
-    names = ["k_prof", "k_wmaxmin", "k_cycle" + ("+k_ideal" if p.ideal else ""), "k_agg"]
+    names = ["k_fused" + ("+k_ideal" if p.ideal else ""), "k_agg"]
+    out_noagg = {k: v for k, v in out.items() if k != "agg"}
     launches = [0]
 
     def step(evs=None):
         if evs: evs[0].record(stream)
-        ds.batch_opt(dp, p, out=out); launches[0] += ds.last_launch_count()
+        ds.eval_batch(dp, p, out=out_noagg, ws=ws); launches[0] += ds.last_launch_count()   # a1-a5 fused
         if evs: evs[1].record(stream)
-        ds.wmaxmin(dp.scen_dnn_off, p.L, out["demand"], out=out["alloc_q16"]); launches[0] += ds.last_launch_count()
+        ds.aggregate(dp, p, out, ws); launches[0] += ds.last_launch_count()                # a8
         if evs: evs[2].record(stream)
-        ds.schedule_cycle(dp, p, out["demand"], out["batch"], out["alloc_q16"], out=out, ws=ws)
-        launches[0] += ds.last_launch_count()
-        if evs: evs[3].record(stream)
-        ds.aggregate(dp, p, out, ws); launches[0] += ds.last_launch_count()
-        if evs: evs[4].record(stream)
         if world > 1:
             dist.all_reduce(out["agg"][:5].view(torch.float64), op=dist.ReduceOp.SUM)   # f64 sums
             dist.all_reduce(out["agg"][5:], op=dist.ReduceOp.SUM)                       # u64 counts
-        if evs: evs[5].record(stream)
+        if evs: evs[3].record(stream)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     launches[0] = 0
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     sampler = ClockSampler(range(world)) if rank == 0 else None
     if world > 1:
         dist.barrier()
@@ -268,8 +264,8 @@ def run_native(args, rank, world, local):
         dist.barrier()
     clocks = sampler.stop() if sampler else None
     ms = t_start.elapsed_time(t_end)
-    kern_ms = [sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps for i in range(4)]
-    comm_ms = sum(e[4].elapsed_time(e[5]) for e in evs) / args.steps
+    kern_ms = [sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps for i in range(2)]
+    comm_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -288,13 +284,13 @@ def run_native(args, rank, world, local):
         return 0
     ab = algorithmic_bytes(dp, args)
     kmap = dict(zip(names, kern_ms))
-    dom = max(range(4), key=lambda i: kern_ms[i])
+    dom = 0   # k_fused: the whole a1-a5 path in one kernel
     dom_name = names[dom]
-    dom_bytes = ab[["k_prof", "k_wmaxmin", "k_cycle", "k_agg"][dom]]
+    dom_bytes = ab["k_fused"]
     peak, peak_src = hbm_peak()
     achieved = dom_bytes / (kern_ms[dom] / 1e3) / 1e9
     traffic = None
-    tr = traffic_per_scenario().get(["k_prof", "k_wmaxmin", "k_cycle", "k_agg"][dom])
+    tr = traffic_per_scenario().get("k_fused")
     if tr:
         traffic = tr * per_gpu
     line = {

@@ -39,6 +39,10 @@ bool disjoint(const dstack_problem_t *pb, const void *o) {
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// workspace layout: [agg partials | d_j(b) slabs | ideal per-row arrays]
+size_t ws_dtab_off() { return align256(agg_ws_bytes()); }
+size_t ws_ideal_off() { return ws_dtab_off() + align256((size_t)DTAB_MAX_WARPS * DTAB_SLAB_BYTES); }
+
 int finish(int rc) {
   if (rc != 0) return rc;
   return cudaGetLastError() == cudaSuccess ? DSTACK_OK : DSTACK_ELAUNCH;
@@ -81,7 +85,7 @@ const char *dstack_status_str(int code) {
 
 size_t dstack_workspace_size(const dstack_problem_t *pb, const dstack_params_t *p) {
   if (!problem_ok(pb) || !params_ok(p)) return 0;
-  size_t sz = align256(agg_ws_bytes());
+  size_t sz = ws_ideal_off();
   if (p->flags & DSTACK_FLAG_IDEAL) sz += align256(ideal_ws_bytes(pb->num_rows));
   return sz;
 }
@@ -125,6 +129,10 @@ int dstack_wmaxmin(int32_t num_scen, const int32_t *scen_dnn_off, int32_t L, con
   return finish(launch_wmaxmin(num_scen, scen_dnn_off, L, demand, alloc_q16, (cudaStream_t)stream, &g_launches));
 }
 
+static int ideal_impl(const dstack_problem_t *pb, const dstack_params_t *p, const uint16_t *demand,
+                      const uint8_t *batch, const dstack_cycle_hook_t *hook, dstack_out_t *out, void *ws,
+                      cudaStream_t s);
+
 static int schedule_impl(const dstack_problem_t *pb, const dstack_params_t *p, const uint16_t *demand,
                          const uint8_t *batch, const uint32_t *alloc_q16, const dstack_cycle_hook_t *hook,
                          dstack_out_t *out, void *ws, size_t ws_bytes, cudaStream_t s) {
@@ -134,18 +142,24 @@ static int schedule_impl(const dstack_problem_t *pb, const dstack_params_t *p, c
   if (hook) { c.hook_level = hook->level; c.hook_d = hook->d_slots; }
   c.level = out->level; c.runs = out->runs; c.served = out->served; c.scen_status = out->scen_status;
   c.T_us = out->T_us; c.u_static = out->u_static; c.u = out->u; c.thr = out->thr; c.misses = out->misses;
+  c.dtab_slab = (uint16_t *)((char *)ws + ws_dtab_off());
   int rc = launch_cycle(c, s, &g_launches);
   if (rc) return rc;
+  return ideal_impl(pb, p, demand, batch, hook, out, ws, s);
+}
+
+static int ideal_impl(const dstack_problem_t *pb, const dstack_params_t *p, const uint16_t *demand,
+                      const uint8_t *batch, const dstack_cycle_hook_t *hook, dstack_out_t *out, void *ws,
+                      cudaStream_t s) {
+  int rc = 0;
   if ((p->flags & DSTACK_FLAG_IDEAL) && !hook) {
     IdealArgs ia;
     std::memset(&ia, 0, sizeof(ia));
     ia.pb = *pb; ia.p = *p; ia.demand = demand; ia.batch = batch; ia.u_ideal = out->u_ideal;
     ia.thr_ideal = out->thr_ideal;
-    rc = launch_ideal(ia, (char *)ws + align256(agg_ws_bytes()), s, &g_launches);
-    if (rc) return rc;
+    rc = launch_ideal(ia, (char *)ws + ws_ideal_off(), s, &g_launches);
   }
-  (void)ws_bytes;
-  return 0;
+  return rc;
 }
 
 int dstack_schedule_cycle(const dstack_problem_t *pb, const dstack_params_t *p, const uint16_t *demand,
@@ -176,12 +190,14 @@ int dstack_eval_batch(const dstack_problem_t *pb, const dstack_params_t *p, dsta
   if (ws_bytes < need || (need > 0 && !ws)) return DSTACK_EWORKSPACE;
   if (!have_device()) return DSTACK_ELAUNCH;
   cudaStream_t s = (cudaStream_t)stream;
-  ProfArgs a;
-  std::memset(&a, 0, sizeof(a));
-  a.pb = *pb; a.p = *p; a.demand = out->demand; a.batch = out->batch; a.knee = out->knee; a.status = out->status;
-  int rc = launch_prof(a, s, &g_launches);
-  if (!rc) rc = launch_wmaxmin(pb->num_scen, pb->scen_dnn_off, p->L, out->demand, out->alloc_q16, s, &g_launches);
-  if (!rc) rc = schedule_impl(pb, p, out->demand, out->batch, out->alloc_q16, nullptr, out, ws, ws_bytes, s);
+  FusedArgs f;
+  std::memset(&f, 0, sizeof(f));
+  f.pb = *pb; f.p = *p; f.demand = out->demand; f.batch = out->batch; f.knee = out->knee; f.status = out->status;
+  f.alloc = out->alloc_q16; f.level = out->level; f.runs = out->runs; f.served = out->served;
+  f.scen_status = out->scen_status; f.T_us = out->T_us; f.u_static = out->u_static; f.u = out->u; f.thr = out->thr;
+  f.misses = out->misses; f.dtab_slab = (uint16_t *)((char *)ws + ws_dtab_off());
+  int rc = launch_fused(f, s, &g_launches);
+  if (!rc) rc = ideal_impl(pb, p, out->demand, out->batch, nullptr, out, ws, s);
   if (!rc && out->agg) rc = aggregate_impl(pb, out, ws, s);
   return finish(rc);
 }

@@ -1,0 +1,237 @@
+// cycle.cuh -- a4 (WMAX-MIN) and a5 (one D-STACK session) device code, one warp per scenario.
+//
+// a4, Algorithm WMAX-MIN: lane j holds DNN j's demand; the ascending (demand, index) order of
+// "Fulfill Lowest Demand First" becomes a per-lane exclusive sum of the demands ranked before it, so
+// grant_j = min(k_j, max(0, L - sum_before)); the surplus split is Q16.16, floored.
+//
+// a5, Alg. 1 / Alg. 3 / Dynamic-schedule (§6.1): the session of
+// nslots = T/Delta slots is a shared-memory u8 occupancy array (levels <= 255).  Static jobs come in
+// EDF order from two warp min-reductions over the lanes' next repeats (deadline; then d(b*), index).
+// A window query is a ballot scan over 32-slot chunks: each lane derives the length of the run of
+// fitting slots ending (Start-Early) or starting (Start-Late) at its slot from the chunk's ballot
+// and the carried run, so one chunk costs two ballots.  The opportunistic fill walks decision times
+// kept in a bitmask, tests every DNN's eligibility in parallel (lane = DNN) and serves the eligible
+// ones in (runs so far, index) order by repeated min-reductions.
+#pragma once
+#include "common.cuh"
+
+namespace dstack {
+
+constexpr uint16_t NONE16 = 0xFFFF;
+
+struct CycSmem {
+  uint8_t occ[DSTACK_MAX_SLOTS];
+  uint32_t dmask[DSTACK_MAX_SLOTS / 32];
+  uint16_t starts[DSTACK_MAX_JOBS];
+};
+
+// dtab layout: per warp, [DSTACK_MAX_DNN_PER_SCEN][DSTACK_MAX_BATCH] u16, entry b-1 = d_j(b) slots
+constexpr int DTAB_WORDS = DSTACK_MAX_DNN_PER_SCEN * DSTACK_MAX_BATCH;
+
+__device__ __forceinline__ uint32_t wmaxmin_lane(uint32_t dem, int lane, int nd, int32_t L) {
+  const uint32_t key = (dem << 5) | (uint32_t)lane;   // dem == 0 for lanes >= nd
+  uint32_t before = 0;
+#pragma unroll 8
+  for (int q = 0; q < 32; ++q) {
+    const uint32_t kq = __shfl_sync(FULL, key, q);
+    if (q < nd && kq < key) before += kq >> 5;
+  }
+  const uint32_t tot = __reduce_add_sync(FULL, dem);
+  const int64_t rem_before = (int64_t)L - (int64_t)before;
+  const uint32_t grant = rem_before <= 0 ? 0u : (uint32_t)((int64_t)dem < rem_before ? (int64_t)dem : rem_before);
+  const uint64_t rem = tot >= (uint32_t)L ? 0ull : (uint64_t)(L - (int32_t)tot);
+  uint64_t share = 0;
+  if (tot > 0) share = (((uint64_t)dem * rem) << 16) / tot;
+  return (uint32_t)(((uint64_t)grant << 16) + share);
+}
+
+// Start-Early: smallest s in [rel, dl-d] with occ[u] + g <= L for u in [s, s+d); -1 if none.
+__device__ __forceinline__ int find_early(const uint8_t *occ, int rel, int dl, int d, int g, int L, int lane) {
+  if (d > dl - rel) return -1;
+  int run = 0;
+  for (int base = rel; base < dl; base += 32) {
+    const int u = base + lane;
+    const bool fit = u < dl && (int)occ[u] + g <= L;
+    const uint32_t mask = __ballot_sync(FULL, fit);
+    const uint32_t z = (~mask) & ((2u << lane) - 1u);
+    const int len = z == 0 ? run + lane + 1 : lane - (31 - __clz(z));
+    const uint32_t hit = __ballot_sync(FULL, fit && len >= d);
+    if (hit) return base + (__ffs(hit) - 1) - d + 1;
+    run = mask == FULL ? run + 32 : __clz(~mask);
+  }
+  return -1;
+}
+
+// Start-Late: largest s in [rel, dl-d] with occ[u] + g <= L for u in [s, s+d); -1 if none.
+__device__ __forceinline__ int find_late(const uint8_t *occ, int rel, int dl, int d, int g, int L, int lane) {
+  if (d > dl - rel) return -1;
+  int run = 0;
+  for (int base = dl - 32; base + 32 > rel; base -= 32) {
+    const int u = base + lane;
+    const bool fit = u >= rel && u < dl && (int)occ[u] + g <= L;
+    const uint32_t mask = __ballot_sync(FULL, fit);
+    const uint32_t z = (~mask) & ~((1u << lane) - 1u);
+    const int len = z == 0 ? (32 - lane) + run : (__ffs(z) - 1) - lane;
+    const uint32_t hit = __ballot_sync(FULL, fit && len >= d);
+    if (hit) return base + (31 - __clz(hit));
+    run = mask == FULL ? run + 32 : __ffs(~mask) - 1;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ void occ_add(uint8_t *occ, int s, int d, int g, int lane) {
+  for (int u = s + lane; u < s + d; u += 32) occ[u] = (uint8_t)(occ[u] + g);
+  __syncwarp();
+}
+
+struct CycRes {
+  uint32_t occ_static, occ_all, served_tot, misses;
+  bool oversub;
+};
+
+// One D-STACK session for the scenario held by this warp.  Lane j (< nd) describes DNN j:
+// active, g (level), bs (b*), sl (SLO in slots), rep (= nslots / sl); dtab rows hold d_j(b).
+// hook_b_only: fill may only use b* (test hook).  runs/served are per-lane in/out.
+__device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, int lane, bool active, uint32_t g,
+                                            uint32_t bs, uint32_t sl, uint32_t rep, int32_t nslots, int32_t L,
+                                            int32_t b_lo, bool hook_b_only, uint32_t &runs, uint32_t &served) {
+  CycRes res; res.occ_static = 0; res.occ_all = 0; res.served_tot = 0; res.misses = 0; res.oversub = false;
+  for (int u = lane; u < nslots; u += 32) sm.occ[u] = 0;
+  for (int w = lane; w < DSTACK_MAX_SLOTS / 32; w += 32) sm.dmask[w] = 0;
+  __syncwarp();
+  uint32_t joff = rep;   // exclusive prefix of rep over lanes
+#pragma unroll
+  for (int dlt = 1; dlt < 32; dlt <<= 1) {
+    const uint32_t v = __shfl_up_sync(FULL, joff, dlt);
+    if (lane >= dlt) joff += v;
+  }
+  joff -= rep;
+  const uint32_t njobs = __reduce_add_sync(FULL, rep);
+  const uint32_t dstar = active ? dtab[lane * DSTACK_MAX_BATCH + bs - 1] : 0u;
+  uint32_t nextr = 0;
+  // ---- static placement in EDF order (Alg. 1 l.5; even repeats Start-Early, odd Start-Late) ----
+  for (uint32_t q = 0; q < njobs; ++q) {
+    const bool has = active && nextr < rep;
+    const uint32_t dl = has ? (nextr + 1) * sl : 0xFFFFFFFFu;
+    const uint32_t mindl = __reduce_min_sync(FULL, dl);
+    const uint32_t key2 = (has && dl == mindl) ? ((dstar << 5) | (uint32_t)lane) : 0xFFFFFFFFu;
+    const uint32_t mk = __reduce_min_sync(FULL, key2);
+    const int j = (int)(mk & 31u);
+    const int rj = (int)__shfl_sync(FULL, nextr, j);
+    const int slj = (int)__shfl_sync(FULL, sl, j);
+    const int gj = (int)__shfl_sync(FULL, g, j);
+    const int dj = (int)(mk >> 5);
+    const int offj = (int)__shfl_sync(FULL, joff, j);
+    const int rel = rj * slj, dlv = rel + slj;
+    const int st = (rj & 1) ? find_late(sm.occ, rel, dlv, dj, gj, L, lane) : find_early(sm.occ, rel, dlv, dj, gj, L, lane);
+    if (st >= 0) {
+      occ_add(sm.occ, st, dj, gj, lane);
+      if (lane == 0) {
+        sm.starts[offj + rj] = (uint16_t)st;
+        const int e = st + dj;
+        if (e < nslots) sm.dmask[e >> 5] |= 1u << (e & 31);
+      }
+      if (lane == j) { runs++; served += bs; }
+    } else {
+      if (lane == 0) sm.starts[offj + rj] = NONE16;
+      res.misses++;
+      res.oversub = true;
+    }
+    if (lane == j) nextr++;
+    __syncwarp();
+  }
+  uint32_t osum = 0;
+  for (int u = lane; u < nslots; u += 32) osum += sm.occ[u];
+  res.occ_static = __reduce_add_sync(FULL, osum);
+  // ---- opportunistic fill at decision times {0} u {run ends} (Dynamic-schedule) ----
+  if (lane == 0) sm.dmask[0] |= 1u;
+  __syncwarp();
+  uint32_t count = runs;
+  int fs = -1, fe = -1;
+  const int nwords = (nslots + 31) >> 5;
+  int t = -1;
+  while (true) {
+    const int start = t + 1;
+    int nt = -1;
+    for (int wb = start >> 5; wb < nwords; wb += 32) {
+      const int w = wb + lane;
+      uint32_t v = w < nwords ? sm.dmask[w] : 0u;
+      if (w == (start >> 5)) v &= ~((1u << (start & 31)) - 1u);
+      const uint32_t bal = __ballot_sync(FULL, v != 0);
+      if (bal) {
+        const int pl = __ffs(bal) - 1;
+        const uint32_t word = __shfl_sync(FULL, v, pl);
+        nt = (wb + pl) * 32 + __ffs(word) - 1;
+        break;
+      }
+    }
+    if (nt < 0 || nt >= nslots) break;
+    t = nt;
+    int occ_t = sm.occ[t];
+    bool elig = false;
+    int ns = nslots;
+    if (active) {
+      const int rr = t / (int)sl;
+      bool covered = (fs <= t && t < fe);
+      if (rr < (int)rep) {
+        const uint16_t s0 = sm.starts[joff + rr];
+        if (s0 != NONE16) {
+          if ((int)s0 <= t && t < (int)s0 + (int)dstar) covered = true;
+          if ((int)s0 > t) ns = s0;
+        }
+        if (ns == nslots) {
+          for (int r2 = rr + 1; r2 < (int)rep; ++r2) {
+            const uint16_t s2 = sm.starts[joff + r2];
+            if (s2 != NONE16) { ns = s2; break; }
+          }
+        }
+      }
+      elig = !covered && occ_t + (int)g <= L;
+    }
+    uint32_t key = elig ? ((count << 5) | (uint32_t)lane) : 0xFFFFFFFFu;
+    while (true) {
+      const uint32_t mk = __reduce_min_sync(FULL, key);
+      if (mk == 0xFFFFFFFFu) break;
+      const int j = (int)(mk & 31u);
+      if (lane == j) key = 0xFFFFFFFFu;
+      const int gj = (int)__shfl_sync(FULL, g, j);
+      if (occ_t + gj > L) continue;
+      const int nsj = (int)__shfl_sync(FULL, ns, j);
+      const int bsj = (int)__shfl_sync(FULL, bs, j);
+      const int limit = nsj < nslots ? nsj : nslots;
+      int kslice = limit - t;   // slice: first u in [t, limit) with occ[u] + g > L
+      for (int base = t; base < limit; base += 32) {
+        const int u = base + lane;
+        const bool blocked = u < limit && (int)sm.occ[u] + gj > L;
+        const uint32_t bal = __ballot_sync(FULL, blocked);
+        if (bal) { kslice = base + __ffs(bal) - 1 - t; break; }
+      }
+      int bsel = 0;   // largest b in [b_lo, b*] with d(b) <= slice (d nondecreasing in b)
+      const uint16_t *dj = dtab + j * DSTACK_MAX_BATCH;
+      if (hook_b_only) {
+        if ((int)dj[bsj - 1] <= kslice) bsel = bsj;
+      } else {
+        for (int b0 = b_lo + 32 * ((bsj - b_lo) >> 5); b0 >= b_lo; b0 -= 32) {
+          const int b = b0 + lane;
+          const bool ok = b <= bsj && (int)dj[b - 1] <= kslice;
+          const uint32_t bal = __ballot_sync(FULL, ok);
+          if (bal) { bsel = b0 + 31 - __clz(bal); break; }
+        }
+      }
+      if (bsel == 0) continue;
+      const int dsel = dj[bsel - 1];
+      occ_add(sm.occ, t, dsel, gj, lane);
+      occ_t += gj;
+      if (lane == 0 && t + dsel < nslots) sm.dmask[(t + dsel) >> 5] |= 1u << ((t + dsel) & 31);
+      __syncwarp();
+      if (lane == j) { count++; runs++; served += (uint32_t)bsel; fs = t; fe = t + dsel; }
+    }
+  }
+  osum = 0;
+  for (int u = lane; u < nslots; u += 32) osum += sm.occ[u];
+  res.occ_all = __reduce_add_sync(FULL, osum);
+  res.served_tot = __reduce_add_sync(FULL, served);
+  return res;
+}
+
+}  // namespace dstack

@@ -1,0 +1,371 @@
+// prof.cuh -- a1-a3 device code: one warp analyses one DNN (knee, batch/GPU% search).
+//
+// Data path per DNN (warp-cooperative):
+//  1. one coalesced pass over the kernel rows (n u32, R u16, d u32): totals RT, D, sum R*n, the
+//     overflow bound X(L, b_hi), and (linear mode) a shared-memory histogram of R and R*n over the
+//     widths n <= S_tot;
+//  2. a chunked warp scan turns the histogram into the coefficient tables
+//        cA[m] = M t_p sum_{1<=n_i<=m} R_i,   cU[m] = M t_p sum_{n_i>m} R_i n_i
+//     so X(l,b) = S*(w_b*C1 + cA[m]) + b*cU[m] + mem, m = floor(S/b), in O(1) per cell;
+//  3. EXACT branch-and-bound for argmax eta = b S / X^2 over feasible (l, b) (Eqs. 9-12):
+//     the b_lo row is evaluated exactly (it is feasible whenever any row is: f_L and C grow with b);
+//     every other b is first bounded by a Jensen relaxation (X >= w_b C1 S + M t_p max(S RT1, b Wn)),
+//     then per run of constant m = floor(S/b) by the continuous supremum of b S/(alpha S + beta)^2,
+//     and only rows whose bound reaches the incumbent are evaluated exactly.  Bounds use f64 with a
+//     1e-9 safety margin; every decision between candidates is exact (float filter + 128-bit products).
+//     Threads mode (N_i(b) = ceil(b theta/2048)) rebuilds the tables per b and evaluates every row.
+//  4. the knee (Eq. 6) at b* is the unconstrained argmax of the b* row, tracked during its evaluation.
+#pragma once
+#include "common.cuh"
+
+namespace dstack {
+
+struct Best {
+  uint32_t found, l, b, S;
+  uint64_t X;
+  float sc;        // float score b S / X^2 (filter only)
+};
+
+__device__ __forceinline__ Best best_none() {
+  Best r; r.found = 0; r.l = 0; r.b = 0; r.S = 0; r.X = 0; r.sc = 0.f;
+  return r;
+}
+
+// exact total order: higher eta = b S / X^2, then smaller l, then smaller b
+__device__ __forceinline__ bool better(const Best &c, const Best &o) {
+  if (!c.found) return false;
+  if (!o.found) return true;
+  if (c.sc > o.sc * 1.0000077f) return true;    // 1 + 2^-17
+  if (o.sc > c.sc * 1.0000077f) return false;
+  const u128 L = (u128)(c.b * c.S) * ((u128)o.X * o.X);
+  const u128 R = (u128)(o.b * o.S) * ((u128)c.X * c.X);
+  if (L != R) return L > R;
+  return c.l < o.l || (c.l == o.l && c.b < o.b);
+}
+
+__device__ __forceinline__ float score_f(uint32_t P, uint64_t X) {
+  const float xf = (float)X;
+  return (float)P * __frcp_rn(xf * xf);
+}
+
+__device__ __forceinline__ Best shfl_best(const Best &v, int src) {
+  Best o;
+  const uint32_t packed = (v.found << 31) | (v.b << 24) | (v.l << 12) | v.S;   // l <= 255, S <= 256 (< 4096), b <= 64
+  const uint32_t pk = __shfl_sync(FULL, packed, src);
+  o.found = pk >> 31; o.b = (pk >> 24) & 127; o.l = (pk >> 12) & 4095; o.S = pk & 4095;
+  o.X = shfl_u64(v.X, src);
+  o.sc = __shfl_sync(FULL, v.sc, src);
+  return o;
+}
+
+// warp argmax: float max + uniqueness test decides almost always; exact butterfly otherwise
+__device__ __forceinline__ Best warp_best(Best v) {
+  const uint32_t sb = v.found ? __float_as_uint(v.sc) : 0u;
+  const uint32_t mx = __reduce_max_sync(FULL, sb);
+  if (mx == 0) return best_none();
+  const float thr = __uint_as_float(mx) * 0.9999847f;   // 1 - 2^-16
+  const uint32_t near = __ballot_sync(FULL, v.found && v.sc >= thr);
+  if (__popc(near) == 1) return shfl_best(v, __ffs(near) - 1);
+#pragma unroll
+  for (int m = 16; m; m >>= 1) {
+    Best o = shfl_best(v, (threadIdx.x & 31) ^ m);
+    if (better(o, v)) v = o;
+  }
+  return v;
+}
+
+struct DnnRes {
+  uint8_t st;
+  uint16_t demand, knee;
+  uint8_t b;
+  uint64_t RT, D;
+};
+
+template <int PAR>
+__device__ __forceinline__ uint64_t cell_X(int32_t S, int32_t b, uint32_t magic, uint64_t wC1, const uint64_t *cA,
+                                           const uint64_t *cU, int mem_mode, uint64_t D) {
+  int32_t m;
+  uint64_t ub;
+  if (PAR == 0) { m = (b == 1) ? S : (int32_t)__umulhi((uint32_t)S, magic); ub = (uint64_t)b; }
+  else { m = S; ub = 1; }
+  uint64_t X = (uint64_t)S * (wC1 + cA[m]) + ub * cU[m];
+  if (mem_mode == 1) X += (uint64_t)b * D;
+  else if (mem_mode == 2) X += (uint64_t)b * D * (uint64_t)S * (uint64_t)S;
+  return X;
+}
+
+__device__ __forceinline__ uint32_t magic_of(int32_t b) { return b == 1 ? 0u : (uint32_t)(0xFFFFFFFFu / (uint32_t)b) + 1u; }
+
+// scan the histogram (counts in cA, weights in cU) into the coefficient tables, lane-chunked
+__device__ __forceinline__ void scan_tables(uint64_t *cA, uint64_t *cU, int S_tot, uint64_t Mtp, uint64_t W, int lane) {
+  __syncwarp();
+  const int C = (S_tot + 32) >> 5;          // bins per lane (S_tot+1 bins)
+  const int m0 = lane * C;
+  uint64_t sa = 0, sw = 0;
+  for (int i = 0; i < C; ++i) {
+    const int m = m0 + i;
+    if (m <= S_tot) { sa += cA[m]; sw += cU[m]; }
+  }
+  uint64_t pa = sa, pw = sw;   // inclusive scan of lane totals
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t ua = shfl_up_u64(pa, d), uw = shfl_up_u64(pw, d);
+    if (lane >= d) { pa += ua; pw += uw; }
+  }
+  pa -= sa; pw -= sw;          // exclusive
+  for (int i = 0; i < C; ++i) {
+    const int m = m0 + i;
+    if (m <= S_tot) {
+      pa += cA[m]; pw += cU[m];
+      cA[m] = Mtp * pa; cU[m] = Mtp * (W - pw);
+    }
+  }
+  __syncwarp();
+}
+
+// threads mode: histogram of N = ceil(b theta / 2048) and its scan
+__device__ __forceinline__ void build_tables_threads(const uint32_t *__restrict__ n, const uint16_t *__restrict__ r,
+                                                     int32_t K, int32_t S_tot, uint64_t Mtp, int32_t b, uint64_t *cA,
+                                                     uint64_t *cU, int lane) {
+  for (int m = lane; m <= S_tot; m += 32) { cA[m] = 0; cU[m] = 0; }
+  __syncwarp();
+  uint64_t W = 0;
+  for (int i = lane; i < K; i += 32) {
+    const uint64_t N = ((uint64_t)b * n[i] + 2047) >> 11;
+    const uint32_t R = r[i];
+    W += (uint64_t)R * N;
+    if (N >= 1 && N <= (uint64_t)S_tot) {
+      atomicAdd((unsigned long long *)&cA[N], (unsigned long long)R);
+      atomicAdd((unsigned long long *)&cU[N], (unsigned long long)(R * N));
+    }
+  }
+  W = warp_sum_u64(W);
+  scan_tables(cA, cU, S_tot, Mtp, W, lane);
+}
+
+struct RowCtx {
+  const uint16_t *Stab;
+  const uint64_t *cA, *cU;
+  int32_t L, mem_mode, wse;
+  uint64_t C1, D, SLOM, aM;
+};
+
+// exact evaluation of row b: feasible argmax (e) and unconstrained argmax (k), warp-reduced
+template <int PAR>
+__device__ __forceinline__ void eval_row(const RowCtx &c, int32_t b, int lane, Best &e, Best &k) {
+  const uint32_t magic = magic_of(b);
+  const uint64_t wC1 = (c.wse == 0 ? (uint64_t)b : 1ull) * c.C1;
+  const uint64_t baM = (uint64_t)b * c.aM;
+  e = best_none(); k = best_none();
+  for (int32_t l = 1 + lane; l <= c.L; l += 32) {
+    const int32_t S = c.Stab[l];
+    const uint64_t X = cell_X<PAR>(S, b, magic, wC1, c.cA, c.cU, c.mem_mode, c.D);
+    Best cand; cand.found = 1; cand.l = l; cand.b = b; cand.S = S; cand.X = X; cand.sc = score_f(b * S, X);
+    if (better(cand, k)) k = cand;
+    const uint64_t cap = (uint64_t)S * c.SLOM;
+    if (X + (uint64_t)S * baM <= cap && 2 * X <= cap && better(cand, e)) e = cand;   // Eq. 11, Eq. 12
+  }
+  e = warp_best(e);
+  k = warp_best(k);
+}
+
+// does sup over real S in [lo, hi] of b S / (alpha S + beta)^2 reach thr?
+__device__ __forceinline__ bool sup_reaches(double b, double alpha, double beta, double lo, double hi, double thr) {
+  if (hi < lo) return false;
+  double S;
+  if (beta <= alpha * lo) S = lo;
+  else if (beta >= alpha * hi) S = hi;
+  else return b >= 4.0 * alpha * beta * thr;            // peak b / (4 alpha beta) at S* = beta / alpha
+  const double x = alpha * S + beta;
+  return b * S >= thr * x * x;
+}
+
+// Analyse DNN k.  knee_only: status + knee at knee_b.  Otherwise (l*, b*), demand, knee(b*).
+template <int PAR>
+__device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k, const uint16_t *Stab,
+                              uint64_t *cA, uint64_t *cU, int lane, int knee_only, int32_t knee_b) {
+  DnnRes res; res.st = DSTACK_ST_OK; res.demand = 0; res.knee = 0; res.b = 0; res.RT = 0; res.D = 0;
+  const int L = p.L, S_tot = p.S_tot;
+  const int64_t r0 = pb.dnn_row_off[k], r1 = pb.dnn_row_off[k + 1];
+  const int64_t K64 = r1 - r0;
+  const int32_t t_p = pb.t_p[k], t_np = pb.t_np[k], slo = pb.slo_us[k], asm_us = pb.asm_us[k];
+  const int32_t bmax = pb.bmax[k], mbw = pb.mem_bw[k];
+  const int mem_mode = p.mem_mode;
+  const uint64_t M = mem_mode == 0 ? 1 : (uint64_t)mbw;
+  const int32_t b_lo = p.b_min, b_hi = bmax < p.b_max ? bmax : p.b_max;
+  const int32_t b_eval = knee_only ? knee_b : b_hi;   // where the overflow bound is checked
+  // ---- header validation (DSTACK_ST_INVALID conditions, dstack.h) ----
+  if (K64 < 1 || K64 > DSTACK_MAX_ROWS_PER_DNN || t_p < 1 || t_np < 0 || slo < 1 || slo > (1 << 30) ||
+      (slo % p.slot_us) != 0 || asm_us < 0 || asm_us > (1 << 24) || bmax < 1 ||
+      (mem_mode != 0 && (mbw < 1 || mbw > (1 << 24)))) {
+    res.st = DSTACK_ST_INVALID;
+    return res;
+  }
+  const int32_t K = (int32_t)K64;
+  const uint32_t *n = pb.n + r0;
+  const uint16_t *r = pb.r + r0;
+  const uint32_t *d = pb.d + r0;
+  // ---- a1: one coalesced pass over the rows ----
+  if (PAR == 0) {
+    for (int m = lane; m <= S_tot; m += 32) { cA[m] = 0; cU[m] = 0; }
+    __syncwarp();
+  }
+  uint64_t RT = 0, D = 0, Wn = 0, Vmax = 0, RT1 = 0;
+  uint32_t anyR0 = 0, anyN = 0;
+  for (int i = lane; i < K; i += 32) {
+    const uint64_t nn = n[i];
+    const uint32_t R = r[i];
+    const uint64_t dd = d[i];
+    RT += R; D += (uint64_t)R * dd; Wn += (uint64_t)R * nn;
+    if (nn != 0) RT1 += R;
+    anyR0 |= (R == 0); anyN |= (nn != 0);
+    const uint64_t Nb = PAR == 0 ? (uint64_t)b_eval * nn : ((uint64_t)b_eval * nn + 2047) >> 11;
+    if (Nb >= 1) Vmax = sat_add(Vmax, (uint64_t)R * (Nb > (uint64_t)S_tot ? Nb : (uint64_t)S_tot));
+    if (PAR == 0 && nn >= 1 && nn <= (uint64_t)S_tot) {
+      atomicAdd((unsigned long long *)&cA[nn], (unsigned long long)R);
+      atomicAdd((unsigned long long *)&cU[nn], (unsigned long long)(R * nn));
+    }
+  }
+  RT = warp_sum_u64(RT); D = warp_sum_u64(D); Wn = warp_sum_u64(Wn); Vmax = warp_sum_sat(Vmax);
+  RT1 = warp_sum_u64(RT1);
+  anyR0 = warp_or(anyR0); anyN = warp_or(anyN);
+  res.RT = RT; res.D = D;
+  if (anyR0 || (t_np == 0 && !anyN && (mem_mode == 0 || D == 0))) { res.st = DSTACK_ST_INVALID; return res; }
+  if (!knee_only && b_hi < b_lo) { res.st = DSTACK_ST_INFEASIBLE; return res; }
+  {
+    // X(L, b_eval) = w t_np RT S_tot M + M t_p Vmax + mem  (the maximum of X over the grid)
+    const u128 w = p.wse_mode == 0 ? (u128)b_eval : (u128)1;
+    u128 Xub = w * (u128)t_np * (u128)RT * (u128)S_tot * (u128)M + (u128)M * (u128)t_p * (u128)Vmax;
+    if (mem_mode == 1) Xub += (u128)b_eval * (u128)D;
+    else if (mem_mode == 2) Xub += (u128)b_eval * (u128)D * (u128)(S_tot * S_tot);
+    if (Vmax >= (1ull << 63) || Xub >= (u128)X_LIMIT) { res.st = DSTACK_ST_OVERFLOW; return res; }
+  }
+  const uint64_t Mtp = M * (uint64_t)t_p;
+  if (PAR == 0) scan_tables(cA, cU, S_tot, Mtp, Wn, lane);
+  RowCtx c;
+  c.Stab = Stab; c.cA = cA; c.cU = cU; c.L = L; c.mem_mode = mem_mode; c.wse = p.wse_mode;
+  c.C1 = (uint64_t)t_np * RT * M; c.D = D; c.SLOM = (uint64_t)slo * M; c.aM = (uint64_t)asm_us * M;
+  Best e, kk;
+  if (knee_only) {
+    if (PAR == 1) build_tables_threads(n, r, K, S_tot, Mtp, knee_b, cA, cU, lane);
+    eval_row<PAR>(c, knee_b, lane, e, kk);
+    res.knee = (uint16_t)kk.l;
+    return res;
+  }
+  // ---- a3: exact branch-and-bound over (l, b) ----
+  if (PAR == 1) build_tables_threads(n, r, K, S_tot, Mtp, b_lo, cA, cU, lane);
+  eval_row<PAR>(c, b_lo, lane, e, kk);
+  if (!e.found) { res.st = DSTACK_ST_INFEASIBLE; return res; }
+  Best best = e;
+  uint32_t knee = kk.l;
+  if (PAR == 1) {
+    for (int32_t b = b_lo + 1; b <= b_hi; ++b) {
+      build_tables_threads(n, r, K, S_tot, Mtp, b, cA, cU, lane);
+      eval_row<1>(c, b, lane, e, kk);
+      if (better(e, best)) { best = e; knee = kk.l; }
+    }
+  } else if (b_hi > b_lo) {
+    // incumbent eta (b S / X^2) with a safety margin for the f64 bounds
+    const double thr = (double)(best.b * best.S) / ((double)best.X * (double)best.X) * (1.0 - 1e-9);
+    const double Mtpd = (double)Mtp, C1d = (double)c.C1, Dd = (double)D, RT1d = (double)RT1, Wnd = (double)Wn;
+    // crude (Jensen) bound per b, lane per b: X >= w_b C1 S + M t_p max(S RT1, b Wn) + mem_lb
+    uint32_t cand_lo = 0, cand_hi = 0;
+    for (int bb = b_lo + 1 + lane; bb <= b_hi; bb += 32) {
+      const double bd = (double)bb;
+      const double a1 = (p.wse_mode == 0 ? bd : 1.0) * C1d;
+      const double m0 = mem_mode == 1 ? bd * Dd : 0.0;
+      bool ok;
+      if (RT1 == 0) {
+        ok = sup_reaches(bd, a1, m0, 1.0, (double)S_tot, thr);
+      } else {
+        const double Sc = bd * Wnd / RT1d;
+        ok = sup_reaches(bd, a1, Mtpd * bd * Wnd + m0, 1.0, fmin(Sc, (double)S_tot), thr) ||
+             sup_reaches(bd, a1 + Mtpd * RT1d, m0, fmax(Sc, 1.0), (double)S_tot, thr);
+      }
+      if (ok) {
+        const int bit = bb - 1;
+        if (bit < 32) cand_lo |= 1u << bit; else cand_hi |= 1u << (bit - 32);
+      }
+    }
+    cand_lo = __reduce_or_sync(FULL, cand_lo);
+    cand_hi = __reduce_or_sync(FULL, cand_hi);
+    uint64_t cand = ((uint64_t)cand_hi << 32) | cand_lo;
+    // per-run bound for the surviving b's, then exact rows for the b's that still reach the incumbent
+    while (cand) {
+      const int bb = __ffsll((long long)cand);   // b = bit index + 1
+      cand &= cand - 1;
+      const double bd = (double)bb;
+      const uint64_t wC1 = (p.wse_mode == 0 ? (uint64_t)bb : 1ull) * c.C1;
+      const int mmax = S_tot / bb;
+      bool ok = false;
+      for (int m = lane; m <= mmax; m += 32) {
+        const int lo = m * bb > 1 ? m * bb : 1;
+        const int hi = m * bb + bb - 1 < S_tot ? m * bb + bb - 1 : S_tot;
+        const uint64_t alpha = wC1 + cA[m] + (mem_mode == 2 ? (uint64_t)bb * D * (uint64_t)lo : 0ull);
+        const uint64_t beta = (uint64_t)bb * cU[m] + (mem_mode == 1 ? (uint64_t)bb * D : 0ull);
+        ok = ok || sup_reaches(bd, (double)alpha, (double)beta, (double)lo, (double)hi, thr);
+      }
+      if (__any_sync(FULL, ok)) {
+        eval_row<0>(c, bb, lane, e, kk);
+        if (better(e, best)) { best = e; knee = kk.l; }
+      }
+    }
+  }
+  const int32_t dm = (int32_t)best.l + p.margin;
+  res.demand = (uint16_t)(dm < L ? dm : L);
+  res.b = (uint8_t)best.b;
+  res.knee = (uint16_t)knee;
+  return res;
+}
+
+// d_j(b) = ceil(X(g, b) / (S(g) M Delta)) for b in [b_lo, b_hi] from the (linear-mode) tables of the
+// DNN just analysed; lanes over b.  Writes dtab[b-1] (u16, clamped).
+__device__ __forceinline__ void dtab_from_tables(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k,
+                                                 const uint64_t *cA, const uint64_t *cU, uint64_t RT, uint64_t D,
+                                                 int32_t g, int32_t b_lo, int32_t b_hi, uint16_t *dtab, int lane) {
+  const uint64_t M = p.mem_mode == 0 ? 1ull : (uint64_t)pb.mem_bw[k];
+  const int32_t S = s_of(g, p.S_tot, p.L);
+  const uint64_t C1 = (uint64_t)pb.t_np[k] * RT * M;
+  const uint64_t den = (uint64_t)S * M * (uint64_t)p.slot_us;
+  for (int32_t b = b_lo + lane; b <= b_hi; b += 32) {
+    const uint64_t X = cell_X<0>(S, b, magic_of(b), (p.wse_mode == 0 ? (uint64_t)b : 1ull) * C1, cA, cU, p.mem_mode, D);
+    const uint64_t ds = (X + den - 1) / den;
+    dtab[b - 1] = (uint16_t)(ds > 0xFFFF ? 0xFFFF : ds);
+  }
+  __syncwarp();
+}
+
+// Same from the rows (any mode): one row pass per b.  RT, D given.
+__device__ __forceinline__ void dtab_from_rows(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k,
+                                               uint64_t RT, uint64_t D, int32_t g, int32_t b_lo, int32_t b_hi,
+                                               uint16_t *dtab, int lane) {
+  const int64_t r0 = pb.dnn_row_off[k];
+  const int32_t K = (int32_t)(pb.dnn_row_off[k + 1] - r0);
+  const uint64_t M = p.mem_mode == 0 ? 1ull : (uint64_t)pb.mem_bw[k];
+  const uint64_t t_p = (uint64_t)pb.t_p[k], t_np = (uint64_t)pb.t_np[k];
+  const uint64_t S = (uint64_t)s_of(g, p.S_tot, p.L);
+  const uint32_t *n = pb.n + r0;
+  const uint16_t *r = pb.r + r0;
+  const uint64_t den = S * M * (uint64_t)p.slot_us;
+  for (int32_t b = b_lo; b <= b_hi; ++b) {
+    uint64_t V = 0;   // sum_i R_i max(S, N_i(b)) over N_i >= 1  (= S*A + U)
+    for (int i = lane; i < K; i += 32) {
+      const uint64_t nn = n[i];
+      const uint64_t N = p.par_mode == 0 ? (uint64_t)b * nn : ((uint64_t)b * nn + 2047) >> 11;
+      if (N >= 1) V += (uint64_t)r[i] * (N > S ? N : S);
+    }
+    V = warp_sum_u64(V);
+    uint64_t X = (p.wse_mode == 0 ? (uint64_t)b : 1ull) * t_np * RT * S * M + M * t_p * V;
+    if (p.mem_mode == 1) X += (uint64_t)b * D;
+    else if (p.mem_mode == 2) X += (uint64_t)b * D * S * S;
+    const uint64_t ds = (X + den - 1) / den;
+    if (lane == 0) dtab[b - 1] = (uint16_t)(ds > 0xFFFF ? 0xFFFF : ds);
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void fill_stab(uint16_t *Stab, int L, int S_tot) {
+  for (int l = threadIdx.x; l <= L; l += blockDim.x) Stab[l] = (uint16_t)s_of(l, S_tot, L);
+}
+
+}  // namespace dstack

@@ -222,3 +222,23 @@ def test_config3_fullsize_sampled_parity(ds):
     agg = ds.agg_to_dict(o["agg"])
     assert agg["n_scen"] == sp.num_scen and agg["n_dnn"] == dp.num_dnn
     assert sum(agg["n_st"]) == dp.num_dnn and sum(agg["n_scen_st"]) == sp.num_scen
+
+
+@pytest.mark.parametrize("variant", ["defaults", "verbatim148", "per_launch", "batching"])
+def test_split_path_parity(ds, variant):
+    """The call-by-call path dstack_batch_opt -> dstack_wmaxmin -> dstack_schedule_cycle (separate kernels)
+    against the oracle; dstack_eval_batch uses the fused kernel instead, so both are covered."""
+    sp, p = synth.config(2, num_scen=150, rows_pct=25, variant="batching" if variant == "batching" else "default")
+    if variant == "verbatim148":
+        p = p.replace(mem_mode=2, L=148)
+    elif variant == "per_launch":
+        p = p.replace(wse_mode=1)
+    pb = synth.generate_host(sp)
+    dp = ds.from_host(pb, "cuda")
+    o = ds.alloc_outputs(dp, agg=False)
+    ws = ds.Workspace(ds.workspace_size(dp, p), dp.device)
+    ds.batch_opt(dp, p, out=o)
+    ds.wmaxmin(dp.scen_dnn_off, p.L, o["demand"], out=o["alloc_q16"])
+    ds.schedule_cycle(dp, p, o["demand"], o["batch"], o["alloc_q16"], out=o, ws=ws)
+    torch.cuda.synchronize()
+    assert_parity(ds.to_numpy(o, pb.num_scen, pb.num_dnn), oracle.evaluate(pb, p), where=f"split-{variant}")
