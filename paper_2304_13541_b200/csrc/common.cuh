@@ -37,6 +37,18 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 }
 __device__ __forceinline__ uint32_t warp_or(uint32_t v) { return __reduce_or_sync(FULL, v); }
 
+// bulk L2 prefetch of [ptr, ptr+bytes) (TMA engine, no registers / no wait): 16-byte aligned chunks
+__device__ __forceinline__ void prefetch_l2(const void *ptr, int64_t bytes) {
+  if (bytes <= 0) return;
+  uintptr_t a0 = (uintptr_t)ptr & ~(uintptr_t)15;
+  uintptr_t a1 = ((uintptr_t)ptr + (uintptr_t)bytes + 15) & ~(uintptr_t)15;
+  while (a0 < a1) {
+    uint32_t sz = (uint32_t)((a1 - a0) > (1u << 20) ? (1u << 20) : (a1 - a0));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(sz) : "memory");
+    a0 += sz;
+  }
+}
+
 // saturating add (sticky at >= 2^63)
 __device__ __forceinline__ uint64_t sat_add(uint64_t a, uint64_t b) {
   uint64_t s = a + b;

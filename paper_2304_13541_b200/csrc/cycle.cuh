@@ -148,6 +148,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   __syncwarp();
   uint32_t count = runs;
   int fs = -1, fe = -1;
+  const uint32_t sl_magic = sl <= 1 ? 0u : (uint32_t)(0xFFFFFFFFu / sl) + 1u;   // t / sl = umulhi(t, magic), t < 2^13
   const int nwords = (nslots + 31) >> 5;
   int t = -1;
   while (true) {
@@ -169,22 +170,13 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     t = nt;
     int occ_t = sm.occ[t];
     bool elig = false;
-    int ns = nslots;
-    if (active) {
-      const int rr = t / (int)sl;
+    int rr = 0;
+    if (active) {   // eligible: not running at t (static run of window rr or the last fill), fits at t
+      rr = sl == 1 ? t : (int)__umulhi((uint32_t)t, sl_magic);
       bool covered = (fs <= t && t < fe);
       if (rr < (int)rep) {
         const uint16_t s0 = sm.starts[joff + rr];
-        if (s0 != NONE16) {
-          if ((int)s0 <= t && t < (int)s0 + (int)dstar) covered = true;
-          if ((int)s0 > t) ns = s0;
-        }
-        if (ns == nslots) {
-          for (int r2 = rr + 1; r2 < (int)rep; ++r2) {
-            const uint16_t s2 = sm.starts[joff + r2];
-            if (s2 != NONE16) { ns = s2; break; }
-          }
-        }
+        if (s0 != NONE16 && (int)s0 <= t && t < (int)s0 + (int)dstar) covered = true;
       }
       elig = !covered && occ_t + (int)g <= L;
     }
@@ -193,33 +185,42 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       const uint32_t mk = __reduce_min_sync(FULL, key);
       if (mk == 0xFFFFFFFFu) break;
       const int j = (int)(mk & 31u);
-      if (lane == j) key = 0xFFFFFFFFu;
       const int gj = (int)__shfl_sync(FULL, g, j);
-      if (occ_t + gj > L) continue;
-      const int nsj = (int)__shfl_sync(FULL, ns, j);
+      if (occ_t + gj > L) { if (lane == j) key = 0xFFFFFFFFu; continue; }
+      int ns = nslots;   // next start of j after t (only static runs can start later)
+      if (lane == j) {
+        key = 0xFFFFFFFFu;
+        for (int r2 = rr; r2 < (int)rep; ++r2) {
+          const uint16_t s2 = sm.starts[joff + r2];
+          if (s2 != NONE16 && (int)s2 > t) { ns = s2; break; }
+        }
+      }
+      const int limit = __shfl_sync(FULL, ns, j);
       const int bsj = (int)__shfl_sync(FULL, bs, j);
-      const int limit = nsj < nslots ? nsj : nslots;
-      int kslice = limit - t;   // slice: first u in [t, limit) with occ[u] + g > L
-      for (int base = t; base < limit; base += 32) {
+      const int dsj = (int)__shfl_sync(FULL, dstar, j);
+      // slice k = first u in [t, limit) with occ[u] + g > L; only k >= d(b*) or its exact value below matters
+      const int stop = t + dsj < limit ? t + dsj : limit;
+      int kslice = stop - t;
+      for (int base = t; base < stop; base += 32) {
         const int u = base + lane;
-        const bool blocked = u < limit && (int)sm.occ[u] + gj > L;
+        const bool blocked = u < stop && (int)sm.occ[u] + gj > L;
         const uint32_t bal = __ballot_sync(FULL, blocked);
         if (bal) { kslice = base + __ffs(bal) - 1 - t; break; }
       }
       int bsel = 0;   // largest b in [b_lo, b*] with d(b) <= slice (d nondecreasing in b)
       const uint16_t *dj = dtab + j * DSTACK_MAX_BATCH;
-      if (hook_b_only) {
-        if ((int)dj[bsj - 1] <= kslice) bsel = bsj;
-      } else {
-        for (int b0 = b_lo + 32 * ((bsj - b_lo) >> 5); b0 >= b_lo; b0 -= 32) {
+      if (kslice >= dsj) {
+        bsel = bsj;
+      } else if (!hook_b_only) {
+        for (int b0 = b_lo + 32 * ((bsj - 1 - b_lo) >> 5); b0 >= b_lo && bsj - 1 >= b_lo; b0 -= 32) {
           const int b = b0 + lane;
-          const bool ok = b <= bsj && (int)dj[b - 1] <= kslice;
+          const bool ok = b < bsj && (int)dj[b - 1] <= kslice;
           const uint32_t bal = __ballot_sync(FULL, ok);
           if (bal) { bsel = b0 + 31 - __clz(bal); break; }
         }
       }
       if (bsel == 0) continue;
-      const int dsel = dj[bsel - 1];
+      const int dsel = bsel == bsj ? dsj : (int)dj[bsel - 1];
       occ_add(sm.occ, t, dsel, gj, lane);
       occ_t += gj;
       if (lane == 0 && t + dsel < nslots) sm.dmask[(t + dsel) >> 5] |= 1u << ((t + dsel) & 31);

@@ -24,7 +24,7 @@ __host__ __device__ inline size_t fused_warp_bytes(int S_tot) {
 }
 
 template <int PAR>
-__global__ void __launch_bounds__(FUSED_WARPS * 32) k_fused(FusedArgs a) {
+__global__ void __launch_bounds__(FUSED_WARPS * 32, 3) k_fused(FusedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int L = a.p.L, S_tot = a.p.S_tot, slot = a.p.slot_us, b_lo = a.p.b_min;
   uint16_t *Stab = (uint16_t *)smem;
@@ -43,6 +43,14 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32) k_fused(FusedArgs a) {
   for (int64_t s = gwarp; s < a.pb.num_scen; s += nwarps) {
     const int32_t k0 = a.pb.scen_dnn_off[s], nd = a.pb.scen_dnn_off[s + 1] - k0;
     const bool fits = nd <= DSTACK_MAX_DNN_PER_SCEN;
+    // stage the rows of this warp's NEXT scenario into L2 while this one is analysed and simulated
+    if (lane == 0 && s + nwarps < a.pb.num_scen) {
+      const int64_t sn = s + nwarps;
+      const int64_t q0 = a.pb.dnn_row_off[a.pb.scen_dnn_off[sn]], q1 = a.pb.dnn_row_off[a.pb.scen_dnn_off[sn + 1]];
+      prefetch_l2(a.pb.n + q0, (q1 - q0) * 4);
+      prefetch_l2(a.pb.r + q0, (q1 - q0) * 2);
+      prefetch_l2(a.pb.d + q0, (q1 - q0) * 4);
+    }
     // ---- (i) a1-a3 per DNN; lane j keeps DNN j's results ----
     uint32_t dem = 0, bs = 0;
     uint64_t RT = 0, D = 0;

@@ -212,10 +212,7 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
   }
   uint64_t RT = 0, D = 0, Wn = 0, Vmax = 0, RT1 = 0;
   uint32_t anyR0 = 0, anyN = 0;
-  for (int i = lane; i < K; i += 32) {
-    const uint64_t nn = n[i];
-    const uint32_t R = r[i];
-    const uint64_t dd = d[i];
+  auto row = [&](uint64_t nn, uint32_t R, uint64_t dd) {
     RT += R; D += (uint64_t)R * dd; Wn += (uint64_t)R * nn;
     if (nn != 0) RT1 += R;
     anyR0 |= (R == 0); anyN |= (nn != 0);
@@ -225,6 +222,18 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
       atomicAdd((unsigned long long *)&cA[nn], (unsigned long long)R);
       atomicAdd((unsigned long long *)&cU[nn], (unsigned long long)(R * nn));
     }
+  };
+  // two rows per lane in flight per iteration (loads issued before the dependent histogram atomics)
+  for (int i0 = lane; i0 < K; i0 += 64) {
+    const int i1 = i0 + 32;
+    const bool h1 = i1 < K;
+    const uint64_t n0 = __ldg(n + i0), d0 = __ldg(d + i0);
+    const uint32_t R0 = __ldg(r + i0);
+    uint64_t n1 = 0, d1 = 0;
+    uint32_t R1 = 0;
+    if (h1) { n1 = __ldg(n + i1); d1 = __ldg(d + i1); R1 = __ldg(r + i1); }
+    row(n0, R0, d0);
+    if (h1) row(n1, R1, d1);
   }
   RT = warp_sum_u64(RT); D = warp_sum_u64(D); Wn = warp_sum_u64(Wn); Vmax = warp_sum_sat(Vmax);
   RT1 = warp_sum_u64(RT1);
