@@ -200,12 +200,13 @@ def algorithmic_bytes(dp, args):
     """Bytes each kernel must move by definition: its inputs once + its outputs once."""
     R, D, S = dp.num_rows, dp.num_dnn, dp.num_scen
     rows = 10 * R                                   # n u32 + R u16 + d u32
-    hdr = D * (8 + 6 * 4) + S * 4                   # dnn_row_off + 6 int32 headers; scen_dnn_off
-    out_dnn = D * (2 + 1 + 2 + 1 + 4 + 2 + 2 + 4)   # demand, batch, knee, status, alloc, level, runs, served
-    out_scen = S * (1 + 4 + 3 * 8 + 4)              # scen_status, T, u_static, u, thr, misses
-    fused = rows + hdr + out_dnn + out_scen
-    agg = out_dnn + out_scen + S * 4
-    return {"k_fused": fused, "k_agg": agg, "path": fused}
+    hdr = D * (8 + 6 * 4)                           # dnn_row_off + t_p, t_np, M, SLO, a, bmax
+    prof = rows + hdr + D * (2 + 1 + 2 + 1)         # -> demand, batch, knee, status
+    wmm = S * 4 + D * (2 + 4)                       # offsets, demand -> alloc
+    cyc = S * 4 + D * (2 + 1 + 4 + 4) + D * (2 + 2 + 4) + S * (1 + 4 + 3 * 8 + 4)
+    agg = S * (4 + 1 + 4 + 3 * 8 + 4) + D * (2 + 1 + 2 + 1 + 4 + 2 + 2 + 4)
+    path = rows + hdr + S * 4 + D * (2 + 1 + 2 + 1 + 4 + 2 + 2 + 4) + S * (1 + 4 + 3 * 8 + 4)
+    return {"k_prof": prof, "k_wmaxmin": wmm, "k_cycle": cyc, "k_ideal": rows, "k_agg": agg, "path": path}
 
 
 def run_native(args, rank, world, local):
@@ -228,26 +229,18 @@ def run_native(args, rank, world, local):
     out = ds.alloc_outputs(dp, agg=True)
     ws = ds.Workspace(ds.workspace_size(dp, p), dev)
     stream = torch.cuda.current_stream(dev)
-    names = ["k_fused" + ("+k_ideal" if p.ideal else ""), "k_agg"]
-    out_noagg = {k: v for k, v in out.items() if k != "agg"}
     launches = [0]
 
-    def step(evs=None):
-        if evs: evs[0].record(stream)
-        ds.eval_batch(dp, p, out=out_noagg, ws=ws); launches[0] += ds.last_launch_count()   # a1-a5 fused
-        if evs: evs[1].record(stream)
-        ds.aggregate(dp, p, out, ws); launches[0] += ds.last_launch_count()                # a8
-        if evs: evs[2].record(stream)
+    def step():
+        ds.eval_batch(dp, p, out=out, ws=ws); launches[0] += ds.last_launch_count()   # a1-a5 (+a6) + a8
         if world > 1:
             dist.all_reduce(out["agg"][:5].view(torch.float64), op=dist.ReduceOp.SUM)   # f64 sums
             dist.all_reduce(out["agg"][5:], op=dist.ReduceOp.SUM)                       # u64 counts
-        if evs: evs[3].record(stream)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     launches[0] = 0
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     sampler = ClockSampler(range(world)) if rank == 0 else None
     if world > 1:
         dist.barrier()
@@ -255,17 +248,18 @@ def run_native(args, rank, world, local):
     if sampler:
         sampler.start(); time.sleep(0.3)
     t_start = torch.cuda.Event(enable_timing=True); t_end = torch.cuda.Event(enable_timing=True)
+    ds.profile_start(args.steps)
     t_start.record(stream)
     for k in range(args.steps):
-        step(evs[k])
+        step()
     t_end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
     ms = t_start.elapsed_time(t_end)
-    kern_ms = [sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps for i in range(2)]
-    comm_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+    kms, ncalls = ds.profile_stop()
+    kern = {k: v / max(ncalls, 1) for k, v in kms.items() if v > 0}
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -283,14 +277,12 @@ def run_native(args, rank, world, local):
             dist.destroy_process_group()
         return 0
     ab = algorithmic_bytes(dp, args)
-    kmap = dict(zip(names, kern_ms))
-    dom = 0   # k_fused: the whole a1-a5 path in one kernel
-    dom_name = names[dom]
-    dom_bytes = ab["k_fused"]
+    dom_name = max(kern, key=kern.get)          # the kernel with the largest share of the step
+    dom_bytes = ab[dom_name]
     peak, peak_src = hbm_peak()
-    achieved = dom_bytes / (kern_ms[dom] / 1e3) / 1e9
+    achieved = dom_bytes / (kern[dom_name] / 1e3) / 1e9
     traffic = None
-    tr = traffic_per_scenario().get("k_fused")
+    tr = traffic_per_scenario().get(dom_name)
     if tr:
         traffic = tr * per_gpu
     line = {
@@ -304,7 +296,7 @@ def run_native(args, rank, world, local):
         "path_roofline": {"algorithmic_bytes_per_step": ab["path"],
                           "achieved_GBps": ab["path"] / (ms_max / args.steps / 1e3) / 1e9,
                           "frac": ab["path"] / (ms_max / args.steps / 1e3) / 1e9 / peak},
-        "kernels_ms": kmap, "allreduce_ms": comm_ms if world > 1 else 0.0,
+        "kernels_ms": kern, "kernels_share": {k: v / (ms_max / args.steps) for k, v in kern.items()},
         "gpu_launches": launches[0],
         "clocks": clocks,
         "e2e": e2e,

@@ -172,6 +172,15 @@ int dstack_eval_batch(const dstack_problem_t *pb, const dstack_params_t *p, dsta
 int dstack_aggregate(const dstack_problem_t *pb, const dstack_params_t *p, dstack_out_t *out, void *ws,
                      size_t ws_bytes, void *stream);
 
+/* Live per-kernel timing of dstack_eval_batch (bench accounting): after dstack_profile_start, each
+ * eval_batch call on this thread records CUDA events on its stream between its kernel launches
+ * (slots: 0 k_prof, 1 k_wmaxmin, 2 k_cycle, 3 k_ideal, 4 k_agg).  dstack_profile_stop synchronises
+ * those events and writes the summed milliseconds per slot into ms_out[DSTACK_PROF_SLOTS] and the
+ * number of profiled calls into *calls.  At most max_calls calls are recorded. */
+#define DSTACK_PROF_SLOTS 5
+int dstack_profile_start(int32_t max_calls);
+int dstack_profile_stop(double *ms_out, int32_t *calls);
+
 /* Number of kernel launches the previous call on this thread enqueued (bench accounting). */
 int dstack_last_launch_count(void);
 

@@ -10,6 +10,21 @@ namespace {
 
 thread_local int g_launches = 0;
 
+// live per-kernel event timing of eval_batch (dstack_profile_start/stop)
+struct ProfState {
+  bool on = false;
+  int max_calls = 0, calls = 0;
+  cudaEvent_t *ev = nullptr;        // [max_calls][DSTACK_PROF_SLOTS + 1]
+  uint8_t *used = nullptr;          // [max_calls][DSTACK_PROF_SLOTS] slot launched?
+};
+thread_local ProfState g_prof;
+
+inline void prof_mark(cudaStream_t s, int slot) {
+  if (!g_prof.on || g_prof.calls >= g_prof.max_calls) return;
+  const int base = g_prof.calls * (DSTACK_PROF_SLOTS + 1);
+  cudaEventRecord(g_prof.ev[base + slot], s);
+}
+
 bool params_ok(const dstack_params_t *p) {
   return p && p->L >= 1 && p->L <= 255 && p->S_tot >= 1 && p->S_tot <= 256 && p->slot_us >= 1 &&
          p->mem_mode >= 0 && p->mem_mode <= 2 && p->par_mode >= 0 && p->par_mode <= 1 && p->wse_mode >= 0 &&
@@ -39,9 +54,20 @@ bool disjoint(const dstack_problem_t *pb, const void *o) {
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// workspace layout: [agg partials | d_j(b) slabs | ideal per-row arrays]
-size_t ws_dtab_off() { return align256(agg_ws_bytes()); }
-size_t ws_ideal_off() { return ws_dtab_off() + align256((size_t)DTAB_MAX_WARPS * DTAB_SLAB_BYTES); }
+// workspace layout: [agg partials | d_j(b) rows u16[num_dnn][64] | RT u32[num_dnn] | D u64[num_dnn] | ideal]
+struct WsLayout {
+  size_t dtab, rt, d, ideal, end;
+};
+WsLayout ws_layout(const dstack_problem_t *pb, const dstack_params_t *p) {
+  WsLayout w;
+  const size_t nd = (size_t)(pb->num_dnn > 0 ? pb->num_dnn : 0);
+  w.dtab = align256(agg_ws_bytes());
+  w.rt = w.dtab + align256(nd * DTAB_ROW * 2);
+  w.d = w.rt + align256(nd * 4);
+  w.ideal = w.d + align256(nd * 8);
+  w.end = w.ideal + ((p->flags & DSTACK_FLAG_IDEAL) ? align256(ideal_ws_bytes(pb->num_rows)) : 0);
+  return w;
+}
 
 int finish(int rc) {
   if (rc != 0) return rc;
@@ -69,6 +95,41 @@ static int aggregate_impl(const dstack_problem_t *pb, dstack_out_t *out, void *w
 
 extern "C" {
 
+int dstack_profile_start(int32_t max_calls) {
+  if (max_calls < 1 || max_calls > 4096) return DSTACK_EINVAL;
+  if (!have_device()) return DSTACK_ELAUNCH;
+  ProfState &P = g_prof;
+  P.ev = new cudaEvent_t[(size_t)max_calls * (DSTACK_PROF_SLOTS + 1)];
+  for (int i = 0; i < max_calls * (DSTACK_PROF_SLOTS + 1); ++i) cudaEventCreate(&P.ev[i]);
+  P.used = new uint8_t[(size_t)max_calls * DSTACK_PROF_SLOTS]();
+  P.max_calls = max_calls; P.calls = 0; P.on = true;
+  return DSTACK_OK;
+}
+
+int dstack_profile_stop(double *ms_out, int32_t *calls) {
+  ProfState &P = g_prof;
+  if (!P.on) return DSTACK_EINVAL;
+  for (int k = 0; k < DSTACK_PROF_SLOTS; ++k) ms_out[k] = 0.0;
+  for (int c = 0; c < P.calls; ++c) {
+    cudaEvent_t *e = P.ev + c * (DSTACK_PROF_SLOTS + 1);
+    cudaEventSynchronize(e[DSTACK_PROF_SLOTS]);
+    for (int k = 0; k < DSTACK_PROF_SLOTS; ++k) {
+      if (!P.used[c * DSTACK_PROF_SLOTS + k]) continue;
+      // slot k spans from its own mark to the next recorded mark
+      int nx = k + 1;
+      while (nx < DSTACK_PROF_SLOTS && !P.used[c * DSTACK_PROF_SLOTS + nx]) ++nx;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e[k], e[nx]);
+      ms_out[k] += ms;
+    }
+  }
+  if (calls) *calls = P.calls;
+  for (int i = 0; i < P.max_calls * (DSTACK_PROF_SLOTS + 1); ++i) cudaEventDestroy(P.ev[i]);
+  delete[] P.ev; delete[] P.used;
+  P = ProfState();
+  return DSTACK_OK;
+}
+
 int dstack_version(void) { return 1; }
 
 int dstack_last_launch_count(void) { return g_launches; }
@@ -85,9 +146,7 @@ const char *dstack_status_str(int code) {
 
 size_t dstack_workspace_size(const dstack_problem_t *pb, const dstack_params_t *p) {
   if (!problem_ok(pb) || !params_ok(p)) return 0;
-  size_t sz = ws_ideal_off();
-  if (p->flags & DSTACK_FLAG_IDEAL) sz += align256(ideal_ws_bytes(pb->num_rows));
-  return sz;
+  return ws_layout(pb, p).end;
 }
 
 int dstack_knee(const dstack_problem_t *pb, const dstack_params_t *p, int32_t batch, uint16_t *knee_out,
@@ -135,16 +194,18 @@ static int ideal_impl(const dstack_problem_t *pb, const dstack_params_t *p, cons
 
 static int schedule_impl(const dstack_problem_t *pb, const dstack_params_t *p, const uint16_t *demand,
                          const uint8_t *batch, const uint32_t *alloc_q16, const dstack_cycle_hook_t *hook,
-                         dstack_out_t *out, void *ws, size_t ws_bytes, cudaStream_t s) {
+                         dstack_out_t *out, void *ws, size_t ws_bytes, cudaStream_t s, bool pre_ws = false) {
   CycArgs c;
   std::memset(&c, 0, sizeof(c));
   c.pb = *pb; c.p = *p; c.demand = demand; c.batch = batch; c.alloc = alloc_q16;
   if (hook) { c.hook_level = hook->level; c.hook_d = hook->d_slots; }
   c.level = out->level; c.runs = out->runs; c.served = out->served; c.scen_status = out->scen_status;
   c.T_us = out->T_us; c.u_static = out->u_static; c.u = out->u; c.thr = out->thr; c.misses = out->misses;
-  c.dtab_slab = (uint16_t *)((char *)ws + ws_dtab_off());
+  c.dtab_rows = (uint16_t *)((char *)ws + ws_layout(pb, p).dtab);
+  if (pre_ws) { c.ws_RT = (const uint32_t *)((char *)ws + ws_layout(pb, p).rt); c.ws_D = (const uint64_t *)((char *)ws + ws_layout(pb, p).d); }
   int rc = launch_cycle(c, s, &g_launches);
   if (rc) return rc;
+  if (pre_ws && (p->flags & DSTACK_FLAG_IDEAL)) prof_mark(s, 3);
   return ideal_impl(pb, p, demand, batch, hook, out, ws, s);
 }
 
@@ -157,7 +218,7 @@ static int ideal_impl(const dstack_problem_t *pb, const dstack_params_t *p, cons
     std::memset(&ia, 0, sizeof(ia));
     ia.pb = *pb; ia.p = *p; ia.demand = demand; ia.batch = batch; ia.u_ideal = out->u_ideal;
     ia.thr_ideal = out->thr_ideal;
-    rc = launch_ideal(ia, (char *)ws + ws_ideal_off(), s, &g_launches);
+    rc = launch_ideal(ia, (char *)ws + ws_layout(pb, p).ideal, s, &g_launches);
   }
   return rc;
 }
@@ -190,15 +251,24 @@ int dstack_eval_batch(const dstack_problem_t *pb, const dstack_params_t *p, dsta
   if (ws_bytes < need || (need > 0 && !ws)) return DSTACK_EWORKSPACE;
   if (!have_device()) return DSTACK_ELAUNCH;
   cudaStream_t s = (cudaStream_t)stream;
-  FusedArgs f;
-  std::memset(&f, 0, sizeof(f));
-  f.pb = *pb; f.p = *p; f.demand = out->demand; f.batch = out->batch; f.knee = out->knee; f.status = out->status;
-  f.alloc = out->alloc_q16; f.level = out->level; f.runs = out->runs; f.served = out->served;
-  f.scen_status = out->scen_status; f.T_us = out->T_us; f.u_static = out->u_static; f.u = out->u; f.thr = out->thr;
-  f.misses = out->misses; f.dtab_slab = (uint16_t *)((char *)ws + ws_dtab_off());
-  int rc = launch_fused(f, s, &g_launches);
-  if (!rc) rc = ideal_impl(pb, p, out->demand, out->batch, nullptr, out, ws, s);
-  if (!rc && out->agg) rc = aggregate_impl(pb, out, ws, s);
+  const WsLayout w = ws_layout(pb, p);
+  ProfArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.pb = *pb; a.p = *p; a.demand = out->demand; a.batch = out->batch; a.knee = out->knee; a.status = out->status;
+  a.dtab_rows = (uint16_t *)((char *)ws + w.dtab);
+  a.ws_RT = (uint32_t *)((char *)ws + w.rt);
+  a.ws_D = (uint64_t *)((char *)ws + w.d);
+  const bool prof = g_prof.on && g_prof.calls < g_prof.max_calls;
+  uint8_t *used = prof ? g_prof.used + g_prof.calls * DSTACK_PROF_SLOTS : nullptr;
+  if (prof) { used[0] = used[1] = used[2] = 1; used[3] = (p->flags & DSTACK_FLAG_IDEAL) ? 1 : 0; used[4] = out->agg ? 1 : 0; }
+  prof_mark(s, 0);
+  int rc = launch_prof(a, s, &g_launches);                                            // a1-a3
+  prof_mark(s, 1);
+  if (!rc) rc = launch_wmaxmin(pb->num_scen, pb->scen_dnn_off, p->L, out->demand, out->alloc_q16, s, &g_launches);
+  prof_mark(s, 2);
+  if (!rc) rc = schedule_impl(pb, p, out->demand, out->batch, out->alloc_q16, nullptr, out, ws, ws_bytes, s, true);
+  if (!rc && out->agg) { prof_mark(s, 4); rc = aggregate_impl(pb, out, ws, s); }
+  if (prof) { prof_mark(s, DSTACK_PROF_SLOTS); g_prof.calls++; }
   return finish(rc);
 }
 

@@ -29,7 +29,6 @@ __global__ void __launch_bounds__(CYC_WARPS * 32) k_cycle(CycArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   CycSmem &sm = reinterpret_cast<CycSmem *>(smem_raw)[warp];
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  uint16_t *dtab = a.dtab_slab + gwarp * DTAB_WORDS;
   const int32_t L = a.p.L, slot = a.p.slot_us, b_lo = a.p.b_min;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t s = gwarp; s < a.pb.num_scen; s += nwarps) {
@@ -67,24 +66,34 @@ __global__ void __launch_bounds__(CYC_WARPS * 32) k_cycle(CycArgs a) {
       if (nslots > DSTACK_MAX_SLOTS || njobs > DSTACK_MAX_JOBS) { sst = DSTACK_ST_INVALID; T = 0; }
     }
     if (sst == DSTACK_ST_OK) {
-      // runtimes d_j(b) = ceil(X(g_j, b) / (S(g_j) M Delta)), b in [b_lo, b*_j]
-      for (int j = 0; j < nd; ++j) {
+      // runtimes d_j(b) = ceil(X(g_j, b) / (S(g_j) M Delta)), b in [b_lo, b*_j], one u16 row per DNN.
+      // On the eval path k_prof already wrote them at g = demand (exact whenever WMAX-MIN did not raise
+      // the level, i.e. every oversubscribed scenario); only raised levels are recomputed from the rows.
+      uint16_t *dtab = a.dtab_rows + (int64_t)k0 * DTAB_ROW;
+      const bool need = active && (a.hook_level != nullptr || a.ws_RT == nullptr || g != dem);
+      uint32_t redo = __ballot_sync(FULL, need);
+      while (redo) {
+        const int j = __ffs(redo) - 1;
+        redo &= redo - 1;
         const uint32_t gj = __shfl_sync(FULL, g, j), bsj = __shfl_sync(FULL, bs, j);
-        if (gj == 0) continue;
         if (a.hook_level) {
           if (lane == 0) {
             const int32_t hd = a.hook_d[k0 + j];
-            dtab[j * DSTACK_MAX_BATCH + bsj - 1] = (uint16_t)(hd > 0xFFFF ? 0xFFFF : (hd < 0 ? 0 : hd));
+            dtab[j * DTAB_ROW + bsj - 1] = (uint16_t)(hd > 0xFFFF ? 0xFFFF : (hd < 0 ? 0 : hd));
           }
           __syncwarp();
           continue;
         }
-        const int64_t r0 = a.pb.dnn_row_off[k0 + j];
-        const int32_t K = (int32_t)(a.pb.dnn_row_off[k0 + j + 1] - r0);
         uint64_t RT = 0, D = 0;
-        for (int i = lane; i < K; i += 32) { RT += a.pb.r[r0 + i]; D += (uint64_t)a.pb.r[r0 + i] * a.pb.d[r0 + i]; }
-        RT = warp_sum_u64(RT); D = warp_sum_u64(D);
-        dtab_from_rows(a.pb, a.p, k0 + j, RT, D, (int32_t)gj, b_lo, (int32_t)bsj, dtab + j * DSTACK_MAX_BATCH, lane);
+        if (a.ws_RT) {
+          RT = a.ws_RT[k0 + j]; D = a.ws_D[k0 + j];
+        } else {
+          const int64_t r0 = a.pb.dnn_row_off[k0 + j];
+          const int32_t K = (int32_t)(a.pb.dnn_row_off[k0 + j + 1] - r0);
+          for (int i = lane; i < K; i += 32) { RT += a.pb.r[r0 + i]; D += (uint64_t)a.pb.r[r0 + i] * a.pb.d[r0 + i]; }
+          RT = warp_sum_u64(RT); D = warp_sum_u64(D);
+        }
+        dtab_from_rows(a.pb, a.p, k0 + j, RT, D, (int32_t)gj, b_lo, (int32_t)bsj, dtab + j * DTAB_ROW, lane);
       }
       cr = cycle_core(sm, dtab, lane, active, g, bs, sl, rep, nslots, L, b_lo, a.hook_level != nullptr, runs, served);
       if (cr.oversub) sst = DSTACK_ST_OVERSUBSCRIBED;
@@ -128,8 +137,7 @@ int launch_cycle(const CycArgs &a, cudaStream_t s, int *launches) {
   if (a.pb.num_scen <= 0) return 0;
   const size_t smem = sizeof(CycSmem) * CYC_WARPS;
   int64_t blocks = (a.pb.num_scen + CYC_WARPS - 1) / CYC_WARPS;
-  int64_t cap = (int64_t)num_sms() * 8;
-  if (cap * CYC_WARPS > DTAB_MAX_WARPS) cap = DTAB_MAX_WARPS / CYC_WARPS;
+  const int64_t cap = (int64_t)num_sms() * 8;
   if (blocks > cap) blocks = cap;
   cudaFuncSetAttribute(k_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_cycle<<<(unsigned)blocks, CYC_WARPS * 32, smem, s>>>(a);

@@ -25,8 +25,7 @@ struct CycSmem {
   uint16_t starts[DSTACK_MAX_JOBS];
 };
 
-// dtab layout: per warp, [DSTACK_MAX_DNN_PER_SCEN][DSTACK_MAX_BATCH] u16, entry b-1 = d_j(b) slots
-constexpr int DTAB_WORDS = DSTACK_MAX_DNN_PER_SCEN * DSTACK_MAX_BATCH;
+// dtab layout: one row of DSTACK_MAX_BATCH u16 per DNN of the scenario, entry b-1 = d_j(b) slots
 
 __device__ __forceinline__ uint32_t wmaxmin_lane(uint32_t dem, int lane, int nd, int32_t L) {
   const uint32_t key = (dem << 5) | (uint32_t)lane;   // dem == 0 for lanes >= nd

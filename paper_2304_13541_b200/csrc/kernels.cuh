@@ -4,8 +4,7 @@
 
 namespace dstack {
 
-constexpr int64_t DTAB_MAX_WARPS = 8192;   // per-warp d_j(b) scratch slabs in the workspace
-constexpr size_t DTAB_SLAB_BYTES = (size_t)DSTACK_MAX_DNN_PER_SCEN * DSTACK_MAX_BATCH * 2;
+constexpr int DTAB_ROW = DSTACK_MAX_BATCH;   // d_j(b) row per DNN in the workspace: u16[64], entry b-1
 
 inline int num_sms() {
   static thread_local int cached = 0;
@@ -27,6 +26,10 @@ struct ProfArgs {
   uint8_t *batch;
   uint16_t *knee;
   uint8_t *status;
+  // eval path extras (workspace, may be NULL): d_j(b) at g = demand for b in [b_lo, b*], RT, D
+  uint16_t *dtab_rows;
+  uint32_t *ws_RT;
+  uint64_t *ws_D;
 };
 
 struct CycArgs {
@@ -44,26 +47,9 @@ struct CycArgs {
   uint32_t *T_us;
   double *u_static, *u, *thr;
   uint32_t *misses;
-  uint16_t *dtab_slab;   // workspace: DTAB_MAX_WARPS slabs
-};
-
-// fused a1-a5 (dstack_eval_batch): warp per scenario
-struct FusedArgs {
-  dstack_problem_t pb;
-  dstack_params_t p;
-  uint16_t *demand;
-  uint8_t *batch;
-  uint16_t *knee;
-  uint8_t *status;
-  uint32_t *alloc;
-  uint16_t *level;
-  uint16_t *runs;
-  uint32_t *served;
-  uint8_t *scen_status;
-  uint32_t *T_us;
-  double *u_static, *u, *thr;
-  uint32_t *misses;
-  uint16_t *dtab_slab;
+  uint16_t *dtab_rows;     // workspace: num_dnn rows of DTAB_ROW u16
+  const uint32_t *ws_RT;   // non-NULL => dtab_rows already hold d_j(b) at g = demand (from k_prof)
+  const uint64_t *ws_D;
 };
 
 struct IdealArgs {
@@ -91,7 +77,6 @@ int launch_prof(const ProfArgs &a, cudaStream_t s, int *launches);
 int launch_wmaxmin(int32_t num_scen, const int32_t *off, int32_t L, const uint16_t *demand, uint32_t *alloc,
                    cudaStream_t s, int *launches);
 int launch_cycle(const CycArgs &a, cudaStream_t s, int *launches);
-int launch_fused(const FusedArgs &a, cudaStream_t s, int *launches);
 int launch_ideal(IdealArgs a, void *ws, cudaStream_t s, int *launches);
 int launch_agg(const AggArgs &a, cudaStream_t s, int *launches);
 size_t ideal_ws_bytes(int64_t num_rows);

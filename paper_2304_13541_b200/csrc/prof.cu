@@ -5,21 +5,34 @@
 
 namespace dstack {
 
+__host__ __device__ inline size_t prof_warp_bytes(int S_tot) {
+  return (((size_t)20 * (S_tot + 1)) + 15) & ~(size_t)15;   // cA, cU u64 + hist u32
+}
+
 template <int PAR>
-__global__ void __launch_bounds__(256) k_prof(ProfArgs a) {
+__global__ void __launch_bounds__(256, 4) k_prof(ProfArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int L = a.p.L, S_tot = a.p.S_tot;
   uint16_t *Stab = (uint16_t *)smem;
   const int stab_bytes = ((L + 1) * 2 + 15) & ~15;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint64_t *cA = (uint64_t *)(smem + stab_bytes) + (size_t)warp * 2 * (S_tot + 1);
+  unsigned char *wreg = smem + stab_bytes + (size_t)warp * prof_warp_bytes(S_tot);
+  uint64_t *cA = (uint64_t *)wreg;
   uint64_t *cU = cA + (S_tot + 1);
+  uint32_t *hist = (uint32_t *)(cU + (S_tot + 1));
   fill_stab(Stab, L, S_tot);
   __syncthreads();
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; k < a.pb.num_dnn; k += nwarps) {
-    const DnnRes r = analyze_dnn<PAR>(a.pb, a.p, k, Stab, cA, cU, lane, a.knee_only, a.knee_b);
+    const DnnRes r = analyze_dnn<PAR>(a.pb, a.p, k, Stab, hist, cA, cU, lane, a.knee_only, a.knee_b);
+    if (a.dtab_rows && r.st == DSTACK_ST_OK) {   // eval path: d_j(b) at g = demand, b in [b_lo, b*]
+      if (PAR == 0)
+        dtab_from_tables(a.pb, a.p, k, cA, cU, r.RT, r.D, r.demand, a.p.b_min, r.b, a.dtab_rows + k * DTAB_ROW, lane);
+      else
+        dtab_from_rows(a.pb, a.p, k, r.RT, r.D, r.demand, a.p.b_min, r.b, a.dtab_rows + k * DTAB_ROW, lane);
+    }
     if (lane == 0) {
+      if (a.ws_RT) { a.ws_RT[k] = (uint32_t)r.RT; a.ws_D[k] = r.D; }
       const bool ok = r.st == DSTACK_ST_OK;
       if (a.knee) a.knee[k] = ok ? r.knee : 0;
       if (a.status) a.status[k] = r.st;
@@ -33,7 +46,7 @@ __global__ void __launch_bounds__(256) k_prof(ProfArgs a) {
 }
 
 size_t prof_smem_bytes(const dstack_params_t *p, int warps) {
-  return (size_t)(((p->L + 1) * 2 + 15) & ~15) + (size_t)warps * 2 * 8 * (p->S_tot + 1);
+  return (size_t)(((p->L + 1) * 2 + 15) & ~15) + (size_t)warps * prof_warp_bytes(p->S_tot);
 }
 
 int launch_prof(const ProfArgs &a, cudaStream_t s, int *launches) {

@@ -96,15 +96,17 @@ __device__ __forceinline__ uint64_t cell_X(int32_t S, int32_t b, uint32_t magic,
 
 __device__ __forceinline__ uint32_t magic_of(int32_t b) { return b == 1 ? 0u : (uint32_t)(0xFFFFFFFFu / (uint32_t)b) + 1u; }
 
-// scan the histogram (counts in cA, weights in cU) into the coefficient tables, lane-chunked
-__device__ __forceinline__ void scan_tables(uint64_t *cA, uint64_t *cU, int S_tot, uint64_t Mtp, uint64_t W, int lane) {
+// Warp scan of the width histogram hist[0..S_tot] (u32 sums of R_i by n_i) into UNSCALED tables
+//   cA[m] = PA[m] = sum_{1<=n<=m} R,   cU[m] = Q[m] = W - sum_{n<=m} n R   (lane-chunked, 1 shuffle scan)
+__device__ __forceinline__ void scan_hist(const uint32_t *hist, uint64_t *cA, uint64_t *cU, int S_tot, uint64_t W,
+                                          int lane) {
   __syncwarp();
   const int C = (S_tot + 32) >> 5;          // bins per lane (S_tot+1 bins)
   const int m0 = lane * C;
   uint64_t sa = 0, sw = 0;
   for (int i = 0; i < C; ++i) {
     const int m = m0 + i;
-    if (m <= S_tot) { sa += cA[m]; sw += cU[m]; }
+    if (m <= S_tot && m >= 1) { const uint64_t h = hist[m]; sa += h; sw += h * (uint64_t)m; }
   }
   uint64_t pa = sa, pw = sw;   // inclusive scan of lane totals
 #pragma unroll
@@ -116,31 +118,34 @@ __device__ __forceinline__ void scan_tables(uint64_t *cA, uint64_t *cU, int S_to
   for (int i = 0; i < C; ++i) {
     const int m = m0 + i;
     if (m <= S_tot) {
-      pa += cA[m]; pw += cU[m];
-      cA[m] = Mtp * pa; cU[m] = Mtp * (W - pw);
+      if (m >= 1) { const uint64_t h = hist[m]; pa += h; pw += h * (uint64_t)m; }
+      cA[m] = pa; cU[m] = W - pw;
     }
   }
   __syncwarp();
 }
 
-// threads mode: histogram of N = ceil(b theta / 2048) and its scan
+__device__ __forceinline__ void scale_tables(uint64_t *cA, uint64_t *cU, int S_tot, uint64_t Mtp, int lane) {
+  for (int m = lane; m <= S_tot; m += 32) { cA[m] *= Mtp; cU[m] *= Mtp; }
+  __syncwarp();
+}
+
+// threads mode: tables of N = ceil(b theta / 2048) (rebuilt per b)
 __device__ __forceinline__ void build_tables_threads(const uint32_t *__restrict__ n, const uint16_t *__restrict__ r,
-                                                     int32_t K, int32_t S_tot, uint64_t Mtp, int32_t b, uint64_t *cA,
-                                                     uint64_t *cU, int lane) {
-  for (int m = lane; m <= S_tot; m += 32) { cA[m] = 0; cU[m] = 0; }
+                                                     int32_t K, int32_t S_tot, uint64_t Mtp, int32_t b,
+                                                     uint32_t *hist, uint64_t *cA, uint64_t *cU, int lane) {
+  for (int m = lane; m <= S_tot; m += 32) hist[m] = 0;
   __syncwarp();
   uint64_t W = 0;
   for (int i = lane; i < K; i += 32) {
     const uint64_t N = ((uint64_t)b * n[i] + 2047) >> 11;
     const uint32_t R = r[i];
     W += (uint64_t)R * N;
-    if (N >= 1 && N <= (uint64_t)S_tot) {
-      atomicAdd((unsigned long long *)&cA[N], (unsigned long long)R);
-      atomicAdd((unsigned long long *)&cU[N], (unsigned long long)(R * N));
-    }
+    if (N <= (uint64_t)S_tot) atomicAdd(&hist[N], R);
   }
   W = warp_sum_u64(W);
-  scan_tables(cA, cU, S_tot, Mtp, W, lane);
+  scan_hist(hist, cA, cU, S_tot, W, lane);
+  scale_tables(cA, cU, S_tot, Mtp, lane);
 }
 
 struct RowCtx {
@@ -181,9 +186,10 @@ __device__ __forceinline__ bool sup_reaches(double b, double alpha, double beta,
 }
 
 // Analyse DNN k.  knee_only: status + knee at knee_b.  Otherwise (l*, b*), demand, knee(b*).
+// Per-warp shared memory: hist[S_tot+1] u32, cA/cU[S_tot+1] u64 (tables stay valid on return).
 template <int PAR>
 __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k, const uint16_t *Stab,
-                              uint64_t *cA, uint64_t *cU, int lane, int knee_only, int32_t knee_b) {
+                              uint32_t *hist, uint64_t *cA, uint64_t *cU, int lane, int knee_only, int32_t knee_b) {
   DnnRes res; res.st = DSTACK_ST_OK; res.demand = 0; res.knee = 0; res.b = 0; res.RT = 0; res.D = 0;
   const int L = p.L, S_tot = p.S_tot;
   const int64_t r0 = pb.dnn_row_off[k], r1 = pb.dnn_row_off[k + 1];
@@ -205,42 +211,49 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
   const uint32_t *n = pb.n + r0;
   const uint16_t *r = pb.r + r0;
   const uint32_t *d = pb.d + r0;
-  // ---- a1: one coalesced pass over the rows ----
+  // ---- a1: one coalesced pass over the rows (two rows per lane in flight) ----
   if (PAR == 0) {
-    for (int m = lane; m <= S_tot; m += 32) { cA[m] = 0; cU[m] = 0; }
+    for (int m = lane; m <= S_tot; m += 32) hist[m] = 0;
     __syncwarp();
   }
-  uint64_t RT = 0, D = 0, Wn = 0, Vmax = 0, RT1 = 0;
-  uint32_t anyR0 = 0, anyN = 0;
-  auto row = [&](uint64_t nn, uint32_t R, uint64_t dd) {
+  uint32_t RT = 0, anyR0 = 0;
+  uint64_t D = 0, Wn = 0, Vmax = 0;
+  auto row = [&](uint32_t nn, uint32_t R, uint32_t dd) {
     RT += R; D += (uint64_t)R * dd; Wn += (uint64_t)R * nn;
-    if (nn != 0) RT1 += R;
-    anyR0 |= (R == 0); anyN |= (nn != 0);
-    const uint64_t Nb = PAR == 0 ? (uint64_t)b_eval * nn : ((uint64_t)b_eval * nn + 2047) >> 11;
-    if (Nb >= 1) Vmax = sat_add(Vmax, (uint64_t)R * (Nb > (uint64_t)S_tot ? Nb : (uint64_t)S_tot));
-    if (PAR == 0 && nn >= 1 && nn <= (uint64_t)S_tot) {
-      atomicAdd((unsigned long long *)&cA[nn], (unsigned long long)R);
-      atomicAdd((unsigned long long *)&cU[nn], (unsigned long long)(R * nn));
+    anyR0 |= (R == 0);
+    if (PAR == 0) {
+      if (nn <= (uint32_t)S_tot) atomicAdd(&hist[nn], R);   // width histogram incl. n = 0 (bin 0)
+    } else {
+      const uint64_t Nb = ((uint64_t)b_eval * nn + 2047) >> 11;
+      if (Nb >= 1) Vmax = sat_add(Vmax, (uint64_t)R * (Nb > (uint64_t)S_tot ? Nb : (uint64_t)S_tot));
     }
   };
-  // two rows per lane in flight per iteration (loads issued before the dependent histogram atomics)
   for (int i0 = lane; i0 < K; i0 += 64) {
     const int i1 = i0 + 32;
     const bool h1 = i1 < K;
-    const uint64_t n0 = __ldg(n + i0), d0 = __ldg(d + i0);
+    const uint32_t n0 = __ldg(n + i0), d0 = __ldg(d + i0);
     const uint32_t R0 = __ldg(r + i0);
-    uint64_t n1 = 0, d1 = 0;
-    uint32_t R1 = 0;
+    uint32_t n1 = 0, d1 = 0, R1 = 0;
     if (h1) { n1 = __ldg(n + i1); d1 = __ldg(d + i1); R1 = __ldg(r + i1); }
     row(n0, R0, d0);
     if (h1) row(n1, R1, d1);
   }
-  RT = warp_sum_u64(RT); D = warp_sum_u64(D); Wn = warp_sum_u64(Wn); Vmax = warp_sum_sat(Vmax);
-  RT1 = warp_sum_u64(RT1);
-  anyR0 = warp_or(anyR0); anyN = warp_or(anyN);
+  RT = __reduce_add_sync(FULL, RT);
+  D = warp_sum_u64(D); Wn = warp_sum_u64(Wn);
+  if (PAR == 1) Vmax = warp_sum_sat(Vmax);
+  anyR0 = warp_or(anyR0);
   res.RT = RT; res.D = D;
-  if (anyR0 || (t_np == 0 && !anyN && (mem_mode == 0 || D == 0))) { res.st = DSTACK_ST_INVALID; return res; }
+  // (R_i >= 1 for all rows) => "some n_i != 0" <=> Wn > 0
+  if (anyR0 || (t_np == 0 && Wn == 0 && (mem_mode == 0 || D == 0))) { res.st = DSTACK_ST_INVALID; return res; }
   if (!knee_only && b_hi < b_lo) { res.st = DSTACK_ST_INFEASIBLE; return res; }
+  if (PAR == 0) {
+    scan_hist(hist, cA, cU, S_tot, Wn, lane);
+    // sum_{N_i >= 1} R_i max(S_tot, b n_i) = S_tot PA[S_tot/b] + b Q[S_tot/b]  (exact, from the tables)
+    const int mb = S_tot / b_eval;
+    Vmax = 0;
+    const u128 v = (u128)S_tot * cA[mb] + (u128)b_eval * cU[mb];
+    Vmax = v >= ((u128)1 << 63) ? (1ull << 63) : (uint64_t)v;
+  }
   {
     // X(L, b_eval) = w t_np RT S_tot M + M t_p Vmax + mem  (the maximum of X over the grid)
     const u128 w = p.wse_mode == 0 ? (u128)b_eval : (u128)1;
@@ -250,26 +263,27 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
     if (Vmax >= (1ull << 63) || Xub >= (u128)X_LIMIT) { res.st = DSTACK_ST_OVERFLOW; return res; }
   }
   const uint64_t Mtp = M * (uint64_t)t_p;
-  if (PAR == 0) scan_tables(cA, cU, S_tot, Mtp, Wn, lane);
+  const uint64_t RT1 = PAR == 0 ? (uint64_t)RT - hist[0] : 0ull;   // sum R over n_i >= 1
+  if (PAR == 0) scale_tables(cA, cU, S_tot, Mtp, lane);
   RowCtx c;
   c.Stab = Stab; c.cA = cA; c.cU = cU; c.L = L; c.mem_mode = mem_mode; c.wse = p.wse_mode;
   c.C1 = (uint64_t)t_np * RT * M; c.D = D; c.SLOM = (uint64_t)slo * M; c.aM = (uint64_t)asm_us * M;
   Best e, kk;
   if (knee_only) {
-    if (PAR == 1) build_tables_threads(n, r, K, S_tot, Mtp, knee_b, cA, cU, lane);
+    if (PAR == 1) build_tables_threads(n, r, K, S_tot, Mtp, knee_b, hist, cA, cU, lane);
     eval_row<PAR>(c, knee_b, lane, e, kk);
     res.knee = (uint16_t)kk.l;
     return res;
   }
   // ---- a3: exact branch-and-bound over (l, b) ----
-  if (PAR == 1) build_tables_threads(n, r, K, S_tot, Mtp, b_lo, cA, cU, lane);
+  if (PAR == 1) build_tables_threads(n, r, K, S_tot, Mtp, b_lo, hist, cA, cU, lane);
   eval_row<PAR>(c, b_lo, lane, e, kk);
   if (!e.found) { res.st = DSTACK_ST_INFEASIBLE; return res; }
   Best best = e;
   uint32_t knee = kk.l;
   if (PAR == 1) {
     for (int32_t b = b_lo + 1; b <= b_hi; ++b) {
-      build_tables_threads(n, r, K, S_tot, Mtp, b, cA, cU, lane);
+      build_tables_threads(n, r, K, S_tot, Mtp, b, hist, cA, cU, lane);
       eval_row<1>(c, b, lane, e, kk);
       if (better(e, best)) { best = e; knee = kk.l; }
     }

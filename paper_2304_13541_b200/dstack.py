@@ -78,6 +78,8 @@ def _load():
                                           P(COut), C.c_void_p, C.c_size_t, C.c_void_p]
     lib.dstack_eval_batch.argtypes = [P(CProblem), P(CParams), P(COut), C.c_void_p, C.c_size_t, C.c_void_p]
     lib.dstack_aggregate.argtypes = [P(CProblem), P(CParams), P(COut), C.c_void_p, C.c_size_t, C.c_void_p]
+    lib.dstack_profile_start.argtypes = [C.c_int32]
+    lib.dstack_profile_stop.argtypes = [C.c_void_p, C.c_void_p]
     lib.dstack_status_str.restype = C.c_char_p
     lib.dstack_last_launch_count.restype = C.c_int
     return lib
@@ -87,7 +89,8 @@ _lib = _load()
 
 # every symbol include/dstack.h declares (checked by tests/test_abi.py)
 EXPORTS = ("dstack_workspace_size", "dstack_knee", "dstack_batch_opt", "dstack_wmaxmin", "dstack_schedule_cycle",
-           "dstack_eval_batch", "dstack_aggregate", "dstack_last_launch_count", "dstack_status_str", "dstack_version")
+           "dstack_eval_batch", "dstack_aggregate", "dstack_profile_start", "dstack_profile_stop",
+           "dstack_last_launch_count", "dstack_status_str", "dstack_version")
 
 
 def lib():
@@ -263,6 +266,22 @@ def eval_batch(dp: DeviceProblem, p, out=None, ws: Workspace | None = None, agg=
     _check(_lib.dstack_eval_batch(C.byref(dp.c()), C.byref(cparams(p)), C.byref(_cout(o)), ws.ptr(), ws.nbytes,
                                   _stream(dev)), "dstack_eval_batch")
     return o
+
+
+PROF_SLOTS = ("k_prof", "k_wmaxmin", "k_cycle", "k_ideal", "k_agg")
+
+
+def profile_start(max_calls: int):
+    """Record CUDA events between the kernels of the next eval_batch calls on this thread."""
+    _check(_lib.dstack_profile_start(max_calls), "dstack_profile_start")
+
+
+def profile_stop() -> tuple[dict, int]:
+    """Synchronise the recorded events: (summed ms per kernel slot, number of profiled calls)."""
+    ms = (C.c_double * len(PROF_SLOTS))()
+    calls = C.c_int32()
+    _check(_lib.dstack_profile_stop(ms, C.byref(calls)), "dstack_profile_stop")
+    return {k: ms[i] for i, k in enumerate(PROF_SLOTS)}, calls.value
 
 
 def last_launch_count() -> int:
