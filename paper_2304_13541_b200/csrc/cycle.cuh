@@ -78,9 +78,57 @@ __device__ __forceinline__ int find_late(const uint8_t *occ, int rel, int dl, in
   return -1;
 }
 
+// byte mask of slots [lo, hi) of a 4-slot word (0 <= lo, hi <= 4)
+__device__ __forceinline__ uint32_t bytes_mask(int lo, int hi) {
+  if (hi <= lo) return 0u;
+  const uint32_t up = hi >= 4 ? 0xFFFFFFFFu : ((1u << (8 * hi)) - 1u);
+  return up & ~((1u << (8 * lo)) - 1u);
+}
+
+// occ[u] += g for u in [s, s+d): 4 slots per lane per step (packed u32; callers guarantee occ + g <= L <= 255,
+// so no byte carries).
 __device__ __forceinline__ void occ_add(uint8_t *occ, int s, int d, int g, int lane) {
-  for (int u = s + lane; u < s + d; u += 32) occ[u] = (uint8_t)(occ[u] + g);
+  const int e = s + d;
+  uint32_t *w32 = reinterpret_cast<uint32_t *>(occ);
+  const uint32_t gg = (uint32_t)g * 0x01010101u;
+  for (int w0 = s >> 2; (w0 << 2) < e; w0 += 32) {
+    const int w = w0 + lane, base = w << 2;
+    if (base < e) {
+      const uint32_t m = bytes_mask(s - base > 0 ? s - base : 0, e - base < 4 ? e - base : 4);
+      if (m) w32[w] += gg & m;
+    }
+  }
   __syncwarp();
+}
+
+// first u in [t, stop) with occ[u] > thr, or stop (4 slots per lane per step)
+__device__ __forceinline__ int first_above(const uint8_t *occ, int t, int stop, int thr, int lane) {
+  const uint32_t *w32 = reinterpret_cast<const uint32_t *>(occ);
+  const uint32_t th = (uint32_t)thr * 0x01010101u;
+  for (int w0 = t >> 2; (w0 << 2) < stop; w0 += 32) {
+    const int w = w0 + lane, base = w << 2;
+    uint32_t bb = 0;
+    if (base < stop) {
+      bb = __vcmpgtu4(w32[w], th) & bytes_mask(t - base > 0 ? t - base : 0, stop - base < 4 ? stop - base : 4);
+    }
+    const uint32_t bal = __ballot_sync(FULL, bb != 0);
+    if (bal) {
+      const int pl = __ffs(bal) - 1;
+      const uint32_t b = __shfl_sync(FULL, bb, pl);
+      return ((w0 + pl) << 2) + ((__ffs(b) - 1) >> 3);
+    }
+  }
+  return stop;
+}
+
+__device__ __forceinline__ uint32_t occ_sum(const uint8_t *occ, int nslots, int lane) {
+  const uint32_t *w32 = reinterpret_cast<const uint32_t *>(occ);
+  uint32_t s = 0;
+  for (int w = lane; (w << 2) < nslots; w += 32) {
+    const int base = w << 2;
+    s += __vsadu4(w32[w] & bytes_mask(0, nslots - base < 4 ? nslots - base : 4), 0u);
+  }
+  return __reduce_add_sync(FULL, s);
 }
 
 struct CycRes {
@@ -95,7 +143,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
                                             uint32_t bs, uint32_t sl, uint32_t rep, int32_t nslots, int32_t L,
                                             int32_t b_lo, bool hook_b_only, uint32_t &runs, uint32_t &served) {
   CycRes res; res.occ_static = 0; res.occ_all = 0; res.served_tot = 0; res.misses = 0; res.oversub = false;
-  for (int u = lane; u < nslots; u += 32) sm.occ[u] = 0;
+  for (int w = lane; (w << 2) < nslots; w += 32) reinterpret_cast<uint32_t *>(sm.occ)[w] = 0u;
   for (int w = lane; w < DSTACK_MAX_SLOTS / 32; w += 32) sm.dmask[w] = 0;
   __syncwarp();
   uint32_t joff = rep;   // exclusive prefix of rep over lanes
@@ -139,14 +187,13 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     if (lane == j) nextr++;
     __syncwarp();
   }
-  uint32_t osum = 0;
-  for (int u = lane; u < nslots; u += 32) osum += sm.occ[u];
-  res.occ_static = __reduce_add_sync(FULL, osum);
+  res.occ_static = occ_sum(sm.occ, nslots, lane);
   // ---- opportunistic fill at decision times {0} u {run ends} (Dynamic-schedule) ----
   if (lane == 0) sm.dmask[0] |= 1u;
   __syncwarp();
   uint32_t count = runs;
-  int fs = -1, fe = -1;
+  int fs = -1, fe = -1;       // last fill run of this lane's DNN
+  int nsr = 0;                // first static window whose run starts after t (amortised, t only grows)
   const uint32_t sl_magic = sl <= 1 ? 0u : (uint32_t)(0xFFFFFFFFu / sl) + 1u;   // t / sl = umulhi(t, magic), t < 2^13
   const int nwords = (nslots + 31) >> 5;
   int t = -1;
@@ -169,49 +216,41 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     t = nt;
     int occ_t = sm.occ[t];
     bool elig = false;
-    int rr = 0;
-    if (active) {   // eligible: not running at t (static run of window rr or the last fill), fits at t
-      rr = sl == 1 ? t : (int)__umulhi((uint32_t)t, sl_magic);
+    int ns = nslots;
+    if (active) {   // eligible: not running at t (static run of window t/sl or the last fill), fits at t
+      const int rr = sl == 1 ? t : (int)__umulhi((uint32_t)t, sl_magic);
       bool covered = (fs <= t && t < fe);
       if (rr < (int)rep) {
         const uint16_t s0 = sm.starts[joff + rr];
         if (s0 != NONE16 && (int)s0 <= t && t < (int)s0 + (int)dstar) covered = true;
       }
+      while (nsr < (int)rep) {
+        const uint16_t s2 = sm.starts[joff + nsr];
+        if (s2 != NONE16 && (int)s2 > t) { ns = s2; break; }
+        ++nsr;
+      }
       elig = !covered && occ_t + (int)g <= L;
     }
+    // candidates in (runs so far, index) order; a placement raises occ[t], so re-test the rest in parallel
     uint32_t key = elig ? ((count << 5) | (uint32_t)lane) : 0xFFFFFFFFu;
     while (true) {
       const uint32_t mk = __reduce_min_sync(FULL, key);
       if (mk == 0xFFFFFFFFu) break;
       const int j = (int)(mk & 31u);
+      if (lane == j) key = 0xFFFFFFFFu;
       const int gj = (int)__shfl_sync(FULL, g, j);
-      if (occ_t + gj > L) { if (lane == j) key = 0xFFFFFFFFu; continue; }
-      int ns = nslots;   // next start of j after t (only static runs can start later)
-      if (lane == j) {
-        key = 0xFFFFFFFFu;
-        for (int r2 = rr; r2 < (int)rep; ++r2) {
-          const uint16_t s2 = sm.starts[joff + r2];
-          if (s2 != NONE16 && (int)s2 > t) { ns = s2; break; }
-        }
-      }
       const int limit = __shfl_sync(FULL, ns, j);
       const int bsj = (int)__shfl_sync(FULL, bs, j);
       const int dsj = (int)__shfl_sync(FULL, dstar, j);
       // slice k = first u in [t, limit) with occ[u] + g > L; only k >= d(b*) or its exact value below matters
       const int stop = t + dsj < limit ? t + dsj : limit;
-      int kslice = stop - t;
-      for (int base = t; base < stop; base += 32) {
-        const int u = base + lane;
-        const bool blocked = u < stop && (int)sm.occ[u] + gj > L;
-        const uint32_t bal = __ballot_sync(FULL, blocked);
-        if (bal) { kslice = base + __ffs(bal) - 1 - t; break; }
-      }
+      const int kslice = first_above(sm.occ, t, stop, L - gj, lane) - t;
       int bsel = 0;   // largest b in [b_lo, b*] with d(b) <= slice (d nondecreasing in b)
       const uint16_t *dj = dtab + j * DSTACK_MAX_BATCH;
       if (kslice >= dsj) {
         bsel = bsj;
-      } else if (!hook_b_only) {
-        for (int b0 = b_lo + 32 * ((bsj - 1 - b_lo) >> 5); b0 >= b_lo && bsj - 1 >= b_lo; b0 -= 32) {
+      } else if (!hook_b_only && bsj - 1 >= b_lo) {
+        for (int b0 = b_lo + 32 * ((bsj - 1 - b_lo) >> 5); b0 >= b_lo; b0 -= 32) {
           const int b = b0 + lane;
           const bool ok = b < bsj && (int)dj[b - 1] <= kslice;
           const uint32_t bal = __ballot_sync(FULL, ok);
@@ -225,11 +264,10 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       if (lane == 0 && t + dsel < nslots) sm.dmask[(t + dsel) >> 5] |= 1u << ((t + dsel) & 31);
       __syncwarp();
       if (lane == j) { count++; runs++; served += (uint32_t)bsel; fs = t; fe = t + dsel; }
+      if (occ_t + (int)g > L) key = 0xFFFFFFFFu;
     }
   }
-  osum = 0;
-  for (int u = lane; u < nslots; u += 32) osum += sm.occ[u];
-  res.occ_all = __reduce_add_sync(FULL, osum);
+  res.occ_all = occ_sum(sm.occ, nslots, lane);
   res.served_tot = __reduce_add_sync(FULL, served);
   return res;
 }

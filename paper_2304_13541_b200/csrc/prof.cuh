@@ -96,10 +96,11 @@ __device__ __forceinline__ uint64_t cell_X(int32_t S, int32_t b, uint32_t magic,
 
 __device__ __forceinline__ uint32_t magic_of(int32_t b) { return b == 1 ? 0u : (uint32_t)(0xFFFFFFFFu / (uint32_t)b) + 1u; }
 
-// Warp scan of the width histogram hist[0..S_tot] (u32 sums of R_i by n_i) into UNSCALED tables
-//   cA[m] = PA[m] = sum_{1<=n<=m} R,   cU[m] = Q[m] = W - sum_{n<=m} n R   (lane-chunked, 1 shuffle scan)
+// Warp scan of the width histogram hist[0..S_tot] (u32 sums of R_i by n_i) into the SCALED tables
+//   cA[m] = Mtp * PA[m], PA[m] = sum_{1<=n<=m} R;   cU[m] = Mtp * Q[m], Q[m] = W - sum_{n<=m} n R
+// (lane-chunked, one shuffle scan).  Returns the unscaled PA[mb], Q[mb] in *pa_mb, *q_mb (all lanes).
 __device__ __forceinline__ void scan_hist(const uint32_t *hist, uint64_t *cA, uint64_t *cU, int S_tot, uint64_t W,
-                                          int lane) {
+                                          uint64_t Mtp, int mb, uint64_t *pa_mb, uint64_t *q_mb, int lane) {
   __syncwarp();
   const int C = (S_tot + 32) >> 5;          // bins per lane (S_tot+1 bins)
   const int m0 = lane * C;
@@ -115,18 +116,18 @@ __device__ __forceinline__ void scan_hist(const uint32_t *hist, uint64_t *cA, ui
     if (lane >= d) { pa += ua; pw += uw; }
   }
   pa -= sa; pw -= sw;          // exclusive
+  uint64_t a_mb = 0, q_m = 0;
   for (int i = 0; i < C; ++i) {
     const int m = m0 + i;
     if (m <= S_tot) {
       if (m >= 1) { const uint64_t h = hist[m]; pa += h; pw += h * (uint64_t)m; }
-      cA[m] = pa; cU[m] = W - pw;
+      cA[m] = Mtp * pa; cU[m] = Mtp * (W - pw);
+      if (m == mb) { a_mb = pa; q_m = W - pw; }
     }
   }
-  __syncwarp();
-}
-
-__device__ __forceinline__ void scale_tables(uint64_t *cA, uint64_t *cU, int S_tot, uint64_t Mtp, int lane) {
-  for (int m = lane; m <= S_tot; m += 32) { cA[m] *= Mtp; cU[m] *= Mtp; }
+  const int owner = mb / C;
+  *pa_mb = shfl_u64(a_mb, owner);
+  *q_mb = shfl_u64(q_m, owner);
   __syncwarp();
 }
 
@@ -144,8 +145,8 @@ __device__ __forceinline__ void build_tables_threads(const uint32_t *__restrict_
     if (N <= (uint64_t)S_tot) atomicAdd(&hist[N], R);
   }
   W = warp_sum_u64(W);
-  scan_hist(hist, cA, cU, S_tot, W, lane);
-  scale_tables(cA, cU, S_tot, Mtp, lane);
+  uint64_t pa, q;
+  scan_hist(hist, cA, cU, S_tot, W, Mtp, 0, &pa, &q, lane);
 }
 
 struct RowCtx {
@@ -246,25 +247,35 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
   // (R_i >= 1 for all rows) => "some n_i != 0" <=> Wn > 0
   if (anyR0 || (t_np == 0 && Wn == 0 && (mem_mode == 0 || D == 0))) { res.st = DSTACK_ST_INVALID; return res; }
   if (!knee_only && b_hi < b_lo) { res.st = DSTACK_ST_INFEASIBLE; return res; }
+  const uint64_t Mtp = M * (uint64_t)t_p;
   if (PAR == 0) {
-    scan_hist(hist, cA, cU, S_tot, Wn, lane);
-    // sum_{N_i >= 1} R_i max(S_tot, b n_i) = S_tot PA[S_tot/b] + b Q[S_tot/b]  (exact, from the tables)
+    // sum_{N_i >= 1} R_i max(S_tot, b n_i) = S_tot PA[S_tot/b] + b Q[S_tot/b]  (exact, from the scan)
     const int mb = S_tot / b_eval;
-    Vmax = 0;
-    const u128 v = (u128)S_tot * cA[mb] + (u128)b_eval * cU[mb];
+    uint64_t pa_mb, q_mb;
+    scan_hist(hist, cA, cU, S_tot, Wn, Mtp, mb, &pa_mb, &q_mb, lane);
+    const u128 v = (u128)S_tot * pa_mb + (u128)b_eval * q_mb;
     Vmax = v >= ((u128)1 << 63) ? (1ull << 63) : (uint64_t)v;
   }
   {
-    // X(L, b_eval) = w t_np RT S_tot M + M t_p Vmax + mem  (the maximum of X over the grid)
-    const u128 w = p.wse_mode == 0 ? (u128)b_eval : (u128)1;
-    u128 Xub = w * (u128)t_np * (u128)RT * (u128)S_tot * (u128)M + (u128)M * (u128)t_p * (u128)Vmax;
-    if (mem_mode == 1) Xub += (u128)b_eval * (u128)D;
-    else if (mem_mode == 2) Xub += (u128)b_eval * (u128)D * (u128)(S_tot * S_tot);
-    if (Vmax >= (1ull << 63) || Xub >= (u128)X_LIMIT) { res.st = DSTACK_ST_OVERFLOW; return res; }
+    // X(L, b_eval) = w t_np RT S_tot M + M t_p Vmax + mem  (the maximum of X over the grid).  An f64
+    // estimate settles all but |X - 2^56| < 1e-4 X; those are decided in exact 128-bit arithmetic.
+    const double wd = p.wse_mode == 0 ? (double)b_eval : 1.0;
+    double xe = wd * (double)t_np * (double)RT * (double)S_tot * (double)M + (double)M * (double)t_p * (double)Vmax;
+    if (mem_mode == 1) xe += (double)b_eval * (double)D;
+    else if (mem_mode == 2) xe += (double)b_eval * (double)D * (double)(S_tot * S_tot);
+    bool over;
+    if (Vmax >= (1ull << 63) || xe >= 72057594037927936.0 * 1.0001) over = true;
+    else if (xe < 72057594037927936.0 * 0.9999) over = false;
+    else {
+      const u128 w = p.wse_mode == 0 ? (u128)b_eval : (u128)1;
+      u128 Xub = w * (u128)t_np * (u128)RT * (u128)S_tot * (u128)M + (u128)M * (u128)t_p * (u128)Vmax;
+      if (mem_mode == 1) Xub += (u128)b_eval * (u128)D;
+      else if (mem_mode == 2) Xub += (u128)b_eval * (u128)D * (u128)(S_tot * S_tot);
+      over = Xub >= (u128)X_LIMIT;
+    }
+    if (over) { res.st = DSTACK_ST_OVERFLOW; return res; }
   }
-  const uint64_t Mtp = M * (uint64_t)t_p;
   const uint64_t RT1 = PAR == 0 ? (uint64_t)RT - hist[0] : 0ull;   // sum R over n_i >= 1
-  if (PAR == 0) scale_tables(cA, cU, S_tot, Mtp, lane);
   RowCtx c;
   c.Stab = Stab; c.cA = cA; c.cU = cU; c.L = L; c.mem_mode = mem_mode; c.wse = p.wse_mode;
   c.C1 = (uint64_t)t_np * RT * M; c.D = D; c.SLOM = (uint64_t)slo * M; c.aM = (uint64_t)asm_us * M;
