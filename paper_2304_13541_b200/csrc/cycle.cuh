@@ -78,11 +78,10 @@ __device__ __forceinline__ int find_late(const uint8_t *occ, int rel, int dl, in
   return -1;
 }
 
-// byte mask of slots [lo, hi) of a 4-slot word (0 <= lo, hi <= 4)
-__device__ __forceinline__ uint32_t bytes_mask(int lo, int hi) {
-  if (hi <= lo) return 0u;
-  const uint32_t up = hi >= 4 ? 0xFFFFFFFFu : ((1u << (8 * hi)) - 1u);
-  return up & ~((1u << (8 * lo)) - 1u);
+// byte mask of slots [lo, hi) of a 4-slot word starting at slot `base` (lo/hi are clamped to [0, 4])
+__device__ __forceinline__ uint32_t bytes_mask(int s, int e, int base) {
+  const int lo = min(max(s - base, 0), 4), hi = min(max(e - base, 0), 4);
+  return (uint32_t)((0xFFFFFFFFull << (8 * lo)) & (0xFFFFFFFFull >> (32 - 8 * hi)));
 }
 
 // occ[u] += g for u in [s, s+d): 4 slots per lane per step (packed u32; callers guarantee occ + g <= L <= 255,
@@ -94,8 +93,7 @@ __device__ __forceinline__ void occ_add(uint8_t *occ, int s, int d, int g, int l
   for (int w0 = s >> 2; (w0 << 2) < e; w0 += 32) {
     const int w = w0 + lane, base = w << 2;
     if (base < e) {
-      const uint32_t m = bytes_mask(s - base > 0 ? s - base : 0, e - base < 4 ? e - base : 4);
-      if (m) w32[w] += gg & m;
+      w32[w] += gg & bytes_mask(s, e, base);
     }
   }
   __syncwarp();
@@ -107,10 +105,7 @@ __device__ __forceinline__ int first_above(const uint8_t *occ, int t, int stop, 
   const uint32_t th = (uint32_t)thr * 0x01010101u;
   for (int w0 = t >> 2; (w0 << 2) < stop; w0 += 32) {
     const int w = w0 + lane, base = w << 2;
-    uint32_t bb = 0;
-    if (base < stop) {
-      bb = __vcmpgtu4(w32[w], th) & bytes_mask(t - base > 0 ? t - base : 0, stop - base < 4 ? stop - base : 4);
-    }
+    const uint32_t bb = base < stop ? (__vcmpgtu4(w32[w], th) & bytes_mask(t, stop, base)) : 0u;
     const uint32_t bal = __ballot_sync(FULL, bb != 0);
     if (bal) {
       const int pl = __ffs(bal) - 1;
@@ -126,7 +121,7 @@ __device__ __forceinline__ uint32_t occ_sum(const uint8_t *occ, int nslots, int 
   uint32_t s = 0;
   for (int w = lane; (w << 2) < nslots; w += 32) {
     const int base = w << 2;
-    s += __vsadu4(w32[w] & bytes_mask(0, nslots - base < 4 ? nslots - base : 4), 0u);
+    s += __vsadu4(w32[w] & bytes_mask(0, nslots, base), 0u);
   }
   return __reduce_add_sync(FULL, s);
 }

@@ -31,16 +31,22 @@ __device__ __forceinline__ Best best_none() {
   return r;
 }
 
+// exact comparison of two candidates whose float scores are within the filter tolerance (rare)
+static __device__ __noinline__ bool better_exact(uint32_t cb, uint32_t cS, uint64_t cX, uint32_t cl, uint32_t ob, uint32_t oS,
+                                          uint64_t oX, uint32_t ol) {
+  const u128 L = (u128)(cb * cS) * ((u128)oX * oX);
+  const u128 R = (u128)(ob * oS) * ((u128)cX * cX);
+  if (L != R) return L > R;
+  return cl < ol || (cl == ol && cb < ob);
+}
+
 // exact total order: higher eta = b S / X^2, then smaller l, then smaller b
 __device__ __forceinline__ bool better(const Best &c, const Best &o) {
   if (!c.found) return false;
   if (!o.found) return true;
   if (c.sc > o.sc * 1.0000077f) return true;    // 1 + 2^-17
   if (o.sc > c.sc * 1.0000077f) return false;
-  const u128 L = (u128)(c.b * c.S) * ((u128)o.X * o.X);
-  const u128 R = (u128)(o.b * o.S) * ((u128)c.X * c.X);
-  if (L != R) return L > R;
-  return c.l < o.l || (c.l == o.l && c.b < o.b);
+  return better_exact(c.b, c.S, c.X, c.l, o.b, o.S, o.X, o.l);
 }
 
 __device__ __forceinline__ float score_f(uint32_t P, uint64_t X) {
@@ -58,6 +64,15 @@ __device__ __forceinline__ Best shfl_best(const Best &v, int src) {
   return o;
 }
 
+static __device__ __noinline__ Best warp_best_exact(Best v) {
+#pragma unroll 1
+  for (int m = 16; m; m >>= 1) {
+    Best o = shfl_best(v, (threadIdx.x & 31) ^ m);
+    if (better(o, v)) v = o;
+  }
+  return v;
+}
+
 // warp argmax: float max + uniqueness test decides almost always; exact butterfly otherwise
 __device__ __forceinline__ Best warp_best(Best v) {
   const uint32_t sb = v.found ? __float_as_uint(v.sc) : 0u;
@@ -66,12 +81,7 @@ __device__ __forceinline__ Best warp_best(Best v) {
   const float thr = __uint_as_float(mx) * 0.9999847f;   // 1 - 2^-16
   const uint32_t near = __ballot_sync(FULL, v.found && v.sc >= thr);
   if (__popc(near) == 1) return shfl_best(v, __ffs(near) - 1);
-#pragma unroll
-  for (int m = 16; m; m >>= 1) {
-    Best o = shfl_best(v, (threadIdx.x & 31) ^ m);
-    if (better(o, v)) v = o;
-  }
-  return v;
+  return warp_best_exact(v);
 }
 
 struct DnnRes {
@@ -158,7 +168,7 @@ struct RowCtx {
 
 // exact evaluation of row b: feasible argmax (e) and unconstrained argmax (k), warp-reduced
 template <int PAR>
-__device__ __forceinline__ void eval_row(const RowCtx &c, int32_t b, int lane, Best &e, Best &k) {
+static __device__ __noinline__ void eval_row(const RowCtx &c, int32_t b, int lane, Best &e, Best &k) {
   const uint32_t magic = magic_of(b);
   const uint64_t wC1 = (c.wse == 0 ? (uint64_t)b : 1ull) * c.C1;
   const uint64_t baM = (uint64_t)b * c.aM;
@@ -175,6 +185,15 @@ __device__ __forceinline__ void eval_row(const RowCtx &c, int32_t b, int lane, B
   k = warp_best(k);
 }
 
+// exact X(L, b_eval) >= 2^56 test (only when the f64 estimate is within 1e-4 of the limit)
+static __device__ __noinline__ bool xub_exact_over(uint32_t w, uint64_t t_np, uint64_t RT, uint32_t S_tot, uint64_t M,
+                                            uint64_t t_p, uint64_t Vmax, int mem_mode, uint32_t b, uint64_t D) {
+  u128 Xub = (u128)w * t_np * RT * S_tot * M + (u128)M * t_p * Vmax;
+  if (mem_mode == 1) Xub += (u128)b * D;
+  else if (mem_mode == 2) Xub += (u128)b * D * (u128)(S_tot * S_tot);
+  return Xub >= (u128)X_LIMIT;
+}
+
 // does sup over real S in [lo, hi] of b S / (alpha S + beta)^2 reach thr?
 __device__ __forceinline__ bool sup_reaches(double b, double alpha, double beta, double lo, double hi, double thr) {
   if (hi < lo) return false;
@@ -184,6 +203,55 @@ __device__ __forceinline__ bool sup_reaches(double b, double alpha, double beta,
   else return b >= 4.0 * alpha * beta * thr;            // peak b / (4 alpha beta) at S* = beta / alpha
   const double x = alpha * S + beta;
   return b * S >= thr * x * x;
+}
+
+// Branch-and-bound pruning for linear mode: which b in (b_lo, b_hi] can still beat the incumbent?
+// First a Jensen bound per b (lane per b): X >= w_b C1 S + M t_p max(S RT1, b Wn) + mem_lb; then, for the
+// b's that survive it, the continuous supremum of b S/(alpha S + beta)^2 over every run of constant
+// m = floor(S/b) (lanes over m).  f64 with a 1e-9 safety margin; returns a bit mask (bit b-1).
+static __device__ __noinline__ uint64_t bound_survivors(const RowCtx &c, const uint64_t *cA, const uint64_t *cU, const Best &best,
+                                                 int b_lo, int b_hi, int S_tot, int mem_mode, int wse, uint64_t Mtp,
+                                                 uint64_t RT1, uint64_t Wn, int lane) {
+  const double thr = (double)(best.b * best.S) / ((double)best.X * (double)best.X) * (1.0 - 1e-9);
+  const double Mtpd = (double)Mtp, C1d = (double)c.C1, Dd = (double)c.D, RT1d = (double)RT1, Wnd = (double)Wn;
+  uint32_t cand_lo = 0, cand_hi = 0;
+  for (int bb = b_lo + 1 + lane; bb <= b_hi; bb += 32) {
+    const double bd = (double)bb;
+    const double a1 = (wse == 0 ? bd : 1.0) * C1d;
+    const double m0 = mem_mode == 1 ? bd * Dd : 0.0;
+    bool ok;
+    if (RT1 == 0) {
+      ok = sup_reaches(bd, a1, m0, 1.0, (double)S_tot, thr);
+    } else {
+      const double Sc = bd * Wnd / RT1d;
+      ok = sup_reaches(bd, a1, Mtpd * bd * Wnd + m0, 1.0, fmin(Sc, (double)S_tot), thr) ||
+           sup_reaches(bd, a1 + Mtpd * RT1d, m0, fmax(Sc, 1.0), (double)S_tot, thr);
+    }
+    if (ok) {
+      const int bit = bb - 1;
+      if (bit < 32) cand_lo |= 1u << bit; else cand_hi |= 1u << (bit - 32);
+    }
+  }
+  cand_lo = __reduce_or_sync(FULL, cand_lo);
+  cand_hi = __reduce_or_sync(FULL, cand_hi);
+  uint64_t cand = ((uint64_t)cand_hi << 32) | cand_lo, out = 0;
+  while (cand) {
+    const int bb = __ffsll((long long)cand);
+    cand &= cand - 1;
+    const double bd = (double)bb;
+    const uint64_t wC1 = (wse == 0 ? (uint64_t)bb : 1ull) * c.C1;
+    const int mmax = S_tot / bb;
+    bool ok = false;
+    for (int m = lane; m <= mmax; m += 32) {
+      const int lo = m * bb > 1 ? m * bb : 1;
+      const int hi = m * bb + bb - 1 < S_tot ? m * bb + bb - 1 : S_tot;
+      const uint64_t alpha = wC1 + cA[m] + (mem_mode == 2 ? (uint64_t)bb * c.D * (uint64_t)lo : 0ull);
+      const uint64_t beta = (uint64_t)bb * cU[m] + (mem_mode == 1 ? (uint64_t)bb * c.D : 0ull);
+      ok = ok || sup_reaches(bd, (double)alpha, (double)beta, (double)lo, (double)hi, thr);
+    }
+    if (__any_sync(FULL, ok)) out |= 1ull << (bb - 1);
+  }
+  return out;
 }
 
 // Analyse DNN k.  knee_only: status + knee at knee_b.  Otherwise (l*, b*), demand, knee(b*).
@@ -266,13 +334,8 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
     bool over;
     if (Vmax >= (1ull << 63) || xe >= 72057594037927936.0 * 1.0001) over = true;
     else if (xe < 72057594037927936.0 * 0.9999) over = false;
-    else {
-      const u128 w = p.wse_mode == 0 ? (u128)b_eval : (u128)1;
-      u128 Xub = w * (u128)t_np * (u128)RT * (u128)S_tot * (u128)M + (u128)M * (u128)t_p * (u128)Vmax;
-      if (mem_mode == 1) Xub += (u128)b_eval * (u128)D;
-      else if (mem_mode == 2) Xub += (u128)b_eval * (u128)D * (u128)(S_tot * S_tot);
-      over = Xub >= (u128)X_LIMIT;
-    }
+    else over = xub_exact_over(p.wse_mode == 0 ? (uint32_t)b_eval : 1u, (uint64_t)t_np, (uint64_t)RT, (uint32_t)S_tot,
+                               M, (uint64_t)t_p, Vmax, mem_mode, (uint32_t)b_eval, D);
     if (over) { res.st = DSTACK_ST_OVERFLOW; return res; }
   }
   const uint64_t RT1 = PAR == 0 ? (uint64_t)RT - hist[0] : 0ull;   // sum R over n_i >= 1
@@ -299,50 +362,12 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
       if (better(e, best)) { best = e; knee = kk.l; }
     }
   } else if (b_hi > b_lo) {
-    // incumbent eta (b S / X^2) with a safety margin for the f64 bounds
-    const double thr = (double)(best.b * best.S) / ((double)best.X * (double)best.X) * (1.0 - 1e-9);
-    const double Mtpd = (double)Mtp, C1d = (double)c.C1, Dd = (double)D, RT1d = (double)RT1, Wnd = (double)Wn;
-    // crude (Jensen) bound per b, lane per b: X >= w_b C1 S + M t_p max(S RT1, b Wn) + mem_lb
-    uint32_t cand_lo = 0, cand_hi = 0;
-    for (int bb = b_lo + 1 + lane; bb <= b_hi; bb += 32) {
-      const double bd = (double)bb;
-      const double a1 = (p.wse_mode == 0 ? bd : 1.0) * C1d;
-      const double m0 = mem_mode == 1 ? bd * Dd : 0.0;
-      bool ok;
-      if (RT1 == 0) {
-        ok = sup_reaches(bd, a1, m0, 1.0, (double)S_tot, thr);
-      } else {
-        const double Sc = bd * Wnd / RT1d;
-        ok = sup_reaches(bd, a1, Mtpd * bd * Wnd + m0, 1.0, fmin(Sc, (double)S_tot), thr) ||
-             sup_reaches(bd, a1 + Mtpd * RT1d, m0, fmax(Sc, 1.0), (double)S_tot, thr);
-      }
-      if (ok) {
-        const int bit = bb - 1;
-        if (bit < 32) cand_lo |= 1u << bit; else cand_hi |= 1u << (bit - 32);
-      }
-    }
-    cand_lo = __reduce_or_sync(FULL, cand_lo);
-    cand_hi = __reduce_or_sync(FULL, cand_hi);
-    uint64_t cand = ((uint64_t)cand_hi << 32) | cand_lo;
-    // per-run bound for the surviving b's, then exact rows for the b's that still reach the incumbent
-    while (cand) {
+    uint64_t cand = bound_survivors(c, cA, cU, best, b_lo, b_hi, S_tot, mem_mode, p.wse_mode, Mtp, RT1, Wn, lane);
+    while (cand) {   // exact rows only for the b's whose bound still reaches the incumbent
       const int bb = __ffsll((long long)cand);   // b = bit index + 1
       cand &= cand - 1;
-      const double bd = (double)bb;
-      const uint64_t wC1 = (p.wse_mode == 0 ? (uint64_t)bb : 1ull) * c.C1;
-      const int mmax = S_tot / bb;
-      bool ok = false;
-      for (int m = lane; m <= mmax; m += 32) {
-        const int lo = m * bb > 1 ? m * bb : 1;
-        const int hi = m * bb + bb - 1 < S_tot ? m * bb + bb - 1 : S_tot;
-        const uint64_t alpha = wC1 + cA[m] + (mem_mode == 2 ? (uint64_t)bb * D * (uint64_t)lo : 0ull);
-        const uint64_t beta = (uint64_t)bb * cU[m] + (mem_mode == 1 ? (uint64_t)bb * D : 0ull);
-        ok = ok || sup_reaches(bd, (double)alpha, (double)beta, (double)lo, (double)hi, thr);
-      }
-      if (__any_sync(FULL, ok)) {
-        eval_row<0>(c, bb, lane, e, kk);
-        if (better(e, best)) { best = e; knee = kk.l; }
-      }
+      eval_row<0>(c, bb, lane, e, kk);
+      if (better(e, best)) { best = e; knee = kk.l; }
     }
   }
   const int32_t dm = (int32_t)best.l + p.margin;
