@@ -75,6 +75,15 @@ def build_product(force=False, verbose=False):
     return out
 
 
+def build_variant(out_name, defines):
+    """Extra product build with -D flags (A/B experiments); never the default library."""
+    cus, _ = product_sources()
+    out = os.path.join(ROOT, "paper_2304_13541_b200", out_name)
+    _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+          "-I", os.path.join(ROOT, "include"), *[f"-D{d}" for d in defines], *cus, "-o", out])
+    return out
+
+
 def build_all(force=False, verbose=False):
     build_synth(force)
     build_oracle(force)

@@ -109,8 +109,9 @@ __device__ __forceinline__ uint32_t magic_of(int32_t b) { return b == 1 ? 0u : (
 // Warp scan of the width histogram hist[0..S_tot] (u32 sums of R_i by n_i) into the SCALED tables
 //   cA[m] = Mtp * PA[m], PA[m] = sum_{1<=n<=m} R;   cU[m] = Mtp * Q[m], Q[m] = W - sum_{n<=m} n R
 // (lane-chunked, one shuffle scan).  Returns the unscaled PA[mb], Q[mb] in *pa_mb, *q_mb (all lanes).
-__device__ __forceinline__ void scan_hist(const uint32_t *hist, uint64_t *cA, uint64_t *cU, int S_tot, uint64_t W,
-                                          uint64_t Mtp, int mb, uint64_t *pa_mb, uint64_t *q_mb, int lane) {
+__device__ __forceinline__ void scan_hist(const uint32_t *hist, uint64_t *cA, uint64_t *cU, float *cAf, float *cUf,
+                                          int S_tot, uint64_t W, uint64_t Mtp, int mb, uint64_t *pa_mb, uint64_t *q_mb,
+                                          int lane) {
   __syncwarp();
   const int C = (S_tot + 32) >> 5;          // bins per lane (S_tot+1 bins)
   const int m0 = lane * C;
@@ -131,7 +132,8 @@ __device__ __forceinline__ void scan_hist(const uint32_t *hist, uint64_t *cA, ui
     const int m = m0 + i;
     if (m <= S_tot) {
       if (m >= 1) { const uint64_t h = hist[m]; pa += h; pw += h * (uint64_t)m; }
-      cA[m] = Mtp * pa; cU[m] = Mtp * (W - pw);
+      const uint64_t va = Mtp * pa, vu = Mtp * (W - pw);
+      cA[m] = va; cU[m] = vu; cAf[m] = (float)va; cUf[m] = (float)vu;
       if (m == mb) { a_mb = pa; q_m = W - pw; }
     }
   }
@@ -144,7 +146,8 @@ __device__ __forceinline__ void scan_hist(const uint32_t *hist, uint64_t *cA, ui
 // threads mode: tables of N = ceil(b theta / 2048) (rebuilt per b)
 __device__ __forceinline__ void build_tables_threads(const uint32_t *__restrict__ n, const uint16_t *__restrict__ r,
                                                      int32_t K, int32_t S_tot, uint64_t Mtp, int32_t b,
-                                                     uint32_t *hist, uint64_t *cA, uint64_t *cU, int lane) {
+                                                     uint32_t *hist, uint64_t *cA, uint64_t *cU, float *cAf,
+                                                     float *cUf, int lane) {
   for (int m = lane; m <= S_tot; m += 32) hist[m] = 0;
   __syncwarp();
   uint64_t W = 0;
@@ -156,33 +159,127 @@ __device__ __forceinline__ void build_tables_threads(const uint32_t *__restrict_
   }
   W = warp_sum_u64(W);
   uint64_t pa, q;
-  scan_hist(hist, cA, cU, S_tot, W, Mtp, 0, &pa, &q, lane);
+  scan_hist(hist, cA, cU, cAf, cUf, S_tot, W, Mtp, 0, &pa, &q, lane);
 }
 
 struct RowCtx {
   const uint16_t *Stab;
   const uint64_t *cA, *cU;
+  const float *cAf, *cUf;
   int32_t L, mem_mode, wse;
   uint64_t C1, D, SLOM, aM;
+  float C1f, Df, SLOMf, aMf;
 };
 
-// exact evaluation of row b: feasible argmax (e) and unconstrained argmax (k), warp-reduced
+constexpr int ROW_CELLS = 8;   // levels per lane: L <= 255 < 8 * 32
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ float warp_max_f(float v) {   // v >= 0
+  return __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(v)));
+}
+
+// Row b: feasible argmax (e) and unconstrained argmax (k) of b S / X^2, warp-reduced, EXACT.
+// Pass 1 scores every level in f32 (float coefficient tables, ~15 ops/cell) and classifies Eqs. 11-12
+// as feasible / infeasible / too-close-to-call with a 1e-5 margin (f32 error here < 1e-6).
+// Pass 2 re-evaluates in exact 64/128-bit arithmetic only the cells whose f32 score is within 2^-16 of
+// the row maximum (normally one cell): no cell below that threshold can be the exact argmax.  If every
+// feasible-or-unsure candidate turns out infeasible, the next tier is examined; once an exactly feasible
+// candidate exists, the cells within 2^-16 of ITS score are added, so the boundary cannot hide a winner.
 template <int PAR>
-static __device__ __noinline__ void eval_row(const RowCtx &c, int32_t b, int lane, Best &e, Best &k) {
+__device__ __forceinline__ void eval_row(const RowCtx &c, int32_t b, int lane, Best &e, Best &k) {
   const uint32_t magic = magic_of(b);
-  const uint64_t wC1 = (c.wse == 0 ? (uint64_t)b : 1ull) * c.C1;
-  const uint64_t baM = (uint64_t)b * c.aM;
-  e = best_none(); k = best_none();
-  for (int32_t l = 1 + lane; l <= c.L; l += 32) {
-    const int32_t S = c.Stab[l];
-    const uint64_t X = cell_X<PAR>(S, b, magic, wC1, c.cA, c.cU, c.mem_mode, c.D);
-    Best cand; cand.found = 1; cand.l = l; cand.b = b; cand.S = S; cand.X = X; cand.sc = score_f(b * S, X);
-    if (better(cand, k)) k = cand;
-    const uint64_t cap = (uint64_t)S * c.SLOM;
-    if (X + (uint64_t)S * baM <= cap && 2 * X <= cap && better(cand, e)) e = cand;   // Eq. 11, Eq. 12
+  const float bf = (float)b;
+  const float wC1f = (c.wse == 0 ? bf : 1.f) * c.C1f;
+  const float baMf = bf * c.aMf;
+  const float mbw = c.mem_mode == 1 ? bf * c.Df : 0.f;
+  const float mvb = c.mem_mode == 2 ? bf * c.Df : 0.f;
+  const float ubf = PAR == 0 ? bf : 1.f;
+  float sc[ROW_CELLS];
+  uint32_t fe = 0;   // 2 bits per cell: 0 infeasible, 1 feasible, 2 unsure
+  float mk = 0.f, me = 0.f;
+#pragma unroll
+  for (int i = 0; i < ROW_CELLS; ++i) {
+    const int l = 1 + lane + 32 * i;
+    sc[i] = 0.f;
+    if (l <= c.L) {
+      const int S = c.Stab[l];
+      const int m = PAR == 0 ? (b == 1 ? S : (int)__umulhi((uint32_t)S, magic)) : S;
+      const float Sf = (float)S;
+      const float Xf = fmaf(Sf, wC1f + c.cAf[m] + mvb * Sf, fmaf(ubf, c.cUf[m], mbw));
+      const float capf = Sf * c.SLOMf;
+      const float hi = fmaxf(fmaf(Sf, baMf, Xf), 2.f * Xf);
+      const uint32_t f = hi <= capf * 0.99999f ? 1u : (hi > capf * 1.00001f ? 0u : 2u);
+      const float s = (bf * Sf) * rcp_approx(Xf * Xf);
+      sc[i] = s;
+      fe |= f << (2 * i);
+      mk = fmaxf(mk, s);
+      if (f) me = fmaxf(me, s);
+    }
   }
-  e = warp_best(e);
-  k = warp_best(k);
+  const uint64_t wC1 = (c.wse == 0 ? (uint64_t)b : 1ull) * c.C1;
+  auto exact = [&](int i) {
+    const int l = 1 + lane + 32 * i;
+    const int S = c.Stab[l];
+    Best r; r.found = 1; r.l = l; r.b = b; r.S = S; r.sc = sc[i];
+    r.X = cell_X<PAR>(S, b, magic, wC1, c.cA, c.cU, c.mem_mode, c.D);
+    return r;
+  };
+  // ---- knee: exact argmax among the cells near the f32 maximum ----
+  {
+    const float tk = warp_max_f(mk) * 0.9999847f;   // 1 - 2^-16
+    Best kb = best_none();
+#pragma unroll
+    for (int i = 0; i < ROW_CELLS; ++i)
+      if (1 + lane + 32 * i <= c.L && sc[i] >= tk) {
+        const Best r = exact(i);
+        if (better(r, kb)) kb = r;
+      }
+    k = warp_best(kb);
+  }
+  // ---- feasible argmax ----
+  Best eb = best_none();
+  uint32_t verified = 0;   // cells already checked exactly
+  while (true) {
+    const float mw = warp_max_f(me);
+    if (mw == 0.f) break;   // no feasible cell
+    const float t1 = mw * 0.9999847f;
+    me = 0.f;
+#pragma unroll
+    for (int i = 0; i < ROW_CELLS; ++i) {
+      const uint32_t f = (fe >> (2 * i)) & 3u;
+      if (!f) continue;
+      if (sc[i] >= t1 && !((verified >> i) & 1u)) {
+        verified |= 1u << i;
+        const Best r = exact(i);
+        const uint64_t cap = (uint64_t)r.S * c.SLOM;
+        const bool ok = r.X + (uint64_t)r.S * ((uint64_t)b * c.aM) <= cap && 2 * r.X <= cap;   // Eq. 11, 12
+        if (ok) { if (better(r, eb)) eb = r; }
+        else fe &= ~(3u << (2 * i));
+      }
+      if ((fe >> (2 * i)) & 3u && !((verified >> i) & 1u)) me = fmaxf(me, sc[i]);
+    }
+    const uint32_t got = __ballot_sync(FULL, eb.found);
+    if (got) {
+      // add every unverified feasible-or-unsure cell within 2^-16 of the best exactly-feasible score
+      const float t2 = warp_max_f(eb.found ? eb.sc : 0.f) * 0.9999847f;
+#pragma unroll
+      for (int i = 0; i < ROW_CELLS; ++i) {
+        if (((fe >> (2 * i)) & 3u) && !((verified >> i) & 1u) && sc[i] >= t2) {
+          verified |= 1u << i;
+          const Best r = exact(i);
+          const uint64_t cap = (uint64_t)r.S * c.SLOM;
+          if (r.X + (uint64_t)r.S * ((uint64_t)b * c.aM) <= cap && 2 * r.X <= cap && better(r, eb)) eb = r;
+        }
+      }
+      break;
+    }
+  }
+  e = warp_best(eb);
 }
 
 // exact X(L, b_eval) >= 2^56 test (only when the f64 estimate is within 1e-4 of the limit)
@@ -209,11 +306,19 @@ __device__ __forceinline__ bool sup_reaches(double b, double alpha, double beta,
 // First a Jensen bound per b (lane per b): X >= w_b C1 S + M t_p max(S RT1, b Wn) + mem_lb; then, for the
 // b's that survive it, the continuous supremum of b S/(alpha S + beta)^2 over every run of constant
 // m = floor(S/b) (lanes over m).  f64 with a 1e-9 safety margin; returns a bit mask (bit b-1).
-static __device__ __noinline__ uint64_t bound_survivors(const RowCtx &c, const uint64_t *cA, const uint64_t *cU, const Best &best,
-                                                 int b_lo, int b_hi, int S_tot, int mem_mode, int wse, uint64_t Mtp,
-                                                 uint64_t RT1, uint64_t Wn, int lane) {
-  const double thr = (double)(best.b * best.S) / ((double)best.X * (double)best.X) * (1.0 - 1e-9);
-  const double Mtpd = (double)Mtp, C1d = (double)c.C1, Dd = (double)c.D, RT1d = (double)RT1, Wnd = (double)Wn;
+#ifndef DSTACK_BOUND_NOINLINE
+#define DSTACK_BOUND_NOINLINE 0
+#endif
+#if DSTACK_BOUND_NOINLINE
+static __device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+uint64_t bound_survivors(const uint64_t *cA, const uint64_t *cU, double thr, uint64_t C1,
+                                                        uint64_t D, int b_lo, int b_hi, int S_tot, int mem_mode, int wse,
+                                                        uint64_t Mtp, uint64_t RT1, uint64_t Wn, int lane) {
+  const double Mtpd = (double)Mtp, C1d = (double)C1, Dd = (double)D, RT1d = (double)RT1, Wnd = (double)Wn;
+  const double WnR = RT1 ? Wnd / RT1d : 0.0;
   uint32_t cand_lo = 0, cand_hi = 0;
   for (int bb = b_lo + 1 + lane; bb <= b_hi; bb += 32) {
     const double bd = (double)bb;
@@ -223,7 +328,7 @@ static __device__ __noinline__ uint64_t bound_survivors(const RowCtx &c, const u
     if (RT1 == 0) {
       ok = sup_reaches(bd, a1, m0, 1.0, (double)S_tot, thr);
     } else {
-      const double Sc = bd * Wnd / RT1d;
+      const double Sc = bd * WnR;
       ok = sup_reaches(bd, a1, Mtpd * bd * Wnd + m0, 1.0, fmin(Sc, (double)S_tot), thr) ||
            sup_reaches(bd, a1 + Mtpd * RT1d, m0, fmax(Sc, 1.0), (double)S_tot, thr);
     }
@@ -239,14 +344,14 @@ static __device__ __noinline__ uint64_t bound_survivors(const RowCtx &c, const u
     const int bb = __ffsll((long long)cand);
     cand &= cand - 1;
     const double bd = (double)bb;
-    const uint64_t wC1 = (wse == 0 ? (uint64_t)bb : 1ull) * c.C1;
+    const uint64_t wC1 = (wse == 0 ? (uint64_t)bb : 1ull) * C1;
     const int mmax = S_tot / bb;
     bool ok = false;
     for (int m = lane; m <= mmax; m += 32) {
       const int lo = m * bb > 1 ? m * bb : 1;
       const int hi = m * bb + bb - 1 < S_tot ? m * bb + bb - 1 : S_tot;
-      const uint64_t alpha = wC1 + cA[m] + (mem_mode == 2 ? (uint64_t)bb * c.D * (uint64_t)lo : 0ull);
-      const uint64_t beta = (uint64_t)bb * cU[m] + (mem_mode == 1 ? (uint64_t)bb * c.D : 0ull);
+      const uint64_t alpha = wC1 + cA[m] + (mem_mode == 2 ? (uint64_t)bb * D * (uint64_t)lo : 0ull);
+      const uint64_t beta = (uint64_t)bb * cU[m] + (mem_mode == 1 ? (uint64_t)bb * D : 0ull);
       ok = ok || sup_reaches(bd, (double)alpha, (double)beta, (double)lo, (double)hi, thr);
     }
     if (__any_sync(FULL, ok)) out |= 1ull << (bb - 1);
@@ -258,7 +363,8 @@ static __device__ __noinline__ uint64_t bound_survivors(const RowCtx &c, const u
 // Per-warp shared memory: hist[S_tot+1] u32, cA/cU[S_tot+1] u64 (tables stay valid on return).
 template <int PAR>
 __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k, const uint16_t *Stab,
-                              uint32_t *hist, uint64_t *cA, uint64_t *cU, int lane, int knee_only, int32_t knee_b) {
+                              uint32_t *hist, uint64_t *cA, uint64_t *cU, float *cAf, float *cUf, int lane,
+                              int knee_only, int32_t knee_b) {
   DnnRes res; res.st = DSTACK_ST_OK; res.demand = 0; res.knee = 0; res.b = 0; res.RT = 0; res.D = 0;
   const int L = p.L, S_tot = p.S_tot;
   const int64_t r0 = pb.dnn_row_off[k], r1 = pb.dnn_row_off[k + 1];
@@ -320,7 +426,7 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
     // sum_{N_i >= 1} R_i max(S_tot, b n_i) = S_tot PA[S_tot/b] + b Q[S_tot/b]  (exact, from the scan)
     const int mb = S_tot / b_eval;
     uint64_t pa_mb, q_mb;
-    scan_hist(hist, cA, cU, S_tot, Wn, Mtp, mb, &pa_mb, &q_mb, lane);
+    scan_hist(hist, cA, cU, cAf, cUf, S_tot, Wn, Mtp, mb, &pa_mb, &q_mb, lane);
     const u128 v = (u128)S_tot * pa_mb + (u128)b_eval * q_mb;
     Vmax = v >= ((u128)1 << 63) ? (1ull << 63) : (uint64_t)v;
   }
@@ -340,34 +446,34 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
   }
   const uint64_t RT1 = PAR == 0 ? (uint64_t)RT - hist[0] : 0ull;   // sum R over n_i >= 1
   RowCtx c;
-  c.Stab = Stab; c.cA = cA; c.cU = cU; c.L = L; c.mem_mode = mem_mode; c.wse = p.wse_mode;
+  c.Stab = Stab; c.cA = cA; c.cU = cU; c.cAf = cAf; c.cUf = cUf; c.L = L; c.mem_mode = mem_mode; c.wse = p.wse_mode;
   c.C1 = (uint64_t)t_np * RT * M; c.D = D; c.SLOM = (uint64_t)slo * M; c.aM = (uint64_t)asm_us * M;
-  Best e, kk;
-  if (knee_only) {
-    if (PAR == 1) build_tables_threads(n, r, K, S_tot, Mtp, knee_b, hist, cA, cU, lane);
-    eval_row<PAR>(c, knee_b, lane, e, kk);
-    res.knee = (uint16_t)kk.l;
-    return res;
-  }
-  // ---- a3: exact branch-and-bound over (l, b) ----
-  if (PAR == 1) build_tables_threads(n, r, K, S_tot, Mtp, b_lo, hist, cA, cU, lane);
-  eval_row<PAR>(c, b_lo, lane, e, kk);
-  if (!e.found) { res.st = DSTACK_ST_INFEASIBLE; return res; }
-  Best best = e;
-  uint32_t knee = kk.l;
-  if (PAR == 1) {
-    for (int32_t b = b_lo + 1; b <= b_hi; ++b) {
-      build_tables_threads(n, r, K, S_tot, Mtp, b, hist, cA, cU, lane);
-      eval_row<1>(c, b, lane, e, kk);
-      if (better(e, best)) { best = e; knee = kk.l; }
-    }
-  } else if (b_hi > b_lo) {
-    uint64_t cand = bound_survivors(c, cA, cU, best, b_lo, b_hi, S_tot, mem_mode, p.wse_mode, Mtp, RT1, Wn, lane);
-    while (cand) {   // exact rows only for the b's whose bound still reaches the incumbent
-      const int bb = __ffsll((long long)cand);   // b = bit index + 1
-      cand &= cand - 1;
-      eval_row<0>(c, bb, lane, e, kk);
-      if (better(e, best)) { best = e; knee = kk.l; }
+  c.C1f = (float)c.C1; c.Df = (float)D; c.SLOMf = (float)c.SLOM; c.aMf = (float)c.aM;
+  // ---- a2/a3: rows evaluated exactly, b_lo (or the knee batch) first, then the b's the bounds keep ----
+  Best e, kk, best = best_none();
+  uint32_t knee = 0;
+  bool first = true;
+  uint64_t todo = 1ull << ((knee_only ? knee_b : b_lo) - 1);
+  while (todo) {
+    const int b = __ffsll((long long)todo);   // b = bit index + 1
+    todo &= todo - 1;
+    if (PAR == 1) build_tables_threads(n, r, K, S_tot, Mtp, b, hist, cA, cU, cAf, cUf, lane);
+    eval_row<PAR>(c, b, lane, e, kk);
+    if (first) {
+      first = false;
+      if (knee_only) { res.knee = (uint16_t)kk.l; return res; }
+      if (!e.found) { res.st = DSTACK_ST_INFEASIBLE; return res; }   // b_lo row feasible iff any row is
+      best = e; knee = kk.l;
+      if (b_hi > b_lo) {
+        if (PAR == 1) {
+          todo = (b_hi >= 64 ? ~0ull : ((1ull << b_hi) - 1)) & ~((1ull << b_lo) - 1);
+        } else {
+          const double thr = (double)(best.b * best.S) / ((double)best.X * (double)best.X) * (1.0 - 1e-9);
+          todo = bound_survivors(cA, cU, thr, c.C1, D, b_lo, b_hi, S_tot, mem_mode, p.wse_mode, Mtp, RT1, Wn, lane);
+        }
+      }
+    } else if (better(e, best)) {
+      best = e; knee = kk.l;
     }
   }
   const int32_t dm = (int32_t)best.l + p.margin;
@@ -375,6 +481,17 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
   res.b = (uint8_t)best.b;
   res.knee = (uint16_t)knee;
   return res;
+}
+
+// min(ceil(a / b), 0xFFFF) without a 64-bit integer division: f64 quotient estimate, exact fix-up.
+__device__ __forceinline__ uint16_t ceil_div_clamp16(uint64_t a, uint64_t b) {
+  const double qd = (double)a / (double)b;
+  if (qd > 65536.0) return 0xFFFF;
+  uint64_t q = (uint64_t)qd;                 // |qd - a/b| < 1e-10 here
+  while (q > 0 && q * b > a) --q;            // q = floor(a / b)
+  while ((q + 1) * b <= a) ++q;
+  q += (q * b < a);                          // ceil
+  return (uint16_t)(q > 0xFFFF ? 0xFFFF : q);
 }
 
 // d_j(b) = ceil(X(g, b) / (S(g) M Delta)) for b in [b_lo, b_hi] from the (linear-mode) tables of the
@@ -388,8 +505,7 @@ __device__ __forceinline__ void dtab_from_tables(const dstack_problem_t &pb, con
   const uint64_t den = (uint64_t)S * M * (uint64_t)p.slot_us;
   for (int32_t b = b_lo + lane; b <= b_hi; b += 32) {
     const uint64_t X = cell_X<0>(S, b, magic_of(b), (p.wse_mode == 0 ? (uint64_t)b : 1ull) * C1, cA, cU, p.mem_mode, D);
-    const uint64_t ds = (X + den - 1) / den;
-    dtab[b - 1] = (uint16_t)(ds > 0xFFFF ? 0xFFFF : ds);
+    dtab[b - 1] = ceil_div_clamp16(X, den);
   }
   __syncwarp();
 }
@@ -417,8 +533,7 @@ __device__ __forceinline__ void dtab_from_rows(const dstack_problem_t &pb, const
     uint64_t X = (p.wse_mode == 0 ? (uint64_t)b : 1ull) * t_np * RT * S * M + M * t_p * V;
     if (p.mem_mode == 1) X += (uint64_t)b * D;
     else if (p.mem_mode == 2) X += (uint64_t)b * D * S * S;
-    const uint64_t ds = (X + den - 1) / den;
-    if (lane == 0) dtab[b - 1] = (uint16_t)(ds > 0xFFFF ? 0xFFFF : ds);
+    if (lane == 0) dtab[b - 1] = ceil_div_clamp16(X, den);
   }
   __syncwarp();
 }

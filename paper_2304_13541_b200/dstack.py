@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdstack.so")
+LIB_PATH = os.environ.get("DSTACK_LIB") or os.path.join(_HERE, "libdstack.so")   # DSTACK_LIB: A/B builds
 
 DSTACK_OK, DSTACK_EINVAL, DSTACK_EWORKSPACE, DSTACK_ELAUNCH = 0, -1, -2, -3
 ST_OK, ST_INFEASIBLE, ST_OVERFLOW, ST_INVALID, ST_OVERSUBSCRIBED = 0, 1, 2, 3, 4
