@@ -183,13 +183,51 @@ __device__ __forceinline__ float warp_max_f(float v) {   // v >= 0
   return __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(v)));
 }
 
+// Row b, EXACT reference evaluation: every level in 64/128-bit arithmetic (fallback for near-ties).
+template <int PAR>
+static __device__ __noinline__ void eval_row_exact(const RowCtx &c, int32_t b, int lane, Best &e, Best &k) {
+  const uint32_t magic = magic_of(b);
+  const uint64_t wC1 = (c.wse == 0 ? (uint64_t)b : 1ull) * c.C1;
+  const uint64_t baM = (uint64_t)b * c.aM;
+  Best le = best_none(), lk = best_none();
+  for (int32_t l = 1 + lane; l <= c.L; l += 32) {
+    const int32_t S = c.Stab[l];
+    const uint64_t X = cell_X<PAR>(S, b, magic, wC1, c.cA, c.cU, c.mem_mode, c.D);
+    Best cand; cand.found = 1; cand.l = l; cand.b = b; cand.S = S; cand.X = X; cand.sc = score_f(b * S, X);
+    if (better(cand, lk)) lk = cand;
+    const uint64_t cap = (uint64_t)S * c.SLOM;
+    if (X + (uint64_t)S * baM <= cap && 2 * X <= cap && better(cand, le)) le = cand;   // Eq. 11, Eq. 12
+  }
+  e = warp_best(le);
+  k = warp_best(lk);
+}
+
+// f32 top-score tracker: exact winner unless another score came within the tolerance
+struct Top {
+  float s;
+  int l;
+  bool amb;
+};
+__device__ __forceinline__ void top_add(Top &t, float s, int l) {
+  if (s > t.s * 1.0000153f) { t.s = s; t.l = l; t.amb = false; }       // clearly above everything so far
+  else if (s >= t.s * 0.9999847f) { t.amb = true; if (s > t.s) { t.s = s; t.l = l; } }
+}
+// winner lane of a warp-wide Top, or -1 if two candidates are within the tolerance (-2: empty)
+__device__ __forceinline__ int top_winner(const Top &t) {
+  const float M = warp_max_f(t.s);
+  if (M == 0.f) return -2;
+  const uint32_t near = __ballot_sync(FULL, t.s >= M * 0.9999847f);
+  const int w = __ffs(near) - 1;
+  const bool amb = __shfl_sync(FULL, (int)t.amb, w);
+  return (__popc(near) == 1 && !amb) ? w : -1;
+}
+
 // Row b: feasible argmax (e) and unconstrained argmax (k) of b S / X^2, warp-reduced, EXACT.
-// Pass 1 scores every level in f32 (float coefficient tables, ~15 ops/cell) and classifies Eqs. 11-12
-// as feasible / infeasible / too-close-to-call with a 1e-5 margin (f32 error here < 1e-6).
-// Pass 2 re-evaluates in exact 64/128-bit arithmetic only the cells whose f32 score is within 2^-16 of
-// the row maximum (normally one cell): no cell below that threshold can be the exact argmax.  If every
-// feasible-or-unsure candidate turns out infeasible, the next tier is examined; once an exactly feasible
-// candidate exists, the cells within 2^-16 of ITS score are added, so the boundary cannot hide a winner.
+// One f32 pass (float coefficient tables, ~25 ops per level) keeps per lane the top score of the sure-
+// feasible levels, the top score of all levels and the top score of the levels whose Eqs. 11-12 test is
+// within 1e-5 of its bound (f32 error here < 1e-6).  When the warp maximum is unique by more than 2^-16
+// (and no unsure level comes that close) it is the exact argmax, and only the winner's X is recomputed
+// in 64-bit; otherwise the row is re-evaluated exactly (eval_row_exact), which is rare.
 template <int PAR>
 __device__ __forceinline__ void eval_row(const RowCtx &c, int32_t b, int lane, Best &e, Best &k) {
   const uint32_t magic = magic_of(b);
@@ -199,87 +237,39 @@ __device__ __forceinline__ void eval_row(const RowCtx &c, int32_t b, int lane, B
   const float mbw = c.mem_mode == 1 ? bf * c.Df : 0.f;
   const float mvb = c.mem_mode == 2 ? bf * c.Df : 0.f;
   const float ubf = PAR == 0 ? bf : 1.f;
-  float sc[ROW_CELLS];
-  uint32_t fe = 0;   // 2 bits per cell: 0 infeasible, 1 feasible, 2 unsure
-  float mk = 0.f, me = 0.f;
-#pragma unroll
-  for (int i = 0; i < ROW_CELLS; ++i) {
-    const int l = 1 + lane + 32 * i;
-    sc[i] = 0.f;
-    if (l <= c.L) {
-      const int S = c.Stab[l];
-      const int m = PAR == 0 ? (b == 1 ? S : (int)__umulhi((uint32_t)S, magic)) : S;
-      const float Sf = (float)S;
-      const float Xf = fmaf(Sf, wC1f + c.cAf[m] + mvb * Sf, fmaf(ubf, c.cUf[m], mbw));
-      const float capf = Sf * c.SLOMf;
-      const float hi = fmaxf(fmaf(Sf, baMf, Xf), 2.f * Xf);
-      const uint32_t f = hi <= capf * 0.99999f ? 1u : (hi > capf * 1.00001f ? 0u : 2u);
-      const float s = (bf * Sf) * rcp_approx(Xf * Xf);
-      sc[i] = s;
-      fe |= f << (2 * i);
-      mk = fmaxf(mk, s);
-      if (f) me = fmaxf(me, s);
-    }
-  }
-  const uint64_t wC1 = (c.wse == 0 ? (uint64_t)b : 1ull) * c.C1;
-  auto exact = [&](int i) {
-    const int l = 1 + lane + 32 * i;
+  Top tk = {0.f, 0, false}, te = {0.f, 0, false};
+  float tu = 0.f;   // top score among unsure levels
+  for (int l = 1 + lane; l <= c.L; l += 32) {
     const int S = c.Stab[l];
-    Best r; r.found = 1; r.l = l; r.b = b; r.S = S; r.sc = sc[i];
+    const int m = PAR == 0 ? (b == 1 ? S : (int)__umulhi((uint32_t)S, magic)) : S;
+    const float Sf = (float)S;
+    const float Xf = fmaf(Sf, wC1f + c.cAf[m] + mvb * Sf, fmaf(ubf, c.cUf[m], mbw));
+    const float capf = Sf * c.SLOMf;
+    const float hi = fmaxf(fmaf(Sf, baMf, Xf), 2.f * Xf);
+    const float s = (bf * Sf) * rcp_approx(Xf * Xf);
+    top_add(tk, s, l);
+    if (hi <= capf * 0.99999f) top_add(te, s, l);
+    else if (hi <= capf * 1.00001f) tu = fmaxf(tu, s);
+  }
+  const int wk = top_winner(tk);
+  int we = top_winner(te);
+  if (we >= -1) {   // an unsure level near the feasible top could win
+    const float Me = warp_max_f(te.s), Mu = warp_max_f(tu);
+    if (Mu >= Me * 0.9999847f) we = -1;
+  } else if (warp_max_f(tu) > 0.f) {
+    we = -1;        // no sure-feasible level, some unsure ones
+  }
+  if (wk == -1 || we == -1) { eval_row_exact<PAR>(c, b, lane, e, k); return; }
+  const uint64_t wC1 = (c.wse == 0 ? (uint64_t)b : 1ull) * c.C1;
+  auto exact = [&](int src, const Top &t) {
+    const int l = __shfl_sync(FULL, t.l, src);
+    const int S = c.Stab[l];
+    Best r; r.found = 1; r.l = l; r.b = b; r.S = S; r.sc = __shfl_sync(FULL, t.s, src);
     r.X = cell_X<PAR>(S, b, magic, wC1, c.cA, c.cU, c.mem_mode, c.D);
     return r;
   };
-  // ---- knee: exact argmax among the cells near the f32 maximum ----
-  {
-    const float tk = warp_max_f(mk) * 0.9999847f;   // 1 - 2^-16
-    Best kb = best_none();
-#pragma unroll
-    for (int i = 0; i < ROW_CELLS; ++i)
-      if (1 + lane + 32 * i <= c.L && sc[i] >= tk) {
-        const Best r = exact(i);
-        if (better(r, kb)) kb = r;
-      }
-    k = warp_best(kb);
-  }
-  // ---- feasible argmax ----
-  Best eb = best_none();
-  uint32_t verified = 0;   // cells already checked exactly
-  while (true) {
-    const float mw = warp_max_f(me);
-    if (mw == 0.f) break;   // no feasible cell
-    const float t1 = mw * 0.9999847f;
-    me = 0.f;
-#pragma unroll
-    for (int i = 0; i < ROW_CELLS; ++i) {
-      const uint32_t f = (fe >> (2 * i)) & 3u;
-      if (!f) continue;
-      if (sc[i] >= t1 && !((verified >> i) & 1u)) {
-        verified |= 1u << i;
-        const Best r = exact(i);
-        const uint64_t cap = (uint64_t)r.S * c.SLOM;
-        const bool ok = r.X + (uint64_t)r.S * ((uint64_t)b * c.aM) <= cap && 2 * r.X <= cap;   // Eq. 11, 12
-        if (ok) { if (better(r, eb)) eb = r; }
-        else fe &= ~(3u << (2 * i));
-      }
-      if ((fe >> (2 * i)) & 3u && !((verified >> i) & 1u)) me = fmaxf(me, sc[i]);
-    }
-    const uint32_t got = __ballot_sync(FULL, eb.found);
-    if (got) {
-      // add every unverified feasible-or-unsure cell within 2^-16 of the best exactly-feasible score
-      const float t2 = warp_max_f(eb.found ? eb.sc : 0.f) * 0.9999847f;
-#pragma unroll
-      for (int i = 0; i < ROW_CELLS; ++i) {
-        if (((fe >> (2 * i)) & 3u) && !((verified >> i) & 1u) && sc[i] >= t2) {
-          verified |= 1u << i;
-          const Best r = exact(i);
-          const uint64_t cap = (uint64_t)r.S * c.SLOM;
-          if (r.X + (uint64_t)r.S * ((uint64_t)b * c.aM) <= cap && 2 * r.X <= cap && better(r, eb)) eb = r;
-        }
-      }
-      break;
-    }
-  }
-  e = warp_best(eb);
+  k = exact(wk, tk);
+  e = we >= 0 ? exact(we, te) : best_none();
 }
 
 // exact X(L, b_eval) >= 2^56 test (only when the f64 estimate is within 1e-4 of the limit)
