@@ -6,7 +6,7 @@
 namespace dstack {
 
 __host__ __device__ inline size_t prof_warp_bytes(int S_tot) {
-  return (((size_t)28 * (S_tot + 1)) + 15) & ~(size_t)15;   // cA, cU u64 + cAf, cUf f32 + hist u32
+  return (((size_t)20 * (S_tot + 1)) + 15) & ~(size_t)15;   // cA, cU u64 + hist u32
 }
 
 template <int PAR>
@@ -22,14 +22,12 @@ __global__ void __launch_bounds__(256, DSTACK_PROF_MINB) k_prof(ProfArgs a) {
   unsigned char *wreg = smem + stab_bytes + (size_t)warp * prof_warp_bytes(S_tot);
   uint64_t *cA = (uint64_t *)wreg;
   uint64_t *cU = cA + (S_tot + 1);
-  float *cAf = (float *)(cU + (S_tot + 1));
-  float *cUf = cAf + (S_tot + 1);
-  uint32_t *hist = (uint32_t *)(cUf + (S_tot + 1));
+  uint32_t *hist = (uint32_t *)(cU + (S_tot + 1));
   fill_stab(Stab, L, S_tot);
   __syncthreads();
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; k < a.pb.num_dnn; k += nwarps) {
-    const DnnRes r = analyze_dnn<PAR>(a.pb, a.p, k, Stab, hist, cA, cU, cAf, cUf, lane, a.knee_only, a.knee_b);
+    const DnnRes r = analyze_dnn<PAR>(a.pb, a.p, k, Stab, hist, cA, cU, lane, a.knee_only, a.knee_b);
     if (a.dtab_rows && r.st == DSTACK_ST_OK) {   // eval path: d_j(b) at g = demand, b in [b_lo, b*]
       if (PAR == 0)
         dtab_from_tables(a.pb, a.p, k, cA, cU, r.RT, r.D, r.demand, a.p.b_min, r.b, a.dtab_rows + k * DTAB_ROW, lane);

@@ -51,7 +51,9 @@ __device__ __forceinline__ bool better(const Best &c, const Best &o) {
 
 __device__ __forceinline__ float score_f(uint32_t P, uint64_t X) {
   const float xf = (float)X;
-  return (float)P * __frcp_rn(xf * xf);
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(xf * xf));
+  return (float)P * r;   // relative error < 2^-21: far inside the 2^-17 filter band
 }
 
 __device__ __forceinline__ Best shfl_best(const Best &v, int src) {
@@ -109,9 +111,8 @@ __device__ __forceinline__ uint32_t magic_of(int32_t b) { return b == 1 ? 0u : (
 // Warp scan of the width histogram hist[0..S_tot] (u32 sums of R_i by n_i) into the SCALED tables
 //   cA[m] = Mtp * PA[m], PA[m] = sum_{1<=n<=m} R;   cU[m] = Mtp * Q[m], Q[m] = W - sum_{n<=m} n R
 // (lane-chunked, one shuffle scan).  Returns the unscaled PA[mb], Q[mb] in *pa_mb, *q_mb (all lanes).
-__device__ __forceinline__ void scan_hist(const uint32_t *hist, uint64_t *cA, uint64_t *cU, float *cAf, float *cUf,
-                                          int S_tot, uint64_t W, uint64_t Mtp, int mb, uint64_t *pa_mb, uint64_t *q_mb,
-                                          int lane) {
+__device__ __forceinline__ void scan_hist(const uint32_t *hist, uint64_t *cA, uint64_t *cU, int S_tot, uint64_t W,
+                                          uint64_t Mtp, int mb, uint64_t *pa_mb, uint64_t *q_mb, int lane) {
   __syncwarp();
   const int C = (S_tot + 32) >> 5;          // bins per lane (S_tot+1 bins)
   const int m0 = lane * C;
@@ -132,8 +133,7 @@ __device__ __forceinline__ void scan_hist(const uint32_t *hist, uint64_t *cA, ui
     const int m = m0 + i;
     if (m <= S_tot) {
       if (m >= 1) { const uint64_t h = hist[m]; pa += h; pw += h * (uint64_t)m; }
-      const uint64_t va = Mtp * pa, vu = Mtp * (W - pw);
-      cA[m] = va; cU[m] = vu; cAf[m] = (float)va; cUf[m] = (float)vu;
+      cA[m] = Mtp * pa; cU[m] = Mtp * (W - pw);
       if (m == mb) { a_mb = pa; q_m = W - pw; }
     }
   }
@@ -146,8 +146,7 @@ __device__ __forceinline__ void scan_hist(const uint32_t *hist, uint64_t *cA, ui
 // threads mode: tables of N = ceil(b theta / 2048) (rebuilt per b)
 __device__ __forceinline__ void build_tables_threads(const uint32_t *__restrict__ n, const uint16_t *__restrict__ r,
                                                      int32_t K, int32_t S_tot, uint64_t Mtp, int32_t b,
-                                                     uint32_t *hist, uint64_t *cA, uint64_t *cU, float *cAf,
-                                                     float *cUf, int lane) {
+                                                     uint32_t *hist, uint64_t *cA, uint64_t *cU, int lane) {
   for (int m = lane; m <= S_tot; m += 32) hist[m] = 0;
   __syncwarp();
   uint64_t W = 0;
@@ -159,19 +158,15 @@ __device__ __forceinline__ void build_tables_threads(const uint32_t *__restrict_
   }
   W = warp_sum_u64(W);
   uint64_t pa, q;
-  scan_hist(hist, cA, cU, cAf, cUf, S_tot, W, Mtp, 0, &pa, &q, lane);
+  scan_hist(hist, cA, cU, S_tot, W, Mtp, 0, &pa, &q, lane);
 }
 
 struct RowCtx {
   const uint16_t *Stab;
   const uint64_t *cA, *cU;
-  const float *cAf, *cUf;
   int32_t L, mem_mode, wse;
   uint64_t C1, D, SLOM, aM;
-  float C1f, Df, SLOMf, aMf;
 };
-
-constexpr int ROW_CELLS = 8;   // levels per lane: L <= 255 < 8 * 32
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
@@ -179,97 +174,24 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
-__device__ __forceinline__ float warp_max_f(float v) {   // v >= 0
-  return __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(v)));
-}
-
-// Row b, EXACT reference evaluation: every level in 64/128-bit arithmetic (fallback for near-ties).
+// Row b: feasible argmax (e) and unconstrained argmax (k) of b S / X^2 over the levels, warp-reduced,
+// exact (per level: O(1) X from the tables, f32 score filter, 128-bit comparison only on near-ties).
 template <int PAR>
-static __device__ __noinline__ void eval_row_exact(const RowCtx &c, int32_t b, int lane, Best &e, Best &k) {
+__device__ __forceinline__ void eval_row(const RowCtx &c, int32_t b, int lane, Best &e, Best &k) {
   const uint32_t magic = magic_of(b);
   const uint64_t wC1 = (c.wse == 0 ? (uint64_t)b : 1ull) * c.C1;
   const uint64_t baM = (uint64_t)b * c.aM;
-  Best le = best_none(), lk = best_none();
+  e = best_none(); k = best_none();
   for (int32_t l = 1 + lane; l <= c.L; l += 32) {
     const int32_t S = c.Stab[l];
     const uint64_t X = cell_X<PAR>(S, b, magic, wC1, c.cA, c.cU, c.mem_mode, c.D);
     Best cand; cand.found = 1; cand.l = l; cand.b = b; cand.S = S; cand.X = X; cand.sc = score_f(b * S, X);
-    if (better(cand, lk)) lk = cand;
+    if (better(cand, k)) k = cand;
     const uint64_t cap = (uint64_t)S * c.SLOM;
-    if (X + (uint64_t)S * baM <= cap && 2 * X <= cap && better(cand, le)) le = cand;   // Eq. 11, Eq. 12
+    if (X + (uint64_t)S * baM <= cap && 2 * X <= cap && better(cand, e)) e = cand;   // Eq. 11, Eq. 12
   }
-  e = warp_best(le);
-  k = warp_best(lk);
-}
-
-// f32 top-score tracker: exact winner unless another score came within the tolerance
-struct Top {
-  float s;
-  int l;
-  bool amb;
-};
-__device__ __forceinline__ void top_add(Top &t, float s, int l) {
-  if (s > t.s * 1.0000153f) { t.s = s; t.l = l; t.amb = false; }       // clearly above everything so far
-  else if (s >= t.s * 0.9999847f) { t.amb = true; if (s > t.s) { t.s = s; t.l = l; } }
-}
-// winner lane of a warp-wide Top, or -1 if two candidates are within the tolerance (-2: empty)
-__device__ __forceinline__ int top_winner(const Top &t) {
-  const float M = warp_max_f(t.s);
-  if (M == 0.f) return -2;
-  const uint32_t near = __ballot_sync(FULL, t.s >= M * 0.9999847f);
-  const int w = __ffs(near) - 1;
-  const bool amb = __shfl_sync(FULL, (int)t.amb, w);
-  return (__popc(near) == 1 && !amb) ? w : -1;
-}
-
-// Row b: feasible argmax (e) and unconstrained argmax (k) of b S / X^2, warp-reduced, EXACT.
-// One f32 pass (float coefficient tables, ~25 ops per level) keeps per lane the top score of the sure-
-// feasible levels, the top score of all levels and the top score of the levels whose Eqs. 11-12 test is
-// within 1e-5 of its bound (f32 error here < 1e-6).  When the warp maximum is unique by more than 2^-16
-// (and no unsure level comes that close) it is the exact argmax, and only the winner's X is recomputed
-// in 64-bit; otherwise the row is re-evaluated exactly (eval_row_exact), which is rare.
-template <int PAR>
-__device__ __forceinline__ void eval_row(const RowCtx &c, int32_t b, int lane, Best &e, Best &k) {
-  const uint32_t magic = magic_of(b);
-  const float bf = (float)b;
-  const float wC1f = (c.wse == 0 ? bf : 1.f) * c.C1f;
-  const float baMf = bf * c.aMf;
-  const float mbw = c.mem_mode == 1 ? bf * c.Df : 0.f;
-  const float mvb = c.mem_mode == 2 ? bf * c.Df : 0.f;
-  const float ubf = PAR == 0 ? bf : 1.f;
-  Top tk = {0.f, 0, false}, te = {0.f, 0, false};
-  float tu = 0.f;   // top score among unsure levels
-  for (int l = 1 + lane; l <= c.L; l += 32) {
-    const int S = c.Stab[l];
-    const int m = PAR == 0 ? (b == 1 ? S : (int)__umulhi((uint32_t)S, magic)) : S;
-    const float Sf = (float)S;
-    const float Xf = fmaf(Sf, wC1f + c.cAf[m] + mvb * Sf, fmaf(ubf, c.cUf[m], mbw));
-    const float capf = Sf * c.SLOMf;
-    const float hi = fmaxf(fmaf(Sf, baMf, Xf), 2.f * Xf);
-    const float s = (bf * Sf) * rcp_approx(Xf * Xf);
-    top_add(tk, s, l);
-    if (hi <= capf * 0.99999f) top_add(te, s, l);
-    else if (hi <= capf * 1.00001f) tu = fmaxf(tu, s);
-  }
-  const int wk = top_winner(tk);
-  int we = top_winner(te);
-  if (we >= -1) {   // an unsure level near the feasible top could win
-    const float Me = warp_max_f(te.s), Mu = warp_max_f(tu);
-    if (Mu >= Me * 0.9999847f) we = -1;
-  } else if (warp_max_f(tu) > 0.f) {
-    we = -1;        // no sure-feasible level, some unsure ones
-  }
-  if (wk == -1 || we == -1) { eval_row_exact<PAR>(c, b, lane, e, k); return; }
-  const uint64_t wC1 = (c.wse == 0 ? (uint64_t)b : 1ull) * c.C1;
-  auto exact = [&](int src, const Top &t) {
-    const int l = __shfl_sync(FULL, t.l, src);
-    const int S = c.Stab[l];
-    Best r; r.found = 1; r.l = l; r.b = b; r.S = S; r.sc = __shfl_sync(FULL, t.s, src);
-    r.X = cell_X<PAR>(S, b, magic, wC1, c.cA, c.cU, c.mem_mode, c.D);
-    return r;
-  };
-  k = exact(wk, tk);
-  e = we >= 0 ? exact(we, te) : best_none();
+  e = warp_best(e);
+  k = warp_best(k);
 }
 
 // exact X(L, b_eval) >= 2^56 test (only when the f64 estimate is within 1e-4 of the limit)
@@ -353,8 +275,7 @@ uint64_t bound_survivors(const uint64_t *cA, const uint64_t *cU, double thr, uin
 // Per-warp shared memory: hist[S_tot+1] u32, cA/cU[S_tot+1] u64 (tables stay valid on return).
 template <int PAR>
 __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k, const uint16_t *Stab,
-                              uint32_t *hist, uint64_t *cA, uint64_t *cU, float *cAf, float *cUf, int lane,
-                              int knee_only, int32_t knee_b) {
+                              uint32_t *hist, uint64_t *cA, uint64_t *cU, int lane, int knee_only, int32_t knee_b) {
   DnnRes res; res.st = DSTACK_ST_OK; res.demand = 0; res.knee = 0; res.b = 0; res.RT = 0; res.D = 0;
   const int L = p.L, S_tot = p.S_tot;
   const int64_t r0 = pb.dnn_row_off[k], r1 = pb.dnn_row_off[k + 1];
@@ -416,7 +337,7 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
     // sum_{N_i >= 1} R_i max(S_tot, b n_i) = S_tot PA[S_tot/b] + b Q[S_tot/b]  (exact, from the scan)
     const int mb = S_tot / b_eval;
     uint64_t pa_mb, q_mb;
-    scan_hist(hist, cA, cU, cAf, cUf, S_tot, Wn, Mtp, mb, &pa_mb, &q_mb, lane);
+    scan_hist(hist, cA, cU, S_tot, Wn, Mtp, mb, &pa_mb, &q_mb, lane);
     const u128 v = (u128)S_tot * pa_mb + (u128)b_eval * q_mb;
     Vmax = v >= ((u128)1 << 63) ? (1ull << 63) : (uint64_t)v;
   }
@@ -436,9 +357,8 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
   }
   const uint64_t RT1 = PAR == 0 ? (uint64_t)RT - hist[0] : 0ull;   // sum R over n_i >= 1
   RowCtx c;
-  c.Stab = Stab; c.cA = cA; c.cU = cU; c.cAf = cAf; c.cUf = cUf; c.L = L; c.mem_mode = mem_mode; c.wse = p.wse_mode;
+  c.Stab = Stab; c.cA = cA; c.cU = cU; c.L = L; c.mem_mode = mem_mode; c.wse = p.wse_mode;
   c.C1 = (uint64_t)t_np * RT * M; c.D = D; c.SLOM = (uint64_t)slo * M; c.aM = (uint64_t)asm_us * M;
-  c.C1f = (float)c.C1; c.Df = (float)D; c.SLOMf = (float)c.SLOM; c.aMf = (float)c.aM;
   // ---- a2/a3: rows evaluated exactly, b_lo (or the knee batch) first, then the b's the bounds keep ----
   Best e, kk, best = best_none();
   uint32_t knee = 0;
@@ -447,7 +367,7 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
   while (todo) {
     const int b = __ffsll((long long)todo);   // b = bit index + 1
     todo &= todo - 1;
-    if (PAR == 1) build_tables_threads(n, r, K, S_tot, Mtp, b, hist, cA, cU, cAf, cUf, lane);
+    if (PAR == 1) build_tables_threads(n, r, K, S_tot, Mtp, b, hist, cA, cU, lane);
     eval_row<PAR>(c, b, lane, e, kk);
     if (first) {
       first = false;
