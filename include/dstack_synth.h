@@ -27,15 +27,19 @@ extern "C" {
 int synth_host_ndnn(const synth_spec_t *spec, int32_t *ndnn /*[num_scen]*/);
 int synth_host_headers(const synth_spec_t *spec, const int32_t *scen_dnn_off,
                        int32_t *nrows, int32_t *t_p, int32_t *t_np, int32_t *mem_bw, int32_t *slo_us,
-                       int32_t *asm_us, int32_t *bmax, int32_t *shape /*[num_dnn] each*/);
+                       int32_t *asm_us, int32_t *bmax, int32_t *shape, int32_t *lam_pct /*[num_dnn] each*/);
 int synth_host_rows(const synth_spec_t *spec, const int32_t *scen_dnn_off, const int64_t *dnn_row_off,
                     uint32_t *n, uint16_t *r, uint32_t *d /*[num_rows] each*/);
+
+/* Gaps (us) of arrivals k0 .. k0+count-1 of the (gscen, dnn) Poisson stream with mean gap mean_q32 (Q32 us). */
+int synth_host_arrival_gaps(uint64_t seed, int32_t cfg_tag, int64_t gscen, uint32_t dnn, uint64_t mean_q32,
+                            uint32_t k0, uint32_t count, uint64_t *gaps);
 
 /* Device build: same semantics, device pointers, asynchronous on `stream` (a cudaStream_t). */
 int synth_dev_ndnn(const synth_spec_t *spec, int32_t *ndnn, void *stream);
 int synth_dev_headers(const synth_spec_t *spec, const int32_t *scen_dnn_off,
                       int32_t *nrows, int32_t *t_p, int32_t *t_np, int32_t *mem_bw, int32_t *slo_us,
-                      int32_t *asm_us, int32_t *bmax, int32_t *shape, void *stream);
+                      int32_t *asm_us, int32_t *bmax, int32_t *shape, int32_t *lam_pct, void *stream);
 int synth_dev_rows(const synth_spec_t *spec, const int32_t *scen_dnn_off, const int64_t *dnn_row_off,
                    uint32_t *n, uint16_t *r, uint32_t *d, void *stream);
 

@@ -49,6 +49,11 @@ class OrCycSum(C.Structure):
                 ("misses", C.c_int32), ("status", C.c_int32), ("trace_n", C.c_int32)]
 
 
+class OrSimOut(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("status", "T_us", "arrived", "in_slo", "late", "unserved", "occ_sum", "runs",
+                                          "misses")]
+
+
 _lib = None
 
 
@@ -64,8 +69,10 @@ def lib():
         L.oracle_knee.argtypes = [P(OrProblem), P(OrParams), C.c_int32, C.c_void_p, C.c_void_p]
         L.oracle_batch_opt.argtypes = [P(OrProblem), P(OrParams)] + [C.c_void_p] * 4
         L.oracle_wmaxmin.argtypes = [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]
-        L.oracle_cycle_direct.argtypes = ([C.c_int32] + [C.c_void_p] * 4 + [C.c_int32] * 3 + [C.c_void_p] * 3
+        L.oracle_cycle_direct.argtypes = ([C.c_int32] + [C.c_void_p] * 4 + [C.c_int32] * 3 + [C.c_void_p] * 4
                                           + [P(OrCycSum), C.c_int32] + [C.c_void_p] * 6)
+        L.oracle_simulate.argtypes = [P(OrProblem), P(OrParams), C.c_void_p, C.c_int32, C.c_uint64, C.c_int32,
+                                      C.c_int64, P(OrSimOut), C.c_void_p, C.c_int64, C.c_int32]
         L.oracle_ideal_direct.argtypes = ([C.c_int32] + [C.c_void_p] * 6 + [C.c_int32, C.c_int64]
                                           + [C.c_void_p] * 3)
         L.oracle_ideal_rows.argtypes = [P(OrProblem), P(OrParams), C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]
@@ -122,7 +129,7 @@ def wmaxmin(demand, L: int) -> np.ndarray:
     return a
 
 
-def cycle_direct(g, sl_slots, bstar, dtab, b_lo: int, L: int, nslots: int, trace_cap: int = 4096):
+def cycle_direct(g, sl_slots, bstar, dtab, b_lo: int, L: int, nslots: int, trace_cap: int = 4096, count0=None):
     """O5 with direct per-DNN inputs. dtab: array [n, 64], dtab[j, b-1] = d_j(b) slots."""
     g = np.ascontiguousarray(g, np.int32); sl = np.ascontiguousarray(sl_slots, np.int32)
     bs = np.ascontiguousarray(bstar, np.int32)
@@ -133,7 +140,8 @@ def cycle_direct(g, sl_slots, bstar, dtab, b_lo: int, L: int, nslots: int, trace
     runs = np.zeros(n, np.int32); served = np.zeros(n, np.int64); jm = np.zeros(n, np.int32)
     s = OrCycSum()
     tr = [np.zeros(trace_cap, np.int32) for _ in range(6)]
-    rc = lib().oracle_cycle_direct(n, _p(g), _p(sl), _p(bs), _p(dt), b_lo, L, nslots, _p(runs), _p(served), _p(jm),
+    c0 = None if count0 is None else np.ascontiguousarray(count0, np.int64)
+    rc = lib().oracle_cycle_direct(n, _p(g), _p(sl), _p(bs), _p(dt), b_lo, L, nslots, _p(c0), _p(runs), _p(served), _p(jm),
                                    C.byref(s), trace_cap, *[_p(t) for t in tr])
     assert rc == 0
     k = s.trace_n
@@ -194,4 +202,20 @@ def evaluate(pb: Problem, p: Params, nthreads: int = 0, subset=None):
         rc = lib().oracle_eval_subset(C.byref(_problem(pb)), C.byref(_params(p)), C.byref(oo), _p(idx),
                                       idx.shape[0], nthreads)
     assert rc == 0, rc
+    return o
+
+
+def simulate(pb: Problem, p: Params, cycles: int, seed: int, cfg_tag: int, scen_base: int = 0, subset=None,
+             nthreads: int = 0):
+    """O7 long-horizon simulation; per-scenario dict (subset: scenario indices, others left zero)."""
+    S = pb.num_scen
+    o = dict(status=np.zeros(S, np.uint8), T_us=np.zeros(S, np.uint32),
+             **{k: np.zeros(S, np.uint64) for k in ("arrived", "in_slo", "late", "unserved", "occ_sum", "runs",
+                                                     "misses")})
+    oo = OrSimOut(*[_p(o[k]) for k, _ in OrSimOut._fields_])
+    lam = np.ascontiguousarray(pb.lam_pct, np.int32)
+    idx = None if subset is None else np.ascontiguousarray(np.asarray(list(subset)), np.int64)
+    rc = lib().oracle_simulate(C.byref(_problem(pb)), C.byref(_params(p)), _p(lam), cycles, seed, cfg_tag, scen_base,
+                               C.byref(oo), _p(idx), 0 if idx is None else idx.shape[0], nthreads)
+    assert rc == 0
     return o

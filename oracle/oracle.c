@@ -11,6 +11,7 @@
  * Shares no code with the CUDA path (paper_2304_13541_b200/csrc).
  */
 #include "oracle.h"
+#include "../synth/synth_core.h"   /* the shared input generator: arrival sampler only */
 #include <stdlib.h>
 #include <string.h>
 #ifdef _OPENMP
@@ -249,11 +250,11 @@ static int fits(const int32_t *occ, int32_t s, int64_t d, int32_t g, int32_t L) 
  *    not running at t, fits at t; slice to the next blocking slot / own next start; largest batch
  *    b <= b* whose runtime fits the slice ("a batch size that can complete within the time slice",
  *    P:2330-2331).                                                                                  */
-int oracle_cycle_direct(int32_t n, const int32_t *g, const int32_t *sl, const int32_t *bstar,
-                        const int64_t *dtab, int32_t b_lo, int32_t L, int32_t nslots,
-                        int32_t *runs, int64_t *served, int32_t *jmiss, or_cyc_sum_t *sum,
-                        int32_t trace_cap, int32_t *tr_dnn, int32_t *tr_start, int32_t *tr_end,
-                        int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep) {
+static int cycle_core(int32_t n, const int32_t *g, const int32_t *sl, const int32_t *bstar,
+                      const int64_t *dtab, int32_t b_lo, int32_t L, int32_t nslots, const int64_t *count0,
+                      int32_t *runs, int64_t *served, int32_t *jmiss, or_cyc_sum_t *sum,
+                      int32_t trace_cap, int32_t *tr_dnn, int32_t *tr_start, int32_t *tr_end,
+                      int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep, run_t **runs_out, int64_t *nrun_out) {
   if (n < 0 || n > 1024 || nslots < 0 || nslots > (1 << 20)) return -1;
   int32_t *occ = (int32_t *)calloc((size_t)nslots + 1, sizeof(int32_t));
   uint8_t *decide = (uint8_t *)calloc((size_t)nslots + 1, 1);
@@ -263,9 +264,9 @@ int oracle_cycle_direct(int32_t n, const int32_t *g, const int32_t *sl, const in
   int64_t runcap = njobs + 16 + 4 * (int64_t)nslots * (n + 1);
   run_t *rl = (run_t *)malloc(sizeof(run_t) * (size_t)runcap);
   int64_t nrun = 0;
-  int32_t count[OR_MAX_DNN_PER_SCEN + 1024];
+  int64_t count[OR_MAX_DNN_PER_SCEN + 1024];
   memset(sum, 0, sizeof(*sum));
-  for (int32_t j = 0; j < n; ++j) { runs[j] = 0; served[j] = 0; jmiss[j] = 0; count[j] = 0; }
+  for (int32_t j = 0; j < n; ++j) { runs[j] = 0; served[j] = 0; jmiss[j] = 0; count[j] = count0 ? count0[j] : 0; }
 
   /* Alg.1 l.3: repeat[] <- S-Length / SLO; jobs with EDF key */
   int64_t q = 0;
@@ -354,8 +355,18 @@ int oracle_cycle_direct(int32_t n, const int32_t *g, const int32_t *sl, const in
     tr_batch[k] = rl[k].batch; tr_kind[k] = rl[k].kind; tr_rep[k] = rl[k].rep;
     sum->trace_n++;
   }
-  free(occ); free(decide); free(jobs); free(rl);
+  free(occ); free(decide); free(jobs);
+  if (runs_out) { *runs_out = rl; *nrun_out = nrun; } else free(rl);
   return 0;
+}
+
+int oracle_cycle_direct(int32_t n, const int32_t *g, const int32_t *sl, const int32_t *bstar,
+                        const int64_t *dtab, int32_t b_lo, int32_t L, int32_t nslots, const int64_t *count0,
+                        int32_t *runs, int64_t *served, int32_t *jmiss, or_cyc_sum_t *sum,
+                        int32_t trace_cap, int32_t *tr_dnn, int32_t *tr_start, int32_t *tr_end,
+                        int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep) {
+  return cycle_core(n, g, sl, bstar, dtab, b_lo, L, nslots, count0, runs, served, jmiss, sum, trace_cap, tr_dnn,
+                    tr_start, tr_end, tr_batch, tr_kind, tr_rep, NULL, NULL);
 }
 
 /* ---------------------------------------------------------------- O6 --- */
@@ -524,7 +535,7 @@ static void eval_scenario(const or_problem_t *pb, const or_params_t *p, or_out_t
   int32_t runs[OR_MAX_DNN_PER_SCEN], jmiss[OR_MAX_DNN_PER_SCEN];
   int64_t served[OR_MAX_DNN_PER_SCEN];
   or_cyc_sum_t cs;
-  oracle_cycle_direct(nd, g, sl, bst, dtab, p->b_min, p->L, (int32_t)nslots, runs, served, jmiss, &cs, 0,
+  oracle_cycle_direct(nd, g, sl, bst, dtab, p->b_min, p->L, (int32_t)nslots, NULL, runs, served, jmiss, &cs, 0,
                       NULL, NULL, NULL, NULL, NULL, NULL);
   for (int32_t j = 0; j < nd; ++j) {
     o->runs[k0 + j] = (uint16_t)runs[j];
@@ -602,5 +613,161 @@ int oracle_eval_subset(const or_problem_t *pb, const or_params_t *p, or_out_t *o
 #endif
 #pragma omp parallel for schedule(dynamic, 1)
   for (int64_t q = 0; q < count; ++q) eval_scenario(pb, p, o, idx[q]);
+  return 0;
+}
+
+/* ---------------------------------------------------------------- O7 --- */
+
+/* Arrival cursor of one DNN's Poisson stream (input generator, synth_core.h): index of the next arrival
+ * and its absolute time in us. */
+typedef struct { uint64_t idx, time, mean_q32; uint64_t seed; int32_t cfg; int64_t gs; uint32_t j; } arr_t;
+
+static void arr_init(arr_t *a, uint64_t seed, int32_t cfg, int64_t gs, uint32_t j, uint64_t mean_q32) {
+  a->seed = seed; a->cfg = cfg; a->gs = gs; a->j = j; a->mean_q32 = mean_q32; a->idx = 0;
+  a->time = sy_arrival_gap(mean_q32, sy_arrival_word(seed, cfg, gs, j, 0));
+}
+static void arr_next(arr_t *a) {
+  a->idx++;
+  a->time += sy_arrival_gap(a->mean_q32, sy_arrival_word(a->seed, a->cfg, a->gs, a->j, (uint32_t)a->idx));
+}
+/* A(t): number of arrivals with time <= t */
+static uint64_t arr_count(arr_t *a, uint64_t t) {
+  while (a->time <= t) arr_next(a);
+  return a->idx;
+}
+
+static int run_cmp(const void *x, const void *y) {
+  const run_t *a = (const run_t *)x, *b = (const run_t *)y;
+  if (a->j != b->j) return a->j < b->j ? -1 : 1;
+  return a->start < b->start ? -1 : (a->start > b->start);
+}
+
+/* O7 -- long-horizon simulation (config 5, readings in DESIGN.md §3):
+ *  cycle c spans [c T, (c+1) T), T = max SLO over the servable DNNs (status OK);
+ *  Poisson arrivals, mean gap = f_L(l*, b*) / (lam_pct/100 * b_star) (load as a fraction of standalone
+ *  capacity b_star / f_L); at each cycle start the active DNNs are those with queued requests; WMAX-MIN over
+ *  their demands ("dynamic re-allocation"); one O5 session with the fill ordered by the scoreboard
+ *  (runs in the last 10 sessions + this one); the runs then execute in time order, each serving
+ *  FIFO min(planned batch, queue at its start) requests; a run that finds an empty queue is void (not
+ *  counted, no occupancy).  A request is late iff completion - arrival > SLO; requests still queued at
+ *  the horizon are unserved (both are SLO violations). */
+static void simulate_scenario(const or_problem_t *pb, const or_params_t *p, const int32_t *lam_pct, int32_t cycles,
+                              uint64_t seed, int32_t cfg_tag, int64_t scen_base, or_sim_out_t *o, int64_t s) {
+  const int32_t k0 = pb->scen_dnn_off[s], k1 = pb->scen_dnn_off[s + 1];
+  const int32_t nd = k1 - k0;
+  o->status[s] = OR_OK; o->T_us[s] = 0; o->arrived[s] = 0; o->in_slo[s] = 0; o->late[s] = 0;
+  o->unserved[s] = 0; o->occ_sum[s] = 0; o->runs[s] = 0; o->misses[s] = 0;
+  if (nd > OR_MAX_DNN_PER_SCEN) { o->status[s] = OR_INVALID; return; }
+  if (nd <= 0) { o->status[s] = OR_INFEASIBLE; return; }
+  uint16_t dem[OR_MAX_DNN_PER_SCEN], knee[OR_MAX_DNN_PER_SCEN];
+  uint8_t bst8[OR_MAX_DNN_PER_SCEN], st[OR_MAX_DNN_PER_SCEN];
+  int64_t T = 0;
+  for (int32_t j = 0; j < nd; ++j) {
+    dnn_t m = get_dnn(pb, p, k0 + j);
+    batch_opt_one(&m, p, dem + j, bst8 + j, knee + j, st + j);
+    if (st[j] == OR_OK && pb->slo_us[k0 + j] > T) T = pb->slo_us[k0 + j];
+  }
+  if (T == 0) { o->status[s] = OR_INFEASIBLE; return; }
+  const int64_t nslots = T / p->slot_us;
+  int64_t njobs = 0;
+  for (int32_t j = 0; j < nd; ++j) if (st[j] == OR_OK) njobs += nslots / (pb->slo_us[k0 + j] / p->slot_us);
+  if (nslots > OR_MAX_SLOTS || njobs > OR_MAX_JOBS) { o->status[s] = OR_INVALID; return; }
+  o->T_us[s] = (uint32_t)T;
+  arr_t arr[OR_MAX_DNN_PER_SCEN], head[OR_MAX_DNN_PER_SCEN];
+  uint64_t served[OR_MAX_DNN_PER_SCEN];
+  int64_t ring[10][OR_MAX_DNN_PER_SCEN], sb[OR_MAX_DNN_PER_SCEN];
+  memset(ring, 0, sizeof(ring)); memset(sb, 0, sizeof(sb));
+  for (int32_t j = 0; j < nd; ++j) {
+    served[j] = 0;
+    if (st[j] != OR_OK) continue;
+    /* mean gap (us) = f_L(l*, b*) * 100 / (lam_pct * b*),  f_L = X / (S M); Q32, capped at 2^30 us */
+    dnn_t m = get_dnn(pb, p, k0 + j);
+    const int64_t ls = dem[j] - p->margin > 0 ? dem[j] - p->margin : 1;   /* l* (demand = l* + margin) */
+    const int64_t S = S_of(p, ls);
+    const u128 X = X_of(&m, p, S, bst8[j]);
+    const u128 den = (u128)S * (u128)m.M * (u128)lam_pct[k0 + j] * (u128)bst8[j];
+    u128 mq = ((X * 100) << 32) / den;
+    if (mq > ((u128)1 << 62)) mq = (u128)1 << 62;
+    arr_init(arr + j, seed, cfg_tag, scen_base + s, (uint32_t)j, (uint64_t)mq);
+    arr_init(head + j, seed, cfg_tag, scen_base + s, (uint32_t)j, (uint64_t)mq);
+  }
+  int32_t g[OR_MAX_DNN_PER_SCEN], sl[OR_MAX_DNN_PER_SCEN], bst[OR_MAX_DNN_PER_SCEN];
+  int64_t dtab[OR_MAX_DNN_PER_SCEN * 64];
+  uint16_t dm[OR_MAX_DNN_PER_SCEN];
+  uint32_t alloc[OR_MAX_DNN_PER_SCEN];
+  for (int32_t c = 0; c < cycles; ++c) {
+    const uint64_t t0 = (uint64_t)c * (uint64_t)T;
+    for (int32_t j = 0; j < nd; ++j) {
+      dm[j] = 0;
+      if (st[j] != OR_OK) continue;
+      const uint64_t A = arr_count(arr + j, t0);
+      if (A > served[j]) dm[j] = dem[j];                 /* active: requests queued at the cycle start */
+    }
+    oracle_wmaxmin(nd, dm, p->L, alloc);
+    for (int32_t j = 0; j < nd; ++j) {
+      g[j] = 0; sl[j] = pb->slo_us[k0 + j] / p->slot_us; bst[j] = bst8[j];
+      if (dm[j] == 0) continue;
+      const int32_t al = (int32_t)(alloc[j] >> 16);
+      g[j] = dm[j] > al ? dm[j] : al;
+      dnn_t m = get_dnn(pb, p, k0 + j);
+      const int64_t S = S_of(p, g[j]);
+      const u128 den = (u128)S * (u128)m.M * (u128)p->slot_us;
+      for (int32_t b = p->b_min; b <= bst[j]; ++b) {
+        const u128 X = X_of(&m, p, S, b);
+        const u128 dd = (X + den - 1) / den;
+        dtab[j * 64 + b - 1] = dd > (u128)0x7FFFFFFFFFFFLL ? 0x7FFFFFFFFFFFLL : (int64_t)dd;
+      }
+    }
+    int32_t runs[OR_MAX_DNN_PER_SCEN], jmiss[OR_MAX_DNN_PER_SCEN];
+    int64_t srv[OR_MAX_DNN_PER_SCEN];
+    or_cyc_sum_t cs;
+    run_t *rl = NULL;
+    int64_t nrun = 0;
+    cycle_core(nd, g, sl, bst, dtab, p->b_min, p->L, (int32_t)nslots, sb, runs, srv, jmiss, &cs, 0, NULL, NULL,
+               NULL, NULL, NULL, NULL, &rl, &nrun);
+    o->misses[s] += (uint64_t)cs.misses;
+    qsort(rl, (size_t)nrun, sizeof(run_t), run_cmp);     /* per DNN, in start order */
+    int64_t cnt[OR_MAX_DNN_PER_SCEN];
+    for (int32_t j = 0; j < nd; ++j) cnt[j] = 0;
+    for (int64_t q = 0; q < nrun; ++q) {
+      const int32_t j = rl[q].j;
+      const uint64_t ts = t0 + (uint64_t)rl[q].start * (uint64_t)p->slot_us;
+      const uint64_t te = t0 + (uint64_t)rl[q].end * (uint64_t)p->slot_us;
+      const uint64_t A = arr_count(arr + j, ts);
+      uint64_t k = A - served[j];
+      if (k > (uint64_t)rl[q].batch) k = (uint64_t)rl[q].batch;
+      if (k == 0) continue;                               /* empty queue: the run is void */
+      for (uint64_t i = 0; i < k; ++i) {
+        if (te - head[j].time > (uint64_t)pb->slo_us[k0 + j]) o->late[s]++; else o->in_slo[s]++;
+        arr_next(head + j);
+      }
+      served[j] += k;
+      cnt[j]++;
+      o->occ_sum[s] += (uint64_t)g[j] * (uint64_t)(rl[q].end - rl[q].start);
+      o->runs[s]++;
+    }
+    free(rl);
+    for (int32_t j = 0; j < nd; ++j) { sb[j] += cnt[j] - ring[c % 10][j]; ring[c % 10][j] = cnt[j]; }
+  }
+  const uint64_t tend = (uint64_t)cycles * (uint64_t)T;
+  for (int32_t j = 0; j < nd; ++j) {
+    if (st[j] != OR_OK) continue;
+    const uint64_t A = arr_count(arr + j, tend);
+    o->arrived[s] += A;
+    o->unserved[s] += A - served[j];
+  }
+}
+
+int oracle_simulate(const or_problem_t *pb, const or_params_t *p, const int32_t *lam_pct, int32_t cycles,
+                    uint64_t seed, int32_t cfg_tag, int64_t scen_base, or_sim_out_t *o, const int64_t *scen_idx,
+                    int64_t count, int32_t nthreads) {
+  if (!pb || !p || !o || !lam_pct || cycles < 0 || check_params(p)) return -1;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+  const int64_t n = scen_idx ? count : pb->num_scen;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t q = 0; q < n; ++q)
+    simulate_scenario(pb, p, lam_pct, cycles, seed, cfg_tag, scen_base, o, scen_idx ? scen_idx[q] : q);
   return 0;
 }

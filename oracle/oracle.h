@@ -68,6 +68,7 @@ int oracle_wmaxmin(int32_t n, const uint16_t *demand, int32_t L, uint32_t *alloc
 
 /* O5 with direct per-DNN inputs (test hook; also used internally).
  * dtab[j*64 + b-1] = d_j(b) in slots for b in [b_lo, bstar_j]. g_j == 0 => inactive.
+ * count0 (nullable): initial fill-priority counts (config-5 scoreboard); NULL = 0.
  * Trace (optional, cap may be 0): one entry per placed run. kind 0 static, 1 fill. */
 typedef struct {
   int64_t occ_static_sum, occ_sum, served_total;
@@ -75,7 +76,7 @@ typedef struct {
   int32_t trace_n;
 } or_cyc_sum_t;
 int oracle_cycle_direct(int32_t n, const int32_t *g, const int32_t *sl_slots, const int32_t *bstar,
-                        const int64_t *dtab, int32_t b_lo, int32_t L, int32_t nslots,
+                        const int64_t *dtab, int32_t b_lo, int32_t L, int32_t nslots, const int64_t *count0,
                         int32_t *runs, int64_t *served, int32_t *jmiss, or_cyc_sum_t *sum,
                         int32_t trace_cap, int32_t *tr_dnn, int32_t *tr_start, int32_t *tr_end,
                         int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep);
@@ -90,6 +91,15 @@ int oracle_ideal_direct(int32_t n, const int64_t *chain_off, const int32_t *ex_g
 /* Per-kernel ideal demand/duration for the rows of DNN `dnn` at batch b (O6 setup). */
 int oracle_ideal_rows(const or_problem_t *pb, const or_params_t *p, int64_t dnn, int32_t b,
                       int32_t *g_out, int64_t *tau_out);
+
+/* O7 long-horizon simulation (config 5).  Per scenario outputs [num_scen]. */
+typedef struct {
+  uint8_t *status; uint32_t *T_us;
+  uint64_t *arrived, *in_slo, *late, *unserved, *occ_sum, *runs, *misses;
+} or_sim_out_t;
+int oracle_simulate(const or_problem_t *pb, const or_params_t *p, const int32_t *lam_pct, int32_t cycles,
+                    uint64_t seed, int32_t cfg_tag, int64_t scen_base, or_sim_out_t *out, const int64_t *scen_idx,
+                    int64_t count, int32_t nthreads);
 
 /* Whole path a1-a6 over every scenario (OpenMP over scenarios, nthreads <= 0 => default). */
 int oracle_eval(const or_problem_t *pb, const or_params_t *p, or_out_t *out, int32_t nthreads);

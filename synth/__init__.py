@@ -98,6 +98,7 @@ class Problem:
     r: np.ndarray              # uint16 [R]
     d: np.ndarray              # uint32 [R]
     shape: np.ndarray = field(default=None)  # int32 [D] (reporting only)
+    lam_pct: np.ndarray = field(default=None)  # int32 [D] config-5 offered load, % of standalone capacity
 
     @property
     def num_scen(self) -> int:
@@ -121,7 +122,7 @@ class Problem:
     def subset(self, scen) -> "Problem":
         scen = [int(s) for s in scen]
         offs = [0]; dnn_rows = [0]
-        tp, tnp, mb, slo, asm, bm, shp, ns, rs, ds = ([] for _ in range(10))
+        tp, tnp, mb, slo, asm, bm, shp, ns, rs, ds, lp = ([] for _ in range(11))
         for s in scen:
             k0, k1 = int(self.scen_dnn_off[s]), int(self.scen_dnn_off[s + 1])
             offs.append(offs[-1] + (k1 - k0))
@@ -133,12 +134,14 @@ class Problem:
             slo.append(self.slo_us[k0:k1]); asm.append(self.asm_us[k0:k1]); bm.append(self.bmax[k0:k1])
             if self.shape is not None:
                 shp.append(self.shape[k0:k1])
+            if self.lam_pct is not None:
+                lp.append(self.lam_pct[k0:k1])
         cat = lambda xs, dt: (np.concatenate(xs).astype(dt) if xs else np.zeros(0, dt))
         return make_problem(
             np.asarray(offs, np.int32), np.asarray(dnn_rows, np.int64), cat(tp, np.int32), cat(tnp, np.int32),
             cat(mb, np.int32), cat(slo, np.int32), cat(asm, np.int32), cat(bm, np.int32),
             cat(ns, np.uint32), cat(rs, np.uint16), cat(ds, np.uint32),
-            cat(shp, np.int32) if shp else None)
+            cat(shp, np.int32) if shp else None, cat(lp, np.int32) if lp else None)
 
 
 def _pad(a: np.ndarray, extra: int = 8) -> np.ndarray:
@@ -147,7 +150,8 @@ def _pad(a: np.ndarray, extra: int = 8) -> np.ndarray:
     return out
 
 
-def make_problem(scen_dnn_off, dnn_row_off, t_p, t_np, mem_bw, slo_us, asm_us, bmax, n, r, d, shape=None) -> Problem:
+def make_problem(scen_dnn_off, dnn_row_off, t_p, t_np, mem_bw, slo_us, asm_us, bmax, n, r, d, shape=None,
+                 lam_pct=None) -> Problem:
     """Build a Problem from explicit arrays (hand-written test instances)."""
     R = int(np.asarray(dnn_row_off)[-1])
     n = np.asarray(n, np.uint32)[:R]; r = np.asarray(r, np.uint16)[:R]; d = np.asarray(d, np.uint32)[:R]
@@ -156,7 +160,8 @@ def make_problem(scen_dnn_off, dnn_row_off, t_p, t_np, mem_bw, slo_us, asm_us, b
         np.ascontiguousarray(t_p, np.int32), np.ascontiguousarray(t_np, np.int32),
         np.ascontiguousarray(mem_bw, np.int32), np.ascontiguousarray(slo_us, np.int32),
         np.ascontiguousarray(asm_us, np.int32), np.ascontiguousarray(bmax, np.int32),
-        _pad(n), _pad(r), _pad(d), None if shape is None else np.ascontiguousarray(shape, np.int32))
+        _pad(n), _pad(r), _pad(d), None if shape is None else np.ascontiguousarray(shape, np.int32),
+        None if lam_pct is None else np.ascontiguousarray(lam_pct, np.int32))
 
 
 _host = None
@@ -170,8 +175,10 @@ def _host_lib():
         lib = C.CDLL(HOST_LIB)
         P = C.POINTER
         lib.synth_host_ndnn.argtypes = [P(SynthSpec), C.c_void_p]
-        lib.synth_host_headers.argtypes = [P(SynthSpec)] + [C.c_void_p] * 9
+        lib.synth_host_headers.argtypes = [P(SynthSpec)] + [C.c_void_p] * 10
         lib.synth_host_rows.argtypes = [P(SynthSpec)] + [C.c_void_p] * 5
+        lib.synth_host_arrival_gaps.argtypes = [C.c_uint64, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_uint32,
+                                                C.c_uint32, C.c_void_p]
         _host = lib
     return _host
 
@@ -189,15 +196,15 @@ def generate_host(spec: Spec) -> Problem:
     off = np.zeros(S + 1, np.int32)
     np.cumsum(ndnn, out=off[1:])
     D = int(off[-1])
-    hdr = [np.zeros(D, np.int32) for _ in range(8)]
+    hdr = [np.zeros(D, np.int32) for _ in range(9)]
     assert lib.synth_host_headers(C.byref(cs), _ptr(off), *[_ptr(h) for h in hdr]) == 0
-    nrows, t_p, t_np, mem_bw, slo, asm, bmax, shape = hdr
+    nrows, t_p, t_np, mem_bw, slo, asm, bmax, shape, lam = hdr
     roff = np.zeros(D + 1, np.int64)
     np.cumsum(nrows.astype(np.int64), out=roff[1:])
     R = int(roff[-1])
     n = np.zeros(R + 8, np.uint32); r = np.zeros(R + 8, np.uint16); d = np.zeros(R + 8, np.uint32)
     assert lib.synth_host_rows(C.byref(cs), _ptr(off), _ptr(roff), _ptr(n), _ptr(r), _ptr(d)) == 0
-    return Problem(off, roff, t_p, t_np, mem_bw, slo, asm, bmax, n, r, d, shape)
+    return Problem(off, roff, t_p, t_np, mem_bw, slo, asm, bmax, n, r, d, shape, lam)
 
 
 _dev = None
@@ -211,7 +218,7 @@ def _dev_lib():
         lib = C.CDLL(DEV_LIB)
         P = C.POINTER
         lib.synth_dev_ndnn.argtypes = [P(SynthSpec), C.c_void_p, C.c_void_p]
-        lib.synth_dev_headers.argtypes = [P(SynthSpec)] + [C.c_void_p] * 10
+        lib.synth_dev_headers.argtypes = [P(SynthSpec)] + [C.c_void_p] * 11
         lib.synth_dev_rows.argtypes = [P(SynthSpec)] + [C.c_void_p] * 6
         _dev = lib
     return _dev
@@ -232,11 +239,11 @@ def generate_device(spec: Spec, device="cuda"):
     off = torch.zeros(S + 1, **i32)
     off[1:] = torch.cumsum(ndnn, 0, dtype=torch.int32)
     D = int(off[-1].item())
-    hdr = [torch.zeros(max(D, 1), **i32) for _ in range(8)]
+    hdr = [torch.zeros(max(D, 1), **i32) for _ in range(9)]
     assert lib.synth_dev_headers(C.byref(cs), C.c_void_p(off.data_ptr()),
                                  *[C.c_void_p(h.data_ptr()) for h in hdr], C.c_void_p(stream)) == 0
     hdr = [h[:D] for h in hdr]
-    nrows, t_p, t_np, mem_bw, slo, asm, bmax, shape = hdr
+    nrows, t_p, t_np, mem_bw, slo, asm, bmax, shape, lam = hdr
     roff = torch.zeros(D + 1, dtype=torch.int64, device=dev)
     roff[1:] = torch.cumsum(nrows.to(torch.int64), 0)
     R = int(roff[-1].item())
@@ -248,7 +255,7 @@ def generate_device(spec: Spec, device="cuda"):
                               C.c_void_p(n.data_ptr()), C.c_void_p(r.data_ptr()), C.c_void_p(d.data_ptr()),
                               C.c_void_p(stream)) == 0
     return dict(scen_dnn_off=off, dnn_row_off=roff, t_p=t_p, t_np=t_np, mem_bw=mem_bw, slo_us=slo,
-                asm_us=asm, bmax=bmax, n=n, r=r, d=d, shape=shape)
+                asm_us=asm, bmax=bmax, n=n, r=r, d=d, shape=shape, lam_pct=lam)
 
 
 # ---------------------------------------------------------------- configs ---
@@ -290,7 +297,7 @@ def concat(problems) -> Problem:
     problems = list(problems)
     offs, roffs = [np.zeros(1, np.int32)], [np.zeros(1, np.int64)]
     d0, r0 = 0, 0
-    cols = {k: [] for k in ("t_p", "t_np", "mem_bw", "slo_us", "asm_us", "bmax", "shape")}
+    cols = {k: [] for k in ("t_p", "t_np", "mem_bw", "slo_us", "asm_us", "bmax", "shape", "lam_pct")}
     rows = {k: [] for k in ("n", "r", "d")}
     for pb in problems:
         offs.append(pb.scen_dnn_off[1:] + d0)
@@ -305,10 +312,18 @@ def concat(problems) -> Problem:
         r0 += R
     return make_problem(np.concatenate(offs), np.concatenate(roffs), *[np.concatenate(cols[k]) for k in
                         ("t_p", "t_np", "mem_bw", "slo_us", "asm_us", "bmax")],
-                        *[np.concatenate(rows[k]) for k in ("n", "r", "d")], np.concatenate(cols["shape"]))
+                        *[np.concatenate(rows[k]) for k in ("n", "r", "d")], np.concatenate(cols["shape"]),
+                        np.concatenate(cols["lam_pct"]))
 
 
 def sample(spec: Spec, indices) -> Problem:
     """Scenarios at the given local indices of `spec`, drawn one by one on the host (stratified samples
     of device-generated workloads: same bytes as the device draw)."""
     return concat(generate_host(spec.replace(scen_base=spec.scen_base + int(i), num_scen=1)) for i in indices)
+
+
+def arrival_gaps(seed: int, cfg_tag: int, gscen: int, dnn: int, mean_q32: int, k0: int, count: int) -> np.ndarray:
+    """Gaps (us) of arrivals k0.. of one Poisson stream (config 5), from the shared integer sampler."""
+    out = np.zeros(count, np.uint64)
+    assert _host_lib().synth_host_arrival_gaps(seed, cfg_tag, gscen, dnn, mean_q32, k0, count, _ptr(out)) == 0
+    return out

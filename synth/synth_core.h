@@ -98,6 +98,7 @@ SY_FN int32_t sy_ndnn(const synth_spec_t *sp, int64_t s) {
 typedef struct {
   int32_t shape, nrows, t_p, t_np, slo_us, asm_us, bmax, mem_bw;
   int32_t n0;      /* ResNet: first-kernel width; BERT: block length */
+  int32_t lam_pct; /* config 5: offered load as % of standalone capacity, U{30..120} */
 } sy_dnn_t;
 
 SY_FN int32_t sy_pick_shape(const synth_spec_t *sp, uint32_t u) {
@@ -130,6 +131,7 @@ SY_FN sy_dnn_t sy_dnn(const synth_spec_t *sp, int64_t s, int32_t j) {
   }
   h.bmax = sp->bmax;
   h.mem_bw = sp->mem_bw;
+  h.lam_pct = (int32_t)sy_uni(w2.v[3], 30, 120);
   h.t_np = (int32_t)sy_uni(w2.v[1], 3, 8) * (sp->heavy ? 2 : 1);
   switch (h.shape) {
     case SY_MOBILENET:
@@ -222,6 +224,76 @@ SY_FN sy_row_t sy_row(const synth_spec_t *sp, int64_t s, int32_t j, const sy_dnn
     o.n = (uint32_t)n;
   }
   return o;
+}
+
+
+/* ---------------------------------------------------------------- arrivals ----
+ * Poisson request arrivals for the long-horizon simulation (config 5): gap_k =
+ * max(1, floor(mean * E_k)) us, E_k = -ln U_k, U_k = (u_k + 1) / 2^32, u_k the k-th Philox word of the
+ * (scenario, dnn) stream.  -ln U is evaluated in Q31 fixed point (log2 by a 257-entry table with linear
+ * interpolation) so host and device draw IDENTICAL integer gaps.  The mean gap (Q32 us) is an input:
+ * the generator holds no method arithmetic. */
+static const uint32_t SY_LOG2_Q31[257] = {
+  0u, 12078627u, 24110347u, 36095523u, 48034513u, 59927671u, 71775349u, 83577893u,
+  95335645u, 107048945u, 118718126u, 130343521u, 141925456u, 153464255u, 164960239u, 176413723u,
+  187825021u, 199194443u, 210522295u, 221808880u, 233054496u, 244259442u, 255424009u, 266548488u,
+  277633165u, 288678325u, 299684247u, 310651211u, 321579490u, 332469358u, 343321082u, 354134928u,
+  364911162u, 375650043u, 386351829u, 397016776u, 407645136u, 418237160u, 428793095u, 439313187u,
+  449797678u, 460246807u, 470660814u, 481039932u, 491384396u, 501694436u, 511970279u, 522212153u,
+  532420281u, 542594885u, 552736183u, 562844395u, 572919734u, 582962413u, 592972645u, 602950638u,
+  612896598u, 622810731u, 632693241u, 642544327u, 652364189u, 662153025u, 671911030u, 681638398u,
+  691335320u, 701001986u, 710638585u, 720245302u, 729822324u, 739369832u, 748888009u, 758377033u,
+  767837083u, 777268336u, 786670965u, 796045145u, 805391046u, 814708840u, 823998694u, 833260775u,
+  842495250u, 851702282u, 860882034u, 870034667u, 879160341u, 888259214u, 897331443u, 906377184u,
+  915396590u, 924389816u, 933357012u, 942298328u, 951213914u, 960103918u, 968968484u, 977807760u,
+  986621888u, 995411012u, 1004175273u, 1012914810u, 1021629764u, 1030320272u, 1038986470u, 1047628495u,
+  1056246482u, 1064840562u, 1073410869u, 1081957534u, 1090480686u, 1098980456u, 1107456970u, 1115910356u,
+  1124340739u, 1132748245u, 1141132997u, 1149495118u, 1157834731u, 1166151954u, 1174446910u, 1182719716u,
+  1190970490u, 1199199350u, 1207406412u, 1215591791u, 1223755601u, 1231897955u, 1240018966u, 1248118746u,
+  1256197405u, 1264255053u, 1272291800u, 1280307752u, 1288303019u, 1296277705u, 1304231918u, 1312165761u,
+  1320079339u, 1327972754u, 1335846110u, 1343699509u, 1351533050u, 1359346835u, 1367140963u, 1374915531u,
+  1382670639u, 1390406384u, 1398122861u, 1405820167u, 1413498396u, 1421157644u, 1428798003u, 1436419566u,
+  1444022426u, 1451606675u, 1459172403u, 1466719700u, 1474248656u, 1481759361u, 1489251901u, 1496726366u,
+  1504182841u, 1511621414u, 1519042169u, 1526445193u, 1533830570u, 1541198383u, 1548548716u, 1555881652u,
+  1563197273u, 1570495661u, 1577776895u, 1585041058u, 1592288229u, 1599518487u, 1606731910u, 1613928578u,
+  1621108567u, 1628271955u, 1635418819u, 1642549234u, 1649663276u, 1656761020u, 1663842541u, 1670907913u,
+  1677957208u, 1684990500u, 1692007863u, 1699009366u, 1705995083u, 1712965083u, 1719919439u, 1726858219u,
+  1733781493u, 1740689331u, 1747581801u, 1754458972u, 1761320910u, 1768167684u, 1774999361u, 1781816006u,
+  1788617686u, 1795404466u, 1802176412u, 1808933588u, 1815676059u, 1822403888u, 1829117139u, 1835815874u,
+  1842500157u, 1849170050u, 1855825614u, 1862466912u, 1869094003u, 1875706949u, 1882305810u, 1888890646u,
+  1895461516u, 1902018479u, 1908561594u, 1915090920u, 1921606515u, 1928108435u, 1934596739u, 1941071483u,
+  1947532725u, 1953980519u, 1960414922u, 1966835990u, 1973243777u, 1979638338u, 1986019729u, 1992388003u,
+  1998743213u, 2005085414u, 2011414658u, 2017730999u, 2024034488u, 2030325179u, 2036603122u, 2042868370u,
+  2049120974u, 2055360984u, 2061588451u, 2067803426u, 2074005959u, 2080196099u, 2086373895u, 2092539398u,
+  2098692655u, 2104833716u, 2110962628u, 2117079439u, 2123184198u, 2129276951u, 2135357746u, 2141426629u,
+  2147483648u,
+};
+
+SY_FN uint32_t sy_arrival_word(uint64_t seed, int32_t cfg_tag, int64_t gscen, uint32_t dnn, uint32_t k) {
+  sy_u4 w = sy_philox(((uint32_t)cfg_tag << 16) | SY_F_ARR, (uint32_t)gscen,
+                      dnn ^ ((uint32_t)((uint64_t)gscen >> 32) << 24), k >> 2, (uint32_t)seed, (uint32_t)(seed >> 32));
+  return w.v[k & 3u];
+}
+
+/* -ln((u + 1) / 2^32) in Q31 (0 <= result < 22.2 * 2^31) */
+SY_FN uint64_t sy_neglog_q31(uint32_t u) {
+  const uint64_t v = (uint64_t)u + 1u;            /* 1 .. 2^32 */
+  if (v >> 32) return 0;                          /* U = 1 */
+  int e = 31;
+  while (!((v >> e) & 1u)) --e;                   /* floor(log2 v) */
+  const uint32_t mant = (uint32_t)(v << (31 - e)); /* 1.f in Q31, top bit set */
+  const uint32_t frac = mant & 0x7FFFFFFFu;
+  const uint32_t i = frac >> 23, rem = frac & 0x7FFFFFu;
+  const uint64_t l2f = SY_LOG2_Q31[i] + (((uint64_t)(SY_LOG2_Q31[i + 1] - SY_LOG2_Q31[i]) * rem) >> 23);
+  const uint64_t l2 = ((uint64_t)e << 31) + l2f;  /* log2 v in Q31 */
+  const uint64_t d = ((uint64_t)32 << 31) - l2;   /* -log2 U in Q31, < 2^36 */
+  return (uint64_t)(((unsigned __int128)d * 1488522236u) >> 31);   /* x ln 2 (Q31) */
+}
+
+/* gap in us for the mean gap mean_q32 (Q32 us, < 2^62): max(1, floor(mean * E)) */
+SY_FN uint64_t sy_arrival_gap(uint64_t mean_q32, uint32_t u) {
+  const uint64_t g = (uint64_t)(((unsigned __int128)mean_q32 * sy_neglog_q31(u)) >> 63);
+  return g < 1 ? 1 : g;
 }
 
 #endif

@@ -12,13 +12,14 @@ __global__ void k_ndnn(synth_spec_t sp, int32_t *ndnn) {
 }
 
 __global__ void k_headers(synth_spec_t sp, const int32_t *off, int32_t *nrows, int32_t *t_p, int32_t *t_np,
-                          int32_t *mem_bw, int32_t *slo_us, int32_t *asm_us, int32_t *bmax, int32_t *shape) {
+                          int32_t *mem_bw, int32_t *slo_us, int32_t *asm_us, int32_t *bmax, int32_t *shape,
+                          int32_t *lam_pct) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < sp.num_scen;
        s += (int64_t)gridDim.x * blockDim.x) {
     for (int32_t k = off[s]; k < off[s + 1]; ++k) {
       sy_dnn_t h = sy_dnn(&sp, s, k - off[s]);
       nrows[k] = h.nrows; t_p[k] = h.t_p; t_np[k] = h.t_np; mem_bw[k] = h.mem_bw;
-      slo_us[k] = h.slo_us; asm_us[k] = h.asm_us; bmax[k] = h.bmax; shape[k] = h.shape;
+      slo_us[k] = h.slo_us; asm_us[k] = h.asm_us; bmax[k] = h.bmax; shape[k] = h.shape; lam_pct[k] = h.lam_pct;
     }
   }
 }
@@ -59,11 +60,11 @@ extern "C" int synth_dev_ndnn(const synth_spec_t *sp, int32_t *ndnn, void *strea
 
 extern "C" int synth_dev_headers(const synth_spec_t *sp, const int32_t *off, int32_t *nrows, int32_t *t_p,
                                  int32_t *t_np, int32_t *mem_bw, int32_t *slo_us, int32_t *asm_us,
-                                 int32_t *bmax, int32_t *shape, void *stream) {
+                                 int32_t *bmax, int32_t *shape, int32_t *lam_pct, void *stream) {
   if (!sp || !off || sp->num_scen < 0) return -1;
   if (sp->num_scen == 0) return 0;
   k_headers<<<grid_for(sp->num_scen, 256), 256, 0, (cudaStream_t)stream>>>(*sp, off, nrows, t_p, t_np, mem_bw,
-                                                                          slo_us, asm_us, bmax, shape);
+                                                                          slo_us, asm_us, bmax, shape, lam_pct);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
