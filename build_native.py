@@ -64,7 +64,7 @@ def build_product(force=False, verbose=False):
     if not cus:
         return None
     out = os.path.join(ROOT, "paper_2304_13541_b200", "libdstack.so")
-    deps = cus + hdrs + [os.path.join(ROOT, "include", "dstack.h")]
+    deps = cus + hdrs + [os.path.join(ROOT, "include", "dstack.h"), os.path.join(ROOT, "synth", "synth_core.h")]
     if force or _stale(out, deps):
         log = _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v", "-shared", "-Xcompiler", "-fPIC",
                     "-I", os.path.join(ROOT, "include"), *cus, "-o", out])

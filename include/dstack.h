@@ -63,6 +63,8 @@ extern "C" {
 #define DSTACK_MAX_ROWS_PER_DNN 65535
 #define DSTACK_MAX_BATCH 64
 
+#define DSTACK_MAX_FILL_RUNS 2048   /* dstack_simulate: fill runs per session (more => scenario INVALID) */
+
 #define DSTACK_FLAG_IDEAL 1u   /* run a6, the ideal per-kernel scheduler */
 
 /* Structure-of-arrays problem set, CSR-indexed.  Scenario s owns DNNs
@@ -171,6 +173,25 @@ int dstack_eval_batch(const dstack_problem_t *pb, const dstack_params_t *p, dsta
  * two-level reduction, fixed grid).  Used when the path is driven call by call. */
 int dstack_aggregate(const dstack_problem_t *pb, const dstack_params_t *p, dstack_out_t *out, void *ws,
                      size_t ws_bytes, void *stream);
+
+/* a7: long-horizon simulation (config 5, readings in DESIGN.md §3).  Per scenario:
+ * cycles sessions of T = max SLO over its servable DNNs; Poisson request arrivals per DNN with mean gap
+ * f_L(l*, b*) * 100 / (lam_pct * b*) us drawn by the counter-based sampler of synth/synth_core.h keyed by
+ * (seed, cfg_tag, scen_base + s, dnn, k); each session: active = queued requests at its start, WMAX-MIN
+ * over their demands, one D-STACK session with the fill ordered by the runs of the last 10 sessions, then
+ * every run serves FIFO min(batch, queue at its start) requests (void if the queue is empty).
+ * Outputs per scenario (all device arrays [num_scen]): status, T_us, arrived, in_slo, late (completed
+ * after arrival + SLO), unserved (queued at the horizon), occ_sum (sum over non-void runs of level x
+ * slots; mean utilisation = occ_sum / (nslots L cycles)), runs (non-void), misses (unplaced static jobs).
+ * Workspace: dstack_sim_workspace_size(). */
+typedef struct {
+  uint8_t *status; uint32_t *T_us;
+  uint64_t *arrived, *in_slo, *late, *unserved, *occ_sum, *runs, *misses;
+} dstack_sim_out_t;
+size_t dstack_sim_workspace_size(const dstack_problem_t *pb, const dstack_params_t *p);
+int dstack_simulate(const dstack_problem_t *pb, const dstack_params_t *p, const int32_t *lam_pct, int32_t cycles,
+                    uint64_t seed, int32_t cfg_tag, int64_t scen_base, dstack_sim_out_t *out, void *ws,
+                    size_t ws_bytes, void *stream);
 
 /* Live per-kernel timing of dstack_eval_batch (bench accounting): after dstack_profile_start, each
  * eval_batch call on this thread records CUDA events on its stream between its kernel launches

@@ -726,6 +726,14 @@ static void simulate_scenario(const or_problem_t *pb, const or_params_t *p, cons
     cycle_core(nd, g, sl, bst, dtab, p->b_min, p->L, (int32_t)nslots, sb, runs, srv, jmiss, &cs, 0, NULL, NULL,
                NULL, NULL, NULL, NULL, &rl, &nrun);
     o->misses[s] += (uint64_t)cs.misses;
+    int64_t nfill = 0;
+    for (int64_t q = 0; q < nrun; ++q) nfill += rl[q].kind == 1;
+    if (nfill > OR_MAX_FILL_RUNS) {                       /* ABI capacity limit: scenario INVALID */
+      free(rl);
+      o->status[s] = OR_INVALID; o->T_us[s] = 0; o->in_slo[s] = o->late[s] = o->occ_sum[s] = o->runs[s] = 0;
+      o->misses[s] = 0;
+      return;
+    }
     qsort(rl, (size_t)nrun, sizeof(run_t), run_cmp);     /* per DNN, in start order */
     int64_t cnt[OR_MAX_DNN_PER_SCEN];
     for (int32_t j = 0; j < nd; ++j) cnt[j] = 0;

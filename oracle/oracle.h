@@ -27,6 +27,7 @@ enum { OR_OK = 0, OR_INFEASIBLE = 1, OR_OVERFLOW = 2, OR_INVALID = 3, OR_OVERSUB
 #define OR_MAX_SLOTS 4096
 #define OR_MAX_JOBS 512
 #define OR_MAX_ROWS_PER_DNN 65535
+#define OR_MAX_FILL_RUNS 2048   /* O7: fill runs per session */
 
 typedef struct {
   int32_t num_scen, num_dnn;

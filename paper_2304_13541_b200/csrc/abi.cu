@@ -272,6 +272,63 @@ int dstack_eval_batch(const dstack_problem_t *pb, const dstack_params_t *p, dsta
   return finish(rc);
 }
 
+// simulate workspace: [eval layout without ideal | demand u16 | knee u16 | batch u8 | status u8 | fill logs]
+struct SimLayout {
+  size_t dem, knee, bat, st, log, end;
+};
+static SimLayout sim_layout(const dstack_problem_t *pb, const dstack_params_t *p) {
+  dstack_params_t q = *p;
+  q.flags = 0;
+  const size_t nd = (size_t)(pb->num_dnn > 0 ? pb->num_dnn : 0);
+  SimLayout l;
+  l.dem = ws_layout(pb, &q).end;
+  l.knee = l.dem + align256(nd * 2);
+  l.bat = l.knee + align256(nd * 2);
+  l.st = l.bat + align256(nd);
+  l.log = l.st + align256(nd);
+  l.end = l.log + align256(sim_fill_log_bytes());
+  return l;
+}
+
+size_t dstack_sim_workspace_size(const dstack_problem_t *pb, const dstack_params_t *p) {
+  if (!problem_ok(pb) || !params_ok(p)) return 0;
+  return sim_layout(pb, p).end;
+}
+
+int dstack_simulate(const dstack_problem_t *pb, const dstack_params_t *p, const int32_t *lam_pct, int32_t cycles,
+                    uint64_t seed, int32_t cfg_tag, int64_t scen_base, dstack_sim_out_t *out, void *ws,
+                    size_t ws_bytes, void *stream) {
+  g_launches = 0;
+  if (!problem_ok(pb) || !params_ok(p) || !out || cycles < 0 || (pb->num_dnn > 0 && !lam_pct)) return DSTACK_EINVAL;
+  if (pb->num_scen > 0 && (!out->status || !out->T_us || !out->arrived || !out->in_slo || !out->late ||
+                           !out->unserved || !out->occ_sum || !out->runs || !out->misses))
+    return DSTACK_EINVAL;
+  const size_t need = dstack_sim_workspace_size(pb, p);
+  if (ws_bytes < need || !ws) return DSTACK_EWORKSPACE;
+  if (!have_device()) return DSTACK_ELAUNCH;
+  cudaStream_t s = (cudaStream_t)stream;
+  const SimLayout sl = sim_layout(pb, p);
+  dstack_params_t q = *p;
+  q.flags = 0;
+  const WsLayout w = ws_layout(pb, &q);
+  char *base = (char *)ws;
+  ProfArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.pb = *pb; a.p = q;
+  a.demand = (uint16_t *)(base + sl.dem); a.knee = (uint16_t *)(base + sl.knee);
+  a.batch = (uint8_t *)(base + sl.bat); a.status = (uint8_t *)(base + sl.st);
+  a.ws_RT = (uint32_t *)(base + w.rt); a.ws_D = (uint64_t *)(base + w.d);
+  int rc = launch_prof(a, s, &g_launches);   // a1-a3 (RT, D for the arrival rates and d_j(b))
+  if (rc) return finish(rc);
+  SimArgs m;
+  std::memset(&m, 0, sizeof(m));
+  m.pb = *pb; m.p = q; m.lam_pct = lam_pct; m.cycles = cycles; m.cfg_tag = cfg_tag; m.seed = seed;
+  m.scen_base = scen_base; m.demand = a.demand; m.batch = a.batch; m.status = a.status; m.ws_RT = a.ws_RT;
+  m.ws_D = a.ws_D; m.dtab_rows = (uint16_t *)(base + w.dtab); m.fill_log = (uint64_t *)(base + sl.log);
+  m.out = *out;
+  return finish(launch_sim(m, s, &g_launches));
+}
+
 int dstack_aggregate(const dstack_problem_t *pb, const dstack_params_t *p, dstack_out_t *out, void *ws,
                      size_t ws_bytes, void *stream) {
   g_launches = 0;

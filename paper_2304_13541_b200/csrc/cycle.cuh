@@ -134,9 +134,17 @@ struct CycRes {
 // One D-STACK session for the scenario held by this warp.  Lane j (< nd) describes DNN j:
 // active, g (level), bs (b*), sl (SLO in slots), rep (= nslots / sl); dtab rows hold d_j(b).
 // hook_b_only: fill may only use b* (test hook).  runs/served are per-lane in/out.
+// count0: per-lane initial fill priority (config-5 scoreboard; 0 for one session).  fill_log (nullable):
+// every fill run appended as pack_run(j, t, d, b) up to fill_cap entries; *fill_n counts them (may exceed cap).
+__device__ __forceinline__ uint64_t pack_run(uint32_t j, uint32_t t, uint32_t d, uint32_t b) {
+  return ((uint64_t)j << 56) | ((uint64_t)t << 32) | ((uint64_t)d << 8) | b;
+}
+
 __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, int lane, bool active, uint32_t g,
                                             uint32_t bs, uint32_t sl, uint32_t rep, int32_t nslots, int32_t L,
-                                            int32_t b_lo, bool hook_b_only, uint32_t &runs, uint32_t &served) {
+                                            int32_t b_lo, bool hook_b_only, uint32_t &runs, uint32_t &served,
+                                            uint32_t count0 = 0, uint64_t *fill_log = nullptr, uint32_t fill_cap = 0,
+                                            uint32_t *fill_n = nullptr) {
   CycRes res; res.occ_static = 0; res.occ_all = 0; res.served_tot = 0; res.misses = 0; res.oversub = false;
   for (int w = lane; (w << 2) < nslots; w += 32) reinterpret_cast<uint32_t *>(sm.occ)[w] = 0u;
   for (int w = lane; w < DSTACK_MAX_SLOTS / 32; w += 32) sm.dmask[w] = 0;
@@ -186,8 +194,9 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   // ---- opportunistic fill at decision times {0} u {run ends} (Dynamic-schedule) ----
   if (lane == 0) sm.dmask[0] |= 1u;
   __syncwarp();
-  uint32_t count = runs;
+  uint32_t count = runs + count0;
   int fs = -1, fe = -1;       // last fill run of this lane's DNN
+  uint32_t nfill = 0;
   int nsr = 0;                // first static window whose run starts after t (amortised, t only grows)
   const uint32_t sl_magic = sl <= 1 ? 0u : (uint32_t)(0xFFFFFFFFu / sl) + 1u;   // t / sl = umulhi(t, magic), t < 2^13
   const int nwords = (nslots + 31) >> 5;
@@ -256,13 +265,18 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       const int dsel = bsel == bsj ? dsj : (int)dj[bsel - 1];
       occ_add(sm.occ, t, dsel, gj, lane);
       occ_t += gj;
-      if (lane == 0 && t + dsel < nslots) sm.dmask[(t + dsel) >> 5] |= 1u << ((t + dsel) & 31);
+      if (lane == 0) {
+        if (t + dsel < nslots) sm.dmask[(t + dsel) >> 5] |= 1u << ((t + dsel) & 31);
+        if (fill_log && nfill < fill_cap) fill_log[nfill] = pack_run((uint32_t)j, (uint32_t)t, (uint32_t)dsel, (uint32_t)bsel);
+      }
+      nfill++;
       __syncwarp();
       if (lane == j) { count++; runs++; served += (uint32_t)bsel; fs = t; fe = t + dsel; }
       if (occ_t + (int)g > L) key = 0xFFFFFFFFu;
     }
   }
   res.occ_all = occ_sum(sm.occ, nslots, lane);
+  if (fill_n) *fill_n = nfill;
   res.served_tot = __reduce_add_sync(FULL, served);
   return res;
 }

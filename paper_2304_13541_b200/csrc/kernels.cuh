@@ -52,6 +52,26 @@ struct CycArgs {
   const uint64_t *ws_D;
 };
 
+constexpr int64_t SIM_MAX_WARPS = 148 * 32;   // persistent-grid cap (sizes the fill-run logs)
+
+struct SimArgs {
+  dstack_problem_t pb;
+  dstack_params_t p;
+  const int32_t *lam_pct;
+  int32_t cycles;
+  int32_t cfg_tag;
+  uint64_t seed;
+  int64_t scen_base;
+  const uint16_t *demand;
+  const uint8_t *batch;
+  const uint8_t *status;
+  const uint32_t *ws_RT;
+  const uint64_t *ws_D;
+  uint16_t *dtab_rows;
+  uint64_t *fill_log;   // SIM_MAX_WARPS x DSTACK_MAX_FILL_RUNS
+  dstack_sim_out_t out;
+};
+
 struct IdealArgs {
   dstack_problem_t pb;
   dstack_params_t p;
@@ -78,6 +98,8 @@ int launch_wmaxmin(int32_t num_scen, const int32_t *off, int32_t L, const uint16
                    cudaStream_t s, int *launches);
 int launch_cycle(const CycArgs &a, cudaStream_t s, int *launches);
 int launch_ideal(IdealArgs a, void *ws, cudaStream_t s, int *launches);
+int launch_sim(const SimArgs &a, cudaStream_t s, int *launches);
+size_t sim_fill_log_bytes();
 int launch_agg(const AggArgs &a, cudaStream_t s, int *launches);
 size_t ideal_ws_bytes(int64_t num_rows);
 size_t agg_ws_bytes();

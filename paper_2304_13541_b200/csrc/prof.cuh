@@ -420,29 +420,37 @@ __device__ __forceinline__ void dtab_from_tables(const dstack_problem_t &pb, con
   __syncwarp();
 }
 
-// Same from the rows (any mode): one row pass per b.  RT, D given.
-__device__ __forceinline__ void dtab_from_rows(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k,
-                                               uint64_t RT, uint64_t D, int32_t g, int32_t b_lo, int32_t b_hi,
-                                               uint16_t *dtab, int lane) {
+// X(l, b) = E_t S M at S = S(l) from the rows (any mode), warp-cooperative; RT, D given.
+__device__ __forceinline__ uint64_t x_from_rows(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k,
+                                                uint64_t RT, uint64_t D, uint64_t S, int32_t b, int lane) {
   const int64_t r0 = pb.dnn_row_off[k];
   const int32_t K = (int32_t)(pb.dnn_row_off[k + 1] - r0);
   const uint64_t M = p.mem_mode == 0 ? 1ull : (uint64_t)pb.mem_bw[k];
   const uint64_t t_p = (uint64_t)pb.t_p[k], t_np = (uint64_t)pb.t_np[k];
-  const uint64_t S = (uint64_t)s_of(g, p.S_tot, p.L);
   const uint32_t *n = pb.n + r0;
   const uint16_t *r = pb.r + r0;
+  uint64_t V = 0;   // sum_i R_i max(S, N_i(b)) over N_i >= 1  (= S*A + U)
+  for (int i = lane; i < K; i += 32) {
+    const uint64_t nn = n[i];
+    const uint64_t N = p.par_mode == 0 ? (uint64_t)b * nn : ((uint64_t)b * nn + 2047) >> 11;
+    if (N >= 1) V += (uint64_t)r[i] * (N > S ? N : S);
+  }
+  V = warp_sum_u64(V);
+  uint64_t X = (p.wse_mode == 0 ? (uint64_t)b : 1ull) * t_np * RT * S * M + M * t_p * V;
+  if (p.mem_mode == 1) X += (uint64_t)b * D;
+  else if (p.mem_mode == 2) X += (uint64_t)b * D * S * S;
+  return X;
+}
+
+// d_j(b) at level g for b in [b_lo, b_hi] from the rows (any mode): one row pass per b.
+__device__ __forceinline__ void dtab_from_rows(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k,
+                                               uint64_t RT, uint64_t D, int32_t g, int32_t b_lo, int32_t b_hi,
+                                               uint16_t *dtab, int lane) {
+  const uint64_t M = p.mem_mode == 0 ? 1ull : (uint64_t)pb.mem_bw[k];
+  const uint64_t S = (uint64_t)s_of(g, p.S_tot, p.L);
   const uint64_t den = S * M * (uint64_t)p.slot_us;
   for (int32_t b = b_lo; b <= b_hi; ++b) {
-    uint64_t V = 0;   // sum_i R_i max(S, N_i(b)) over N_i >= 1  (= S*A + U)
-    for (int i = lane; i < K; i += 32) {
-      const uint64_t nn = n[i];
-      const uint64_t N = p.par_mode == 0 ? (uint64_t)b * nn : ((uint64_t)b * nn + 2047) >> 11;
-      if (N >= 1) V += (uint64_t)r[i] * (N > S ? N : S);
-    }
-    V = warp_sum_u64(V);
-    uint64_t X = (p.wse_mode == 0 ? (uint64_t)b : 1ull) * t_np * RT * S * M + M * t_p * V;
-    if (p.mem_mode == 1) X += (uint64_t)b * D;
-    else if (p.mem_mode == 2) X += (uint64_t)b * D * S * S;
+    const uint64_t X = x_from_rows(pb, p, k, RT, D, S, b, lane);
     if (lane == 0) dtab[b - 1] = ceil_div_clamp16(X, den);
   }
   __syncwarp();

@@ -59,6 +59,13 @@ class COut(C.Structure):
     _fields_ = [(k, C.c_void_p) for k in _OUT_FIELDS]
 
 
+_SIM_FIELDS = ("status", "T_us", "arrived", "in_slo", "late", "unserved", "occ_sum", "runs", "misses")
+
+
+class CSimOut(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in _SIM_FIELDS]
+
+
 class CHook(C.Structure):
     _fields_ = [("level", C.c_void_p), ("d_slots", C.c_void_p)]
 
@@ -78,6 +85,10 @@ def _load():
                                           P(COut), C.c_void_p, C.c_size_t, C.c_void_p]
     lib.dstack_eval_batch.argtypes = [P(CProblem), P(CParams), P(COut), C.c_void_p, C.c_size_t, C.c_void_p]
     lib.dstack_aggregate.argtypes = [P(CProblem), P(CParams), P(COut), C.c_void_p, C.c_size_t, C.c_void_p]
+    lib.dstack_sim_workspace_size.argtypes = [P(CProblem), P(CParams)]
+    lib.dstack_sim_workspace_size.restype = C.c_size_t
+    lib.dstack_simulate.argtypes = [P(CProblem), P(CParams), C.c_void_p, C.c_int32, C.c_uint64, C.c_int32, C.c_int64,
+                                    P(CSimOut), C.c_void_p, C.c_size_t, C.c_void_p]
     lib.dstack_profile_start.argtypes = [C.c_int32]
     lib.dstack_profile_stop.argtypes = [C.c_void_p, C.c_void_p]
     lib.dstack_status_str.restype = C.c_char_p
@@ -89,7 +100,8 @@ _lib = _load()
 
 # every symbol include/dstack.h declares (checked by tests/test_abi.py)
 EXPORTS = ("dstack_workspace_size", "dstack_knee", "dstack_batch_opt", "dstack_wmaxmin", "dstack_schedule_cycle",
-           "dstack_eval_batch", "dstack_aggregate", "dstack_profile_start", "dstack_profile_stop",
+           "dstack_eval_batch", "dstack_aggregate", "dstack_sim_workspace_size", "dstack_simulate",
+           "dstack_profile_start", "dstack_profile_stop",
            "dstack_last_launch_count", "dstack_status_str", "dstack_version")
 
 
@@ -127,6 +139,7 @@ class DeviceProblem:
     n: torch.Tensor              # int32 storage of u32 (+ >= 16 B slack)
     r: torch.Tensor              # int16 storage of u16
     d: torch.Tensor              # int32 storage of u32
+    lam_pct: torch.Tensor | None = None   # int32 [num_dnn], config-5 offered load (dstack_simulate only)
 
     @property
     def device(self):
@@ -158,7 +171,8 @@ def from_host(pb, device="cuda", pin=False) -> DeviceProblem:
     return DeviceProblem(int(pb.scen_dnn_off.shape[0] - 1), int(pb.dnn_row_off.shape[0] - 1), R,
                          t(pb.scen_dnn_off, np.int32), t(pb.dnn_row_off, np.int64), t(pb.t_p, np.int32),
                          t(pb.t_np, np.int32), t(pb.mem_bw, np.int32), t(pb.slo_us, np.int32), t(pb.asm_us, np.int32),
-                         t(pb.bmax, np.int32), t(pad(pb.n), np.int32), t(pad(pb.r), np.int16), t(pad(pb.d), np.int32))
+                         t(pb.bmax, np.int32), t(pad(pb.n), np.int32), t(pad(pb.r), np.int16), t(pad(pb.d), np.int32),
+                         None if getattr(pb, "lam_pct", None) is None else t(pb.lam_pct, np.int32))
 
 
 def from_device_dict(g: dict) -> DeviceProblem:
@@ -167,7 +181,7 @@ def from_device_dict(g: dict) -> DeviceProblem:
     D = g["dnn_row_off"].numel() - 1
     R = int(g["dnn_row_off"][-1].item())
     return DeviceProblem(S, D, R, g["scen_dnn_off"], g["dnn_row_off"], g["t_p"], g["t_np"], g["mem_bw"],
-                         g["slo_us"], g["asm_us"], g["bmax"], g["n"], g["r"], g["d"])
+                         g["slo_us"], g["asm_us"], g["bmax"], g["n"], g["r"], g["d"], g.get("lam_pct"))
 
 
 def cparams(p) -> CParams:
@@ -282,6 +296,20 @@ def profile_stop() -> tuple[dict, int]:
     calls = C.c_int32()
     _check(_lib.dstack_profile_stop(ms, C.byref(calls)), "dstack_profile_stop")
     return {k: ms[i] for i, k in enumerate(PROF_SLOTS)}, calls.value
+
+
+def simulate(dp: DeviceProblem, p, cycles: int, seed: int, cfg_tag: int, scen_base: int = 0):
+    """dstack_simulate (a7, config 5): per-scenario counters as device tensors (uint64 stored as int64)."""
+    dev = dp.device
+    S = max(dp.num_scen, 1)
+    o = dict(status=torch.zeros(S, dtype=torch.uint8, device=dev), T_us=torch.zeros(S, dtype=torch.int32, device=dev),
+             **{k: torch.zeros(S, dtype=torch.int64, device=dev) for k in _SIM_FIELDS[2:]})
+    wsz = int(_lib.dstack_sim_workspace_size(C.byref(dp.c()), C.byref(cparams(p))))
+    ws = Workspace(wsz, dev)
+    _check(_lib.dstack_simulate(C.byref(dp.c()), C.byref(cparams(p)), _ptr(dp.lam_pct), cycles, seed, cfg_tag,
+                                scen_base, C.byref(CSimOut(*[o[k].data_ptr() for k in _SIM_FIELDS])), ws.ptr(),
+                                ws.nbytes, _stream(dev)), "dstack_simulate")
+    return {k: v[: dp.num_scen] for k, v in o.items()}
 
 
 def last_launch_count() -> int:

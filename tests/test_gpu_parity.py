@@ -242,3 +242,24 @@ def test_split_path_parity(ds, variant):
     ds.schedule_cycle(dp, p, o["demand"], o["batch"], o["alloc_q16"], out=o, ws=ws)
     torch.cuda.synchronize()
     assert_parity(ds.to_numpy(o, pb.num_scen, pb.num_dnn), oracle.evaluate(pb, p), where=f"split-{variant}")
+
+
+def test_simulate_parity_and_shard_invariance(ds):
+    """a7 (config 5) through dstack_simulate vs the oracle's O7; two shards reproduce the single run."""
+    sp, p = synth.config(5, num_scen=160, rows_pct=30)
+    pb = synth.generate_host(sp)
+    cycles = 25
+    dp = ds.from_host(pb, "cuda")
+    g = ds.simulate(dp, p, cycles, sp.seed, sp.cfg_tag)
+    torch.cuda.synchronize()
+    want = oracle.simulate(pb, p, cycles, sp.seed, sp.cfg_tag)
+    for k in want:
+        a = g[k].cpu().numpy().astype(np.int64)
+        assert np.array_equal(a, want[k].astype(np.int64)), (k, np.flatnonzero(a != want[k].astype(np.int64))[:5])
+    assert want["arrived"].sum() > 0 and (want["in_slo"] > 0).any()
+    # shard [80, 160) drawn and simulated on its own (global scenario index via scen_base)
+    sh = synth.generate_host(sp.replace(scen_base=80, num_scen=80))
+    g2 = ds.simulate(ds.from_host(sh, "cuda"), p, cycles, sp.seed, sp.cfg_tag, scen_base=80)
+    torch.cuda.synchronize()
+    for k in want:
+        assert np.array_equal(g2[k].cpu().numpy().astype(np.int64), want[k][80:].astype(np.int64)), k
