@@ -263,3 +263,16 @@ def test_simulate_parity_and_shard_invariance(ds):
     torch.cuda.synchronize()
     for k in want:
         assert np.array_equal(g2[k].cpu().numpy().astype(np.int64), want[k][80:].astype(np.int64)), k
+
+
+def test_aggregate_matches_host_reference(ds):
+    """a8: the device aggregate (deterministic two-level reduction) equals the host reference computed
+    from the same per-DNN / per-scenario outputs (integers exact, f64 sums to 1e-12)."""
+    from tests.aggref import host_agg
+    sp, p = synth.config(2, num_scen=700, rows_pct=20)
+    pb = synth.generate_host(sp)
+    g, o = run_gpu(ds, pb, p)
+    want = host_agg(g)
+    got = o["agg"].cpu().numpy()
+    assert np.array_equal(got[5:], want[5:])
+    np.testing.assert_allclose(got[:5].view(np.float64), want[:5].view(np.float64), rtol=1e-12)
