@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-per-step", type=int, default=48, help="oracle scenarios per reference step")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="cpu_baseline time budget")
+    ap.add_argument("--cycles", type=int, default=20, help="config 5: sessions simulated per step")
     return ap.parse_args()
 
 
@@ -415,11 +416,66 @@ def run_e2e(args, sp, p, dev, world):
             "chunks": len(host_chunks), "api": "paper_2304_13541_b200.dstack.eval_batch (dstack_eval_batch)"}
 
 
+def run_sim(args, rank, world, local):
+    """Config 5 (a7): dstack_simulate over the shard; unit scenario-cycles/s."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2304_13541_b200 import dstack as ds
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    sp0, p = synth.config(5, num_scen=args.scen or None)
+    per_gpu = sp0.num_scen
+    sp = sp0.replace(scen_base=rank * per_gpu)
+    dp = ds.from_device_dict(synth.generate_device(sp, dev))
+    run = lambda: ds.simulate(dp, p, args.cycles, sp.seed, sp.cfg_tag, scen_base=sp.scen_base)
+    for _ in range(args.warmup):
+        run()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        o = run()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    tot = torch.stack([o[k].sum() for k in ("arrived", "in_slo", "late", "unserved", "occ_sum", "runs")]).to(torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    ms = float(t.item())
+    if rank == 0:
+        arrived, in_slo, late, unserved, occ, runs = tot.tolist()
+        nslots = (o["T_us"].to(torch.float64) / p.slot_us)
+        line = {"metric": "scenario-cycles/sec (config 5 long-horizon simulation, a7)",
+                "value": per_gpu * world * args.cycles * args.steps / (ms / 1e3), "unit": "scenario-cycles/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+                "data": "synthetic", "config": {"workload": f"config5: {per_gpu} scenarios/GPU x {args.cycles} cycles"},
+                "stats": {"arrived": arrived, "in_slo_frac": in_slo / max(arrived, 1),
+                          "late_frac": late / max(arrived, 1), "unserved_frac": unserved / max(arrived, 1),
+                          "mean_u_rank0": float((o["occ_sum"].to(torch.float64) /
+                                                 (nslots * p.L * args.cycles).clamp(min=1)).mean().item()),
+                          "runs": runs}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.config == 5:
+        return run_sim(args, rank, world, local)
     return run_native(args, rank, world, local)
 
 

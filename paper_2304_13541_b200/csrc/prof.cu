@@ -26,7 +26,21 @@ __global__ void __launch_bounds__(256, DSTACK_PROF_MINB) k_prof(ProfArgs a) {
   fill_stab(Stab, L, S_tot);
   __syncthreads();
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; k < a.pb.num_dnn; k += nwarps) {
+  const int64_t k_first = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  // software-pipelined L2 staging: while DNN k is analysed, the rows of this warp's next DNN are bulk-
+  // prefetched into L2 (offsets loaded one iteration ahead so the prefetch never waits on them)
+  int64_t pf0 = 0, pf1 = 0;
+  if (lane == 0 && k_first + nwarps < a.pb.num_dnn) { pf0 = a.pb.dnn_row_off[k_first + nwarps]; pf1 = a.pb.dnn_row_off[k_first + nwarps + 1]; }
+  for (int64_t k = k_first; k < a.pb.num_dnn; k += nwarps) {
+    if (lane == 0) {
+      if (pf1 > pf0) {
+        prefetch_l2(a.pb.n + pf0, (pf1 - pf0) * 4);
+        prefetch_l2(a.pb.r + pf0, (pf1 - pf0) * 2);
+        prefetch_l2(a.pb.d + pf0, (pf1 - pf0) * 4);
+      }
+      const int64_t kn = k + 2 * nwarps;
+      if (kn < a.pb.num_dnn) { pf0 = a.pb.dnn_row_off[kn]; pf1 = a.pb.dnn_row_off[kn + 1]; } else { pf0 = pf1 = 0; }
+    }
     const DnnRes r = analyze_dnn<PAR>(a.pb, a.p, k, Stab, hist, cA, cU, lane, a.knee_only, a.knee_b);
     if (a.dtab_rows && r.st == DSTACK_ST_OK) {   // eval path: d_j(b) at g = demand, b in [b_lo, b*]
       if (PAR == 0)
