@@ -5,6 +5,15 @@
 
 #include "dstack.h"
 
+#ifndef DSTACK_SMALL_CODE
+#define DSTACK_SMALL_CODE 0
+#endif
+#if DSTACK_SMALL_CODE
+#define DSTACK_UNROLL_SMALL _Pragma("unroll 1")
+#else
+#define DSTACK_UNROLL_SMALL _Pragma("unroll")
+#endif
+
 namespace dstack {
 
 typedef unsigned __int128 u128;
@@ -31,7 +40,7 @@ __device__ __forceinline__ uint64_t shfl_up_u64(uint64_t v, int d) {
   return ((uint64_t)hi << 32) | lo;
 }
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
-#pragma unroll
+  DSTACK_UNROLL_SMALL
   for (int m = 16; m; m >>= 1) v += shfl_xor_u64(v, m);
   return v;
 }
@@ -55,7 +64,7 @@ __device__ __forceinline__ uint64_t sat_add(uint64_t a, uint64_t b) {
   return (s < a || s >= (1ull << 63)) ? (1ull << 63) : s;
 }
 __device__ __forceinline__ uint64_t warp_sum_sat(uint64_t v) {
-#pragma unroll
+  DSTACK_UNROLL_SMALL
   for (int m = 16; m; m >>= 1) v = sat_add(v, shfl_xor_u64(v, m));
   return v;
 }

@@ -200,6 +200,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   int nsr = 0;                // first static window whose run starts after t (amortised, t only grows)
   const uint32_t sl_magic = sl <= 1 ? 0u : (uint32_t)(0xFFFFFFFFu / sl) + 1u;   // t / sl = umulhi(t, magic), t < 2^13
   const int nwords = (nslots + 31) >> 5;
+  const int gmin = (int)__reduce_min_sync(FULL, active ? g : 0xFFFFu);   // no model can start where occ > L - gmin
   int t = -1;
   while (true) {
     const int start = t + 1;
@@ -219,6 +220,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     if (nt < 0 || nt >= nslots) break;
     t = nt;
     int occ_t = sm.occ[t];
+    if (occ_t + gmin > L) continue;
     bool elig = false;
     int ns = nslots;
     if (active) {   // eligible: not running at t (static run of window t/sl or the last fill), fits at t
@@ -248,6 +250,27 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       const int dsj = (int)__shfl_sync(FULL, dstar, j);
       // slice k = first u in [t, limit) with occ[u] + g > L; only k >= d(b*) or its exact value below matters
       const int stop = t + dsj < limit ? t + dsj : limit;
+      if (stop - t == dsj && dsj <= 124) {
+        // common case, one pass: the whole run fits in one 128-slot chunk; test it and place b* at once
+        uint32_t *w32 = reinterpret_cast<uint32_t *>(sm.occ);
+        const int w = (t >> 2) + lane, base = w << 2;
+        const uint32_t m = base < stop ? bytes_mask(t, stop, base) : 0u;
+        const uint32_t word = m ? w32[w] : 0u;
+        const uint32_t bb = __vcmpgtu4(word, (uint32_t)(L - gj) * 0x01010101u) & m;
+        if (__ballot_sync(FULL, bb != 0) == 0) {
+          if (m) w32[w] = word + (((uint32_t)gj * 0x01010101u) & m);
+          occ_t += gj;
+          if (lane == 0) {
+            if (stop < nslots) sm.dmask[stop >> 5] |= 1u << (stop & 31);
+            if (fill_log && nfill < fill_cap) fill_log[nfill] = pack_run((uint32_t)j, (uint32_t)t, (uint32_t)dsj, (uint32_t)bsj);
+          }
+          nfill++;
+          __syncwarp();
+          if (lane == j) { count++; runs++; served += (uint32_t)bsj; fs = t; fe = stop; }
+          if (occ_t + (int)g > L) key = 0xFFFFFFFFu;
+          continue;
+        }
+      }
       const int kslice = first_above(sm.occ, t, stop, L - gj, lane) - t;
       int bsel = 0;   // largest b in [b_lo, b*] with d(b) <= slice (d nondecreasing in b)
       const uint16_t *dj = dtab + j * DSTACK_MAX_BATCH;

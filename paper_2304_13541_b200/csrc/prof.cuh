@@ -122,7 +122,7 @@ __device__ __forceinline__ void scan_hist(const uint32_t *hist, uint64_t *cA, ui
     if (m <= S_tot && m >= 1) { const uint64_t h = hist[m]; sa += h; sw += h * (uint64_t)m; }
   }
   uint64_t pa = sa, pw = sw;   // inclusive scan of lane totals
-#pragma unroll
+  DSTACK_UNROLL_SMALL
   for (int d = 1; d < 32; d <<= 1) {
     const uint64_t ua = shfl_up_u64(pa, d), uw = shfl_up_u64(pw, d);
     if (lane >= d) { pa += ua; pw += uw; }
