@@ -19,6 +19,13 @@ namespace dstack {
 
 constexpr uint16_t NONE16 = 0xFFFF;
 
+#ifndef DSTACK_CYC_GMIN
+#define DSTACK_CYC_GMIN 0
+#endif
+#ifndef DSTACK_CYC_ONEPASS
+#define DSTACK_CYC_ONEPASS 0
+#endif
+
 struct CycSmem {
   uint8_t occ[DSTACK_MAX_SLOTS];
   uint32_t dmask[DSTACK_MAX_SLOTS / 32];
@@ -220,7 +227,9 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     if (nt < 0 || nt >= nslots) break;
     t = nt;
     int occ_t = sm.occ[t];
+#if DSTACK_CYC_GMIN
     if (occ_t + gmin > L) continue;
+#endif
     bool elig = false;
     int ns = nslots;
     if (active) {   // eligible: not running at t (static run of window t/sl or the last fill), fits at t
@@ -250,7 +259,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       const int dsj = (int)__shfl_sync(FULL, dstar, j);
       // slice k = first u in [t, limit) with occ[u] + g > L; only k >= d(b*) or its exact value below matters
       const int stop = t + dsj < limit ? t + dsj : limit;
-      if (stop - t == dsj && dsj <= 124) {
+      if (DSTACK_CYC_ONEPASS && stop - t == dsj && dsj <= 124) {
         // common case, one pass: the whole run fits in one 128-slot chunk; test it and place b* at once
         uint32_t *w32 = reinterpret_cast<uint32_t *>(sm.occ);
         const int w = (t >> 2) + lane, base = w << 2;

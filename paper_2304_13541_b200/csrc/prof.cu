@@ -10,6 +10,9 @@ __host__ __device__ inline size_t prof_warp_bytes(int S_tot) {
 }
 
 template <int PAR>
+#ifndef DSTACK_PROF_PF
+#define DSTACK_PROF_PF 0   // L2 bulk prefetch of the next DNN's rows: measured slower (r01), off
+#endif
 #ifndef DSTACK_PROF_MINB
 #define DSTACK_PROF_MINB 4
 #endif
@@ -30,9 +33,9 @@ __global__ void __launch_bounds__(256, DSTACK_PROF_MINB) k_prof(ProfArgs a) {
   // software-pipelined L2 staging: while DNN k is analysed, the rows of this warp's next DNN are bulk-
   // prefetched into L2 (offsets loaded one iteration ahead so the prefetch never waits on them)
   int64_t pf0 = 0, pf1 = 0;
-  if (lane == 0 && k_first + nwarps < a.pb.num_dnn) { pf0 = a.pb.dnn_row_off[k_first + nwarps]; pf1 = a.pb.dnn_row_off[k_first + nwarps + 1]; }
+  if (DSTACK_PROF_PF && lane == 0 && k_first + nwarps < a.pb.num_dnn) { pf0 = a.pb.dnn_row_off[k_first + nwarps]; pf1 = a.pb.dnn_row_off[k_first + nwarps + 1]; }
   for (int64_t k = k_first; k < a.pb.num_dnn; k += nwarps) {
-    if (lane == 0) {
+    if (DSTACK_PROF_PF && lane == 0) {
       if (pf1 > pf0) {
         prefetch_l2(a.pb.n + pf0, (pf1 - pf0) * 4);
         prefetch_l2(a.pb.r + pf0, (pf1 - pf0) * 2);
