@@ -20,6 +20,18 @@
 
 namespace dstack {
 
+// Optional instrumentation build (-DDSTACK_PROF_STATS=1, never the default library): event counters of the
+// branch-and-bound, read back by dstack_debug_stats().
+#ifndef DSTACK_PROF_STATS
+#define DSTACK_PROF_STATS 0
+#endif
+#if DSTACK_PROF_STATS
+static __device__ unsigned long long g_pstats[16];   // per TU; k_prof's copy is prof.cu's
+#define PSTAT(i, v) atomicAdd(&g_pstats[i], (unsigned long long)(v))
+#else
+#define PSTAT(i, v) ((void)0)
+#endif
+
 struct Best {
   uint32_t found, l, b, S;
   uint64_t X;
@@ -34,6 +46,7 @@ __device__ __forceinline__ Best best_none() {
 // exact comparison of two candidates whose float scores are within the filter tolerance (rare)
 static __device__ __noinline__ bool better_exact(uint32_t cb, uint32_t cS, uint64_t cX, uint32_t cl, uint32_t ob, uint32_t oS,
                                           uint64_t oX, uint32_t ol) {
+  PSTAT(4, 1);
   const u128 L = (u128)(cb * cS) * ((u128)oX * oX);
   const u128 R = (u128)(ob * oS) * ((u128)cX * cX);
   if (L != R) return L > R;
@@ -67,6 +80,7 @@ __device__ __forceinline__ Best shfl_best(const Best &v, int src) {
 }
 
 static __device__ __noinline__ Best warp_best_exact(Best v) {
+  if ((threadIdx.x & 31) == 0) PSTAT(5, 1);
 #pragma unroll 1
   for (int m = 16; m; m >>= 1) {
     Best o = shfl_best(v, (threadIdx.x & 31) ^ m);
@@ -268,6 +282,7 @@ uint64_t bound_survivors(const uint64_t *cA, const uint64_t *cU, double thr, uin
     }
     if (__any_sync(FULL, ok)) out |= 1ull << (bb - 1);
   }
+  if (lane == 0) { PSTAT(2, __popcll(((uint64_t)cand_hi << 32) | cand_lo)); PSTAT(3, __popcll(out)); }
   return out;
 }
 
@@ -386,6 +401,7 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
       best = e; knee = kk.l;
     }
   }
+  if (lane == 0) { PSTAT(0, 1); PSTAT(1, b_hi > b_lo); PSTAT(6, best.b > b_lo); PSTAT(7, K); }
   const int32_t dm = (int32_t)best.l + p.margin;
   res.demand = (uint16_t)(dm < L ? dm : L);
   res.b = (uint8_t)best.b;
