@@ -79,241 +79,258 @@ static __device__ __noinline__ void prof_one_cold(const ProfArgs *a, int64_t k, 
   __syncwarp();
 }
 
-// cold: exact argmax of S / X^2 (ties -> smaller S) over the band members scr[S] != 0, S in [1, S_tot]
-static __device__ __noinline__ void band_exact(const uint64_t *scr, int S_tot, int lane, uint32_t *S_out,
-                                               uint64_t *X_out) {
+// cold: exact argmax of S / X^2 (ties -> smaller S) over the candidates S in [1, S_tot] whose float score
+// reaches `band` (X = scr[S]; candidate set: attained widths, and 2X <= S F when F != 0)
+struct SX {
+  uint64_t X;
+  uint32_t S;
+};
+static __device__ __noinline__ SX band_exact(const uint64_t *scr, const uint16_t *lmin, int S_tot, uint64_t F, float band,
+                                             int lane) {
   Best v = best_none();
   for (int S = 1 + lane; S <= S_tot; S += 32) {
     const uint64_t X = scr[S];
-    if (!X) continue;
-    Best c; c.found = 1; c.l = (uint32_t)S; c.b = 1; c.S = (uint32_t)S; c.X = X; c.sc = score_f((uint32_t)S, X);
+    const float f = score_f((uint32_t)S, X);
+    if (!lmin[S] || f < band || (F != 0 && 2 * X > (uint64_t)S * F)) continue;
+    Best c; c.found = 1; c.l = (uint32_t)S; c.b = 1; c.S = (uint32_t)S; c.X = X; c.sc = f;
     if (better(c, v)) v = c;
   }
   v = warp_best_exact(v);
-  *S_out = v.found ? v.S : 0u;
-  *X_out = v.X;
+  SX o;
+  o.S = v.found ? v.S : 0u;
+  o.X = v.X;
+  return o;
 }
 
-// Warp argmax over the register-resident candidates (bins S = m0 + i with bit i of `mask`): the float
-// maximum decides unless a second candidate lies within 2^-16 of it (float scores are within 2^-20 of the
-// exact ones, so the exact winner is always in that band); then the band is resolved exactly.
-template <int CB>
-__device__ __forceinline__ void fast_argmax(float vmax, uint32_t mask, const float (&sc)[CB], const uint64_t (&xs)[CB],
-                                            int m0, int S_tot, uint64_t *scr, int lane, uint32_t &Sw, uint64_t &Xw) {
-  const uint32_t mx = __reduce_max_sync(FULL, __float_as_uint(vmax));   // scores > 0: u32 order = float order
-  Sw = 0; Xw = 0;
-  if (mx == 0) return;
-  const float band = __uint_as_float(mx) * 0.9999847f;   // 1 - 2^-16
-  uint32_t cnt = 0, sel = 0;
-  uint64_t xsel = 0;
-#pragma unroll
-  for (int i = 0; i < CB; ++i)
-    if (((mask >> i) & 1u) && sc[i] >= band) { ++cnt; sel = (uint32_t)(m0 + i); xsel = xs[i]; }
+// Per-lane top-2 tracker of float scores (t1 >= t2; s1 = width of t1, first occurrence).
+struct Top2 {
+  float t1, t2;
+  uint32_t s1;
+};
+__device__ __forceinline__ void top2_add(Top2 &t, float f, uint32_t S) {
+  if (f > t.t1) { t.t2 = t.t1; t.t1 = f; t.s1 = S; }
+  else t.t2 = fmaxf(t.t2, f);
+}
+
+// Warp argmax from the per-lane top-2 trackers: the float maximum decides unless a second candidate lies
+// within 2^-19 of it (float scores are within 2^-21 of the exact ones, so the exact winner is always in
+// that band); then the band is resolved exactly from the X values staged in scr[S].  F != 0: the
+// feasible set (2X <= S F), else all attained widths.  One call site for both argmaxes (unroll 1).
+__device__ __forceinline__ SX fast_argmax(const Top2 &t, const uint64_t *scr, const uint16_t *lmin, int S_tot,
+                                          uint64_t F, int lane) {
+  SX o;
+  o.S = 0; o.X = 0;
+  const uint32_t mx = __reduce_max_sync(FULL, __float_as_uint(t.t1));   // scores > 0: u32 order = float order
+  if (mx == 0) return o;
+  const float band = __uint_as_float(mx) * 0.99999809f;   // 1 - 2^-19 (score_f error <= 6 * 2^-24)
+  const uint32_t cnt = (uint32_t)(t.t1 >= band) + (uint32_t)(t.t2 >= band);
   if (__reduce_add_sync(FULL, cnt) == 1) {
-    const int src = __ffs(__ballot_sync(FULL, cnt != 0)) - 1;
-    Sw = __shfl_sync(FULL, sel, src);
-    Xw = shfl_u64(xsel, src);
-    return;
+    o.S = __shfl_sync(FULL, t.s1, __ffs(__ballot_sync(FULL, cnt != 0)) - 1);
+    o.X = scr[o.S];
+    return o;
   }
   PSTAT(9, lane == 0);
-#pragma unroll
-  for (int i = 0; i < CB; ++i)
-    if (m0 + i <= S_tot) scr[m0 + i] = (((mask >> i) & 1u) && sc[i] >= band) ? xs[i] : 0ull;
-  __syncwarp();
-  band_exact(scr, S_tot, lane, &Sw, &Xw);
-  __syncwarp();
+  return band_exact(scr, lmin, S_tot, F, band, lane);
 }
 
+// Exact sum over the warp of per-lane values < 2^59 from three 32-bit reductions (22/22/15-bit limbs).
+// *top = the reduced top limb (the total is >= top * 2^44; the returned sum wraps only if top >= 2^20).
+__device__ __forceinline__ uint64_t warp_sum_limbs(uint64_t v, uint32_t *top) {
+  const uint32_t c0 = __reduce_add_sync(FULL, (uint32_t)v & 0x3FFFFFu);
+  const uint32_t c1 = __reduce_add_sync(FULL, (uint32_t)(v >> 22) & 0x3FFFFFu);
+  const uint32_t c2 = __reduce_add_sync(FULL, (uint32_t)(v >> 44));
+  *top = c2;
+  return (uint64_t)c0 + ((uint64_t)c1 << 22) + ((uint64_t)c2 << 44);
+}
+
+// min(ceil(X / den), 0xFFFF) for den >= 1: f32 quotient estimate (error < 0.05 below the clamp), exact fix-up
+__device__ __forceinline__ uint32_t ceil_div_clamp16_fast(uint64_t X, uint64_t den) {
+  const float qf = (float)X * rcp_approx((float)den);
+  if (qf > 65600.f) return 0xFFFFu;
+  uint64_t q = (uint64_t)qf;
+  if (q * den > X) --q;
+  else if ((q + 1) * den <= X) ++q;
+  q += (q * den < X);
+  return q > 0xFFFFu ? 0xFFFFu : (uint32_t)q;
+}
+
+// One DNN on the fast path.  Header values arrive warp-uniform (broadcast from the lane that loaded them).
+// Returns false when the DNN must be decided by the generic path (the caller runs prof_one_cold).
 template <int CB>
-__device__ __forceinline__ void fast_one(const ProfArgs &a, int64_t k, const uint16_t *Stab, const uint16_t *lmin,
-                                         uint32_t *hist, uint64_t *cA, uint64_t *cU, int lane) {
+__device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r0, int32_t K, uint32_t okb,
+                                         uint32_t M, uint32_t t_np, uint64_t Mtp, uint64_t F, uint32_t vmask,
+                                         const uint16_t *Stab, const uint16_t *lmin, uint32_t *hist, uint64_t *cA,
+                                         uint64_t *cU, int lane, uint32_t &st, uint32_t &RT, uint64_t &D,
+                                         uint32_t &knee, uint32_t &demand, uint32_t &dslots) {
   const dstack_problem_t &pb = a.pb;
   const dstack_params_t &p = a.p;
-  const int L = p.L, S_tot = p.S_tot;
-  const int64_t r0 = pb.dnn_row_off[k], K64 = pb.dnn_row_off[k + 1] - r0;
-  const int32_t t_p = pb.t_p[k], t_np = pb.t_np[k], slo = pb.slo_us[k], asm_us = pb.asm_us[k];
-  const int32_t bmax = pb.bmax[k], mbw = pb.mem_bw[k];
-  const int mem_mode = p.mem_mode;
-  const uint64_t M = mem_mode == 0 ? 1 : (uint64_t)mbw;
-  const int32_t b_hi = bmax < p.b_max ? bmax : p.b_max;   // b_lo = 1 on this path
-  uint8_t st = DSTACK_ST_OK;
-  uint32_t RT = 0, knee = 0, demand = 0, dslots = 0;
-  uint64_t D = 0;
-  do {
-    // ---- header validation (DSTACK_ST_INVALID conditions, dstack.h) ----
-    if (K64 < 1 || K64 > DSTACK_MAX_ROWS_PER_DNN || t_p < 1 || t_np < 0 || slo < 1 || slo > (1 << 30) ||
-        (slo % p.slot_us) != 0 || asm_us < 0 || asm_us > (1 << 24) || bmax < 1 ||
-        (mem_mode != 0 && (mbw < 1 || mbw > (1 << 24)))) {
-      st = DSTACK_ST_INVALID;
-      break;
+  const int L = p.L, S_tot = p.S_tot, mem_mode = p.mem_mode;
+  st = DSTACK_ST_OK; RT = 0; D = 0; knee = demand = dslots = 0;
+  if (!(okb & 1u)) { st = DSTACK_ST_INVALID; return true; }
+  const int32_t b_hi = (int32_t)(okb >> 8);
+  // ---- a1: one coalesced pass over the rows: RT, min R, D = sum R d, W> = sum_{n > S_tot} R n, and the
+  //      width histogram of R over n <= S_tot (smem) ----
+  const uint32_t *n = pb.n + r0;
+  const uint16_t *r = pb.r + r0;
+  const uint32_t *d = pb.d + r0;
+  uint32_t Rmin = 0xFFFFFFFFu;
+  uint64_t Wb = 0;
+  for (int i0 = lane; i0 < K; i0 += 64) {
+    const int i1 = i0 + 32;
+    const bool h1 = i1 < K;
+    const uint32_t n0 = __ldg(n + i0), d0 = __ldg(d + i0), R0 = __ldg(r + i0);
+    uint32_t n1 = 0, d1 = 0, R1 = 0;
+    if (h1) { n1 = __ldg(n + i1); d1 = __ldg(d + i1); R1 = __ldg(r + i1); }
+    RT += R0; D += (uint64_t)R0 * d0; Rmin = min(Rmin, R0);
+    if (n0 <= (uint32_t)S_tot) atomicAdd(&hist[n0], R0); else Wb += (uint64_t)R0 * n0;
+    if (h1) {
+      RT += R1; D += (uint64_t)R1 * d1; Rmin = min(Rmin, R1);
+      if (n1 <= (uint32_t)S_tot) atomicAdd(&hist[n1], R1); else Wb += (uint64_t)R1 * n1;
     }
-    // ---- a1: one coalesced pass over the rows: RT, D, W = sum R n, width histogram (smem) ----
-    const int32_t K = (int32_t)K64;
-    const uint32_t *n = pb.n + r0;
-    const uint16_t *r = pb.r + r0;
-    const uint32_t *d = pb.d + r0;
-    uint32_t anyR0 = 0;
-    uint64_t Wn = 0;
-    for (int i0 = lane; i0 < K; i0 += 64) {
-      const int i1 = i0 + 32;
-      const bool h1 = i1 < K;
-      const uint32_t n0 = __ldg(n + i0), d0 = __ldg(d + i0), R0 = __ldg(r + i0);
-      uint32_t n1 = 0, d1 = 0, R1 = 0;
-      if (h1) { n1 = __ldg(n + i1); d1 = __ldg(d + i1); R1 = __ldg(r + i1); }
-      RT += R0; D += (uint64_t)R0 * d0; Wn += (uint64_t)R0 * n0; anyR0 |= (R0 == 0);
-      if (n0 <= (uint32_t)S_tot) atomicAdd(&hist[n0], R0);
-      if (h1) {
-        RT += R1; D += (uint64_t)R1 * d1; Wn += (uint64_t)R1 * n1; anyR0 |= (R1 == 0);
-        if (n1 <= (uint32_t)S_tot) atomicAdd(&hist[n1], R1);
-      }
-    }
-    RT = __reduce_add_sync(FULL, RT);
-    D = warp_sum_u64(D);
-    Wn = warp_sum_u64(Wn);
-    anyR0 = __reduce_or_sync(FULL, anyR0);
-    __syncwarp();
-    // ---- scan of the histogram into registers: lane owns widths m0..m0+CB-1; re-zero the histogram ----
-    //   pa[i] = PA[m] = sum_{1<=n<=m} R,   pw[i] = sum_{n<=m} n R   (Q[m] = W - pw[i])
-    const int m0 = lane * CB;
-    uint32_t pa[CB];
-    uint64_t pw[CB];
-    {
-      uint32_t h[CB], sa = 0;
-      uint64_t sw = 0;
-#pragma unroll
-      for (int i = 0; i < CB; ++i) {
-        const int m = m0 + i;
-        h[i] = 0;
-        if (m <= S_tot) { h[i] = hist[m]; hist[m] = 0; }
-        if (m == 0) h[i] = 0;   // n = 0 rows: in neither PA nor sum n R
-        sa += h[i]; sw += (uint64_t)h[i] * (uint32_t)m;
-      }
-      uint32_t ia = sa;
-      uint64_t iw = sw;
-#pragma unroll
-      for (int dd = 1; dd < 32; dd <<= 1) {
-        const uint32_t ua = __shfl_up_sync(FULL, ia, dd);
-        const uint64_t uw = shfl_up_u64(iw, dd);
-        if (lane >= dd) { ia += ua; iw += uw; }
-      }
-      uint32_t ra = ia - sa;
-      uint64_t rw = iw - sw;
-#pragma unroll
-      for (int i = 0; i < CB; ++i) {
-        ra += h[i]; rw += (uint64_t)h[i] * (uint32_t)(m0 + i);
-        pa[i] = ra; pw[i] = rw;
-      }
-    }
-    __syncwarp();
-    if (anyR0 || (t_np == 0 && Wn == 0 && (mem_mode == 0 || D == 0))) { st = DSTACK_ST_INVALID; break; }
-    if (b_hi < 1) { st = DSTACK_ST_INFEASIBLE; break; }
-    // ---- overflow: X(L, b_hi) = b_hi t_np RT S_tot M + M t_p (S_tot PA[mb] + b_hi Q[mb]) + mem < 2^56 ----
-    {
-      const int mb = S_tot / b_hi;
-      uint32_t pam = 0;
-      uint64_t pwm = 0;
-#pragma unroll
-      for (int i = 0; i < CB; ++i)
-        if (m0 + i == mb) { pam = pa[i]; pwm = pw[i]; }
-      pam = __shfl_sync(FULL, pam, mb / CB);
-      pwm = shfl_u64(pwm, mb / CB);
-      const u128 v = (u128)S_tot * pam + (u128)b_hi * (Wn - pwm);
-      const uint64_t Vmax = v >= ((u128)1 << 63) ? (1ull << 63) : (uint64_t)v;
-      double xe = (double)b_hi * (double)t_np * (double)RT * (double)S_tot * (double)M +
-                  (double)M * (double)t_p * (double)Vmax;
-      if (mem_mode == 1) xe += (double)b_hi * (double)D;
-      else if (mem_mode == 2) xe += (double)b_hi * (double)D * (double)(S_tot * S_tot);
-      bool over;
-      if (Vmax >= (1ull << 63) || xe >= 72057594037927936.0 * 1.0001) over = true;
-      else if (xe < 72057594037927936.0 * 0.9999) over = false;
-      else over = xub_exact_over((uint32_t)b_hi, (uint64_t)t_np, (uint64_t)RT, (uint32_t)S_tot, M, (uint64_t)t_p, Vmax,
-                                 mem_mode, (uint32_t)b_hi, D);
-      if (over) { st = DSTACK_ST_OVERFLOW; break; }
-    }
-    // ---- a2/a3 at b = 1: X(S, 1) = S (C1 + Mtp PA[S]) + Mtp Q[S] + mem for every attained S; in the same
-    //      pass the batch certificate G (below) over the segments m <= S_tot/2 ----
-    const uint64_t Mtp = M * (uint64_t)t_p, C1 = (uint64_t)t_np * RT * M;
-    const uint64_t SLOM = (uint64_t)slo * M, aM = (uint64_t)asm_us * M;
-    const uint64_t memb = mem_mode == 1 ? D : 0ull;
-    const float half = 0.5f * (float)S_tot;
-    const int mh = S_tot >> 1;
-    uint64_t xs[CB];
-    float sc[CB];
-    uint32_t va = 0, fe = 0;
-    float kmax = 0.f, emax = 0.f, G = 0.f;
+  }
+  RT = __reduce_add_sync(FULL, RT);
+  Rmin = __reduce_min_sync(FULL, Rmin);
+  uint32_t Dtop, Wtop;
+  D = warp_sum_limbs(D, &Dtop);
+  Wb = warp_sum_limbs(Wb, &Wtop);
+  __syncwarp();
+  // ---- scan of the histogram (lane owns widths m0..m0+CB-1, re-zeroing them): exclusive lane offsets;
+  //      the per-width prefixes PA[m] = sum_{1<=n<=m} R, PW[m] = sum_{n<=m} n R (u32: RT < 2^24 here) are
+  //      formed in the candidate pass below ----
+  const int m0 = lane * CB;
+  uint32_t h[CB], ra, rw, Wsm;
+  {
+    uint32_t sa = 0, sw = 0;
 #pragma unroll
     for (int i = 0; i < CB; ++i) {
-      const int S = m0 + i;
-      const uint64_t cAi = Mtp * pa[i], cUi = Mtp * (Wn - pw[i]);
-      uint64_t X = (uint64_t)S * (C1 + cAi) + cUi;
-      if (mem_mode == 1) X += D;
-      else if (mem_mode == 2) X += D * (uint64_t)(S * S);
-      xs[i] = X;
-      const float f = score_f((uint32_t)S, X);
-      sc[i] = f;
-      const bool valid = S >= 1 && S <= S_tot && lmin[S <= S_tot ? S : 0] != 0;
-      const uint64_t cap = (uint64_t)S * SLOM;
-      const bool feas = valid && X + (uint64_t)S * aM <= cap && 2 * X <= cap;   // Eq. 11, Eq. 12
-      if (valid) { va |= 1u << i; kmax = fmaxf(kmax, f); }
-      if (feas) { fe |= 1u << i; emax = fmaxf(emax, f); }
-      // Batch certificate: for b >= 2 and s = S/b in segment m = floor(s),
-      // X(S, b) >= b (alpha s + beta), alpha = 2 C1 + Mtp PA[m], beta = Mtp Q[m] + mem, hence
-      // eta(S, b) <= s / (alpha s + beta)^2; G = max over m <= S_tot/2 of its supremum on [m, m+1).
-      if (S <= mh) {
-        const float af = (float)(2 * C1 + cAi), bf = (float)(cUi + memb);
-        const float lo = (float)S, hi = fminf((float)(S + 1), half);
-        float v;
-        if (bf == 0.f) v = __int_as_float(0x7f800000);          // s/(alpha s)^2 is unbounded at s -> 0
-        else if (bf <= af * lo) { const float x = af * lo + bf; v = lo * rcp_approx(x * x); }
-        else if (bf >= af * hi) { const float x = af * hi + bf; v = hi * rcp_approx(x * x); }
-        else v = rcp_approx(4.f * af * bf);                     // interior peak at s = beta / alpha
-        G = fmaxf(G, v);
-      }
+      const int m = m0 + i;
+      h[i] = 0;
+      if (m <= S_tot) { h[i] = hist[m]; hist[m] = 0; }
+      if (m == 0) h[i] = 0;   // n = 0 rows: in neither PA nor sum n R
+      sa += h[i]; sw += h[i] * (uint32_t)m;
     }
-    uint32_t Sk, Se;
-    uint64_t Xk, Xe;
-    fast_argmax<CB>(kmax, va, sc, xs, m0, S_tot, cA, lane, Sk, Xk);
-    fast_argmax<CB>(emax, fe, sc, xs, m0, S_tot, cA, lane, Se, Xe);
-    if (Se == 0) { st = DSTACK_ST_INFEASIBLE; break; }   // b = 1 is feasible whenever any b is (O3)
-    // b* = 1 is certified when the incumbent beats G with a 2^-12 margin (f32 rounding of both sides is
-    // < 2^-19); otherwise the generic exact branch-and-bound decides this DNN.
-    if (b_hi >= 2) {
-      const float Gw = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(G)));
-      if (!(score_f(Se, Xe) * 0.99975586f > Gw)) { prof_one_cold(&a, k, Stab, hist, cA, cU, lane); return; }
-    }
-    knee = lmin[Sk];
-    const uint32_t le = lmin[Se];
-    demand = le + (uint32_t)p.margin < (uint32_t)L ? le + (uint32_t)p.margin : (uint32_t)L;
-    // d_j(1) = ceil(X(S(g), 1) / (S(g) M Delta)) at g = demand
-    if (a.dtab_rows) {
-      const uint32_t Sg = Stab[demand];
-      uint64_t Xg = Xe;
-      if (Sg != Se) {
-        uint64_t xo = 0;
+    uint32_t ia = sa, iw = sw;
 #pragma unroll
-        for (int i = 0; i < CB; ++i)
-          if ((uint32_t)(m0 + i) == Sg) xo = xs[i];
-        Xg = shfl_u64(xo, Sg / CB);
-      }
-      dslots = ceil_div_clamp16(Xg, (uint64_t)Sg * M * (uint64_t)p.slot_us);
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      const uint32_t ua = __shfl_up_sync(FULL, ia, dd), uw = __shfl_up_sync(FULL, iw, dd);
+      if (lane >= dd) { ia += ua; iw += uw; }
     }
-  } while (0);
-  if (lane == 0) {
-    const bool ok = st == DSTACK_ST_OK;
-    if (a.ws_RT) { a.ws_RT[k] = RT; a.ws_D[k] = D; }
-    if (a.dtab_rows && ok) a.dtab_rows[k * DTAB_ROW] = (uint16_t)dslots;
-    if (a.knee) a.knee[k] = ok ? (uint16_t)knee : 0;
-    if (a.status) a.status[k] = st;
-    if (a.demand) a.demand[k] = ok ? (uint16_t)demand : 0;
-    if (a.batch) a.batch[k] = ok ? 1 : 0;
+    Wsm = __shfl_sync(FULL, iw, 31);
+    ra = ia - sa; rw = iw - sw;
+  }
+  // ---- status (same order as the generic path) ----
+  if (Rmin == 0 || (t_np == 0 && Wb == 0 && Wtop == 0 && Wsm == 0 && (mem_mode == 0 || (D == 0 && Dtop == 0)))) {
+    st = DSTACK_ST_INVALID;
+    return true;
+  }
+  if (b_hi < 1) { st = DSTACK_ST_INFEASIBLE; return true; }
+  if (RT >= (1u << 24) || Wtop >= (1u << 19) || Dtop >= (1u << 19)) {   // outside the u32 / u64 fast ranges
+    return false;
+  }
+  // ---- a2/a3 at b = 1: X(S, 1) = S C1 + Mtp (S PA[S] + Q[S]) + mem for every attained S (exact u64 once the
+  //      overflow test below passes; staged in scr[S] for the argmax), per-lane top-2 trackers of the
+  //      scores, and the batch certificate G over the segments m <= S_tot/2 ----
+  const uint64_t C1 = (uint64_t)t_np * M * RT;
+  const uint64_t memb = mem_mode == 1 ? D : 0ull;
+  const uint64_t base = Mtp * Wb + memb;
+  const float C1f2 = 2.f * (float)C1, Mtpf = (float)Mtp, Wbf = (float)Wb, membf = (float)memb;
+  const float half = 0.5f * (float)S_tot;
+  const int mh = S_tot >> 1, mb = S_tot / b_hi;
+  uint64_t *scr = cA;
+  Top2 tk = {0.f, 0.f, 0u}, te = {0.f, 0.f, 0u};
+  float G = 0.f;
+  uint32_t pam = 0, pwm = 0;
+#pragma unroll
+  for (int i = 0; i < CB; ++i) {
+    const uint32_t S = (uint32_t)(m0 + i);
+    ra += h[i]; rw += h[i] * S;                          // PA[S], PW[S]
+    if ((int)S == mb) { pam = ra; pwm = rw; }
+    const uint32_t q = Wsm - rw;                         // Q[S] - W>
+    uint64_t X = (uint64_t)S * C1 + Mtp * ((uint64_t)S * ra + q) + base;
+    if (mem_mode == 2) X += D * (uint64_t)(S * S);
+    if ((int)S <= S_tot) scr[S] = X;
+    const float f = score_f(S, X);
+    if ((vmask >> i) & 1u) {
+      top2_add(tk, f, S);
+      if (2 * X <= (uint64_t)S * F) top2_add(te, f, S);   // Eqs. 11-12
+    }
+    // Batch certificate: for b >= 2 and s = S/b in segment m = floor(s),
+    // X(S, b) >= b (alpha s + beta), alpha = 2 C1 + Mtp PA[m], beta = Mtp Q[m] + mem, hence
+    // eta(S, b) <= s / (alpha s + beta)^2; G = max over m <= S_tot/2 of its supremum on [m, m+1).
+    if ((int)S <= mh) {
+      const float af = fmaf(Mtpf, (float)ra, C1f2), bf = fmaf(Mtpf, (float)q + Wbf, membf);
+      const float lo = (float)S, hi = fminf(lo + 1.f, half);
+      float v;
+      if (bf == 0.f) v = __int_as_float(0x7f800000);          // s/(alpha s)^2 is unbounded at s -> 0
+      else if (bf <= af * lo) { const float x = fmaf(af, lo, bf); v = lo * rcp_approx(x * x); }
+      else if (bf >= af * hi) { const float x = fmaf(af, hi, bf); v = hi * rcp_approx(x * x); }
+      else v = rcp_approx(4.f * af * bf);                     // interior peak at s = beta / alpha
+      G = fmaxf(G, v);
+    }
+  }
+  {
+    // overflow: X(L, b_hi) = b_hi t_np RT S_tot M + M t_p (S_tot PA[mb] + b_hi Q[mb]) + mem is the grid
+    // maximum (f64; within 1e-4 of 2^56 the generic path decides exactly)
+    pam = __shfl_sync(FULL, pam, mb / CB);
+    pwm = __shfl_sync(FULL, pwm, mb / CB);
+    const double bd = (double)b_hi, Sd = (double)S_tot;
+    double xe = bd * (double)t_np * (double)M * (double)RT * Sd +
+                (double)Mtp * (Sd * (double)pam + bd * ((double)Wb + (double)(Wsm - pwm)));
+    if (mem_mode == 1) xe += bd * (double)D;
+    else if (mem_mode == 2) xe += bd * (double)D * Sd * Sd;
+    if (xe >= 72057594037927936.0 * 1.0001) { st = DSTACK_ST_OVERFLOW; return true; }
+    if (xe >= 72057594037927936.0 * 0.9999) return false;
   }
   __syncwarp();
+  uint32_t Sk = 0, Se = 0;
+  uint64_t Xe = 0;
+#pragma unroll 1
+  for (int w = 0; w < 2; ++w) {   // w = 0: knee (all attained widths), w = 1: feasible argmax
+    Top2 t;
+    t.t1 = w ? te.t1 : tk.t1; t.t2 = w ? te.t2 : tk.t2; t.s1 = w ? te.s1 : tk.s1;
+    const SX r = fast_argmax(t, scr, lmin, S_tot, w ? (F == 0 ? 1ull : F) : 0ull, lane);
+    if (w) { Se = r.S; Xe = r.X; } else Sk = r.S;
+  }
+  if (Se == 0) { st = DSTACK_ST_INFEASIBLE; return true; }   // b = 1 is feasible whenever any b is (O3)
+  // b* = 1 is certified when the incumbent beats G with a 2^-12 margin (f32 rounding of both sides is
+  // < 2^-19); otherwise the generic exact branch-and-bound decides this DNN.
+  if (b_hi >= 2) {
+    const float Gw = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(G)));
+    if (!(score_f(Se, Xe) * 0.99975586f > Gw)) return false;
+  }
+  knee = lmin[Sk];
+  const uint32_t le = lmin[Se];
+  demand = le + (uint32_t)p.margin < (uint32_t)L ? le + (uint32_t)p.margin : (uint32_t)L;
+  // d_j(1) = ceil(X(S(g), 1) / (S(g) M Delta)) at g = demand
+  if (a.dtab_rows) {
+    const uint32_t Sg = Stab[demand];
+    dslots = ceil_div_clamp16_fast(Sg == Se ? Xe : scr[Sg], (uint64_t)Sg * M * (uint64_t)p.slot_us);
+  }
+  return true;
 }
 
+// per-warp staging of 32 DNN headers / results in shared memory (keeps them out of the register file)
+struct __align__(16) FastHdr {
+  int64_t r0;
+  uint64_t Mtp, F;
+  int32_t K;
+  uint32_t okb, M, tnp;
+};
+struct __align__(8) FastOut {
+  uint64_t D;
+  uint32_t RT, kd, sd, pad;   // kd: knee | demand << 16; sd: d_j(1) | status << 16 | cold << 24
+};
+constexpr size_t FAST_STAGE_BYTES = 32 * (sizeof(FastHdr) + sizeof(FastOut));
+
+// Fast-path kernel: each warp owns a contiguous range of DNNs and walks it 32 at a time; lane j loads and
+// validates DNN kb+j's header (coalesced, one pass per 32 DNNs) and buffers its outputs, which are
+// written back coalesced after the 32 analyses.
 template <int CB>
 __global__ void __launch_bounds__(256, DSTACK_PROF_MINB) k_prof_fast(const __grid_constant__ ProfArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int L = a.p.L, S_tot = a.p.S_tot;
+  const dstack_problem_t &pb = a.pb;
+  const dstack_params_t &p = a.p;
+  const int L = p.L, S_tot = p.S_tot;
   uint16_t *Stab = (uint16_t *)smem;
   uint16_t *lmin = Stab + (L + 1);
   const int tab_bytes = ((L + 1 + S_tot + 1) * 2 + 15) & ~15;
@@ -322,6 +339,9 @@ __global__ void __launch_bounds__(256, DSTACK_PROF_MINB) k_prof_fast(const __gri
   uint64_t *cA = (uint64_t *)wreg;
   uint64_t *cU = cA + (S_tot + 1);
   uint32_t *hist = (uint32_t *)(cU + (S_tot + 1));
+  FastHdr *shdr = reinterpret_cast<FastHdr *>(smem + tab_bytes + (size_t)(blockDim.x >> 5) * prof_warp_bytes(S_tot) +
+                                              (size_t)warp * FAST_STAGE_BYTES);
+  FastOut *sout = reinterpret_cast<FastOut *>(shdr + 32);
   fill_stab(Stab, L, S_tot);
   // lmin[S] = smallest level l with S(l) = S (0: S not attained); ties between levels -> smaller l
   for (int S = threadIdx.x; S <= S_tot; S += blockDim.x) {
@@ -330,13 +350,77 @@ __global__ void __launch_bounds__(256, DSTACK_PROF_MINB) k_prof_fast(const __gri
   }
   for (int m = lane; m <= S_tot; m += 32) hist[m] = 0;
   __syncthreads();
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; k < a.pb.num_dnn; k += nwarps)
-    fast_one<CB>(a, k, Stab, lmin, hist, cA, cU, lane);
+  uint32_t vmask = 0;   // bit i: width S = lane*CB + i is attained by some level
+#pragma unroll
+  for (int i = 0; i < CB; ++i) {
+    const int S = lane * CB + i;
+    if (S >= 1 && S <= S_tot && lmin[S]) vmask |= 1u << i;
+  }
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t per = (pb.num_dnn + nw - 1) / nw;
+  const int64_t kbeg = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * per;
+  const int64_t kend = kbeg + per < pb.num_dnn ? kbeg + per : pb.num_dnn;
+  for (int64_t kb = kbeg; kb < kend; kb += 32) {
+    const int nj = kend - kb < 32 ? (int)(kend - kb) : 32;
+    const int64_t kl = kb + lane;
+    const bool have = lane < nj;
+    // ---- lane-parallel header: load + validate (DSTACK_ST_INVALID conditions, dstack.h) ----
+    if (have) {
+      FastHdr h;
+      h.r0 = pb.dnn_row_off[kl];
+      const int64_t K64 = pb.dnn_row_off[kl + 1] - h.r0;
+      const int32_t t_p = pb.t_p[kl], t_np = pb.t_np[kl], slo = pb.slo_us[kl], asm_us = pb.asm_us[kl];
+      const int32_t bmax = pb.bmax[kl], mbw = pb.mem_bw[kl];
+      const bool ok = !(K64 < 1 || K64 > DSTACK_MAX_ROWS_PER_DNN || t_p < 1 || t_np < 0 || slo < 1 ||
+                        slo > (1 << 30) || (slo % p.slot_us) != 0 || asm_us < 0 || asm_us > (1 << 24) || bmax < 1 ||
+                        (p.mem_mode != 0 && (mbw < 1 || mbw > (1 << 24))));
+      h.K = ok ? (int32_t)K64 : 0;
+      h.M = p.mem_mode == 0 ? 1u : (uint32_t)mbw;
+      h.tnp = (uint32_t)t_np;
+      h.Mtp = (uint64_t)h.M * (uint32_t)t_p;
+      // Eqs. 11-12 at b = 1 as one test 2X <= S F:  F = min(2 (SLO - a) M, SLO M)  (0 if a > SLO)
+      const uint64_t SLOM = (uint64_t)slo * h.M, aM = (uint64_t)asm_us * h.M;
+      h.F = SLOM < aM ? 0ull : (2 * (SLOM - aM) < SLOM ? 2 * (SLOM - aM) : SLOM);
+      const int32_t b_hi = bmax < p.b_max ? bmax : p.b_max;
+      h.okb = ok ? (1u | ((uint32_t)b_hi << 8)) : 0u;
+      shdr[lane] = h;
+    }
+    __syncwarp();
+    for (int jj = 0; jj < nj; ++jj) {
+      const FastHdr h = shdr[jj];
+      uint32_t st, RT, knee, dem, ds;
+      uint64_t D;
+      const bool done = fast_dnn<CB>(a, kb + jj, h.r0, h.K, h.okb, h.M, h.tnp, h.Mtp, h.F, vmask, Stab, lmin, hist, cA,
+                                     cU, lane, st, RT, D, knee, dem, ds);
+      if (!done) prof_one_cold(&a, kb + jj, Stab, hist, cA, cU, lane);
+      if (lane == 0) {
+        FastOut o;
+        o.D = D; o.RT = RT; o.kd = knee | (dem << 16); o.sd = ds | (st << 16) | (done ? 0u : (1u << 24)); o.pad = 0;
+        sout[jj] = o;
+      }
+    }
+    __syncwarp();
+    // ---- coalesced write-back of the 32 DNNs' outputs ----
+    if (have) {
+      const FastOut o = sout[lane];
+      if (!(o.sd >> 24)) {
+        const uint32_t st = (o.sd >> 16) & 0xFFu;
+        const bool ok = st == DSTACK_ST_OK;
+        if (a.ws_RT) { a.ws_RT[kl] = o.RT; a.ws_D[kl] = o.D; }
+        if (a.dtab_rows && ok) a.dtab_rows[kl * DTAB_ROW] = (uint16_t)(o.sd & 0xFFFFu);
+        if (a.knee) a.knee[kl] = ok ? (uint16_t)(o.kd & 0xFFFFu) : 0;
+        if (a.status) a.status[kl] = (uint8_t)st;
+        if (a.demand) a.demand[kl] = ok ? (uint16_t)(o.kd >> 16) : 0;
+        if (a.batch) a.batch[kl] = ok ? 1 : 0;
+      }
+    }
+    __syncwarp();
+  }
 }
 
 size_t prof_smem_bytes(const dstack_params_t *p, int warps) {
-  return (size_t)(((p->L + 1 + p->S_tot + 1) * 2 + 15) & ~15) + (size_t)warps * prof_warp_bytes(p->S_tot);
+  return (size_t)(((p->L + 1 + p->S_tot + 1) * 2 + 15) & ~15) + (size_t)warps * prof_warp_bytes(p->S_tot) +
+         (size_t)warps * FAST_STAGE_BYTES;
 }
 
 template <typename KernelT>
