@@ -276,3 +276,44 @@ def test_aggregate_matches_host_reference(ds):
     got = o["agg"].cpu().numpy()
     assert np.array_equal(got[5:], want[5:])
     np.testing.assert_allclose(got[:5].view(np.float64), want[:5].view(np.float64), rtol=1e-12)
+
+
+def fast_path_problem(S_tot):
+    """DNNs that drive every branch of k_prof_fast (prof.cu): certificate failure (t_np = 0, so the b >= 2
+    bound has no gap), RT >= 2^24 (u32 prefix range exceeded), X(L, b_hi) within 1e-4 of 2^56 on either
+    side, b_hi = 1 (no certificate), an SLO below every latency (INFEASIBLE), n = 0 rows, and ordinary
+    DNNs, all under the default (linear, per_request, b_min = 1) model."""
+    from tests.helpers import multi_dnn_problem
+    base = dict(rows=[(10, 1, 1000), (3, 2, 500), (0, 1, 0), (200, 1, 5000)], t_p=20, t_np=5, M=50000, slo=20000,
+                a=300, bmax=64)
+    dnns = [base,
+            dict(base, t_np=0),                                                  # certificate fails
+            dict(base, rows=[(3, 65535, 7)] * 260 + [(90, 1, 0)], t_p=1, t_np=1, M=1, slo=10**9),   # RT > 2^24
+            # X(L, 1) = M t_p S_tot just below 2^56 (OK) and just above (OVERFLOW), both within 1e-4 of it
+            dict(base, rows=[(1, 1, 0)], t_p=(2**32 - 1) // S_tot, t_np=0, M=2**24, bmax=1, slo=10**9),
+            dict(base, rows=[(1, 1, 0)], t_p=(2**32 - 1) // S_tot + 1, t_np=0, M=2**24, bmax=1, slo=10**9),
+            dict(base, bmax=1),
+            dict(base, slo=100, a=5000),                                          # INFEASIBLE
+            dict(base, rows=[(0, 2, 10), (7, 1, 0)]),
+            dict(base, rows=[(i % 40 + 1, 1 + i % 3, 100 * i) for i in range(150)], t_p=7, t_np=3)]
+    return multi_dnn_problem(dnns, [3, 3, 3])
+
+
+@pytest.mark.parametrize("L,S_tot", [(148, 148), (100, 80), (100, 148), (200, 200), (255, 256)])
+def test_fast_path_branches_parity(ds, L, S_tot):
+    pb = fast_path_problem(S_tot)
+    p = Params(L=L, S_tot=S_tot, mem_mode=1)
+    g, _ = run_gpu(ds, pb, p)
+    want = oracle.evaluate(pb, p)
+    assert_parity(g, want, where=f"fast L={L} S_tot={S_tot}")
+    assert oracle.OVERFLOW in want["status"].tolist() and oracle.INFEASIBLE in want["status"].tolist()
+
+
+@pytest.mark.parametrize("S_tot", [200, 256])
+def test_wide_smcount_parity(ds, S_tot):
+    """S_tot > 159 takes the 9-widths-per-lane fast kernel (k_prof_fast<9>)."""
+    sp, p = synth.config(2, num_scen=60, rows_pct=15)
+    pb = synth.generate_host(sp)
+    p = p.replace(L=min(255, S_tot), S_tot=S_tot, ideal=0)
+    g, _ = run_gpu(ds, pb, p)
+    assert_parity(g, oracle.evaluate(pb, p), ideal=False, where=f"S_tot={S_tot}")
