@@ -24,7 +24,10 @@ __global__ void __launch_bounds__(256) k_wmaxmin(int32_t num_scen, const int32_t
   }
 }
 
-__global__ void __launch_bounds__(CYC_WARPS * 32) k_cycle(CycArgs a) {
+#ifndef DSTACK_CYC_MINB
+#define DSTACK_CYC_MINB 4
+#endif
+__global__ void __launch_bounds__(CYC_WARPS * 32, DSTACK_CYC_MINB) k_cycle(CycArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   CycSmem &sm = reinterpret_cast<CycSmem *>(smem_raw)[warp];
@@ -146,3 +149,15 @@ int launch_cycle(const CycArgs &a, cudaStream_t s, int *launches) {
 }
 
 }  // namespace dstack
+
+#if DSTACK_PROF_STATS
+extern "C" int dstack_debug_stats_cycle(unsigned long long *out16, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out16, dstack::g_cstats, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(dstack::g_cstats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -17,20 +17,30 @@
 
 namespace dstack {
 
+#ifndef DSTACK_PROF_STATS
+#define DSTACK_PROF_STATS 0
+#endif
+#if DSTACK_PROF_STATS
+static __device__ unsigned long long g_cstats[16];   // per TU (instrumentation builds only)
+#define CSTAT(i, v) atomicAdd(&g_cstats[i], (unsigned long long)(v))
+#else
+#define CSTAT(i, v) ((void)0)
+#endif
+
 constexpr uint16_t NONE16 = 0xFFFF;
 
-#ifndef DSTACK_CYC_GMIN
-#define DSTACK_CYC_GMIN 0
-#endif
-#ifndef DSTACK_CYC_ONEPASS
-#define DSTACK_CYC_ONEPASS 0
-#endif
 
 struct CycSmem {
   uint8_t occ[DSTACK_MAX_SLOTS];
-  uint32_t dmask[DSTACK_MAX_SLOTS / 32];
+  uint32_t dmask[DSTACK_MAX_SLOTS / 32];   // decision times (bit u of word w <=> slot 32 w + u)
   uint16_t starts[DSTACK_MAX_JOBS];
 };
+
+// bytes of a lane's 4-slot word (first slot `base`) below slot x
+__device__ __forceinline__ uint32_t bytes_below(int x, int base) {
+  const int hb = min(max(x - base, 0), 4);
+  return __funnelshift_rc(0xFFFFFFFFu, 0u, (uint32_t)(32 - 8 * hb));
+}
 
 // dtab layout: one row of DSTACK_MAX_BATCH u16 per DNN of the scenario, entry b-1 = d_j(b) slots
 
@@ -181,6 +191,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     const int offj = (int)__shfl_sync(FULL, joff, j);
     const int rel = rj * slj, dlv = rel + slj;
     const int st = (rj & 1) ? find_late(sm.occ, rel, dlv, dj, gj, L, lane) : find_early(sm.occ, rel, dlv, dj, gj, L, lane);
+    if (lane == 0) { CSTAT(1, 1); CSTAT(2, st >= 0 ? ((rj & 1) ? (dlv - st - dj) / 32 + 1 : (st - rel) / 32 + 1) : 0); }
     if (st >= 0) {
       occ_add(sm.occ, st, dj, gj, lane);
       if (lane == 0) {
@@ -199,15 +210,29 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   }
   res.occ_static = occ_sum(sm.occ, nslots, lane);
   // ---- opportunistic fill at decision times {0} u {run ends} (Dynamic-schedule) ----
+  // Per decision time t the warp holds the occupancy of slots [t & ~3, (t & ~3) + 128) in registers (one packed
+  // word per lane); slice queries and placements inside that window touch no shared memory except the
+  // write-through of placed runs.  Longer runs fall back to the shared-memory scans.
   if (lane == 0) sm.dmask[0] |= 1u;
   __syncwarp();
   uint32_t count = runs + count0;
   int fs = -1, fe = -1;       // last fill run of this lane's DNN
   uint32_t nfill = 0;
-  int nsr = 0;                // first static window whose run starts after t (amortised, t only grows)
-  const uint32_t sl_magic = sl <= 1 ? 0u : (uint32_t)(0xFFFFFFFFu / sl) + 1u;   // t / sl = umulhi(t, magic), t < 2^13
+  // this lane's next placed static run not yet over: index p into its windows, start sp (its end sp + d*)
+  int p = 0, sp = -1;
+  auto adv = [&](int tt) {
+    while (p < (int)rep) {
+      if (sp < 0) { const uint16_t v = sm.starts[joff + p]; sp = v == NONE16 ? -2 : (int)v; }
+      if (sp == -2 || sp + (int)dstar <= tt) { ++p; sp = -1; continue; }
+      break;
+    }
+  };
+  const uint32_t pk = (g & 0xFFu) | ((bs & 0xFFu) << 8) | (dstar << 16);   // dstar <= 0xFFFF (u16 rows)
   const int nwords = (nslots + 31) >> 5;
-  const int gmin = (int)__reduce_min_sync(FULL, active ? g : 0xFFFFu);   // no model can start where occ > L - gmin
+  uint32_t *w32 = reinterpret_cast<uint32_t *>(sm.occ);
+  // a candidate whose slice at t is too short for d(b_lo) stays too short at every later decision time
+  // t' < blk: the slot that ended its slice never loses occupancy (or it was its own next static start)
+  int blk = 0;
   int t = -1;
   while (true) {
     const int start = t + 1;
@@ -219,32 +244,24 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       const uint32_t bal = __ballot_sync(FULL, v != 0);
       if (bal) {
         const int pl = __ffs(bal) - 1;
-        const uint32_t word = __shfl_sync(FULL, v, pl);
-        nt = (wb + pl) * 32 + __ffs(word) - 1;
+        nt = (wb + pl) * 32 + __ffs(__shfl_sync(FULL, v, pl)) - 1;
         break;
       }
     }
     if (nt < 0 || nt >= nslots) break;
     t = nt;
-    int occ_t = sm.occ[t];
-#if DSTACK_CYC_GMIN
-    if (occ_t + gmin > L) continue;
-#endif
+    if (lane == 0) CSTAT(3, 1);
+    const int bt = t & ~3, mybase = bt + 4 * lane, wi = (t >> 2) + lane;
+    uint32_t wv = wi < DSTACK_MAX_SLOTS / 4 ? w32[wi] : 0u;
+    const uint32_t lo_mask = lane == 0 ? (0xFFFFFFFFu << (8 * (t & 3))) : 0xFFFFFFFFu;
+    int occ_t = (int)((__shfl_sync(FULL, wv, 0) >> (8 * (t & 3))) & 0xFFu);
     bool elig = false;
     int ns = nslots;
-    if (active) {   // eligible: not running at t (static run of window t/sl or the last fill), fits at t
-      const int rr = sl == 1 ? t : (int)__umulhi((uint32_t)t, sl_magic);
-      bool covered = (fs <= t && t < fe);
-      if (rr < (int)rep) {
-        const uint16_t s0 = sm.starts[joff + rr];
-        if (s0 != NONE16 && (int)s0 <= t && t < (int)s0 + (int)dstar) covered = true;
-      }
-      while (nsr < (int)rep) {
-        const uint16_t s2 = sm.starts[joff + nsr];
-        if (s2 != NONE16 && (int)s2 > t) { ns = s2; break; }
-        ++nsr;
-      }
-      elig = !covered && occ_t + (int)g <= L;
+    if (active) {   // eligible: not running at t (static or last fill run), fits at t
+      adv(t);
+      const bool cov_static = p < (int)rep && sp <= t;
+      if (p < (int)rep && sp > t) ns = sp;
+      elig = t >= blk && !cov_static && !(fs <= t && t < fe) && occ_t + (int)g <= L;
     }
     // candidates in (runs so far, index) order; a placement raises occ[t], so re-test the rest in parallel
     uint32_t key = elig ? ((count << 5) | (uint32_t)lane) : 0xFFFFFFFFu;
@@ -252,35 +269,26 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       const uint32_t mk = __reduce_min_sync(FULL, key);
       if (mk == 0xFFFFFFFFu) break;
       const int j = (int)(mk & 31u);
+      if (lane == 0) CSTAT(4, 1);
       if (lane == j) key = 0xFFFFFFFFu;
-      const int gj = (int)__shfl_sync(FULL, g, j);
+      const uint32_t pj = __shfl_sync(FULL, pk, j);
+      const int gj = (int)(pj & 0xFFu), bsj = (int)((pj >> 8) & 0xFFu), dsj = (int)(pj >> 16);
       const int limit = __shfl_sync(FULL, ns, j);
-      const int bsj = (int)__shfl_sync(FULL, bs, j);
-      const int dsj = (int)__shfl_sync(FULL, dstar, j);
-      // slice k = first u in [t, limit) with occ[u] + g > L; only k >= d(b*) or its exact value below matters
+      // slice: first u in [t, stop) with occ[u] + g > L (stop = min(t + d(b*), next own static start))
       const int stop = t + dsj < limit ? t + dsj : limit;
-      if (DSTACK_CYC_ONEPASS && stop - t == dsj && dsj <= 124) {
-        // common case, one pass: the whole run fits in one 128-slot chunk; test it and place b* at once
-        uint32_t *w32 = reinterpret_cast<uint32_t *>(sm.occ);
-        const int w = (t >> 2) + lane, base = w << 2;
-        const uint32_t m = base < stop ? bytes_mask(t, stop, base) : 0u;
-        const uint32_t word = m ? w32[w] : 0u;
-        const uint32_t bb = __vcmpgtu4(word, (uint32_t)(L - gj) * 0x01010101u) & m;
-        if (__ballot_sync(FULL, bb != 0) == 0) {
-          if (m) w32[w] = word + (((uint32_t)gj * 0x01010101u) & m);
-          occ_t += gj;
-          if (lane == 0) {
-            if (stop < nslots) sm.dmask[stop >> 5] |= 1u << (stop & 31);
-            if (fill_log && nfill < fill_cap) fill_log[nfill] = pack_run((uint32_t)j, (uint32_t)t, (uint32_t)dsj, (uint32_t)bsj);
-          }
-          nfill++;
-          __syncwarp();
-          if (lane == j) { count++; runs++; served += (uint32_t)bsj; fs = t; fe = stop; }
-          if (occ_t + (int)g > L) key = 0xFFFFFFFFu;
-          continue;
+      int kend;
+      if (stop <= bt + 128) {
+        const uint32_t bb = __vcmpgtu4(wv, (uint32_t)(L - gj) * 0x01010101u) & lo_mask & bytes_below(stop, mybase);
+        const uint32_t bal = __ballot_sync(FULL, bb != 0);
+        kend = stop;
+        if (bal) {
+          const int pl = __ffs(bal) - 1;
+          kend = bt + 4 * pl + ((__ffs(__shfl_sync(FULL, bb, pl)) - 1) >> 3);
         }
+      } else {
+        kend = first_above(sm.occ, t, stop, L - gj, lane);
       }
-      const int kslice = first_above(sm.occ, t, stop, L - gj, lane) - t;
+      const int kslice = kend - t;
       int bsel = 0;   // largest b in [b_lo, b*] with d(b) <= slice (d nondecreasing in b)
       const uint16_t *dj = dtab + j * DSTACK_MAX_BATCH;
       if (kslice >= dsj) {
@@ -293,21 +301,33 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
           if (bal) { bsel = b0 + 31 - __clz(bal); break; }
         }
       }
-      if (bsel == 0) continue;
+      if (bsel == 0) {
+        if (lane == j) blk = kend;
+        continue;
+      }
+      if (lane == 0) { CSTAT(5, 1); CSTAT(6, bsel != bsj); CSTAT(7, kslice < dsj); }
       const int dsel = bsel == bsj ? dsj : (int)dj[bsel - 1];
-      occ_add(sm.occ, t, dsel, gj, lane);
+      const int e = t + dsel;
+      if (e <= bt + 128) {   // place inside the window: register word + write-through
+        const uint32_t add = ((uint32_t)gj * 0x01010101u) & lo_mask & bytes_below(e, mybase);
+        if (add) { wv += add; w32[wi] = wv; }
+      } else {
+        occ_add(sm.occ, t, dsel, gj, lane);
+        wv = wi < DSTACK_MAX_SLOTS / 4 ? w32[wi] : 0u;
+      }
       occ_t += gj;
       if (lane == 0) {
-        if (t + dsel < nslots) sm.dmask[(t + dsel) >> 5] |= 1u << ((t + dsel) & 31);
+        if (e < nslots) sm.dmask[e >> 5] |= 1u << (e & 31);
         if (fill_log && nfill < fill_cap) fill_log[nfill] = pack_run((uint32_t)j, (uint32_t)t, (uint32_t)dsel, (uint32_t)bsel);
       }
       nfill++;
       __syncwarp();
-      if (lane == j) { count++; runs++; served += (uint32_t)bsel; fs = t; fe = t + dsel; }
+      if (lane == j) { count++; runs++; served += (uint32_t)bsel; fs = t; fe = e; }
       if (occ_t + (int)g > L) key = 0xFFFFFFFFu;
     }
   }
   res.occ_all = occ_sum(sm.occ, nslots, lane);
+  if (lane == 0) CSTAT(0, 1);
   if (fill_n) *fill_n = nfill;
   res.served_tot = __reduce_add_sync(FULL, served);
   return res;

@@ -15,6 +15,8 @@ dp = dstack.from_device_dict(g)
 lib = dstack.lib()
 buf = (C.c_ulonglong * 16)()
 lib.dstack_debug_stats(buf, 1)
+cbuf = (C.c_ulonglong * 16)()
+lib.dstack_debug_stats_cycle(cbuf, 1)
 out = dstack.eval_batch(dp, p)
 torch.cuda.synchronize()
 lib.dstack_debug_stats(buf, 1)
@@ -23,3 +25,10 @@ names = ["dnn_searched", "b_range>1", "jensen_surv", "run_surv", "better_exact_t
 nd = max(v[0], 1)
 for i, nm in enumerate(names):
     print(f"{nm:18s} {v[i]:14d}  per DNN {v[i]/nd:8.3f}")
+lib.dstack_debug_stats_cycle(cbuf, 1)
+c = list(cbuf)
+cn = ["sessions", "static_jobs", "static_scan_chunks", "decision_times", "fill_candidates", "fill_placed",
+      "fill_smaller_b", "fill_slice_short"]
+ns = max(c[0], 1)
+for i, nm in enumerate(cn):
+    print(f"{nm:18s} {c[i]:14d}  per session {c[i]/ns:8.3f}")
