@@ -31,21 +31,39 @@ __device__ __forceinline__ double block_sum_f64(double v, double *red) {
   return t;   // valid in thread 0
 }
 
+// warp-aggregated shared-memory histogram increment (native 32-bit atomics; lanes with equal keys
+// are merged first, so the all-equal common case costs one atomic per warp)
+__device__ __forceinline__ void hist_inc(uint32_t *h, uint32_t key, bool on) {
+  const uint32_t act = __ballot_sync(FULL, on);
+  if (!on) return;
+  const uint32_t peers = __match_any_sync(act, key);
+  if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&h[key], (uint32_t)__popc(peers));
+}
+
+// per-block u32 histograms (a block covers < 2^32 items), widened into the u64 partial at the end
+struct AggHist {
+  uint32_t n_st[5], n_scen_st[5], batch[DSTACK_MAX_BATCH + 1], demand[256];
+};
+
 __global__ void __launch_bounds__(AGG_THREADS) k_agg1(AggArgs a) {
-  __shared__ dstack_agg_t sa;
+  __shared__ AggHist hs;
   __shared__ double red[AGG_THREADS / 32];
-  uint64_t *z = reinterpret_cast<uint64_t *>(&sa);
-  for (int i = threadIdx.x; i < (int)(sizeof(dstack_agg_t) / 8); i += blockDim.x) z[i] = 0;
+  __shared__ unsigned long long cnt[7];
+  uint32_t *hz = reinterpret_cast<uint32_t *>(&hs);
+  for (int i = threadIdx.x; i < (int)(sizeof(AggHist) / 4); i += blockDim.x) hz[i] = 0;
+  if (threadIdx.x < 7) cnt[threadIdx.x] = 0;
   __syncthreads();
   const int64_t per = ((int64_t)a.num_scen + AGG_BLOCKS - 1) / AGG_BLOCKS;
   const int64_t s0 = (int64_t)blockIdx.x * per;
   const int64_t s1 = s0 + per < a.num_scen ? s0 + per : a.num_scen;
   double f[5] = {0, 0, 0, 0, 0};
   uint64_t sched = 0, misses = 0, cks = 0, runs = 0, served = 0, ndnn = 0, nok = 0;
-  for (int64_t s = s0 + threadIdx.x; s < s1; s += blockDim.x) {
-    const uint8_t ss = a.scen_status ? a.scen_status[s] : 0;
-    if (ss < 5) atomicAdd((unsigned long long *)&sa.n_scen_st[ss], 1ull);
-    const uint32_t T = a.T_us ? a.T_us[s] : 0;
+  // loop bounds rounded up to whole blocks so every warp reaches the warp-collective histogram updates
+  for (int64_t s = s0 + threadIdx.x; s - threadIdx.x < s1; s += blockDim.x) {
+    const bool in = s < s1;
+    const uint8_t ss = in ? (a.scen_status ? a.scen_status[s] : 0) : 0;
+    hist_inc(hs.n_scen_st, ss, in && ss < 5);
+    const uint32_t T = in && a.T_us ? a.T_us[s] : 0;
     if (T > 0) {
       sched++;
       if (a.u_static) f[0] += a.u_static[s];
@@ -54,45 +72,51 @@ __global__ void __launch_bounds__(AGG_THREADS) k_agg1(AggArgs a) {
       if (a.u_ideal) f[3] += a.u_ideal[s];
       if (a.thr_ideal) f[4] += a.thr_ideal[s];
     }
-    if (a.misses) misses += a.misses[s];
+    if (in && a.misses) misses += a.misses[s];
   }
   // DNN range of this block's scenarios
   const int64_t k0 = s0 < s1 ? a.off[s0] : 0, k1 = s0 < s1 ? a.off[s1] : 0;
-  for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-    ndnn++;
-    const uint8_t st = a.status ? a.status[k] : 0;
-    if (st < 5) atomicAdd((unsigned long long *)&sa.n_st[st], 1ull);
-    const uint32_t dm = a.demand ? a.demand[k] : 0, bt = a.batch ? a.batch[k] : 0;
-    if (st == DSTACK_ST_OK) {
-      nok++;
-      atomicAdd((unsigned long long *)&sa.batch_hist[bt <= DSTACK_MAX_BATCH ? bt : 0], 1ull);
-      atomicAdd((unsigned long long *)&sa.demand_hist[dm & 255], 1ull);
+  for (int64_t k = k0 + threadIdx.x; k - threadIdx.x < k1; k += blockDim.x) {
+    const bool in = k < k1;
+    const uint8_t st = in ? (a.status ? a.status[k] : 0) : 0xFF;
+    const uint32_t dm = in && a.demand ? a.demand[k] : 0, bt = in && a.batch ? a.batch[k] : 0;
+    hist_inc(hs.n_st, st, st < 5);
+    const bool ok = st == DSTACK_ST_OK;
+    hist_inc(hs.batch, bt <= DSTACK_MAX_BATCH ? bt : 0, ok);
+    hist_inc(hs.demand, dm & 255, ok);
+    if (in) {
+      ndnn++;
+      nok += ok;
+      const uint32_t rn = a.runs ? a.runs[k] : 0, sv = a.served ? a.served[k] : 0;
+      runs += rn; served += sv;
+      const uint64_t v = ((uint64_t)k << 40) ^ ((uint64_t)dm << 24) ^ ((uint64_t)bt << 16) ^
+                         ((uint64_t)(a.knee ? a.knee[k] : 0)) ^ ((uint64_t)(a.alloc ? a.alloc[k] : 0) << 8) ^
+                         ((uint64_t)rn << 44) ^ ((uint64_t)sv << 20) ^ ((uint64_t)st << 60);
+      cks += mix64(v);
     }
-    const uint32_t rn = a.runs ? a.runs[k] : 0, sv = a.served ? a.served[k] : 0;
-    runs += rn; served += sv;
-    const uint64_t v = ((uint64_t)k << 40) ^ ((uint64_t)dm << 24) ^ ((uint64_t)bt << 16) ^
-                       ((uint64_t)(a.knee ? a.knee[k] : 0)) ^ ((uint64_t)(a.alloc ? a.alloc[k] : 0) << 8) ^
-                       ((uint64_t)rn << 44) ^ ((uint64_t)sv << 20) ^ ((uint64_t)st << 60);
-    cks += mix64(v);
   }
-  atomicAdd((unsigned long long *)&sa.n_scen_scheduled, (unsigned long long)sched);
-  atomicAdd((unsigned long long *)&sa.misses, (unsigned long long)misses);
-  atomicAdd((unsigned long long *)&sa.checksum, (unsigned long long)cks);
-  atomicAdd((unsigned long long *)&sa.runs, (unsigned long long)runs);
-  atomicAdd((unsigned long long *)&sa.served, (unsigned long long)served);
-  atomicAdd((unsigned long long *)&sa.n_dnn, (unsigned long long)ndnn);
-  atomicAdd((unsigned long long *)&sa.n_dnn_ok, (unsigned long long)nok);
+  const uint64_t vals[7] = {sched, misses, cks, runs, served, ndnn, nok};
+#pragma unroll
+  for (int i = 0; i < 7; ++i) {
+    uint64_t v = vals[i];
+#pragma unroll
+    for (int m = 16; m; m >>= 1) v += __shfl_xor_sync(FULL, v, m);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&cnt[i], (unsigned long long)v);
+  }
   double tot[5];
   for (int i = 0; i < 5; ++i) tot[i] = block_sum_f64(f[i], red);
   __syncthreads();
+  dstack_agg_t *dst = &a.partials[blockIdx.x];
   if (threadIdx.x == 0) {
-    sa.sum_u_static = tot[0]; sa.sum_u = tot[1]; sa.sum_thr = tot[2]; sa.sum_u_ideal = tot[3];
-    sa.sum_thr_ideal = tot[4];
-    sa.n_scen = (uint64_t)(s1 > s0 ? s1 - s0 : 0);
+    dst->sum_u_static = tot[0]; dst->sum_u = tot[1]; dst->sum_thr = tot[2]; dst->sum_u_ideal = tot[3];
+    dst->sum_thr_ideal = tot[4];
+    dst->n_scen = (uint64_t)(s1 > s0 ? s1 - s0 : 0);
+    dst->n_scen_scheduled = cnt[0]; dst->misses = cnt[1]; dst->checksum = cnt[2]; dst->runs = cnt[3];
+    dst->served = cnt[4]; dst->n_dnn = cnt[5]; dst->n_dnn_ok = cnt[6];
   }
-  __syncthreads();
-  uint64_t *dst = reinterpret_cast<uint64_t *>(&a.partials[blockIdx.x]);
-  for (int i = threadIdx.x; i < (int)(sizeof(dstack_agg_t) / 8); i += blockDim.x) dst[i] = z[i];
+  for (int i = threadIdx.x; i < 5; i += blockDim.x) { dst->n_st[i] = hs.n_st[i]; dst->n_scen_st[i] = hs.n_scen_st[i]; }
+  for (int i = threadIdx.x; i <= DSTACK_MAX_BATCH; i += blockDim.x) dst->batch_hist[i] = hs.batch[i];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) dst->demand_hist[i] = hs.demand[i];
 }
 
 __global__ void __launch_bounds__(AGG_THREADS) k_agg2(AggArgs a) {
