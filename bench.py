@@ -122,14 +122,27 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def traffic_per_scenario():
-    """ncu dram bytes per scenario for each kernel, from the committed profile summary (or None)."""
-    p = os.path.join(ROOT, "profiles", "traffic.json")
+def kernel_counters(config):
+    """ncu per-scenario counters of each kernel slot (warp instructions, DRAM bytes) for config 3, measured on
+    the committed build (profiles/counters.json, tools/ncu_counters.py); {} for other configs."""
+    if config != 3:
+        return {}
     try:
-        with open(p) as f:
-            return json.load(f)
+        with open(os.path.join(ROOT, "profiles", "counters.json")) as f:
+            return json.load(f)["per_scenario"]
     except Exception:
         return {}
+
+
+def issue_peak():
+    """Issue-slot peak: 148 SMs x 4 SMSPs x 1 warp-instruction/cycle (B300_MICROARCH.md 'SMSPs per SM',
+    B200_PROFILING.md SM count) at the measured max SM clock."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f)["sm_max_mhz"])
+    except Exception:
+        mhz = 1965.0
+    return 148 * 4 * mhz / 1e3, f"148 SMs x 4 SMSP x 1 warp-inst/clk x {mhz:.0f} MHz (Gwarp-inst/s)"
 
 
 # --------------------------------------------------------------- reference ---
@@ -278,22 +291,38 @@ def run_native(args, rank, world, local):
             dist.destroy_process_group()
         return 0
     ab = algorithmic_bytes(dp, args)
-    dom_name = max(kern, key=kern.get)          # the kernel with the largest share of the step
-    dom_bytes = ab[dom_name]
     peak, peak_src = hbm_peak()
-    achieved = dom_bytes / (kern[dom_name] / 1e3) / 1e9
-    traffic = None
-    tr = traffic_per_scenario().get(dom_name)
-    if tr:
-        traffic = tr * per_gpu
+    cnt = kernel_counters(args.config)
+
+    def kernel_roofline(name):
+        """The kernel's binding roofline: issue slots (ALU-bound; executed warp instructions per launch from
+        the committed ncu counters / live launch time) with its HBM roofline (algorithmic bytes) beside it."""
+        sec = kern[name] / 1e3
+        hbm_ach = ab[name] / sec / 1e9
+        c = cnt.get(name)
+        traffic = c["dram_bytes"] * per_gpu if c else None
+        hbm = {"algorithmic_bytes_per_launch": ab[name], "achieved": hbm_ach, "peak": peak, "unit": "GB/s",
+               "frac": hbm_ach / peak, "traffic": traffic, "peak_source": peak_src}
+        if not c:
+            return dict({"bound": "hbm", "kernel": name}, **hbm)
+        ipk, ipk_src = issue_peak()
+        inst = c["warp_inst"] * per_gpu
+        ach = inst / sec / 1e9
+        if hbm["frac"] > ach / ipk:                 # the resource closer to saturation is the bound
+            return dict({"bound": "hbm", "kernel": name, "issue": {"achieved": ach, "peak": ipk, "frac": ach / ipk}}, **hbm)
+        return {"bound": "alu", "kernel": name, "achieved": ach, "peak": ipk, "unit": "Gwarp-inst/s",
+                "frac": ach / ipk, "traffic": traffic, "peak_source": ipk_src,
+                "counted": f"ncu smsp__inst_executed.sum per launch = {inst:.4g} (profiles/counters.json)",
+                "hbm": hbm}
+
+    dom_name = max(kern, key=kern.get)          # the kernel with the largest share of the step
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int64", "data": "synthetic (seeded Philox generator, SURVEY §8(d) recipe)",
         "config": workload_config(args, sp0, p, world),
-        "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": dom_bytes},
+        "roofline": kernel_roofline(dom_name),
+        "roofline_by_kernel": {k: kernel_roofline(k) for k in kern},
         "path_roofline": {"algorithmic_bytes_per_step": ab["path"],
                           "achieved_GBps": ab["path"] / (ms_max / args.steps / 1e3) / 1e9,
                           "frac": ab["path"] / (ms_max / args.steps / 1e3) / 1e9 / peak},
