@@ -197,7 +197,8 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
   // ---- scan of the histogram (lane owns widths m0..m0+CB-1, re-zeroing them): exclusive lane offsets;
   //      the per-width prefixes PA[m] = sum_{1<=n<=m} R, PW[m] = sum_{n<=m} n R (u32: RT < 2^24 here) are
   //      formed in the candidate pass below ----
-  const int m0 = lane * CB;
+  int m0 = lane * CB;
+  asm volatile("" : "+r"(m0));   // per-DNN value: keeps the per-width constants out of the loop-invariant (spilled) set
   uint32_t h[CB], ra, rw, Wsm;
   {
     uint32_t sa = 0, sw = 0;
