@@ -107,9 +107,11 @@ struct Top2 {
   float t1, t2;
   uint32_t s1;
 };
-__device__ __forceinline__ void top2_add(Top2 &t, float f, uint32_t S) {
-  if (f > t.t1) { t.t2 = t.t1; t.t1 = f; t.s1 = S; }
-  else t.t2 = fmaxf(t.t2, f);
+__device__ __forceinline__ void top2_add(Top2 &t, float f, uint32_t S) {   // branch-free
+  const bool gt = f > t.t1;
+  t.t2 = fmaxf(t.t2, fminf(t.t1, f));
+  t.s1 = gt ? S : t.s1;
+  t.t1 = fmaxf(t.t1, f);
 }
 
 // Warp argmax from the per-lane top-2 trackers: the float maximum decides unless a second candidate lies
@@ -236,51 +238,46 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
   const uint64_t base = Mtp * Wb + memb;
   const float C1f2 = 2.f * (float)C1, Mtpf = (float)Mtp, Wbf = (float)Wb, membf = (float)memb;
   const float half = 0.5f * (float)S_tot;
-  const int mh = S_tot >> 1, mb = S_tot / b_hi;
+  const int mh = S_tot >> 1;
   uint64_t *scr = cA;
   Top2 tk = {0.f, 0.f, 0u}, te = {0.f, 0.f, 0u};
   float G = 0.f;
-  uint32_t pam = 0, pwm = 0;
+  {
+    // overflow: X(L, b_hi) = b_hi t_np RT S_tot M + M t_p (S_tot PA[mb] + b_hi Q[mb]) + mem is the grid maximum;
+    // with PA[mb] <= RT and Q[mb] <= W this bound (f64) settles it unless within 1e-4 of 2^56, where the
+    // generic path decides exactly
+    const double bd = (double)b_hi, Sd = (double)S_tot;
+    double xe = bd * (double)t_np * (double)M * (double)RT * Sd +
+                (double)Mtp * (Sd * (double)RT + bd * ((double)Wb + (double)Wsm));
+    if (mem_mode == 1) xe += bd * (double)D;
+    else if (mem_mode == 2) xe += bd * (double)D * Sd * Sd;
+    if (xe >= 72057594037927936.0 * 0.9999) return false;
+  }
 #pragma unroll
   for (int i = 0; i < CB; ++i) {
     const uint32_t S = (uint32_t)(m0 + i);
     ra += h[i]; rw += h[i] * S;                          // PA[S], PW[S]
-    if ((int)S == mb) { pam = ra; pwm = rw; }
     const uint32_t q = Wsm - rw;                         // Q[S] - W>
     uint64_t X = (uint64_t)S * C1 + Mtp * ((uint64_t)S * ra + q) + base;
     if (mem_mode == 2) X += D * (uint64_t)(S * S);
     if ((int)S <= S_tot) scr[S] = X;
     const float f = score_f(S, X);
-    if ((vmask >> i) & 1u) {
-      top2_add(tk, f, S);
-      if (2 * X <= (uint64_t)S * F) top2_add(te, f, S);   // Eqs. 11-12
-    }
+    const bool valid = (vmask >> i) & 1u;
+    top2_add(tk, valid ? f : 0.f, S);
+    top2_add(te, valid && 2 * X <= (uint64_t)S * F ? f : 0.f, S);   // Eqs. 11-12
     // Batch certificate: for b >= 2 and s = S/b in segment m = floor(s),
     // X(S, b) >= b (alpha s + beta), alpha = 2 C1 + Mtp PA[m], beta = Mtp Q[m] + mem, hence
     // eta(S, b) <= s / (alpha s + beta)^2; G = max over m <= S_tot/2 of its supremum on [m, m+1).
     if ((int)S <= mh) {
       const float af = fmaf(Mtpf, (float)ra, C1f2), bf = fmaf(Mtpf, (float)q + Wbf, membf);
+      // the curve is unimodal with its peak at s = beta / alpha: evaluate it at that point clamped to [lo, hi]
+      // (an approximate interior maximiser only lowers the value by O(2^-44) relative, far inside the margin)
       const float lo = (float)S, hi = fminf(lo + 1.f, half);
-      float v;
-      if (bf == 0.f) v = __int_as_float(0x7f800000);          // s/(alpha s)^2 is unbounded at s -> 0
-      else if (bf <= af * lo) { const float x = fmaf(af, lo, bf); v = lo * rcp_approx(x * x); }
-      else if (bf >= af * hi) { const float x = fmaf(af, hi, bf); v = hi * rcp_approx(x * x); }
-      else v = rcp_approx(4.f * af * bf);                     // interior peak at s = beta / alpha
+      const float sx = fminf(fmaxf(bf * rcp_approx(af), lo), hi);
+      const float x = fmaf(af, sx, bf);
+      const float v = bf == 0.f ? __int_as_float(0x7f800000) : sx * rcp_approx(x * x);   // unbounded at s -> 0
       G = fmaxf(G, v);
     }
-  }
-  {
-    // overflow: X(L, b_hi) = b_hi t_np RT S_tot M + M t_p (S_tot PA[mb] + b_hi Q[mb]) + mem is the grid
-    // maximum (f64; within 1e-4 of 2^56 the generic path decides exactly)
-    pam = __shfl_sync(FULL, pam, mb / CB);
-    pwm = __shfl_sync(FULL, pwm, mb / CB);
-    const double bd = (double)b_hi, Sd = (double)S_tot;
-    double xe = bd * (double)t_np * (double)M * (double)RT * Sd +
-                (double)Mtp * (Sd * (double)pam + bd * ((double)Wb + (double)(Wsm - pwm)));
-    if (mem_mode == 1) xe += bd * (double)D;
-    else if (mem_mode == 2) xe += bd * (double)D * Sd * Sd;
-    if (xe >= 72057594037927936.0 * 1.0001) { st = DSTACK_ST_OVERFLOW; return true; }
-    if (xe >= 72057594037927936.0 * 0.9999) return false;
   }
   __syncwarp();
   uint32_t Sk = 0, Se = 0;
