@@ -96,6 +96,43 @@ __device__ __forceinline__ int find_late(const uint8_t *occ, int rel, int dl, in
 }
 
 // byte mask of slots [lo, hi) of a 4-slot word starting at slot `base` (lo/hi are clamped to [0, 4])
+__device__ __forceinline__ uint32_t bytes_mask(int s, int e, int base);
+
+// Packed-word searches for runs of d <= 124 slots (the run [s, s+d) lies in the 128 slots from s & ~3, one u32
+// word of 4 slots per lane): jump over the blocking slot nearest to the far end of the candidate run.
+// Start-Early: smallest feasible s in [rel, dl-d]; -1 if none.
+__device__ __forceinline__ int find_early_packed(const uint8_t *occ, int rel, int dl, int d, int g, int L, int lane) {
+  const uint32_t *w32 = reinterpret_cast<const uint32_t *>(occ);
+  const uint32_t th = (uint32_t)(L - g) * 0x01010101u;
+  int s = rel;
+  while (s + d <= dl) {
+    const int bt = s & ~3, wi = (bt >> 2) + lane, mybase = bt + 4 * lane;
+    const uint32_t word = wi < DSTACK_MAX_SLOTS / 4 ? w32[wi] : 0u;
+    const uint32_t bb = __vcmpgtu4(word, th) & bytes_mask(s, s + d, mybase);   // blocking slots in the run
+    const uint32_t lb = bb ? (uint32_t)(mybase + ((31 - __clz(bb)) >> 3) + 1) : 0u;
+    const uint32_t last = __reduce_max_sync(FULL, lb);   // (last blocking slot) + 1, or 0
+    if (last == 0) return s;
+    s = (int)last;
+  }
+  return -1;
+}
+// Start-Late: largest feasible s in [rel, dl-d]; -1 if none.
+__device__ __forceinline__ int find_late_packed(const uint8_t *occ, int rel, int dl, int d, int g, int L, int lane) {
+  const uint32_t *w32 = reinterpret_cast<const uint32_t *>(occ);
+  const uint32_t th = (uint32_t)(L - g) * 0x01010101u;
+  int s = dl - d;
+  while (s >= rel) {
+    const int bt = s & ~3, wi = (bt >> 2) + lane, mybase = bt + 4 * lane;
+    const uint32_t word = wi < DSTACK_MAX_SLOTS / 4 ? w32[wi] : 0u;
+    const uint32_t bb = __vcmpgtu4(word, th) & bytes_mask(s, s + d, mybase);
+    const uint32_t fb = bb ? (uint32_t)(mybase + ((__ffs(bb) - 1) >> 3)) : 0xFFFFFFFFu;
+    const uint32_t first = __reduce_min_sync(FULL, fb);   // first blocking slot, or none
+    if (first == 0xFFFFFFFFu) return s;
+    s = (int)first - d;
+  }
+  return -1;
+}
+
 __device__ __forceinline__ uint32_t bytes_mask(int s, int e, int base) {
   const int lo = min(max(s - base, 0), 4), hi = min(max(e - base, 0), 4);
   return (uint32_t)((0xFFFFFFFFull << (8 * lo)) & (0xFFFFFFFFull >> (32 - 8 * hi)));
@@ -164,8 +201,16 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
                                             uint32_t *fill_n = nullptr) {
   CycRes res; res.occ_static = 0; res.occ_all = 0; res.served_tot = 0; res.misses = 0; res.oversub = false;
   for (int w = lane; (w << 2) < nslots; w += 32) reinterpret_cast<uint32_t *>(sm.occ)[w] = 0u;
-  for (int w = lane; w < DSTACK_MAX_SLOTS / 32; w += 32) sm.dmask[w] = 0;
+  // decision-time bits: one register word per lane (word = lane) when nslots <= 1024, else shared memory
+  const bool dreg = nslots <= 1024;
+  uint32_t dmw = 0;
+  if (!dreg)
+    for (int w = lane; w < DSTACK_MAX_SLOTS / 32; w += 32) sm.dmask[w] = 0;
   __syncwarp();
+  auto dset = [&](int e) {   // warp-uniform e < nslots
+    if (dreg) { if (lane == (e >> 5)) dmw |= 1u << (e & 31); }
+    else if (lane == 0) sm.dmask[e >> 5] |= 1u << (e & 31);
+  };
   uint32_t joff = rep;   // exclusive prefix of rep over lanes
 #pragma unroll
   for (int dlt = 1; dlt < 32; dlt <<= 1) {
@@ -190,15 +235,16 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     const int dj = (int)(mk >> 5);
     const int offj = (int)__shfl_sync(FULL, joff, j);
     const int rel = rj * slj, dlv = rel + slj;
-    const int st = (rj & 1) ? find_late(sm.occ, rel, dlv, dj, gj, L, lane) : find_early(sm.occ, rel, dlv, dj, gj, L, lane);
-    if (lane == 0) { CSTAT(1, 1); CSTAT(2, st >= 0 ? ((rj & 1) ? (dlv - st - dj) / 32 + 1 : (st - rel) / 32 + 1) : 0); }
+    int st;
+    if (dj > dlv - rel) st = -1;
+    else if (dj <= 124) st = (rj & 1) ? find_late_packed(sm.occ, rel, dlv, dj, gj, L, lane)
+                                      : find_early_packed(sm.occ, rel, dlv, dj, gj, L, lane);
+    else st = (rj & 1) ? find_late(sm.occ, rel, dlv, dj, gj, L, lane) : find_early(sm.occ, rel, dlv, dj, gj, L, lane);
+    if (lane == 0) CSTAT(1, 1);
     if (st >= 0) {
       occ_add(sm.occ, st, dj, gj, lane);
-      if (lane == 0) {
-        sm.starts[offj + rj] = (uint16_t)st;
-        const int e = st + dj;
-        if (e < nslots) sm.dmask[e >> 5] |= 1u << (e & 31);
-      }
+      if (lane == 0) sm.starts[offj + rj] = (uint16_t)st;
+      if (st + dj < nslots) dset(st + dj);
       if (lane == j) { runs++; served += bs; }
     } else {
       if (lane == 0) sm.starts[offj + rj] = NONE16;
@@ -213,7 +259,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   // Per decision time t the warp holds the occupancy of slots [t & ~3, (t & ~3) + 128) in registers (one packed
   // word per lane); slice queries and placements inside that window touch no shared memory except the
   // write-through of placed runs.  Longer runs fall back to the shared-memory scans.
-  if (lane == 0) sm.dmask[0] |= 1u;
+  dset(0);
   __syncwarp();
   uint32_t count = runs + count0;
   int fs = -1, fe = -1;       // last fill run of this lane's DNN
@@ -237,15 +283,26 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   while (true) {
     const int start = t + 1;
     int nt = -1;
-    for (int wb = start >> 5; wb < nwords; wb += 32) {
-      const int w = wb + lane;
-      uint32_t v = w < nwords ? sm.dmask[w] : 0u;
-      if (w == (start >> 5)) v &= ~((1u << (start & 31)) - 1u);
+    if (dreg) {
+      const int sw = start >> 5;
+      uint32_t v = lane < sw ? 0u : dmw;
+      if (lane == sw) v &= ~((1u << (start & 31)) - 1u);
       const uint32_t bal = __ballot_sync(FULL, v != 0);
       if (bal) {
         const int pl = __ffs(bal) - 1;
-        nt = (wb + pl) * 32 + __ffs(__shfl_sync(FULL, v, pl)) - 1;
-        break;
+        nt = pl * 32 + __ffs(__shfl_sync(FULL, v, pl)) - 1;
+      }
+    } else {
+      for (int wb = start >> 5; wb < nwords; wb += 32) {
+        const int w = wb + lane;
+        uint32_t v = w < nwords ? sm.dmask[w] : 0u;
+        if (w == (start >> 5)) v &= ~((1u << (start & 31)) - 1u);
+        const uint32_t bal = __ballot_sync(FULL, v != 0);
+        if (bal) {
+          const int pl = __ffs(bal) - 1;
+          nt = (wb + pl) * 32 + __ffs(__shfl_sync(FULL, v, pl)) - 1;
+          break;
+        }
       }
     }
     if (nt < 0 || nt >= nslots) break;
@@ -316,10 +373,8 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
         wv = wi < DSTACK_MAX_SLOTS / 4 ? w32[wi] : 0u;
       }
       occ_t += gj;
-      if (lane == 0) {
-        if (e < nslots) sm.dmask[e >> 5] |= 1u << (e & 31);
-        if (fill_log && nfill < fill_cap) fill_log[nfill] = pack_run((uint32_t)j, (uint32_t)t, (uint32_t)dsel, (uint32_t)bsel);
-      }
+      if (e < nslots) dset(e);
+      if (lane == 0 && fill_log && nfill < fill_cap) fill_log[nfill] = pack_run((uint32_t)j, (uint32_t)t, (uint32_t)dsel, (uint32_t)bsel);
       nfill++;
       __syncwarp();
       if (lane == j) { count++; runs++; served += (uint32_t)bsel; fs = t; fe = e; }
