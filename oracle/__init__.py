@@ -71,6 +71,13 @@ def lib():
         L.oracle_wmaxmin.argtypes = [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]
         L.oracle_cycle_direct.argtypes = ([C.c_int32] + [C.c_void_p] * 4 + [C.c_int32] * 3 + [C.c_void_p] * 4
                                           + [P(OrCycSum), C.c_int32] + [C.c_void_p] * 6)
+        L.oracle_cycle_direct_ex.argtypes = ([C.c_int32] + [C.c_void_p] * 4 + [C.c_int32] * 3 + [C.c_void_p]
+                                             + [C.c_int32] + [C.c_void_p] * 4 + [P(OrCycSum), C.c_int32]
+                                             + [C.c_void_p] * 6)
+        L.oracle_temporal_direct.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32] + [C.c_void_p] * 3
+        L.oracle_gslice_direct.argtypes = ([C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]
+                                           + [C.c_void_p] * 5)
+        L.oracle_compare.argtypes = [P(OrProblem), P(OrParams)] + [C.c_void_p] * 4 + [C.c_int64, C.c_int32]
         L.oracle_simulate.argtypes = [P(OrProblem), P(OrParams), C.c_void_p, C.c_int32, C.c_uint64, C.c_int32,
                                       C.c_int64, P(OrSimOut), C.c_void_p, C.c_int64, C.c_int32]
         L.oracle_ideal_direct.argtypes = ([C.c_int32] + [C.c_void_p] * 6 + [C.c_int32, C.c_int64]
@@ -129,8 +136,11 @@ def wmaxmin(demand, L: int) -> np.ndarray:
     return a
 
 
-def cycle_direct(g, sl_slots, bstar, dtab, b_lo: int, L: int, nslots: int, trace_cap: int = 4096, count0=None):
-    """O5 with direct per-DNN inputs. dtab: array [n, 64], dtab[j, b-1] = d_j(b) slots."""
+def cycle_direct(g, sl_slots, bstar, dtab, b_lo: int, L: int, nslots: int, trace_cap: int = 4096, count0=None,
+                 fill_order: int = 0):
+    """O5 with direct per-DNN inputs. dtab: array [n, 64], dtab[j, b-1] = d_j(b) slots.
+    fill_order (O9): 0 D-STACK (runs so far), 1 Max-Min fair (smallest GPU% first), 2 max-throughput (shortest
+    run first); ties by index.  Returns also busy[j] = slots covered by j's runs."""
     g = np.ascontiguousarray(g, np.int32); sl = np.ascontiguousarray(sl_slots, np.int32)
     bs = np.ascontiguousarray(bstar, np.int32)
     n = g.shape[0]
@@ -141,15 +151,53 @@ def cycle_direct(g, sl_slots, bstar, dtab, b_lo: int, L: int, nslots: int, trace
     s = OrCycSum()
     tr = [np.zeros(trace_cap, np.int32) for _ in range(6)]
     c0 = None if count0 is None else np.ascontiguousarray(count0, np.int64)
-    rc = lib().oracle_cycle_direct(n, _p(g), _p(sl), _p(bs), _p(dt), b_lo, L, nslots, _p(c0), _p(runs), _p(served), _p(jm),
-                                   C.byref(s), trace_cap, *[_p(t) for t in tr])
+    busy = np.zeros(n, np.int64)
+    rc = lib().oracle_cycle_direct_ex(n, _p(g), _p(sl), _p(bs), _p(dt), b_lo, L, nslots, _p(c0), fill_order, _p(runs),
+                                      _p(served), _p(jm), _p(busy), C.byref(s), trace_cap, *[_p(t) for t in tr])
     assert rc == 0
     k = s.trace_n
     trace = dict(dnn=tr[0][:k], start=tr[1][:k], end=tr[2][:k], batch=tr[3][:k], kind=tr[4][:k], rep=tr[5][:k])
     return dict(occ_static_sum=s.occ_static_sum, occ_sum=s.occ_sum, served_total=s.served_total,
-                misses=s.misses, status=s.status, runs=runs, served=served, jmiss=jm, trace=trace,
+                misses=s.misses, status=s.status, runs=runs, served=served, jmiss=jm, trace=trace, busy=busy,
                 u_static=s.occ_static_sum / (nslots * L) if nslots else 0.0,
                 u=s.occ_sum / (nslots * L) if nslots else 0.0)
+
+
+def temporal_direct(lvl, sl_slots, dL, nslots: int):
+    """O9 temporal sharing with direct inputs: slices proportional to SLO, back-to-back runs at 100% GPU."""
+    lv = np.ascontiguousarray(lvl, np.int32); sl = np.ascontiguousarray(sl_slots, np.int32)
+    d = np.ascontiguousarray(dL, np.int64)
+    n = lv.shape[0]
+    slice_, runs = np.zeros(n, np.int64), np.zeros(n, np.int64)
+    occ = C.c_int64()
+    assert lib().oracle_temporal_direct(n, _p(lv), _p(sl), _p(d), nslots, _p(slice_), _p(runs), C.byref(occ)) == 0
+    return dict(slice=slice_, runs=runs, occ_num=occ.value)
+
+
+def gslice_direct(lvl, dk, nslots: int, L: int):
+    """O9 static spatial sharing (GSLICE CSS) with direct inputs; home[j] = -1 resident, slot index, -2 idle."""
+    lv = np.ascontiguousarray(lvl, np.int32); d = np.ascontiguousarray(dk, np.int64)
+    n = lv.shape[0]
+    home = np.zeros(n, np.int32); runs, busy = np.zeros(n, np.int64), np.zeros(n, np.int64)
+    K = C.c_int32(); occ = C.c_int64()
+    assert lib().oracle_gslice_direct(n, _p(lv), _p(d), nslots, L, _p(home), C.byref(K), _p(runs), _p(busy),
+                                      C.byref(occ)) == 0
+    return dict(home=home, nbins=K.value, runs=runs, busy=busy, occ_num=occ.value)
+
+
+CMP_NAMES = ("dstack", "maxmin", "maxthr", "temporal", "gslice")
+
+
+def compare(pb: Problem, p: Params, nthreads: int = 0, subset=None):
+    """O9: U, throughput and Jain fairness of the five schedulers per scenario, arrays [num_scen, 5] in the
+    order of CMP_NAMES (subset: scenario indices, others left zero)."""
+    S = pb.num_scen
+    u, thr, jain = (np.zeros((S, 5), np.float64) for _ in range(3))
+    idx = None if subset is None else np.ascontiguousarray(np.asarray(list(subset)), np.int64)
+    rc = lib().oracle_compare(C.byref(_problem(pb)), C.byref(_params(p)), _p(u), _p(thr), _p(jain), _p(idx),
+                              0 if idx is None else idx.shape[0], nthreads)
+    assert rc == 0
+    return dict(u=u, thr=thr, jain=jain)
 
 
 def ideal_direct(chains, slo_us, active, L: int, T_us: int, bstar=None):

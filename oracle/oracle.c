@@ -254,7 +254,8 @@ static int cycle_core(int32_t n, const int32_t *g, const int32_t *sl, const int3
                       const int64_t *dtab, int32_t b_lo, int32_t L, int32_t nslots, const int64_t *count0,
                       int32_t *runs, int64_t *served, int32_t *jmiss, or_cyc_sum_t *sum,
                       int32_t trace_cap, int32_t *tr_dnn, int32_t *tr_start, int32_t *tr_end,
-                      int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep, run_t **runs_out, int64_t *nrun_out) {
+                      int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep, run_t **runs_out, int64_t *nrun_out,
+                      int32_t fill_order, int64_t *busy) {
   if (n < 0 || n > 1024 || nslots < 0 || nslots > (1 << 20)) return -1;
   int32_t *occ = (int32_t *)calloc((size_t)nslots + 1, sizeof(int32_t));
   uint8_t *decide = (uint8_t *)calloc((size_t)nslots + 1, 1);
@@ -312,12 +313,19 @@ static int cycle_core(int32_t n, const int32_t *g, const int32_t *sl, const int3
   int32_t order[OR_MAX_DNN_PER_SCEN + 1024];
   for (int32_t t = 0; t < nslots; ++t) {
     if (!decide[t]) continue;
-    /* priority: fewest runs first (scoreboard), then index; snapshot at time t */
+    /* priority, snapshot at time t: D-STACK fewest runs first (scoreboard); O9 comparison
+       schedulers: Max-Min fair smallest GPU% first, max-throughput shortest run first;
+       ties by index */
     int32_t no = 0;
-    for (int32_t j = 0; j < n; ++j) if (g[j] > 0) order[no++] = j;
+    int64_t key[OR_MAX_DNN_PER_SCEN + 1024];
+    for (int32_t j = 0; j < n; ++j) {
+      if (g[j] <= 0) continue;
+      key[j] = fill_order == 0 ? count[j] : fill_order == 1 ? (int64_t)g[j] : dtab[(int64_t)j * 64 + bstar[j] - 1];
+      order[no++] = j;
+    }
     for (int32_t i = 1; i < no; ++i) {
       int32_t v = order[i], k = i - 1;
-      while (k >= 0 && (count[order[k]] > count[v] || (count[order[k]] == count[v] && order[k] > v))) {
+      while (k >= 0 && (key[order[k]] > key[v] || (key[order[k]] == key[v] && order[k] > v))) {
         order[k + 1] = order[k]; --k;
       }
       order[k + 1] = v;
@@ -349,6 +357,10 @@ static int cycle_core(int32_t n, const int32_t *g, const int32_t *sl, const int3
   }
   for (int32_t u = 0; u < nslots; ++u) sum->occ_sum += occ[u];
   for (int32_t j = 0; j < n; ++j) sum->served_total += served[j];
+  if (busy) {
+    for (int32_t j = 0; j < n; ++j) busy[j] = 0;
+    for (int64_t k = 0; k < nrun; ++k) busy[rl[k].j] += rl[k].end - rl[k].start;
+  }
   sum->trace_n = 0;
   for (int64_t k = 0; k < nrun && k < trace_cap; ++k) {
     tr_dnn[k] = rl[k].j; tr_start[k] = rl[k].start; tr_end[k] = rl[k].end;
@@ -366,7 +378,98 @@ int oracle_cycle_direct(int32_t n, const int32_t *g, const int32_t *sl, const in
                         int32_t trace_cap, int32_t *tr_dnn, int32_t *tr_start, int32_t *tr_end,
                         int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep) {
   return cycle_core(n, g, sl, bstar, dtab, b_lo, L, nslots, count0, runs, served, jmiss, sum, trace_cap, tr_dnn,
-                    tr_start, tr_end, tr_batch, tr_kind, tr_rep, NULL, NULL);
+                    tr_start, tr_end, tr_batch, tr_kind, tr_rep, NULL, NULL, 0, NULL);
+}
+
+int oracle_cycle_direct_ex(int32_t n, const int32_t *g, const int32_t *sl, const int32_t *bstar,
+                           const int64_t *dtab, int32_t b_lo, int32_t L, int32_t nslots, const int64_t *count0,
+                           int32_t fill_order, int32_t *runs, int64_t *served, int32_t *jmiss, int64_t *busy,
+                           or_cyc_sum_t *sum, int32_t trace_cap, int32_t *tr_dnn, int32_t *tr_start, int32_t *tr_end,
+                           int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep) {
+  if (fill_order < 0 || fill_order > 2) return -1;
+  return cycle_core(n, g, sl, bstar, dtab, b_lo, L, nslots, count0, runs, served, jmiss, sum, trace_cap, tr_dnn,
+                    tr_start, tr_end, tr_batch, tr_kind, tr_rep, NULL, NULL, fill_order, busy);
+}
+
+/* ---------------------------------------------------------------- O9 ---
+ * Comparison schedulers of §6.3, readings in DESIGN.md §3.2.
+ *
+ * Temporal sharing: over the session of nslots slots, model j gets the contiguous slice
+ * slice_j = floor(nslots * sl_j / sum sl) ("time slices proportional to the model's SLOs") holding the whole
+ * GPU; in it it runs back-to-back batches of b*_j at 100% GPU, d^L_j slots each; the GPU utilization
+ * counts its knee% over the slice ("We compute GPU utilization by using Knee% for each model").   */
+int oracle_temporal_direct(int32_t n, const int32_t *lvl, const int32_t *sl, const int64_t *dL, int32_t nslots,
+                           int64_t *slice_out, int64_t *runs_out, int64_t *occ_num) {
+  int64_t tot = 0;
+  *occ_num = 0;
+  for (int32_t j = 0; j < n; ++j) if (lvl[j] > 0) tot += sl[j];
+  for (int32_t j = 0; j < n; ++j) {
+    slice_out[j] = 0; runs_out[j] = 0;
+    if (lvl[j] <= 0 || tot == 0) continue;
+    slice_out[j] = (int64_t)nslots * sl[j] / tot;
+    runs_out[j] = dL[j] > 0 ? slice_out[j] / dL[j] : 0;
+    *occ_num += slice_out[j] * lvl[j];
+  }
+  return 0;
+}
+
+/* Static spatial sharing, GSLICE-style CSS: models keep their knee GPU% for the
+ * whole slot they run in.  When the knees do not fit together, the session is cut into K equal time slots:
+ * the lightest models that fit beside every other model stay resident in all slots ("Alexnet and
+ * Mobilenet concurrently in both time slots"), the others are packed first-fit decreasing into slots of the
+ * remaining capacity ("VGG-19 in the first time slot, and ResNet-50 in the second").  In each of its
+ * slots a model runs back-to-back batches of b*_j, dk_j slots each.  home[j] = -1 resident, else its slot. */
+int oracle_gslice_direct(int32_t n, const int32_t *lvl, const int64_t *dk, int32_t nslots, int32_t L,
+                         int32_t *home, int32_t *nbins, int64_t *runs_out, int64_t *busy_out, int64_t *occ_num) {
+  if (n < 0 || n > 1024) return -1;
+  int32_t ord[1024], na = 0;
+  for (int32_t j = 0; j < n; ++j) { home[j] = -2; runs_out[j] = 0; busy_out[j] = 0; if (lvl[j] > 0) ord[na++] = j; }
+  *occ_num = 0; *nbins = 0;
+  if (na == 0) return 0;
+  for (int32_t i = 1; i < na; ++i) {   /* ascending (level, index) */
+    int32_t v = ord[i], k = i - 1;
+    while (k >= 0 && (lvl[ord[k]] > lvl[v] || (lvl[ord[k]] == lvl[v] && ord[k] > v))) { ord[k + 1] = ord[k]; --k; }
+    ord[k + 1] = v;
+  }
+  /* residents: the longest ascending prefix P with sum_P + (largest level outside P) <= L */
+  int64_t pre = 0;
+  int32_t np = 0;
+  for (int32_t p = na; p >= 0; --p) {
+    int64_t sp = 0;
+    for (int32_t i = 0; i < p; ++i) sp += lvl[ord[i]];
+    const int64_t mx = p < na ? lvl[ord[na - 1]] : 0;
+    if (sp + mx <= L) { np = p; pre = sp; break; }
+  }
+  for (int32_t i = 0; i < np; ++i) home[ord[i]] = -1;
+  /* the rest, first-fit decreasing (level desc, index asc) into slots of capacity L - sum_P */
+  int32_t rest[1024], nr = 0;
+  for (int32_t i = np; i < na; ++i) rest[nr++] = ord[i];
+  for (int32_t i = 1; i < nr; ++i) {   /* (level desc, index asc) */
+    int32_t v = rest[i], k = i - 1;
+    while (k >= 0 && (lvl[rest[k]] < lvl[v] || (lvl[rest[k]] == lvl[v] && rest[k] > v))) { rest[k + 1] = rest[k]; --k; }
+    rest[k + 1] = v;
+  }
+  int64_t resid[1024];
+  int32_t K = 0;
+  for (int32_t i = 0; i < nr; ++i) {
+    const int32_t j = rest[i];
+    int32_t b = 0;
+    while (b < K && resid[b] < lvl[j]) ++b;   /* first fit */
+    if (b == K) resid[K++] = L - pre;
+    resid[b] -= lvl[j];
+    home[j] = b;
+  }
+  if (K == 0) K = 1;
+  *nbins = K;
+  const int64_t w = nslots / K;
+  for (int32_t j = 0; j < n; ++j) {
+    if (lvl[j] <= 0 || dk[j] <= 0) continue;
+    const int64_t nsl = home[j] == -1 ? K : 1;
+    runs_out[j] = nsl * (w / dk[j]);
+    busy_out[j] = runs_out[j] * dk[j];
+    *occ_num += busy_out[j] * lvl[j];
+  }
+  return 0;
 }
 
 /* ---------------------------------------------------------------- O6 --- */
@@ -616,6 +719,107 @@ int oracle_eval_subset(const or_problem_t *pb, const or_params_t *p, or_out_t *o
   return 0;
 }
 
+/* O9 over every scenario: the five schedulers on the same a1-a4 outputs.
+ * out[s*5 + c], c = 0 D-STACK, 1 Max-Min fair fill, 2 max-throughput fill, 3 temporal, 4 static spatial. */
+static uint64_t jain_num(const int64_t *x, int32_t n, const int32_t *act, uint64_t *den) {
+  uint64_t s1 = 0, s2 = 0, na = 0;
+  for (int32_t j = 0; j < n; ++j) if (act[j]) { s1 += (uint64_t)x[j]; s2 += (uint64_t)(x[j] * x[j]); ++na; }
+  *den = na * s2;
+  return s1 * s1;
+}
+static double jain_of(const int64_t *x, int32_t n, const int32_t *act) {
+  uint64_t den, num = jain_num(x, n, act, &den);
+  return den ? (double)num / (double)den : 0.0;   /* Jain's index (sum x)^2 / (n sum x^2) */
+}
+
+static void compare_scenario(const or_problem_t *pb, const or_params_t *p, int64_t s, double *u, double *thr,
+                             double *jain) {
+  for (int c = 0; c < 5; ++c) { u[s * 5 + c] = 0; thr[s * 5 + c] = 0; jain[s * 5 + c] = 0; }
+  const int32_t k0 = pb->scen_dnn_off[s], nd = pb->scen_dnn_off[s + 1] - k0;
+  if (nd <= 0 || nd > OR_MAX_DNN_PER_SCEN) return;
+  uint16_t dem[OR_MAX_DNN_PER_SCEN], knee[OR_MAX_DNN_PER_SCEN];
+  uint8_t bt[OR_MAX_DNN_PER_SCEN], st[OR_MAX_DNN_PER_SCEN];
+  uint32_t alloc[OR_MAX_DNN_PER_SCEN];
+  for (int32_t j = 0; j < nd; ++j) {
+    dnn_t m = get_dnn(pb, p, k0 + j);
+    batch_opt_one(&m, p, dem + j, bt + j, knee + j, st + j);
+    if (st[j] != OR_OK) dem[j] = 0;
+  }
+  oracle_wmaxmin(nd, dem, p->L, alloc);
+  int64_t T = 0;
+  for (int32_t j = 0; j < nd; ++j) if (dem[j] > 0 && pb->slo_us[k0 + j] > T) T = pb->slo_us[k0 + j];
+  if (T == 0) return;
+  const int64_t nslots = T / p->slot_us;
+  int64_t njobs = 0;
+  for (int32_t j = 0; j < nd; ++j) if (dem[j] > 0) njobs += nslots / (pb->slo_us[k0 + j] / p->slot_us);
+  if (nslots > OR_MAX_SLOTS || njobs > OR_MAX_JOBS) return;
+  int32_t g[OR_MAX_DNN_PER_SCEN], sl[OR_MAX_DNN_PER_SCEN], bst[OR_MAX_DNN_PER_SCEN], act[OR_MAX_DNN_PER_SCEN];
+  int32_t lvl[OR_MAX_DNN_PER_SCEN];
+  int64_t dtab[OR_MAX_DNN_PER_SCEN * 64], dL[OR_MAX_DNN_PER_SCEN], dk[OR_MAX_DNN_PER_SCEN];
+  for (int32_t j = 0; j < nd; ++j) {
+    const int32_t k = k0 + j;
+    g[j] = 0; lvl[j] = 0; sl[j] = pb->slo_us[k] / p->slot_us; bst[j] = bt[j]; act[j] = dem[j] > 0;
+    dL[j] = 0; dk[j] = 0;
+    if (!act[j]) continue;
+    const int32_t al = (int32_t)(alloc[j] >> 16);
+    g[j] = dem[j] > al ? dem[j] : al;
+    lvl[j] = dem[j];
+    dnn_t m = get_dnn(pb, p, k);
+    const int64_t S = S_of(p, g[j]);
+    const u128 den = (u128)S * (u128)m.M * (u128)p->slot_us;
+    for (int32_t b = p->b_min; b <= bst[j]; ++b) {
+      u128 dd = (X_of(&m, p, S, b) + den - 1) / den;
+      dtab[j * 64 + b - 1] = dd > (u128)0x7FFFFFFFFFFFLL ? 0x7FFFFFFFFFFFLL : (int64_t)dd;
+    }
+    /* run time of one b* batch at 100% GPU (temporal) and at the knee level (static spatial) */
+    const u128 denL = (u128)p->S_tot * (u128)m.M * (u128)p->slot_us;
+    dL[j] = (int64_t)((X_of(&m, p, p->S_tot, bst[j]) + denL - 1) / denL);
+    const int64_t Sk = S_of(p, dem[j]);
+    const u128 denk = (u128)Sk * (u128)m.M * (u128)p->slot_us;
+    dk[j] = (int64_t)((X_of(&m, p, Sk, bst[j]) + denk - 1) / denk);
+  }
+  const double NL = (double)nslots * (double)p->L;
+  for (int32_t c = 0; c < 3; ++c) {
+    int32_t runs[OR_MAX_DNN_PER_SCEN], jmiss[OR_MAX_DNN_PER_SCEN];
+    int64_t served[OR_MAX_DNN_PER_SCEN], busy[OR_MAX_DNN_PER_SCEN];
+    or_cyc_sum_t cs;
+    cycle_core(nd, g, sl, bst, dtab, p->b_min, p->L, (int32_t)nslots, NULL, runs, served, jmiss, &cs, 0, NULL, NULL,
+               NULL, NULL, NULL, NULL, NULL, NULL, c, busy);
+    u[s * 5 + c] = (double)cs.occ_sum / NL;
+    thr[s * 5 + c] = (double)cs.served_total * 1e6 / (double)T;
+    jain[s * 5 + c] = jain_of(busy, nd, act);
+  }
+  {
+    int64_t slice[OR_MAX_DNN_PER_SCEN], runs[OR_MAX_DNN_PER_SCEN], occn = 0, srv = 0;
+    oracle_temporal_direct(nd, lvl, sl, dL, (int32_t)nslots, slice, runs, &occn);
+    for (int32_t j = 0; j < nd; ++j) srv += runs[j] * bst[j];
+    u[s * 5 + 3] = (double)occn / NL;
+    thr[s * 5 + 3] = (double)srv * 1e6 / (double)T;
+    jain[s * 5 + 3] = jain_of(slice, nd, act);
+  }
+  {
+    int32_t home[OR_MAX_DNN_PER_SCEN], K = 0;
+    int64_t runs[OR_MAX_DNN_PER_SCEN], busy[OR_MAX_DNN_PER_SCEN], occn = 0, srv = 0;
+    oracle_gslice_direct(nd, lvl, dk, (int32_t)nslots, p->L, home, &K, runs, busy, &occn);
+    for (int32_t j = 0; j < nd; ++j) srv += runs[j] * bst[j];
+    u[s * 5 + 4] = (double)occn / NL;
+    thr[s * 5 + 4] = (double)srv * 1e6 / (double)T;
+    jain[s * 5 + 4] = jain_of(busy, nd, act);
+  }
+}
+
+int oracle_compare(const or_problem_t *pb, const or_params_t *p, double *u, double *thr, double *jain,
+                   const int64_t *idx, int64_t count, int32_t nthreads) {
+  if (!pb || !p || !u || !thr || !jain || check_params(p)) return -1;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+  const int64_t n = idx ? count : pb->num_scen;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t q = 0; q < n; ++q) compare_scenario(pb, p, idx ? idx[q] : q, u, thr, jain);
+  return 0;
+}
+
 /* ---------------------------------------------------------------- O7 --- */
 
 /* Arrival cursor of one DNN's Poisson stream (input generator, synth_core.h): index of the next arrival
@@ -724,7 +928,7 @@ static void simulate_scenario(const or_problem_t *pb, const or_params_t *p, cons
     run_t *rl = NULL;
     int64_t nrun = 0;
     cycle_core(nd, g, sl, bst, dtab, p->b_min, p->L, (int32_t)nslots, sb, runs, srv, jmiss, &cs, 0, NULL, NULL,
-               NULL, NULL, NULL, NULL, &rl, &nrun);
+               NULL, NULL, NULL, NULL, &rl, &nrun, 0, NULL);
     o->misses[s] += (uint64_t)cs.misses;
     int64_t nfill = 0;
     for (int64_t q = 0; q < nrun; ++q) nfill += rl[q].kind == 1;

@@ -82,6 +82,26 @@ int oracle_cycle_direct(int32_t n, const int32_t *g, const int32_t *sl_slots, co
                         int32_t trace_cap, int32_t *tr_dnn, int32_t *tr_start, int32_t *tr_end,
                         int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep);
 
+/* O5 with a fill order (O9 comparison schedulers): 0 D-STACK (runs so far, index), 1 Max-Min fair (g, index),
+ * 2 max-throughput (d_j(b*), index).  busy (nullable): per DNN, slots covered by its runs. */
+int oracle_cycle_direct_ex(int32_t n, const int32_t *g, const int32_t *sl, const int32_t *bstar,
+                           const int64_t *dtab, int32_t b_lo, int32_t L, int32_t nslots, const int64_t *count0,
+                           int32_t fill_order, int32_t *runs, int64_t *served, int32_t *jmiss, int64_t *busy,
+                           or_cyc_sum_t *sum, int32_t trace_cap, int32_t *tr_dnn, int32_t *tr_start, int32_t *tr_end,
+                           int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep);
+
+/* O9 temporal sharing: lvl[j] > 0 active (knee level), sl[j] SLO in slots, dL[j] run slots at 100% GPU.
+ * slice_out, runs_out per DNN; *occ_num = sum slice_j * lvl_j (utilisation numerator). */
+int oracle_temporal_direct(int32_t n, const int32_t *lvl, const int32_t *sl, const int64_t *dL, int32_t nslots,
+                           int64_t *slice_out, int64_t *runs_out, int64_t *occ_num);
+/* O9 static spatial sharing (GSLICE CSS): home[j] = -1 resident in all slots, >= 0 its slot, -2 inactive. */
+int oracle_gslice_direct(int32_t n, const int32_t *lvl, const int64_t *dk, int32_t nslots, int32_t L,
+                         int32_t *home, int32_t *nbins, int64_t *runs_out, int64_t *busy_out, int64_t *occ_num);
+/* O9 over every scenario (idx NULL) or the listed ones: out[s*5 + c], c = 0 D-STACK, 1 Max-Min fair,
+ * 2 max-throughput, 3 temporal, 4 static spatial; U, throughput (req/s), Jain fairness of GPU time. */
+int oracle_compare(const or_problem_t *pb, const or_params_t *p, double *u, double *thr, double *jain,
+                   const int64_t *idx, int64_t count, int32_t nthreads);
+
 /* O6 with direct per-DNN chains (test hook; also used internally).
  * chain_off[j]..chain_off[j+1] index executions (g_e levels, tau_e us) of DNN j's batch,
  * slo_us[j], bstar[j]; active[j] != 0.  Returns util (sum g*dt) and completed batches. */
