@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--ref-per-step", type=int, default=48, help="oracle scenarios per reference step")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="cpu_baseline time budget")
     ap.add_argument("--cycles", type=int, default=20, help="config 5: sessions simulated per step")
+    ap.add_argument("--no-compare", action="store_true", help="skip the O9 comparison-scheduler leg")
     return ap.parse_args()
 
 
@@ -281,6 +282,11 @@ def run_native(args, rank, world, local):
     value = per_gpu * world * args.steps / (ms_max / 1e3)
     agg = ds.agg_to_dict(out["agg"])
 
+    # ---- O9 comparison schedulers (dstack_compare) on this step's a3/a4 outputs, timed separately ----
+    cmp_line = None
+    if not args.no_compare:
+        cmp_line = run_compare_leg(args, ds, dp, p, out, ws, stream, per_gpu, world)
+
     # ---- e2e: the public API from pinned host buffers, H2D + compute + D2H of results each step ----
     e2e = None
     if not args.no_e2e:
@@ -330,6 +336,7 @@ def run_native(args, rank, world, local):
         "gpu_launches": launches[0],
         "clocks": clocks,
         "e2e": e2e,
+        "compare": cmp_line,
         "stats": {"mean_u": agg["sum_u"] / max(agg["n_scen_scheduled"], 1),
                   "mean_u_static": agg["sum_u_static"] / max(agg["n_scen_scheduled"], 1),
                   "scen_status": agg["n_scen_st"], "dnn_status": agg["n_st"],
@@ -342,6 +349,36 @@ def run_native(args, rank, world, local):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_compare_leg(args, ds, dp, p, out, ws, stream, per_gpu, world):
+    """SURVEY §8(f) item 2 measured: dstack_compare over the whole workload (five schedulers per scenario),
+    device-timed with CUDA events; reports the per-scheduler means that reproduce §6.3's comparisons."""
+    import torch
+    import torch.distributed as dist
+    c = ds.compare(dp, p, out["demand"], out["batch"], out["alloc_q16"], ws=ws)
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 5))
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        ds.compare(dp, p, out["demand"], out["batch"], out["alloc_q16"], out=c, ws=ws)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=stream.device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ok = c["u"][:, 0] > 0
+    means = {}
+    for i, name in enumerate(ds.CMP_NAMES):
+        means[name] = {k: float(c[k][ok, i].mean().item()) for k in ("u", "thr", "jain")}
+    d = means["dstack"]["thr"]
+    return {"api": "paper_2304_13541_b200.dstack.compare (dstack_compare)", "ms_per_call": ms,
+            "scenarios_per_s": per_gpu * world / (ms / 1e3), "gpu_launches": ds.last_launch_count(),
+            "schedulers": list(ds.CMP_NAMES), "means_over_scheduled_scenarios": means,
+            "dstack_throughput_ratio": {k: d / means[k]["thr"] for k in ds.CMP_NAMES if means[k]["thr"] > 0}}
 
 
 def run_e2e(args, sp, p, dev, world):

@@ -193,6 +193,29 @@ int dstack_simulate(const dstack_problem_t *pb, const dstack_params_t *p, const 
                     uint64_t seed, int32_t cfg_tag, int64_t scen_base, dstack_sim_out_t *out, void *ws,
                     size_t ws_bytes, void *stream);
 
+/* O9 comparison schedulers of §6.3 (readings in DESIGN.md §3.2), evaluated on the
+ * a3/a4 results (demand, batch, alloc_q16 as written by dstack_eval_batch / dstack_batch_opt +
+ * dstack_wmaxmin).  For each scenario s and scheduler c (DSTACK_CMP_*), writes
+ *   u[s*DSTACK_NCMP + c]    GPU utilisation: occupied level-slots / (nslots L)  (knee% accounting)
+ *   thr[s*DSTACK_NCMP + c]  requests served per second of session (saturating load)
+ *   jain[s*DSTACK_NCMP + c] Jain's index (sum x)^2 / (n sum x^2) of the per-model GPU time x_j (slots)
+ * c = DSTACK_CMP_DSTACK: the D-STACK session (identical to dstack_schedule_cycle's u / thr);
+ *     DSTACK_CMP_MAXMIN: same session, fill in ascending (GPU%, index) order (Max-Min fair);
+ *     DSTACK_CMP_MAXTHR: same session, fill in ascending (run time of b*, index) order (max-throughput);
+ *     DSTACK_CMP_TEMPORAL: slices proportional to SLO at 100% GPU, knee% accounting;
+ *     DSTACK_CMP_GSLICE: static spatial sharing at the knees, residents + first-fit decreasing time slots.
+ * Scenarios that are INVALID / INFEASIBLE for the D-STACK session get zeros.  All pointers are device
+ * pointers; u/thr/jain are [num_scen * DSTACK_NCMP] f64.  Workspace: dstack_workspace_size() (d_j(b) rows). */
+#define DSTACK_CMP_DSTACK 0
+#define DSTACK_CMP_MAXMIN 1
+#define DSTACK_CMP_MAXTHR 2
+#define DSTACK_CMP_TEMPORAL 3
+#define DSTACK_CMP_GSLICE 4
+#define DSTACK_NCMP 5
+int dstack_compare(const dstack_problem_t *pb, const dstack_params_t *p, const uint16_t *demand, const uint8_t *batch,
+                   const uint32_t *alloc_q16, double *u, double *thr, double *jain, void *ws, size_t ws_bytes,
+                   void *stream);
+
 /* Live per-kernel timing of dstack_eval_batch (bench accounting): after dstack_profile_start, each
  * eval_batch call on this thread records CUDA events on its stream between its kernel launches
  * (slots: 0 k_prof, 1 k_wmaxmin, 2 k_cycle, 3 k_ideal, 4 k_agg).  dstack_profile_stop synchronises

@@ -329,6 +329,28 @@ int dstack_simulate(const dstack_problem_t *pb, const dstack_params_t *p, const 
   return finish(launch_sim(m, s, &g_launches));
 }
 
+int dstack_compare(const dstack_problem_t *pb, const dstack_params_t *p, const uint16_t *demand, const uint8_t *batch,
+                   const uint32_t *alloc_q16, double *u, double *thr, double *jain, void *ws, size_t ws_bytes,
+                   void *stream) {
+  g_launches = 0;
+  if (!problem_ok(pb) || !params_ok(p)) return DSTACK_EINVAL;
+  if (pb->num_dnn > 0 && (!demand || !batch || !alloc_q16)) return DSTACK_EINVAL;
+  if (pb->num_scen > 0 && (!u || !thr || !jain)) return DSTACK_EINVAL;
+  const void *outs[] = {u, thr, jain};
+  for (const void *o : outs)
+    if (!disjoint(pb, o) || o == (const void *)demand || o == (const void *)batch || o == (const void *)alloc_q16)
+      return DSTACK_EINVAL;
+  const size_t need = dstack_workspace_size(pb, p);
+  if (ws_bytes < need || (need > 0 && !ws)) return DSTACK_EWORKSPACE;
+  if (!have_device()) return DSTACK_ELAUNCH;
+  CmpArgs c;
+  std::memset(&c, 0, sizeof(c));
+  c.pb = *pb; c.p = *p; c.demand = demand; c.batch = batch; c.alloc = alloc_q16;
+  c.dtab_rows = (uint16_t *)((char *)ws + ws_layout(pb, p).dtab);
+  c.u = u; c.thr = thr; c.jain = jain;
+  return finish(launch_compare(c, (cudaStream_t)stream, &g_launches));
+}
+
 int dstack_aggregate(const dstack_problem_t *pb, const dstack_params_t *p, dstack_out_t *out, void *ws,
                      size_t ws_bytes, void *stream) {
   g_launches = 0;

@@ -198,7 +198,9 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
                                             uint32_t bs, uint32_t sl, uint32_t rep, int32_t nslots, int32_t L,
                                             int32_t b_lo, bool hook_b_only, uint32_t &runs, uint32_t &served,
                                             uint32_t count0 = 0, uint64_t *fill_log = nullptr, uint32_t fill_cap = 0,
-                                            uint32_t *fill_n = nullptr) {
+                                            uint32_t *fill_n = nullptr, int fill_order = 0, uint32_t *busy = nullptr) {
+  // fill_order (O9 comparison schedulers): 0 D-STACK (runs so far), 1 Max-Min fair (smallest g
+  // first), 2 max-throughput (shortest d(b*) first); ties by index.  busy (nullable): this lane's run slots.
   CycRes res; res.occ_static = 0; res.occ_all = 0; res.served_tot = 0; res.misses = 0; res.oversub = false;
   for (int w = lane; (w << 2) < nslots; w += 32) reinterpret_cast<uint32_t *>(sm.occ)[w] = 0u;
   // decision-time bits: one register word per lane (word = lane) when nslots <= 1024, else shared memory
@@ -245,7 +247,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       occ_add(sm.occ, st, dj, gj, lane);
       if (lane == 0) sm.starts[offj + rj] = (uint16_t)st;
       if (st + dj < nslots) dset(st + dj);
-      if (lane == j) { runs++; served += bs; }
+      if (lane == j) { runs++; served += bs; if (busy) *busy += (uint32_t)dj; }
     } else {
       if (lane == 0) sm.starts[offj + rj] = NONE16;
       res.misses++;
@@ -321,7 +323,8 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       elig = t >= blk && !cov_static && !(fs <= t && t < fe) && occ_t + (int)g <= L;
     }
     // candidates in (runs so far, index) order; a placement raises occ[t], so re-test the rest in parallel
-    uint32_t key = elig ? ((count << 5) | (uint32_t)lane) : 0xFFFFFFFFu;
+    const uint32_t prio = fill_order == 0 ? count : (fill_order == 1 ? g : dstar);
+    uint32_t key = elig ? ((prio << 5) | (uint32_t)lane) : 0xFFFFFFFFu;
     while (true) {
       const uint32_t mk = __reduce_min_sync(FULL, key);
       if (mk == 0xFFFFFFFFu) break;
@@ -377,7 +380,10 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       if (lane == 0 && fill_log && nfill < fill_cap) fill_log[nfill] = pack_run((uint32_t)j, (uint32_t)t, (uint32_t)dsel, (uint32_t)bsel);
       nfill++;
       __syncwarp();
-      if (lane == j) { count++; runs++; served += (uint32_t)bsel; fs = t; fe = e; }
+      if (lane == j) {
+        count++; runs++; served += (uint32_t)bsel; fs = t; fe = e;
+        if (busy) *busy += (uint32_t)dsel;
+      }
       if (occ_t + (int)g > L) key = 0xFFFFFFFFu;
     }
   }

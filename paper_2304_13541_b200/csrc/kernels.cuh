@@ -82,6 +82,16 @@ struct IdealArgs {
   double *u_ideal, *thr_ideal;
 };
 
+struct CmpArgs {
+  dstack_problem_t pb;
+  dstack_params_t p;
+  const uint16_t *demand;
+  const uint8_t *batch;
+  const uint32_t *alloc;
+  uint16_t *dtab_rows;      // workspace
+  double *u, *thr, *jain;   // [num_scen * DSTACK_NCMP]
+};
+
 struct AggArgs {
   int32_t num_scen;
   const int32_t *off;
@@ -101,6 +111,7 @@ int launch_ideal(IdealArgs a, void *ws, cudaStream_t s, int *launches);
 int launch_sim(const SimArgs &a, cudaStream_t s, int *launches);
 size_t sim_fill_log_bytes();
 int launch_agg(const AggArgs &a, cudaStream_t s, int *launches);
+int launch_compare(const CmpArgs &a, cudaStream_t s, int *launches);
 size_t ideal_ws_bytes(int64_t num_rows);
 size_t agg_ws_bytes();
 

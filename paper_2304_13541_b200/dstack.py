@@ -89,6 +89,7 @@ def _load():
     lib.dstack_sim_workspace_size.restype = C.c_size_t
     lib.dstack_simulate.argtypes = [P(CProblem), P(CParams), C.c_void_p, C.c_int32, C.c_uint64, C.c_int32, C.c_int64,
                                     P(CSimOut), C.c_void_p, C.c_size_t, C.c_void_p]
+    lib.dstack_compare.argtypes = [P(CProblem), P(CParams)] + [C.c_void_p] * 7 + [C.c_size_t, C.c_void_p]
     lib.dstack_profile_start.argtypes = [C.c_int32]
     lib.dstack_profile_stop.argtypes = [C.c_void_p, C.c_void_p]
     lib.dstack_status_str.restype = C.c_char_p
@@ -101,7 +102,7 @@ _lib = _load()
 # every symbol include/dstack.h declares (checked by tests/test_abi.py)
 EXPORTS = ("dstack_workspace_size", "dstack_knee", "dstack_batch_opt", "dstack_wmaxmin", "dstack_schedule_cycle",
            "dstack_eval_batch", "dstack_aggregate", "dstack_sim_workspace_size", "dstack_simulate",
-           "dstack_profile_start", "dstack_profile_stop",
+           "dstack_compare", "dstack_profile_start", "dstack_profile_stop",
            "dstack_last_launch_count", "dstack_status_str", "dstack_version")
 
 
@@ -280,6 +281,24 @@ def eval_batch(dp: DeviceProblem, p, out=None, ws: Workspace | None = None, agg=
     _check(_lib.dstack_eval_batch(C.byref(dp.c()), C.byref(cparams(p)), C.byref(_cout(o)), ws.ptr(), ws.nbytes,
                                   _stream(dev)), "dstack_eval_batch")
     return o
+
+
+CMP_NAMES = ("dstack", "maxmin", "maxthr", "temporal", "gslice")   # DSTACK_CMP_* order
+
+
+def compare(dp: DeviceProblem, p, demand, batch, alloc_q16, out=None, ws: Workspace | None = None):
+    """dstack_compare (O9): U, throughput and Jain fairness of the five schedulers of CMP_NAMES per scenario,
+    f64 tensors [num_scen, 5], from the a3/a4 outputs (e.g. eval_batch's demand, batch, alloc_q16)."""
+    dev = dp.device
+    if out is None:
+        out = {k: torch.zeros((dp.num_scen, len(CMP_NAMES)), dtype=torch.float64, device=dev)
+               for k in ("u", "thr", "jain")}
+    if ws is None:
+        ws = Workspace(workspace_size(dp, p), dev)
+    _check(_lib.dstack_compare(C.byref(dp.c()), C.byref(cparams(p)), _ptr(demand), _ptr(batch), _ptr(alloc_q16),
+                               _ptr(out["u"]), _ptr(out["thr"]), _ptr(out["jain"]), ws.ptr(), ws.nbytes,
+                               _stream(dev)), "dstack_compare")
+    return out
 
 
 PROF_SLOTS = ("k_prof", "k_wmaxmin", "k_cycle", "k_ideal", "k_agg")

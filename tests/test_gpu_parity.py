@@ -317,3 +317,55 @@ def test_wide_smcount_parity(ds, S_tot):
     p = p.replace(L=min(255, S_tot), S_tot=S_tot, ideal=0)
     g, _ = run_gpu(ds, pb, p)
     assert_parity(g, oracle.evaluate(pb, p), ideal=False, where=f"S_tot={S_tot}")
+
+
+def run_compare(ds, pb, p):
+    dp = ds.from_host(pb, "cuda")
+    o = ds.eval_batch(dp, p)
+    c = ds.compare(dp, p, o["demand"], o["batch"], o["alloc_q16"])
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in c.items()}, ds.to_numpy(o, pb.num_scen, pb.num_dnn)
+
+
+def assert_compare_parity(g, want, where=""):
+    for k in ("u", "thr", "jain"):
+        a, b = g[k], want[k]
+        np.testing.assert_allclose(a, b, rtol=1e-6, atol=0, err_msg=f"{where} {k}")
+        assert np.array_equal(a, b), f"{where} {k}: not bit-identical"
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_compare_parity(ds, cfg):
+    """O9 comparison schedulers (dstack_compare) vs the oracle, every scheduler column, bit-identical."""
+    sp, p = synth.config(cfg, num_scen=None if cfg == 1 else 120, rows_pct=20)
+    pb = synth.generate_host(sp)
+    g, ev = run_compare(ds, pb, p)
+    want = oracle.compare(pb, p)
+    assert_compare_parity(g, want, where=f"config {cfg}")
+    ok = ev["T_us"] > 0
+    assert np.array_equal(g["u"][ok, 0], ev["u"][ok])      # the D-STACK column is the eval path's session
+
+
+def test_compare_parity_edges(ds):
+    for p in (Params(L=100, S_tot=148), Params(L=148, S_tot=148, mem_mode=2)):
+        pb = edge_problem()
+        g, _ = run_compare(ds, pb, p)
+        assert_compare_parity(g, oracle.compare(pb, p), where="edge")
+    pb = fast_path_problem(148)
+    g, _ = run_compare(ds, pb, Params(L=148, S_tot=148, mem_mode=1))
+    assert_compare_parity(g, oracle.compare(pb, Params(L=148, S_tot=148, mem_mode=1)), where="fast")
+
+
+def test_compare_config3_sampled(ds):
+    """Config 3 at full size in the bench configuration; 150 scenarios re-drawn on the host for the oracle."""
+    sp, p = synth.config(3)
+    g = synth.generate_device(sp, "cuda")
+    dp = ds.from_device_dict(g)
+    o = ds.eval_batch(dp, p)
+    c = ds.compare(dp, p, o["demand"], o["batch"], o["alloc_q16"])
+    torch.cuda.synchronize()
+    idx = np.random.default_rng(11).choice(sp.num_scen, 150, replace=False)
+    pb = synth.sample(sp, idx)
+    want = oracle.compare(pb, p)
+    got = {k: v[torch.as_tensor(idx, device=v.device)].cpu().numpy() for k, v in c.items()}
+    assert_compare_parity(got, want, where="config3 sample")
