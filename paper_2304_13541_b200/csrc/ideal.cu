@@ -6,12 +6,12 @@
 // S >= N_i), so the knee scan is a register loop over the L levels with the same exact comparison
 // as the batch search.
 //
-// k_ideal_sim (thread per scenario): event-driven preemptive schedule.  Each active DNN runs batches
-// of b* back-to-back; at every event the eligible set is each DNN's current kernel execution (chain
-// constraint of Eq. 14); the subset maximising sum g <= L (Eq. 13's per-slot maximisation, slot -> 0
-// limit) is found with a 256-bit subset-sum bitset DP over the items in priority order (batch
-// deadline, index), and the lexicographically-first optimal subset is read back from the suffix
-// reachability sets.  Selected executions progress to the first completion.
+// k_ideal_sim (warp per scenario, lane per DNN): event-driven preemptive schedule.  Each active DNN runs
+// batches of b* back-to-back; at every event the eligible set is each DNN's current kernel execution
+// (chain constraint of Eq. 14); the subset maximising sum g <= L (Eq. 13's per-slot maximisation, slot -> 0
+// limit) is found with a 256-bit subset-sum DP over the items in priority order (batch deadline, index),
+// and the lexicographically-first optimal subset is read back from the suffix reachability sets.
+// Selected executions progress to the first completion.
 #include "kernels.cuh"
 
 namespace dstack {
@@ -53,132 +53,144 @@ __global__ void __launch_bounds__(256) k_ideal_rows(IdealArgs a) {
   }
 }
 
-struct Bits256 { uint64_t w[4]; };
+// k_ideal_sim: one warp per scenario, lane j = DNN j.  Per event the subset-sum DP runs over the live
+// executions in priority order with the 256 capacities distributed over the lanes (lane c holds capacities
+// c, c+32, ..., c+224 as an 8-bit mask): adding an item of weight g = 32a + b is one shuffle from lane c-b and
+// a shift by a (or a+1 across the wrap), so each item costs a handful of instructions.  The suffix sets stay
+// in shared memory for the lexicographic read-back.  Each lane keeps its chain position in registers and
+// prefetches its next row, so a completion does not wait on global memory.
+constexpr int IDEAL_WARPS = 8;
 
-__device__ __forceinline__ Bits256 shl_or(const Bits256 &x, int g, int L) {
-  // x | (x << g), truncated to bits 0..L
-  Bits256 y;
-  const int ws = g >> 6, bs = g & 63;
-#pragma unroll
-  for (int i = 3; i >= 0; --i) {
-    uint64_t v = 0;
-    const int src = i - ws;
-    if (src >= 0) {
-      v = x.w[src] << bs;
-      if (bs && src - 1 >= 0) v |= x.w[src - 1] >> (64 - bs);
-    }
-    y.w[i] = x.w[i] | v;
-  }
-  // truncate above L
-  const int lw = L >> 6, lb = L & 63;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (i > lw) y.w[i] = 0;
-    else if (i == lw && lb < 63) y.w[i] &= (2ull << lb) - 1ull;
-  }
-  return y;
+struct IdealRow {
+  int64_t i;      // absolute row index (r1 = end of chain)
+  uint32_t R, tau, g;
+};
+
+__device__ __forceinline__ IdealRow ideal_row_at(const IdealArgs &a, int64_t i, int64_t r1) {
+  IdealRow w;
+  while (i < r1 && a.ex_tau[i] == 0) ++i;    // zero-duration rows complete instantly
+  w.i = i;
+  w.R = 0; w.tau = 0; w.g = 0;
+  if (i < r1) { w.R = a.pb.r[i]; w.tau = a.ex_tau[i]; w.g = a.ex_g[i]; }
+  return w;
 }
 
-__device__ __forceinline__ bool bit_at(const Bits256 &x, int s) { return (x.w[s >> 6] >> (s & 63)) & 1ull; }
-
-__global__ void __launch_bounds__(128) k_ideal_sim(IdealArgs a) {
+__global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
+  __shared__ uint8_t reach_all[IDEAL_WARPS][DSTACK_MAX_DNN_PER_SCEN + 1][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t(*reach)[32] = reach_all[warp];
   const int32_t L = a.p.L, slot = a.p.slot_us;
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.pb.num_scen;
-       s += (int64_t)gridDim.x * blockDim.x) {
+  uint32_t capmask = 0;   // bits k with capacity lane + 32 k <= L
+  for (int k = 0; k < 8; ++k)
+    if (lane + 32 * k <= L) capmask |= 1u << k;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < a.pb.num_scen; s += nwarps) {
     const int32_t k0 = a.pb.scen_dnn_off[s], nd = a.pb.scen_dnn_off[s + 1] - k0;
     double ui = 0.0, ti = 0.0;
-    bool run = nd >= 1 && nd <= DSTACK_MAX_DNN_PER_SCEN;
-    uint32_t T = 0;
-    if (run) {
-      uint32_t njobs = 0;
-      for (int j = 0; j < nd; ++j)
-        if (a.demand[k0 + j] > 0 && (uint32_t)a.pb.slo_us[k0 + j] > T) T = (uint32_t)a.pb.slo_us[k0 + j];
-      if (T == 0) run = false;
-      else {
-        const uint32_t nslots = T / (uint32_t)slot;
-        for (int j = 0; j < nd; ++j)
-          if (a.demand[k0 + j] > 0) njobs += nslots / ((uint32_t)a.pb.slo_us[k0 + j] / (uint32_t)slot);
-        if (nslots > DSTACK_MAX_SLOTS || njobs > DSTACK_MAX_JOBS) run = false;
-      }
+    const bool mine = lane < nd && nd <= DSTACK_MAX_DNN_PER_SCEN;
+    const int k = k0 + lane;
+    const bool act = mine && a.demand[k] > 0;
+    const uint32_t slo = mine ? (uint32_t)a.pb.slo_us[k] : 0u;
+    uint32_t T = nd > DSTACK_MAX_DNN_PER_SCEN ? 0u : __reduce_max_sync(FULL, act ? slo : 0u);
+    if (T > 0) {
+      const uint32_t nslots = T / (uint32_t)slot;
+      const uint32_t njobs = __reduce_add_sync(FULL, act ? nslots / (slo / (uint32_t)slot) : 0u);
+      if (nslots > DSTACK_MAX_SLOTS || njobs > DSTACK_MAX_JOBS) T = 0;
     }
-    if (run) {
-      int64_t rowpos[DSTACK_MAX_DNN_PER_SCEN];   // current row (absolute index)
-      uint32_t rep[DSTACK_MAX_DNN_PER_SCEN];     // executions of the current row done
-      uint64_t rem[DSTACK_MAX_DNN_PER_SCEN];
-      uint32_t dline[DSTACK_MAX_DNN_PER_SCEN];   // batch start + SLO
-      uint32_t comp[DSTACK_MAX_DNN_PER_SCEN];
-      uint8_t ord[DSTACK_MAX_DNN_PER_SCEN];
-      Bits256 reach[DSTACK_MAX_DNN_PER_SCEN + 1];
-      int no = 0;
-      for (int j = 0; j < nd; ++j) {
-        comp[j] = 0;
-        const int k = k0 + j;
-        if (a.demand[k] == 0) continue;
-        const int64_t r0 = a.pb.dnn_row_off[k], r1 = a.pb.dnn_row_off[k + 1];
-        int64_t i = r0;
-        while (i < r1 && a.ex_tau[i] == 0) ++i;
-        if (i >= r1) continue;                 // all-zero chain: never runs
-        rowpos[j] = i; rep[j] = 0; rem[j] = a.ex_tau[i];
-        dline[j] = (uint32_t)a.pb.slo_us[k];
-        ord[no++] = (uint8_t)j;
+    if (T > 0) {
+      int64_t r0 = 0, r1 = 0;
+      IdealRow first, cur, nxt;
+      first.i = cur.i = nxt.i = 0; first.R = cur.R = nxt.R = 0; first.tau = cur.tau = nxt.tau = 0;
+      first.g = cur.g = nxt.g = 0;
+      bool live = false;
+      if (act) {
+        r0 = a.pb.dnn_row_off[k]; r1 = a.pb.dnn_row_off[k + 1];
+        first = ideal_row_at(a, r0, r1);
+        live = first.i < r1;                  // an all-zero chain never runs
+        cur = first;
+        if (live) nxt = ideal_row_at(a, cur.i + 1, r1);
       }
+      uint32_t rp = 0, rem = cur.tau, dl = slo, comp = 0, rank = 0;
+      const uint32_t n = (uint32_t)__popc(__ballot_sync(FULL, live));
+      bool dirty = true;
       uint64_t util = 0, t = 0;
-      while (no > 0 && t < T) {
-        // priority order: (deadline, index) -- insertion sort (nearly sorted between events)
-        for (int q = 1; q < no; ++q) {
-          const uint8_t v = ord[q];
-          int p = q - 1;
-          while (p >= 0 && (dline[ord[p]] > dline[v] || (dline[ord[p]] == dline[v] && ord[p] > v))) {
-            ord[p + 1] = ord[p]; --p;
+      while (n > 0 && t < T) {
+        if (dirty) {   // priority rank among the live DNNs: (batch deadline, index)
+          const uint64_t key = ((uint64_t)dl << 5) | (uint32_t)lane;
+          rank = 0;
+          for (int q = 0; q < 32; ++q) {
+            const uint64_t kq = shfl_u64(key, q);
+            const bool lq = __shfl_sync(FULL, (int)live, q) != 0;
+            if (lq && kq < key) ++rank;
           }
-          ord[p + 1] = v;
+          dirty = false;
         }
-        reach[no].w[0] = 1; reach[no].w[1] = reach[no].w[2] = reach[no].w[3] = 0;
-        for (int q = no - 1; q >= 0; --q) reach[q] = shl_or(reach[q + 1], a.ex_g[rowpos[ord[q]]], L);
-        int target = L;
-        while (target > 0 && !bit_at(reach[0], target)) --target;
-        const uint64_t gsum = (uint64_t)target;
-        uint64_t dt = ~0ull;
-        uint32_t selmask = 0;
-        for (int q = 0; q < no; ++q) {
-          const int j = ord[q];
-          const int gk = a.ex_g[rowpos[j]];
-          if (gk <= target && bit_at(reach[q + 1], target - gk)) {
-            selmask |= 1u << j; target -= gk;
-            if (rem[j] < dt) dt = rem[j];
+        // suffix reachability: reach[q] = subset sums of the items of rank >= q
+        uint32_t m = lane == 0 ? 1u : 0u;
+        reach[n][lane] = (uint8_t)m;
+        for (int q = (int)n - 1; q >= 0; --q) {
+          const int own = __ffs(__ballot_sync(FULL, live && rank == (uint32_t)q)) - 1;
+          const uint32_t gq = __shfl_sync(FULL, cur.g, own);
+          const uint32_t sa = gq >> 5, sb = gq & 31u;
+          const uint32_t v = __shfl_sync(FULL, m, (lane - (int)sb) & 31);
+          m |= (v << ((uint32_t)lane >= sb ? sa : sa + 1u)) & 0xFFu;
+          reach[q][lane] = (uint8_t)m;
+        }
+        // largest achievable sum <= L
+        const uint32_t mm = m & capmask;
+        const uint32_t top = mm ? (uint32_t)lane + 32u * (31u - __clz(mm)) + 1u : 0u;
+        int target = (int)__reduce_max_sync(FULL, top) - 1;
+        const uint64_t gsum = (uint64_t)(target > 0 ? target : 0);
+        __syncwarp();
+        // lexicographic read-back in priority order: include an item iff the rest can still complete target
+        bool sel = false;
+        for (uint32_t q = 0; q < n; ++q) {
+          const int own = __ffs(__ballot_sync(FULL, live && rank == q)) - 1;
+          const int gq = (int)__shfl_sync(FULL, cur.g, own);
+          if (gq <= target) {
+            const int c = target - gq;
+            if ((reach[q + 1][c & 31] >> (c >> 5)) & 1u) {
+              if (lane == own) sel = true;
+              target -= gq;
+            }
           }
         }
-        if (selmask == 0 || dt == 0) break;
-        if (dt > (uint64_t)T - t) dt = (uint64_t)T - t;
+        uint32_t dt = __reduce_min_sync(FULL, sel ? rem : 0xFFFFFFFFu);
+        if (!__any_sync(FULL, sel) || dt == 0) break;
+        if ((uint64_t)dt > (uint64_t)T - t) dt = (uint32_t)((uint64_t)T - t);
         util += gsum * dt;
         t += dt;
-        for (int q = 0; q < no; ++q) {
-          const int j = ord[q];
-          if (!((selmask >> j) & 1u)) continue;
-          rem[j] -= dt;
-          if (rem[j] > 0) continue;
-          const int k = k0 + j;
-          const int64_t r0 = a.pb.dnn_row_off[k], r1 = a.pb.dnn_row_off[k + 1];
-          int64_t i = rowpos[j];
-          uint32_t rp = rep[j] + 1;
-          if (rp >= a.pb.r[i]) { rp = 0; ++i; while (i < r1 && a.ex_tau[i] == 0) ++i; }
-          if (i >= r1) {                       // batch complete: next batch back-to-back
-            comp[j]++;
-            dline[j] = (uint32_t)t + (uint32_t)a.pb.slo_us[k];
-            i = r0;
-            while (a.ex_tau[i] == 0) ++i;
-            rp = 0;
+        bool done_batch = false;
+        if (sel) {
+          rem -= dt;
+          if (rem == 0) {   // next execution of the chain
+            if (++rp >= cur.R) {
+              rp = 0;
+              if (nxt.i >= r1) {              // batch complete: next batch back-to-back
+                comp++;
+                dl = (uint32_t)t + slo;
+                done_batch = true;
+                cur = first;
+              } else {
+                cur = nxt;
+              }
+              nxt = ideal_row_at(a, cur.i + 1, r1);
+            }
+            rem = cur.tau;
           }
-          rowpos[j] = i; rep[j] = rp; rem[j] = a.ex_tau[i];
         }
+        dirty = __any_sync(FULL, done_batch);
+        __syncwarp();
       }
-      uint64_t bsum = 0;
-      for (int j = 0; j < nd; ++j) bsum += (uint64_t)comp[j] * a.batch[k0 + j];
+      const uint64_t bsum = warp_sum_u64(act ? (uint64_t)comp * a.batch[k] : 0ull);
       ui = (double)util / ((double)L * (double)T);
       ti = (double)bsum * 1e6 / (double)T;
     }
-    if (a.u_ideal) a.u_ideal[s] = ui;
-    if (a.thr_ideal) a.thr_ideal[s] = ti;
+    if (lane == 0) {
+      if (a.u_ideal) a.u_ideal[s] = ui;
+      if (a.thr_ideal) a.thr_ideal[s] = ti;
+    }
+    __syncwarp();
   }
 }
 
@@ -199,9 +211,9 @@ int launch_ideal(IdealArgs a, void *ws, cudaStream_t s, int *launches) {
     k_ideal_rows<<<(unsigned)blocks, 256, 0, s>>>(a);
     ++*launches;
   }
-  int64_t blocks = (a.pb.num_scen + 127) / 128;
-  if (blocks > 148 * 64) blocks = 148 * 64;
-  k_ideal_sim<<<(unsigned)blocks, 128, 0, s>>>(a);
+  int64_t blocks = (a.pb.num_scen + IDEAL_WARPS - 1) / IDEAL_WARPS;
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  k_ideal_sim<<<(unsigned)blocks, IDEAL_WARPS * 32, 0, s>>>(a);
   ++*launches;
   return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;
 }
