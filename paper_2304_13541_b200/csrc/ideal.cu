@@ -77,8 +77,10 @@ __device__ __forceinline__ IdealRow ideal_row_at(const IdealArgs &a, int64_t i, 
 
 __global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
   __shared__ uint8_t reach_all[IDEAL_WARPS][DSTACK_MAX_DNN_PER_SCEN + 1][32];
+  __shared__ uint8_t grank_all[IDEAL_WARPS][32];   // g of the live item of each priority rank
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t(*reach)[32] = reach_all[warp];
+  uint8_t *grank = grank_all[warp];
   const int32_t L = a.p.L, slot = a.p.slot_us;
   uint32_t capmask = 0;   // bits k with capacity lane + 32 k <= L
   for (int k = 0; k < 8; ++k)
@@ -125,33 +127,70 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
           }
           dirty = false;
         }
-        // suffix reachability: reach[q] = subset sums of the items of rank >= q
-        uint32_t m = lane == 0 ? 1u : 0u;
-        reach[n][lane] = (uint8_t)m;
-        for (int q = (int)n - 1; q >= 0; --q) {
-          const int own = __ffs(__ballot_sync(FULL, live && rank == (uint32_t)q)) - 1;
-          const uint32_t gq = __shfl_sync(FULL, cur.g, own);
-          const uint32_t sa = gq >> 5, sb = gq & 31u;
-          const uint32_t v = __shfl_sync(FULL, m, (lane - (int)sb) & 31);
-          m |= (v << ((uint32_t)lane >= sb ? sa : sa + 1u)) & 0xFFu;
-          reach[q][lane] = (uint8_t)m;
-        }
-        // largest achievable sum <= L
-        const uint32_t mm = m & capmask;
-        const uint32_t top = mm ? (uint32_t)lane + 32u * (31u - __clz(mm)) + 1u : 0u;
-        int target = (int)__reduce_max_sync(FULL, top) - 1;
-        const uint64_t gsum = (uint64_t)(target > 0 ? target : 0);
-        __syncwarp();
-        // lexicographic read-back in priority order: include an item iff the rest can still complete target
         bool sel = false;
-        for (uint32_t q = 0; q < n; ++q) {
-          const int own = __ffs(__ballot_sync(FULL, live && rank == q)) - 1;
-          const int gq = (int)__shfl_sync(FULL, cur.g, own);
-          if (gq <= target) {
-            const int c = target - gq;
-            if ((reach[q + 1][c & 31] >> (c >> 5)) & 1u) {
-              if (lane == own) sel = true;
-              target -= gq;
+        uint64_t gsum = 0;
+        if (n <= 10) {
+          // <= 1024 subsets: enumerate them all (8 per lane per round, 2^(n-8) rounds).  Subset index bit p <->
+          // the item of rank n-1-p, so the largest index among the max-sum subsets is the lexicographically-
+          // first (priority order) optimal subset -- the one the read-back below selects -- and one
+          // max-reduction over (sum, index) decides.
+          if (live) grank[rank] = (uint8_t)cur.g;
+          __syncwarp();
+          uint32_t gp[10];
+#pragma unroll
+          for (int p = 0; p < 10; ++p) gp[p] = p < (int)n ? grank[n - 1 - p] : 0u;
+          uint32_t lbase = 0;
+#pragma unroll
+          for (int p = 3; p < 8; ++p)
+            if ((lane >> (p - 3)) & 1) lbase += gp[p];
+          uint32_t best = 0;
+          const uint32_t nsub = 1u << n;
+          auto scan8 = [&](uint32_t base, uint32_t r) {
+#pragma unroll
+            for (int lo = 0; lo < 8; ++lo) {
+              const uint32_t idx = (r << 8) | ((uint32_t)lane << 3) | (uint32_t)lo;
+              const uint32_t sum = base + ((lo & 1) ? gp[0] : 0u) + ((lo & 2) ? gp[1] : 0u) + ((lo & 4) ? gp[2] : 0u);
+              const uint32_t key = (sum << 10) | idx;
+              if (idx < nsub && sum <= (uint32_t)L && key > best) best = key;
+            }
+          };
+          if (n <= 8) {
+            scan8(lbase, 0u);
+          } else {
+            for (uint32_t r = 0; r < (1u << (n - 8)); ++r)
+              scan8(lbase + ((r & 1u) ? gp[8] : 0u) + ((r & 2u) ? gp[9] : 0u), r);
+          }
+          best = __reduce_max_sync(FULL, best);   // the empty subset (key 0) is always feasible
+          gsum = best >> 10;
+          sel = live && ((best >> (n - 1 - rank)) & 1u);
+        } else {
+          // suffix reachability: reach[q] = subset sums of the items of rank >= q
+          uint32_t m = lane == 0 ? 1u : 0u;
+          reach[n][lane] = (uint8_t)m;
+          for (int q = (int)n - 1; q >= 0; --q) {
+            const int own = __ffs(__ballot_sync(FULL, live && rank == (uint32_t)q)) - 1;
+            const uint32_t gq = __shfl_sync(FULL, cur.g, own);
+            const uint32_t sa = gq >> 5, sb = gq & 31u;
+            const uint32_t v = __shfl_sync(FULL, m, (lane - (int)sb) & 31);
+            m |= (v << ((uint32_t)lane >= sb ? sa : sa + 1u)) & 0xFFu;
+            reach[q][lane] = (uint8_t)m;
+          }
+          // largest achievable sum <= L
+          const uint32_t mm = m & capmask;
+          const uint32_t top = mm ? (uint32_t)lane + 32u * (31u - __clz(mm)) + 1u : 0u;
+          int target = (int)__reduce_max_sync(FULL, top) - 1;
+          gsum = (uint64_t)(target > 0 ? target : 0);
+          __syncwarp();
+          // lexicographic read-back in priority order: include an item iff the rest can still complete target
+          for (uint32_t q = 0; q < n; ++q) {
+            const int own = __ffs(__ballot_sync(FULL, live && rank == q)) - 1;
+            const int gq = (int)__shfl_sync(FULL, cur.g, own);
+            if (gq <= target) {
+              const int c = target - gq;
+              if ((reach[q + 1][c & 31] >> (c >> 5)) & 1u) {
+                if (lane == own) sel = true;
+                target -= gq;
+              }
             }
           }
         }
