@@ -1,0 +1,78 @@
+"""Parity at BASELINE.json's full sizes (configs 2, 4, 5), in the launch configuration bench.py uses:
+the whole workload is generated on the device and evaluated through the C-ABI in one call, and a
+stratified sample of scenarios is re-drawn on the host (byte-identical, tests/test_gpu_parity.py
+::test_device_generator_matches_host) and computed one by one by the oracle.
+
+Config 3's full-size check is test_gpu_parity.py::test_config3_fullsize_sampled_parity.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from tests.test_gpu_parity import assert_parity  # noqa: E402
+
+PER_DNN = ("demand", "batch", "knee", "status", "alloc_q16", "level", "runs", "served")
+
+
+@pytest.fixture(scope="module")
+def ds():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2304_13541_b200 import dstack
+    return dstack
+
+
+def sampled_outputs(o, off, idx):
+    """Per-scenario / per-DNN device outputs of the scenarios idx, packed like the oracle's arrays for
+    synth.sample(spec, idx)."""
+    out = {}
+    dnn_idx = np.concatenate([np.arange(off[s], off[s + 1]) for s in idx]).astype(np.int64)
+    for k, v in o.items():
+        if k == "agg":
+            continue
+        sel = dnn_idx if k in PER_DNN else np.asarray(idx, np.int64)
+        a = v[torch.as_tensor(sel, device=v.device)].cpu().numpy()
+        out[k] = a.view(np.uint16) if a.dtype == np.int16 else (a.view(np.uint32) if a.dtype == np.int32 else a)
+    return out
+
+
+@pytest.mark.parametrize("cfg,stride", [(2, 10), (4, 250)])
+def test_fullsize_sampled_parity(ds, cfg, stride):
+    """Config 2 (10k scenarios, L = 100, ideal on) every 10th scenario; config 4 (100k oversubscribed
+    scenarios, ideal on) every 250th: every a1-a6 output bit-exact."""
+    sp, p = synth.config(cfg)
+    g = synth.generate_device(sp, "cuda")
+    dp = ds.from_device_dict(g)
+    o = ds.eval_batch(dp, p)
+    torch.cuda.synchronize()
+    off = g["scen_dnn_off"].cpu().numpy()
+    idx = np.arange(0, sp.num_scen, stride)
+    want = oracle.evaluate(synth.sample(sp, idx), p)
+    assert_parity(sampled_outputs(o, off, idx), want, where=f"config {cfg} full size")
+    if cfg == 4:   # the oversubscribed configuration really is oversubscribed (R20)
+        assert (want["scen_status"] == oracle.OVERSUBSCRIBED).mean() > 0.5
+
+
+def test_config5_fullsize_sampled_parity(ds):
+    """Config 5 at full size: 100k scenarios x 1000 sessions through dstack_simulate (one call, the
+    persistent k_sim grid); 40 scenarios simulated by the oracle's O7, each at its global index."""
+    sp, p = synth.config(5)
+    cycles = 1000
+    g = synth.generate_device(sp, "cuda")
+    dp = ds.from_device_dict(g)
+    r = ds.simulate(dp, p, cycles, sp.seed, sp.cfg_tag)
+    torch.cuda.synchronize()
+    idx = np.arange(0, sp.num_scen, 2500)
+    for s in idx:
+        pb = synth.generate_host(sp.replace(scen_base=int(s), num_scen=1))
+        want = oracle.simulate(pb, p, cycles, sp.seed, sp.cfg_tag, scen_base=int(s))
+        for k, v in want.items():
+            got = int(r[k][int(s)].item())
+            assert got == int(v[0]), (s, k, got, int(v[0]))
+    arrived = r["arrived"].cpu().numpy()
+    kept = (r["in_slo"] + r["late"] + r["unserved"]).cpu().numpy()
+    assert np.array_equal(arrived, kept)   # conservation over all 100k scenarios
