@@ -35,18 +35,19 @@ class OrProblem(C.Structure):
 
 class OrParams(C.Structure):
     _fields_ = [(k, C.c_int32) for k in
-                ("L", "S_tot", "slot_us", "mem_mode", "margin", "par_mode", "wse_mode", "b_min", "b_max", "ideal")]
+                ("L", "S_tot", "slot_us", "mem_mode", "margin", "par_mode", "wse_mode", "b_min", "b_max", "ideal",
+                 "below_knee", "reconf_us")]
 
 
 class OrOut(C.Structure):
     _fields_ = [(k, C.c_void_p) for k in
                 ("demand", "batch", "knee", "status", "alloc_q16", "level", "runs", "served",
-                 "scen_status", "T_us", "u_static", "u", "thr", "misses", "u_ideal", "thr_ideal")]
+                 "scen_status", "T_us", "u_static", "u", "thr", "misses", "u_ideal", "thr_ideal", "below")]
 
 
 class OrCycSum(C.Structure):
     _fields_ = [("occ_static_sum", C.c_int64), ("occ_sum", C.c_int64), ("served_total", C.c_int64),
-                ("misses", C.c_int32), ("status", C.c_int32), ("trace_n", C.c_int32)]
+                ("misses", C.c_int32), ("status", C.c_int32), ("trace_n", C.c_int32), ("below", C.c_int32)]
 
 
 class OrSimOut(C.Structure):
@@ -74,6 +75,8 @@ def lib():
         L.oracle_cycle_direct_ex.argtypes = ([C.c_int32] + [C.c_void_p] * 4 + [C.c_int32] * 3 + [C.c_void_p]
                                              + [C.c_int32] + [C.c_void_p] * 4 + [P(OrCycSum), C.c_int32]
                                              + [C.c_void_p] * 6)
+        L.oracle_cycle_direct_bk.argtypes = ([C.c_int32] + [C.c_void_p] * 5 + [C.c_int32] * 3 + [C.c_void_p] * 3
+                                             + [P(OrCycSum), C.c_int32] + [C.c_void_p] * 7)
         L.oracle_temporal_direct.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32] + [C.c_void_p] * 3
         L.oracle_gslice_direct.argtypes = ([C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]
                                            + [C.c_void_p] * 5)
@@ -100,7 +103,7 @@ def _problem(pb: Problem) -> OrProblem:
 
 def _params(p: Params) -> OrParams:
     return OrParams(p.L, p.S_tot, p.slot_us, p.mem_mode, p.margin, p.par_mode, p.wse_mode, p.b_min, p.b_max,
-                    p.ideal)
+                    p.ideal, p.below_knee, p.reconf_us)
 
 
 def X(pb: Problem, p: Params, dnn: int, l: int, b: int) -> int:
@@ -159,6 +162,34 @@ def cycle_direct(g, sl_slots, bstar, dtab, b_lo: int, L: int, nslots: int, trace
     trace = dict(dnn=tr[0][:k], start=tr[1][:k], end=tr[2][:k], batch=tr[3][:k], kind=tr[4][:k], rep=tr[5][:k])
     return dict(occ_static_sum=s.occ_static_sum, occ_sum=s.occ_sum, served_total=s.served_total,
                 misses=s.misses, status=s.status, runs=runs, served=served, jmiss=jm, trace=trace, busy=busy,
+                u_static=s.occ_static_sum / (nslots * L) if nslots else 0.0,
+                u=s.occ_sum / (nslots * L) if nslots else 0.0)
+
+
+def cycle_direct_bk(g, sl_slots, bstar, dtab, dlow, b_lo: int, L: int, nslots: int, trace_cap: int = 4096):
+    """O5 + F1 below-knee fallback. dlow: array [n, 256], dlow[j, l] = run slots of j's b*
+    batch at level l < g_j including the launch latency (0 = unusable). Trace kind 2 = below-knee static run,
+    trace level = the run's GPU% level."""
+    g = np.ascontiguousarray(g, np.int32); sl = np.ascontiguousarray(sl_slots, np.int32)
+    bs = np.ascontiguousarray(bstar, np.int32)
+    n = g.shape[0]
+    dt = np.zeros((n, 64), np.int64)
+    dtab = np.asarray(dtab, np.int64)
+    dt[:, : dtab.shape[1]] = dtab
+    dl = np.zeros((n, 256), np.int64)
+    dlow = np.asarray(dlow, np.int64)
+    dl[:, : dlow.shape[1]] = dlow
+    runs = np.zeros(n, np.int32); served = np.zeros(n, np.int64); jm = np.zeros(n, np.int32)
+    s = OrCycSum()
+    tr = [np.zeros(trace_cap, np.int32) for _ in range(7)]
+    rc = lib().oracle_cycle_direct_bk(n, _p(g), _p(sl), _p(bs), _p(dt), _p(dl), b_lo, L, nslots, _p(runs),
+                                      _p(served), _p(jm), C.byref(s), trace_cap, *[_p(t) for t in tr])
+    assert rc == 0
+    k = s.trace_n
+    trace = dict(dnn=tr[0][:k], start=tr[1][:k], end=tr[2][:k], batch=tr[3][:k], kind=tr[4][:k], rep=tr[5][:k],
+                 level=tr[6][:k])
+    return dict(occ_static_sum=s.occ_static_sum, occ_sum=s.occ_sum, served_total=s.served_total,
+                misses=s.misses, status=s.status, below=s.below, runs=runs, served=served, jmiss=jm, trace=trace,
                 u_static=s.occ_static_sum / (nslots * L) if nslots else 0.0,
                 u=s.occ_sum / (nslots * L) if nslots else 0.0)
 
@@ -236,7 +267,7 @@ def out_arrays(num_scen: int, num_dnn: int):
                 runs=np.zeros(D, np.uint16), served=np.zeros(D, np.uint32),
                 scen_status=np.zeros(S, np.uint8), T_us=np.zeros(S, np.uint32), u_static=np.zeros(S, np.float64),
                 u=np.zeros(S, np.float64), thr=np.zeros(S, np.float64), misses=np.zeros(S, np.uint32),
-                u_ideal=np.zeros(S, np.float64), thr_ideal=np.zeros(S, np.float64))
+                u_ideal=np.zeros(S, np.float64), thr_ideal=np.zeros(S, np.float64), below=np.zeros(S, np.uint32))
 
 
 def evaluate(pb: Problem, p: Params, nthreads: int = 0, subset=None):

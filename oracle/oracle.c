@@ -232,7 +232,7 @@ static int job_cmp(const void *a, const void *b) {
   return x->r < y->r ? -1 : (x->r > y->r);
 }
 
-typedef struct { int32_t j, start, end, batch, kind, rep; } run_t;
+typedef struct { int32_t j, start, end, batch, kind, rep, level; } run_t;
 
 /* occ[u] + g <= L for all u in [s, s+d)  (Eq. 14 `eq:constraints`: G_ui <= 100%) */
 static int fits(const int32_t *occ, int32_t s, int64_t d, int32_t g, int32_t L) {
@@ -255,7 +255,7 @@ static int cycle_core(int32_t n, const int32_t *g, const int32_t *sl, const int3
                       int32_t *runs, int64_t *served, int32_t *jmiss, or_cyc_sum_t *sum,
                       int32_t trace_cap, int32_t *tr_dnn, int32_t *tr_start, int32_t *tr_end,
                       int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep, run_t **runs_out, int64_t *nrun_out,
-                      int32_t fill_order, int64_t *busy) {
+                      int32_t fill_order, int64_t *busy, const int64_t *dlow, int32_t *tr_level) {
   if (n < 0 || n > 1024 || nslots < 0 || nslots > (1 << 20)) return -1;
   int32_t *occ = (int32_t *)calloc((size_t)nslots + 1, sizeof(int32_t));
   uint8_t *decide = (uint8_t *)calloc((size_t)nslots + 1, 1);
@@ -299,10 +299,30 @@ static int cycle_core(int32_t n, const int32_t *g, const int32_t *sl, const int3
           if (fits(occ, s, d, g[j], L)) { s_found = s; break; }
       }
     }
+    int32_t lv = g[j];
+    int64_t dd = d;
+    if (s_found < 0 && dlow) {
+      /* F1 ("schedule a model with GPU% lower than its Knee, albeit with high inference latency
+         when necessary", including "the additional latency of launching a new DNN model at lower GPU%"):
+         levels g_j - 1 down to 1, the first one with a feasible start in the window, same start rule. */
+      for (int32_t l = g[j] - 1; l >= 1 && s_found < 0; --l) {
+        const int64_t dl_ = dlow[(int64_t)j * 256 + l];
+        if (dl_ <= 0 || dl_ > dl - rel) continue;
+        if (r % 2 == 0) {
+          for (int32_t s = rel; s + dl_ <= dl; ++s)
+            if (fits(occ, s, dl_, l, L)) { s_found = s; break; }
+        } else {
+          for (int32_t s = (int32_t)(dl - dl_); s >= rel; --s)
+            if (fits(occ, s, dl_, l, L)) { s_found = s; break; }
+        }
+        if (s_found >= 0) { lv = l; dd = dl_; }
+      }
+    }
     if (s_found < 0) { jmiss[j]++; sum->misses++; sum->status = OR_OVERSUBSCRIBED; continue; }
-    for (int64_t u = s_found; u < s_found + d; ++u) occ[u] += g[j];
-    rl[nrun].j = j; rl[nrun].start = s_found; rl[nrun].end = (int32_t)(s_found + d);
-    rl[nrun].batch = bstar[j]; rl[nrun].kind = 0; rl[nrun].rep = r; ++nrun;
+    for (int64_t u = s_found; u < s_found + dd; ++u) occ[u] += lv;
+    rl[nrun].j = j; rl[nrun].start = s_found; rl[nrun].end = (int32_t)(s_found + dd);
+    rl[nrun].batch = bstar[j]; rl[nrun].kind = lv == g[j] ? 0 : 2; rl[nrun].rep = r; rl[nrun].level = lv; ++nrun;
+    if (lv != g[j]) sum->below++;
     runs[j]++; served[j] += bstar[j]; count[j]++;
   }
   for (int32_t u = 0; u < nslots; ++u) sum->occ_static_sum += occ[u];
@@ -350,7 +370,7 @@ static int cycle_core(int32_t n, const int32_t *g, const int32_t *sl, const int3
       const int64_t d = dtab[(int64_t)j * 64 + b - 1];   /* Run-Batch(model, batch) */
       for (int64_t u = t; u < t + d; ++u) occ[u] += g[j];
       rl[nrun].j = j; rl[nrun].start = t; rl[nrun].end = (int32_t)(t + d);
-      rl[nrun].batch = b; rl[nrun].kind = 1; rl[nrun].rep = -1; ++nrun;
+      rl[nrun].batch = b; rl[nrun].kind = 1; rl[nrun].rep = -1; rl[nrun].level = g[j]; ++nrun;
       runs[j]++; served[j] += b; count[j]++;
       if (t + d < nslots) decide[t + d] = 1;
     }
@@ -365,6 +385,7 @@ static int cycle_core(int32_t n, const int32_t *g, const int32_t *sl, const int3
   for (int64_t k = 0; k < nrun && k < trace_cap; ++k) {
     tr_dnn[k] = rl[k].j; tr_start[k] = rl[k].start; tr_end[k] = rl[k].end;
     tr_batch[k] = rl[k].batch; tr_kind[k] = rl[k].kind; tr_rep[k] = rl[k].rep;
+    if (tr_level) tr_level[k] = rl[k].level;
     sum->trace_n++;
   }
   free(occ); free(decide); free(jobs);
@@ -378,7 +399,16 @@ int oracle_cycle_direct(int32_t n, const int32_t *g, const int32_t *sl, const in
                         int32_t trace_cap, int32_t *tr_dnn, int32_t *tr_start, int32_t *tr_end,
                         int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep) {
   return cycle_core(n, g, sl, bstar, dtab, b_lo, L, nslots, count0, runs, served, jmiss, sum, trace_cap, tr_dnn,
-                    tr_start, tr_end, tr_batch, tr_kind, tr_rep, NULL, NULL, 0, NULL);
+                    tr_start, tr_end, tr_batch, tr_kind, tr_rep, NULL, NULL, 0, NULL, NULL, NULL);
+}
+
+int oracle_cycle_direct_bk(int32_t n, const int32_t *g, const int32_t *sl, const int32_t *bstar, const int64_t *dtab,
+                           const int64_t *dlow, int32_t b_lo, int32_t L, int32_t nslots, int32_t *runs,
+                           int64_t *served, int32_t *jmiss, or_cyc_sum_t *sum, int32_t trace_cap, int32_t *tr_dnn,
+                           int32_t *tr_start, int32_t *tr_end, int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep,
+                           int32_t *tr_level) {
+  return cycle_core(n, g, sl, bstar, dtab, b_lo, L, nslots, NULL, runs, served, jmiss, sum, trace_cap, tr_dnn,
+                    tr_start, tr_end, tr_batch, tr_kind, tr_rep, NULL, NULL, 0, NULL, dlow, tr_level);
 }
 
 int oracle_cycle_direct_ex(int32_t n, const int32_t *g, const int32_t *sl, const int32_t *bstar,
@@ -388,7 +418,7 @@ int oracle_cycle_direct_ex(int32_t n, const int32_t *g, const int32_t *sl, const
                            int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep) {
   if (fill_order < 0 || fill_order > 2) return -1;
   return cycle_core(n, g, sl, bstar, dtab, b_lo, L, nslots, count0, runs, served, jmiss, sum, trace_cap, tr_dnn,
-                    tr_start, tr_end, tr_batch, tr_kind, tr_rep, NULL, NULL, fill_order, busy);
+                    tr_start, tr_end, tr_batch, tr_kind, tr_rep, NULL, NULL, fill_order, busy, NULL, NULL);
 }
 
 /* ---------------------------------------------------------------- O9 ---
@@ -595,6 +625,7 @@ static void eval_scenario(const or_problem_t *pb, const or_params_t *p, or_out_t
   }
   o->scen_status[s] = OR_OK; o->T_us[s] = 0; o->u_static[s] = 0; o->u[s] = 0; o->thr[s] = 0;
   o->misses[s] = 0;
+  if (o->below) o->below[s] = 0;
   if (o->u_ideal) o->u_ideal[s] = 0;
   if (o->thr_ideal) o->thr_ideal[s] = 0;
   if (nd > OR_MAX_DNN_PER_SCEN) { o->scen_status[s] = OR_INVALID; return; }
@@ -635,11 +666,30 @@ static void eval_scenario(const or_problem_t *pb, const or_params_t *p, or_out_t
       dtab[j * 64 + b - 1] = dd > (u128)0x7FFFFFFFFFFFLL ? 0x7FFFFFFFFFFFLL : (int64_t)dd;
     }
   }
+  /* F1: run slots of the b* batch at every level below g_j, plus the launch latency of the new
+     instance, ceil(reconf_us / Delta) slots (P:2821 switchover) */
+  int64_t *dlow = NULL;
+  if (p->below_knee) {
+    dlow = (int64_t *)calloc((size_t)nd * 256, sizeof(int64_t));
+    const int64_t c = ((int64_t)p->reconf_us + p->slot_us - 1) / p->slot_us;
+    for (int32_t j = 0; j < nd; ++j) {
+      if (g[j] == 0) continue;
+      dnn_t m = get_dnn(pb, p, k0 + j);
+      for (int32_t l = 1; l < g[j]; ++l) {
+        const int64_t S = S_of(p, l);
+        const u128 den = (u128)S * (u128)m.M * (u128)p->slot_us;
+        u128 dd = (X_of(&m, p, S, bst[j]) + den - 1) / den + (u128)c;
+        dlow[(int64_t)j * 256 + l] = dd > (u128)0x7FFFFFFFFFFFLL ? 0x7FFFFFFFFFFFLL : (int64_t)dd;
+      }
+    }
+  }
   int32_t runs[OR_MAX_DNN_PER_SCEN], jmiss[OR_MAX_DNN_PER_SCEN];
   int64_t served[OR_MAX_DNN_PER_SCEN];
   or_cyc_sum_t cs;
-  oracle_cycle_direct(nd, g, sl, bst, dtab, p->b_min, p->L, (int32_t)nslots, NULL, runs, served, jmiss, &cs, 0,
-                      NULL, NULL, NULL, NULL, NULL, NULL);
+  oracle_cycle_direct_bk(nd, g, sl, bst, dtab, dlow, p->b_min, p->L, (int32_t)nslots, runs, served, jmiss, &cs, 0,
+                         NULL, NULL, NULL, NULL, NULL, NULL, NULL);
+  free(dlow);
+  if (o->below) o->below[s] = (uint32_t)cs.below;
   for (int32_t j = 0; j < nd; ++j) {
     o->runs[k0 + j] = (uint16_t)runs[j];
     o->served[k0 + j] = (uint32_t)served[j];
@@ -695,6 +745,7 @@ static int check_params(const or_params_t *p) {
   if (p->mem_mode < 0 || p->mem_mode > 2 || p->par_mode < 0 || p->par_mode > 1) return -1;
   if (p->wse_mode < 0 || p->wse_mode > 1 || p->b_min < 1 || p->b_max > 64 || p->b_min > p->b_max) return -1;
   if (p->margin < 0 || p->margin > p->L) return -1;
+  if (p->below_knee < 0 || p->below_knee > 1 || p->reconf_us < 0) return -1;
   return 0;
 }
 
@@ -784,7 +835,7 @@ static void compare_scenario(const or_problem_t *pb, const or_params_t *p, int64
     int64_t served[OR_MAX_DNN_PER_SCEN], busy[OR_MAX_DNN_PER_SCEN];
     or_cyc_sum_t cs;
     cycle_core(nd, g, sl, bst, dtab, p->b_min, p->L, (int32_t)nslots, NULL, runs, served, jmiss, &cs, 0, NULL, NULL,
-               NULL, NULL, NULL, NULL, NULL, NULL, c, busy);
+               NULL, NULL, NULL, NULL, NULL, NULL, c, busy, NULL, NULL);
     u[s * 5 + c] = (double)cs.occ_sum / NL;
     thr[s * 5 + c] = (double)cs.served_total * 1e6 / (double)T;
     jain[s * 5 + c] = jain_of(busy, nd, act);
@@ -928,7 +979,7 @@ static void simulate_scenario(const or_problem_t *pb, const or_params_t *p, cons
     run_t *rl = NULL;
     int64_t nrun = 0;
     cycle_core(nd, g, sl, bst, dtab, p->b_min, p->L, (int32_t)nslots, sb, runs, srv, jmiss, &cs, 0, NULL, NULL,
-               NULL, NULL, NULL, NULL, &rl, &nrun, 0, NULL);
+               NULL, NULL, NULL, NULL, &rl, &nrun, 0, NULL, NULL, NULL);
     o->misses[s] += (uint64_t)cs.misses;
     int64_t nfill = 0;
     for (int64_t q = 0; q < nrun; ++q) nfill += rl[q].kind == 1;

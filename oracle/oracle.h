@@ -45,6 +45,8 @@ typedef struct {
   int32_t wse_mode;   /* 0 per_request (Eq. 4 printed), 1 per_launch */
   int32_t b_min, b_max;
   int32_t ideal;      /* 1: run the ideal per-kernel scheduler (O6) */
+  int32_t below_knee; /* 1: F1 below-knee fallback for unplaced static jobs */
+  int32_t reconf_us;  /* F1: launch latency of an instance at a lower GPU% (switchover), us >= 0 */
 } or_params_t;
 
 typedef struct {
@@ -54,6 +56,7 @@ typedef struct {
   /* per scenario [num_scen] */
   uint8_t *scen_status; uint32_t *T_us; double *u_static; double *u; double *thr;
   uint32_t *misses; double *u_ideal; double *thr_ideal;
+  uint32_t *below;    /* F1: static jobs placed below the knee (nullable) */
 } or_out_t;
 
 /* O1: X(l, b) = E_t * S * M for DNN `dnn` (Eqs. 1-5), returned as lo/hi 64-bit halves. */
@@ -75,6 +78,7 @@ typedef struct {
   int64_t occ_static_sum, occ_sum, served_total;
   int32_t misses, status;
   int32_t trace_n;
+  int32_t below;      /* F1: static jobs placed below the knee (kind 2 in the trace) */
 } or_cyc_sum_t;
 int oracle_cycle_direct(int32_t n, const int32_t *g, const int32_t *sl_slots, const int32_t *bstar,
                         const int64_t *dtab, int32_t b_lo, int32_t L, int32_t nslots, const int64_t *count0,
@@ -89,6 +93,15 @@ int oracle_cycle_direct_ex(int32_t n, const int32_t *g, const int32_t *sl, const
                            int32_t fill_order, int32_t *runs, int64_t *served, int32_t *jmiss, int64_t *busy,
                            or_cyc_sum_t *sum, int32_t trace_cap, int32_t *tr_dnn, int32_t *tr_start, int32_t *tr_end,
                            int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep);
+
+/* O5 + F1 below-knee fallback.  dlow[j*256 + l] = run slots of DNN j's b* batch at
+ * level l < g_j including the launch latency (0 = level unusable); an unplaced static job is retried at
+ * l = g_j - 1 .. 1 and placed at the first level with a feasible start (trace kind 2, tr_level = l). */
+int oracle_cycle_direct_bk(int32_t n, const int32_t *g, const int32_t *sl, const int32_t *bstar, const int64_t *dtab,
+                           const int64_t *dlow, int32_t b_lo, int32_t L, int32_t nslots, int32_t *runs,
+                           int64_t *served, int32_t *jmiss, or_cyc_sum_t *sum, int32_t trace_cap, int32_t *tr_dnn,
+                           int32_t *tr_start, int32_t *tr_end, int32_t *tr_batch, int32_t *tr_kind, int32_t *tr_rep,
+                           int32_t *tr_level);
 
 /* O9 temporal sharing: lvl[j] > 0 active (knee level), sl[j] SLO in slots, dL[j] run slots at 100% GPU.
  * slice_out, runs_out per DNN; *occ_num = sum slice_j * lvl_j (utilisation numerator). */

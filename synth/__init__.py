@@ -78,6 +78,8 @@ class Params:
     b_min: int = 1
     b_max: int = 64
     ideal: int = 0
+    below_knee: int = 0    # F1 below-knee fallback
+    reconf_us: int = 100   # F1 launch latency of a lower-GPU% instance (P:2821 switchover)
 
     def replace(self, **kw) -> "Params":
         return dataclasses.replace(self, **kw)
