@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="cpu_baseline time budget")
     ap.add_argument("--cycles", type=int, default=20, help="config 5: sessions simulated per step")
     ap.add_argument("--no-compare", action="store_true", help="skip the O9 comparison-scheduler leg")
+    ap.add_argument("--no-below-knee", action="store_true", help="skip the F1 below-knee fallback leg")
     return ap.parse_args()
 
 
@@ -287,6 +288,11 @@ def run_native(args, rank, world, local):
     if not args.no_compare:
         cmp_line = run_compare_leg(args, ds, dp, p, out, ws, stream, per_gpu, world)
 
+    # ---- F1 below-knee fallback (DSTACK_FLAG_BELOW_KNEE) on the same inputs, timed separately ----
+    bk_line = None
+    if not args.no_below_knee:
+        bk_line = run_below_knee_leg(args, ds, dp, p, out, stream, per_gpu, world)
+
     # ---- e2e: the public API from pinned host buffers, H2D + compute + D2H of results each step ----
     e2e = None
     if not args.no_e2e:
@@ -337,6 +343,7 @@ def run_native(args, rank, world, local):
         "clocks": clocks,
         "e2e": e2e,
         "compare": cmp_line,
+        "below_knee": bk_line,
         "stats": {"mean_u": agg["sum_u"] / max(agg["n_scen_scheduled"], 1),
                   "mean_u_static": agg["sum_u_static"] / max(agg["n_scen_scheduled"], 1),
                   "scen_status": agg["n_scen_st"], "dnn_status": agg["n_st"],
@@ -379,6 +386,38 @@ def run_compare_leg(args, ds, dp, p, out, ws, stream, per_gpu, world):
             "scenarios_per_s": per_gpu * world / (ms / 1e3), "gpu_launches": ds.last_launch_count(),
             "schedulers": list(ds.CMP_NAMES), "means_over_scheduled_scenarios": means,
             "dstack_throughput_ratio": {k: d / means[k]["thr"] for k in ds.CMP_NAMES if means[k]["thr"] > 0}}
+
+
+def run_below_knee_leg(args, ds, dp, p, out, stream, per_gpu, world):
+    """SURVEY §8(f) item 1 measured: dstack_eval_batch with DSTACK_FLAG_BELOW_KNEE (unplaced static jobs retried
+    below the knee) over the whole workload, device-timed; misses and utilisation beside the
+    default path's (this step's `out`)."""
+    import torch
+    import torch.distributed as dist
+    q = p.replace(below_knee=1)
+    o = ds.alloc_outputs(dp, agg=True)
+    ws = ds.Workspace(ds.workspace_size(dp, q), stream.device)
+    ds.eval_batch(dp, q, out=o, ws=ws)
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 5))
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        ds.eval_batch(dp, q, out=o, ws=ws)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=stream.device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    a0, a1 = ds.agg_to_dict(out["agg"]), ds.agg_to_dict(o["agg"])
+    n0, n1 = max(a0["n_scen_scheduled"], 1), max(a1["n_scen_scheduled"], 1)
+    return {"api": "paper_2304_13541_b200.dstack.eval_batch (dstack_eval_batch, DSTACK_FLAG_BELOW_KNEE)",
+            "reconf_us": q.reconf_us, "ms_per_call": ms, "scenarios_per_s": per_gpu * world / (ms / 1e3),
+            "below_knee_runs": int(o["below"].sum().item()), "misses": a1["misses"], "misses_default": a0["misses"],
+            "oversubscribed_scenarios": a1["n_scen_st"][4], "oversubscribed_default": a0["n_scen_st"][4],
+            "mean_u": a1["sum_u"] / n1, "mean_u_default": a0["sum_u"] / n0}
 
 
 def run_e2e(args, sp, p, dev, world):

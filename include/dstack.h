@@ -66,6 +66,15 @@ extern "C" {
 #define DSTACK_MAX_FILL_RUNS 2048   /* dstack_simulate: fill runs per session (more => scenario INVALID) */
 
 #define DSTACK_FLAG_IDEAL 1u   /* run a6, the ideal per-kernel scheduler */
+/* F1 below-knee fallback ("D-STACK's scheduler can also schedule a model with
+ * GPU% lower than its Knee, albeit with high inference latency when necessary ... also considers the
+ * additional latency of launching a new DNN model at lower GPU%"; reading R21): a static
+ * job with no feasible start at g_j is retried at levels g_j - 1 .. 1 and placed, under the same
+ * Start-Early / Start-Late rule, at the first level whose run fits in its window; that run lasts
+ * ceil(f_L(l, b*) / Delta) + ceil(reconf_us / Delta) slots at level l.  Only unplaced jobs count as misses.
+ * Applies to dstack_schedule_cycle and dstack_eval_batch (not with a test hook); dstack_simulate and
+ * dstack_compare reject it (DSTACK_EINVAL). */
+#define DSTACK_FLAG_BELOW_KNEE 2u
 
 /* Structure-of-arrays problem set, CSR-indexed.  Scenario s owns DNNs
  * [scen_dnn_off[s], scen_dnn_off[s+1]); DNN k owns kernel rows [dnn_row_off[k], dnn_row_off[k+1]). */
@@ -95,7 +104,9 @@ typedef struct {
   int32_t par_mode;   /* Eq. 1: 0 linear N_i(b) = b n_i, 1 threads N_i(b) = ceil(b theta_i / 2048) */
   int32_t wse_mode;   /* Eq. 4: 0 per_request (printed), 1 per_launch (t_np once per kernel) */
   int32_t b_min, b_max;  /* batch range, 1 <= b_min <= b_max <= 64; per DNN b_hi = min(b_max, bmax_j) */
-  uint32_t flags;     /* DSTACK_FLAG_IDEAL */
+  uint32_t flags;     /* DSTACK_FLAG_IDEAL | DSTACK_FLAG_BELOW_KNEE */
+  int32_t reconf_us;  /* F1 launch latency of an instance at a lower GPU%, us >= 0 (~100 us switchover
+                         with active-standby overlap); read only with DSTACK_FLAG_BELOW_KNEE */
 } dstack_params_t;
 
 /* Aggregate statistics over the scenarios of one call (one struct, device memory). */
@@ -132,6 +143,7 @@ typedef struct {
   double   *u_ideal;     /* = (double)sum_events(sum g * dt) / ((double)L * (double)T_us) */
   double   *thr_ideal;   /* = (double)sum_j(completed_j * b*_j) * 1e6 / (double)T_us */
   dstack_agg_t *agg;     /* optional, one struct */
+  uint32_t *below;       /* per scenario: static jobs placed below the knee (DSTACK_FLAG_BELOW_KNEE; else 0) */
 } dstack_out_t;
 
 /* Optional test hook for dstack_schedule_cycle (Table 4 pins): per-DNN level g_j

@@ -29,7 +29,9 @@ bool params_ok(const dstack_params_t *p) {
   return p && p->L >= 1 && p->L <= 255 && p->S_tot >= 1 && p->S_tot <= 256 && p->slot_us >= 1 &&
          p->mem_mode >= 0 && p->mem_mode <= 2 && p->par_mode >= 0 && p->par_mode <= 1 && p->wse_mode >= 0 &&
          p->wse_mode <= 1 && p->b_min >= 1 && p->b_max <= DSTACK_MAX_BATCH && p->b_min <= p->b_max &&
-         p->margin >= 0 && p->margin <= p->L && (p->flags & ~DSTACK_FLAG_IDEAL) == 0;
+         p->margin >= 0 && p->margin <= p->L &&
+         (p->flags & ~(DSTACK_FLAG_IDEAL | DSTACK_FLAG_BELOW_KNEE)) == 0 &&
+         (!(p->flags & DSTACK_FLAG_BELOW_KNEE) || p->reconf_us >= 0);
 }
 
 bool problem_ok(const dstack_problem_t *pb) {
@@ -201,6 +203,7 @@ static int schedule_impl(const dstack_problem_t *pb, const dstack_params_t *p, c
   if (hook) { c.hook_level = hook->level; c.hook_d = hook->d_slots; }
   c.level = out->level; c.runs = out->runs; c.served = out->served; c.scen_status = out->scen_status;
   c.T_us = out->T_us; c.u_static = out->u_static; c.u = out->u; c.thr = out->thr; c.misses = out->misses;
+  c.below = out->below;
   c.dtab_rows = (uint16_t *)((char *)ws + ws_layout(pb, p).dtab);
   if (pre_ws) { c.ws_RT = (const uint32_t *)((char *)ws + ws_layout(pb, p).rt); c.ws_D = (const uint64_t *)((char *)ws + ws_layout(pb, p).d); }
   int rc = launch_cycle(c, s, &g_launches);
@@ -244,7 +247,7 @@ int dstack_eval_batch(const dstack_problem_t *pb, const dstack_params_t *p, dsta
     return DSTACK_EINVAL;
   const void *outs[] = {out->demand, out->batch, out->knee, out->status, out->alloc_q16, out->level, out->runs,
                         out->served, out->scen_status, out->T_us, out->u_static, out->u, out->thr, out->misses,
-                        out->u_ideal, out->thr_ideal, out->agg};
+                        out->u_ideal, out->thr_ideal, out->agg, out->below};
   for (const void *o : outs)
     if (!disjoint(pb, o)) return DSTACK_EINVAL;
   const size_t need = dstack_workspace_size(pb, p);
@@ -300,6 +303,7 @@ int dstack_simulate(const dstack_problem_t *pb, const dstack_params_t *p, const 
                     size_t ws_bytes, void *stream) {
   g_launches = 0;
   if (!problem_ok(pb) || !params_ok(p) || !out || cycles < 0 || (pb->num_dnn > 0 && !lam_pct)) return DSTACK_EINVAL;
+  if (p->flags & DSTACK_FLAG_BELOW_KNEE) return DSTACK_EINVAL;
   if (pb->num_scen > 0 && (!out->status || !out->T_us || !out->arrived || !out->in_slo || !out->late ||
                            !out->unserved || !out->occ_sum || !out->runs || !out->misses))
     return DSTACK_EINVAL;
@@ -333,7 +337,7 @@ int dstack_compare(const dstack_problem_t *pb, const dstack_params_t *p, const u
                    const uint32_t *alloc_q16, double *u, double *thr, double *jain, void *ws, size_t ws_bytes,
                    void *stream) {
   g_launches = 0;
-  if (!problem_ok(pb) || !params_ok(p)) return DSTACK_EINVAL;
+  if (!problem_ok(pb) || !params_ok(p) || (p->flags & DSTACK_FLAG_BELOW_KNEE)) return DSTACK_EINVAL;
   if (pb->num_dnn > 0 && (!demand || !batch || !alloc_q16)) return DSTACK_EINVAL;
   if (pb->num_scen > 0 && (!u || !thr || !jain)) return DSTACK_EINVAL;
   const void *outs[] = {u, thr, jain};

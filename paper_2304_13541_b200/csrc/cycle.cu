@@ -27,7 +27,9 @@ __global__ void __launch_bounds__(256) k_wmaxmin(int32_t num_scen, const int32_t
 #ifndef DSTACK_CYC_MINB
 #define DSTACK_CYC_MINB 4
 #endif
-__global__ void __launch_bounds__(CYC_WARPS * 32, DSTACK_CYC_MINB) k_cycle(CycArgs a) {
+// BK: F1 below-knee fallback compiled in (DSTACK_FLAG_BELOW_KNEE); the default instantiation has no trace of it.
+template <bool BK>
+__global__ void __launch_bounds__(CYC_WARPS * 32, DSTACK_CYC_MINB) k_cycle(const __grid_constant__ CycArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   CycSmem &sm = reinterpret_cast<CycSmem *>(smem_raw)[warp];
@@ -38,7 +40,7 @@ __global__ void __launch_bounds__(CYC_WARPS * 32, DSTACK_CYC_MINB) k_cycle(CycAr
     const int32_t k0 = a.pb.scen_dnn_off[s], nd = a.pb.scen_dnn_off[s + 1] - k0;
     uint8_t sst = DSTACK_ST_OK;
     uint32_t T = 0;
-    CycRes cr; cr.occ_static = cr.occ_all = cr.served_tot = cr.misses = 0; cr.oversub = false;
+    CycRes cr; cr.occ_static = cr.occ_all = cr.served_tot = cr.misses = cr.below = 0; cr.oversub = false;
     const bool mine = lane < nd && nd <= DSTACK_MAX_DNN_PER_SCEN;
     const int k = k0 + lane;
     uint32_t dem = 0, bs = 0, g = 0, sl = 1, rep = 0, slo = 0, runs = 0, served = 0;
@@ -98,7 +100,14 @@ __global__ void __launch_bounds__(CYC_WARPS * 32, DSTACK_CYC_MINB) k_cycle(CycAr
         }
         dtab_from_rows(a.pb, a.p, k0 + j, RT, D, (int32_t)gj, b_lo, (int32_t)bsj, dtab + j * DTAB_ROW, lane);
       }
-      cr = cycle_core(sm, dtab, lane, active, g, bs, sl, rep, nslots, L, b_lo, a.hook_level != nullptr, runs, served);
+      BelowKnee bk;
+      const bool use_bk = BK && a.hook_level == nullptr;
+      if (use_bk) {
+        bk.pb = &a.pb; bk.p = &a.p; bk.k0 = k0; bk.ws_RT = a.ws_RT; bk.ws_D = a.ws_D;
+        bk.c_slots = ((uint64_t)a.p.reconf_us + (uint64_t)slot - 1) / (uint64_t)slot;
+      }
+      cr = cycle_core(sm, dtab, lane, active, g, bs, sl, rep, nslots, L, b_lo, a.hook_level != nullptr, runs, served,
+                      0, nullptr, 0, nullptr, 0, nullptr, use_bk ? &bk : nullptr);
       if (cr.oversub) sst = DSTACK_ST_OVERSUBSCRIBED;
     }
     if (mine) {
@@ -120,6 +129,7 @@ __global__ void __launch_bounds__(CYC_WARPS * 32, DSTACK_CYC_MINB) k_cycle(CycAr
       if (a.u) a.u[s] = sch ? (double)cr.occ_all / ((double)nslots * (double)L) : 0.0;
       if (a.thr) a.thr[s] = sch ? (double)cr.served_tot * 1e6 / (double)T : 0.0;
       if (a.misses) a.misses[s] = cr.misses;
+      if (a.below) a.below[s] = cr.below;
     }
     __syncwarp();
   }
@@ -142,8 +152,13 @@ int launch_cycle(const CycArgs &a, cudaStream_t s, int *launches) {
   int64_t blocks = (a.pb.num_scen + CYC_WARPS - 1) / CYC_WARPS;
   const int64_t cap = (int64_t)num_sms() * 8;
   if (blocks > cap) blocks = cap;
-  cudaFuncSetAttribute(k_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_cycle<<<(unsigned)blocks, CYC_WARPS * 32, smem, s>>>(a);
+  if (a.p.flags & DSTACK_FLAG_BELOW_KNEE) {
+    cudaFuncSetAttribute(k_cycle<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_cycle<true><<<(unsigned)blocks, CYC_WARPS * 32, smem, s>>>(a);
+  } else {
+    cudaFuncSetAttribute(k_cycle<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_cycle<false><<<(unsigned)blocks, CYC_WARPS * 32, smem, s>>>(a);
+  }
   ++*launches;
   return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;
 }

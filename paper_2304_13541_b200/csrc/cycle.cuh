@@ -14,6 +14,7 @@
 // ones in (runs so far, index) order by repeated min-reductions.
 #pragma once
 #include "common.cuh"
+#include "prof.cuh"
 
 namespace dstack {
 
@@ -28,12 +29,25 @@ static __device__ unsigned long long g_cstats[16];   // per TU (instrumentation 
 #endif
 
 constexpr uint16_t NONE16 = 0xFFFF;
+constexpr uint32_t NONE32 = 0xFFFFFFFFu;
+
+// F1 below-knee fallback context (DSTACK_FLAG_BELOW_KNEE): where the scenario's DNN
+// rows live, so that a static job that found no start at g_j can re-derive its run length at a lower level
+// from O1 (one row pass per level), plus the launch latency in slots.
+struct BelowKnee {
+  const dstack_problem_t *pb;
+  const dstack_params_t *p;
+  int64_t k0;              // first DNN of the scenario
+  const uint32_t *ws_RT;   // per-DNN sum R and sum R d from k_prof (NULL: recomputed from the rows)
+  const uint64_t *ws_D;
+  uint64_t c_slots;        // ceil(reconf_us / Delta)
+};
 
 
 struct CycSmem {
   uint8_t occ[DSTACK_MAX_SLOTS];
   uint32_t dmask[DSTACK_MAX_SLOTS / 32];   // decision times (bit u of word w <=> slot 32 w + u)
-  uint16_t starts[DSTACK_MAX_JOBS];
+  uint32_t sr[DSTACK_MAX_JOBS];   // static job (j, r): start | run slots << 16, or NONE32 (miss)
 };
 
 // bytes of a lane's 4-slot word (first slot `base`) below slot x
@@ -180,8 +194,41 @@ __device__ __forceinline__ uint32_t occ_sum(const uint8_t *occ, int nslots, int 
   return __reduce_add_sync(FULL, s);
 }
 
+// F1 retry of static job (j, r) over the window [rel, dlv) at levels g_j - 1 .. 1 (warp-uniform arguments): the
+// first level whose run ceil(X(S(l), b*) / (S(l) M Delta)) + launch latency has a feasible start under the job's
+// rule.  Returns start | d << 16 | l << 32, or 0 if no level fits.  Out of line: only misses reach it.
+static __device__ __noinline__ uint64_t below_knee_retry(const uint8_t *occ, const BelowKnee &bk, int j, int rj, int rel,
+                                                         int dlv, int gj, int32_t bsj, int L, int lane) {
+  const int64_t kj = bk.k0 + j;
+  const dstack_problem_t &bpb = *bk.pb;
+  const dstack_params_t &bp = *bk.p;
+  uint64_t RT, D;
+  if (bk.ws_RT) { RT = bk.ws_RT[kj]; D = bk.ws_D[kj]; }
+  else {
+    const int64_t r0 = bpb.dnn_row_off[kj];
+    const int32_t K = (int32_t)(bpb.dnn_row_off[kj + 1] - r0);
+    RT = 0; D = 0;
+    for (int i = lane; i < K; i += 32) { RT += bpb.r[r0 + i]; D += (uint64_t)bpb.r[r0 + i] * bpb.d[r0 + i]; }
+    RT = warp_sum_u64(RT); D = warp_sum_u64(D);
+  }
+  const uint64_t M = bp.mem_mode == 0 ? 1ull : (uint64_t)bpb.mem_bw[kj];
+  for (int l = gj - 1; l >= 1; --l) {
+    const uint64_t S = (uint64_t)s_of(l, bp.S_tot, bp.L);
+    const uint64_t X = x_from_rows(bpb, bp, kj, RT, D, S, bsj, lane);
+    const uint64_t den = S * M * (uint64_t)bp.slot_us;
+    const uint64_t d64 = (X + den - 1) / den + bk.c_slots;
+    if (d64 > (uint64_t)(dlv - rel)) continue;
+    const int d = (int)d64;
+    const int s = d <= 124 ? ((rj & 1) ? find_late_packed(occ, rel, dlv, d, l, L, lane)
+                                       : find_early_packed(occ, rel, dlv, d, l, L, lane))
+                           : ((rj & 1) ? find_late(occ, rel, dlv, d, l, L, lane) : find_early(occ, rel, dlv, d, l, L, lane));
+    if (s >= 0) return (uint64_t)s | ((uint64_t)d << 16) | ((uint64_t)l << 32);
+  }
+  return 0;
+}
+
 struct CycRes {
-  uint32_t occ_static, occ_all, served_tot, misses;
+  uint32_t occ_static, occ_all, served_tot, misses, below;
   bool oversub;
 };
 
@@ -198,10 +245,11 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
                                             uint32_t bs, uint32_t sl, uint32_t rep, int32_t nslots, int32_t L,
                                             int32_t b_lo, bool hook_b_only, uint32_t &runs, uint32_t &served,
                                             uint32_t count0 = 0, uint64_t *fill_log = nullptr, uint32_t fill_cap = 0,
-                                            uint32_t *fill_n = nullptr, int fill_order = 0, uint32_t *busy = nullptr) {
+                                            uint32_t *fill_n = nullptr, int fill_order = 0, uint32_t *busy = nullptr,
+                                            const BelowKnee *bk = nullptr) {
   // fill_order (O9 comparison schedulers): 0 D-STACK (runs so far), 1 Max-Min fair (smallest g
   // first), 2 max-throughput (shortest d(b*) first); ties by index.  busy (nullable): this lane's run slots.
-  CycRes res; res.occ_static = 0; res.occ_all = 0; res.served_tot = 0; res.misses = 0; res.oversub = false;
+  CycRes res; res.occ_static = 0; res.occ_all = 0; res.served_tot = 0; res.misses = 0; res.below = 0; res.oversub = false;
   for (int w = lane; (w << 2) < nslots; w += 32) reinterpret_cast<uint32_t *>(sm.occ)[w] = 0u;
   // decision-time bits: one register word per lane (word = lane) when nslots <= 1024, else shared memory
   const bool dreg = nslots <= 1024;
@@ -243,13 +291,18 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
                                       : find_early_packed(sm.occ, rel, dlv, dj, gj, L, lane);
     else st = (rj & 1) ? find_late(sm.occ, rel, dlv, dj, gj, L, lane) : find_early(sm.occ, rel, dlv, dj, gj, L, lane);
     if (lane == 0) CSTAT(1, 1);
+    int lv = gj, dd = dj;
+    if (st < 0 && bk != nullptr) {
+      const uint64_t r = below_knee_retry(sm.occ, *bk, j, rj, rel, dlv, gj, (int32_t)__shfl_sync(FULL, bs, j), L, lane);
+      if (r != 0) { st = (int)(r & 0xFFFFu); dd = (int)((r >> 16) & 0xFFFFu); lv = (int)(r >> 32); res.below++; }
+    }
     if (st >= 0) {
-      occ_add(sm.occ, st, dj, gj, lane);
-      if (lane == 0) sm.starts[offj + rj] = (uint16_t)st;
-      if (st + dj < nslots) dset(st + dj);
-      if (lane == j) { runs++; served += bs; if (busy) *busy += (uint32_t)dj; }
+      occ_add(sm.occ, st, dd, lv, lane);
+      if (lane == 0) sm.sr[offj + rj] = (uint32_t)st | ((uint32_t)dd << 16);
+      if (st + dd < nslots) dset(st + dd);
+      if (lane == j) { runs++; served += bs; if (busy) *busy += (uint32_t)dd; }
     } else {
-      if (lane == 0) sm.starts[offj + rj] = NONE16;
+      if (lane == 0) sm.sr[offj + rj] = NONE32;
       res.misses++;
       res.oversub = true;
     }
@@ -266,12 +319,16 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   uint32_t count = runs + count0;
   int fs = -1, fe = -1;       // last fill run of this lane's DNN
   uint32_t nfill = 0;
-  // this lane's next placed static run not yet over: index p into its windows, start sp (its end sp + d*)
-  int p = 0, sp = -1;
+  // this lane's next placed static run not yet over: index p into its windows, start sp, end se
+  int p = 0, sp = -1, se = 0;
   auto adv = [&](int tt) {
     while (p < (int)rep) {
-      if (sp < 0) { const uint16_t v = sm.starts[joff + p]; sp = v == NONE16 ? -2 : (int)v; }
-      if (sp == -2 || sp + (int)dstar <= tt) { ++p; sp = -1; continue; }
+      if (sp < 0) {
+        const uint32_t v = sm.sr[joff + p];
+        sp = v == NONE32 ? -2 : (int)(v & 0xFFFFu);
+        se = sp + (int)(v >> 16);
+      }
+      if (sp == -2 || se <= tt) { ++p; sp = -1; continue; }
       break;
     }
   };

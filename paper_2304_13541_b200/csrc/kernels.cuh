@@ -47,6 +47,7 @@ struct CycArgs {
   uint32_t *T_us;
   double *u_static, *u, *thr;
   uint32_t *misses;
+  uint32_t *below;         // F1: static jobs placed below the knee
   uint16_t *dtab_rows;     // workspace: num_dnn rows of DTAB_ROW u16
   const uint32_t *ws_RT;   // non-NULL => dtab_rows already hold d_j(b) at g = demand (from k_prof)
   const uint64_t *ws_D;

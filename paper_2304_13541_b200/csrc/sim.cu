@@ -117,14 +117,13 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) k_sim(SimArgs a) {
         }
         jo -= active ? rep : 0u;
         if (active) {
-          const uint32_t dstar = dtab[lane * DTAB_ROW + bs - 1];
           uint32_t r = 0, f = 0;
           while (true) {
             // next static run of this DNN
-            uint32_t ss = 0xFFFFFFFFu;
+            uint32_t ss = 0xFFFFFFFFu, sd = 0;
             while (r < rep) {
-              const uint16_t st = sm.starts[jo + r];
-              if (st != NONE16) { ss = st; break; }
+              const uint32_t v = sm.sr[jo + r];
+              if (v != NONE32) { ss = v & 0xFFFFu; sd = v >> 16; break; }
               ++r;
             }
             // next fill run of this DNN
@@ -137,7 +136,7 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) k_sim(SimArgs a) {
             }
             if (ss == 0xFFFFFFFFu && fsv == 0xFFFFFFFFu) break;
             uint32_t st, d, b;
-            if (ss <= fsv) { st = ss; d = dstar; b = bs; ++r; }
+            if (ss <= fsv) { st = ss; d = sd; b = bs; ++r; }
             else { st = fsv; d = (uint32_t)(fr >> 8) & 0xFFFFFFu; b = (uint32_t)fr & 0xFFu; ++f; }
             const uint64_t ts = t0 + (uint64_t)st * slot, te = t0 + (uint64_t)(st + d) * slot;
             while (arr.time <= ts) arr_next(arr, a, gs, (uint32_t)lane, mq);

@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("DSTACK_LIB") or os.path.join(_HERE, "libdstack.so")  
 DSTACK_OK, DSTACK_EINVAL, DSTACK_EWORKSPACE, DSTACK_ELAUNCH = 0, -1, -2, -3
 ST_OK, ST_INFEASIBLE, ST_OVERFLOW, ST_INVALID, ST_OVERSUBSCRIBED = 0, 1, 2, 3, 4
 FLAG_IDEAL = 1
+FLAG_BELOW_KNEE = 2
 MAX_BATCH = 64
 
 
@@ -37,7 +38,7 @@ class CProblem(C.Structure):
 class CParams(C.Structure):
     _fields_ = [("L", C.c_int32), ("S_tot", C.c_int32), ("slot_us", C.c_int32), ("mem_mode", C.c_int32),
                 ("margin", C.c_int32), ("par_mode", C.c_int32), ("wse_mode", C.c_int32), ("b_min", C.c_int32),
-                ("b_max", C.c_int32), ("flags", C.c_uint32)]
+                ("b_max", C.c_int32), ("flags", C.c_uint32), ("reconf_us", C.c_int32)]
 
 
 class CAgg(C.Structure):
@@ -52,7 +53,7 @@ class CAgg(C.Structure):
 AGG_WORDS = C.sizeof(CAgg) // 8
 
 _OUT_FIELDS = ("demand", "batch", "knee", "status", "alloc_q16", "level", "runs", "served",
-               "scen_status", "T_us", "u_static", "u", "thr", "misses", "u_ideal", "thr_ideal", "agg")
+               "scen_status", "T_us", "u_static", "u", "thr", "misses", "u_ideal", "thr_ideal", "agg", "below")
 
 
 class COut(C.Structure):
@@ -186,8 +187,9 @@ def from_device_dict(g: dict) -> DeviceProblem:
 
 
 def cparams(p) -> CParams:
-    flags = FLAG_IDEAL if getattr(p, "ideal", 0) else 0
-    return CParams(p.L, p.S_tot, p.slot_us, p.mem_mode, p.margin, p.par_mode, p.wse_mode, p.b_min, p.b_max, flags)
+    flags = (FLAG_IDEAL if getattr(p, "ideal", 0) else 0) | (FLAG_BELOW_KNEE if getattr(p, "below_knee", 0) else 0)
+    return CParams(p.L, p.S_tot, p.slot_us, p.mem_mode, p.margin, p.par_mode, p.wse_mode, p.b_min, p.b_max, flags,
+                   getattr(p, "reconf_us", 100))
 
 
 def workspace_size(dp: DeviceProblem, p) -> int:
@@ -248,7 +250,7 @@ def alloc_outputs(dp: DeviceProblem, agg=True):
              alloc_q16=z(D, torch.int32), level=z(D, torch.int16), runs=z(D, torch.int16), served=z(D, torch.int32),
              scen_status=z(S, torch.uint8), T_us=z(S, torch.int32), u_static=z(S, torch.float64),
              u=z(S, torch.float64), thr=z(S, torch.float64), misses=z(S, torch.int32), u_ideal=z(S, torch.float64),
-             thr_ideal=z(S, torch.float64))
+             thr_ideal=z(S, torch.float64), below=z(S, torch.int32))
     if agg:
         o["agg"] = z(AGG_WORDS, torch.int64)
     return o

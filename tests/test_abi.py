@@ -41,12 +41,18 @@ def test_host_side_argument_checks():
     assert lib.dstack_workspace_size(C.byref(pb), C.byref(good)) > 0
     for bad in (ds.CParams(0, 148, 100, 1, 0, 0, 0, 1, 64, 0), ds.CParams(100, 300, 100, 1, 0, 0, 0, 1, 64, 0),
                 ds.CParams(100, 148, 100, 3, 0, 0, 0, 1, 64, 0), ds.CParams(100, 148, 100, 1, 0, 0, 0, 2, 1, 0),
-                ds.CParams(100, 148, 100, 1, 0, 0, 0, 1, 65, 0), ds.CParams(100, 148, 0, 1, 0, 0, 0, 1, 64, 0)):
+                ds.CParams(100, 148, 100, 1, 0, 0, 0, 1, 65, 0), ds.CParams(100, 148, 0, 1, 0, 0, 0, 1, 64, 0),
+                ds.CParams(100, 148, 100, 1, 0, 0, 0, 1, 64, 4), ds.CParams(100, 148, 100, 1, 0, 0, 0, 1, 64, 2, -1)):
         assert lib.dstack_batch_opt(C.byref(pb), C.byref(bad), None, None, None, None, None, 0, None) == ds.DSTACK_EINVAL
     # missing outputs for a non-empty problem
     pb1 = ds.CProblem(1, 1, 1, *([8] * 11))
     assert lib.dstack_batch_opt(C.byref(pb1), C.byref(good), None, None, None, None, None, 0, None) == ds.DSTACK_EINVAL
     assert lib.dstack_status_str(ds.DSTACK_EWORKSPACE).startswith(b"EWORKSPACE")
+    # F1 is rejected where it is not implemented (dstack.h)
+    bk = ds.CParams(100, 148, 100, 1, 0, 0, 0, 1, 64, ds.FLAG_BELOW_KNEE, 100)
+    assert lib.dstack_workspace_size(C.byref(pb), C.byref(bk)) > 0
+    assert lib.dstack_compare(C.byref(pb), C.byref(bk), None, None, None, None, None, None, None, 0,
+                              None) == ds.DSTACK_EINVAL
 
 
 def test_struct_layouts_match_header():
@@ -54,8 +60,8 @@ def test_struct_layouts_match_header():
     # dstack_agg_t: 5 doubles + 4 + 5 + 5 + 3 + 65 + 256 + 1 u64
     assert C.sizeof(ds.CAgg) == 8 * (5 + 4 + 5 + 5 + 3 + 65 + 256 + 1)
     assert C.sizeof(ds.CProblem) == 4 + 4 + 8 + 11 * 8
-    assert C.sizeof(ds.CParams) == 10 * 4
-    assert C.sizeof(ds.COut) == 17 * 8
+    assert C.sizeof(ds.CParams) == 11 * 4
+    assert C.sizeof(ds.COut) == 18 * 8
 
 
 @pytest.mark.skipif(os.environ.get("CUDA_VISIBLE_DEVICES", None) is not None and False, reason="")

@@ -40,11 +40,12 @@ def sampled_outputs(o, off, idx):
     return out
 
 
-@pytest.mark.parametrize("cfg,stride", [(2, 10), (4, 250)])
-def test_fullsize_sampled_parity(ds, cfg, stride):
+@pytest.mark.parametrize("cfg,stride,bk", [(2, 10, 0), (4, 250, 0), (4, 500, 1)])
+def test_fullsize_sampled_parity(ds, cfg, stride, bk):
     """Config 2 (10k scenarios, L = 100, ideal on) every 10th scenario; config 4 (100k oversubscribed
-    scenarios, ideal on) every 250th: every a1-a6 output bit-exact."""
+    scenarios, ideal on) every 250th, and with the F1 below-knee fallback every 500th: every output bit-exact."""
     sp, p = synth.config(cfg)
+    p = p.replace(below_knee=bk)
     g = synth.generate_device(sp, "cuda")
     dp = ds.from_device_dict(g)
     o = ds.eval_batch(dp, p)
@@ -53,8 +54,10 @@ def test_fullsize_sampled_parity(ds, cfg, stride):
     idx = np.arange(0, sp.num_scen, stride)
     want = oracle.evaluate(synth.sample(sp, idx), p)
     assert_parity(sampled_outputs(o, off, idx), want, where=f"config {cfg} full size")
-    if cfg == 4:   # the oversubscribed configuration really is oversubscribed (R20)
+    if cfg == 4 and not bk:   # the oversubscribed configuration really is oversubscribed (R20)
         assert (want["scen_status"] == oracle.OVERSUBSCRIBED).mean() > 0.5
+    if bk:
+        assert want["below"].sum() > 0
 
 
 def test_config5_fullsize_sampled_parity(ds):

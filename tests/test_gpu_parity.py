@@ -14,7 +14,7 @@ import synth  # noqa: E402
 from synth import Params  # noqa: E402
 
 INT_KEYS = ("demand", "batch", "knee", "status", "alloc_q16", "level", "runs", "served", "scen_status", "T_us",
-            "misses")
+            "misses", "below")
 F_KEYS = ("u_static", "u", "thr", "u_ideal", "thr_ideal")
 
 
@@ -369,3 +369,45 @@ def test_compare_config3_sampled(ds):
     want = oracle.compare(pb, p)
     got = {k: v[torch.as_tensor(idx, device=v.device)].cpu().numpy() for k, v in c.items()}
     assert_compare_parity(got, want, where="config3 sample")
+
+
+# ---------------------------------------------------------------- F1 below-knee fallback ---
+
+@pytest.mark.parametrize("variant", ["cfg4", "cfg4_reconf0", "cfg2_verbatim148", "cfg4_batching"])
+def test_below_knee_parity(ds, variant):
+    """F1 (DSTACK_FLAG_BELOW_KNEE) through dstack_eval_batch: every output, including the
+    per-scenario below-knee counts, bit-exact against the oracle."""
+    if variant.startswith("cfg4"):
+        sp, p = synth.config(4, num_scen=100, variant="batching" if variant == "cfg4_batching" else "default")
+    else:
+        sp, p = synth.config(2, num_scen=150, rows_pct=40)
+        p = p.replace(mem_mode=2, L=148)
+    p = p.replace(below_knee=1, reconf_us=0 if variant == "cfg4_reconf0" else 100)
+    pb = synth.generate_host(sp)
+    g, _ = run_gpu(ds, pb, p)
+    want = oracle.evaluate(pb, p)
+    assert_parity(g, want, where=f"below-knee {variant}")
+    if variant.startswith("cfg4"):
+        assert want["below"].sum() > 0
+
+
+def test_below_knee_split_path_and_edges(ds):
+    """F1 through the call-by-call path (dstack_schedule_cycle recomputes sum R and sum R d from the rows) and on
+    the hand-made edge cases."""
+    sp, p = synth.config(4, num_scen=60)
+    p = p.replace(below_knee=1)
+    pb = synth.generate_host(sp)
+    dp = ds.from_host(pb, "cuda")
+    o = ds.alloc_outputs(dp, agg=False)
+    ws = ds.Workspace(ds.workspace_size(dp, p), dp.device)
+    ds.batch_opt(dp, p, out=o)
+    ds.wmaxmin(dp.scen_dnn_off, p.L, o["demand"], out=o["alloc_q16"])
+    ds.schedule_cycle(dp, p, o["demand"], o["batch"], o["alloc_q16"], out=o, ws=ws)
+    torch.cuda.synchronize()
+    want = oracle.evaluate(pb, p)
+    assert_parity(ds.to_numpy(o, pb.num_scen, pb.num_dnn), want, where="below-knee split")
+    assert want["below"].sum() > 0
+    pe = edge_problem()
+    for q in (Params(L=100, S_tot=148, ideal=1, below_knee=1), Params(L=148, S_tot=148, mem_mode=2, below_knee=1)):
+        g, _ = run_gpu(ds, pe, q)
+        assert_parity(g, oracle.evaluate(pe, q), where="below-knee edge")
