@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--cycles", type=int, default=20, help="config 5: sessions simulated per step")
     ap.add_argument("--no-compare", action="store_true", help="skip the O9 comparison-scheduler leg")
     ap.add_argument("--no-below-knee", action="store_true", help="skip the F1 below-knee fallback leg")
+    ap.add_argument("--no-knee-probe", action="store_true", help="skip the F3 online knee discovery leg")
     return ap.parse_args()
 
 
@@ -293,6 +294,11 @@ def run_native(args, rank, world, local):
     if not args.no_below_knee:
         bk_line = run_below_knee_leg(args, ds, dp, p, out, stream, per_gpu, world)
 
+    # ---- F3 online knee discovery (dstack_knee_probe) over every DNN of the shard, timed separately ----
+    kp_line = None
+    if not args.no_knee_probe:
+        kp_line = run_knee_probe_leg(args, ds, dp, p, stream, world)
+
     # ---- e2e: the public API from pinned host buffers, H2D + compute + D2H of results each step ----
     e2e = None
     if not args.no_e2e:
@@ -344,6 +350,7 @@ def run_native(args, rank, world, local):
         "e2e": e2e,
         "compare": cmp_line,
         "below_knee": bk_line,
+        "knee_probe": kp_line,
         "stats": {"mean_u": agg["sum_u"] / max(agg["n_scen_scheduled"], 1),
                   "mean_u_static": agg["sum_u_static"] / max(agg["n_scen_scheduled"], 1),
                   "scen_status": agg["n_scen_st"], "dnn_status": agg["n_st"],
@@ -418,6 +425,36 @@ def run_below_knee_leg(args, ds, dp, p, out, stream, per_gpu, world):
             "below_knee_runs": int(o["below"].sum().item()), "misses": a1["misses"], "misses_default": a0["misses"],
             "oversubscribed_scenarios": a1["n_scen_st"][4], "oversubscribed_default": a0["n_scen_st"][4],
             "mean_u": a1["sum_u"] / n1, "mean_u_default": a0["sum_u"] / n0}
+
+
+def run_knee_probe_leg(args, ds, dp, p, stream, world):
+    """SURVEY §8(f) item 3 measured: dstack_knee_probe (binary search from 30%) at b = 1 over every
+    DNN, device-timed, with the fraction of DNNs whose probed knee equals Eq. 6's exact knee (dstack_knee)."""
+    import torch
+    import torch.distributed as dist
+    k, pr, st = ds.knee_probe(dp, p, 1)
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 5))
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        k, pr, st = ds.knee_probe(dp, p, 1)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=stream.device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    kx, stx = ds.knee(dp, p, 1)
+    ok = st == 0
+    n_ok = int(ok.sum().item())
+    match = int(((k == kx) & ok).sum().item())
+    return {"api": "paper_2304_13541_b200.dstack.knee_probe (dstack_knee_probe)", "batch": 1, "ms_per_call": ms,
+            "dnns_per_s": dp.num_dnn * world / (ms / 1e3), "dnns_ok": n_ok,
+            "exact_knee_match_frac": match / max(n_ok, 1),
+            "mean_steps": float(pr[ok].float().mean().item()) if n_ok else 0.0,
+            "max_steps": int(pr.max().item()) if dp.num_dnn else 0}
 
 
 def run_e2e(args, sp, p, dev, world):

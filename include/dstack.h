@@ -161,6 +161,18 @@ size_t dstack_workspace_size(const dstack_problem_t *pb, const dstack_params_t *
 int dstack_knee(const dstack_problem_t *pb, const dstack_params_t *p, int32_t batch, uint16_t *knee_out,
                 uint8_t *st_out, void *ws, size_t ws_bytes, void *stream);
 
+/* F3, online knee discovery ("our platform initially provides it a nominal, 30%,
+ * GPU. The GPU% is then readjusted using Dynamic GPU resource reconfiguration to find the knee based on the
+ * inference latency using a simple binary search"; reading R22).  Per DNN at batch b: lo = 1,
+ * hi = L; the first step probes m = ceil(0.3 L), later ones m = floor((lo + hi) / 2), m clamped to
+ * [lo, hi - 1]; each step measures the latency at m and m + 1 and moves lo = m + 1 iff
+ * 1/(f_L(m+1,b)^2 S(m+1)) > 1/(f_L(m,b)^2 S(m)) (Eq. 6's objective, exact), else hi = m; stops at lo == hi.
+ * knee_out[k] = lo (0 unless st_out[k] is OK), probes_out[k] = the number of steps (<= ceil(log2 L) + 1).
+ * The result is a discrete local maximum of Eq. 6's objective; it equals dstack_knee's exact argmax whenever
+ * that objective is unimodal over the levels.  Statuses as dstack_knee.  Device arrays [num_dnn]. */
+int dstack_knee_probe(const dstack_problem_t *pb, const dstack_params_t *p, int32_t batch, uint16_t *knee_out,
+                      uint8_t *probes_out, uint8_t *st_out, void *ws, size_t ws_bytes, void *stream);
+
 /* a1-a3: per DNN (l*, b*) = argmax of eta = b/(f_L^2 GPU%) (Eq. 9) over feasible cells (Eqs. 10-12),
  * ties to smaller l then smaller b; demand = min(L, l* + margin); knee = knee(b*). */
 int dstack_batch_opt(const dstack_problem_t *pb, const dstack_params_t *p, uint16_t *demand, uint8_t *batch,

@@ -68,6 +68,7 @@ def lib():
         L.oracle_X.argtypes = [P(OrProblem), P(OrParams), C.c_int64, C.c_int32, C.c_int32,
                                P(C.c_uint64), P(C.c_uint64)]
         L.oracle_knee.argtypes = [P(OrProblem), P(OrParams), C.c_int32, C.c_void_p, C.c_void_p]
+        L.oracle_knee_probe.argtypes = [P(OrProblem), P(OrParams), C.c_int32] + [C.c_void_p] * 4
         L.oracle_batch_opt.argtypes = [P(OrProblem), P(OrParams)] + [C.c_void_p] * 4
         L.oracle_wmaxmin.argtypes = [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]
         L.oracle_cycle_direct.argtypes = ([C.c_int32] + [C.c_void_p] * 4 + [C.c_int32] * 3 + [C.c_void_p] * 4
@@ -119,6 +120,15 @@ def knee(pb: Problem, p: Params, b: int):
     k = np.zeros(pb.num_dnn, np.uint16); st = np.zeros(pb.num_dnn, np.uint8)
     assert lib().oracle_knee(C.byref(_problem(pb)), C.byref(_params(p)), b, _p(k), _p(st)) == 0
     return k, st
+
+
+def knee_probe(pb: Problem, p: Params, b: int, trace: bool = False):
+    """F3: binary-search knee from the nominal 30%. Returns (knee, probes, status[, trace[D, 16]])."""
+    D = pb.num_dnn
+    k = np.zeros(D, np.uint16); pr = np.zeros(D, np.uint8); st = np.zeros(D, np.uint8)
+    tr = np.full((D, 16), -1, np.int32) if trace else None
+    assert lib().oracle_knee_probe(C.byref(_problem(pb)), C.byref(_params(p)), b, _p(k), _p(pr), _p(st), _p(tr)) == 0
+    return (k, pr, st, tr) if trace else (k, pr, st)
 
 
 def batch_opt(pb: Problem, p: Params):

@@ -179,6 +179,45 @@ int oracle_knee(const or_problem_t *pb, const or_params_t *p, int32_t b, uint16_
   return 0;
 }
 
+/* F3 -- online knee discovery: "our platform initially provides it a nominal, 30%, GPU. The GPU% is
+ * then readjusted ... to find the knee based on the inference latency using a simple binary search."
+ * Reading R22: lo = 1, hi = L; step 1 probes m = ceil(0.3 L), later steps the midpoint
+ * floor((lo + hi) / 2), m kept in [lo, hi - 1]; the latencies at m and m + 1 decide: Eq. 6's objective
+ * g = 1/(f_L^2 S) larger at m + 1 (g(m+1) > g(m) <=> S(m+1) X(m)^2 > S(m) X(m+1)^2) => lo = m + 1, else hi = m.
+ * trace (nullable, >= 16 entries): the probed m of every step. */
+static int64_t knee_probe_of(const dnn_t *m, const or_params_t *p, int64_t b, int32_t *steps, int32_t *trace) {
+  int64_t lo = 1, hi = p->L;
+  int32_t n = 0;
+  while (lo < hi) {
+    int64_t mid = n == 0 ? (3 * (int64_t)p->L + 9) / 10 : (lo + hi) / 2;
+    if (mid < lo) mid = lo;
+    if (mid > hi - 1) mid = hi - 1;
+    const int64_t S0 = S_of(p, mid), S1 = S_of(p, mid + 1);
+    const u128 X0 = X_of(m, p, S0, b), X1 = X_of(m, p, S1, b);
+    if (trace && n < 16) trace[n] = (int32_t)mid;
+    if ((u128)S1 * X0 * X0 > (u128)S0 * X1 * X1) lo = mid + 1; else hi = mid;
+    ++n;
+  }
+  *steps = n;
+  return lo;
+}
+
+int oracle_knee_probe(const or_problem_t *pb, const or_params_t *p, int32_t b, uint16_t *knee_out, uint8_t *probes_out,
+                      uint8_t *st_out, int32_t *trace) {
+  if (!pb || !p || b < 1) return -1;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t k = 0; k < pb->num_dnn; ++k) {
+    dnn_t m = get_dnn(pb, p, k);
+    int st = validate_basic(&m, p);
+    if (st == OR_OK && X_of(&m, p, S_of(p, p->L), b) >= X_LIMIT) st = OR_OVERFLOW;
+    st_out[k] = (uint8_t)st;
+    int32_t steps = 0;
+    knee_out[k] = (st == OR_OK) ? (uint16_t)knee_probe_of(&m, p, b, &steps, trace ? trace + 16 * k : NULL) : 0;
+    probes_out[k] = (uint8_t)steps;
+  }
+  return 0;
+}
+
 int oracle_batch_opt(const or_problem_t *pb, const or_params_t *p, uint16_t *demand, uint8_t *batch,
                      uint16_t *knee, uint8_t *status) {
   if (!pb || !p) return -1;

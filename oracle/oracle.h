@@ -64,6 +64,10 @@ int oracle_X(const or_problem_t *pb, const or_params_t *p, int64_t dnn, int32_t 
              uint64_t *lo, uint64_t *hi);
 /* O2: knee(b) for every DNN (Eq. 6); st_out gets the validation status (knee valid iff OK). */
 int oracle_knee(const or_problem_t *pb, const or_params_t *p, int32_t b, uint16_t *knee_out, uint8_t *st_out);
+/* F3: online knee discovery by binary search from 30%.  probes_out = steps;
+ * trace (nullable): [num_dnn * 16] probed levels per step. */
+int oracle_knee_probe(const or_problem_t *pb, const or_params_t *p, int32_t b, uint16_t *knee_out, uint8_t *probes_out,
+                      uint8_t *st_out, int32_t *trace);
 /* O3: batch/GPU% optimisation (Eqs. 7-12) for every DNN. */
 int oracle_batch_opt(const or_problem_t *pb, const or_params_t *p, uint16_t *demand, uint8_t *batch,
                      uint16_t *knee, uint8_t *status);

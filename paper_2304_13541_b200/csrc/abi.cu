@@ -165,6 +165,24 @@ int dstack_knee(const dstack_problem_t *pb, const dstack_params_t *p, int32_t ba
   return finish(launch_prof(a, (cudaStream_t)stream, &g_launches));
 }
 
+int dstack_knee_probe(const dstack_problem_t *pb, const dstack_params_t *p, int32_t batch, uint16_t *knee_out,
+                      uint8_t *probes_out, uint8_t *st_out, void *ws, size_t ws_bytes, void *stream) {
+  (void)ws; (void)ws_bytes;
+  g_launches = 0;
+  if (!problem_ok(pb) || !params_ok(p) || batch < 1 || batch > DSTACK_MAX_BATCH) return DSTACK_EINVAL;
+  if (pb->num_dnn > 0 && (!knee_out || !probes_out || !st_out)) return DSTACK_EINVAL;
+  if (!disjoint(pb, knee_out) || !disjoint(pb, probes_out) || !disjoint(pb, st_out)) return DSTACK_EINVAL;
+  if ((const void *)knee_out == (const void *)probes_out || (const void *)knee_out == (const void *)st_out ||
+      (const void *)probes_out == (const void *)st_out)
+    return DSTACK_EINVAL;
+  if (!have_device()) return DSTACK_ELAUNCH;
+  ProfArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.pb = *pb; a.p = *p; a.knee_only = 1; a.knee_b = batch; a.knee = knee_out; a.status = st_out;
+  a.probes = probes_out;
+  return finish(launch_knee_probe(a, (cudaStream_t)stream, &g_launches));
+}
+
 int dstack_batch_opt(const dstack_problem_t *pb, const dstack_params_t *p, uint16_t *demand, uint8_t *batch,
                      uint16_t *knee, uint8_t *status, void *ws, size_t ws_bytes, void *stream) {
   (void)ws; (void)ws_bytes;

@@ -26,6 +26,7 @@ struct ProfArgs {
   uint8_t *batch;
   uint16_t *knee;
   uint8_t *status;
+  uint8_t *probes;     // dstack_knee_probe (F3): non-NULL => knee = the binary-search result, probes = its steps
   // eval path extras (workspace, may be NULL): d_j(b) at g = demand for b in [b_lo, b*], RT, D
   uint16_t *dtab_rows;
   uint32_t *ws_RT;
@@ -105,6 +106,7 @@ struct AggArgs {
 };
 
 int launch_prof(const ProfArgs &a, cudaStream_t s, int *launches);
+int launch_knee_probe(const ProfArgs &a, cudaStream_t s, int *launches);
 int launch_wmaxmin(int32_t num_scen, const int32_t *off, int32_t L, const uint16_t *demand, uint32_t *alloc,
                    cudaStream_t s, int *launches);
 int launch_cycle(const CycArgs &a, cudaStream_t s, int *launches);

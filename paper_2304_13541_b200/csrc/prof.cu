@@ -24,11 +24,45 @@ __host__ __device__ inline size_t prof_warp_bytes(int S_tot) {
 #define DSTACK_PROF_FAST 1   // 0: every launch takes the generic kernel (A/B switch)
 #endif
 
+// F3, online knee discovery: from the nominal level ceil(0.3 L), a binary search over
+// l in [1, L] that compares the Eq. 6 objective g(l) = 1/(f_L(l,b)^2 S(l)) of adjacent levels m, m+1 (two latency
+// measurements per step): g(m+1) > g(m) <=> S(m+1) X(m)^2 > S(m) X(m+1)^2 (exact, u128) moves right, else left.
+// X from the DNN's O(1) tables (valid after analyze_dnn at batch b).  Warp-uniform; returns knee | steps << 16.
+template <int PAR>
+__device__ __forceinline__ uint32_t knee_probe_search(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k,
+                                                      const uint16_t *Stab, const uint64_t *cA, const uint64_t *cU,
+                                                      uint64_t RT, uint64_t D, int32_t b) {
+  const uint64_t M = p.mem_mode == 0 ? 1ull : (uint64_t)pb.mem_bw[k];
+  const uint64_t wC1 = (p.wse_mode == 0 ? (uint64_t)b : 1ull) * (uint64_t)pb.t_np[k] * RT * M;
+  const uint32_t magic = magic_of(b);
+  int32_t lo = 1, hi = p.L, steps = 0;
+  int32_t m = (3 * p.L + 9) / 10;   // ceil(0.3 L): the nominal 30% start
+  while (lo < hi) {
+    if (steps > 0) m = (lo + hi) >> 1;
+    m = m < lo ? lo : (m > hi - 1 ? hi - 1 : m);
+    const int32_t S0 = Stab[m], S1 = Stab[m + 1];
+    const uint64_t X0 = cell_X<PAR>(S0, b, magic, wC1, cA, cU, p.mem_mode, D);
+    const uint64_t X1 = cell_X<PAR>(S1, b, magic, wC1, cA, cU, p.mem_mode, D);
+    const bool right = (u128)(uint32_t)S1 * ((u128)X0 * X0) > (u128)(uint32_t)S0 * ((u128)X1 * X1);
+    if (right) lo = m + 1; else hi = m;
+    ++steps;
+  }
+  return (uint32_t)lo | ((uint32_t)steps << 16);
+}
+
 // generic per-DNN analysis and its outputs
 template <int PAR>
 __device__ __forceinline__ void prof_one(const ProfArgs &a, int64_t k, const uint16_t *Stab, uint32_t *hist,
                                          uint64_t *cA, uint64_t *cU, int lane) {
-  const DnnRes r = analyze_dnn<PAR>(a.pb, a.p, k, Stab, hist, cA, cU, lane, a.knee_only, a.knee_b);
+  DnnRes r = analyze_dnn<PAR>(a.pb, a.p, k, Stab, hist, cA, cU, lane, a.knee_only, a.knee_b);
+  if (a.probes) {   // F3: the probe's knee replaces Eq. 6's exact argmax
+    uint32_t steps = 0;
+    if (r.st == DSTACK_ST_OK) {
+      const uint32_t v = knee_probe_search<PAR>(a.pb, a.p, k, Stab, cA, cU, r.RT, r.D, a.knee_b);
+      r.knee = (uint16_t)(v & 0xFFFFu); steps = v >> 16;
+    }
+    if (lane == 0) a.probes[k] = (uint8_t)steps;
+  }
   if (a.dtab_rows && r.st == DSTACK_ST_OK) {   // eval path: d_j(b) at g = demand, b in [b_lo, b*]
     if (PAR == 0)
       dtab_from_tables(a.pb, a.p, k, cA, cU, r.RT, r.D, r.demand, a.p.b_min, r.b, a.dtab_rows + k * DTAB_ROW, lane);
@@ -438,6 +472,19 @@ int launch_prof(const ProfArgs &a, cudaStream_t s, int *launches) {
   if (fast && a.p.S_tot < 5 * 32) launch_k(k_prof_fast<5>, a, blocks, threads, smem, s);
   else if (fast) launch_k(k_prof_fast<9>, a, blocks, threads, smem, s);
   else if (a.p.par_mode == 0) launch_k(k_prof<0>, a, blocks, threads, smem, s);
+  else launch_k(k_prof<1>, a, blocks, threads, smem, s);
+  ++*launches;
+  return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;
+}
+
+int launch_knee_probe(const ProfArgs &a, cudaStream_t s, int *launches) {
+  if (a.pb.num_dnn <= 0) return 0;
+  const int threads = 256, warps = threads / 32;
+  const size_t smem = prof_smem_bytes(&a.p, warps);
+  int64_t blocks = (a.pb.num_dnn + warps - 1) / warps;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (a.p.par_mode == 0) launch_k(k_prof<0>, a, blocks, threads, smem, s);
   else launch_k(k_prof<1>, a, blocks, threads, smem, s);
   ++*launches;
   return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;

@@ -80,6 +80,8 @@ def _load():
     lib.dstack_workspace_size.restype = C.c_size_t
     lib.dstack_knee.argtypes = [P(CProblem), P(CParams), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                 C.c_size_t, C.c_void_p]
+    lib.dstack_knee_probe.argtypes = [P(CProblem), P(CParams), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_size_t, C.c_void_p]
     lib.dstack_batch_opt.argtypes = [P(CProblem), P(CParams)] + [C.c_void_p] * 5 + [C.c_size_t, C.c_void_p]
     lib.dstack_wmaxmin.argtypes = [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.dstack_schedule_cycle.argtypes = [P(CProblem), P(CParams), C.c_void_p, C.c_void_p, C.c_void_p, P(CHook),
@@ -101,7 +103,7 @@ def _load():
 _lib = _load()
 
 # every symbol include/dstack.h declares (checked by tests/test_abi.py)
-EXPORTS = ("dstack_workspace_size", "dstack_knee", "dstack_batch_opt", "dstack_wmaxmin", "dstack_schedule_cycle",
+EXPORTS = ("dstack_workspace_size", "dstack_knee", "dstack_knee_probe", "dstack_batch_opt", "dstack_wmaxmin", "dstack_schedule_cycle",
            "dstack_eval_batch", "dstack_aggregate", "dstack_sim_workspace_size", "dstack_simulate",
            "dstack_compare", "dstack_profile_start", "dstack_profile_stop",
            "dstack_last_launch_count", "dstack_status_str", "dstack_version")
@@ -215,6 +217,17 @@ def knee(dp: DeviceProblem, p, batch: int):
     _check(_lib.dstack_knee(C.byref(dp.c()), C.byref(cparams(p)), batch, _ptr(k), _ptr(st), None, 0,
                             _stream(dev)), "dstack_knee")
     return k[: dp.num_dnn], st[: dp.num_dnn]
+
+
+def knee_probe(dp: DeviceProblem, p, batch: int):
+    """dstack_knee_probe (F3, online knee discovery): (knee u16-in-int16, probes u8, status u8) device tensors."""
+    dev = dp.device
+    k = torch.zeros(max(dp.num_dnn, 1), dtype=torch.int16, device=dev)
+    pr = torch.zeros(max(dp.num_dnn, 1), dtype=torch.uint8, device=dev)
+    st = torch.zeros(max(dp.num_dnn, 1), dtype=torch.uint8, device=dev)
+    _check(_lib.dstack_knee_probe(C.byref(dp.c()), C.byref(cparams(p)), batch, _ptr(k), _ptr(pr), _ptr(st), None, 0,
+                                  _stream(dev)), "dstack_knee_probe")
+    return k[: dp.num_dnn], pr[: dp.num_dnn], st[: dp.num_dnn]
 
 
 def batch_opt(dp: DeviceProblem, p, out=None):

@@ -411,3 +411,31 @@ def test_below_knee_split_path_and_edges(ds):
     for q in (Params(L=100, S_tot=148, ideal=1, below_knee=1), Params(L=148, S_tot=148, mem_mode=2, below_knee=1)):
         g, _ = run_gpu(ds, pe, q)
         assert_parity(g, oracle.evaluate(pe, q), where="below-knee edge")
+
+
+# ---------------------------------------------------------------- F3 online knee discovery ---
+
+def test_knee_probe_parity(ds):
+    """F3 (dstack_knee_probe): knee found by the binary search from 30%, its step count and the
+    statuses bit-exact against the oracle, in every model mode, with L < S_tot, L = S_tot and L > S_tot."""
+    sp, p = synth.config(2, num_scen=80, rows_pct=30)
+    pb = synth.generate_host(sp)
+    dp = ds.from_host(pb, "cuda")
+    pbt = synth.generate_host(sp.replace(threads=1))
+    dpt = ds.from_host(pbt, "cuda")
+    for pp in (p, p.replace(mem_mode=2), p.replace(mem_mode=0, L=148), p.replace(L=200, S_tot=148),
+               p.replace(par_mode=1, wse_mode=1), p.replace(wse_mode=1, L=37)):
+        pbx, dpx = (pbt, dpt) if pp.par_mode == 1 else (pb, dp)
+        for b in (1, 3, 16, 64):
+            k, pr, st = ds.knee_probe(dpx, pp, b)
+            ko, pro, sto = oracle.knee_probe(pbx, pp, b)
+            assert np.array_equal(st.cpu().numpy(), sto), (b, pp)
+            assert np.array_equal(k.cpu().numpy().view(np.uint16), ko), (b, pp)
+            assert np.array_equal(pr.cpu().numpy(), pro), (b, pp)
+    pe = edge_problem()
+    dpe = ds.from_host(pe, "cuda")
+    q = Params(L=100, S_tot=148)
+    k, pr, st = ds.knee_probe(dpe, q, 2)
+    ko, pro, sto = oracle.knee_probe(pe, q, 2)
+    assert np.array_equal(st.cpu().numpy(), sto) and np.array_equal(k.cpu().numpy().view(np.uint16), ko)
+    assert np.array_equal(pr.cpu().numpy(), pro)
