@@ -82,6 +82,7 @@ def lib():
         L.oracle_gslice_direct.argtypes = ([C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]
                                            + [C.c_void_p] * 5)
         L.oracle_compare.argtypes = [P(OrProblem), P(OrParams)] + [C.c_void_p] * 4 + [C.c_int64, C.c_int32]
+        L.oracle_cluster.argtypes = [P(OrProblem), P(OrParams), C.c_int32] + [C.c_void_p] * 3 + [C.c_int64, C.c_int32]
         L.oracle_simulate.argtypes = [P(OrProblem), P(OrParams), C.c_void_p, C.c_int32, C.c_uint64, C.c_int32,
                                       C.c_int64, P(OrSimOut), C.c_void_p, C.c_int64, C.c_int32]
         L.oracle_ideal_direct.argtypes = ([C.c_int32] + [C.c_void_p] * 6 + [C.c_int32, C.c_int64]
@@ -239,6 +240,21 @@ def compare(pb: Problem, p: Params, nthreads: int = 0, subset=None):
                               0 if idx is None else idx.shape[0], nthreads)
     assert rc == 0
     return dict(u=u, thr=thr, jain=jain)
+
+
+CLUSTER_NAMES = ("exclusive", "temporal", "dstack", "dstack_ffd")
+
+
+def cluster(pb: Problem, p: Params, G: int, nthreads: int = 0, subset=None):
+    """F4: multi-GPU cluster policies of §7.1 over G modelled GPUs; dict u, thr of shape [num_scen, 4]
+    (columns CLUSTER_NAMES)."""
+    S = pb.num_scen
+    u = np.zeros((S, 4), np.float64); thr = np.zeros((S, 4), np.float64)
+    idx = None if subset is None else np.ascontiguousarray(np.asarray(list(subset)), np.int64)
+    rc = lib().oracle_cluster(C.byref(_problem(pb)), C.byref(_params(p)), G, _p(u), _p(thr), _p(idx),
+                              0 if idx is None else idx.shape[0], nthreads)
+    assert rc == 0
+    return dict(u=u, thr=thr)
 
 
 def ideal_direct(chains, slo_us, active, L: int, T_us: int, bstar=None):

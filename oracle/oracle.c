@@ -822,9 +822,10 @@ static double jain_of(const int64_t *x, int32_t n, const int32_t *act) {
   return den ? (double)num / (double)den : 0.0;   /* Jain's index (sum x)^2 / (n sum x^2) */
 }
 
-static void compare_scenario(const or_problem_t *pb, const or_params_t *p, int64_t s, double *u, double *thr,
-                             double *jain) {
-  for (int c = 0; c < 5; ++c) { u[s * 5 + c] = 0; thr[s * 5 + c] = 0; jain[s * 5 + c] = 0; }
+/* scenario s's five columns into u[0..4], thr[0..4], jain[0..4] */
+static void compare_one(const or_problem_t *pb, const or_params_t *p, int64_t s, double *u, double *thr,
+                        double *jain) {
+  for (int c = 0; c < 5; ++c) { u[c] = 0; thr[c] = 0; jain[c] = 0; }
   const int32_t k0 = pb->scen_dnn_off[s], nd = pb->scen_dnn_off[s + 1] - k0;
   if (nd <= 0 || nd > OR_MAX_DNN_PER_SCEN) return;
   uint16_t dem[OR_MAX_DNN_PER_SCEN], knee[OR_MAX_DNN_PER_SCEN];
@@ -875,27 +876,32 @@ static void compare_scenario(const or_problem_t *pb, const or_params_t *p, int64
     or_cyc_sum_t cs;
     cycle_core(nd, g, sl, bst, dtab, p->b_min, p->L, (int32_t)nslots, NULL, runs, served, jmiss, &cs, 0, NULL, NULL,
                NULL, NULL, NULL, NULL, NULL, NULL, c, busy, NULL, NULL);
-    u[s * 5 + c] = (double)cs.occ_sum / NL;
-    thr[s * 5 + c] = (double)cs.served_total * 1e6 / (double)T;
-    jain[s * 5 + c] = jain_of(busy, nd, act);
+    u[c] = (double)cs.occ_sum / NL;
+    thr[c] = (double)cs.served_total * 1e6 / (double)T;
+    jain[c] = jain_of(busy, nd, act);
   }
   {
     int64_t slice[OR_MAX_DNN_PER_SCEN], runs[OR_MAX_DNN_PER_SCEN], occn = 0, srv = 0;
     oracle_temporal_direct(nd, lvl, sl, dL, (int32_t)nslots, slice, runs, &occn);
     for (int32_t j = 0; j < nd; ++j) srv += runs[j] * bst[j];
-    u[s * 5 + 3] = (double)occn / NL;
-    thr[s * 5 + 3] = (double)srv * 1e6 / (double)T;
-    jain[s * 5 + 3] = jain_of(slice, nd, act);
+    u[3] = (double)occn / NL;
+    thr[3] = (double)srv * 1e6 / (double)T;
+    jain[3] = jain_of(slice, nd, act);
   }
   {
     int32_t home[OR_MAX_DNN_PER_SCEN], K = 0;
     int64_t runs[OR_MAX_DNN_PER_SCEN], busy[OR_MAX_DNN_PER_SCEN], occn = 0, srv = 0;
     oracle_gslice_direct(nd, lvl, dk, (int32_t)nslots, p->L, home, &K, runs, busy, &occn);
     for (int32_t j = 0; j < nd; ++j) srv += runs[j] * bst[j];
-    u[s * 5 + 4] = (double)occn / NL;
-    thr[s * 5 + 4] = (double)srv * 1e6 / (double)T;
-    jain[s * 5 + 4] = jain_of(busy, nd, act);
+    u[4] = (double)occn / NL;
+    thr[4] = (double)srv * 1e6 / (double)T;
+    jain[4] = jain_of(busy, nd, act);
   }
+}
+
+static void compare_scenario(const or_problem_t *pb, const or_params_t *p, int64_t s, double *u, double *thr,
+                             double *jain) {
+  compare_one(pb, p, s, u + s * 5, thr + s * 5, jain + s * 5);
 }
 
 int oracle_compare(const or_problem_t *pb, const or_params_t *p, double *u, double *thr, double *jain,
@@ -907,6 +913,145 @@ int oracle_compare(const or_problem_t *pb, const or_params_t *p, double *u, doub
   const int64_t n = idx ? count : pb->num_scen;
 #pragma omp parallel for schedule(dynamic, 1)
   for (int64_t q = 0; q < n; ++q) compare_scenario(pb, p, idx ? idx[q] : q, u, thr, jain);
+  return 0;
+}
+
+/* ---------------------------------------------------------------- F4 ---
+ * Multi-GPU cluster of §7.1 (reading R23): G modelled GPUs
+ * of L levels each serve the scenario's active models (status OK).  out[s*4 + c]:
+ *  c = 0 exclusive ("one T4 GPU for each DNN model exclusively"): the q-th active model (index order) runs on
+ *        GPU q mod G; a GPU holding several models shares them temporally (O9 temporal on its subset);
+ *  c = 1 temporal ("all 4 models in each GPU, temporally sharing the GPU"): every GPU runs O9 temporal over all
+ *        models, the load spread over the G replicas;
+ *  c = 2 D-STACK on every GPU ("D-STACK with the 4 DNN models"): every GPU runs the O5 session over all models;
+ *  c = 3 D-STACK with placement: models first-fit decreasing by demand (desc, index) onto GPUs of capacity L,
+ *        a model that fits nowhere to the least-loaded GPU (lowest index on ties); each GPU runs WMAX-MIN (O4) and
+ *        one O5 session over its subset.
+ * Per GPU i with a non-empty subset: T_i = max SLO over it, nslots_i = T_i / Delta, U_i = occupied level-slots /
+ * (nslots_i L), throughput_i = served * 1e6 / T_i.  Cluster: U = sum_i U_i / G (an idle GPU counts 0),
+ * throughput = sum_i throughput_i. */
+static void cluster_scenario(const or_problem_t *pb, const or_params_t *p, int32_t G, int64_t s, double *u,
+                             double *thr) {
+  for (int c = 0; c < 4; ++c) { u[s * 4 + c] = 0; thr[s * 4 + c] = 0; }
+  const int32_t k0 = pb->scen_dnn_off[s], nd = pb->scen_dnn_off[s + 1] - k0;
+  if (nd <= 0 || nd > OR_MAX_DNN_PER_SCEN) return;
+  uint16_t dem[OR_MAX_DNN_PER_SCEN], knee[OR_MAX_DNN_PER_SCEN];
+  uint8_t bt[OR_MAX_DNN_PER_SCEN], st[OR_MAX_DNN_PER_SCEN];
+  int32_t sl[OR_MAX_DNN_PER_SCEN];
+  for (int32_t j = 0; j < nd; ++j) {
+    dnn_t m = get_dnn(pb, p, k0 + j);
+    batch_opt_one(&m, p, dem + j, bt + j, knee + j, st + j);
+    if (st[j] != OR_OK) dem[j] = 0;
+    sl[j] = pb->slo_us[k0 + j] / p->slot_us;
+  }
+  int64_t T = 0;
+  for (int32_t j = 0; j < nd; ++j) if (dem[j] > 0 && pb->slo_us[k0 + j] > T) T = pb->slo_us[k0 + j];
+  if (T == 0) return;
+  {
+    const int64_t nslots = T / p->slot_us;
+    int64_t njobs = 0;
+    for (int32_t j = 0; j < nd; ++j) if (dem[j] > 0) njobs += nslots / sl[j];
+    if (nslots > OR_MAX_SLOTS || njobs > OR_MAX_JOBS) return;   /* the scenario is INVALID for the session */
+  }
+  /* c = 1, 2: every GPU runs the whole mix: the single-GPU O9 temporal / D-STACK numbers, G replicas */
+  {
+    double cu[5], ct[5], cj[5];
+    compare_one(pb, p, s, cu, ct, cj);
+    u[s * 4 + 1] = cu[3]; thr[s * 4 + 1] = (double)G * ct[3];
+    u[s * 4 + 2] = cu[0]; thr[s * 4 + 2] = (double)G * ct[0];
+  }
+  /* placements for c = 0 (round robin over active models) and c = 3 (first-fit decreasing by demand) */
+  int32_t home0[OR_MAX_DNN_PER_SCEN], home3[OR_MAX_DNN_PER_SCEN];
+  {
+    int32_t q = 0;
+    for (int32_t j = 0; j < nd; ++j) home0[j] = dem[j] > 0 ? (q++) % G : -1;
+    int32_t ord[OR_MAX_DNN_PER_SCEN], na = 0;
+    for (int32_t j = 0; j < nd; ++j) { home3[j] = -1; if (dem[j] > 0) ord[na++] = j; }
+    for (int32_t i = 1; i < na; ++i) {   /* (demand desc, index asc) */
+      int32_t v = ord[i], k = i - 1;
+      while (k >= 0 && (dem[ord[k]] < dem[v] || (dem[ord[k]] == dem[v] && ord[k] > v))) { ord[k + 1] = ord[k]; --k; }
+      ord[k + 1] = v;
+    }
+    int64_t load[64] = {0};
+    for (int32_t i = 0; i < na; ++i) {
+      const int32_t j = ord[i];
+      int32_t gi = -1;
+      for (int32_t c = 0; c < G; ++c) if (load[c] + dem[j] <= p->L) { gi = c; break; }   /* first fit */
+      if (gi < 0) { gi = 0; for (int32_t c = 1; c < G; ++c) if (load[c] < load[gi]) gi = c; }   /* least loaded */
+      home3[j] = gi;
+      load[gi] += dem[j];
+    }
+  }
+  for (int32_t gi = 0; gi < G; ++gi) {
+    /* c = 0: O9 temporal over the models on GPU gi */
+    {
+      int64_t Ti = 0;
+      for (int32_t j = 0; j < nd; ++j) if (home0[j] == gi && pb->slo_us[k0 + j] > Ti) Ti = pb->slo_us[k0 + j];
+      if (Ti > 0) {
+        const int32_t ns = (int32_t)(Ti / p->slot_us);
+        int32_t lvl[OR_MAX_DNN_PER_SCEN];
+        int64_t dL[OR_MAX_DNN_PER_SCEN], slice[OR_MAX_DNN_PER_SCEN], runs[OR_MAX_DNN_PER_SCEN], occn = 0, srv = 0;
+        for (int32_t j = 0; j < nd; ++j) {
+          lvl[j] = home0[j] == gi ? dem[j] : 0;
+          dL[j] = 0;
+          if (!lvl[j]) continue;
+          dnn_t m = get_dnn(pb, p, k0 + j);
+          const u128 denL = (u128)p->S_tot * (u128)m.M * (u128)p->slot_us;   /* b* batch at 100% GPU */
+          dL[j] = (int64_t)((X_of(&m, p, p->S_tot, bt[j]) + denL - 1) / denL);
+        }
+        oracle_temporal_direct(nd, lvl, sl, dL, ns, slice, runs, &occn);
+        for (int32_t j = 0; j < nd; ++j) srv += runs[j] * bt[j];
+        u[s * 4 + 0] += (double)occn / ((double)ns * (double)p->L) / (double)G;
+        thr[s * 4 + 0] += (double)srv * 1e6 / (double)Ti;
+      }
+    }
+    /* c = 3: WMAX-MIN and one D-STACK session over the models placed on GPU gi */
+    {
+      int64_t Ti = 0;
+      for (int32_t j = 0; j < nd; ++j) if (home3[j] == gi && pb->slo_us[k0 + j] > Ti) Ti = pb->slo_us[k0 + j];
+      if (Ti > 0) {
+        const int32_t ns = (int32_t)(Ti / p->slot_us);
+        uint16_t sd[OR_MAX_DNN_PER_SCEN];
+        uint32_t sa[OR_MAX_DNN_PER_SCEN];
+        int32_t idx[OR_MAX_DNN_PER_SCEN], nsub = 0;
+        for (int32_t j = 0; j < nd; ++j) if (home3[j] == gi) { idx[nsub] = j; sd[nsub] = dem[j]; ++nsub; }
+        oracle_wmaxmin(nsub, sd, p->L, sa);
+        int32_t g[OR_MAX_DNN_PER_SCEN], bst[OR_MAX_DNN_PER_SCEN];
+        int64_t dtab[OR_MAX_DNN_PER_SCEN * 64];
+        for (int32_t j = 0; j < nd; ++j) { g[j] = 0; bst[j] = bt[j] > 0 ? bt[j] : 1; }
+        for (int32_t q = 0; q < nsub; ++q) {
+          const int32_t j = idx[q];
+          const int32_t al = (int32_t)(sa[q] >> 16);
+          g[j] = dem[j] > al ? dem[j] : al;
+          dnn_t m = get_dnn(pb, p, k0 + j);
+          const int64_t S = S_of(p, g[j]);
+          const u128 den = (u128)S * (u128)m.M * (u128)p->slot_us;
+          for (int32_t b = p->b_min; b <= bt[j]; ++b) {
+            const u128 dd = (X_of(&m, p, S, b) + den - 1) / den;
+            dtab[j * 64 + b - 1] = dd > (u128)0x7FFFFFFFFFFFLL ? 0x7FFFFFFFFFFFLL : (int64_t)dd;
+          }
+        }
+        int32_t runs[OR_MAX_DNN_PER_SCEN], jmiss[OR_MAX_DNN_PER_SCEN];
+        int64_t served[OR_MAX_DNN_PER_SCEN];
+        or_cyc_sum_t cs;
+        cycle_core(nd, g, sl, bst, dtab, p->b_min, p->L, ns, NULL, runs, served, jmiss, &cs, 0, NULL, NULL, NULL, NULL,
+                   NULL, NULL, NULL, NULL, 0, NULL, NULL, NULL);
+        u[s * 4 + 3] += (double)cs.occ_sum / ((double)ns * (double)p->L) / (double)G;
+        thr[s * 4 + 3] += (double)cs.served_total * 1e6 / (double)Ti;
+      }
+    }
+  }
+}
+
+int oracle_cluster(const or_problem_t *pb, const or_params_t *p, int32_t G, double *u, double *thr,
+                   const int64_t *idx, int64_t count, int32_t nthreads) {
+  if (!pb || !p || !u || !thr || check_params(p) || G < 1 || G > 64) return -1;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+  const int64_t n = idx ? count : pb->num_scen;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t q = 0; q < n; ++q) cluster_scenario(pb, p, G, idx ? idx[q] : q, u, thr);
   return 0;
 }
 

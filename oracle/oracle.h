@@ -119,6 +119,12 @@ int oracle_gslice_direct(int32_t n, const int32_t *lvl, const int64_t *dk, int32
 int oracle_compare(const or_problem_t *pb, const or_params_t *p, double *u, double *thr, double *jain,
                    const int64_t *idx, int64_t count, int32_t nthreads);
 
+/* F4 multi-GPU cluster of §7.1: G modelled GPUs; out[s*4 + c], c = 0 exclusive (round robin,
+ * temporal within a GPU), 1 temporal on every GPU, 2 D-STACK on every GPU, 3 D-STACK with first-fit-decreasing
+ * placement; U = mean over the G GPUs, throughput = sum (req/s). */
+int oracle_cluster(const or_problem_t *pb, const or_params_t *p, int32_t G, double *u, double *thr,
+                   const int64_t *idx, int64_t count, int32_t nthreads);
+
 /* O6 with direct per-DNN chains (test hook; also used internally).
  * chain_off[j]..chain_off[j+1] index executions (g_e levels, tau_e us) of DNN j's batch,
  * slo_us[j], bstar[j]; active[j] != 0.  Returns util (sum g*dt) and completed batches. */
