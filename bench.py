@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-compare", action="store_true", help="skip the O9 comparison-scheduler leg")
     ap.add_argument("--no-below-knee", action="store_true", help="skip the F1 below-knee fallback leg")
     ap.add_argument("--no-knee-probe", action="store_true", help="skip the F3 online knee discovery leg")
+    ap.add_argument("--no-cluster", action="store_true", help="skip the F4 multi-GPU cluster leg")
+    ap.add_argument("--cluster-gpus", type=int, default=4, help="F4: modelled GPUs per scenario (paper: 4 x T4)")
     return ap.parse_args()
 
 
@@ -294,6 +296,11 @@ def run_native(args, rank, world, local):
     if not args.no_below_knee:
         bk_line = run_below_knee_leg(args, ds, dp, p, out, stream, per_gpu, world)
 
+    # ---- F4 multi-GPU cluster policies of §7.1 (dstack_cluster) on this step's a3 outputs, timed separately ----
+    clu_line = None
+    if not args.no_cluster:
+        clu_line = run_cluster_leg(args, ds, dp, p, out, ws, stream, per_gpu, world)
+
     # ---- F3 online knee discovery (dstack_knee_probe) over every DNN of the shard, timed separately ----
     kp_line = None
     if not args.no_knee_probe:
@@ -351,6 +358,7 @@ def run_native(args, rank, world, local):
         "compare": cmp_line,
         "below_knee": bk_line,
         "knee_probe": kp_line,
+        "cluster": clu_line,
         "stats": {"mean_u": agg["sum_u"] / max(agg["n_scen_scheduled"], 1),
                   "mean_u_static": agg["sum_u_static"] / max(agg["n_scen_scheduled"], 1),
                   "scen_status": agg["n_scen_st"], "dnn_status": agg["n_st"],
@@ -425,6 +433,36 @@ def run_below_knee_leg(args, ds, dp, p, out, stream, per_gpu, world):
             "below_knee_runs": int(o["below"].sum().item()), "misses": a1["misses"], "misses_default": a0["misses"],
             "oversubscribed_scenarios": a1["n_scen_st"][4], "oversubscribed_default": a0["n_scen_st"][4],
             "mean_u": a1["sum_u"] / n1, "mean_u_default": a0["sum_u"] / n0}
+
+
+def run_cluster_leg(args, ds, dp, p, out, ws, stream, per_gpu, world):
+    """SURVEY §8(f) item 4 measured: dstack_cluster (exclusive / temporal / D-STACK replicas / D-STACK with FFD
+    placement on --cluster-gpus modelled GPUs) over the whole workload, device-timed; the means
+    reproduce §7.1's comparison (the paper: D-STACK +160% over temporal on 4 T4s)."""
+    import torch
+    import torch.distributed as dist
+    G = args.cluster_gpus
+    c = ds.cluster(dp, p, G, out["demand"], out["batch"], ws=ws)
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 5))
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        c = ds.cluster(dp, p, G, out["demand"], out["batch"], ws=ws)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=stream.device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ok = c["thr"][:, 1] > 0
+    means = {name: {k: float(c[k][ok, i].mean().item()) for k in ("u", "thr")} for i, name in enumerate(ds.CLU_NAMES)}
+    tt = means["temporal"]["thr"]
+    return {"api": "paper_2304_13541_b200.dstack.cluster (dstack_cluster)", "gpus_modelled": G, "ms_per_call": ms,
+            "scenarios_per_s": per_gpu * world / (ms / 1e3), "policies": list(ds.CLU_NAMES),
+            "means_over_scheduled_scenarios": means,
+            "throughput_vs_temporal": {k: means[k]["thr"] / tt for k in ds.CLU_NAMES} if tt > 0 else None}
 
 
 def run_knee_probe_leg(args, ds, dp, p, stream, world):

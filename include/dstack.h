@@ -240,6 +240,29 @@ int dstack_compare(const dstack_problem_t *pb, const dstack_params_t *p, const u
                    const uint32_t *alloc_q16, double *u, double *thr, double *jain, void *ws, size_t ws_bytes,
                    void *stream);
 
+/* F4 multi-GPU cluster of §7.1 ("one T4 GPU for each DNN model exclusively",
+ * "all 4 models in each GPU, temporally sharing the GPU", "D-STACK with the 4 DNN models"; reading R23,
+ * DESIGN.md §3.5): `gpus` = G modelled GPUs of L levels (1 <= G <= 32) serve each scenario's active models
+ * (demand > 0, from dstack_batch_opt / dstack_eval_batch).  For scenario s and policy c (DSTACK_CLU_*):
+ *   u[s*DSTACK_NCLU + c]   = (1/G) sum over GPUs i with models of occ_i / (nslots_i L)  (idle GPUs count 0)
+ *   thr[s*DSTACK_NCLU + c] = sum over GPUs i of served_i * 1e6 / T_i   (requests/s; T_i = max SLO on GPU i)
+ * c = DSTACK_CLU_EXCLUSIVE: the q-th active model (index order) on GPU q mod G, temporal sharing (as
+ *     DSTACK_CMP_TEMPORAL) among the models that share a GPU (one model per GPU when G >= their number);
+ *     DSTACK_CLU_TEMPORAL: every GPU runs DSTACK_CMP_TEMPORAL over the whole mix (G replicas);
+ *     DSTACK_CLU_DSTACK: every GPU runs the D-STACK session over the whole mix (G replicas);
+ *     DSTACK_CLU_DSTACK_FFD: models first-fit decreasing by (demand desc, index) onto GPUs of L levels, one that
+ *     fits nowhere to the least-loaded GPU (lowest index on ties); each GPU runs WMAX-MIN over its models and
+ *     one D-STACK session.
+ * Scenarios INVALID / INFEASIBLE for the single-GPU session get zeros.  u, thr: device f64 [num_scen * 4].
+ * Workspace: dstack_workspace_size().  DSTACK_FLAG_BELOW_KNEE is rejected (DSTACK_EINVAL). */
+#define DSTACK_CLU_EXCLUSIVE 0
+#define DSTACK_CLU_TEMPORAL 1
+#define DSTACK_CLU_DSTACK 2
+#define DSTACK_CLU_DSTACK_FFD 3
+#define DSTACK_NCLU 4
+int dstack_cluster(const dstack_problem_t *pb, const dstack_params_t *p, int32_t gpus, const uint16_t *demand,
+                   const uint8_t *batch, double *u, double *thr, void *ws, size_t ws_bytes, void *stream);
+
 /* Live per-kernel timing of dstack_eval_batch (bench accounting): after dstack_profile_start, each
  * eval_batch call on this thread records CUDA events on its stream between its kernel launches
  * (slots: 0 k_prof, 1 k_wmaxmin, 2 k_cycle, 3 k_ideal, 4 k_agg).  dstack_profile_stop synchronises

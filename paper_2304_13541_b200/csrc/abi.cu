@@ -373,6 +373,23 @@ int dstack_compare(const dstack_problem_t *pb, const dstack_params_t *p, const u
   return finish(launch_compare(c, (cudaStream_t)stream, &g_launches));
 }
 
+int dstack_cluster(const dstack_problem_t *pb, const dstack_params_t *p, int32_t gpus, const uint16_t *demand,
+                   const uint8_t *batch, double *u, double *thr, void *ws, size_t ws_bytes, void *stream) {
+  g_launches = 0;
+  if (!problem_ok(pb) || !params_ok(p) || (p->flags & DSTACK_FLAG_BELOW_KNEE) || gpus < 1 || gpus > 32)
+    return DSTACK_EINVAL;
+  if (pb->num_dnn > 0 && (!demand || !batch)) return DSTACK_EINVAL;
+  if (pb->num_scen > 0 && (!u || !thr || u == thr)) return DSTACK_EINVAL;
+  const void *outs[] = {u, thr};
+  for (const void *o : outs)
+    if (!disjoint(pb, o) || o == (const void *)demand || o == (const void *)batch) return DSTACK_EINVAL;
+  const size_t need = dstack_workspace_size(pb, p);
+  if (ws_bytes < need || (need > 0 && !ws)) return DSTACK_EWORKSPACE;
+  if (!have_device()) return DSTACK_ELAUNCH;
+  return finish(launch_cluster(*pb, *p, gpus, demand, batch, (uint16_t *)((char *)ws + ws_layout(pb, p).dtab), u, thr,
+                               (cudaStream_t)stream, &g_launches));
+}
+
 int dstack_aggregate(const dstack_problem_t *pb, const dstack_params_t *p, dstack_out_t *out, void *ws,
                      size_t ws_bytes, void *stream) {
   g_launches = 0;

@@ -1,0 +1,179 @@
+// cluster.cu -- F4, the multi-GPU cluster of §7.1 (reading R23 in DESIGN.md
+// §3.5): G modelled GPUs serve each scenario's active models under four policies, one warp per scenario:
+//   c = 0 exclusive: the q-th active model on GPU q mod G, temporal sharing within a GPU;
+//   c = 1 temporal on every GPU (G replicas of the whole mix);
+//   c = 2 D-STACK on every GPU (G replicas: WMAX-MIN over the whole mix + one session);
+//   c = 3 D-STACK with placement: first-fit decreasing by demand onto GPUs of L levels, overflow to the least
+//         loaded; per GPU WMAX-MIN over its subset and one session (cycle_core with the subset active).
+// U = mean over the G GPUs of occupied level-slots / (nslots_i L), throughput = sum of served * 1e6 / T_i.
+// The oracle's F4 (oracle/oracle.c, cluster_scenario) is the parity reference.
+#include "cycle.cuh"
+#include "kernels.cuh"
+#include "prof.cuh"
+
+namespace dstack {
+
+constexpr int CLU_WARPS = 8;
+
+struct CluArgs {
+  dstack_problem_t pb;
+  dstack_params_t p;
+  int32_t G;
+  const uint16_t *demand;
+  const uint8_t *batch;
+  uint16_t *dtab_rows;   // workspace
+  double *u, *thr;       // [num_scen * DSTACK_NCLU]
+};
+
+__global__ void __launch_bounds__(CLU_WARPS * 32) k_cluster(const __grid_constant__ CluArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  CycSmem &sm = reinterpret_cast<CycSmem *>(smem_raw)[warp];
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int32_t L = a.p.L, slot = a.p.slot_us, b_lo = a.p.b_min, G = a.G;
+  const double NLg = (double)L;
+  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < a.pb.num_scen; s += nwarps) {
+    const int32_t k0 = a.pb.scen_dnn_off[s], nd = a.pb.scen_dnn_off[s + 1] - k0;
+    double ou = 0.0, othr = 0.0;   // lane c < 4 holds policy c's results
+    const bool mine = lane < nd && nd <= DSTACK_MAX_DNN_PER_SCEN;
+    const int k = k0 + lane;
+    uint32_t dem = 0, bs = 0, slo = 0, sl = 1;
+    if (mine) { dem = a.demand[k]; bs = a.batch[k]; slo = (uint32_t)a.pb.slo_us[k]; sl = slo / (uint32_t)slot; }
+    const bool active = mine && dem > 0;
+    uint32_t T = nd > DSTACK_MAX_DNN_PER_SCEN ? 0u : __reduce_max_sync(FULL, active ? slo : 0u);
+    int32_t nslots = 0;
+    if (T > 0) {
+      nslots = (int32_t)(T / (uint32_t)slot);
+      const uint32_t njobs = __reduce_add_sync(FULL, active ? (uint32_t)nslots / sl : 0u);
+      if (nslots > DSTACK_MAX_SLOTS || njobs > DSTACK_MAX_JOBS) T = 0;
+    }
+    if (T > 0) {
+      uint16_t *dtab = a.dtab_rows + (int64_t)k0 * DTAB_ROW;
+      // ---- per active model: sum R, sum R d (one row pass) and the b* run at 100% GPU, d^L ----
+      uint64_t RTl = 0, Dl = 0;
+      uint32_t dL = 0;
+      {
+        uint32_t todo = __ballot_sync(FULL, active);
+        while (todo) {
+          const int j = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const int64_t kj = k0 + j;
+          const int64_t r0 = a.pb.dnn_row_off[kj];
+          const int32_t K = (int32_t)(a.pb.dnn_row_off[kj + 1] - r0);
+          uint64_t RT = 0, D = 0;
+          for (int i = lane; i < K; i += 32) { RT += a.pb.r[r0 + i]; D += (uint64_t)a.pb.r[r0 + i] * a.pb.d[r0 + i]; }
+          RT = warp_sum_u64(RT); D = warp_sum_u64(D);
+          const uint64_t M = a.p.mem_mode == 0 ? 1ull : (uint64_t)a.pb.mem_bw[kj];
+          const uint64_t SL = (uint64_t)a.p.S_tot;
+          const uint64_t XL = x_from_rows(a.pb, a.p, kj, RT, D, SL, (int32_t)__shfl_sync(FULL, bs, j), lane);
+          if (lane == j) { RTl = RT; Dl = D; dL = ceil_div_clamp16(XL, SL * M * (uint64_t)slot); }
+        }
+      }
+      // one D-STACK session over the members (WMAX-MIN over their demands first); returns occ | served << 32
+      auto session = [&](bool member, int32_t ns) -> uint64_t {
+        const uint32_t alloc = wmaxmin_lane(member ? dem : 0u, lane, nd, L);
+        const uint32_t al = alloc >> 16;
+        const uint32_t g = member ? (dem > al ? dem : al) : 0u;
+        uint32_t todo = __ballot_sync(FULL, member);
+        while (todo) {
+          const int j = __ffs(todo) - 1;
+          todo &= todo - 1;
+          dtab_from_rows(a.pb, a.p, k0 + j, shfl_u64(RTl, j), shfl_u64(Dl, j), (int32_t)__shfl_sync(FULL, g, j), b_lo,
+                         (int32_t)__shfl_sync(FULL, bs, j), dtab + j * DTAB_ROW, lane);
+        }
+        const uint32_t rep = member ? (uint32_t)ns / sl : 0u;
+        uint32_t runs = 0, served = 0;
+        const CycRes cr = cycle_core(sm, dtab, lane, member, g, bs, sl, rep, ns, L, b_lo, false, runs, served);
+        return (uint64_t)cr.occ_all | ((uint64_t)cr.served_tot << 32);
+      };
+      // temporal sharing over the members (O9): slices proportional to SLO, back-to-back b* runs at 100%
+      auto temporal = [&](bool member, int32_t ns, uint64_t &occn, uint64_t &srv) {
+        const uint64_t tot = warp_sum_u64(member ? (uint64_t)sl : 0ull);
+        const uint64_t slice = member ? (uint64_t)ns * sl / tot : 0ull;
+        const uint64_t truns = member && dL ? slice / dL : 0ull;
+        occn = warp_sum_u64(slice * dem);
+        srv = warp_sum_u64(truns * bs);
+      };
+      const double NL = (double)nslots * (double)L;
+      // ---- c = 1, 2: the whole mix on every GPU ----
+      {
+        uint64_t occn, srv;
+        temporal(active, nslots, occn, srv);
+        const double u1 = (double)occn / NL, t1 = (double)G * ((double)srv * 1e6 / (double)T);
+        const uint64_t r = session(active, nslots);
+        const double u2 = (double)(uint32_t)r / NL, t2 = (double)G * ((double)(r >> 32) * 1e6 / (double)T);
+        if (lane == 1) { ou = u1; othr = t1; }
+        if (lane == 2) { ou = u2; othr = t2; }
+      }
+      // ---- placements: home0 = (rank among active, index order) mod G; home3 = first-fit decreasing ----
+      const uint32_t below = __ballot_sync(FULL, active) & ((1u << lane) - 1u);
+      const int32_t home0 = active ? (int32_t)((uint32_t)__popc(below) % (uint32_t)G) : -1;
+      int32_t home3 = -1;
+      {
+        uint32_t rank = 0;   // (demand desc, index asc) among the active
+        for (int q = 0; q < 32; ++q) {
+          const uint32_t dq = __shfl_sync(FULL, dem, q);
+          const bool aq = __shfl_sync(FULL, (int)active, q) != 0;
+          if (aq && (dq > dem || (dq == dem && q < lane))) ++rank;
+        }
+        const uint32_t na = (uint32_t)__popc(__ballot_sync(FULL, active));
+        uint32_t load = 0;   // lane i < G: GPU i's summed demand
+        for (uint32_t q = 0; q < na; ++q) {
+          const int own = __ffs(__ballot_sync(FULL, active && rank == q)) - 1;
+          const uint32_t dq = __shfl_sync(FULL, dem, own);
+          const uint32_t fit = __ballot_sync(FULL, lane < G && load + dq <= (uint32_t)L);
+          int gi;
+          if (fit) gi = __ffs(fit) - 1;
+          else gi = (int)(__reduce_min_sync(FULL, lane < G ? (load << 5) | (uint32_t)lane : 0xFFFFFFFFu) & 31u);
+          if (lane == gi) load += dq;
+          if (lane == own) home3 = gi;
+        }
+      }
+      double u0 = 0.0, t0 = 0.0, u3 = 0.0, t3 = 0.0;
+      for (int gi = 0; gi < G; ++gi) {
+        {   // c = 0
+          const bool m0 = home0 == gi;
+          const uint32_t Ti = __reduce_max_sync(FULL, m0 ? slo : 0u);
+          if (Ti > 0) {
+            const int32_t ns = (int32_t)(Ti / (uint32_t)slot);
+            uint64_t occn, srv;
+            temporal(m0, ns, occn, srv);
+            u0 += (double)occn / ((double)ns * NLg) / (double)G;
+            t0 += (double)srv * 1e6 / (double)Ti;
+          }
+        }
+        {   // c = 3
+          const bool m3 = home3 == gi;
+          const uint32_t Ti = __reduce_max_sync(FULL, m3 ? slo : 0u);
+          if (Ti > 0) {
+            const int32_t ns = (int32_t)(Ti / (uint32_t)slot);
+            const uint64_t r = session(m3, ns);
+            u3 += (double)(uint32_t)r / ((double)ns * NLg) / (double)G;
+            t3 += (double)(r >> 32) * 1e6 / (double)Ti;
+          }
+        }
+      }
+      if (lane == 0) { ou = u0; othr = t0; }
+      if (lane == 3) { ou = u3; othr = t3; }
+    }
+    if (lane < DSTACK_NCLU) { a.u[s * DSTACK_NCLU + lane] = ou; a.thr[s * DSTACK_NCLU + lane] = othr; }
+    __syncwarp();
+  }
+}
+
+int launch_cluster(const dstack_problem_t &pb, const dstack_params_t &p, int32_t G, const uint16_t *demand,
+                   const uint8_t *batch, uint16_t *dtab_rows, double *u, double *thr, cudaStream_t s, int *launches) {
+  if (pb.num_scen <= 0) return 0;
+  CluArgs a;
+  a.pb = pb; a.p = p; a.G = G; a.demand = demand; a.batch = batch; a.dtab_rows = dtab_rows; a.u = u; a.thr = thr;
+  const size_t smem = sizeof(CycSmem) * CLU_WARPS;
+  int64_t blocks = (pb.num_scen + CLU_WARPS - 1) / CLU_WARPS;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  cudaFuncSetAttribute(k_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_cluster<<<(unsigned)blocks, CLU_WARPS * 32, smem, s>>>(a);
+  ++*launches;
+  return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;
+}
+
+}  // namespace dstack

@@ -115,6 +115,8 @@ int launch_sim(const SimArgs &a, cudaStream_t s, int *launches);
 size_t sim_fill_log_bytes();
 int launch_agg(const AggArgs &a, cudaStream_t s, int *launches);
 int launch_compare(const CmpArgs &a, cudaStream_t s, int *launches);
+int launch_cluster(const dstack_problem_t &pb, const dstack_params_t &p, int32_t G, const uint16_t *demand,
+                   const uint8_t *batch, uint16_t *dtab_rows, double *u, double *thr, cudaStream_t s, int *launches);
 size_t ideal_ws_bytes(int64_t num_rows);
 size_t agg_ws_bytes();
 

@@ -93,6 +93,7 @@ def _load():
     lib.dstack_simulate.argtypes = [P(CProblem), P(CParams), C.c_void_p, C.c_int32, C.c_uint64, C.c_int32, C.c_int64,
                                     P(CSimOut), C.c_void_p, C.c_size_t, C.c_void_p]
     lib.dstack_compare.argtypes = [P(CProblem), P(CParams)] + [C.c_void_p] * 7 + [C.c_size_t, C.c_void_p]
+    lib.dstack_cluster.argtypes = [P(CProblem), P(CParams), C.c_int32] + [C.c_void_p] * 5 + [C.c_size_t, C.c_void_p]
     lib.dstack_profile_start.argtypes = [C.c_int32]
     lib.dstack_profile_stop.argtypes = [C.c_void_p, C.c_void_p]
     lib.dstack_status_str.restype = C.c_char_p
@@ -105,7 +106,7 @@ _lib = _load()
 # every symbol include/dstack.h declares (checked by tests/test_abi.py)
 EXPORTS = ("dstack_workspace_size", "dstack_knee", "dstack_knee_probe", "dstack_batch_opt", "dstack_wmaxmin", "dstack_schedule_cycle",
            "dstack_eval_batch", "dstack_aggregate", "dstack_sim_workspace_size", "dstack_simulate",
-           "dstack_compare", "dstack_profile_start", "dstack_profile_stop",
+           "dstack_compare", "dstack_cluster", "dstack_profile_start", "dstack_profile_stop",
            "dstack_last_launch_count", "dstack_status_str", "dstack_version")
 
 
@@ -299,6 +300,21 @@ def eval_batch(dp: DeviceProblem, p, out=None, ws: Workspace | None = None, agg=
 
 
 CMP_NAMES = ("dstack", "maxmin", "maxthr", "temporal", "gslice")   # DSTACK_CMP_* order
+CLU_NAMES = ("exclusive", "temporal", "dstack", "dstack_ffd")         # DSTACK_CLU_* order
+
+
+def cluster(dp: DeviceProblem, p, gpus: int, demand, batch, out=None, ws: Workspace | None = None):
+    """dstack_cluster (F4): U and throughput of the CLU_NAMES policies on `gpus` modelled GPUs, f64 tensors
+    [num_scen, 4], from the a3 outputs (demand, batch)."""
+    dev = dp.device
+    if out is None:
+        out = {k: torch.zeros((max(dp.num_scen, 1), len(CLU_NAMES)), dtype=torch.float64, device=dev)
+               for k in ("u", "thr")}
+    if ws is None:
+        ws = Workspace(workspace_size(dp, p), dev)
+    _check(_lib.dstack_cluster(C.byref(dp.c()), C.byref(cparams(p)), gpus, _ptr(demand), _ptr(batch), _ptr(out["u"]),
+                               _ptr(out["thr"]), ws.ptr(), ws.nbytes, _stream(dev)), "dstack_cluster")
+    return {k: v[: dp.num_scen] for k, v in out.items()}
 
 
 def compare(dp: DeviceProblem, p, demand, batch, alloc_q16, out=None, ws: Workspace | None = None):

@@ -53,6 +53,9 @@ def test_host_side_argument_checks():
     assert lib.dstack_workspace_size(C.byref(pb), C.byref(bk)) > 0
     assert lib.dstack_compare(C.byref(pb), C.byref(bk), None, None, None, None, None, None, None, 0,
                               None) == ds.DSTACK_EINVAL
+    assert lib.dstack_cluster(C.byref(pb), C.byref(bk), 4, None, None, None, None, None, 0, None) == ds.DSTACK_EINVAL
+    assert lib.dstack_cluster(C.byref(pb), C.byref(good), 0, None, None, None, None, None, 0, None) == ds.DSTACK_EINVAL
+    assert lib.dstack_cluster(C.byref(pb), C.byref(good), 33, None, None, None, None, None, 0, None) == ds.DSTACK_EINVAL
 
 
 def test_struct_layouts_match_header():

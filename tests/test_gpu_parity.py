@@ -439,3 +439,44 @@ def test_knee_probe_parity(ds):
     ko, pro, sto = oracle.knee_probe(pe, q, 2)
     assert np.array_equal(st.cpu().numpy(), sto) and np.array_equal(k.cpu().numpy().view(np.uint16), ko)
     assert np.array_equal(pr.cpu().numpy(), pro)
+
+
+# ---------------------------------------------------------------- F4 multi-GPU cluster ---
+
+def run_cluster(ds, pb, p, G):
+    dp = ds.from_host(pb, "cuda")
+    o = ds.eval_batch(dp, p)
+    c = ds.cluster(dp, p, G, o["demand"], o["batch"])
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in c.items()}
+
+
+@pytest.mark.parametrize("cfg,G", [(1, 4), (2, 1), (2, 3), (4, 4), (4, 8), (3, 2)])
+def test_cluster_parity(ds, cfg, G):
+    """F4 (dstack_cluster): every policy's U and throughput bit-identical to the oracle."""
+    sp, p = synth.config(cfg, num_scen=None if cfg == 1 else 100, rows_pct=30)
+    pb = synth.generate_host(sp)
+    g = run_cluster(ds, pb, p, G)
+    want = oracle.cluster(pb, p, G)
+    for k in ("u", "thr"):
+        np.testing.assert_allclose(g[k], want[k], rtol=1e-6, atol=0, err_msg=f"cluster {cfg} G={G} {k}")
+        assert np.array_equal(g[k], want[k]), (cfg, G, k)
+
+
+def test_cluster_edges_and_config3_sample(ds):
+    pe = edge_problem()
+    for p in (Params(L=100, S_tot=148), Params(L=148, S_tot=148, mem_mode=2)):
+        g = run_cluster(ds, pe, p, 4)
+        want = oracle.cluster(pe, p, 4)
+        assert np.array_equal(g["u"], want["u"]) and np.array_equal(g["thr"], want["thr"])
+    sp, p = synth.config(3)
+    gd = synth.generate_device(sp, "cuda")
+    dp = ds.from_device_dict(gd)
+    o = ds.eval_batch(dp, p)
+    c = ds.cluster(dp, p, 4, o["demand"], o["batch"])
+    torch.cuda.synchronize()
+    idx = np.random.default_rng(12).choice(sp.num_scen, 100, replace=False)
+    want = oracle.cluster(synth.sample(sp, idx), p, 4)
+    for k in ("u", "thr"):
+        got = c[k][torch.as_tensor(idx, device=c[k].device)].cpu().numpy()
+        assert np.array_equal(got, want[k]), k
