@@ -20,6 +20,9 @@ __host__ __device__ inline size_t prof_warp_bytes(int S_tot) {
 #ifndef DSTACK_PROF_MINB
 #define DSTACK_PROF_MINB 4
 #endif
+#ifndef DSTACK_PROF_VEC
+#define DSTACK_PROF_VEC 0   // 1: 16-byte vector row loads in k_prof_fast (A/B at config 3: 12.9 vs 12.3 ms scalar)
+#endif
 #ifndef DSTACK_PROF_FAST
 #define DSTACK_PROF_FAST 1   // 0: every launch takes the generic kernel (A/B switch)
 #endif
@@ -206,11 +209,46 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
   const int32_t b_hi = (int32_t)(okb >> 8);
   // ---- a1: one coalesced pass over the rows: RT, min R, D = sum R d, W> = sum_{n > S_tot} R n, and the
   //      width histogram of R over n <= S_tot (smem) ----
+  uint32_t Rmin = 0xFFFFFFFFu;
+  uint64_t Wb = 0;
+#if DSTACK_PROF_VEC
+  // 16-byte vector loads: lane v covers rows [base + 4v, base + 4v + 4) of n, d (uint4) and r (uint2), base = r0
+  // rounded down to a multiple of 4 (the arrays are 256-byte aligned, so 4-row groups are 16-byte aligned; rows
+  // outside [r0, r0 + K) are masked; reads stay within the ABI's 16 bytes of slack).  Two vectors per lane in
+  // flight: a DNN of <= 253 rows is one round trip.
+  {
+    const int64_t base = r0 & ~(int64_t)3;
+    const int32_t lo = (int32_t)(r0 - base), hi = lo + K;   // valid rows, relative to base
+    const int nvec = (hi + 3) >> 2;
+    auto row = [&](uint32_t nn, uint32_t R, uint32_t dd) {
+      RT += R; D += (uint64_t)R * dd; Rmin = min(Rmin, R);
+      if (nn <= (uint32_t)S_tot) atomicAdd(&hist[nn], R); else Wb += (uint64_t)R * nn;
+    };
+    auto vec = [&](int v, const uint4 &nv, const uint4 &dv, const uint2 &rv) {
+      const int e0 = 4 * v;
+      const uint32_t nn[4] = {nv.x, nv.y, nv.z, nv.w}, dd[4] = {dv.x, dv.y, dv.z, dv.w};
+      const uint32_t RR[4] = {rv.x & 0xFFFFu, rv.x >> 16, rv.y & 0xFFFFu, rv.y >> 16};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (e0 + e >= lo && e0 + e < hi) row(nn[e], RR[e], dd[e]);
+    };
+    const uint4 *n4 = reinterpret_cast<const uint4 *>(pb.n + base);
+    const uint4 *d4 = reinterpret_cast<const uint4 *>(pb.d + base);
+    const uint2 *r2 = reinterpret_cast<const uint2 *>(pb.r + base);
+    for (int v0 = 0; v0 < nvec; v0 += 64) {
+      const int va = v0 + lane, vb = va + 32;
+      uint4 na = make_uint4(0, 0, 0, 0), da = na, nb = na, db = na;
+      uint2 ra = make_uint2(0, 0), rb = ra;
+      if (va < nvec) { na = __ldg(n4 + va); da = __ldg(d4 + va); ra = __ldg(r2 + va); }
+      if (vb < nvec) { nb = __ldg(n4 + vb); db = __ldg(d4 + vb); rb = __ldg(r2 + vb); }
+      if (va < nvec) vec(va, na, da, ra);
+      if (vb < nvec) vec(vb, nb, db, rb);
+    }
+  }
+#else
   const uint32_t *n = pb.n + r0;
   const uint16_t *r = pb.r + r0;
   const uint32_t *d = pb.d + r0;
-  uint32_t Rmin = 0xFFFFFFFFu;
-  uint64_t Wb = 0;
   for (int i0 = lane; i0 < K; i0 += 64) {
     const int i1 = i0 + 32;
     const bool h1 = i1 < K;
@@ -224,6 +262,7 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
       if (n1 <= (uint32_t)S_tot) atomicAdd(&hist[n1], R1); else Wb += (uint64_t)R1 * n1;
     }
   }
+#endif
   RT = __reduce_add_sync(FULL, RT);
   Rmin = __reduce_min_sync(FULL, Rmin);
   uint32_t Dtop, Wtop;
