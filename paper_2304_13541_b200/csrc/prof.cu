@@ -23,6 +23,9 @@ __host__ __device__ inline size_t prof_warp_bytes(int S_tot) {
 #ifndef DSTACK_PROF_VEC
 #define DSTACK_PROF_VEC 0   // 1: 16-byte vector row loads in k_prof_fast (A/B at config 3: 12.9 vs 12.3 ms scalar)
 #endif
+#ifndef DSTACK_FAST_KNEE_FIRST
+#define DSTACK_FAST_KNEE_FIRST 1   // 0: track the feasible argmax beside the knee in the width pass (A/B switch)
+#endif
 #ifndef DSTACK_PROF_FAST
 #define DSTACK_PROF_FAST 1   // 0: every launch takes the generic kernel (A/B switch)
 #endif
@@ -172,6 +175,19 @@ __device__ __forceinline__ SX fast_argmax(const Top2 &t, const uint64_t *scr, co
   return band_exact(scr, lmin, S_tot, F, band, lane);
 }
 
+// cold: argmax of S / X^2 over the attained widths with 2X <= S F, from the staged X values (float filter, exact
+// band resolution as fast_argmax)
+static __device__ __noinline__ SX feasible_argmax(const uint64_t *scr, const uint16_t *lmin, int S_tot, uint64_t F,
+                                                  int lane) {
+  Top2 te = {0.f, 0.f, 0u};
+  for (int S = 1 + lane; S <= S_tot; S += 32) {
+    const uint64_t X = scr[S];
+    const bool ok = lmin[S] != 0 && 2 * X <= (uint64_t)S * F;
+    top2_add(te, ok ? score_f((uint32_t)S, X) : 0.f, (uint32_t)S);
+  }
+  return fast_argmax(te, scr, lmin, S_tot, F, lane);
+}
+
 // Exact sum over the warp of per-lane values < 2^59 from three 32-bit reductions (22/22/15-bit limbs).
 // *top = the reduced top limb (the total is >= top * 2^44; the returned sum wraps only if top >= 2^20).
 __device__ __forceinline__ uint64_t warp_sum_limbs(uint64_t v, uint32_t *top) {
@@ -313,7 +329,10 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
   const float half = 0.5f * (float)S_tot;
   const int mh = S_tot >> 1;
   uint64_t *scr = cA;
-  Top2 tk = {0.f, 0.f, 0u}, te = {0.f, 0.f, 0u};
+  Top2 tk = {0.f, 0.f, 0u};
+#if !DSTACK_FAST_KNEE_FIRST
+  Top2 te = {0.f, 0.f, 0u};
+#endif
   float G = 0.f;
   {
     // overflow: X(L, b_hi) = b_hi t_np RT S_tot M + M t_p (S_tot PA[mb] + b_hi Q[mb]) + mem is the grid maximum;
@@ -337,7 +356,9 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
     const float f = score_f(S, X);
     const bool valid = (vmask >> i) & 1u;
     top2_add(tk, valid ? f : 0.f, S);
+#if !DSTACK_FAST_KNEE_FIRST
     top2_add(te, valid && 2 * X <= (uint64_t)S * F ? f : 0.f, S);   // Eqs. 11-12
+#endif
     // Batch certificate: for b >= 2 and s = S/b in segment m = floor(s),
     // X(S, b) >= b (alpha s + beta), alpha = 2 C1 + Mtp PA[m], beta = Mtp Q[m] + mem, hence
     // eta(S, b) <= s / (alpha s + beta)^2; G = max over m <= S_tot/2 of its supremum on [m, m+1).
@@ -355,6 +376,17 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
   __syncwarp();
   uint32_t Sk = 0, Se = 0;
   uint64_t Xe = 0;
+#if DSTACK_FAST_KNEE_FIRST
+  {
+    // knee = the exact argmax over every attained width (ties -> smaller S); when that width is feasible
+    // (Eqs. 11-12: 2X <= S F) it is also the exact argmax over the feasible widths (a subset containing it),
+    // else the feasible argmax is searched over the staged X values (cold)
+    const SX r = fast_argmax(tk, scr, lmin, S_tot, 0ull, lane);
+    Sk = r.S;
+    if (F != 0 && 2 * r.X <= (uint64_t)r.S * F) { Se = r.S; Xe = r.X; }
+    else { const SX e = feasible_argmax(scr, lmin, S_tot, F == 0 ? 1ull : F, lane); Se = e.S; Xe = e.X; }
+  }
+#else
 #pragma unroll 1
   for (int w = 0; w < 2; ++w) {   // w = 0: knee (all attained widths), w = 1: feasible argmax
     Top2 t;
@@ -362,6 +394,7 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
     const SX r = fast_argmax(t, scr, lmin, S_tot, w ? (F == 0 ? 1ull : F) : 0ull, lane);
     if (w) { Se = r.S; Xe = r.X; } else Sk = r.S;
   }
+#endif
   if (Se == 0) { st = DSTACK_ST_INFEASIBLE; return true; }   // b = 1 is feasible whenever any b is (O3)
   // b* = 1 is certified when the incumbent beats G with a 2^-12 margin (f32 rounding of both sides is
   // < 2^-19); otherwise the generic exact branch-and-bound decides this DNN.
