@@ -23,6 +23,9 @@ __host__ __device__ inline size_t prof_warp_bytes(int S_tot) {
 #ifndef DSTACK_PROF_VEC
 #define DSTACK_PROF_VEC 0   // 1: 16-byte vector row loads in k_prof_fast (A/B at config 3: 12.9 vs 12.3 ms scalar)
 #endif
+#ifndef DSTACK_FAST_CERT_PASS
+#define DSTACK_FAST_CERT_PASS 1   // 0: batch certificate inside the width pass (every lane's CB widths; A/B switch)
+#endif
 #ifndef DSTACK_FAST_KNEE_FIRST
 #define DSTACK_FAST_KNEE_FIRST 1   // 0: track the feasible argmax beside the knee in the width pass (A/B switch)
 #endif
@@ -362,6 +365,9 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
     // Batch certificate: for b >= 2 and s = S/b in segment m = floor(s),
     // X(S, b) >= b (alpha s + beta), alpha = 2 C1 + Mtp PA[m], beta = Mtp Q[m] + mem, hence
     // eta(S, b) <= s / (alpha s + beta)^2; G = max over m <= S_tot/2 of its supremum on [m, m+1).
+#if DSTACK_FAST_CERT_PASS
+    if ((int)S <= mh) cU[S] = ((uint64_t)q << 32) | ra;   // (PA[m], Q[m] - W>) for the certificate pass below
+#else
     if ((int)S <= mh) {
       const float af = fmaf(Mtpf, (float)ra, C1f2), bf = fmaf(Mtpf, (float)q + Wbf, membf);
       // the curve is unimodal with its peak at s = beta / alpha: evaluate it at that point clamped to [lo, hi]
@@ -372,6 +378,7 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
       const float v = bf == 0.f ? __int_as_float(0x7f800000) : sx * rcp_approx(x * x);   // unbounded at s -> 0
       G = fmaxf(G, v);
     }
+#endif
   }
   __syncwarp();
   uint32_t Sk = 0, Se = 0;
@@ -399,6 +406,19 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
   // b* = 1 is certified when the incumbent beats G with a 2^-12 margin (f32 rounding of both sides is
   // < 2^-19); otherwise the generic exact branch-and-bound decides this DNN.
   if (b_hi >= 2) {
+#if DSTACK_FAST_CERT_PASS
+    // lanes over the segments m = 0 .. S_tot/2 (instead of every lane's CB widths): the same bound per m
+    for (int m = lane; m <= mh; m += 32) {
+      const uint64_t pv = cU[m];
+      const uint32_t ra = (uint32_t)pv, q = (uint32_t)(pv >> 32);
+      const float af = fmaf(Mtpf, (float)ra, C1f2), bf = fmaf(Mtpf, (float)q + Wbf, membf);
+      const float lo = (float)m, hi = fminf(lo + 1.f, half);
+      const float sx = fminf(fmaxf(bf * rcp_approx(af), lo), hi);
+      const float x = fmaf(af, sx, bf);
+      const float v = bf == 0.f ? __int_as_float(0x7f800000) : sx * rcp_approx(x * x);
+      G = fmaxf(G, v);
+    }
+#endif
     const float Gw = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(G)));
     if (!(score_f(Se, Xe) * 0.99975586f > Gw)) return false;
   }
