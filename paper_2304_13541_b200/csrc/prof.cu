@@ -20,6 +20,9 @@ __host__ __device__ inline size_t prof_warp_bytes(int S_tot) {
 #ifndef DSTACK_PROF_MINB
 #define DSTACK_PROF_MINB 4
 #endif
+#ifndef DSTACK_PROF_ROWS_U
+#define DSTACK_PROF_ROWS_U 6   // rows per lane in flight in the row pass (A/B at config 3: 2 -> 10.86, 4 -> 11.41, 6 -> 10.44, 8 -> 10.71 ms)
+#endif
 #ifndef DSTACK_PROF_VEC
 #define DSTACK_PROF_VEC 0   // 1: 16-byte vector row loads in k_prof_fast (A/B at config 3: 12.9 vs 12.3 ms scalar)
 #endif
@@ -268,6 +271,25 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
   const uint32_t *n = pb.n + r0;
   const uint16_t *r = pb.r + r0;
   const uint32_t *d = pb.d + r0;
+#if DSTACK_PROF_ROWS_U > 2
+  // DSTACK_PROF_ROWS_U rows per lane in flight per iteration
+  for (int i0 = lane; i0 < K; i0 += 32 * DSTACK_PROF_ROWS_U) {
+    uint32_t nn[DSTACK_PROF_ROWS_U], dd[DSTACK_PROF_ROWS_U], RR[DSTACK_PROF_ROWS_U];
+#pragma unroll
+    for (int u = 0; u < DSTACK_PROF_ROWS_U; ++u) {
+      const int i = i0 + 32 * u;
+      nn[u] = 0; dd[u] = 0; RR[u] = 0;
+      if (i < K) { nn[u] = __ldg(n + i); dd[u] = __ldg(d + i); RR[u] = __ldg(r + i); }
+    }
+#pragma unroll
+    for (int u = 0; u < DSTACK_PROF_ROWS_U; ++u) {
+      if (i0 + 32 * u < K) {
+        RT += RR[u]; D += (uint64_t)RR[u] * dd[u]; Rmin = min(Rmin, RR[u]);
+        if (nn[u] <= (uint32_t)S_tot) atomicAdd(&hist[nn[u]], RR[u]); else Wb += (uint64_t)RR[u] * nn[u];
+      }
+    }
+  }
+#else
   for (int i0 = lane; i0 < K; i0 += 64) {
     const int i1 = i0 + 32;
     const bool h1 = i1 < K;
@@ -281,6 +303,7 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
       if (n1 <= (uint32_t)S_tot) atomicAdd(&hist[n1], R1); else Wb += (uint64_t)R1 * n1;
     }
   }
+#endif
 #endif
   RT = __reduce_add_sync(FULL, RT);
   Rmin = __reduce_min_sync(FULL, Rmin);
