@@ -127,16 +127,30 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def kernel_counters(config):
+def kernel_counters(config, key="per_scenario"):
     """ncu per-scenario counters of each kernel slot (warp instructions, DRAM bytes) for config 3, measured on
-    the committed build (profiles/counters.json, tools/ncu_counters.py); {} for other configs."""
+    the committed build (profiles/counters.json, tools/ncu_counters.py; key "legs": the next-row legs' kernels);
+    {} for other configs."""
     if config != 3:
         return {}
     try:
         with open(os.path.join(ROOT, "profiles", "counters.json")) as f:
-            return json.load(f)["per_scenario"]
+            return json.load(f).get(key, {})
     except Exception:
         return {}
+
+
+def leg_roofline(args, slot, ms, per_gpu):
+    """Issue-slot roofline of a next-row leg's kernel: ncu warp instructions per scenario (profiles/counters.json
+    "legs") x scenarios per call / the live device time of that kernel per call."""
+    c = kernel_counters(args.config, "legs").get(slot)
+    if not c or ms <= 0:
+        return None
+    ipk, src = issue_peak()
+    ach = c["warp_inst"] * per_gpu / (ms / 1e3) / 1e9
+    return {"bound": "alu", "kernel": slot, "achieved": ach, "peak": ipk, "unit": "Gwarp-inst/s", "frac": ach / ipk,
+            "traffic": c["dram_bytes"] * per_gpu, "peak_source": src,
+            "counted": f"ncu smsp__inst_executed.sum per launch = {c['warp_inst'] * per_gpu:.4g} (profiles/counters.json legs)"}
 
 
 def issue_peak():
@@ -398,6 +412,7 @@ def run_compare_leg(args, ds, dp, p, out, ws, stream, per_gpu, world):
         means[name] = {k: float(c[k][ok, i].mean().item()) for k in ("u", "thr", "jain")}
     d = means["dstack"]["thr"]
     return {"api": "paper_2304_13541_b200.dstack.compare (dstack_compare)", "ms_per_call": ms,
+            "roofline": leg_roofline(args, "k_compare", ms, per_gpu),
             "scenarios_per_s": per_gpu * world / (ms / 1e3), "gpu_launches": ds.last_launch_count(),
             "schedulers": list(ds.CMP_NAMES), "means_over_scheduled_scenarios": means,
             "dstack_throughput_ratio": {k: d / means[k]["thr"] for k in ds.CMP_NAMES if means[k]["thr"] > 0}}
@@ -416,11 +431,14 @@ def run_below_knee_leg(args, ds, dp, p, out, stream, per_gpu, world):
     torch.cuda.synchronize()
     steps = max(1, min(args.steps, 5))
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    ds.profile_start(steps)
     e0.record(stream)
     for _ in range(steps):
         ds.eval_batch(dp, q, out=o, ws=ws)
     e1.record(stream)
     torch.cuda.synchronize()
+    kms, ncalls = ds.profile_stop()
+    cyc_ms = kms.get("k_cycle", 0.0) / max(ncalls, 1)
     ms = e0.elapsed_time(e1) / steps
     t = torch.tensor([ms], dtype=torch.float64, device=stream.device)
     if world > 1:
@@ -430,6 +448,7 @@ def run_below_knee_leg(args, ds, dp, p, out, stream, per_gpu, world):
     n0, n1 = max(a0["n_scen_scheduled"], 1), max(a1["n_scen_scheduled"], 1)
     return {"api": "paper_2304_13541_b200.dstack.eval_batch (dstack_eval_batch, DSTACK_FLAG_BELOW_KNEE)",
             "reconf_us": q.reconf_us, "ms_per_call": ms, "scenarios_per_s": per_gpu * world / (ms / 1e3),
+            "k_cycle_ms": cyc_ms, "roofline": leg_roofline(args, "k_cycle_bk", cyc_ms, per_gpu),
             "below_knee_runs": int(o["below"].sum().item()), "misses": a1["misses"], "misses_default": a0["misses"],
             "oversubscribed_scenarios": a1["n_scen_st"][4], "oversubscribed_default": a0["n_scen_st"][4],
             "mean_u": a1["sum_u"] / n1, "mean_u_default": a0["sum_u"] / n0}
@@ -460,6 +479,7 @@ def run_cluster_leg(args, ds, dp, p, out, ws, stream, per_gpu, world):
     means = {name: {k: float(c[k][ok, i].mean().item()) for k in ("u", "thr")} for i, name in enumerate(ds.CLU_NAMES)}
     tt = means["temporal"]["thr"]
     return {"api": "paper_2304_13541_b200.dstack.cluster (dstack_cluster)", "gpus_modelled": G, "ms_per_call": ms,
+            "roofline": leg_roofline(args, "k_cluster", ms, per_gpu),
             "scenarios_per_s": per_gpu * world / (ms / 1e3), "policies": list(ds.CLU_NAMES),
             "means_over_scheduled_scenarios": means,
             "throughput_vs_temporal": {k: means[k]["thr"] / tt for k in ds.CLU_NAMES} if tt > 0 else None}
@@ -489,6 +509,7 @@ def run_knee_probe_leg(args, ds, dp, p, stream, world):
     n_ok = int(ok.sum().item())
     match = int(((k == kx) & ok).sum().item())
     return {"api": "paper_2304_13541_b200.dstack.knee_probe (dstack_knee_probe)", "batch": 1, "ms_per_call": ms,
+            "roofline": leg_roofline(args, "k_knee_probe", ms, dp.num_scen),
             "dnns_per_s": dp.num_dnn * world / (ms / 1e3), "dnns_ok": n_ok,
             "exact_knee_match_frac": match / max(n_ok, 1),
             "mean_steps": float(pr[ok].float().mean().item()) if n_ok else 0.0,
