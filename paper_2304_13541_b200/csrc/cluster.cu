@@ -14,6 +14,9 @@
 namespace dstack {
 
 constexpr int CLU_WARPS = 8;
+#ifndef DSTACK_CLU_MINB
+#define DSTACK_CLU_MINB 4   // resident blocks per SM the register allocation targets (A/B: 1 -> 226, 3 -> 223, 4 -> 202 ms)
+#endif
 
 struct CluArgs {
   dstack_problem_t pb;
@@ -25,7 +28,7 @@ struct CluArgs {
   double *u, *thr;       // [num_scen * DSTACK_NCLU]
 };
 
-__global__ void __launch_bounds__(CLU_WARPS * 32) k_cluster(const __grid_constant__ CluArgs a) {
+__global__ void __launch_bounds__(CLU_WARPS * 32, DSTACK_CLU_MINB) k_cluster(const __grid_constant__ CluArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   CycSmem &sm = reinterpret_cast<CycSmem *>(smem_raw)[warp];
