@@ -13,6 +13,9 @@
 namespace dstack {
 
 constexpr int CMP_WARPS = 8;
+#ifndef DSTACK_CMP_MINB
+#define DSTACK_CMP_MINB 4   // resident blocks per SM the register allocation targets (A/B: 1 -> 120, 3 -> 102, 4 -> 95 ms)
+#endif
 
 __device__ __forceinline__ double jain_idx(uint64_t x, bool act) {
   const uint64_t s1 = warp_sum_u64(act ? x : 0ull), s2 = warp_sum_u64(act ? x * x : 0ull);
@@ -21,7 +24,7 @@ __device__ __forceinline__ double jain_idx(uint64_t x, bool act) {
   return den ? (double)(s1 * s1) / (double)den : 0.0;
 }
 
-__global__ void __launch_bounds__(CMP_WARPS * 32) k_compare(CmpArgs a) {
+__global__ void __launch_bounds__(CMP_WARPS * 32, DSTACK_CMP_MINB) k_compare(CmpArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   CycSmem &sm = reinterpret_cast<CycSmem *>(smem_raw)[warp];

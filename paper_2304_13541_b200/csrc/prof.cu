@@ -66,7 +66,7 @@ __device__ __forceinline__ uint32_t knee_probe_search(const dstack_problem_t &pb
 template <int PAR>
 __device__ __forceinline__ void prof_one(const ProfArgs &a, int64_t k, const uint16_t *Stab, uint32_t *hist,
                                          uint64_t *cA, uint64_t *cU, int lane) {
-  DnnRes r = analyze_dnn<PAR>(a.pb, a.p, k, Stab, hist, cA, cU, lane, a.knee_only, a.knee_b);
+  DnnRes r = analyze_dnn<PAR>(a.pb, a.p, k, Stab, hist, cA, cU, lane, a.probes ? 2 : a.knee_only, a.knee_b);
   if (a.probes) {   // F3: the probe's knee replaces Eq. 6's exact argmax
     uint32_t steps = 0;
     if (r.st == DSTACK_ST_OK) {

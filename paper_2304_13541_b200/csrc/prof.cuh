@@ -32,6 +32,10 @@ static __device__ unsigned long long g_pstats[16];   // per TU; k_prof's copy is
 #define PSTAT(i, v) ((void)0)
 #endif
 
+#ifndef DSTACK_GEN_ROWS_U
+#define DSTACK_GEN_ROWS_U 6   // rows per lane in flight in the generic row pass (A/B knee probe: 2 -> 34.6, 4 -> 34.4, 6 -> 33.1 ms)
+#endif
+
 struct Best {
   uint32_t found, l, b, S;
   uint64_t X;
@@ -286,7 +290,8 @@ uint64_t bound_survivors(const uint64_t *cA, const uint64_t *cU, double thr, uin
   return out;
 }
 
-// Analyse DNN k.  knee_only: status + knee at knee_b.  Otherwise (l*, b*), demand, knee(b*).
+// Analyse DNN k.  knee_only: 1 status + knee at knee_b, 2 status + the tables at knee_b only.  Otherwise (l*, b*),
+// demand, knee(b*).
 // Per-warp shared memory: hist[S_tot+1] u32, cA/cU[S_tot+1] u64 (tables stay valid on return).
 template <int PAR>
 __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k, const uint16_t *Stab,
@@ -329,15 +334,17 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
       if (Nb >= 1) Vmax = sat_add(Vmax, (uint64_t)R * (Nb > (uint64_t)S_tot ? Nb : (uint64_t)S_tot));
     }
   };
-  for (int i0 = lane; i0 < K; i0 += 64) {
-    const int i1 = i0 + 32;
-    const bool h1 = i1 < K;
-    const uint32_t n0 = __ldg(n + i0), d0 = __ldg(d + i0);
-    const uint32_t R0 = __ldg(r + i0);
-    uint32_t n1 = 0, d1 = 0, R1 = 0;
-    if (h1) { n1 = __ldg(n + i1); d1 = __ldg(d + i1); R1 = __ldg(r + i1); }
-    row(n0, R0, d0);
-    if (h1) row(n1, R1, d1);
+  for (int i0 = lane; i0 < K; i0 += 32 * DSTACK_GEN_ROWS_U) {   // DSTACK_GEN_ROWS_U rows per lane in flight
+    uint32_t nn[DSTACK_GEN_ROWS_U], dd[DSTACK_GEN_ROWS_U], RR[DSTACK_GEN_ROWS_U];
+#pragma unroll
+    for (int u = 0; u < DSTACK_GEN_ROWS_U; ++u) {
+      const int i = i0 + 32 * u;
+      nn[u] = 0; dd[u] = 0; RR[u] = 0;
+      if (i < K) { nn[u] = __ldg(n + i); dd[u] = __ldg(d + i); RR[u] = __ldg(r + i); }
+    }
+#pragma unroll
+    for (int u = 0; u < DSTACK_GEN_ROWS_U; ++u)
+      if (i0 + 32 * u < K) row(nn[u], RR[u], dd[u]);
   }
   RT = __reduce_add_sync(FULL, RT);
   D = warp_sum_u64(D); Wn = warp_sum_u64(Wn);
@@ -383,6 +390,7 @@ __device__ DnnRes analyze_dnn(const dstack_problem_t &pb, const dstack_params_t 
     const int b = __ffsll((long long)todo);   // b = bit index + 1
     todo &= todo - 1;
     if (PAR == 1) build_tables_threads(n, r, K, S_tot, Mtp, b, hist, cA, cU, lane);
+    if (knee_only == 2) return res;   // tables only (F3 knee probe): cA / cU valid at knee_b, RT and D set
     eval_row<PAR>(c, b, lane, e, kk);
     if (first) {
       first = false;
