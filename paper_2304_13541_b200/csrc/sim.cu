@@ -17,6 +17,9 @@
 namespace dstack {
 
 constexpr int SIM_WARPS = 8;
+#ifndef DSTACK_SIM_MINB
+#define DSTACK_SIM_MINB 2   // resident blocks per SM (and the grid: one wave); A/B config 5: grid 4/SM at 2 resident 155 ms, 2 -> 95, 3 -> 96, 4 -> 133 ms
+#endif
 
 struct ArrCursor {
   uint64_t idx, time;
@@ -27,7 +30,7 @@ __device__ __forceinline__ void arr_next(ArrCursor &a, const SimArgs &s, int64_t
   a.time += sy_arrival_gap(mq, sy_arrival_word(s.seed, s.cfg_tag, gs, j, (uint32_t)a.idx));
 }
 
-__global__ void __launch_bounds__(SIM_WARPS * 32) k_sim(SimArgs a) {
+__global__ void __launch_bounds__(SIM_WARPS * 32, DSTACK_SIM_MINB) k_sim(SimArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   CycSmem &sm = reinterpret_cast<CycSmem *>(smem_raw)[warp];
@@ -184,7 +187,7 @@ int launch_sim(const SimArgs &a, cudaStream_t s, int *launches) {
   if (a.pb.num_scen <= 0) return 0;
   const size_t smem = (sizeof(CycSmem) + 10 * 32 * 4) * SIM_WARPS;
   int64_t blocks = (a.pb.num_scen + SIM_WARPS - 1) / SIM_WARPS;
-  int64_t cap = (int64_t)num_sms() * 4;
+  int64_t cap = (int64_t)num_sms() * (DSTACK_SIM_MINB > 1 ? DSTACK_SIM_MINB : 4);   // one wave of resident blocks
   if (cap * SIM_WARPS > SIM_MAX_WARPS) cap = SIM_MAX_WARPS / SIM_WARPS;
   if (blocks > cap) blocks = cap;
   cudaFuncSetAttribute(k_sim, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
