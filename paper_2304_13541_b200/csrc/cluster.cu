@@ -14,6 +14,9 @@
 namespace dstack {
 
 constexpr int CLU_WARPS = 8;
+#ifndef DSTACK_CLU_GRID
+#define DSTACK_CLU_GRID 64   // grid: blocks per SM (A/B ms: 8 -> 203, 32 -> 201, 64 -> 197)
+#endif
 #ifndef DSTACK_CLU_MINB
 #define DSTACK_CLU_MINB 4   // resident blocks per SM the register allocation targets (A/B: 1 -> 226, 3 -> 223, 4 -> 202 ms)
 #endif
@@ -171,7 +174,7 @@ int launch_cluster(const dstack_problem_t &pb, const dstack_params_t &p, int32_t
   a.pb = pb; a.p = p; a.G = G; a.demand = demand; a.batch = batch; a.dtab_rows = dtab_rows; a.u = u; a.thr = thr;
   const size_t smem = sizeof(CycSmem) * CLU_WARPS;
   int64_t blocks = (pb.num_scen + CLU_WARPS - 1) / CLU_WARPS;
-  const int64_t cap = (int64_t)num_sms() * 8;
+  const int64_t cap = (int64_t)num_sms() * DSTACK_CLU_GRID;
   if (blocks > cap) blocks = cap;
   cudaFuncSetAttribute(k_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_cluster<<<(unsigned)blocks, CLU_WARPS * 32, smem, s>>>(a);

@@ -13,6 +13,9 @@
 namespace dstack {
 
 constexpr int CMP_WARPS = 8;
+#ifndef DSTACK_CMP_GRID
+#define DSTACK_CMP_GRID 64   // grid: blocks per SM (A/B ms: 8 -> 95.3, 32 -> 94.2, 64 -> 93.1)
+#endif
 #ifndef DSTACK_CMP_MINB
 #define DSTACK_CMP_MINB 4   // resident blocks per SM the register allocation targets (A/B: 1 -> 120, 3 -> 102, 4 -> 95 ms)
 #endif
@@ -153,7 +156,7 @@ int launch_compare(const CmpArgs &a, cudaStream_t s, int *launches) {
   if (a.pb.num_scen <= 0) return 0;
   const size_t smem = sizeof(CycSmem) * CMP_WARPS;
   int64_t blocks = (a.pb.num_scen + CMP_WARPS - 1) / CMP_WARPS;
-  const int64_t cap = (int64_t)num_sms() * 8;
+  const int64_t cap = (int64_t)num_sms() * DSTACK_CMP_GRID;
   if (blocks > cap) blocks = cap;
   cudaFuncSetAttribute(k_compare, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_compare<<<(unsigned)blocks, CMP_WARPS * 32, smem, s>>>(a);

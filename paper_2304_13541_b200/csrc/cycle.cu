@@ -24,6 +24,12 @@ __global__ void __launch_bounds__(256) k_wmaxmin(int32_t num_scen, const int32_t
   }
 }
 
+#ifndef DSTACK_CYC_GRID
+#define DSTACK_CYC_GRID 64   // k_cycle grid: blocks per SM (4 resident; A/B ms: 4 -> 18.7, 8 -> 17.86, 16 -> 17.15, 32 -> 16.85, 64 -> 16.73, 128 -> 16.8, 256 -> 17.2)
+#endif
+#ifndef DSTACK_CYC_BK_GRID
+#define DSTACK_CYC_BK_GRID 8   // k_cycle<true> (F1) grid: blocks per SM (A/B leg: 8 -> 49.5, 64 -> 53.0 ms)
+#endif
 #ifndef DSTACK_CYC_MINB
 #define DSTACK_CYC_MINB 4
 #endif
@@ -150,11 +156,12 @@ int launch_cycle(const CycArgs &a, cudaStream_t s, int *launches) {
   if (a.pb.num_scen <= 0) return 0;
   const size_t smem = sizeof(CycSmem) * CYC_WARPS;
   int64_t blocks = (a.pb.num_scen + CYC_WARPS - 1) / CYC_WARPS;
-  const int64_t cap = (int64_t)num_sms() * 8;
+  const int64_t cap = (int64_t)num_sms() * DSTACK_CYC_GRID;
   if (blocks > cap) blocks = cap;
   if (a.p.flags & DSTACK_FLAG_BELOW_KNEE) {
+    const int64_t bk_blocks = blocks < (int64_t)num_sms() * DSTACK_CYC_BK_GRID ? blocks : (int64_t)num_sms() * DSTACK_CYC_BK_GRID;
     cudaFuncSetAttribute(k_cycle<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_cycle<true><<<(unsigned)blocks, CYC_WARPS * 32, smem, s>>>(a);
+    k_cycle<true><<<(unsigned)bk_blocks, CYC_WARPS * 32, smem, s>>>(a);
   } else {
     cudaFuncSetAttribute(k_cycle<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_cycle<false><<<(unsigned)blocks, CYC_WARPS * 32, smem, s>>>(a);

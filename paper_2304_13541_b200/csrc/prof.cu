@@ -20,6 +20,9 @@ __host__ __device__ inline size_t prof_warp_bytes(int S_tot) {
 #ifndef DSTACK_PROF_MINB
 #define DSTACK_PROF_MINB 4
 #endif
+#ifndef DSTACK_PROF_GRID
+#define DSTACK_PROF_GRID 64   // k_prof grid: blocks per SM (4 resident; A/B ms: 4 -> 10.6, 8 -> 10.31, 16 -> 9.99, 32 -> 9.8, 64 -> 9.7, 128 -> 9.67, 256 -> 9.74)
+#endif
 #ifndef DSTACK_PROF_ROWS_U
 #define DSTACK_PROF_ROWS_U 6   // rows per lane in flight in the row pass (A/B at config 3: 2 -> 10.86, 4 -> 11.41, 6 -> 10.44, 8 -> 10.71 ms)
 #endif
@@ -581,7 +584,7 @@ int launch_prof(const ProfArgs &a, cudaStream_t s, int *launches) {
   const int threads = 256, warps = threads / 32;
   const size_t smem = prof_smem_bytes(&a.p, warps);
   int64_t blocks = (a.pb.num_dnn + warps - 1) / warps;
-  const int64_t cap = (int64_t)num_sms() * 8;
+  const int64_t cap = (int64_t)num_sms() * DSTACK_PROF_GRID;
   if (blocks > cap) blocks = cap;
   const bool fast = DSTACK_PROF_FAST && a.p.par_mode == 0 && a.p.wse_mode == 0 && a.p.b_min == 1 && !a.knee_only;
   if (fast && a.p.S_tot < 5 * 32) launch_k(k_prof_fast<5>, a, blocks, threads, smem, s);
