@@ -58,12 +58,13 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // workspace layout: [agg partials | d_j(b) rows u16[num_dnn][64] | RT u32[num_dnn] | D u64[num_dnn] | ideal]
 struct WsLayout {
-  size_t dtab, rt, d, ideal, end;
+  size_t ctr, dtab, rt, d, ideal, end;
 };
 WsLayout ws_layout(const dstack_problem_t *pb, const dstack_params_t *p) {
   WsLayout w;
   const size_t nd = (size_t)(pb->num_dnn > 0 ? pb->num_dnn : 0);
-  w.dtab = align256(agg_ws_bytes());
+  w.ctr = align256(agg_ws_bytes());          // work counters (k_cycle)
+  w.dtab = w.ctr + 256;
   w.rt = w.dtab + align256(nd * DTAB_ROW * 2);
   w.d = w.rt + align256(nd * 4);
   w.ideal = w.d + align256(nd * 8);
@@ -223,6 +224,7 @@ static int schedule_impl(const dstack_problem_t *pb, const dstack_params_t *p, c
   c.T_us = out->T_us; c.u_static = out->u_static; c.u = out->u; c.thr = out->thr; c.misses = out->misses;
   c.below = out->below;
   c.dtab_rows = (uint16_t *)((char *)ws + ws_layout(pb, p).dtab);
+  c.work_ctr = (uint32_t *)((char *)ws + ws_layout(pb, p).ctr);
   if (pre_ws) { c.ws_RT = (const uint32_t *)((char *)ws + ws_layout(pb, p).rt); c.ws_D = (const uint64_t *)((char *)ws + ws_layout(pb, p).d); }
   int rc = launch_cycle(c, s, &g_launches);
   if (rc) return rc;
@@ -279,6 +281,7 @@ int dstack_eval_batch(const dstack_problem_t *pb, const dstack_params_t *p, dsta
   a.dtab_rows = (uint16_t *)((char *)ws + w.dtab);
   a.ws_RT = (uint32_t *)((char *)ws + w.rt);
   a.ws_D = (uint64_t *)((char *)ws + w.d);
+  a.work_ctr = (uint32_t *)((char *)ws + w.ctr) + 1;   // word 0: k_cycle's counter
   const bool prof = g_prof.on && g_prof.calls < g_prof.max_calls;
   uint8_t *used = prof ? g_prof.used + g_prof.calls * DSTACK_PROF_SLOTS : nullptr;
   if (prof) { used[0] = used[1] = used[2] = 1; used[3] = (p->flags & DSTACK_FLAG_IDEAL) ? 1 : 0; used[4] = out->agg ? 1 : 0; }

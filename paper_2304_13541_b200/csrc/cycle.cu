@@ -27,6 +27,9 @@ __global__ void __launch_bounds__(256) k_wmaxmin(int32_t num_scen, const int32_t
 #ifndef DSTACK_CYC_GRID
 #define DSTACK_CYC_GRID 64   // k_cycle grid: blocks per SM (4 resident; A/B ms: 4 -> 18.7, 8 -> 17.86, 16 -> 17.15, 32 -> 16.85, 64 -> 16.73, 128 -> 16.8, 256 -> 17.2)
 #endif
+#ifndef DSTACK_CYC_DYN
+#define DSTACK_CYC_DYN 1   // 1: k_cycle takes scenarios from a work counter (A/B switch)
+#endif
 #ifndef DSTACK_CYC_BK_GRID
 #define DSTACK_CYC_BK_GRID 8   // k_cycle<true> (F1) grid: blocks per SM (A/B leg: 8 -> 49.5, 64 -> 53.0 ms)
 #endif
@@ -42,7 +45,17 @@ __global__ void __launch_bounds__(CYC_WARPS * 32, DSTACK_CYC_MINB) k_cycle(const
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int32_t L = a.p.L, slot = a.p.slot_us, b_lo = a.p.b_min;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s = gwarp; s < a.pb.num_scen; s += nwarps) {
+  // scenario order: a work counter (one resident wave of warps, each takes the next scenario when it finishes one)
+  // or a grid stride
+  auto fetch = [&](int64_t prev) -> int64_t {
+    if (a.work_ctr) {
+      uint32_t v = 0;
+      if (lane == 0) v = atomicAdd(a.work_ctr, 1u);
+      return (int64_t)__shfl_sync(FULL, v, 0);
+    }
+    return prev < 0 ? gwarp : prev + nwarps;
+  };
+  for (int64_t s = fetch(-1); s < a.pb.num_scen; s = fetch(s)) {
     const int32_t k0 = a.pb.scen_dnn_off[s], nd = a.pb.scen_dnn_off[s + 1] - k0;
     uint8_t sst = DSTACK_ST_OK;
     uint32_t T = 0;
@@ -159,12 +172,22 @@ int launch_cycle(const CycArgs &a, cudaStream_t s, int *launches) {
   const int64_t cap = (int64_t)num_sms() * DSTACK_CYC_GRID;
   if (blocks > cap) blocks = cap;
   if (a.p.flags & DSTACK_FLAG_BELOW_KNEE) {
+    CycArgs b = a;
+    b.work_ctr = nullptr;
     const int64_t bk_blocks = blocks < (int64_t)num_sms() * DSTACK_CYC_BK_GRID ? blocks : (int64_t)num_sms() * DSTACK_CYC_BK_GRID;
     cudaFuncSetAttribute(k_cycle<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_cycle<true><<<(unsigned)bk_blocks, CYC_WARPS * 32, smem, s>>>(a);
-  } else {
+    k_cycle<true><<<(unsigned)bk_blocks, CYC_WARPS * 32, smem, s>>>(b);
+  } else if (DSTACK_CYC_DYN && a.work_ctr) {
+    // one resident wave (DSTACK_CYC_MINB blocks per SM) pulling scenarios from the work counter
+    if (cudaMemsetAsync(a.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
+    const int64_t wave = (int64_t)num_sms() * DSTACK_CYC_MINB;
     cudaFuncSetAttribute(k_cycle<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_cycle<false><<<(unsigned)blocks, CYC_WARPS * 32, smem, s>>>(a);
+    k_cycle<false><<<(unsigned)(blocks < wave ? blocks : wave), CYC_WARPS * 32, smem, s>>>(a);
+  } else {
+    CycArgs b = a;
+    b.work_ctr = nullptr;
+    cudaFuncSetAttribute(k_cycle<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_cycle<false><<<(unsigned)blocks, CYC_WARPS * 32, smem, s>>>(b);
   }
   ++*launches;
   return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;

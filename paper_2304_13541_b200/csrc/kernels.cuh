@@ -31,6 +31,7 @@ struct ProfArgs {
   uint16_t *dtab_rows;
   uint32_t *ws_RT;
   uint64_t *ws_D;
+  uint32_t *work_ctr;   // workspace word: k_prof_fast's DNN-group counter (NULL: contiguous ranges)
 };
 
 struct CycArgs {
@@ -52,6 +53,7 @@ struct CycArgs {
   uint16_t *dtab_rows;     // workspace: num_dnn rows of DTAB_ROW u16
   const uint32_t *ws_RT;   // non-NULL => dtab_rows already hold d_j(b) at g = demand (from k_prof)
   const uint64_t *ws_D;
+  uint32_t *work_ctr;      // workspace word: k_cycle's scenario counter (NULL: grid stride)
 };
 
 constexpr int64_t SIM_MAX_WARPS = 148 * 32;   // persistent-grid cap (sizes the fill-run logs)

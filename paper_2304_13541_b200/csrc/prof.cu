@@ -23,6 +23,9 @@ __host__ __device__ inline size_t prof_warp_bytes(int S_tot) {
 #ifndef DSTACK_PROF_GRID
 #define DSTACK_PROF_GRID 64   // k_prof grid: blocks per SM (4 resident; A/B ms: 4 -> 10.6, 8 -> 10.31, 16 -> 9.99, 32 -> 9.8, 64 -> 9.7, 128 -> 9.67, 256 -> 9.74)
 #endif
+#ifndef DSTACK_PROF_DYN
+#define DSTACK_PROF_DYN 1   // 1: k_prof_fast takes groups of 32 DNNs from a work counter (A/B switch)
+#endif
 #ifndef DSTACK_PROF_ROWS_U
 #define DSTACK_PROF_ROWS_U 6   // rows per lane in flight in the row pass (A/B at config 3: 2 -> 10.86, 4 -> 11.41, 6 -> 10.44, 8 -> 10.71 ms)
 #endif
@@ -509,8 +512,18 @@ __global__ void __launch_bounds__(256, DSTACK_PROF_MINB) k_prof_fast(const __gri
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t per = (pb.num_dnn + nw - 1) / nw;
   const int64_t kbeg = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * per;
-  const int64_t kend = kbeg + per < pb.num_dnn ? kbeg + per : pb.num_dnn;
-  for (int64_t kb = kbeg; kb < kend; kb += 32) {
+  // groups of 32 DNNs: taken from the work counter (one resident wave of warps) or the warp's contiguous range
+  const bool dyn = a.work_ctr != nullptr;
+  const int64_t kend = dyn ? pb.num_dnn : (kbeg + per < pb.num_dnn ? kbeg + per : pb.num_dnn);
+  auto fetch = [&](int64_t prev) -> int64_t {
+    if (dyn) {
+      uint32_t v = 0;
+      if (lane == 0) v = atomicAdd(a.work_ctr, 32u);
+      return (int64_t)__shfl_sync(FULL, v, 0);
+    }
+    return prev < 0 ? kbeg : prev + 32;
+  };
+  for (int64_t kb = fetch(-1); kb < kend; kb = fetch(kb)) {
     const int nj = kend - kb < 32 ? (int)(kend - kb) : 32;
     const int64_t kl = kb + lane;
     const bool have = lane < nj;
@@ -587,10 +600,17 @@ int launch_prof(const ProfArgs &a, cudaStream_t s, int *launches) {
   const int64_t cap = (int64_t)num_sms() * DSTACK_PROF_GRID;
   if (blocks > cap) blocks = cap;
   const bool fast = DSTACK_PROF_FAST && a.p.par_mode == 0 && a.p.wse_mode == 0 && a.p.b_min == 1 && !a.knee_only;
-  if (fast && a.p.S_tot < 5 * 32) launch_k(k_prof_fast<5>, a, blocks, threads, smem, s);
-  else if (fast) launch_k(k_prof_fast<9>, a, blocks, threads, smem, s);
-  else if (a.p.par_mode == 0) launch_k(k_prof<0>, a, blocks, threads, smem, s);
-  else launch_k(k_prof<1>, a, blocks, threads, smem, s);
+  ProfArgs b = a;
+  if (!DSTACK_PROF_DYN || !fast) b.work_ctr = nullptr;
+  if (b.work_ctr) {   // one resident wave (DSTACK_PROF_MINB blocks per SM) pulling groups of 32 DNNs
+    if (cudaMemsetAsync(b.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
+    const int64_t wave = (int64_t)num_sms() * DSTACK_PROF_MINB;
+    if (blocks > wave) blocks = wave;
+  }
+  if (fast && a.p.S_tot < 5 * 32) launch_k(k_prof_fast<5>, b, blocks, threads, smem, s);
+  else if (fast) launch_k(k_prof_fast<9>, b, blocks, threads, smem, s);
+  else if (a.p.par_mode == 0) launch_k(k_prof<0>, b, blocks, threads, smem, s);
+  else launch_k(k_prof<1>, b, blocks, threads, smem, s);
   ++*launches;
   return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;
 }
