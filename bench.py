@@ -537,7 +537,9 @@ def run_e2e(args, sp, p, dev, world):
             if cnt <= 0:
                 break
             g = synth.generate_device(sp.replace(scen_base=sp.scen_base + s0, num_scen=cnt), dev)
-            host_chunks.append({k: g[k].cpu().pin_memory() for k in fields})
+            # straight into pinned host buffers (no pageable intermediate: 8 ranks x ~14 GB of rows on one host)
+            host_chunks.append({k: torch.empty(g[k].shape, dtype=g[k].dtype, pin_memory=True).copy_(g[k])
+                                for k in fields})
             del g
     except RuntimeError as e:
         return {"value": None, "unit": UNIT, "error": f"pinned host staging failed: {e}"[:200]}
