@@ -59,6 +59,24 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def bench_device(local):
+    """cuda:LOCAL_RANK.  DSTACK_BENCH_DEVICE (testing only) pins every rank to one device, e.g. to exercise the
+    multi-rank path on a single-GPU box together with DSTACK_BENCH_BACKEND=gloo."""
+    import torch
+    forced = os.environ.get("DSTACK_BENCH_DEVICE")
+    return torch.device("cuda", int(forced) if forced is not None else local)
+
+
+def init_dist(dev):
+    """One process per GPU over NCCL (DSTACK_BENCH_BACKEND overrides the backend, testing only)."""
+    import torch.distributed as dist
+    backend = os.environ.get("DSTACK_BENCH_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -250,10 +268,10 @@ def run_native(args, rank, world, local):
     from paper_2304_13541_b200 import dstack as ds
     from paper_2304_13541_b200.dist import allreduce_agg
 
-    dev = torch.device("cuda", local)
+    dev = bench_device(local)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev)
     n = args.scen or None
     sp0, p = synth.config(args.config, num_scen=n, variant=args.variant)
     per_gpu = sp0.num_scen
@@ -546,12 +564,11 @@ def run_e2e(args, sp, p, dev, world):
     torch.cuda.synchronize()
     copy_s = torch.cuda.Stream(dev)
     comp_s = torch.cuda.current_stream(dev)
-    # two device buffer sets sized for the largest chunk
-    def dev_like(hc):
-        return {k: torch.empty_like(v, device=dev) for k, v in hc.items()}
-    big = max(host_chunks, key=lambda h: h["n"].numel())
-    bufs = [dev_like(big), dev_like(big)]
-    outs = []
+    # two device buffer sets, every field sized for the largest chunk of that field
+    def dev_max():
+        return {k: torch.empty(max(hc[k].numel() for hc in host_chunks), dtype=host_chunks[0][k].dtype, device=dev)
+                for k in fields}
+    bufs = [dev_max(), dev_max()]
     res_fields = ("scen_status", "u_static", "u", "thr", "misses")
     h2d = sum(v.numel() * v.element_size() for hc in host_chunks for v in hc.values())
     d2h = 0
@@ -564,10 +581,20 @@ def run_e2e(args, sp, p, dev, world):
         d2h += sum(v.numel() * v.element_size() for v in host_res[-1].values())
     d2h += ds.AGG_WORDS * 8 * len(host_chunks)
     agg_host = torch.empty(ds.AGG_WORDS * len(host_chunks), dtype=torch.int64, pin_memory=True)
-    ws = None
+    # one workspace for the largest chunk
+    ws_bytes = 0
+    for hc in host_chunks:
+        dpc = ds.DeviceProblem(hc["scen_dnn_off"].numel() - 1, hc["dnn_row_off"].numel() - 1,
+                               int(hc["dnn_row_off"][-1]), *[bufs[0][k] for k in fields])
+        ws_bytes = max(ws_bytes, ds.workspace_size(dpc, p))
+    ws = ds.Workspace(ws_bytes, dev)
+    # two output sets for the largest chunk
+    maxS = max(hc["scen_dnn_off"].numel() - 1 for hc in host_chunks)
+    maxD = max(hc["dnn_row_off"].numel() - 1 for hc in host_chunks)
+    dmax = ds.DeviceProblem(maxS, maxD, 0, *[bufs[0][k] for k in fields])
+    outs = [ds.alloc_outputs(dmax, agg=True), ds.alloc_outputs(dmax, agg=True)]
 
     def one_step():
-        nonlocal ws
         copied = [torch.cuda.Event() for _ in host_chunks]
         done = [torch.cuda.Event() for _ in host_chunks]
         for c, hc in enumerate(host_chunks):
@@ -583,13 +610,7 @@ def run_e2e(args, sp, p, dev, world):
             D = hc["dnn_row_off"].numel() - 1
             R = int(hc["dnn_row_off"][-1])
             dpc = ds.DeviceProblem(S, D, R, *[b[k] for k in fields])
-            if len(outs) < 2:
-                outs.append(ds.alloc_outputs(dpc, agg=True))
             o = outs[c % 2]
-            if o["demand"].numel() < D or o["u"].numel() < S:
-                outs[c % 2] = o = ds.alloc_outputs(dpc, agg=True)
-            if ws is None:
-                ws = ds.Workspace(ds.workspace_size(dpc, p), dev)
             ds.eval_batch(dpc, p, out=o, ws=ws)
             for k in res_fields:
                 host_res[c][k].copy_(o[k][:S], non_blocking=True)
@@ -627,10 +648,10 @@ def run_sim(args, rank, world, local):
     import synth
     from paper_2304_13541_b200 import dstack as ds
 
-    dev = torch.device("cuda", local)
+    dev = bench_device(local)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev)
     sp0, p = synth.config(5, num_scen=args.scen or None)
     per_gpu = sp0.num_scen
     sp = sp0.replace(scen_base=rank * per_gpu)
