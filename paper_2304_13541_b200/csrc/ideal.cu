@@ -60,6 +60,9 @@ __global__ void __launch_bounds__(256) k_ideal_rows(IdealArgs a) {
 // in shared memory for the lexicographic read-back.  Each lane keeps its chain position in registers and
 // prefetches its next row, so a completion does not wait on global memory.
 constexpr int IDEAL_WARPS = 8;
+#ifndef DSTACK_IDEAL_SHORTCUTS
+#define DSTACK_IDEAL_SHORTCUTS 1   // reuse the selection when no (rank, g) changed; all-fit shortcut (A/B switch)
+#endif
 
 struct IdealRow {
   int64_t i;      // absolute row index (r1 = end of chain)
@@ -115,6 +118,9 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
       uint32_t rp = 0, rem = cur.tau, dl = slo, comp = 0, rank = 0;
       const uint32_t n = (uint32_t)__popc(__ballot_sync(FULL, live));
       bool dirty = true;
+      bool resel = true;   // the selection must be recomputed (first event, a rank or a live item's g changed)
+      bool sel = false;
+      uint64_t gsum = 0;
       uint64_t util = 0, t = 0;
       while (n > 0 && t < T) {
         if (dirty) {   // priority rank among the live DNNs: (batch deadline, index)
@@ -127,9 +133,19 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
           }
           dirty = false;
         }
-        bool sel = false;
-        uint64_t gsum = 0;
-        if (n <= 10) {
+        // The max-sum subset depends only on the live items' (rank, g): when no rank and no g changed since the
+        // last event (a repeated execution R_i > 1, or a next kernel of the same demand), the previous selection
+        // is still the lexicographically-first optimum.  When every live item fits (sum g <= L) the unique
+        // optimum is all of them (g >= 1).
+        const uint32_t gtot = DSTACK_IDEAL_SHORTCUTS ? __reduce_add_sync(FULL, live ? cur.g : 0u) : 0xFFFFFFFFu;
+        if (DSTACK_IDEAL_SHORTCUTS && !resel) {
+          // keep sel, gsum
+        } else if (DSTACK_IDEAL_SHORTCUTS && gtot <= (uint32_t)L) {
+          sel = live;
+          gsum = gtot;
+        } else if (n <= 10) {
+          sel = false;
+          gsum = 0;
           // <= 1024 subsets: enumerate them all (8 per lane per round, 2^(n-8) rounds).  Subset index bit p <->
           // the item of rank n-1-p, so the largest index among the max-sum subsets is the lexicographically-
           // first (priority order) optimal subset -- the one the read-back below selects -- and one
@@ -164,6 +180,8 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
           gsum = best >> 10;
           sel = live && ((best >> (n - 1 - rank)) & 1u);
         } else {
+          sel = false;
+          gsum = 0;
           // suffix reachability: reach[q] = subset sums of the items of rank >= q
           uint32_t m = lane == 0 ? 1u : 0u;
           reach[n][lane] = (uint8_t)m;
@@ -200,6 +218,7 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
         util += gsum * dt;
         t += dt;
         bool done_batch = false;
+        const uint32_t g_before = cur.g;
         if (sel) {
           rem -= dt;
           if (rem == 0) {   // next execution of the chain
@@ -219,6 +238,7 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
           }
         }
         dirty = __any_sync(FULL, done_batch);
+        resel = dirty || __any_sync(FULL, cur.g != g_before);
         __syncwarp();
       }
       const uint64_t bsum = warp_sum_u64(act ? (uint64_t)comp * a.batch[k] : 0ull);
