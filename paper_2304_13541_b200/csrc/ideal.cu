@@ -182,12 +182,14 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
         } else {
           sel = false;
           gsum = 0;
-          // suffix reachability: reach[q] = subset sums of the items of rank >= q
+          // suffix reachability: reach[q] = subset sums of the items of rank >= q; the items' weights by rank
+          // come from shared memory (grank), so both passes are warp-uniform loops without owner look-ups
+          if (live) grank[rank] = (uint8_t)cur.g;
+          __syncwarp();
           uint32_t m = lane == 0 ? 1u : 0u;
           reach[n][lane] = (uint8_t)m;
           for (int q = (int)n - 1; q >= 0; --q) {
-            const int own = __ffs(__ballot_sync(FULL, live && rank == (uint32_t)q)) - 1;
-            const uint32_t gq = __shfl_sync(FULL, cur.g, own);
+            const uint32_t gq = grank[q];
             const uint32_t sa = gq >> 5, sb = gq & 31u;
             const uint32_t v = __shfl_sync(FULL, m, (lane - (int)sb) & 31);
             m |= (v << ((uint32_t)lane >= sb ? sa : sa + 1u)) & 0xFFu;
@@ -200,17 +202,16 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
           gsum = (uint64_t)(target > 0 ? target : 0);
           __syncwarp();
           // lexicographic read-back in priority order: include an item iff the rest can still complete target
+          uint32_t selmask = 0;
           for (uint32_t q = 0; q < n; ++q) {
-            const int own = __ffs(__ballot_sync(FULL, live && rank == q)) - 1;
-            const int gq = (int)__shfl_sync(FULL, cur.g, own);
-            if (gq <= target) {
-              const int c = target - gq;
-              if ((reach[q + 1][c & 31] >> (c >> 5)) & 1u) {
-                if (lane == own) sel = true;
-                target -= gq;
-              }
+            const int gq = (int)grank[q];
+            const int c = target - gq;
+            if (c >= 0 && ((reach[q + 1][c & 31] >> (c >> 5)) & 1u)) {
+              selmask |= 1u << q;
+              target = c;
             }
           }
+          sel = live && ((selmask >> rank) & 1u);
         }
         uint32_t dt = __reduce_min_sync(FULL, sel ? rem : 0xFFFFFFFFu);
         if (!__any_sync(FULL, sel) || dt == 0) break;
