@@ -60,6 +60,9 @@ __global__ void __launch_bounds__(256) k_ideal_rows(IdealArgs a) {
 // in shared memory for the lexicographic read-back.  Each lane keeps its chain position in registers and
 // prefetches its next row, so a completion does not wait on global memory.
 constexpr int IDEAL_WARPS = 8;
+#ifndef DSTACK_IDEAL_ENUM_MAX
+#define DSTACK_IDEAL_ENUM_MAX 10   // live items up to which every subset is enumerated (else the DP; <= 10)
+#endif
 #ifndef DSTACK_IDEAL_SHORTCUTS
 #define DSTACK_IDEAL_SHORTCUTS 1   // reuse the selection when no (rank, g) changed; all-fit shortcut (A/B switch)
 #endif
@@ -137,13 +140,14 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
         // last event (a repeated execution R_i > 1, or a next kernel of the same demand), the previous selection
         // is still the lexicographically-first optimum.  When every live item fits (sum g <= L) the unique
         // optimum is all of them (g >= 1).
-        const uint32_t gtot = DSTACK_IDEAL_SHORTCUTS ? __reduce_add_sync(FULL, live ? cur.g : 0u) : 0xFFFFFFFFu;
+        uint32_t gtot = 0xFFFFFFFFu;
+        if (DSTACK_IDEAL_SHORTCUTS && resel) gtot = __reduce_add_sync(FULL, live ? cur.g : 0u);
         if (DSTACK_IDEAL_SHORTCUTS && !resel) {
           // keep sel, gsum
         } else if (DSTACK_IDEAL_SHORTCUTS && gtot <= (uint32_t)L) {
           sel = live;
           gsum = gtot;
-        } else if (n <= 10) {
+        } else if (n <= DSTACK_IDEAL_ENUM_MAX) {
           sel = false;
           gsum = 0;
           // <= 1024 subsets: enumerate them all (8 per lane per round, 2^(n-8) rounds).  Subset index bit p <->
