@@ -65,10 +65,10 @@ __device__ __forceinline__ uint32_t bytes_below(int x, int base) {
 __device__ __forceinline__ uint32_t wmaxmin_lane(uint32_t dem, int lane, int nd, int32_t L) {
   const uint32_t key = (dem << 5) | (uint32_t)lane;   // dem == 0 for lanes >= nd
   uint32_t before = 0;
-#pragma unroll 8
-  for (int q = 0; q < 32; ++q) {
+#pragma unroll 4
+  for (int q = 0; q < nd; ++q) {   // nd <= 32, warp-uniform
     const uint32_t kq = __shfl_sync(FULL, key, q);
-    if (q < nd && kq < key) before += kq >> 5;
+    if (kq < key) before += kq >> 5;
   }
   const uint32_t tot = __reduce_add_sync(FULL, dem);
   const int64_t rem_before = (int64_t)L - (int64_t)before;
