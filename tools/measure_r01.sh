@@ -10,3 +10,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 ncu --set full --import-source on --clock-control none -k 'regex:k_prof_fast|k_cycle' -c 2 -o gpurun_out/full_final python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-compare --no-below-knee --no-knee-probe --no-cluster > gpurun_out/full_bench.log 2>&1
 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err
 tail -c 400 gpurun_out/final_bench.err
+python bench.py --config 2 --no-cpu-baseline > gpurun_out/final_bench_cfg2.json 2>&1
+python bench.py --config 4 --no-cpu-baseline > gpurun_out/final_bench_cfg4.json 2>&1
+python bench.py --config 5 > gpurun_out/final_bench_cfg5.json 2>&1
