@@ -241,6 +241,7 @@ static int ideal_impl(const dstack_problem_t *pb, const dstack_params_t *p, cons
     std::memset(&ia, 0, sizeof(ia));
     ia.pb = *pb; ia.p = *p; ia.demand = demand; ia.batch = batch; ia.u_ideal = out->u_ideal;
     ia.thr_ideal = out->thr_ideal;
+    ia.work_ctr = (uint32_t *)((char *)ws + ws_layout(pb, p).ctr) + 2;
     rc = launch_ideal(ia, (char *)ws + ws_layout(pb, p).ideal, s, &g_launches);
   }
   return rc;
@@ -373,6 +374,7 @@ int dstack_compare(const dstack_problem_t *pb, const dstack_params_t *p, const u
   c.pb = *pb; c.p = *p; c.demand = demand; c.batch = batch; c.alloc = alloc_q16;
   c.dtab_rows = (uint16_t *)((char *)ws + ws_layout(pb, p).dtab);
   c.u = u; c.thr = thr; c.jain = jain;
+  c.work_ctr = (uint32_t *)((char *)ws + ws_layout(pb, p).ctr) + 3;
   return finish(launch_compare(c, (cudaStream_t)stream, &g_launches));
 }
 
@@ -390,7 +392,7 @@ int dstack_cluster(const dstack_problem_t *pb, const dstack_params_t *p, int32_t
   if (ws_bytes < need || (need > 0 && !ws)) return DSTACK_EWORKSPACE;
   if (!have_device()) return DSTACK_ELAUNCH;
   return finish(launch_cluster(*pb, *p, gpus, demand, batch, (uint16_t *)((char *)ws + ws_layout(pb, p).dtab), u, thr,
-                               (cudaStream_t)stream, &g_launches));
+                               (uint32_t *)((char *)ws + ws_layout(pb, p).ctr) + 4, (cudaStream_t)stream, &g_launches));
 }
 
 int dstack_aggregate(const dstack_problem_t *pb, const dstack_params_t *p, dstack_out_t *out, void *ws,

@@ -29,6 +29,7 @@ struct CluArgs {
   const uint8_t *batch;
   uint16_t *dtab_rows;   // workspace
   double *u, *thr;       // [num_scen * DSTACK_NCLU]
+  uint32_t *work_ctr;    // workspace word: scenario counter (NULL: grid stride)
 };
 
 __global__ void __launch_bounds__(CLU_WARPS * 32, DSTACK_CLU_MINB) k_cluster(const __grid_constant__ CluArgs a) {
@@ -38,7 +39,9 @@ __global__ void __launch_bounds__(CLU_WARPS * 32, DSTACK_CLU_MINB) k_cluster(con
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int32_t L = a.p.L, slot = a.p.slot_us, b_lo = a.p.b_min, G = a.G;
   const double NLg = (double)L;
-  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < a.pb.num_scen; s += nwarps) {
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int64_t s = warp_next_item(a.work_ctr, -1, gwarp, nwarps, lane); s < a.pb.num_scen;
+       s = warp_next_item(a.work_ctr, s, gwarp, nwarps, lane)) {
     const int32_t k0 = a.pb.scen_dnn_off[s], nd = a.pb.scen_dnn_off[s + 1] - k0;
     double ou = 0.0, othr = 0.0;   // lane c < 4 holds policy c's results
     const bool mine = lane < nd && nd <= DSTACK_MAX_DNN_PER_SCEN;
@@ -168,15 +171,21 @@ __global__ void __launch_bounds__(CLU_WARPS * 32, DSTACK_CLU_MINB) k_cluster(con
 }
 
 int launch_cluster(const dstack_problem_t &pb, const dstack_params_t &p, int32_t G, const uint16_t *demand,
-                   const uint8_t *batch, uint16_t *dtab_rows, double *u, double *thr, cudaStream_t s, int *launches) {
+                   const uint8_t *batch, uint16_t *dtab_rows, double *u, double *thr, uint32_t *work_ctr, cudaStream_t s,
+                   int *launches) {
   if (pb.num_scen <= 0) return 0;
   CluArgs a;
   a.pb = pb; a.p = p; a.G = G; a.demand = demand; a.batch = batch; a.dtab_rows = dtab_rows; a.u = u; a.thr = thr;
+  a.work_ctr = DSTACK_DYN_SCEN ? work_ctr : nullptr;
   const size_t smem = sizeof(CycSmem) * CLU_WARPS;
   int64_t blocks = (pb.num_scen + CLU_WARPS - 1) / CLU_WARPS;
   const int64_t cap = (int64_t)num_sms() * DSTACK_CLU_GRID;
   if (blocks > cap) blocks = cap;
   cudaFuncSetAttribute(k_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (a.work_ctr) {
+    if (cudaMemsetAsync(a.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
+    blocks = resident_wave(k_cluster, CLU_WARPS * 32, smem, blocks);
+  }
   k_cluster<<<(unsigned)blocks, CLU_WARPS * 32, smem, s>>>(a);
   ++*launches;
   return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;

@@ -46,6 +46,22 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 }
 __device__ __forceinline__ uint32_t warp_or(uint32_t v) { return __reduce_or_sync(FULL, v); }
 
+#ifndef DSTACK_DYN_SCEN
+#define DSTACK_DYN_SCEN 1   // 1: k_ideal_sim, k_compare, k_cluster pull scenarios from a work counter (A/B switch)
+#endif
+
+// Work distribution of warp-per-item kernels: with a counter (a resident wave of warps, each taking the next item
+// when it finishes one -- items of very different cost balance themselves) or else a grid stride.
+__device__ __forceinline__ int64_t warp_next_item(uint32_t *ctr, int64_t prev, int64_t gwarp, int64_t nwarps,
+                                                  int lane) {
+  if (ctr) {
+    uint32_t v = 0;
+    if (lane == 0) v = atomicAdd(ctr, 1u);
+    return (int64_t)__shfl_sync(FULL, v, 0);
+  }
+  return prev < 0 ? gwarp : prev + nwarps;
+}
+
 // bulk L2 prefetch of [ptr, ptr+bytes) (TMA engine, no registers / no wait): 16-byte aligned chunks
 __device__ __forceinline__ void prefetch_l2(const void *ptr, int64_t bytes) {
   if (bytes <= 0) return;

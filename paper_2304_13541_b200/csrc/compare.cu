@@ -33,7 +33,9 @@ __global__ void __launch_bounds__(CMP_WARPS * 32, DSTACK_CMP_MINB) k_compare(Cmp
   CycSmem &sm = reinterpret_cast<CycSmem *>(smem_raw)[warp];
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int32_t L = a.p.L, slot = a.p.slot_us, b_lo = a.p.b_min;
-  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < a.pb.num_scen; s += nwarps) {
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int64_t s = warp_next_item(a.work_ctr, -1, gwarp, nwarps, lane); s < a.pb.num_scen;
+       s = warp_next_item(a.work_ctr, s, gwarp, nwarps, lane)) {
     const int32_t k0 = a.pb.scen_dnn_off[s], nd = a.pb.scen_dnn_off[s + 1] - k0;
     double ou = 0.0, othr = 0.0, oj = 0.0;   // lane c < 5 holds scheduler c's results
     const bool mine = lane < nd && nd <= DSTACK_MAX_DNN_PER_SCEN;
@@ -159,7 +161,13 @@ int launch_compare(const CmpArgs &a, cudaStream_t s, int *launches) {
   const int64_t cap = (int64_t)num_sms() * DSTACK_CMP_GRID;
   if (blocks > cap) blocks = cap;
   cudaFuncSetAttribute(k_compare, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_compare<<<(unsigned)blocks, CMP_WARPS * 32, smem, s>>>(a);
+  CmpArgs b = a;
+  if (!DSTACK_DYN_SCEN) b.work_ctr = nullptr;
+  if (b.work_ctr) {
+    if (cudaMemsetAsync(b.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
+    blocks = resident_wave(k_compare, CMP_WARPS * 32, smem, blocks);
+  }
+  k_compare<<<(unsigned)blocks, CMP_WARPS * 32, smem, s>>>(b);
   ++*launches;
   return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;
 }

@@ -92,7 +92,9 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
   for (int k = 0; k < 8; ++k)
     if (lane + 32 * k <= L) capmask |= 1u << k;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < a.pb.num_scen; s += nwarps) {
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (int64_t s = warp_next_item(a.work_ctr, -1, gwarp, nwarps, lane); s < a.pb.num_scen;
+       s = warp_next_item(a.work_ctr, s, gwarp, nwarps, lane)) {
     const int32_t k0 = a.pb.scen_dnn_off[s], nd = a.pb.scen_dnn_off[s + 1] - k0;
     double ui = 0.0, ti = 0.0;
     const bool mine = lane < nd && nd <= DSTACK_MAX_DNN_PER_SCEN;
@@ -277,6 +279,11 @@ int launch_ideal(IdealArgs a, void *ws, cudaStream_t s, int *launches) {
   }
   int64_t blocks = (a.pb.num_scen + IDEAL_WARPS - 1) / IDEAL_WARPS;
   if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  if (!DSTACK_DYN_SCEN) a.work_ctr = nullptr;
+  if (a.work_ctr) {   // one resident wave pulling scenarios (their event counts differ by orders of magnitude)
+    if (cudaMemsetAsync(a.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
+    blocks = resident_wave(k_ideal_sim, IDEAL_WARPS * 32, 0, blocks);
+  }
   k_ideal_sim<<<(unsigned)blocks, IDEAL_WARPS * 32, 0, s>>>(a);
   ++*launches;
   return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;

@@ -84,6 +84,7 @@ struct IdealArgs {
   uint16_t *ex_g;     // [num_rows] workspace
   uint32_t *ex_tau;   // [num_rows] workspace
   double *u_ideal, *thr_ideal;
+  uint32_t *work_ctr;   // workspace word: k_ideal_sim's scenario counter (NULL: grid stride)
 };
 
 struct CmpArgs {
@@ -94,6 +95,7 @@ struct CmpArgs {
   const uint32_t *alloc;
   uint16_t *dtab_rows;      // workspace
   double *u, *thr, *jain;   // [num_scen * DSTACK_NCMP]
+  uint32_t *work_ctr;       // workspace word: scenario counter (NULL: grid stride)
 };
 
 struct AggArgs {
@@ -118,7 +120,17 @@ size_t sim_fill_log_bytes();
 int launch_agg(const AggArgs &a, cudaStream_t s, int *launches);
 int launch_compare(const CmpArgs &a, cudaStream_t s, int *launches);
 int launch_cluster(const dstack_problem_t &pb, const dstack_params_t &p, int32_t G, const uint16_t *demand,
-                   const uint8_t *batch, uint16_t *dtab_rows, double *u, double *thr, cudaStream_t s, int *launches);
+                   const uint8_t *batch, uint16_t *dtab_rows, double *u, double *thr, uint32_t *work_ctr, cudaStream_t s,
+                   int *launches);
+
+// one resident wave of `kern` (blocks per SM from the occupancy calculator x SMs), at most `blocks`
+template <typename K>
+inline int64_t resident_wave(K kern, int threads, size_t smem, int64_t blocks) {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem) != cudaSuccess || nb <= 0) nb = 1;
+  const int64_t w = (int64_t)nb * num_sms();
+  return blocks < w ? blocks : w;
+}
 size_t ideal_ws_bytes(int64_t num_rows);
 size_t agg_ws_bytes();
 
