@@ -352,6 +352,7 @@ int dstack_simulate(const dstack_problem_t *pb, const dstack_params_t *p, const 
   m.scen_base = scen_base; m.demand = a.demand; m.batch = a.batch; m.status = a.status; m.ws_RT = a.ws_RT;
   m.ws_D = a.ws_D; m.dtab_rows = (uint16_t *)(base + w.dtab); m.fill_log = (uint64_t *)(base + sl.log);
   m.out = *out;
+  m.work_ctr = (uint32_t *)(base + w.ctr) + 5;
   return finish(launch_sim(m, s, &g_launches));
 }
 

@@ -74,6 +74,7 @@ struct SimArgs {
   uint16_t *dtab_rows;
   uint64_t *fill_log;   // SIM_MAX_WARPS x DSTACK_MAX_FILL_RUNS
   dstack_sim_out_t out;
+  uint32_t *work_ctr;   // workspace word: scenario counter (NULL: grid stride)
 };
 
 struct IdealArgs {

@@ -39,7 +39,8 @@ __global__ void __launch_bounds__(SIM_WARPS * 32, DSTACK_SIM_MINB) k_sim(SimArgs
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint64_t *fill_log = a.fill_log + gwarp * DSTACK_MAX_FILL_RUNS;
   const int32_t L = a.p.L, slot = a.p.slot_us, b_lo = a.p.b_min;
-  for (int64_t s = gwarp; s < a.pb.num_scen; s += nwarps) {
+  for (int64_t s = warp_next_item(a.work_ctr, -1, gwarp, nwarps, lane); s < a.pb.num_scen;
+       s = warp_next_item(a.work_ctr, s, gwarp, nwarps, lane)) {
     const int32_t k0 = a.pb.scen_dnn_off[s], nd = a.pb.scen_dnn_off[s + 1] - k0;
     const int64_t gs = a.scen_base + s;
     uint8_t sst = DSTACK_ST_OK;
@@ -191,7 +192,10 @@ int launch_sim(const SimArgs &a, cudaStream_t s, int *launches) {
   if (cap * SIM_WARPS > SIM_MAX_WARPS) cap = SIM_MAX_WARPS / SIM_WARPS;
   if (blocks > cap) blocks = cap;
   cudaFuncSetAttribute(k_sim, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_sim<<<(unsigned)blocks, SIM_WARPS * 32, smem, s>>>(a);
+  SimArgs b = a;
+  if (!DSTACK_DYN_SCEN) b.work_ctr = nullptr;
+  if (b.work_ctr && cudaMemsetAsync(b.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
+  k_sim<<<(unsigned)blocks, SIM_WARPS * 32, smem, s>>>(b);
   ++*launches;
   return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;
 }
