@@ -169,7 +169,8 @@ int dstack_knee(const dstack_problem_t *pb, const dstack_params_t *p, int32_t ba
  * 1/(f_L(m+1,b)^2 S(m+1)) > 1/(f_L(m,b)^2 S(m)) (Eq. 6's objective, exact), else hi = m; stops at lo == hi.
  * knee_out[k] = lo (0 unless st_out[k] is OK), probes_out[k] = the number of steps (<= ceil(log2 L) + 1).
  * The result is a discrete local maximum of Eq. 6's objective; it equals dstack_knee's exact argmax whenever
- * that objective is unimodal over the levels.  Statuses as dstack_knee.  Device arrays [num_dnn]. */
+ * that objective is unimodal over the levels.  Statuses as dstack_knee.  Device arrays [num_dnn].  ws may be NULL;
+ * with >= dstack_workspace_size() bytes the DNNs are distributed by a work counter in it (faster, same results). */
 int dstack_knee_probe(const dstack_problem_t *pb, const dstack_params_t *p, int32_t batch, uint16_t *knee_out,
                       uint8_t *probes_out, uint8_t *st_out, void *ws, size_t ws_bytes, void *stream);
 

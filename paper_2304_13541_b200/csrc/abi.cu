@@ -168,7 +168,6 @@ int dstack_knee(const dstack_problem_t *pb, const dstack_params_t *p, int32_t ba
 
 int dstack_knee_probe(const dstack_problem_t *pb, const dstack_params_t *p, int32_t batch, uint16_t *knee_out,
                       uint8_t *probes_out, uint8_t *st_out, void *ws, size_t ws_bytes, void *stream) {
-  (void)ws; (void)ws_bytes;
   g_launches = 0;
   if (!problem_ok(pb) || !params_ok(p) || batch < 1 || batch > DSTACK_MAX_BATCH) return DSTACK_EINVAL;
   if (pb->num_dnn > 0 && (!knee_out || !probes_out || !st_out)) return DSTACK_EINVAL;
@@ -181,6 +180,8 @@ int dstack_knee_probe(const dstack_problem_t *pb, const dstack_params_t *p, int3
   std::memset(&a, 0, sizeof(a));
   a.pb = *pb; a.p = *p; a.knee_only = 1; a.knee_b = batch; a.knee = knee_out; a.status = st_out;
   a.probes = probes_out;
+  // with a workspace of dstack_workspace_size() bytes the DNNs are handed out by a counter, else grid stride
+  if (ws && ws_bytes >= dstack_workspace_size(pb, p)) a.work_ctr = (uint32_t *)((char *)ws + ws_layout(pb, p).ctr) + 6;
   return finish(launch_knee_probe(a, (cudaStream_t)stream, &g_launches));
 }
 

@@ -114,7 +114,9 @@ __global__ void __launch_bounds__(256, DSTACK_PROF_MINB) k_prof(ProfArgs a) {
   fill_stab(Stab, L, S_tot);
   __syncthreads();
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; k < a.pb.num_dnn; k += nwarps)
+  const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  for (int64_t k = warp_next_item(a.work_ctr, -1, gwarp, nwarps, lane); k < a.pb.num_dnn;
+       k = warp_next_item(a.work_ctr, k, gwarp, nwarps, lane))
     prof_one<PAR>(a, k, Stab, hist, cA, cU, lane);
 }
 
@@ -601,8 +603,8 @@ int launch_prof(const ProfArgs &a, cudaStream_t s, int *launches) {
   if (blocks > cap) blocks = cap;
   const bool fast = DSTACK_PROF_FAST && a.p.par_mode == 0 && a.p.wse_mode == 0 && a.p.b_min == 1 && !a.knee_only;
   ProfArgs b = a;
-  if (!DSTACK_PROF_DYN || !fast) b.work_ctr = nullptr;
-  if (b.work_ctr) {   // one resident wave (DSTACK_PROF_MINB blocks per SM) pulling groups of 32 DNNs
+  if (!DSTACK_PROF_DYN) b.work_ctr = nullptr;
+  if (b.work_ctr) {   // one resident wave (DSTACK_PROF_MINB blocks per SM) pulling groups of 32 DNNs (fast) or DNNs
     if (cudaMemsetAsync(b.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
     const int64_t wave = (int64_t)num_sms() * DSTACK_PROF_MINB;
     if (blocks > wave) blocks = wave;
@@ -622,8 +624,15 @@ int launch_knee_probe(const ProfArgs &a, cudaStream_t s, int *launches) {
   int64_t blocks = (a.pb.num_dnn + warps - 1) / warps;
   const int64_t cap = (int64_t)num_sms() * 8;
   if (blocks > cap) blocks = cap;
-  if (a.p.par_mode == 0) launch_k(k_prof<0>, a, blocks, threads, smem, s);
-  else launch_k(k_prof<1>, a, blocks, threads, smem, s);
+  ProfArgs b = a;
+  if (!DSTACK_PROF_DYN) b.work_ctr = nullptr;
+  if (b.work_ctr) {
+    if (cudaMemsetAsync(b.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
+    const int64_t wave = (int64_t)num_sms() * DSTACK_PROF_MINB;
+    if (blocks > wave) blocks = wave;
+  }
+  if (a.p.par_mode == 0) launch_k(k_prof<0>, b, blocks, threads, smem, s);
+  else launch_k(k_prof<1>, b, blocks, threads, smem, s);
   ++*launches;
   return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;
 }

@@ -226,8 +226,9 @@ def knee_probe(dp: DeviceProblem, p, batch: int):
     k = torch.zeros(max(dp.num_dnn, 1), dtype=torch.int16, device=dev)
     pr = torch.zeros(max(dp.num_dnn, 1), dtype=torch.uint8, device=dev)
     st = torch.zeros(max(dp.num_dnn, 1), dtype=torch.uint8, device=dev)
-    _check(_lib.dstack_knee_probe(C.byref(dp.c()), C.byref(cparams(p)), batch, _ptr(k), _ptr(pr), _ptr(st), None, 0,
-                                  _stream(dev)), "dstack_knee_probe")
+    ws = Workspace(workspace_size(dp, p), dev)
+    _check(_lib.dstack_knee_probe(C.byref(dp.c()), C.byref(cparams(p)), batch, _ptr(k), _ptr(pr), _ptr(st), ws.ptr(),
+                                  ws.nbytes, _stream(dev)), "dstack_knee_probe")
     return k[: dp.num_dnn], pr[: dp.num_dnn], st[: dp.num_dnn]
 
 
