@@ -383,6 +383,12 @@ def run_native(args, rank, world, local):
         "path_roofline": {"algorithmic_bytes_per_step": ab["path"],
                           "achieved_GBps": ab["path"] / (ms_max / args.steps / 1e3) / 1e9,
                           "frac": ab["path"] / (ms_max / args.steps / 1e3) / 1e9 / peak},
+        # a1-a4 alone (k_prof + k_wmaxmin) as the HBM-bound sub-path, algorithmic bytes / their time
+        "a1_a4_subpath": ({"ms": kern["k_prof"] + kern["k_wmaxmin"],
+                           "algorithmic_bytes": ab["k_prof"] + ab["k_wmaxmin"],
+                           "achieved_GBps": (ab["k_prof"] + ab["k_wmaxmin"]) / ((kern["k_prof"] + kern["k_wmaxmin"]) / 1e3) / 1e9,
+                           "frac": (ab["k_prof"] + ab["k_wmaxmin"]) / ((kern["k_prof"] + kern["k_wmaxmin"]) / 1e3) / 1e9 / peak}
+                          if "k_prof" in kern and "k_wmaxmin" in kern else None),
         "kernels_ms": kern, "kernels_share": {k: v / (ms_max / args.steps) for k, v in kern.items()},
         "gpu_launches": launches[0],
         "clocks": clocks,
