@@ -79,3 +79,20 @@ def test_config5_fullsize_sampled_parity(ds):
     arrived = r["arrived"].cpu().numpy()
     kept = (r["in_slo"] + r["late"] + r["unserved"]).cpu().numpy()
     assert np.array_equal(arrived, kept)   # conservation over all 100k scenarios
+
+
+def test_knee_probe_config3_fullsize_sampled(ds):
+    """F3 (dstack_knee_probe) over config 3's 10M DNNs in one call; every DNN of 200 sampled scenarios against
+    the oracle (level found, step count, status)."""
+    sp, p = synth.config(3)
+    g = synth.generate_device(sp, "cuda")
+    dp = ds.from_device_dict(g)
+    k, pr, st = ds.knee_probe(dp, p, 1)
+    torch.cuda.synchronize()
+    off = g["scen_dnn_off"].cpu().numpy()
+    idx = np.random.default_rng(5).choice(sp.num_scen, 200, replace=False)
+    dnn = torch.as_tensor(np.concatenate([np.arange(off[s], off[s + 1]) for s in idx]), device=k.device)
+    ko, pro, sto = oracle.knee_probe(synth.sample(sp, idx), p, 1)
+    assert np.array_equal(st[dnn].cpu().numpy(), sto)
+    assert np.array_equal(k[dnn].cpu().numpy().view(np.uint16), ko)
+    assert np.array_equal(pr[dnn].cpu().numpy(), pro)
