@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) k_ideal_rows(IdealArgs a) {
 // prefetches its next row, so a completion does not wait on global memory.
 constexpr int IDEAL_WARPS = 8;
 #ifndef DSTACK_IDEAL_ENUM_MAX
-#define DSTACK_IDEAL_ENUM_MAX 10   // live items up to which every subset is enumerated (else the DP; <= 10)
+#define DSTACK_IDEAL_ENUM_MAX 10   // live items up to which every subset is enumerated (else the DP; <= 12)
 #endif
 #ifndef DSTACK_IDEAL_SHORTCUTS
 #define DSTACK_IDEAL_SHORTCUTS 1   // reuse the selection when no (rank, g) changed; all-fit shortcut (A/B switch)
@@ -158,9 +158,10 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
           // max-reduction over (sum, index) decides.
           if (live) grank[rank] = (uint8_t)cur.g;
           __syncwarp();
-          uint32_t gp[10];
+          constexpr int NE = DSTACK_IDEAL_ENUM_MAX > 8 ? DSTACK_IDEAL_ENUM_MAX : 8;   // items enumerable
+          uint32_t gp[NE];
 #pragma unroll
-          for (int p = 0; p < 10; ++p) gp[p] = p < (int)n ? grank[n - 1 - p] : 0u;
+          for (int p = 0; p < NE; ++p) gp[p] = p < (int)n ? grank[n - 1 - p] : 0u;
           uint32_t lbase = 0;
 #pragma unroll
           for (int p = 3; p < 8; ++p)
@@ -172,18 +173,23 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
             for (int lo = 0; lo < 8; ++lo) {
               const uint32_t idx = (r << 8) | ((uint32_t)lane << 3) | (uint32_t)lo;
               const uint32_t sum = base + ((lo & 1) ? gp[0] : 0u) + ((lo & 2) ? gp[1] : 0u) + ((lo & 4) ? gp[2] : 0u);
-              const uint32_t key = (sum << 10) | idx;
+              const uint32_t key = (sum << NE) | idx;
               if (idx < nsub && sum <= (uint32_t)L && key > best) best = key;
             }
           };
           if (n <= 8) {
             scan8(lbase, 0u);
           } else {
-            for (uint32_t r = 0; r < (1u << (n - 8)); ++r)
-              scan8(lbase + ((r & 1u) ? gp[8] : 0u) + ((r & 2u) ? gp[9] : 0u), r);
+            for (uint32_t r = 0; r < (1u << (n - 8)); ++r) {
+              uint32_t rb = lbase;
+#pragma unroll
+              for (int p = 8; p < NE; ++p)
+                if ((r >> (p - 8)) & 1u) rb += gp[p];
+              scan8(rb, r);
+            }
           }
           best = __reduce_max_sync(FULL, best);   // the empty subset (key 0) is always feasible
-          gsum = best >> 10;
+          gsum = best >> NE;
           sel = live && ((best >> (n - 1 - rank)) & 1u);
         } else {
           sel = false;
