@@ -63,6 +63,9 @@ constexpr int IDEAL_WARPS = 8;
 #ifndef DSTACK_IDEAL_ENUM_MAX
 #define DSTACK_IDEAL_ENUM_MAX 10   // live items up to which every subset is enumerated (else the DP; <= 12)
 #endif
+#ifndef DSTACK_IDEAL_MITM
+#define DSTACK_IDEAL_MITM 1   // 11..16 live items: meet-in-the-middle enumeration instead of the DP (A/B switch)
+#endif
 #ifndef DSTACK_IDEAL_SHORTCUTS
 #define DSTACK_IDEAL_SHORTCUTS 1   // reuse the selection when no (rank, g) changed; all-fit shortcut (A/B switch)
 #endif
@@ -81,12 +84,19 @@ __device__ __forceinline__ IdealRow ideal_row_at(const IdealArgs &a, int64_t i, 
   return w;
 }
 
-__global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
+#ifndef DSTACK_IDEAL_MINB
+#define DSTACK_IDEAL_MINB 4   // 64 registers (the meet-in-the-middle branch would take 109)
+#endif
+__global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_sim(IdealArgs a) {
   __shared__ uint8_t reach_all[IDEAL_WARPS][DSTACK_MAX_DNN_PER_SCEN + 1][32];
   __shared__ uint8_t grank_all[IDEAL_WARPS][32];   // g of the live item of each priority rank
+  __shared__ uint32_t mbb_all[IDEAL_WARPS][8];     // meet in the middle: achievable B sums (256-bit set)
+  __shared__ int32_t mbl_all[IDEAL_WARPS][8];      // ... highest achievable B sum below each word
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t(*reach)[32] = reach_all[warp];
   uint8_t *grank = grank_all[warp];
+  uint32_t *mb_bits = mbb_all[warp];
+  int32_t *mb_below = mbl_all[warp];
   const int32_t L = a.p.L, slot = a.p.slot_us;
   uint32_t capmask = 0;   // bits k with capacity lane + 32 k <= L
   for (int k = 0; k < 8; ++k)
@@ -191,6 +201,61 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32) k_ideal_sim(IdealArgs a) {
           best = __reduce_max_sync(FULL, best);   // the empty subset (key 0) is always feasible
           gsum = best >> NE;
           sel = live && ((best >> (n - 1 - rank)) & 1u);
+        } else if (DSTACK_IDEAL_MITM && n <= 16) {
+          // meet in the middle: A = ranks 0..7 (A index bit p <-> rank 7 - p), B = ranks 8..n-1 (B index bit p <->
+          // rank n - 1 - p), 256 subsets each, 8 per lane.  The lexicographically-first optimal subset has the
+          // largest (A index, B index): first the largest A index among the A subsets that complete to the
+          // optimum (a + max{B sum <= L - a} maximal), then the largest B index whose sum completes it exactly.
+          if (live) grank[rank] = (uint8_t)cur.g;
+          if (lane < 8) mb_bits[lane] = 0u;
+          __syncwarp();
+          const uint32_t nB = n - 8;
+          uint32_t gA[8], gB[8];
+#pragma unroll
+          for (int p = 0; p < 8; ++p) { gA[p] = grank[7 - p]; gB[p] = p < (int)nB ? grank[n - 1 - p] : 0u; }
+          uint32_t baseA = 0, baseB = 0;
+#pragma unroll
+          for (int p = 3; p < 8; ++p)
+            if ((lane >> (p - 3)) & 1) { baseA += gA[p]; baseB += gB[p]; }
+          const bool bvalid_lane = ((uint32_t)lane << 3) < (1u << nB);
+          uint32_t sA[8], sB[8];
+#pragma unroll
+          for (int lo = 0; lo < 8; ++lo) {
+            sA[lo] = baseA + ((lo & 1) ? gA[0] : 0u) + ((lo & 2) ? gA[1] : 0u) + ((lo & 4) ? gA[2] : 0u);
+            sB[lo] = baseB + ((lo & 1) ? gB[0] : 0u) + ((lo & 2) ? gB[1] : 0u) + ((lo & 4) ? gB[2] : 0u);
+            if (bvalid_lane && sB[lo] <= (uint32_t)L) atomicOr(&mb_bits[sB[lo] >> 5], 1u << (sB[lo] & 31));
+          }
+          __syncwarp();
+          // highest achievable B sum in the words below w (the empty B subset makes sum 0 always achievable)
+          if (lane < 8) {
+            int h = -1;
+            for (int w = 0; w < lane; ++w) if (mb_bits[w]) h = 32 * w + 31 - __clz(mb_bits[w]);
+            mb_below[lane] = h;
+          }
+          __syncwarp();
+          uint32_t bestA = 0;
+#pragma unroll
+          for (int lo = 0; lo < 8; ++lo) {
+            if (sA[lo] > (uint32_t)L) continue;
+            const uint32_t c = (uint32_t)L - sA[lo], w = c >> 5;
+            const uint32_t m = mb_bits[w] & (0xFFFFFFFFu >> (31u - (c & 31u)));
+            const uint32_t mbs = m ? 32u * w + 31u - __clz(m) : (uint32_t)mb_below[w];
+            const uint32_t key = ((sA[lo] + mbs) << 8) | ((uint32_t)lane << 3) | (uint32_t)lo;
+            if (key > bestA) bestA = key;
+          }
+          bestA = __reduce_max_sync(FULL, bestA);   // the empty A subset always qualifies
+          const uint32_t best = bestA >> 8, ia = bestA & 255u;
+          uint32_t sa = 0;
+#pragma unroll
+          for (int p = 0; p < 8; ++p) if ((ia >> p) & 1u) sa += gA[p];
+          const uint32_t tb = best - sa;
+          uint32_t kb = 0;
+#pragma unroll
+          for (int lo = 0; lo < 8; ++lo)
+            if (bvalid_lane && sB[lo] == tb) kb = ((uint32_t)lane << 3) + (uint32_t)lo + 1u;   // ascending lo
+          const uint32_t ib = __reduce_max_sync(FULL, kb) - 1u;
+          gsum = best;
+          sel = live && (rank < 8 ? ((ia >> (7 - rank)) & 1u) : ((ib >> (n - 1 - rank)) & 1u));
         } else {
           sel = false;
           gsum = 0;
