@@ -17,6 +17,8 @@
  *    Inputs must stay alive and unmodified, outputs untouched, until the stream is synchronised.
  *  - No call allocates device memory.  Scratch comes from the caller's workspace of
  *    >= dstack_workspace_size() bytes (256-byte aligned); ws may be NULL when that size is 0.
+ *    The workspace holds the calls' intermediate tables and work counters (reset by the call, on its stream),
+ *    so one workspace must not serve two calls that may run concurrently (e.g. on different streams).
  *  - Return value: DSTACK_OK (0) or a negative DSTACK_E* code: a synchronous argument or launch
  *    error, in which case no work was enqueued (EINVAL/EWORKSPACE) or the launch failed (ELAUNCH).
  *  - Per-DNN / per-scenario data conditions are VALUES written to status arrays, not errors:
