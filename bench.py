@@ -339,9 +339,11 @@ def run_native(args, rank, world, local):
         kp_line = run_knee_probe_leg(args, ds, dp, p, stream, world)
 
     # ---- e2e: the public API from pinned host buffers, H2D + compute + D2H of results each step ----
-    e2e = None
+    e2e = e2e_wide = None
     if not args.no_e2e:
-        e2e = run_e2e(args, sp, p, dev, world)
+        e2e = run_e2e(args, sp, p, dev, world, packed=True)
+        if world == 1 and e2e.get("transport", "").startswith("compact"):
+            e2e_wide = run_e2e(args, sp, p, dev, world, packed=False)   # the same path with the rows sent wide
 
     if rank != 0:
         if world > 1:
@@ -393,6 +395,7 @@ def run_native(args, rank, world, local):
         "gpu_launches": launches[0],
         "clocks": clocks,
         "e2e": e2e,
+        "e2e_wide_rows": e2e_wide,
         "compare": cmp_line,
         "below_knee": bk_line,
         "knee_probe": kp_line,
@@ -540,10 +543,12 @@ def run_knee_probe_leg(args, ds, dp, p, stream, world):
             "max_steps": int(pr.max().item()) if dp.num_dnn else 0}
 
 
-def run_e2e(args, sp, p, dev, world):
+def run_e2e(args, sp, p, dev, world, packed=True):
     """End-to-end through the public API: per step, every chunk's inputs are copied host->device from
     pinned memory (copy stream, double-buffered), evaluated with dstack_eval_batch, and its per-scenario
-    results copied back device->host.  Device-timed with CUDA events (max over ranks)."""
+    results copied back device->host.  Device-timed with CUDA events (max over ranks).
+    packed: the rows travel in the compact transport (nr = n | R << 12 as u16 beside d as u32, 6 B/row instead of
+    10; dstack_unpack_nr expands them on the device inside the timed region) when every row fits it."""
     import torch
     import torch.distributed as dist
 
@@ -552,7 +557,8 @@ def run_e2e(args, sp, p, dev, world):
 
     nch = max(1, args.e2e_chunks)
     per = (sp.num_scen + nch - 1) // nch
-    fields = ("scen_dnn_off", "dnn_row_off", "t_p", "t_np", "mem_bw", "slo_us", "asm_us", "bmax", "n", "r", "d")
+    hdr_fields = ("scen_dnn_off", "dnn_row_off", "t_p", "t_np", "mem_bw", "slo_us", "asm_us", "bmax")
+    prob_fields = hdr_fields + ("n", "r", "d")
     host_chunks = []
     try:
         for c in range(nch):
@@ -561,19 +567,53 @@ def run_e2e(args, sp, p, dev, world):
             if cnt <= 0:
                 break
             g = synth.generate_device(sp.replace(scen_base=sp.scen_base + s0, num_scen=cnt), dev)
-            # straight into pinned host buffers (no pageable intermediate: 8 ranks x ~14 GB of rows on one host)
+            fields = hdr_fields + ("d",)
+            if packed:
+                R = int(g["dnn_row_off"][-1].item())
+                nn = g["n"][:R].to(torch.int64) & 0xFFFFFFFF
+                rr = g["r"][:R].to(torch.int64) & 0xFFFF
+                if R and (int(nn.max()) >= 4096 or int(rr.min()) < 1 or int(rr.max()) > 15):
+                    packed = False
+                else:
+                    nr = torch.zeros(g["r"].numel(), dtype=torch.int16, device=dev)
+                    nr[:R] = (nn | (rr << 12)).to(torch.int32).to(torch.int16)
+                    g["nr"] = nr
+                del nn, rr
+            fields += ("nr",) if packed else ("n", "r")
+            # straight into pinned host buffers (no pageable intermediate: 8 ranks x several GB of rows on one host)
             host_chunks.append({k: torch.empty(g[k].shape, dtype=g[k].dtype, pin_memory=True).copy_(g[k])
                                 for k in fields})
             del g
     except RuntimeError as e:
         return {"value": None, "unit": UNIT, "error": f"pinned host staging failed: {e}"[:200]}
+    if not packed:   # some chunk could not be packed: every chunk travels wide (re-stage the packed ones)
+        if any("nr" in hc for hc in host_chunks):
+            host_chunks.clear()
+            return run_e2e(args, sp, p, dev, world, packed=False)
+        return _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, False)
+    return _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, True)
+
+
+def _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, packed):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2304_13541_b200 import dstack as ds
+
     torch.cuda.synchronize()
     copy_s = torch.cuda.Stream(dev)
     comp_s = torch.cuda.current_stream(dev)
-    # two device buffer sets, every field sized for the largest chunk of that field
+    tfields = tuple(host_chunks[0].keys())   # the transported fields
+    maxrows = max(hc["d"].numel() for hc in host_chunks)
+
+    # two device buffer sets, every field sized for the largest chunk of that field (+ the unpacked rows)
     def dev_max():
-        return {k: torch.empty(max(hc[k].numel() for hc in host_chunks), dtype=host_chunks[0][k].dtype, device=dev)
-                for k in fields}
+        b = {k: torch.empty(max(hc[k].numel() for hc in host_chunks), dtype=host_chunks[0][k].dtype, device=dev)
+             for k in tfields}
+        if packed:
+            b["n"] = torch.empty(maxrows + 16, dtype=torch.int32, device=dev)
+            b["r"] = torch.empty(maxrows + 16, dtype=torch.int16, device=dev)
+        return b
     bufs = [dev_max(), dev_max()]
     res_fields = ("scen_status", "u_static", "u", "thr", "misses")
     h2d = sum(v.numel() * v.element_size() for hc in host_chunks for v in hc.values())
@@ -591,14 +631,15 @@ def run_e2e(args, sp, p, dev, world):
     ws_bytes = 0
     for hc in host_chunks:
         dpc = ds.DeviceProblem(hc["scen_dnn_off"].numel() - 1, hc["dnn_row_off"].numel() - 1,
-                               int(hc["dnn_row_off"][-1]), *[bufs[0][k] for k in fields])
+                               int(hc["dnn_row_off"][-1]), *[bufs[0][k] for k in prob_fields])
         ws_bytes = max(ws_bytes, ds.workspace_size(dpc, p))
     ws = ds.Workspace(ws_bytes, dev)
     # two output sets for the largest chunk
     maxS = max(hc["scen_dnn_off"].numel() - 1 for hc in host_chunks)
     maxD = max(hc["dnn_row_off"].numel() - 1 for hc in host_chunks)
-    dmax = ds.DeviceProblem(maxS, maxD, 0, *[bufs[0][k] for k in fields])
+    dmax = ds.DeviceProblem(maxS, maxD, 0, *[bufs[0][k] for k in prob_fields])
     outs = [ds.alloc_outputs(dmax, agg=True), ds.alloc_outputs(dmax, agg=True)]
+    launches = [0]
 
     def one_step():
         copied = [torch.cuda.Event() for _ in host_chunks]
@@ -615,9 +656,13 @@ def run_e2e(args, sp, p, dev, world):
             S = hc["scen_dnn_off"].numel() - 1
             D = hc["dnn_row_off"].numel() - 1
             R = int(hc["dnn_row_off"][-1])
-            dpc = ds.DeviceProblem(S, D, R, *[b[k] for k in fields])
+            if packed:
+                ds.unpack_nr(b["nr"], b["n"], b["r"], R)
+                launches[0] += ds.last_launch_count()
+            dpc = ds.DeviceProblem(S, D, R, *[b[k] for k in prob_fields])
             o = outs[c % 2]
             ds.eval_batch(dpc, p, out=o, ws=ws)
+            launches[0] += ds.last_launch_count()
             for k in res_fields:
                 host_res[c][k].copy_(o[k][:S], non_blocking=True)
             agg_host[c * ds.AGG_WORDS:(c + 1) * ds.AGG_WORDS].copy_(o["agg"], non_blocking=True)
@@ -627,6 +672,7 @@ def run_e2e(args, sp, p, dev, world):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    launches[0] = 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(comp_s)
@@ -643,7 +689,11 @@ def run_e2e(args, sp, p, dev, world):
     ms = float(t.item())
     return {"value": sp.num_scen * world * args.e2e_steps / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms / args.e2e_steps,
-            "chunks": len(host_chunks), "api": "paper_2304_13541_b200.dstack.eval_batch (dstack_eval_batch)"}
+            "chunks": len(host_chunks), "gpu_launches_per_step": launches[0] // max(args.e2e_steps, 1),
+            "transport": ("compact rows: nr = n | R << 12 (u16) + d (u32), 6 B/row, expanded on the device by "
+                          "dstack_unpack_nr inside the timed region") if packed else "wide rows: n u32 + r u16 + d u32",
+            "api": ("paper_2304_13541_b200.dstack.unpack_nr + eval_batch (dstack_unpack_nr, dstack_eval_batch)"
+                    if packed else "paper_2304_13541_b200.dstack.eval_batch (dstack_eval_batch)")}
 
 
 def run_sim(args, rank, world, local):

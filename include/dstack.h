@@ -278,6 +278,13 @@ int dstack_profile_stop(double *ms_out, int32_t *calls);
 /* Number of kernel launches the previous call on this thread enqueued (bench accounting). */
 int dstack_last_launch_count(void);
 
+/* Compact row transport (host -> device): a row whose n_i < 4096 and 1 <= R_i <= 15 travels as
+ * nr = n_i | R_i << 12 (u16) beside its d_i (u32), 6 bytes instead of 10; this call expands nr[0..num_rows) into
+ * the problem's n (u32) and r (u16) arrays on the device (pure data movement, results identical to copying the
+ * wide arrays).  All three pointers must be 16-byte aligned; the output arrays need the ABI's 16 bytes of slack.
+ * Rows outside that range must travel wide.  Used by the end-to-end path (bench.py e2e). */
+int dstack_unpack_nr(int64_t num_rows, const uint16_t *nr, uint32_t *n_out, uint16_t *r_out, void *stream);
+
 const char *dstack_status_str(int code);
 int dstack_version(void);
 

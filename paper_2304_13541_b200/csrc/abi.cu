@@ -135,6 +135,14 @@ int dstack_profile_stop(double *ms_out, int32_t *calls) {
 
 int dstack_version(void) { return 1; }
 
+int dstack_unpack_nr(int64_t num_rows, const uint16_t *nr, uint32_t *n_out, uint16_t *r_out, void *stream) {
+  g_launches = 0;
+  if (num_rows < 0 || (num_rows > 0 && (!nr || !n_out || !r_out))) return DSTACK_EINVAL;
+  if ((((uintptr_t)nr) | ((uintptr_t)n_out) | ((uintptr_t)r_out)) & 15u) return DSTACK_EINVAL;
+  if (!have_device()) return DSTACK_ELAUNCH;
+  return finish(launch_unpack_nr(num_rows, nr, n_out, r_out, (cudaStream_t)stream, &g_launches));
+}
+
 int dstack_last_launch_count(void) { return g_launches; }
 
 const char *dstack_status_str(int code) {

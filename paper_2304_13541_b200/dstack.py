@@ -94,6 +94,7 @@ def _load():
                                     P(CSimOut), C.c_void_p, C.c_size_t, C.c_void_p]
     lib.dstack_compare.argtypes = [P(CProblem), P(CParams)] + [C.c_void_p] * 7 + [C.c_size_t, C.c_void_p]
     lib.dstack_cluster.argtypes = [P(CProblem), P(CParams), C.c_int32] + [C.c_void_p] * 5 + [C.c_size_t, C.c_void_p]
+    lib.dstack_unpack_nr.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.dstack_profile_start.argtypes = [C.c_int32]
     lib.dstack_profile_stop.argtypes = [C.c_void_p, C.c_void_p]
     lib.dstack_status_str.restype = C.c_char_p
@@ -106,7 +107,7 @@ _lib = _load()
 # every symbol include/dstack.h declares (checked by tests/test_abi.py)
 EXPORTS = ("dstack_workspace_size", "dstack_knee", "dstack_knee_probe", "dstack_batch_opt", "dstack_wmaxmin", "dstack_schedule_cycle",
            "dstack_eval_batch", "dstack_aggregate", "dstack_sim_workspace_size", "dstack_simulate",
-           "dstack_compare", "dstack_cluster", "dstack_profile_start", "dstack_profile_stop",
+           "dstack_compare", "dstack_cluster", "dstack_unpack_nr", "dstack_profile_start", "dstack_profile_stop",
            "dstack_last_launch_count", "dstack_status_str", "dstack_version")
 
 
@@ -302,6 +303,22 @@ def eval_batch(dp: DeviceProblem, p, out=None, ws: Workspace | None = None, agg=
 
 CMP_NAMES = ("dstack", "maxmin", "maxthr", "temporal", "gslice")   # DSTACK_CMP_* order
 CLU_NAMES = ("exclusive", "temporal", "dstack", "dstack_ffd")         # DSTACK_CLU_* order
+
+
+def pack_nr(n, r):
+    """Host side of the compact row transport: nr = n | R << 12 (u16 torch tensor), or None when some row does not
+    fit (n >= 4096 or R outside 1..15) and the rows must travel wide.  n, r: int32 / int16 storage of the ABI's
+    u32 / u16 rows (CPU tensors)."""
+    nn = n.to(torch.int64) & 0xFFFFFFFF
+    rr = r.to(torch.int64) & 0xFFFF
+    if nn.numel() and (int(nn.max()) >= 4096 or int(rr.min()) < 1 or int(rr.max()) > 15):
+        return None
+    return (nn | (rr << 12)).to(torch.int32).to(torch.int16)
+
+
+def unpack_nr(nr, n_out, r_out, num_rows: int):
+    """dstack_unpack_nr: expand the compact rows on the device into the problem's n / r arrays."""
+    _check(_lib.dstack_unpack_nr(num_rows, _ptr(nr), _ptr(n_out), _ptr(r_out), _stream(nr.device)), "dstack_unpack_nr")
 
 
 def cluster(dp: DeviceProblem, p, gpus: int, demand, batch, out=None, ws: Workspace | None = None):

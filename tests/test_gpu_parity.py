@@ -480,3 +480,30 @@ def test_cluster_edges_and_config3_sample(ds):
     for k in ("u", "thr"):
         got = c[k][torch.as_tensor(idx, device=c[k].device)].cpu().numpy()
         assert np.array_equal(got, want[k]), k
+
+
+# ---------------------------------------------------------------- compact row transport ---
+
+def test_unpack_nr_round_trip_and_eval(ds):
+    """dstack_unpack_nr expands the compact rows (n | R << 12) into exactly the wide arrays, and the path evaluated
+    on the expanded rows equals the path on the original rows (config 2 sample, ragged row count)."""
+    sp, p = synth.config(2, num_scen=300, rows_pct=40)
+    g = synth.generate_device(sp, "cuda")
+    R = int(g["dnn_row_off"][-1].item())
+    nr = ds.pack_nr(g["n"][:R].cpu(), g["r"][:R].cpu())
+    assert nr is not None
+    nr_d = torch.zeros(R + 16, dtype=torch.int16, device="cuda")
+    nr_d[:R] = nr.cuda()
+    n2 = torch.full((R + 16,), -1, dtype=torch.int32, device="cuda")
+    r2 = torch.full((R + 16,), -1, dtype=torch.int16, device="cuda")
+    ds.unpack_nr(nr_d, n2, r2, R)
+    torch.cuda.synchronize()
+    assert torch.equal(n2[:R], g["n"][:R]) and torch.equal(r2[:R], g["r"][:R])
+    assert int((n2[R:] != -1).sum()) == 0 and int((r2[R:] != -1).sum()) == 0   # nothing written past the rows
+    o1 = ds.eval_batch(ds.from_device_dict(g), p)
+    g2 = dict(g, n=n2, r=r2)
+    o2 = ds.eval_batch(ds.from_device_dict(g2), p)
+    torch.cuda.synchronize()
+    for k in ("demand", "batch", "alloc_q16", "runs", "served", "u", "thr", "u_ideal"):
+        assert torch.equal(o1[k], o2[k]), k
+    assert ds.pack_nr(torch.tensor([4096], dtype=torch.int32), torch.tensor([1], dtype=torch.int16)) is None
