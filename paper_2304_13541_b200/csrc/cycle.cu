@@ -30,6 +30,9 @@ __global__ void __launch_bounds__(256) k_wmaxmin(int32_t num_scen, const int32_t
 #ifndef DSTACK_CYC_DYN
 #define DSTACK_CYC_DYN 1   // 1: k_cycle takes scenarios from a work counter (A/B switch)
 #endif
+#ifndef DSTACK_CYC_BK_MINB
+#define DSTACK_CYC_BK_MINB 4   // k_cycle<true> resident blocks per SM (A/B switch)
+#endif
 #ifndef DSTACK_CYC_BK_GRID
 #define DSTACK_CYC_BK_GRID 8   // k_cycle<true> (F1) grid: blocks per SM (A/B leg: 8 -> 49.5, 64 -> 53.0 ms)
 #endif
@@ -38,7 +41,7 @@ __global__ void __launch_bounds__(256) k_wmaxmin(int32_t num_scen, const int32_t
 #endif
 // BK: F1 below-knee fallback compiled in (DSTACK_FLAG_BELOW_KNEE); the default instantiation has no trace of it.
 template <bool BK>
-__global__ void __launch_bounds__(CYC_WARPS * 32, DSTACK_CYC_MINB) k_cycle(const __grid_constant__ CycArgs a) {
+__global__ void __launch_bounds__(CYC_WARPS * 32, BK ? DSTACK_CYC_BK_MINB : DSTACK_CYC_MINB) k_cycle(const __grid_constant__ CycArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   CycSmem &sm = reinterpret_cast<CycSmem *>(smem_raw)[warp];
@@ -173,9 +176,14 @@ int launch_cycle(const CycArgs &a, cudaStream_t s, int *launches) {
   if (blocks > cap) blocks = cap;
   if (a.p.flags & DSTACK_FLAG_BELOW_KNEE) {
     CycArgs b = a;
-    b.work_ctr = nullptr;
-    const int64_t bk_blocks = blocks < (int64_t)num_sms() * DSTACK_CYC_BK_GRID ? blocks : (int64_t)num_sms() * DSTACK_CYC_BK_GRID;
+    int64_t bk_blocks = blocks < (int64_t)num_sms() * DSTACK_CYC_BK_GRID ? blocks : (int64_t)num_sms() * DSTACK_CYC_BK_GRID;
     cudaFuncSetAttribute(k_cycle<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (DSTACK_CYC_DYN && b.work_ctr) {   // retries make F1 sessions very uneven: one resident wave pulling scenarios
+      if (cudaMemsetAsync(b.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
+      bk_blocks = resident_wave(k_cycle<true>, CYC_WARPS * 32, smem, blocks);
+    } else {
+      b.work_ctr = nullptr;
+    }
     k_cycle<true><<<(unsigned)bk_blocks, CYC_WARPS * 32, smem, s>>>(b);
   } else if (DSTACK_CYC_DYN && a.work_ctr) {
     // one resident wave (DSTACK_CYC_MINB blocks per SM) pulling scenarios from the work counter
