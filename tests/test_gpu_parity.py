@@ -507,3 +507,36 @@ def test_unpack_nr_round_trip_and_eval(ds):
     for k in ("demand", "batch", "alloc_q16", "runs", "served", "u", "thr", "u_ideal"):
         assert torch.equal(o1[k], o2[k]), k
     assert ds.pack_nr(torch.tensor([4096], dtype=torch.int32), torch.tensor([1], dtype=torch.int16)) is None
+
+
+def test_long_sessions_parity(ds):
+    """Sessions of 1001..4000 slots (SLOs x4: 100-400 ms): k_cycle's shared-memory decision mask (> 1024 slots), the
+    long-run occupancy paths and the ideal scheduler over longer horizons, against the oracle; with and without F1."""
+    sp, p = synth.config(2, num_scen=60, rows_pct=30)
+    pb = synth.generate_host(sp)
+    pb.slo_us[:] = pb.slo_us * 4
+    for q in (p, p.replace(below_knee=1), p.replace(L=148, ideal=0)):
+        g, _ = run_gpu(ds, pb, q)
+        want = oracle.evaluate(pb, q)
+        assert_parity(g, want, ideal=bool(q.ideal), where=f"long sessions {q}")
+        assert (want["T_us"] // q.slot_us > 1024).any()
+
+
+def test_long_sessions_compare_cluster_simulate(ds):
+    """The other session users (O9 compare, F4 cluster, a7 simulate) on sessions of more than 1024 slots."""
+    sp, p = synth.config(2, num_scen=40, rows_pct=30)
+    pb = synth.generate_host(sp)
+    pb.slo_us[:] = pb.slo_us * 4
+    g, _ = run_compare(ds, pb, p)
+    assert_compare_parity(g, oracle.compare(pb, p), where="long compare")
+    gc = run_cluster(ds, pb, p, 3)
+    wc = oracle.cluster(pb, p, 3)
+    assert np.array_equal(gc["u"], wc["u"]) and np.array_equal(gc["thr"], wc["thr"])
+    sp5, p5 = synth.config(5, num_scen=40, rows_pct=30)
+    pb5 = synth.generate_host(sp5)
+    pb5.slo_us[:] = pb5.slo_us * 4
+    r = ds.simulate(ds.from_host(pb5, "cuda"), p5, 6, sp5.seed, sp5.cfg_tag)
+    torch.cuda.synchronize()
+    want = oracle.simulate(pb5, p5, 6, sp5.seed, sp5.cfg_tag)
+    for k in want:
+        assert np.array_equal(r[k].cpu().numpy().astype(np.int64), want[k].astype(np.int64)), k
