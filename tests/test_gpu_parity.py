@@ -540,3 +540,31 @@ def test_long_sessions_compare_cluster_simulate(ds):
     want = oracle.simulate(pb5, p5, 6, sp5.seed, sp5.cfg_tag)
     for k in want:
         assert np.array_equal(r[k].cpu().numpy().astype(np.int64), want[k].astype(np.int64)), k
+
+
+def test_wide_scenarios_parity(ds):
+    """Scenarios of 17..32 DNNs (every lane of the warp-per-scenario kernels holds a DNN): eval with the ideal
+    scheduler, F1, O9 compare and F4 cluster against the oracle."""
+    sp, p = synth.config(2, num_scen=40, rows_pct=15)
+    sp = sp.replace(ndnn_min=17, ndnn_max=32)
+    pb = synth.generate_host(sp)
+    assert pb.num_dnn > 40 * 20
+    for q in (p, p.replace(below_knee=1, ideal=0), p.replace(L=148, S_tot=148)):
+        g, _ = run_gpu(ds, pb, q)
+        assert_parity(g, oracle.evaluate(pb, q), ideal=bool(q.ideal), where=f"wide scenarios {q}")
+    gcmp, _ = run_compare(ds, pb, p)
+    assert_compare_parity(gcmp, oracle.compare(pb, p), where="wide compare")
+    gc = run_cluster(ds, pb, p, 8)
+    wc = oracle.cluster(pb, p, 8)
+    assert np.array_equal(gc["u"], wc["u"]) and np.array_equal(gc["thr"], wc["thr"])
+    sp5, p5 = synth.config(5, num_scen=30, rows_pct=15)
+    sp5 = sp5.replace(ndnn_min=17, ndnn_max=32)
+    pb5 = synth.generate_host(sp5)
+    r = ds.simulate(ds.from_host(pb5, "cuda"), p5, 8, sp5.seed, sp5.cfg_tag)
+    torch.cuda.synchronize()
+    want = oracle.simulate(pb5, p5, 8, sp5.seed, sp5.cfg_tag)
+    for k in want:
+        assert np.array_equal(r[k].cpu().numpy().astype(np.int64), want[k].astype(np.int64)), k
+    k, pr, st = ds.knee_probe(ds.from_host(pb, "cuda"), p, 2)
+    ko, pro, sto = oracle.knee_probe(pb, p, 2)
+    assert np.array_equal(k.cpu().numpy().view(np.uint16), ko) and np.array_equal(pr.cpu().numpy(), pro)
