@@ -568,3 +568,21 @@ def test_wide_scenarios_parity(ds):
     k, pr, st = ds.knee_probe(ds.from_host(pb, "cuda"), p, 2)
     ko, pro, sto = oracle.knee_probe(pb, p, 2)
     assert np.array_equal(k.cpu().numpy().view(np.uint16), ko) and np.array_equal(pr.cpu().numpy(), pro)
+
+
+def test_empty_problem_calls(ds):
+    """Zero scenarios / zero DNNs: every entry point returns OK without touching outputs."""
+    pb = synth.make_problem([0], [0], [], [], [], [], [], [], [], [], [])
+    dp = ds.from_host(pb, "cuda")
+    for q in (Params(L=100, S_tot=148, ideal=1), Params(L=148, S_tot=148, below_knee=1)):
+        o = ds.eval_batch(dp, q)
+        torch.cuda.synchronize()
+        agg = ds.agg_to_dict(o["agg"])
+        assert agg["n_scen"] == 0 and agg["n_dnn"] == 0
+    p = Params(L=100, S_tot=148)
+    ds.knee(dp, p, 1); ds.knee_probe(dp, p, 1); ds.batch_opt(dp, p)
+    ds.compare(dp, p, torch.zeros(1, dtype=torch.int16, device="cuda"), torch.zeros(1, dtype=torch.uint8, device="cuda"),
+               torch.zeros(1, dtype=torch.int32, device="cuda"))
+    ds.cluster(dp, p, 4, torch.zeros(1, dtype=torch.int16, device="cuda"), torch.zeros(1, dtype=torch.uint8, device="cuda"))
+    ds.simulate(dp, p, 3, 1, 5)
+    torch.cuda.synchronize()
