@@ -341,9 +341,9 @@ def run_native(args, rank, world, local):
     # ---- e2e: the public API from pinned host buffers, H2D + compute + D2H of results each step ----
     e2e = e2e_wide = None
     if not args.no_e2e:
-        e2e = run_e2e(args, sp, p, dev, world, packed=True)
+        e2e = run_e2e(args, sp, p, dev, world, "w5")
         if world == 1 and e2e.get("transport", "").startswith("compact"):
-            e2e_wide = run_e2e(args, sp, p, dev, world, packed=False)   # the same path with the rows sent wide
+            e2e_wide = run_e2e(args, sp, p, dev, world, "wide")   # the same path with the rows sent wide
 
     if rank != 0:
         if world > 1:
@@ -543,17 +543,16 @@ def run_knee_probe_leg(args, ds, dp, p, stream, world):
             "max_steps": int(pr.max().item()) if dp.num_dnn else 0}
 
 
-def run_e2e(args, sp, p, dev, world, packed=True):
+def run_e2e(args, sp, p, dev, world, mode="w5"):
     """End-to-end through the public API: per step, every chunk's inputs are copied host->device from
     pinned memory (copy stream, double-buffered), evaluated with dstack_eval_batch, and its per-scenario
     results copied back device->host.  Device-timed with CUDA events (max over ranks).
-    packed: the rows travel in the compact transport (nr = n | R << 12 as u16 beside d as u32, 6 B/row instead of
-    10; dstack_unpack_nr expands them on the device inside the timed region) when every row fits it."""
+    mode: how the rows travel -- "w5" 5 B/row (dstack_unpack_w5), "nr" 6 B/row (dstack_unpack_nr), "wide" 10 B/row;
+    the compact modes expand the rows on the device inside the timed region and fall back to the next wider mode
+    when some row does not fit them."""
     import torch
-    import torch.distributed as dist
 
     import synth
-    from paper_2304_13541_b200 import dstack as ds
 
     nch = max(1, args.e2e_chunks)
     per = (sp.num_scen + nch - 1) // nch
@@ -567,34 +566,46 @@ def run_e2e(args, sp, p, dev, world, packed=True):
             if cnt <= 0:
                 break
             g = synth.generate_device(sp.replace(scen_base=sp.scen_base + s0, num_scen=cnt), dev)
-            fields = hdr_fields + ("d",)
-            if packed:
-                R = int(g["dnn_row_off"][-1].item())
-                nn = g["n"][:R].to(torch.int64) & 0xFFFFFFFF
-                rr = g["r"][:R].to(torch.int64) & 0xFFFF
-                if R and (int(nn.max()) >= 4096 or int(rr.min()) < 1 or int(rr.max()) > 15):
-                    packed = False
-                else:
-                    nr = torch.zeros(g["r"].numel(), dtype=torch.int16, device=dev)
-                    nr[:R] = (nn | (rr << 12)).to(torch.int32).to(torch.int16)
-                    g["nr"] = nr
-                del nn, rr
-            fields += ("nr",) if packed else ("n", "r")
+            R = int(g["dnn_row_off"][-1].item())
+            nn = g["n"][:R].to(torch.int64) & 0xFFFFFFFF
+            rr = g["r"][:R].to(torch.int64) & 0xFFFF
+            dd = g["d"][:R].to(torch.int64) & 0xFFFFFFFF
+            nmax, rmin, rmax, dmax = (int(nn.max()), int(rr.min()), int(rr.max()), int(dd.max())) if R else (0, 1, 1, 0)
+            fits = {"w5": nmax < 4096 and rmin >= 1 and rmax <= 4 and dmax < (1 << 26),
+                    "nr": nmax < 4096 and rmin >= 1 and rmax <= 15, "wide": True}
+            if not fits[mode]:
+                del g, nn, rr, dd
+                host_chunks.clear()
+                return run_e2e(args, sp, p, dev, world, "nr" if mode == "w5" else "wide")
+            fields = hdr_fields
+            if mode == "w5":
+                pad = g["d"].numel()
+                w = torch.zeros(pad, dtype=torch.int64, device=dev)
+                w[:R] = dd | ((rr - 1) << 26) | ((nn >> 8) << 28)
+                g["w"] = w.to(torch.int32)   # low 32 bits (two's-complement storage of the u32 word)
+                lo = torch.zeros(pad, dtype=torch.uint8, device=dev)
+                lo[:R] = (nn & 255).to(torch.uint8)
+                g["lo"] = lo
+                del w
+                fields += ("w", "lo")
+            elif mode == "nr":
+                nr = torch.zeros(g["r"].numel(), dtype=torch.int16, device=dev)
+                nr[:R] = (nn | (rr << 12)).to(torch.int32).to(torch.int16)
+                g["nr"] = nr
+                fields += ("nr", "d")
+            else:
+                fields += ("n", "r", "d")
+            del nn, rr, dd
             # straight into pinned host buffers (no pageable intermediate: 8 ranks x several GB of rows on one host)
             host_chunks.append({k: torch.empty(g[k].shape, dtype=g[k].dtype, pin_memory=True).copy_(g[k])
                                 for k in fields})
             del g
     except RuntimeError as e:
         return {"value": None, "unit": UNIT, "error": f"pinned host staging failed: {e}"[:200]}
-    if not packed:   # some chunk could not be packed: every chunk travels wide (re-stage the packed ones)
-        if any("nr" in hc for hc in host_chunks):
-            host_chunks.clear()
-            return run_e2e(args, sp, p, dev, world, packed=False)
-        return _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, False)
-    return _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, True)
+    return _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, mode)
 
 
-def _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, packed):
+def _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, mode):
     import torch
     import torch.distributed as dist
 
@@ -604,15 +615,18 @@ def _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, packed):
     copy_s = torch.cuda.Stream(dev)
     comp_s = torch.cuda.current_stream(dev)
     tfields = tuple(host_chunks[0].keys())   # the transported fields
-    maxrows = max(hc["d"].numel() for hc in host_chunks)
+    rowkey = "w" if mode == "w5" else "d"
+    maxrows = max(hc[rowkey].numel() for hc in host_chunks)
 
     # two device buffer sets, every field sized for the largest chunk of that field (+ the unpacked rows)
     def dev_max():
         b = {k: torch.empty(max(hc[k].numel() for hc in host_chunks), dtype=host_chunks[0][k].dtype, device=dev)
              for k in tfields}
-        if packed:
+        if mode != "wide":
             b["n"] = torch.empty(maxrows + 16, dtype=torch.int32, device=dev)
             b["r"] = torch.empty(maxrows + 16, dtype=torch.int16, device=dev)
+        if mode == "w5":
+            b["d"] = torch.empty(maxrows + 16, dtype=torch.int32, device=dev)
         return b
     bufs = [dev_max(), dev_max()]
     res_fields = ("scen_status", "u_static", "u", "thr", "misses")
@@ -656,7 +670,10 @@ def _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, packed):
             S = hc["scen_dnn_off"].numel() - 1
             D = hc["dnn_row_off"].numel() - 1
             R = int(hc["dnn_row_off"][-1])
-            if packed:
+            if mode == "w5":
+                ds.unpack_w5(b["w"], b["lo"], b["n"], b["r"], b["d"], R)
+                launches[0] += ds.last_launch_count()
+            elif mode == "nr":
                 ds.unpack_nr(b["nr"], b["n"], b["r"], R)
                 launches[0] += ds.last_launch_count()
             dpc = ds.DeviceProblem(S, D, R, *[b[k] for k in prob_fields])
@@ -690,10 +707,14 @@ def _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, packed):
     return {"value": sp.num_scen * world * args.e2e_steps / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms / args.e2e_steps,
             "chunks": len(host_chunks), "gpu_launches_per_step": launches[0] // max(args.e2e_steps, 1),
-            "transport": ("compact rows: nr = n | R << 12 (u16) + d (u32), 6 B/row, expanded on the device by "
-                          "dstack_unpack_nr inside the timed region") if packed else "wide rows: n u32 + r u16 + d u32",
-            "api": ("paper_2304_13541_b200.dstack.unpack_nr + eval_batch (dstack_unpack_nr, dstack_eval_batch)"
-                    if packed else "paper_2304_13541_b200.dstack.eval_batch (dstack_eval_batch)")}
+            "transport": {"w5": "compact rows: w = d | (R-1) << 26 | (n >> 8) << 28 (u32) + n & 255 (u8), 5 B/row, "
+                                "expanded on the device by dstack_unpack_w5 inside the timed region",
+                          "nr": "compact rows: nr = n | R << 12 (u16) + d (u32), 6 B/row, expanded on the device by "
+                                "dstack_unpack_nr inside the timed region",
+                          "wide": "wide rows: n u32 + r u16 + d u32"}[mode],
+            "api": {"w5": "paper_2304_13541_b200.dstack.unpack_w5 + eval_batch (dstack_unpack_w5, dstack_eval_batch)",
+                    "nr": "paper_2304_13541_b200.dstack.unpack_nr + eval_batch (dstack_unpack_nr, dstack_eval_batch)",
+                    "wide": "paper_2304_13541_b200.dstack.eval_batch (dstack_eval_batch)"}[mode]}
 
 
 def run_sim(args, rank, world, local):

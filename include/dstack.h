@@ -284,6 +284,11 @@ int dstack_last_launch_count(void);
  * wide arrays).  All three pointers must be 16-byte aligned; the output arrays need the ABI's 16 bytes of slack.
  * Rows outside that range must travel wide.  Used by the end-to-end path (bench.py e2e). */
 int dstack_unpack_nr(int64_t num_rows, const uint16_t *nr, uint32_t *n_out, uint16_t *r_out, void *stream);
+/* 5-byte variant of the compact transport for rows with n_i < 4096, 1 <= R_i <= 4 and d_i < 2^26:
+ * w = d_i | (R_i - 1) << 26 | (n_i >> 8) << 28 (u32) and lo = n_i & 255 (u8); expands into n, r and d.  w, n_out,
+ * d_out 16-byte aligned, lo 4-byte, r_out 8-byte aligned; outputs need the ABI's 16 bytes of slack. */
+int dstack_unpack_w5(int64_t num_rows, const uint32_t *w, const uint8_t *lo, uint32_t *n_out, uint16_t *r_out,
+                     uint32_t *d_out, void *stream);
 
 const char *dstack_status_str(int code);
 int dstack_version(void);

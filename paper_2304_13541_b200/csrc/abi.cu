@@ -135,6 +135,16 @@ int dstack_profile_stop(double *ms_out, int32_t *calls) {
 
 int dstack_version(void) { return 1; }
 
+int dstack_unpack_w5(int64_t num_rows, const uint32_t *w, const uint8_t *lo, uint32_t *n_out, uint16_t *r_out,
+                     uint32_t *d_out, void *stream) {
+  g_launches = 0;
+  if (num_rows < 0 || (num_rows > 0 && (!w || !lo || !n_out || !r_out || !d_out))) return DSTACK_EINVAL;
+  if ((((uintptr_t)w) | ((uintptr_t)n_out) | ((uintptr_t)d_out)) & 15u) return DSTACK_EINVAL;
+  if ((((uintptr_t)lo) & 3u) || (((uintptr_t)r_out) & 7u)) return DSTACK_EINVAL;
+  if (!have_device()) return DSTACK_ELAUNCH;
+  return finish(launch_unpack_w5(num_rows, w, lo, n_out, r_out, d_out, (cudaStream_t)stream, &g_launches));
+}
+
 int dstack_unpack_nr(int64_t num_rows, const uint16_t *nr, uint32_t *n_out, uint16_t *r_out, void *stream) {
   g_launches = 0;
   if (num_rows < 0 || (num_rows > 0 && (!nr || !n_out || !r_out))) return DSTACK_EINVAL;

@@ -121,6 +121,8 @@ size_t sim_fill_log_bytes();
 int launch_agg(const AggArgs &a, cudaStream_t s, int *launches);
 int launch_compare(const CmpArgs &a, cudaStream_t s, int *launches);
 int launch_unpack_nr(int64_t num_rows, const uint16_t *nr, uint32_t *n, uint16_t *r, cudaStream_t s, int *launches);
+int launch_unpack_w5(int64_t num_rows, const uint32_t *w, const uint8_t *lo, uint32_t *n, uint16_t *r, uint32_t *d,
+                     cudaStream_t s, int *launches);
 int launch_cluster(const dstack_problem_t &pb, const dstack_params_t &p, int32_t G, const uint16_t *demand,
                    const uint8_t *batch, uint16_t *dtab_rows, double *u, double *thr, uint32_t *work_ctr, cudaStream_t s,
                    int *launches);

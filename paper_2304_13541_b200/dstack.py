@@ -95,6 +95,7 @@ def _load():
     lib.dstack_compare.argtypes = [P(CProblem), P(CParams)] + [C.c_void_p] * 7 + [C.c_size_t, C.c_void_p]
     lib.dstack_cluster.argtypes = [P(CProblem), P(CParams), C.c_int32] + [C.c_void_p] * 5 + [C.c_size_t, C.c_void_p]
     lib.dstack_unpack_nr.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.dstack_unpack_w5.argtypes = [C.c_int64] + [C.c_void_p] * 6
     lib.dstack_profile_start.argtypes = [C.c_int32]
     lib.dstack_profile_stop.argtypes = [C.c_void_p, C.c_void_p]
     lib.dstack_status_str.restype = C.c_char_p
@@ -107,7 +108,7 @@ _lib = _load()
 # every symbol include/dstack.h declares (checked by tests/test_abi.py)
 EXPORTS = ("dstack_workspace_size", "dstack_knee", "dstack_knee_probe", "dstack_batch_opt", "dstack_wmaxmin", "dstack_schedule_cycle",
            "dstack_eval_batch", "dstack_aggregate", "dstack_sim_workspace_size", "dstack_simulate",
-           "dstack_compare", "dstack_cluster", "dstack_unpack_nr", "dstack_profile_start", "dstack_profile_stop",
+           "dstack_compare", "dstack_cluster", "dstack_unpack_nr", "dstack_unpack_w5", "dstack_profile_start", "dstack_profile_stop",
            "dstack_last_launch_count", "dstack_status_str", "dstack_version")
 
 
@@ -319,6 +320,12 @@ def pack_nr(n, r):
 def unpack_nr(nr, n_out, r_out, num_rows: int):
     """dstack_unpack_nr: expand the compact rows on the device into the problem's n / r arrays."""
     _check(_lib.dstack_unpack_nr(num_rows, _ptr(nr), _ptr(n_out), _ptr(r_out), _stream(nr.device)), "dstack_unpack_nr")
+
+
+def unpack_w5(w, lo, n_out, r_out, d_out, num_rows: int):
+    """dstack_unpack_w5: expand 5-byte rows (w = d | (R - 1) << 26 | (n >> 8) << 28, lo = n & 255) on the device."""
+    _check(_lib.dstack_unpack_w5(num_rows, _ptr(w), _ptr(lo), _ptr(n_out), _ptr(r_out), _ptr(d_out), _stream(w.device)),
+           "dstack_unpack_w5")
 
 
 def cluster(dp: DeviceProblem, p, gpus: int, demand, batch, out=None, ws: Workspace | None = None):

@@ -586,3 +586,26 @@ def test_empty_problem_calls(ds):
     ds.cluster(dp, p, 4, torch.zeros(1, dtype=torch.int16, device="cuda"), torch.zeros(1, dtype=torch.uint8, device="cuda"))
     ds.simulate(dp, p, 3, 1, 5)
     torch.cuda.synchronize()
+
+
+def test_unpack_w5_round_trip(ds):
+    """dstack_unpack_w5 (5-byte rows) expands exactly into the wide n / r / d arrays (ragged row count)."""
+    sp, p = synth.config(3, num_scen=200, rows_pct=40)
+    g = synth.generate_device(sp, "cuda")
+    R = int(g["dnn_row_off"][-1].item())
+    nn = g["n"][:R].to(torch.int64) & 0xFFFFFFFF
+    rr = g["r"][:R].to(torch.int64) & 0xFFFF
+    dd = g["d"][:R].to(torch.int64) & 0xFFFFFFFF
+    assert int(nn.max()) < 4096 and int(rr.max()) <= 4 and int(dd.max()) < (1 << 26)
+    w = torch.zeros(R + 16, dtype=torch.int64, device="cuda")
+    w[:R] = dd | ((rr - 1) << 26) | ((nn >> 8) << 28)
+    w = w.to(torch.int32)
+    lo = torch.zeros(R + 16, dtype=torch.uint8, device="cuda")
+    lo[:R] = (nn & 255).to(torch.uint8)
+    n2 = torch.full((R + 16,), -1, dtype=torch.int32, device="cuda")
+    r2 = torch.full((R + 16,), -1, dtype=torch.int16, device="cuda")
+    d2 = torch.full((R + 16,), -1, dtype=torch.int32, device="cuda")
+    ds.unpack_w5(w, lo, n2, r2, d2, R)
+    torch.cuda.synchronize()
+    assert torch.equal(n2[:R], g["n"][:R]) and torch.equal(r2[:R], g["r"][:R]) and torch.equal(d2[:R], g["d"][:R])
+    assert int((n2[R:] != -1).sum()) == 0 and int((r2[R:] != -1).sum()) == 0 and int((d2[R:] != -1).sum()) == 0
