@@ -28,9 +28,6 @@ static __device__ unsigned long long g_cstats[16];   // per TU (instrumentation 
 #define CSTAT(i, v) ((void)0)
 #endif
 
-#ifndef DSTACK_CYC_MICRO
-#define DSTACK_CYC_MICRO 1   // 0: decision bits set under a lane branch, occ[t] by shuffle (A/B switch)
-#endif
 
 constexpr uint16_t NONE16 = 0xFFFF;
 constexpr uint32_t NONE32 = 0xFFFFFFFFu;
@@ -262,11 +259,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     for (int w = lane; w < DSTACK_MAX_SLOTS / 32; w += 32) sm.dmask[w] = 0;
   __syncwarp();
   auto dset = [&](int e) {   // warp-uniform e < nslots
-#if DSTACK_CYC_MICRO
     if (dreg) dmw |= (uint32_t)(lane == (e >> 5)) << (e & 31);
-#else
-    if (dreg) { if (lane == (e >> 5)) dmw |= 1u << (e & 31); }
-#endif
     else if (lane == 0) sm.dmask[e >> 5] |= 1u << (e & 31);
   };
   uint32_t joff = rep;   // exclusive prefix of rep over lanes
@@ -378,11 +371,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     const int bt = t & ~3, mybase = bt + 4 * lane, wi = (t >> 2) + lane;
     uint32_t wv = wi < DSTACK_MAX_SLOTS / 4 ? w32[wi] : 0u;
     const uint32_t lo_mask = lane == 0 ? (0xFFFFFFFFu << (8 * (t & 3))) : 0xFFFFFFFFu;
-#if DSTACK_CYC_MICRO
     int occ_t = (int)sm.occ[t];   // broadcast byte load
-#else
-    int occ_t = (int)((__shfl_sync(FULL, wv, 0) >> (8 * (t & 3))) & 0xFFu);
-#endif
     bool elig = false;
     int ns = nslots;
     if (active) {   // eligible: not running at t (static or last fill run), fits at t

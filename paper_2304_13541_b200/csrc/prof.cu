@@ -29,15 +29,6 @@ __host__ __device__ inline size_t prof_warp_bytes(int S_tot) {
 #ifndef DSTACK_PROF_ROWS_U
 #define DSTACK_PROF_ROWS_U 6   // rows per lane in flight in the row pass (A/B at config 3: 2 -> 10.86, 4 -> 11.41, 6 -> 10.44, 8 -> 10.71 ms)
 #endif
-#ifndef DSTACK_PROF_VEC
-#define DSTACK_PROF_VEC 0   // 1: 16-byte vector row loads in k_prof_fast (A/B at config 3: 12.9 vs 12.3 ms scalar)
-#endif
-#ifndef DSTACK_FAST_CERT_PASS
-#define DSTACK_FAST_CERT_PASS 1   // 0: batch certificate inside the width pass (every lane's CB widths; A/B switch)
-#endif
-#ifndef DSTACK_FAST_KNEE_FIRST
-#define DSTACK_FAST_KNEE_FIRST 1   // 0: track the feasible argmax beside the knee in the width pass (A/B switch)
-#endif
 #ifndef DSTACK_PROF_FAST
 #define DSTACK_PROF_FAST 1   // 0: every launch takes the generic kernel (A/B switch)
 #endif
@@ -241,45 +232,9 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
   //      width histogram of R over n <= S_tot (smem) ----
   uint32_t Rmin = 0xFFFFFFFFu;
   uint64_t Wb = 0;
-#if DSTACK_PROF_VEC
-  // 16-byte vector loads: lane v covers rows [base + 4v, base + 4v + 4) of n, d (uint4) and r (uint2), base = r0
-  // rounded down to a multiple of 4 (the arrays are 256-byte aligned, so 4-row groups are 16-byte aligned; rows
-  // outside [r0, r0 + K) are masked; reads stay within the ABI's 16 bytes of slack).  Two vectors per lane in
-  // flight: a DNN of <= 253 rows is one round trip.
-  {
-    const int64_t base = r0 & ~(int64_t)3;
-    const int32_t lo = (int32_t)(r0 - base), hi = lo + K;   // valid rows, relative to base
-    const int nvec = (hi + 3) >> 2;
-    auto row = [&](uint32_t nn, uint32_t R, uint32_t dd) {
-      RT += R; D += (uint64_t)R * dd; Rmin = min(Rmin, R);
-      if (nn <= (uint32_t)S_tot) atomicAdd(&hist[nn], R); else Wb += (uint64_t)R * nn;
-    };
-    auto vec = [&](int v, const uint4 &nv, const uint4 &dv, const uint2 &rv) {
-      const int e0 = 4 * v;
-      const uint32_t nn[4] = {nv.x, nv.y, nv.z, nv.w}, dd[4] = {dv.x, dv.y, dv.z, dv.w};
-      const uint32_t RR[4] = {rv.x & 0xFFFFu, rv.x >> 16, rv.y & 0xFFFFu, rv.y >> 16};
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (e0 + e >= lo && e0 + e < hi) row(nn[e], RR[e], dd[e]);
-    };
-    const uint4 *n4 = reinterpret_cast<const uint4 *>(pb.n + base);
-    const uint4 *d4 = reinterpret_cast<const uint4 *>(pb.d + base);
-    const uint2 *r2 = reinterpret_cast<const uint2 *>(pb.r + base);
-    for (int v0 = 0; v0 < nvec; v0 += 64) {
-      const int va = v0 + lane, vb = va + 32;
-      uint4 na = make_uint4(0, 0, 0, 0), da = na, nb = na, db = na;
-      uint2 ra = make_uint2(0, 0), rb = ra;
-      if (va < nvec) { na = __ldg(n4 + va); da = __ldg(d4 + va); ra = __ldg(r2 + va); }
-      if (vb < nvec) { nb = __ldg(n4 + vb); db = __ldg(d4 + vb); rb = __ldg(r2 + vb); }
-      if (va < nvec) vec(va, na, da, ra);
-      if (vb < nvec) vec(vb, nb, db, rb);
-    }
-  }
-#else
   const uint32_t *n = pb.n + r0;
   const uint16_t *r = pb.r + r0;
   const uint32_t *d = pb.d + r0;
-#if DSTACK_PROF_ROWS_U > 2
   // DSTACK_PROF_ROWS_U rows per lane in flight per iteration
   for (int i0 = lane; i0 < K; i0 += 32 * DSTACK_PROF_ROWS_U) {
     uint32_t nn[DSTACK_PROF_ROWS_U], dd[DSTACK_PROF_ROWS_U], RR[DSTACK_PROF_ROWS_U];
@@ -297,22 +252,6 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
       }
     }
   }
-#else
-  for (int i0 = lane; i0 < K; i0 += 64) {
-    const int i1 = i0 + 32;
-    const bool h1 = i1 < K;
-    const uint32_t n0 = __ldg(n + i0), d0 = __ldg(d + i0), R0 = __ldg(r + i0);
-    uint32_t n1 = 0, d1 = 0, R1 = 0;
-    if (h1) { n1 = __ldg(n + i1); d1 = __ldg(d + i1); R1 = __ldg(r + i1); }
-    RT += R0; D += (uint64_t)R0 * d0; Rmin = min(Rmin, R0);
-    if (n0 <= (uint32_t)S_tot) atomicAdd(&hist[n0], R0); else Wb += (uint64_t)R0 * n0;
-    if (h1) {
-      RT += R1; D += (uint64_t)R1 * d1; Rmin = min(Rmin, R1);
-      if (n1 <= (uint32_t)S_tot) atomicAdd(&hist[n1], R1); else Wb += (uint64_t)R1 * n1;
-    }
-  }
-#endif
-#endif
   RT = __reduce_add_sync(FULL, RT);
   Rmin = __reduce_min_sync(FULL, Rmin);
   uint32_t Dtop, Wtop;
@@ -364,9 +303,6 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
   const int mh = S_tot >> 1;
   uint64_t *scr = cA;
   Top2 tk = {0.f, 0.f, 0u};
-#if !DSTACK_FAST_KNEE_FIRST
-  Top2 te = {0.f, 0.f, 0u};
-#endif
   float G = 0.f;
   {
     // overflow: X(L, b_hi) = b_hi t_np RT S_tot M + M t_p (S_tot PA[mb] + b_hi Q[mb]) + mem is the grid maximum;
@@ -390,31 +326,14 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
     const float f = score_f(S, X);
     const bool valid = (vmask >> i) & 1u;
     top2_add(tk, valid ? f : 0.f, S);
-#if !DSTACK_FAST_KNEE_FIRST
-    top2_add(te, valid && 2 * X <= (uint64_t)S * F ? f : 0.f, S);   // Eqs. 11-12
-#endif
     // Batch certificate: for b >= 2 and s = S/b in segment m = floor(s),
     // X(S, b) >= b (alpha s + beta), alpha = 2 C1 + Mtp PA[m], beta = Mtp Q[m] + mem, hence
     // eta(S, b) <= s / (alpha s + beta)^2; G = max over m <= S_tot/2 of its supremum on [m, m+1).
-#if DSTACK_FAST_CERT_PASS
     if ((int)S <= mh) cU[S] = ((uint64_t)q << 32) | ra;   // (PA[m], Q[m] - W>) for the certificate pass below
-#else
-    if ((int)S <= mh) {
-      const float af = fmaf(Mtpf, (float)ra, C1f2), bf = fmaf(Mtpf, (float)q + Wbf, membf);
-      // the curve is unimodal with its peak at s = beta / alpha: evaluate it at that point clamped to [lo, hi]
-      // (an approximate interior maximiser only lowers the value by O(2^-44) relative, far inside the margin)
-      const float lo = (float)S, hi = fminf(lo + 1.f, half);
-      const float sx = fminf(fmaxf(bf * rcp_approx(af), lo), hi);
-      const float x = fmaf(af, sx, bf);
-      const float v = bf == 0.f ? __int_as_float(0x7f800000) : sx * rcp_approx(x * x);   // unbounded at s -> 0
-      G = fmaxf(G, v);
-    }
-#endif
   }
   __syncwarp();
   uint32_t Sk = 0, Se = 0;
   uint64_t Xe = 0;
-#if DSTACK_FAST_KNEE_FIRST
   {
     // knee = the exact argmax over every attained width (ties -> smaller S); when that width is feasible
     // (Eqs. 11-12: 2X <= S F) it is also the exact argmax over the feasible widths (a subset containing it),
@@ -424,20 +343,10 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
     if (F != 0 && 2 * r.X <= (uint64_t)r.S * F) { Se = r.S; Xe = r.X; }
     else { const SX e = feasible_argmax(scr, lmin, S_tot, F == 0 ? 1ull : F, lane); Se = e.S; Xe = e.X; }
   }
-#else
-#pragma unroll 1
-  for (int w = 0; w < 2; ++w) {   // w = 0: knee (all attained widths), w = 1: feasible argmax
-    Top2 t;
-    t.t1 = w ? te.t1 : tk.t1; t.t2 = w ? te.t2 : tk.t2; t.s1 = w ? te.s1 : tk.s1;
-    const SX r = fast_argmax(t, scr, lmin, S_tot, w ? (F == 0 ? 1ull : F) : 0ull, lane);
-    if (w) { Se = r.S; Xe = r.X; } else Sk = r.S;
-  }
-#endif
   if (Se == 0) { st = DSTACK_ST_INFEASIBLE; return true; }   // b = 1 is feasible whenever any b is (O3)
   // b* = 1 is certified when the incumbent beats G with a 2^-12 margin (f32 rounding of both sides is
   // < 2^-19); otherwise the generic exact branch-and-bound decides this DNN.
   if (b_hi >= 2) {
-#if DSTACK_FAST_CERT_PASS
     // lanes over the segments m = 0 .. S_tot/2 (instead of every lane's CB widths): the same bound per m
     for (int m = lane; m <= mh; m += 32) {
       const uint64_t pv = cU[m];
@@ -449,7 +358,6 @@ __device__ __forceinline__ bool fast_dnn(const ProfArgs &a, int64_t k, int64_t r
       const float v = bf == 0.f ? __int_as_float(0x7f800000) : sx * rcp_approx(x * x);
       G = fmaxf(G, v);
     }
-#endif
     const float Gw = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(G)));
     if (!(score_f(Se, Xe) * 0.99975586f > Gw)) return false;
   }
