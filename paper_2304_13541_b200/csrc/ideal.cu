@@ -226,11 +226,19 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
             if (bvalid_lane && sB[lo] <= (uint32_t)L) atomicOr(&mb_bits[sB[lo] >> 5], 1u << (sB[lo] & 31));
           }
           __syncwarp();
-          // highest achievable B sum in the words below w (the empty B subset makes sum 0 always achievable)
-          if (lane < 8) {
-            int h = -1;
-            for (int w = 0; w < lane; ++w) if (mb_bits[w]) h = 32 * w + 31 - __clz(mb_bits[w]);
-            mb_below[lane] = h;
+          // highest achievable B sum in the words below w (the empty B subset makes sum 0 always achievable):
+          // an exclusive max-scan over the 8 words' highest set bits (lanes 0..7)
+          {
+            const uint32_t wd = lane < 8 ? mb_bits[lane] : 0u;
+            int h = wd ? 32 * lane + 31 - __clz(wd) : -1;
+            int ex = __shfl_up_sync(FULL, h, 1);
+            if (lane == 0) ex = -1;
+#pragma unroll
+            for (int dd = 1; dd < 8; dd <<= 1) {
+              const int o = __shfl_up_sync(FULL, ex, dd);
+              if (lane >= dd) ex = max(ex, o);
+            }
+            if (lane < 8) mb_below[lane] = ex;
           }
           __syncwarp();
           uint32_t bestA = 0;
