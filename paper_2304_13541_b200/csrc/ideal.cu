@@ -75,6 +75,16 @@ struct IdealRow {
   uint32_t R, tau, g;
 };
 
+// row i as stored (no skipping): the prefetch of a chain's next row, whose loads are only consumed at the next
+// advance, so their latency overlaps the events in between
+__device__ __forceinline__ IdealRow ideal_row_raw(const IdealArgs &a, int64_t i, int64_t r1) {
+  IdealRow w;
+  w.i = i;
+  w.R = 0; w.tau = 0; w.g = 0;
+  if (i < r1) { w.R = a.pb.r[i]; w.tau = a.ex_tau[i]; w.g = a.ex_g[i]; }
+  return w;
+}
+
 __device__ __forceinline__ IdealRow ideal_row_at(const IdealArgs &a, int64_t i, int64_t r1) {
   IdealRow w;
   while (i < r1 && a.ex_tau[i] == 0) ++i;    // zero-duration rows complete instantly
@@ -128,7 +138,7 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
         first = ideal_row_at(a, r0, r1);
         live = first.i < r1;                  // an all-zero chain never runs
         cur = first;
-        if (live) nxt = ideal_row_at(a, cur.i + 1, r1);
+        if (live) nxt = ideal_row_raw(a, cur.i + 1, r1);
       }
       uint32_t rp = 0, rem = cur.tau, dl = slo, comp = 0, rank = 0;
       const uint32_t n = (uint32_t)__popc(__ballot_sync(FULL, live));
@@ -310,6 +320,7 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
           if (rem == 0) {   // next execution of the chain
             if (++rp >= cur.R) {
               rp = 0;
+              while (nxt.i < r1 && nxt.tau == 0) nxt = ideal_row_raw(a, nxt.i + 1, r1);   // zero-duration rows (rare)
               if (nxt.i >= r1) {              // batch complete: next batch back-to-back
                 comp++;
                 dl = (uint32_t)t + slo;
@@ -318,7 +329,7 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
               } else {
                 cur = nxt;
               }
-              nxt = ideal_row_at(a, cur.i + 1, r1);
+              nxt = ideal_row_raw(a, cur.i + 1, r1);
             }
             rem = cur.tau;
           }
