@@ -68,7 +68,7 @@ WsLayout ws_layout(const dstack_problem_t *pb, const dstack_params_t *p) {
   w.rt = w.dtab + align256(nd * DTAB_ROW * 2);
   w.d = w.rt + align256(nd * 4);
   w.ideal = w.d + align256(nd * 8);
-  w.end = w.ideal + ((p->flags & DSTACK_FLAG_IDEAL) ? align256(ideal_ws_bytes(pb->num_rows)) : 0);
+  w.end = w.ideal + ((p->flags & DSTACK_FLAG_IDEAL) ? align256(ideal_ws_bytes(pb->num_rows, pb->num_scen)) : 0);
   return w;
 }
 
@@ -261,6 +261,9 @@ static int ideal_impl(const dstack_problem_t *pb, const dstack_params_t *p, cons
     ia.pb = *pb; ia.p = *p; ia.demand = demand; ia.batch = batch; ia.u_ideal = out->u_ideal;
     ia.thr_ideal = out->thr_ideal;
     ia.work_ctr = (uint32_t *)((char *)ws + ws_layout(pb, p).ctr) + 2;
+    if (!hook) {   // the session's d_j(b) rows and sum R: a per-scenario cost estimate for the heavy-first order
+      ia.dtab_rows = (const uint16_t *)((char *)ws + ws_layout(pb, p).dtab);
+    }
     rc = launch_ideal(ia, (char *)ws + ws_layout(pb, p).ideal, s, &g_launches);
   }
   return rc;

@@ -66,6 +66,9 @@ constexpr int IDEAL_WARPS = 8;
 #ifndef DSTACK_IDEAL_MITM
 #define DSTACK_IDEAL_MITM 1   // 11..16 live items: meet-in-the-middle enumeration instead of the DP (A/B switch)
 #endif
+#ifndef DSTACK_IDEAL_ORDER
+#define DSTACK_IDEAL_ORDER 1   // heavy-first scenario order for k_ideal_sim (A/B switch)
+#endif
 #ifndef DSTACK_IDEAL_SHORTCUTS
 #define DSTACK_IDEAL_SHORTCUTS 1   // reuse the selection when no (rank, g) changed; all-fit shortcut (A/B switch)
 #endif
@@ -113,8 +116,9 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
     if (lane + 32 * k <= L) capmask |= 1u << k;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  for (int64_t s = warp_next_item(a.work_ctr, -1, gwarp, nwarps, lane); s < a.pb.num_scen;
-       s = warp_next_item(a.work_ctr, s, gwarp, nwarps, lane)) {
+  for (int64_t q = warp_next_item(a.work_ctr, -1, gwarp, nwarps, lane); q < a.pb.num_scen;
+       q = warp_next_item(a.work_ctr, q, gwarp, nwarps, lane)) {
+    const int64_t s = a.order ? (int64_t)a.order[q] : q;
     const int32_t k0 = a.pb.scen_dnn_off[s], nd = a.pb.scen_dnn_off[s + 1] - k0;
     double ui = 0.0, ti = 0.0;
     const bool mine = lane < nd && nd <= DSTACK_MAX_DNN_PER_SCEN;
@@ -350,10 +354,54 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
   }
 }
 
-size_t ideal_ws_bytes(int64_t num_rows) {
+size_t ideal_ws_bytes(int64_t num_rows, int64_t num_scen) {
   size_t g = ((size_t)(num_rows + 8) * 2 + 255) & ~(size_t)255;
   size_t t = ((size_t)(num_rows + 8) * 4 + 255) & ~(size_t)255;
-  return g + t;
+  size_t o = ((size_t)(num_scen + 8) * 4 + 255) & ~(size_t)255;
+  return g + t + o + 256;
+}
+
+// Heavy-first scenario order for k_ideal_sim: its cost is the number of events, roughly sum over active DNNs of
+// (executions per batch) x (batches per session) ~ sum_j rows_j * T / (run time of b*_j).  Scenarios are bucketed by
+// floor(log2(estimate)) and listed heaviest bucket first (order inside a bucket arbitrary: the schedule, not the
+// results, depends on it), so the longest event chains start first and the kernel's tail shrinks.
+constexpr int IDEAL_BUCKETS = 40;
+__device__ __forceinline__ uint32_t ideal_cost_bucket(const IdealArgs &a, int64_t s) {
+  const int32_t k0 = a.pb.scen_dnn_off[s], k1 = a.pb.scen_dnn_off[s + 1];
+  if (k1 - k0 > DSTACK_MAX_DNN_PER_SCEN) return 0;
+  uint32_t T = 0;
+  for (int32_t k = k0; k < k1; ++k)
+    if (a.demand[k] > 0 && (uint32_t)a.pb.slo_us[k] > T) T = (uint32_t)a.pb.slo_us[k];
+  double est = 0.0;
+  for (int32_t k = k0; k < k1; ++k) {
+    if (a.demand[k] == 0) continue;
+    const double rows = (double)(a.pb.dnn_row_off[k + 1] - a.pb.dnn_row_off[k]);
+    double d = 1.0;
+    if (a.dtab_rows) {
+      const uint32_t b = a.batch[k];
+      const uint32_t v = b ? a.dtab_rows[(int64_t)k * DSTACK_MAX_BATCH + b - 1] : 0u;
+      d = v ? (double)v * (double)a.p.slot_us : 1.0;
+    }
+    est += rows * (double)T / d;
+  }
+  int e = 0;
+  frexp(est + 1.0, &e);
+  return (uint32_t)(e < 0 ? 0 : (e >= IDEAL_BUCKETS ? IDEAL_BUCKETS - 1 : e));
+}
+
+__global__ void __launch_bounds__(256) k_ideal_order_count(IdealArgs a) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.pb.num_scen; s += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&a.bucket_cnt[ideal_cost_bucket(a, s)], 1u);
+}
+__global__ void k_ideal_order_scan(IdealArgs a) {   // one thread: heaviest bucket first
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    uint32_t off = 0;
+    for (int b = IDEAL_BUCKETS - 1; b >= 0; --b) { const uint32_t c = a.bucket_cnt[b]; a.bucket_cnt[b] = off; off += c; }
+  }
+}
+__global__ void __launch_bounds__(256) k_ideal_order_scatter(IdealArgs a) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.pb.num_scen; s += (int64_t)gridDim.x * blockDim.x)
+    a.order[atomicAdd(&a.bucket_cnt[ideal_cost_bucket(a, s)], 1u)] = (uint32_t)s;
 }
 
 int launch_ideal(IdealArgs a, void *ws, cudaStream_t s, int *launches) {
@@ -361,6 +409,8 @@ int launch_ideal(IdealArgs a, void *ws, cudaStream_t s, int *launches) {
   const int64_t num_rows = a.pb.num_rows;
   a.ex_g = (uint16_t *)ws;
   a.ex_tau = (uint32_t *)((char *)ws + (((size_t)(num_rows + 8) * 2 + 255) & ~(size_t)255));
+  a.order = (uint32_t *)((char *)a.ex_tau + (((size_t)(num_rows + 8) * 4 + 255) & ~(size_t)255));
+  a.bucket_cnt = (uint32_t *)((char *)a.order + (((size_t)(a.pb.num_scen + 8) * 4 + 255) & ~(size_t)255));
   if (a.pb.num_dnn > 0) {
     int64_t blocks = ((int64_t)a.pb.num_dnn * 32 + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
@@ -373,6 +423,19 @@ int launch_ideal(IdealArgs a, void *ws, cudaStream_t s, int *launches) {
   if (a.work_ctr) {   // one resident wave pulling scenarios (their event counts differ by orders of magnitude)
     if (cudaMemsetAsync(a.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
     blocks = resident_wave(k_ideal_sim, IDEAL_WARPS * 32, 0, blocks);
+    if (DSTACK_IDEAL_ORDER) {   // heaviest estimated scenarios first
+      if (cudaMemsetAsync(a.bucket_cnt, 0, sizeof(uint32_t) * IDEAL_BUCKETS, s) != cudaSuccess) return DSTACK_ELAUNCH;
+      int64_t ob = (a.pb.num_scen + 255) / 256;
+      if (ob > (int64_t)num_sms() * 8) ob = (int64_t)num_sms() * 8;
+      k_ideal_order_count<<<(unsigned)ob, 256, 0, s>>>(a);
+      k_ideal_order_scan<<<1, 32, 0, s>>>(a);
+      k_ideal_order_scatter<<<(unsigned)ob, 256, 0, s>>>(a);
+      *launches += 3;
+    } else {
+      a.order = nullptr;
+    }
+  } else {
+    a.order = nullptr;
   }
   k_ideal_sim<<<(unsigned)blocks, IDEAL_WARPS * 32, 0, s>>>(a);
   ++*launches;

@@ -86,6 +86,10 @@ struct IdealArgs {
   uint32_t *ex_tau;   // [num_rows] workspace
   double *u_ideal, *thr_ideal;
   uint32_t *work_ctr;   // workspace word: k_ideal_sim's scenario counter (NULL: grid stride)
+  const uint16_t *dtab_rows;   // d_j(b) rows of the session just computed (cost estimate for the order; may be NULL)
+  const uint32_t *ws_RT;       // sum R per DNN (may be NULL)
+  uint32_t *order;             // [num_scen] scenarios, heaviest estimate first (set by launch_ideal)
+  uint32_t *bucket_cnt;        // [64] workspace
 };
 
 struct CmpArgs {
@@ -135,7 +139,7 @@ inline int64_t resident_wave(K kern, int threads, size_t smem, int64_t blocks) {
   const int64_t w = (int64_t)nb * num_sms();
   return blocks < w ? blocks : w;
 }
-size_t ideal_ws_bytes(int64_t num_rows);
+size_t ideal_ws_bytes(int64_t num_rows, int64_t num_scen);
 size_t agg_ws_bytes();
 
 }  // namespace dstack
