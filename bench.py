@@ -158,6 +158,12 @@ def kernel_counters(config, key="per_scenario"):
         return {}
 
 
+def sp_of(args):
+    """The workload spec of this rank's shard (for the oracle samples of the legs)."""
+    import synth
+    return synth.config(args.config, num_scen=args.scen or None, variant=args.variant)[0]
+
+
 def leg_roofline(args, slot, ms, per_gpu):
     """Issue-slot roofline of a next-row leg's kernel: ncu warp instructions per scenario (profiles/counters.json
     "legs") x scenarios per call / the live device time of that kernel per call."""
@@ -245,6 +251,26 @@ def cpu_baseline(args, sp, p):
     return {"value": done / el, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{done} scenarios (every {stride}th of the config-{args.config} workload), "
                       f"{el:.1f} s wall on {cores} host threads (OpenMP over scenarios)"}
+
+
+def oracle_leg(args, sp, what, call, seconds=2.0, unit=UNIT, per_dnn=False, max_scen=1024):
+    """The CPU oracle of a next-row leg timed beside it (test infrastructure; rank 0, N = 1): `call(pb, cores)` on
+    stratified samples of the workload for about `seconds` of host time; units = scenarios (or DNNs)."""
+    import synth
+    cores = host_cores()
+    total = sp.num_scen
+    chunk, done, units, el, k = 16, 0, 0, 0.0, 0
+    stride = max(1, total // max_scen)
+    while el < seconds and done < max_scen:
+        idx = [((k * chunk + i) * stride) % total for i in range(chunk)]
+        pb = synth.sample(sp, idx)
+        t0 = time.perf_counter()
+        call(pb, cores)
+        el += time.perf_counter() - t0
+        done += chunk; k += 1
+        units += pb.num_dnn if per_dnn else chunk
+    return {"value": units / el, "unit": unit, "cores": cores, "kind": "oracle",
+            "sample": f"{done} scenarios (every {stride}th of the config-{args.config} workload), {el:.1f} s wall, {what}"}
 
 
 def algorithmic_bytes(dp, args):
@@ -438,8 +464,12 @@ def run_compare_leg(args, ds, dp, p, out, ws, stream, per_gpu, world):
     for i, name in enumerate(ds.CMP_NAMES):
         means[name] = {k: float(c[k][ok, i].mean().item()) for k in ("u", "thr", "jain")}
     d = means["dstack"]["thr"]
+    orc = None
+    if world == 1 and not args.no_cpu_baseline:
+        import oracle
+        orc = oracle_leg(args, sp_of(args), "oracle.compare", lambda pb, c: oracle.compare(pb, p, nthreads=c))
     return {"api": "paper_2304_13541_b200.dstack.compare (dstack_compare)", "ms_per_call": ms,
-            "roofline": leg_roofline(args, "k_compare", ms, per_gpu),
+            "roofline": leg_roofline(args, "k_compare", ms, per_gpu), "cpu_oracle": orc,
             "scenarios_per_s": per_gpu * world / (ms / 1e3), "gpu_launches": ds.last_launch_count(),
             "schedulers": list(ds.CMP_NAMES), "means_over_scheduled_scenarios": means,
             "dstack_throughput_ratio": {k: d / means[k]["thr"] for k in ds.CMP_NAMES if means[k]["thr"] > 0}}
@@ -473,7 +503,12 @@ def run_below_knee_leg(args, ds, dp, p, out, stream, per_gpu, world):
     ms = float(t.item())
     a0, a1 = ds.agg_to_dict(out["agg"]), ds.agg_to_dict(o["agg"])
     n0, n1 = max(a0["n_scen_scheduled"], 1), max(a1["n_scen_scheduled"], 1)
-    return {"api": "paper_2304_13541_b200.dstack.eval_batch (dstack_eval_batch, DSTACK_FLAG_BELOW_KNEE)",
+    orc = None
+    if world == 1 and not args.no_cpu_baseline:
+        import oracle
+        orc = oracle_leg(args, sp_of(args), "oracle.evaluate with below_knee",
+                         lambda pb, c: oracle.evaluate(pb, q, nthreads=c))
+    return {"cpu_oracle": orc, "api": "paper_2304_13541_b200.dstack.eval_batch (dstack_eval_batch, DSTACK_FLAG_BELOW_KNEE)",
             "reconf_us": q.reconf_us, "ms_per_call": ms, "scenarios_per_s": per_gpu * world / (ms / 1e3),
             "k_cycle_ms": cyc_ms, "roofline": leg_roofline(args, "k_cycle_bk", cyc_ms, per_gpu),
             "below_knee_runs": int(o["below"].sum().item()), "misses": a1["misses"], "misses_default": a0["misses"],
@@ -505,8 +540,12 @@ def run_cluster_leg(args, ds, dp, p, out, ws, stream, per_gpu, world):
     ok = c["thr"][:, 1] > 0
     means = {name: {k: float(c[k][ok, i].mean().item()) for k in ("u", "thr")} for i, name in enumerate(ds.CLU_NAMES)}
     tt = means["temporal"]["thr"]
+    orc = None
+    if world == 1 and not args.no_cpu_baseline:
+        import oracle
+        orc = oracle_leg(args, sp_of(args), "oracle.cluster", lambda pb, c: oracle.cluster(pb, p, G, nthreads=c))
     return {"api": "paper_2304_13541_b200.dstack.cluster (dstack_cluster)", "gpus_modelled": G, "ms_per_call": ms,
-            "roofline": leg_roofline(args, "k_cluster", ms, per_gpu),
+            "roofline": leg_roofline(args, "k_cluster", ms, per_gpu), "cpu_oracle": orc,
             "scenarios_per_s": per_gpu * world / (ms / 1e3), "policies": list(ds.CLU_NAMES),
             "means_over_scheduled_scenarios": means,
             "throughput_vs_temporal": {k: means[k]["thr"] / tt for k in ds.CLU_NAMES} if tt > 0 else None}
@@ -535,7 +574,12 @@ def run_knee_probe_leg(args, ds, dp, p, stream, world):
     ok = st == 0
     n_ok = int(ok.sum().item())
     match = int(((k == kx) & ok).sum().item())
-    return {"api": "paper_2304_13541_b200.dstack.knee_probe (dstack_knee_probe)", "batch": 1, "ms_per_call": ms,
+    orc = None
+    if world == 1 and not args.no_cpu_baseline:
+        import oracle
+        orc = oracle_leg(args, sp_of(args), "oracle.knee_probe at b = 1",
+                         lambda pb, c: oracle.knee_probe(pb, p, 1), unit="DNNs/s", per_dnn=True, max_scen=65536)
+    return {"cpu_oracle": orc, "api": "paper_2304_13541_b200.dstack.knee_probe (dstack_knee_probe)", "batch": 1, "ms_per_call": ms,
             "roofline": leg_roofline(args, "k_knee_probe", ms, dp.num_scen),
             "dnns_per_s": dp.num_dnn * world / (ms / 1e3), "dnns_ok": n_ok,
             "exact_knee_match_frac": match / max(n_ok, 1),
