@@ -261,7 +261,8 @@ def oracle_leg(args, sp, what, call, seconds=2.0, unit=UNIT, per_dnn=False, max_
     total = sp.num_scen
     chunk, done, units, el, k = 16, 0, 0, 0.0, 0
     stride = max(1, total // max_scen)
-    while el < seconds and done < max_scen:
+    wall0 = time.perf_counter()
+    while el < seconds and done < max_scen and time.perf_counter() - wall0 < 4 * seconds:
         idx = [((k * chunk + i) * stride) % total for i in range(chunk)]
         pb = synth.sample(sp, idx)
         t0 = time.perf_counter()
