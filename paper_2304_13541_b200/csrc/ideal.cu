@@ -18,6 +18,10 @@ namespace dstack {
 
 
 
+#ifndef DSTACK_IDEAL_ROW_CANDIDATES
+#define DSTACK_IDEAL_ROW_CANDIDATES 1   // per-row knee from each regime's ends and real maximum (0: scan every level)
+#endif
+
 __global__ void __launch_bounds__(256) k_ideal_rows(IdealArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -36,15 +40,52 @@ __global__ void __launch_bounds__(256) k_ideal_rows(IdealArgs a) {
       const uint64_t dd = a.pb.d[i];
       uint32_t bestS = 0, bestl = 0;
       uint64_t bestX = 0;
-      for (int32_t l = 1; l <= L; ++l) {
+      auto consider = [&](int32_t l) {   // exact; ties -> the smaller level (the brute-force scan's rule)
+        if (l < 1 || l > L) return;
         const uint64_t S = (uint64_t)s_of(l, S_tot, L);
+        l = (int32_t)(((S - 1) * (uint64_t)L) / (uint64_t)S_tot) + 1;   // the smallest level granting these S SMs
         uint64_t X = wC * S + (N >= 1 ? M * t_p * (N > S ? N : S) : 0ull);
         if (mem_mode == 1) X += b * dd;
         else if (mem_mode == 2) X += b * dd * S * S;
-        if (bestl == 0 || cmp_score((uint32_t)S, X, (float)X, bestS, bestX, (float)bestX) > 0) {
-          bestS = (uint32_t)S; bestl = (uint32_t)l; bestX = X;
+        const int c = bestl == 0 ? 1 : cmp_score((uint32_t)S, X, (float)X, bestS, bestX, (float)bestX);
+        if (c > 0 || (c == 0 && (uint32_t)l < bestl)) { bestS = (uint32_t)S; bestl = (uint32_t)l; bestX = X; }
+      };
+#if DSTACK_IDEAL_ROW_CANDIDATES
+      // One row has two latency regimes, S < N (X = a S^2 + (wC) S + M t_p N + m) and S >= N (X = a S^2 +
+      // (wC + M t_p) S + m); on each, g = S / X^2 is unimodal in S with its real maximum at the positive root of
+      // -3a S^2 - beta S + gamma = 0.  The exact argmax over the levels is therefore among each regime's ends and
+      // the levels adjacent to that maximum (checked with a +-2 margin).
+      const int64_t lmax_lt_N = N >= 1 ? (int64_t)((N - 1 < (uint64_t)S_tot ? N - 1 : (uint64_t)S_tot) * (uint64_t)L / (uint64_t)S_tot) : 0;
+      const double vb = mem_mode == 2 ? (double)(b * dd) : 0.0, m1 = mem_mode == 1 ? (double)(b * dd) : 0.0;
+      for (int seg = 0; seg < 2; ++seg) {
+        // seg 0: S < N (levels 1..lmax_lt_N); seg 1: S >= N (levels lmax_lt_N+1..L)
+        const int64_t l0 = seg == 0 ? 1 : lmax_lt_N + 1, l1 = seg == 0 ? lmax_lt_N : L;
+        if (l0 > l1) continue;
+        consider((int32_t)l0);
+        consider((int32_t)l1);
+        const double beta = (double)wC + (seg == 1 && N >= 1 ? (double)(M * t_p) : 0.0);
+        const double gamma = m1 + (seg == 0 ? (double)(M * t_p * N) : 0.0);
+        double sst;
+        if (vb > 0.0) sst = (-beta + sqrt(beta * beta + 12.0 * vb * gamma)) / (6.0 * vb);
+        else if (beta > 0.0) sst = gamma / beta;
+        else sst = (double)S_tot;   // g increasing: the regime's end
+        if (!(sst >= 0.0)) sst = 0.0;
+        if (sst > (double)S_tot + 4.0) sst = (double)S_tot + 4.0;
+        if (L <= S_tot) {   // levels sparse in S: the levels around S* L / S_tot
+          const int64_t lc = (int64_t)floor(sst * (double)L / (double)S_tot);
+          for (int64_t l = lc - 2; l <= lc + 3; ++l) if (l >= l0 && l <= l1) consider((int32_t)l);
+        } else {            // every S attained: the smallest level of each S around S*
+          const int64_t sc = (int64_t)floor(sst);
+          for (int64_t S = sc - 2; S <= sc + 3; ++S) {
+            if (S < 1 || S > S_tot) continue;
+            const int64_t l = ((S - 1) * L) / S_tot + 1;   // smallest l with S(l) = S
+            if (l >= l0 && l <= l1) consider((int32_t)l);
+          }
         }
       }
+#else
+      for (int32_t l = 1; l <= L; ++l) consider(l);
+#endif
       const uint64_t den = (uint64_t)bestS * M;
       const uint64_t tau = (bestX + den - 1) / den;
       a.ex_g[i] = (uint16_t)bestl;
