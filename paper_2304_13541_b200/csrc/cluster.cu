@@ -104,16 +104,6 @@ __global__ void __launch_bounds__(CLU_WARPS * 32, DSTACK_CLU_MINB) k_cluster(con
         srv = warp_sum_u64(truns * bs);
       };
       const double NL = (double)nslots * (double)L;
-      // ---- c = 1, 2: the whole mix on every GPU ----
-      {
-        uint64_t occn, srv;
-        temporal(active, nslots, occn, srv);
-        const double u1 = (double)occn / NL, t1 = (double)G * ((double)srv * 1e6 / (double)T);
-        const uint64_t r = session(active, nslots);
-        const double u2 = (double)(uint32_t)r / NL, t2 = (double)G * ((double)(r >> 32) * 1e6 / (double)T);
-        if (lane == 1) { ou = u1; othr = t1; }
-        if (lane == 2) { ou = u2; othr = t2; }
-      }
       // ---- placements: home0 = (rank among active, index order) mod G; home3 = first-fit decreasing ----
       const uint32_t below = __ballot_sync(FULL, active) & ((1u << lane) - 1u);
       const int32_t home0 = active ? (int32_t)((uint32_t)__popc(below) % (uint32_t)G) : -1;
@@ -138,27 +128,35 @@ __global__ void __launch_bounds__(CLU_WARPS * 32, DSTACK_CLU_MINB) k_cluster(con
           if (lane == own) home3 = gi;
         }
       }
+      // ---- gi = -1: the whole mix on every GPU (c = 1, 2); gi >= 0: GPU gi under c = 0 and c = 3.  One call site
+      // of the session and of temporal keeps one copy of each in the instruction cache. ----
       double u0 = 0.0, t0 = 0.0, u3 = 0.0, t3 = 0.0;
-      for (int gi = 0; gi < G; ++gi) {
-        {   // c = 0
-          const bool m0 = home0 == gi;
-          const uint32_t Ti = __reduce_max_sync(FULL, m0 ? slo : 0u);
-          if (Ti > 0) {
-            const int32_t ns = (int32_t)(Ti / (uint32_t)slot);
-            uint64_t occn, srv;
-            temporal(m0, ns, occn, srv);
+#pragma unroll 1
+      for (int gi = -1; gi < G; ++gi) {
+        const bool m0 = gi < 0 ? active : home0 == gi, m3 = gi < 0 ? active : home3 == gi;
+        const uint32_t T0 = gi < 0 ? T : __reduce_max_sync(FULL, m0 ? slo : 0u);
+        const uint32_t T3 = gi < 0 ? T : __reduce_max_sync(FULL, m3 ? slo : 0u);
+        if (T0 > 0) {   // temporal over m0 (c = 1 for the whole mix, c = 0 on GPU gi)
+          const int32_t ns = (int32_t)(T0 / (uint32_t)slot);
+          uint64_t occn, srv;
+          temporal(m0, ns, occn, srv);
+          const double thr = (double)srv * 1e6 / (double)T0;
+          if (gi < 0) {
+            if (lane == 1) { ou = (double)occn / NL; othr = (double)G * thr; }
+          } else {
             u0 += (double)occn / ((double)ns * NLg) / (double)G;
-            t0 += (double)srv * 1e6 / (double)Ti;
+            t0 += thr;
           }
         }
-        {   // c = 3
-          const bool m3 = home3 == gi;
-          const uint32_t Ti = __reduce_max_sync(FULL, m3 ? slo : 0u);
-          if (Ti > 0) {
-            const int32_t ns = (int32_t)(Ti / (uint32_t)slot);
-            const uint64_t r = session(m3, ns);
+        if (T3 > 0) {   // D-STACK over m3 (c = 2 for the whole mix, c = 3 on GPU gi)
+          const int32_t ns = (int32_t)(T3 / (uint32_t)slot);
+          const uint64_t r = session(m3, ns);
+          const double thr = (double)(r >> 32) * 1e6 / (double)T3;
+          if (gi < 0) {
+            if (lane == 2) { ou = (double)(uint32_t)r / NL; othr = (double)G * thr; }
+          } else {
             u3 += (double)(uint32_t)r / ((double)ns * NLg) / (double)G;
-            t3 += (double)(r >> 32) * 1e6 / (double)Ti;
+            t3 += thr;
           }
         }
       }

@@ -64,23 +64,25 @@ __global__ void __launch_bounds__(CMP_WARPS * 32, DSTACK_CMP_MINB) k_compare(Cmp
         const int j = __ffs(todo) - 1;
         todo &= todo - 1;
         const int64_t kj = k0 + j;
-        const int64_t r0 = a.pb.dnn_row_off[kj];
-        const int32_t K = (int32_t)(a.pb.dnn_row_off[kj + 1] - r0);
-        uint64_t RT = 0, D = 0;
-        for (int i = lane; i < K; i += 32) { RT += a.pb.r[r0 + i]; D += (uint64_t)a.pb.r[r0 + i] * a.pb.d[r0 + i]; }
-        RT = warp_sum_u64(RT); D = warp_sum_u64(D);
         const int32_t gj = (int32_t)__shfl_sync(FULL, g, j), bj = (int32_t)__shfl_sync(FULL, bs, j);
         const int32_t dj = (int32_t)__shfl_sync(FULL, dem, j);
-        dtab_from_rows(a.pb, a.p, kj, RT, D, gj, b_lo, bj, dtab + j * DTAB_ROW, lane);
         const uint64_t M = a.p.mem_mode == 0 ? 1ull : (uint64_t)a.pb.mem_bw[kj];
         const uint64_t SL = (uint64_t)a.p.S_tot, Sk = (uint64_t)s_of(dj, a.p.S_tot, L);
-        const uint64_t XL = x_from_rows(a.pb, a.p, kj, RT, D, SL, bj, lane);
-        const uint64_t Xk = x_from_rows(a.pb, a.p, kj, RT, D, Sk, bj, lane);
+        const uint64_t Sg = (uint64_t)s_of(gj, a.p.S_tot, L);
+        // one row pass: the sums, X(g, b*), X(L, b*), X(knee, b*); d_j(b) for b < b* (rare) one pass each
+        uint64_t RT, D, Vg, VL, Vk;
+        rows_pass3(a.pb, a.p, kj, bj, Sg, SL, Sk, RT, D, Vg, VL, Vk, lane);
+        if (bj > b_lo) dtab_from_rows(a.pb, a.p, kj, RT, D, gj, b_lo, bj - 1, dtab + j * DTAB_ROW, lane);
+        if (lane == 0)
+          dtab[j * DTAB_ROW + bj - 1] = ceil_div_clamp16(x_of_v(a.pb, a.p, kj, RT, D, Sg, bj, Vg), Sg * M * (uint64_t)slot);
+        const uint64_t XL = x_of_v(a.pb, a.p, kj, RT, D, SL, bj, VL);
+        const uint64_t Xk = x_of_v(a.pb, a.p, kj, RT, D, Sk, bj, Vk);
         if (lane == j) {
           dL = ceil_div_clamp16(XL, SL * M * (uint64_t)slot);
           dk = ceil_div_clamp16(Xk, Sk * M * (uint64_t)slot);
         }
       }
+      __syncwarp();
       const double NL = (double)nslots * (double)L;
       // ---- c = 0, 1, 2: the session with each fill order ----
       for (int c = 0; c < 3; ++c) {

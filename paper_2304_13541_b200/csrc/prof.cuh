@@ -466,6 +466,42 @@ __device__ __forceinline__ uint64_t x_from_rows(const dstack_problem_t &pb, cons
   return X;
 }
 
+// X from the row sum V = sum_i R_i max(S, N_i(b)) over N_i >= 1 (the tail of x_from_rows).
+__device__ __forceinline__ uint64_t x_of_v(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k, uint64_t RT,
+                                           uint64_t D, uint64_t S, int32_t b, uint64_t V) {
+  const uint64_t M = p.mem_mode == 0 ? 1ull : (uint64_t)pb.mem_bw[k];
+  uint64_t X = (p.wse_mode == 0 ? (uint64_t)b : 1ull) * (uint64_t)pb.t_np[k] * RT * S * M + M * (uint64_t)pb.t_p[k] * V;
+  if (p.mem_mode == 1) X += (uint64_t)b * D;
+  else if (p.mem_mode == 2) X += (uint64_t)b * D * S * S;
+  return X;
+}
+
+// One warp-cooperative row pass: RT = sum R, D = sum R d and V_q = sum_i R_i max(S_q, N_i(b)) for three S_q at
+// one batch b -- the four row passes (sums, x_from_rows x 3) a consumer of one b would otherwise make.
+__device__ __forceinline__ void rows_pass3(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k, int32_t b,
+                                           uint64_t S0, uint64_t S1, uint64_t S2, uint64_t &RT, uint64_t &D,
+                                           uint64_t &V0, uint64_t &V1, uint64_t &V2, int lane) {
+  const int64_t r0 = pb.dnn_row_off[k];
+  const int32_t K = (int32_t)(pb.dnn_row_off[k + 1] - r0);
+  const uint32_t *n = pb.n + r0;
+  const uint16_t *r = pb.r + r0;
+  const uint32_t *d = pb.d + r0;
+  uint64_t rt = 0, dd = 0, v0 = 0, v1 = 0, v2 = 0;
+  for (int i = lane; i < K; i += 32) {
+    const uint64_t ri = r[i], nn = n[i];
+    const uint64_t N = p.par_mode == 0 ? (uint64_t)b * nn : ((uint64_t)b * nn + 2047) >> 11;
+    rt += ri;
+    dd += ri * d[i];
+    if (N >= 1) {
+      v0 += ri * (N > S0 ? N : S0);
+      v1 += ri * (N > S1 ? N : S1);
+      v2 += ri * (N > S2 ? N : S2);
+    }
+  }
+  RT = warp_sum_u64(rt); D = warp_sum_u64(dd);
+  V0 = warp_sum_u64(v0); V1 = warp_sum_u64(v1); V2 = warp_sum_u64(v2);
+}
+
 // d_j(b) at level g for b in [b_lo, b_hi] from the rows (any mode): one row pass per b.
 __device__ __forceinline__ void dtab_from_rows(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k,
                                                uint64_t RT, uint64_t D, int32_t g, int32_t b_lo, int32_t b_hi,
