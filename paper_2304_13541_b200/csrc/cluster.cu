@@ -58,52 +58,6 @@ __global__ void __launch_bounds__(CLU_WARPS * 32, DSTACK_CLU_MINB) k_cluster(con
     }
     if (T > 0) {
       uint16_t *dtab = a.dtab_rows + (int64_t)k0 * DTAB_ROW;
-      // ---- per active model: sum R, sum R d (one row pass) and the b* run at 100% GPU, d^L ----
-      uint64_t RTl = 0, Dl = 0;
-      uint32_t dL = 0;
-      {
-        uint32_t todo = __ballot_sync(FULL, active);
-        while (todo) {
-          const int j = __ffs(todo) - 1;
-          todo &= todo - 1;
-          const int64_t kj = k0 + j;
-          const int64_t r0 = a.pb.dnn_row_off[kj];
-          const int32_t K = (int32_t)(a.pb.dnn_row_off[kj + 1] - r0);
-          uint64_t RT = 0, D = 0;
-          for (int i = lane; i < K; i += 32) { RT += a.pb.r[r0 + i]; D += (uint64_t)a.pb.r[r0 + i] * a.pb.d[r0 + i]; }
-          RT = warp_sum_u64(RT); D = warp_sum_u64(D);
-          const uint64_t M = a.p.mem_mode == 0 ? 1ull : (uint64_t)a.pb.mem_bw[kj];
-          const uint64_t SL = (uint64_t)a.p.S_tot;
-          const uint64_t XL = x_from_rows(a.pb, a.p, kj, RT, D, SL, (int32_t)__shfl_sync(FULL, bs, j), lane);
-          if (lane == j) { RTl = RT; Dl = D; dL = ceil_div_clamp16(XL, SL * M * (uint64_t)slot); }
-        }
-      }
-      // one D-STACK session over the members (WMAX-MIN over their demands first); returns occ | served << 32
-      auto session = [&](bool member, int32_t ns) -> uint64_t {
-        const uint32_t alloc = wmaxmin_lane(member ? dem : 0u, lane, nd, L);
-        const uint32_t al = alloc >> 16;
-        const uint32_t g = member ? (dem > al ? dem : al) : 0u;
-        uint32_t todo = __ballot_sync(FULL, member);
-        while (todo) {
-          const int j = __ffs(todo) - 1;
-          todo &= todo - 1;
-          dtab_from_rows(a.pb, a.p, k0 + j, shfl_u64(RTl, j), shfl_u64(Dl, j), (int32_t)__shfl_sync(FULL, g, j), b_lo,
-                         (int32_t)__shfl_sync(FULL, bs, j), dtab + j * DTAB_ROW, lane);
-        }
-        const uint32_t rep = member ? (uint32_t)ns / sl : 0u;
-        uint32_t runs = 0, served = 0;
-        const CycRes cr = cycle_core(sm, dtab, lane, member, g, bs, sl, rep, ns, L, b_lo, false, runs, served);
-        return (uint64_t)cr.occ_all | ((uint64_t)cr.served_tot << 32);
-      };
-      // temporal sharing over the members (O9): slices proportional to SLO, back-to-back b* runs at 100%
-      auto temporal = [&](bool member, int32_t ns, uint64_t &occn, uint64_t &srv) {
-        const uint64_t tot = warp_sum_u64(member ? (uint64_t)sl : 0ull);
-        const uint64_t slice = member ? (uint64_t)ns * sl / tot : 0ull;
-        const uint64_t truns = member && dL ? slice / dL : 0ull;
-        occn = warp_sum_u64(slice * dem);
-        srv = warp_sum_u64(truns * bs);
-      };
-      const double NL = (double)nslots * (double)L;
       // ---- placements: home0 = (rank among active, index order) mod G; home3 = first-fit decreasing ----
       const uint32_t below = __ballot_sync(FULL, active) & ((1u << lane) - 1u);
       const int32_t home0 = active ? (int32_t)((uint32_t)__popc(below) % (uint32_t)G) : -1;
@@ -128,6 +82,69 @@ __global__ void __launch_bounds__(CLU_WARPS * 32, DSTACK_CLU_MINB) k_cluster(con
           if (lane == own) home3 = gi;
         }
       }
+      // ---- session levels: g over the whole mix (c = 2) and on the model's own GPU under FFD (c = 3) ----
+      uint32_t gW, gG = 0;
+      {
+        const uint32_t al = wmaxmin_lane(active ? dem : 0u, lane, nd, L) >> 16;
+        gW = active ? (dem > al ? dem : al) : 0u;
+#pragma unroll 1
+        for (int gi = 0; gi < G; ++gi) {
+          const bool m3 = home3 == gi;
+          const uint32_t ali = wmaxmin_lane(m3 ? dem : 0u, lane, nd, L) >> 16;
+          if (m3) gG = dem > ali ? dem : ali;
+        }
+      }
+      // ---- per active model, one row pass: sum R, sum R d and the b* runs at 100% GPU (d^L), at gW and at gG ----
+      uint64_t RTl = 0, Dl = 0;
+      uint32_t dL = 0, dW = 0, dG = 0;
+      {
+        uint32_t todo = __ballot_sync(FULL, active);
+        while (todo) {
+          const int j = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const int64_t kj = k0 + j;
+          const int32_t bj = (int32_t)__shfl_sync(FULL, bs, j);
+          const uint64_t M = a.p.mem_mode == 0 ? 1ull : (uint64_t)a.pb.mem_bw[kj];
+          const uint64_t SL = (uint64_t)a.p.S_tot;
+          const uint64_t SW = (uint64_t)s_of((int32_t)__shfl_sync(FULL, gW, j), a.p.S_tot, L);
+          const uint64_t SG = (uint64_t)s_of((int32_t)__shfl_sync(FULL, gG, j), a.p.S_tot, L);
+          uint64_t RT, D, VL, VW, VG;
+          rows_pass3(a.pb, a.p, kj, bj, SL, SW, SG, RT, D, VL, VW, VG, lane);
+          if (lane == j) {
+            RTl = RT; Dl = D;
+            dL = ceil_div_clamp16(x_of_v(a.pb, a.p, kj, RT, D, SL, bj, VL), SL * M * (uint64_t)slot);
+            dW = ceil_div_clamp16(x_of_v(a.pb, a.p, kj, RT, D, SW, bj, VW), SW * M * (uint64_t)slot);
+            dG = ceil_div_clamp16(x_of_v(a.pb, a.p, kj, RT, D, SG, bj, VG), SG * M * (uint64_t)slot);
+          }
+        }
+      }
+      // one D-STACK session over the members at levels g (WMAX-MIN over their demands, above) with d_j(b*) = dstar;
+      // d_j(b) for b < b* (rare) from one row pass each.  Returns occ | served << 32.
+      auto session = [&](bool member, int32_t ns, uint32_t g, uint32_t dstar) -> uint64_t {
+        if (member) dtab[lane * DTAB_ROW + bs - 1] = (uint16_t)dstar;
+        uint32_t todo = __ballot_sync(FULL, member && bs > (uint32_t)b_lo);
+        while (todo) {
+          const int j = __ffs(todo) - 1;
+          todo &= todo - 1;
+          dtab_from_rows(a.pb, a.p, k0 + j, shfl_u64(RTl, j), shfl_u64(Dl, j), (int32_t)__shfl_sync(FULL, g, j), b_lo,
+                         (int32_t)__shfl_sync(FULL, bs, j) - 1, dtab + j * DTAB_ROW, lane);
+        }
+        __syncwarp();
+        const uint32_t rep = member ? (uint32_t)ns / sl : 0u;
+        uint32_t runs = 0, served = 0;
+        const CycRes cr = cycle_core(sm, dtab, lane, member, member ? g : 0u, bs, sl, rep, ns, L, b_lo, false, runs,
+                                     served);
+        return (uint64_t)cr.occ_all | ((uint64_t)cr.served_tot << 32);
+      };
+      // temporal sharing over the members (O9): slices proportional to SLO, back-to-back b* runs at 100%
+      auto temporal = [&](bool member, int32_t ns, uint64_t &occn, uint64_t &srv) {
+        const uint64_t tot = warp_sum_u64(member ? (uint64_t)sl : 0ull);
+        const uint64_t slice = member ? (uint64_t)ns * sl / tot : 0ull;
+        const uint64_t truns = member && dL ? slice / dL : 0ull;
+        occn = warp_sum_u64(slice * dem);
+        srv = warp_sum_u64(truns * bs);
+      };
+      const double NL = (double)nslots * (double)L;
       // ---- gi = -1: the whole mix on every GPU (c = 1, 2); gi >= 0: GPU gi under c = 0 and c = 3.  One call site
       // of the session and of temporal keeps one copy of each in the instruction cache. ----
       double u0 = 0.0, t0 = 0.0, u3 = 0.0, t3 = 0.0;
@@ -150,7 +167,7 @@ __global__ void __launch_bounds__(CLU_WARPS * 32, DSTACK_CLU_MINB) k_cluster(con
         }
         if (T3 > 0) {   // D-STACK over m3 (c = 2 for the whole mix, c = 3 on GPU gi)
           const int32_t ns = (int32_t)(T3 / (uint32_t)slot);
-          const uint64_t r = session(m3, ns);
+          const uint64_t r = session(m3, ns, gi < 0 ? gW : gG, gi < 0 ? dW : dG);
           const double thr = (double)(r >> 32) * 1e6 / (double)T3;
           if (gi < 0) {
             if (lane == 2) { ou = (double)(uint32_t)r / NL; othr = (double)G * thr; }
