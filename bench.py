@@ -274,14 +274,26 @@ def oracle_leg(args, sp, what, call, seconds=2.0, unit=UNIT, per_dnn=False, max_
             "sample": f"{done} scenarios (every {stride}th of the config-{args.config} workload), {el:.1f} s wall, {what}"}
 
 
-def algorithmic_bytes(dp, args):
-    """Bytes each kernel must move by definition: its inputs once + its outputs once."""
+def raised_rows(dp, out):
+    """(DNNs, rows) whose session level g_j was raised above the demand by WMAX-MIN: k_cycle must read their rows
+    (and RT, D from the workspace) once to evaluate d_j(b) at g_j."""
+    import torch
+    lv, dem = out["level"].to(torch.int64), out["demand"].to(torch.int64)
+    raised = (lv > 0) & (dem > 0) & (lv != dem)
+    cnt = dp.dnn_row_off[1:] - dp.dnn_row_off[:-1]
+    return int(raised.sum().item()), int(cnt[raised].sum().item())
+
+
+def algorithmic_bytes(dp, args, out=None):
+    """Bytes each kernel must move by definition: its inputs once + its outputs once; for k_cycle
+    also the rows (+ RT, D) of the DNNs whose level WMAX-MIN raised, read once to get d_j(b) at g_j."""
     R, D, S = dp.num_rows, dp.num_dnn, dp.num_scen
+    nr, rr = raised_rows(dp, out) if out is not None else (0, 0)
     rows = 10 * R                                   # n u32 + R u16 + d u32
     hdr = D * (8 + 6 * 4)                           # dnn_row_off + t_p, t_np, M, SLO, a, bmax
     prof = rows + hdr + D * (2 + 1 + 2 + 1)         # -> demand, batch, knee, status
     wmm = S * 4 + D * (2 + 4)                       # offsets, demand -> alloc
-    cyc = S * 4 + D * (2 + 1 + 4 + 4) + D * (2 + 2 + 4) + S * (1 + 4 + 3 * 8 + 4)
+    cyc = S * 4 + D * (2 + 1 + 4 + 4) + D * (2 + 2 + 4) + S * (1 + 4 + 3 * 8 + 4) + 10 * rr + nr * (8 + 4 + 8)
     agg = S * (4 + 1 + 4 + 3 * 8 + 4) + D * (2 + 1 + 2 + 1 + 4 + 2 + 2 + 4)
     path = rows + hdr + S * 4 + D * (2 + 1 + 2 + 1 + 4 + 2 + 2 + 4) + S * (1 + 4 + 3 * 8 + 4)
     return {"k_prof": prof, "k_wmaxmin": wmm, "k_cycle": cyc, "k_ideal": rows, "k_agg": agg, "path": path}
@@ -376,7 +388,7 @@ def run_native(args, rank, world, local):
         if world > 1:
             dist.destroy_process_group()
         return 0
-    ab = algorithmic_bytes(dp, args)
+    ab = algorithmic_bytes(dp, args, out)
     peak, peak_src = hbm_peak()
     cnt = kernel_counters(args.config)
 
@@ -431,7 +443,8 @@ def run_native(args, rank, world, local):
                   "mean_u_static": agg["sum_u_static"] / max(agg["n_scen_scheduled"], 1),
                   "scen_status": agg["n_scen_st"], "dnn_status": agg["n_st"],
                   "bstar_hist_nonzero": {str(b): c for b, c in enumerate(agg["batch_hist"]) if c},
-                  "rows_per_gpu": dp.num_rows, "dnns_per_gpu": dp.num_dnn, "checksum": agg["checksum"]},
+                  "rows_per_gpu": dp.num_rows, "dnns_per_gpu": dp.num_dnn,
+                  "raised_dnns_rows": list(raised_rows(dp, out)), "checksum": agg["checksum"]},
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, sp0, p)

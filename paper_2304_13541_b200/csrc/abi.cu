@@ -56,9 +56,10 @@ bool disjoint(const dstack_problem_t *pb, const void *o) {
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// workspace layout: [agg partials | d_j(b) rows u16[num_dnn][64] | RT u32[num_dnn] | D u64[num_dnn] | ideal]
+// workspace layout: [agg partials | counters | d_j(b) rows u16[num_dnn][64] | RT u32[num_dnn] | D u64[num_dnn] |
+//                    d_j(b*) u16[num_dnn] | ideal]
 struct WsLayout {
-  size_t ctr, dtab, rt, d, ideal, end;
+  size_t ctr, dtab, rt, d, dst, ideal, end;
 };
 WsLayout ws_layout(const dstack_problem_t *pb, const dstack_params_t *p) {
   WsLayout w;
@@ -67,7 +68,8 @@ WsLayout ws_layout(const dstack_problem_t *pb, const dstack_params_t *p) {
   w.dtab = w.ctr + 256;
   w.rt = w.dtab + align256(nd * DTAB_ROW * 2);
   w.d = w.rt + align256(nd * 4);
-  w.ideal = w.d + align256(nd * 8);
+  w.dst = w.d + align256(nd * 8);
+  w.ideal = w.dst + align256(nd * 2);
   w.end = w.ideal + ((p->flags & DSTACK_FLAG_IDEAL) ? align256(ideal_ws_bytes(pb->num_rows, pb->num_scen)) : 0);
   return w;
 }
@@ -243,6 +245,7 @@ static int schedule_impl(const dstack_problem_t *pb, const dstack_params_t *p, c
   c.T_us = out->T_us; c.u_static = out->u_static; c.u = out->u; c.thr = out->thr; c.misses = out->misses;
   c.below = out->below;
   c.dtab_rows = (uint16_t *)((char *)ws + ws_layout(pb, p).dtab);
+  c.dstar = (uint16_t *)((char *)ws + ws_layout(pb, p).dst);
   c.work_ctr = (uint32_t *)((char *)ws + ws_layout(pb, p).ctr);
   if (pre_ws) { c.ws_RT = (const uint32_t *)((char *)ws + ws_layout(pb, p).rt); c.ws_D = (const uint64_t *)((char *)ws + ws_layout(pb, p).d); }
   int rc = launch_cycle(c, s, &g_launches);
@@ -262,7 +265,7 @@ static int ideal_impl(const dstack_problem_t *pb, const dstack_params_t *p, cons
     ia.thr_ideal = out->thr_ideal;
     ia.work_ctr = (uint32_t *)((char *)ws + ws_layout(pb, p).ctr) + 2;
     if (!hook) {   // the session's d_j(b) rows and sum R: a per-scenario cost estimate for the heavy-first order
-      ia.dtab_rows = (const uint16_t *)((char *)ws + ws_layout(pb, p).dtab);
+      ia.dstar = (const uint16_t *)((char *)ws + ws_layout(pb, p).dst);
     }
     rc = launch_ideal(ia, (char *)ws + ws_layout(pb, p).ideal, s, &g_launches);
   }
@@ -302,6 +305,7 @@ int dstack_eval_batch(const dstack_problem_t *pb, const dstack_params_t *p, dsta
   std::memset(&a, 0, sizeof(a));
   a.pb = *pb; a.p = *p; a.demand = out->demand; a.batch = out->batch; a.knee = out->knee; a.status = out->status;
   a.dtab_rows = (uint16_t *)((char *)ws + w.dtab);
+  a.dstar = (uint16_t *)((char *)ws + w.dst);
   a.ws_RT = (uint32_t *)((char *)ws + w.rt);
   a.ws_D = (uint64_t *)((char *)ws + w.d);
   a.work_ctr = (uint32_t *)((char *)ws + w.ctr) + 1;   // word 0: k_cycle's counter

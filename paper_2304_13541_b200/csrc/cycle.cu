@@ -122,6 +122,16 @@ __global__ void __launch_bounds__(CYC_WARPS * 32, BK ? DSTACK_CYC_BK_MINB : DSTA
         }
         dtab_from_rows(a.pb, a.p, k0 + j, RT, D, (int32_t)gj, b_lo, (int32_t)bsj, dtab + j * DTAB_ROW, lane);
       }
+      // d_j(b*) per lane: the dense array k_prof wrote, or the row just recomputed (then stored back for a6)
+      uint32_t dst = 0;
+      if (active) {
+        if (need) {
+          dst = dtab[lane * DTAB_ROW + bs - 1];
+          if (a.dstar) a.dstar[k] = (uint16_t)dst;
+        } else {
+          dst = a.dstar[k];
+        }
+      }
       BelowKnee bk;
       const bool use_bk = BK && a.hook_level == nullptr;
       if (use_bk) {
@@ -129,7 +139,7 @@ __global__ void __launch_bounds__(CYC_WARPS * 32, BK ? DSTACK_CYC_BK_MINB : DSTA
         bk.c_slots = ((uint64_t)a.p.reconf_us + (uint64_t)slot - 1) / (uint64_t)slot;
       }
       cr = cycle_core(sm, dtab, lane, active, g, bs, sl, rep, nslots, L, b_lo, a.hook_level != nullptr, runs, served,
-                      0, nullptr, 0, nullptr, 0, nullptr, use_bk ? &bk : nullptr);
+                      0, nullptr, 0, nullptr, 0, nullptr, use_bk ? &bk : nullptr, active ? dst : 0xFFFFFFFFu);
       if (cr.oversub) sst = DSTACK_ST_OVERSUBSCRIBED;
     }
     if (mine) {

@@ -247,7 +247,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
                                             int32_t b_lo, bool hook_b_only, uint32_t &runs, uint32_t &served,
                                             uint32_t count0 = 0, uint64_t *fill_log = nullptr, uint32_t fill_cap = 0,
                                             uint32_t *fill_n = nullptr, int fill_order = 0, uint32_t *busy = nullptr,
-                                            const BelowKnee *bk = nullptr) {
+                                            const BelowKnee *bk = nullptr, uint32_t dstar_in = 0xFFFFFFFFu) {
   // fill_order (O9 comparison schedulers): 0 D-STACK (runs so far), 1 Max-Min fair (smallest g
   // first), 2 max-throughput (shortest d(b*) first); ties by index.  busy (nullable): this lane's run slots.
   CycRes res; res.occ_static = 0; res.occ_all = 0; res.served_tot = 0; res.misses = 0; res.below = 0; res.oversub = false;
@@ -270,7 +270,8 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   }
   joff -= rep;
   const uint32_t njobs = __reduce_add_sync(FULL, rep);
-  const uint32_t dstar = active ? dtab[lane * DSTACK_MAX_BATCH + bs - 1] : 0u;
+  // d_j(b*): given by the caller (dstar_in) or from the dtab row
+  const uint32_t dstar = active ? (dstar_in != 0xFFFFFFFFu ? dstar_in : (uint32_t)dtab[lane * DSTACK_MAX_BATCH + bs - 1]) : 0u;
   uint32_t nextr = 0;
   // ---- static placement in EDF order (Alg. 1 l.5; even repeats Start-Early, odd Start-Late) ----
   for (uint32_t q = 0; q < njobs; ++q) {

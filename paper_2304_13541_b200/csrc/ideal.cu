@@ -418,9 +418,8 @@ __device__ __forceinline__ uint32_t ideal_cost_bucket(const IdealArgs &a, int64_
     if (a.demand[k] == 0) continue;
     const double rows = (double)(a.pb.dnn_row_off[k + 1] - a.pb.dnn_row_off[k]);
     double d = 1.0;
-    if (a.dtab_rows) {
-      const uint32_t b = a.batch[k];
-      const uint32_t v = b ? a.dtab_rows[(int64_t)k * DSTACK_MAX_BATCH + b - 1] : 0u;
+    if (a.dstar) {
+      const uint32_t v = a.batch[k] ? a.dstar[k] : 0u;
       d = v ? (double)v * (double)a.p.slot_us : 1.0;
     }
     est += rows * (double)T / d;

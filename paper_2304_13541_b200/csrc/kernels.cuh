@@ -29,6 +29,7 @@ struct ProfArgs {
   uint8_t *probes;     // dstack_knee_probe (F3): non-NULL => knee = the binary-search result, probes = its steps
   // eval path extras (workspace, may be NULL): d_j(b) at g = demand for b in [b_lo, b*], RT, D
   uint16_t *dtab_rows;
+  uint16_t *dstar;      // d_j(b*) at g = demand, one u16 per DNN (dense: k_cycle's read of it is coalesced)
   uint32_t *ws_RT;
   uint64_t *ws_D;
   uint32_t *work_ctr;   // workspace word: k_prof_fast's DNN-group counter (NULL: contiguous ranges)
@@ -51,7 +52,8 @@ struct CycArgs {
   uint32_t *misses;
   uint32_t *below;         // F1: static jobs placed below the knee
   uint16_t *dtab_rows;     // workspace: num_dnn rows of DTAB_ROW u16
-  const uint32_t *ws_RT;   // non-NULL => dtab_rows already hold d_j(b) at g = demand (from k_prof)
+  uint16_t *dstar;         // workspace: d_j(b*) at the session level per DNN (read when k_prof wrote it, else written)
+  const uint32_t *ws_RT;   // non-NULL => dtab_rows / dstar already hold d_j(b) at g = demand (from k_prof)
   const uint64_t *ws_D;
   uint32_t *work_ctr;      // workspace word: k_cycle's scenario counter (NULL: grid stride)
 };
@@ -86,7 +88,7 @@ struct IdealArgs {
   uint32_t *ex_tau;   // [num_rows] workspace
   double *u_ideal, *thr_ideal;
   uint32_t *work_ctr;   // workspace word: k_ideal_sim's scenario counter (NULL: grid stride)
-  const uint16_t *dtab_rows;   // d_j(b) rows of the session just computed (cost estimate for the order; may be NULL)
+  const uint16_t *dstar;       // d_j(b*) of the session just computed, per DNN (cost estimate for the order; may be NULL)
   const uint32_t *ws_RT;       // sum R per DNN (may be NULL)
   uint32_t *order;             // [num_scen] scenarios, heaviest estimate first (set by launch_ideal)
   uint32_t *bucket_cnt;        // [64] workspace

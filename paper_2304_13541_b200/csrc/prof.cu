@@ -77,6 +77,7 @@ __device__ __forceinline__ void prof_one(const ProfArgs &a, int64_t k, const uin
       dtab_from_tables(a.pb, a.p, k, cA, cU, r.RT, r.D, r.demand, a.p.b_min, r.b, a.dtab_rows + k * DTAB_ROW, lane);
     else
       dtab_from_rows(a.pb, a.p, k, r.RT, r.D, r.demand, a.p.b_min, r.b, a.dtab_rows + k * DTAB_ROW, lane);
+    if (a.dstar && lane == 0) a.dstar[k] = a.dtab_rows[k * DTAB_ROW + r.b - 1];
   }
   if (lane == 0) {
     if (a.ws_RT) { a.ws_RT[k] = (uint32_t)r.RT; a.ws_D[k] = r.D; }
@@ -480,7 +481,10 @@ __global__ void __launch_bounds__(256, DSTACK_PROF_MINB) k_prof_fast(const __gri
         const uint32_t st = (o.sd >> 16) & 0xFFu;
         const bool ok = st == DSTACK_ST_OK;
         if (a.ws_RT) { a.ws_RT[kl] = o.RT; a.ws_D[kl] = o.D; }
-        if (a.dtab_rows && ok) a.dtab_rows[kl * DTAB_ROW] = (uint16_t)(o.sd & 0xFFFFu);
+        if (ok) {   // d_j(1): the dense array on the eval path, else the row's b = 1 entry
+          if (a.dstar) a.dstar[kl] = (uint16_t)(o.sd & 0xFFFFu);
+          else if (a.dtab_rows) a.dtab_rows[kl * DTAB_ROW] = (uint16_t)(o.sd & 0xFFFFu);
+        }
         if (a.knee) a.knee[kl] = ok ? (uint16_t)(o.kd & 0xFFFFu) : 0;
         if (a.status) a.status[kl] = (uint8_t)st;
         if (a.demand) a.demand[kl] = ok ? (uint16_t)(o.kd >> 16) : 0;
