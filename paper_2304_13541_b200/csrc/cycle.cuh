@@ -34,7 +34,7 @@ constexpr uint32_t NONE32 = 0xFFFFFFFFu;
 
 // F1 below-knee fallback context (DSTACK_FLAG_BELOW_KNEE): where the scenario's DNN
 // rows live, so that a static job that found no start at g_j can re-derive its run length at a lower level
-// from O1 (one row pass per level), plus the launch latency in slots.
+// from O1 (32 levels per serial row pass, lanes over levels), plus the launch latency in slots.
 struct BelowKnee {
   const dstack_problem_t *pb;
   const dstack_params_t *p;
@@ -213,17 +213,43 @@ static __device__ __noinline__ uint64_t below_knee_retry(const uint8_t *occ, con
     RT = warp_sum_u64(RT); D = warp_sum_u64(D);
   }
   const uint64_t M = bp.mem_mode == 0 ? 1ull : (uint64_t)bpb.mem_bw[kj];
-  for (int l = gj - 1; l >= 1; --l) {
-    const uint64_t S = (uint64_t)s_of(l, bp.S_tot, bp.L);
-    const uint64_t X = x_from_rows(bpb, bp, kj, RT, D, S, bsj, lane);
-    const uint64_t den = S * M * (uint64_t)bp.slot_us;
-    const uint64_t d64 = (X + den - 1) / den + bk.c_slots;
-    if (d64 > (uint64_t)(dlv - rel)) continue;
-    const int d = (int)d64;
-    const int s = d <= 124 ? ((rj & 1) ? find_late_packed(occ, rel, dlv, d, l, L, lane)
-                                       : find_early_packed(occ, rel, dlv, d, l, L, lane))
-                           : ((rj & 1) ? find_late(occ, rel, dlv, d, l, L, lane) : find_early(occ, rel, dlv, d, l, L, lane));
-    if (s >= 0) return (uint64_t)s | ((uint64_t)d << 16) | ((uint64_t)l << 32);
+  const uint32_t win = (uint32_t)(dlv - rel);   // <= DSTACK_MAX_SLOTS < 0xFFFF: a clamped d never fits
+  // 32 levels at a time, lane i holding level top - i: each lane sums V(S(l)) over all the DNN's rows itself
+  // (the row loads are warp-wide broadcasts), so a chunk costs one serial row pass instead of 32 warp passes
+  // with their reductions; the levels are then tried top-down exactly as one at a time.
+  const int64_t r0 = bpb.dnn_row_off[kj];
+  const int32_t K = (int32_t)(bpb.dnn_row_off[kj + 1] - r0);
+  const uint32_t *nrow = bpb.n + r0;
+  const uint16_t *rrow = bpb.r + r0;
+  const uint64_t t_p = (uint64_t)bpb.t_p[kj], t_np = (uint64_t)bpb.t_np[kj];
+  for (int top = gj - 1; top >= 1; top -= 32) {
+    const int myl = top - lane;
+    uint32_t dl = 0xFFFFFFFFu;
+    if (myl >= 1) {
+      const uint64_t S = (uint64_t)s_of(myl, bp.S_tot, bp.L);
+      uint64_t V = 0;
+#pragma unroll 4
+      for (int i = 0; i < K; ++i) {
+        const uint64_t nn = nrow[i];
+        const uint64_t N = bp.par_mode == 0 ? (uint64_t)bsj * nn : ((uint64_t)bsj * nn + 2047) >> 11;
+        if (N >= 1) V += (uint64_t)rrow[i] * (N > S ? N : S);
+      }
+      uint64_t X = (bp.wse_mode == 0 ? (uint64_t)bsj : 1ull) * t_np * RT * S * M + M * t_p * V;
+      if (bp.mem_mode == 1) X += (uint64_t)bsj * D;
+      else if (bp.mem_mode == 2) X += (uint64_t)bsj * D * S * S;
+      dl = (uint32_t)ceil_div_clamp16(X, S * M * (uint64_t)bp.slot_us) + (uint32_t)bk.c_slots;
+    }
+    uint32_t cand = __ballot_sync(FULL, myl >= 1 && dl <= win);
+    while (cand) {
+      const int i = __ffs(cand) - 1;
+      cand &= cand - 1;
+      const int l = top - i;
+      const int d = (int)__shfl_sync(FULL, dl, i);
+      const int s = d <= 124 ? ((rj & 1) ? find_late_packed(occ, rel, dlv, d, l, L, lane)
+                                         : find_early_packed(occ, rel, dlv, d, l, L, lane))
+                             : ((rj & 1) ? find_late(occ, rel, dlv, d, l, L, lane) : find_early(occ, rel, dlv, d, l, L, lane));
+      if (s >= 0) return (uint64_t)s | ((uint64_t)d << 16) | ((uint64_t)l << 32);
+    }
   }
   return 0;
 }
