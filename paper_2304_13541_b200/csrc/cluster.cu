@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(CLU_WARPS * 32, DSTACK_CLU_MINB) k_cluster(con
       int32_t home3 = -1;
       {
         uint32_t rank = 0;   // (demand desc, index asc) among the active
+#pragma unroll 4
         for (int q = 0; q < 32; ++q) {
           const uint32_t dq = __shfl_sync(FULL, dem, q);
           const bool aq = __shfl_sync(FULL, (int)active, q) != 0;
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(CLU_WARPS * 32, DSTACK_CLU_MINB) k_cluster(con
         while (todo) {
           const int j = __ffs(todo) - 1;
           todo &= todo - 1;
-          dtab_from_rows(a.pb, a.p, k0 + j, shfl_u64(RTl, j), shfl_u64(Dl, j), (int32_t)__shfl_sync(FULL, g, j), b_lo,
+          dtab_lower(a.pb, a.p, k0 + j, shfl_u64(RTl, j), shfl_u64(Dl, j), (int32_t)__shfl_sync(FULL, g, j), b_lo,
                          (int32_t)__shfl_sync(FULL, bs, j) - 1, dtab + j * DTAB_ROW, lane);
         }
         __syncwarp();

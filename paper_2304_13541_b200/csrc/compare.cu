@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(CMP_WARPS * 32, DSTACK_CMP_MINB) k_compare(Cmp
         // one row pass: the sums, X(g, b*), X(L, b*), X(knee, b*); d_j(b) for b < b* (rare) one pass each
         uint64_t RT, D, Vg, VL, Vk;
         rows_pass3(a.pb, a.p, kj, bj, Sg, SL, Sk, RT, D, Vg, VL, Vk, lane);
-        if (bj > b_lo) dtab_from_rows(a.pb, a.p, kj, RT, D, gj, b_lo, bj - 1, dtab + j * DTAB_ROW, lane);
+        if (bj > b_lo) dtab_lower(a.pb, a.p, kj, RT, D, gj, b_lo, bj - 1, dtab + j * DTAB_ROW, lane);
         if (lane == 0)
           dtab[j * DTAB_ROW + bj - 1] = ceil_div_clamp16(x_of_v(a.pb, a.p, kj, RT, D, Sg, bj, Vg), Sg * M * (uint64_t)slot);
         const uint64_t XL = x_of_v(a.pb, a.p, kj, RT, D, SL, bj, VL);
@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(CMP_WARPS * 32, DSTACK_CMP_MINB) k_compare(Cmp
         const uint32_t lv = active ? dem : 0u;
         const uint32_t key = (lv << 5) | (uint32_t)lane;
         uint32_t rank = 0, pre_lt = 0;
+#pragma unroll 4
         for (int q = 0; q < 32; ++q) {   // ascending (level, index) rank among the active models
           const uint32_t kq = __shfl_sync(FULL, key, q);
           const bool aq = __shfl_sync(FULL, (int)active, q) != 0;
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(CMP_WARPS * 32, DSTACK_CMP_MINB) k_compare(Cmp
         const uint32_t pre = __reduce_add_sync(FULL, res ? lv : 0u);
         const bool rest = active && !res;
         uint32_t rank2 = 0;   // (level desc, index asc) among the rest
+#pragma unroll 4
         for (int q = 0; q < 32; ++q) {
           const uint32_t lq = __shfl_sync(FULL, lv, q);
           const bool rq = __shfl_sync(FULL, (int)rest, q) != 0;

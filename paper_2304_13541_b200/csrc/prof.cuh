@@ -516,6 +516,14 @@ __device__ __forceinline__ void dtab_from_rows(const dstack_problem_t &pb, const
   __syncwarp();
 }
 
+// The same out of line, for the kernels that need it only on a rare path (b < b*) and keep their session's
+// instruction stream small (k_compare, k_cluster).
+static __device__ __noinline__ void dtab_lower(const dstack_problem_t &pb, const dstack_params_t &p, int64_t k,
+                                               uint64_t RT, uint64_t D, int32_t g, int32_t b_lo, int32_t b_hi,
+                                               uint16_t *dtab, int lane) {
+  dtab_from_rows(pb, p, k, RT, D, g, b_lo, b_hi, dtab, lane);
+}
+
 __device__ __forceinline__ void fill_stab(uint16_t *Stab, int L, int S_tot) {
   for (int l = threadIdx.x; l <= L; l += blockDim.x) Stab[l] = (uint16_t)s_of(l, S_tot, L);
 }
