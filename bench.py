@@ -797,12 +797,22 @@ def run_sim(args, rank, world, local):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    sampler = ClockSampler(range(world)) if rank == 0 else None
+    if sampler:
+        sampler.start(); time.sleep(0.3)
+    launches = 0
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > L2 (126 MB)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
+        flush.zero_()
         o = run()
+        launches += ds.last_launch_count()
     e1.record()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     tot = torch.stack([o[k].sum() for k in ("arrived", "in_slo", "late", "unserved", "occ_sum", "runs")]).to(torch.float64)
     if world > 1:
@@ -816,7 +826,9 @@ def run_sim(args, rank, world, local):
                 "value": per_gpu * world * args.cycles * args.steps / (ms / 1e3), "unit": "scenario-cycles/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-                "data": "synthetic", "config": {"workload": f"config5: {per_gpu} scenarios/GPU x {args.cycles} cycles"},
+                "data": "synthetic", "config": {"workload": f"config5: {per_gpu} scenarios/GPU x {args.cycles} cycles",
+                                                 "l2": "flushed before every step (256 MB write, inside the timed region)"},
+                "gpu_launches": launches, "clocks": clocks,
                 "stats": {"arrived": arrived, "in_slo_frac": in_slo / max(arrived, 1),
                           "late_frac": late / max(arrived, 1), "unserved_frac": unserved / max(arrived, 1),
                           "mean_u_rank0": float((o["occ_sum"].to(torch.float64) /
