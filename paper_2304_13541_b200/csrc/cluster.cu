@@ -18,7 +18,8 @@ constexpr int CLU_WARPS = 8;
 #define DSTACK_CLU_GRID 64   // grid: blocks per SM (A/B ms: 8 -> 203, 32 -> 201, 64 -> 197)
 #endif
 #ifndef DSTACK_CLU_MINB
-#define DSTACK_CLU_MINB 4   // resident blocks per SM the register allocation targets (A/B: 1 -> 226, 3 -> 223, 4 -> 202 ms)
+#define DSTACK_CLU_MINB 3   // resident blocks per SM the register allocation targets (A/B, current code: 2 -> 89.5,
+                            // 3 -> 81.3, 4 -> 89.8 ms; at 64 registers lane / smem addresses were rematerialised)
 #endif
 
 struct CluArgs {
