@@ -52,7 +52,26 @@ def parse():
     ap.add_argument("--no-knee-probe", action="store_true", help="skip the F3 online knee discovery leg")
     ap.add_argument("--no-cluster", action="store_true", help="skip the F4 multi-GPU cluster leg")
     ap.add_argument("--cluster-gpus", type=int, default=4, help="F4: modelled GPUs per scenario (paper: 4 x T4)")
+    ap.add_argument("--scaling", choices=("strong", "weak"), default="strong",
+                    help="strong: the config's scenarios split over the ranks (BASELINE: '1M scenarios ... sharded "
+                         "over 1/2/4/8 B200'); weak: every rank evaluates the config's size")
+    ap.add_argument("--no-select", action="store_true",
+                    help="config 4: skip the sum(demand)/L in [2, 5] selection (raw generator stream)")
     return ap.parse_args()
+
+
+L2_BYTES = 126 * 2 ** 20   # B200 L2 (B200_PROFILING.md)
+
+
+def shard_of(args, sp0, rank, world):
+    """(spec of this rank's shard, scenarios over all ranks, this rank's scenarios).  Strong scaling: the
+    contiguous global-index shard [g n / G, (g + 1) n / G) (dist.shard); weak: rank g evaluates
+    [g n, (g + 1) n)."""
+    from paper_2304_13541_b200.dist import shard
+    if args.scaling == "weak":
+        return sp0.replace(scen_base=rank * sp0.num_scen), sp0.num_scen * world, sp0.num_scen
+    b, e = shard(sp0.num_scen, rank, world)
+    return sp0.replace(scen_base=b, num_scen=e - b), sp0.num_scen, e - b
 
 
 def dist_env():
@@ -195,6 +214,7 @@ def run_reference(args, rank, world):
     import numpy as np
     import oracle
     import synth
+    args.no_select = True   # the reference arm samples the generator stream as drawn (config 4: unselected)
     n = args.scen or None
     sp, p = synth.config(args.config, num_scen=n, variant=args.variant)
     total = sp.num_scen
@@ -216,7 +236,7 @@ def run_reference(args, rank, world):
               f"{total}-scenario workload; {args.steps} timed steps")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
             "data": "synthetic", "config": workload_config(args, sp, p, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -224,39 +244,61 @@ def run_reference(args, rank, world):
     return 0
 
 
-def workload_config(args, sp, p, world):
+def workload_config(args, sp, p, world, input_bytes=None, flush=False):
+    """The config the line is quoted on.  sp: the config's whole workload (before sharding)."""
+    dnns = ("the paper's C-4 mix (ResNet-50, VGG-19, BERT, MobileNet; P:2670)" if sp.paper_mix else
+            f"{sp.ndnn_min}-{sp.ndnn_max} DNNs each" + (" (heavy shapes)" if sp.heavy else ""))
+    sel = (", selected: sum(demand)/L in [2, 5] by the product's a3 (synth/select.py)"
+           if args.config == 4 and not args.no_select else "")
+    per = sp.num_scen if args.scaling == "weak" else sp.num_scen // world
+    tot = sp.num_scen * (world if args.scaling == "weak" else 1)
+    if input_bytes is None:
+        l2 = None
+    elif flush:
+        l2 = (f"inputs ({input_bytes / 1e6:.0f} MB per GPU) fit in L2 ({L2_BYTES / 2 ** 20:.0f} MB): L2 flushed before "
+              f"every step by a 256 MB write inside the timed region")
+    else:
+        l2 = f"inputs ({input_bytes / 1e9:.2f} GB per GPU) larger than L2 ({L2_BYTES / 2 ** 20:.0f} MB): no flush"
     return {"workload": f"config{args.config}" + ("" if args.variant == "default" else f"-{args.variant}") +
-            f": {sp.num_scen} scenarios/GPU, {sp.ndnn_min}-{sp.ndnn_max} DNNs each, L={p.L}, S_tot={p.S_tot}, "
+            f": {tot} scenarios ({args.scaling} scaling, ~{per} per GPU), {dnns}{sel}, L={p.L}, S_tot={p.S_tot}, "
             f"batches {p.b_min}-{p.b_max}, slot {p.slot_us} us, mem_mode={p.mem_mode}, par_mode={p.par_mode}, "
             f"wse_mode={p.wse_mode}, ideal={'on' if p.ideal else 'off'}",
-            "scenarios_per_gpu": sp.num_scen, "global_scenarios": sp.num_scen * world,
-            "parallelism": f"dp{world} (scenario shards)", "l2": "inputs larger than L2 (no flush)"}
+            "scenarios_per_gpu": per, "global_scenarios": tot,
+            "parallelism": f"dp{world} (scenario shards, no data-path collective)", "l2": l2}
 
 
 # ------------------------------------------------------------------ native ---
-def cpu_baseline(args, sp, p):
-    import oracle
+def draw(sp, idx, idx_map=None):
+    """Host re-draw of workload scenarios idx (positions in the workload; idx_map: their global indices when the
+    workload is a selection, config 4)."""
     import synth
+    if idx_map is None:
+        return synth.sample(sp, idx)
+    return synth.sample(sp.replace(scen_base=0), [int(idx_map[i]) for i in idx])
+
+
+def cpu_baseline(args, sp, p, idx_map=None):
+    import oracle
     cores = host_cores()
     total = sp.num_scen
     chunk, done, el, k = 32, 0, 0.0, 0
     stride = max(1, total // 4096)
     while el < args.cpu_seconds and done < 4096:
         idx = [((k * chunk + i) * stride) % total for i in range(chunk)]
-        pb = synth.sample(sp, idx)
+        pb = draw(sp, idx, idx_map)
         t0 = time.perf_counter()
         oracle.evaluate(pb, p, nthreads=cores)
         el += time.perf_counter() - t0
         done += chunk; k += 1
     return {"value": done / el, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{done} scenarios (every {stride}th of the config-{args.config} workload), "
-                      f"{el:.1f} s wall on {cores} host threads (OpenMP over scenarios)"}
+            "sample": (f"{done} scenarios (every {stride}th of the config-{args.config} workload)" if total > 1 else
+                       f"the config-{args.config} scenario evaluated {done} times") +
+                      f", {el:.1f} s wall on {cores} host threads (OpenMP over scenarios)"}
 
 
-def oracle_leg(args, sp, what, call, seconds=2.0, unit=UNIT, per_dnn=False, max_scen=1024):
+def oracle_leg(args, sp, what, call, seconds=2.0, unit=UNIT, per_dnn=False, max_scen=1024, idx_map=None):
     """The CPU oracle of a next-row leg timed beside it (test infrastructure; rank 0, N = 1): `call(pb, cores)` on
     stratified samples of the workload for about `seconds` of host time; units = scenarios (or DNNs)."""
-    import synth
     cores = host_cores()
     total = sp.num_scen
     chunk, done, units, el, k = 16, 0, 0, 0.0, 0
@@ -264,7 +306,7 @@ def oracle_leg(args, sp, what, call, seconds=2.0, unit=UNIT, per_dnn=False, max_
     wall0 = time.perf_counter()
     while el < seconds and done < max_scen and time.perf_counter() - wall0 < 4 * seconds:
         idx = [((k * chunk + i) * stride) % total for i in range(chunk)]
-        pb = synth.sample(sp, idx)
+        pb = draw(sp, idx, idx_map)
         t0 = time.perf_counter()
         call(pb, cores)
         el += time.perf_counter() - t0
@@ -299,30 +341,57 @@ def algorithmic_bytes(dp, args, out=None):
     return {"k_prof": prof, "k_wmaxmin": wmm, "k_cycle": cyc, "k_ideal": rows, "k_agg": agg, "path": path}
 
 
+def prepare_workload(args, p, dev, rank, world, ds):
+    """This rank's device problem.  Returns (g, sp0, n_total, n_rank, idx_map, select_stats, chunk_fn):
+    sp0 = the config's whole workload spec; idx_map = global indices of the workload's scenarios when it is a
+    selection (config 4), else None; chunk_fn(s0, cnt) = device dict of the rank's scenarios [s0, s0 + cnt)."""
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_2304_13541_b200.dist import shard
+    sp0, _ = synth.config(args.config, num_scen=args.scen or None, variant=args.variant)
+    if args.config == 4 and not args.no_select:
+        from synth.select import _gather, select_by_demand_ratio
+        need = sp0.num_scen * (world if args.scaling == "weak" else 1)
+        b, e = (rank * sp0.num_scen, (rank + 1) * sp0.num_scen) if args.scaling == "weak" else shard(need, rank, world)
+        a3 = lambda gg: ds.batch_opt(ds.from_device_dict(gg), p)["demand"]   # the product's a3 decides
+        glob, g, stats = select_by_demand_ratio(sp0.replace(scen_base=0), p.L, a3, need, gather_range=(b, e), device=dev)
+        torch.cuda.synchronize()
+        chunk = lambda s0, cnt: _gather(g, torch.arange(s0, s0 + cnt, device=dev), dev)
+        return g, sp0, need, e - b, glob, stats, chunk
+    sp, n_total, n_rank = shard_of(args, sp0, rank, world)
+    g = synth.generate_device(sp, dev)
+    chunk = lambda s0, cnt: synth.generate_device(sp.replace(scen_base=sp.scen_base + s0, num_scen=cnt), dev)
+    return g, sp0, n_total, n_rank, None, None, chunk
+
+
 def run_native(args, rank, world, local):
     import torch
     import torch.distributed as dist
 
-    import synth
     from paper_2304_13541_b200 import dstack as ds
     from paper_2304_13541_b200.dist import allreduce_agg
+    import synth
 
     dev = bench_device(local)
     torch.cuda.set_device(dev)
     if world > 1:
         init_dist(dev)
-    n = args.scen or None
-    sp0, p = synth.config(args.config, num_scen=n, variant=args.variant)
-    per_gpu = sp0.num_scen
-    sp = sp0.replace(scen_base=rank * per_gpu)
-    g = synth.generate_device(sp, dev)
+    _, p = synth.config(args.config, variant=args.variant)
+    g, sp0, n_total, n_rank, idx_map, sel_stats, chunk_fn = prepare_workload(args, p, dev, rank, world, ds)
     dp = ds.from_device_dict(g)
     out = ds.alloc_outputs(dp, agg=True)
     ws = ds.Workspace(ds.workspace_size(dp, p), dev)
     stream = torch.cuda.current_stream(dev)
+    input_bytes = dp.num_rows * 10 + dp.num_dnn * 32 + dp.num_scen * 4
+    flush = input_bytes < 2 * L2_BYTES   # small inputs would be served from L2: flush before every step
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
     launches = [0]
 
     def step():
+        if flush_buf is not None:
+            flush_buf.zero_()
         ds.eval_batch(dp, p, out=out, ws=ws); launches[0] += ds.last_launch_count()   # a1-a5 (+a6) + a8
         if world > 1:
             allreduce_agg(out["agg"])   # the one collective: ~2.8 KB aggregate struct, NCCL over NVLink
@@ -354,35 +423,36 @@ def run_native(args, rank, world, local):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = per_gpu * world * args.steps / (ms_max / 1e3)
+    value = n_total * args.steps / (ms_max / 1e3)
     agg = ds.agg_to_dict(out["agg"])
+    legs = dict(n_rank=n_rank, n_total=n_total, idx_map=idx_map)
 
     # ---- O9 comparison schedulers (dstack_compare) on this step's a3/a4 outputs, timed separately ----
     cmp_line = None
     if not args.no_compare:
-        cmp_line = run_compare_leg(args, ds, dp, p, out, ws, stream, per_gpu, world)
+        cmp_line = run_compare_leg(args, ds, dp, p, out, ws, stream, world, **legs)
 
     # ---- F1 below-knee fallback (DSTACK_FLAG_BELOW_KNEE) on the same inputs, timed separately ----
     bk_line = None
     if not args.no_below_knee:
-        bk_line = run_below_knee_leg(args, ds, dp, p, out, stream, per_gpu, world)
+        bk_line = run_below_knee_leg(args, ds, dp, p, out, stream, world, **legs)
 
     # ---- F4 multi-GPU cluster policies of §7.1 (dstack_cluster) on this step's a3 outputs, timed separately ----
     clu_line = None
     if not args.no_cluster:
-        clu_line = run_cluster_leg(args, ds, dp, p, out, ws, stream, per_gpu, world)
+        clu_line = run_cluster_leg(args, ds, dp, p, out, ws, stream, world, **legs)
 
     # ---- F3 online knee discovery (dstack_knee_probe) over every DNN of the shard, timed separately ----
     kp_line = None
     if not args.no_knee_probe:
-        kp_line = run_knee_probe_leg(args, ds, dp, p, stream, world)
+        kp_line = run_knee_probe_leg(args, ds, dp, p, stream, world, **legs)
 
-    # ---- e2e: the public API from pinned host buffers, H2D + compute + D2H of results each step ----
-    e2e = e2e_wide = None
+    # ---- e2e: the public API from pinned host buffers, H2D + compute + D2H of every result, each step ----
+    e2e = e2e_compact = None
     if not args.no_e2e:
-        e2e = run_e2e(args, sp, p, dev, world, "w5")
-        if world == 1 and e2e.get("transport", "").startswith("compact"):
-            e2e_wide = run_e2e(args, sp, p, dev, world, "wide")   # the same path with the rows sent wide
+        e2e = run_e2e(args, n_rank, n_total, p, dev, world, chunk_fn, out, "wide")
+        if world == 1:
+            e2e_compact = run_e2e(args, n_rank, n_total, p, dev, world, chunk_fn, out, "w5")
 
     if rank != 0:
         if world > 1:
@@ -391,39 +461,52 @@ def run_native(args, rank, world, local):
     ab = algorithmic_bytes(dp, args, out)
     peak, peak_src = hbm_peak()
     cnt = kernel_counters(args.config)
+    step_s = ms_max / args.steps / 1e3
 
     def kernel_roofline(name):
-        """The kernel's binding roofline: issue slots (ALU-bound; executed warp instructions per launch from
-        the committed ncu counters / live launch time) with its HBM roofline (algorithmic bytes) beside it."""
+        """Per kernel: its HBM roofline (algorithmic bytes / live launch time) and, where ncu counted it, its
+        issue-slot use (executed warp instructions per launch / live launch time) -- a diagnostic of how busy the
+        kernel keeps the schedulers, not a fraction of the method's work."""
         sec = kern[name] / 1e3
         hbm_ach = ab[name] / sec / 1e9
         c = cnt.get(name)
-        traffic = c["dram_bytes"] * per_gpu if c else None
-        hbm = {"algorithmic_bytes_per_launch": ab[name], "achieved": hbm_ach, "peak": peak, "unit": "GB/s",
-               "frac": hbm_ach / peak, "traffic": traffic, "peak_source": peak_src}
-        if not c:
-            return dict({"bound": "hbm", "kernel": name}, **hbm)
-        ipk, ipk_src = issue_peak()
-        inst = c["warp_inst"] * per_gpu
-        ach = inst / sec / 1e9
-        if hbm["frac"] > ach / ipk:                 # the resource closer to saturation is the bound
-            return dict({"bound": "hbm", "kernel": name, "issue": {"achieved": ach, "peak": ipk, "frac": ach / ipk}}, **hbm)
-        return {"bound": "alu", "kernel": name, "achieved": ach, "peak": ipk, "unit": "Gwarp-inst/s",
-                "frac": ach / ipk, "traffic": traffic, "peak_source": ipk_src,
-                "counted": f"ncu smsp__inst_executed.sum per launch = {inst:.4g} (profiles/counters.json)",
-                "hbm": hbm}
+        r = {"bound": "hbm", "kernel": name, "algorithmic_bytes_per_launch": ab[name], "achieved": hbm_ach,
+             "peak": peak, "unit": "GB/s", "frac": hbm_ach / peak,
+             "traffic": c["dram_bytes"] * n_rank if c else None, "peak_source": peak_src}
+        if c:
+            ipk, ipk_src = issue_peak()
+            inst = c["warp_inst"] * n_rank
+            r["issue"] = {"achieved": inst / sec / 1e9, "peak": ipk, "unit": "Gwarp-inst/s", "frac": inst / sec / 1e9 / ipk,
+                          "warp_inst_per_scenario": c["warp_inst"], "peak_source": ipk_src}
+        return r
 
     dom_name = max(kern, key=kern.get)          # the kernel with the largest share of the step
+    path_kernels = [k for k in ("k_prof", "k_wmaxmin", "k_cycle", "k_agg") if k in cnt]
+    path_traffic = sum(cnt[k]["dram_bytes"] for k in path_kernels) * n_rank if len(path_kernels) == 4 else None
+    path_ach = ab["path"] / step_s / 1e9
+    roofline = {"bound": "hbm", "kernel": "whole path per step (k_prof + k_wmaxmin + k_cycle + k_agg)",
+                "achieved": path_ach, "peak": peak, "unit": "GB/s", "frac": path_ach / peak, "traffic": path_traffic,
+                "algorithmic_bytes_per_step": ab["path"], "peak_source": peak_src,
+                "bytes_rule": "every row once (10 B) + DNN headers + per-DNN / per-scenario outputs once (DESIGN.md §6)",
+                "dominant_kernel": dom_name}
+    budget = None
+    if cnt:
+        mhz = issue_peak()[0] / (148 * 4) * 1e3
+        t60 = ab["path"] / (0.6 * peak * 1e9)
+        per = {k: v["warp_inst"] for k, v in cnt.items()}
+        budget = {"target_warp_inst_per_scenario": 148 * 4 * mhz * 1e6 * t60 / max(n_rank, 1),
+                  "target_rule": "issue slots of one B200 (148 SM x 4 SMSP x clock) during the step that 60 % of HBM "
+                                 "would allow (algorithmic bytes / (0.6 x peak)), per scenario (SURVEY §8(d): ~4.2k)",
+                  "warp_inst_per_scenario": per, "total": sum(per.values()),
+                  "counted": "ncu smsp__inst_executed.sum per launch / scenarios (profiles/counters.json)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "int64", "data": "synthetic (seeded Philox generator, SURVEY §8(d) recipe)",
-        "config": workload_config(args, sp0, p, world),
-        "roofline": kernel_roofline(dom_name),
+        "config": workload_config(args, sp0, p, world, input_bytes, flush),
+        "roofline": roofline,
+        "budget": budget,
         "roofline_by_kernel": {k: kernel_roofline(k) for k in kern},
-        "path_roofline": {"algorithmic_bytes_per_step": ab["path"],
-                          "achieved_GBps": ab["path"] / (ms_max / args.steps / 1e3) / 1e9,
-                          "frac": ab["path"] / (ms_max / args.steps / 1e3) / 1e9 / peak},
         # SURVEY §8(d): a1-a4 alone (k_prof + k_wmaxmin) as the HBM-bound sub-path, algorithmic bytes / their time
         "a1_a4_subpath": ({"ms": kern["k_prof"] + kern["k_wmaxmin"],
                            "algorithmic_bytes": ab["k_prof"] + ab["k_wmaxmin"],
@@ -434,27 +517,62 @@ def run_native(args, rank, world, local):
         "gpu_launches": launches[0],
         "clocks": clocks,
         "e2e": e2e,
-        "e2e_wide_rows": e2e_wide,
+        "e2e_compact_rows": e2e_compact,
         "compare": cmp_line,
         "below_knee": bk_line,
         "knee_probe": kp_line,
         "cluster": clu_line,
+        "selection": sel_stats,
         "stats": {"mean_u": agg["sum_u"] / max(agg["n_scen_scheduled"], 1),
                   "mean_u_static": agg["sum_u_static"] / max(agg["n_scen_scheduled"], 1),
+                  "mean_u_ideal": agg["sum_u_ideal"] / max(agg["n_scen_scheduled"], 1) if p.ideal else None,
                   "scen_status": agg["n_scen_st"], "dnn_status": agg["n_st"],
                   "bstar_hist_nonzero": {str(b): c for b, c in enumerate(agg["batch_hist"]) if c},
                   "rows_per_gpu": dp.num_rows, "dnns_per_gpu": dp.num_dnn,
-                  "raised_dnns_rows": list(raised_rows(dp, out)), "checksum": agg["checksum"]},
+                  "raised_dnns_rows": list(raised_rows(dp, out)), "checksum_rank0": agg["checksum"]},
     }
+    if sel_stats is not None:   # realised oversubscription of the selected workload (this rank's shard)
+        import numpy as np
+        from synth.select import RATIO_BINS
+        dem = out["demand"][: dp.num_dnn].to(torch.int64)
+        cs = torch.zeros(dem.numel() + 1, dtype=torch.int64, device=dev)
+        cs[1:] = torch.cumsum(dem, 0)
+        off = dp.scen_dnn_off.to(torch.int64)
+        ratio = ((cs[off[1:]] - cs[off[:-1]]).to(torch.float64) / p.L).cpu().numpy()
+        sel_stats["ratio_hist_selected"] = np.histogram(ratio, bins=RATIO_BINS)[0].tolist()
+        sel_stats["selected_frac_in_2_5"] = float(((ratio >= 2) & (ratio <= 5)).mean())
+    if ncalls and p.ideal and "k_ideal" in kern:
+        line["ideal_events"] = ideal_event_stats(args, ds, dp, p, ws, kern["k_ideal"])
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, sp0, p)
+        line["cpu_baseline"] = cpu_baseline(args, sp0, p, idx_map)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
-def run_compare_leg(args, ds, dp, p, out, ws, stream, per_gpu, world):
+def ideal_event_stats(args, ds, dp, p, ws, ms_ideal):
+    """a6 work of the last timed call (dstack_ideal_stats): events (completion intervals) per scenario, how
+    each re-selection was decided, and the device time per event; with ncu counters for this config
+    (profiles/counters.json "ideal_by_config"), warp instructions per event."""
+    st = ds.ideal_stats(dp, p, ws)
+    ev, nsc = max(st["events"], 1), max(st["scenarios"], 1)
+    r = {"counters": st, "events_per_scenario": st["events"] / nsc,
+         "reselection_frac": st["reselections"] / ev,
+         "k_ideal_ms_per_100k_scenarios": ms_ideal * 1e5 / max(dp.num_scen, 1),
+         "ns_per_event": ms_ideal * 1e6 / ev, "api": "paper_2304_13541_b200.dstack.ideal_stats (dstack_ideal_stats)"}
+    try:
+        with open(os.path.join(ROOT, "profiles", "counters.json")) as f:
+            c = json.load(f).get("ideal_by_config", {}).get(str(args.config))
+        if c:
+            r["warp_inst_per_event"] = c["warp_inst_per_scenario"] * nsc / ev
+            r["warp_inst_source"] = c.get("_source")
+    except Exception:
+        pass
+    return r
+
+
+def run_compare_leg(args, ds, dp, p, out, ws, stream, world, n_rank, n_total, idx_map):
     """SURVEY §8(f) item 2 measured: dstack_compare over the whole workload (five schedulers per scenario),
     device-timed with CUDA events; reports the per-scheduler means that reproduce §6.3's comparisons."""
     import torch
@@ -481,15 +599,16 @@ def run_compare_leg(args, ds, dp, p, out, ws, stream, per_gpu, world):
     orc = None
     if world == 1 and not args.no_cpu_baseline:
         import oracle
-        orc = oracle_leg(args, sp_of(args), "oracle.compare", lambda pb, c: oracle.compare(pb, p, nthreads=c))
+        orc = oracle_leg(args, sp_of(args), "oracle.compare", lambda pb, c: oracle.compare(pb, p, nthreads=c),
+                         idx_map=idx_map)
     return {"api": "paper_2304_13541_b200.dstack.compare (dstack_compare)", "ms_per_call": ms,
-            "roofline": leg_roofline(args, "k_compare", ms, per_gpu), "cpu_oracle": orc,
-            "scenarios_per_s": per_gpu * world / (ms / 1e3), "gpu_launches": ds.last_launch_count(),
+            "roofline": leg_roofline(args, "k_compare", ms, n_rank), "cpu_oracle": orc,
+            "scenarios_per_s": n_total / (ms / 1e3), "gpu_launches": ds.last_launch_count(),
             "schedulers": list(ds.CMP_NAMES), "means_over_scheduled_scenarios": means,
             "dstack_throughput_ratio": {k: d / means[k]["thr"] for k in ds.CMP_NAMES if means[k]["thr"] > 0}}
 
 
-def run_below_knee_leg(args, ds, dp, p, out, stream, per_gpu, world):
+def run_below_knee_leg(args, ds, dp, p, out, stream, world, n_rank, n_total, idx_map):
     """SURVEY §8(f) item 1 measured: dstack_eval_batch with DSTACK_FLAG_BELOW_KNEE (unplaced static jobs retried
     below the knee) over the whole workload, device-timed; misses and utilisation beside the
     default path's (this step's `out`)."""
@@ -521,16 +640,16 @@ def run_below_knee_leg(args, ds, dp, p, out, stream, per_gpu, world):
     if world == 1 and not args.no_cpu_baseline:
         import oracle
         orc = oracle_leg(args, sp_of(args), "oracle.evaluate with below_knee",
-                         lambda pb, c: oracle.evaluate(pb, q, nthreads=c))
+                         lambda pb, c: oracle.evaluate(pb, q, nthreads=c), idx_map=idx_map)
     return {"cpu_oracle": orc, "api": "paper_2304_13541_b200.dstack.eval_batch (dstack_eval_batch, DSTACK_FLAG_BELOW_KNEE)",
-            "reconf_us": q.reconf_us, "ms_per_call": ms, "scenarios_per_s": per_gpu * world / (ms / 1e3),
-            "k_cycle_ms": cyc_ms, "roofline": leg_roofline(args, "k_cycle_bk", cyc_ms, per_gpu),
+            "reconf_us": q.reconf_us, "ms_per_call": ms, "scenarios_per_s": n_total / (ms / 1e3),
+            "k_cycle_ms": cyc_ms, "roofline": leg_roofline(args, "k_cycle_bk", cyc_ms, n_rank),
             "below_knee_runs": int(o["below"].sum().item()), "misses": a1["misses"], "misses_default": a0["misses"],
             "oversubscribed_scenarios": a1["n_scen_st"][4], "oversubscribed_default": a0["n_scen_st"][4],
             "mean_u": a1["sum_u"] / n1, "mean_u_default": a0["sum_u"] / n0}
 
 
-def run_cluster_leg(args, ds, dp, p, out, ws, stream, per_gpu, world):
+def run_cluster_leg(args, ds, dp, p, out, ws, stream, world, n_rank, n_total, idx_map):
     """SURVEY §8(f) item 4 measured: dstack_cluster (exclusive / temporal / D-STACK replicas / D-STACK with FFD
     placement on --cluster-gpus modelled GPUs) over the whole workload, device-timed; the means
     reproduce §7.1's comparison (the paper: D-STACK +160% over temporal on 4 T4s)."""
@@ -557,15 +676,16 @@ def run_cluster_leg(args, ds, dp, p, out, ws, stream, per_gpu, world):
     orc = None
     if world == 1 and not args.no_cpu_baseline:
         import oracle
-        orc = oracle_leg(args, sp_of(args), "oracle.cluster", lambda pb, c: oracle.cluster(pb, p, G, nthreads=c))
+        orc = oracle_leg(args, sp_of(args), "oracle.cluster", lambda pb, c: oracle.cluster(pb, p, G, nthreads=c),
+                         idx_map=idx_map)
     return {"api": "paper_2304_13541_b200.dstack.cluster (dstack_cluster)", "gpus_modelled": G, "ms_per_call": ms,
-            "roofline": leg_roofline(args, "k_cluster", ms, per_gpu), "cpu_oracle": orc,
-            "scenarios_per_s": per_gpu * world / (ms / 1e3), "policies": list(ds.CLU_NAMES),
+            "roofline": leg_roofline(args, "k_cluster", ms, n_rank), "cpu_oracle": orc,
+            "scenarios_per_s": n_total / (ms / 1e3), "policies": list(ds.CLU_NAMES),
             "means_over_scheduled_scenarios": means,
             "throughput_vs_temporal": {k: means[k]["thr"] / tt for k in ds.CLU_NAMES} if tt > 0 else None}
 
 
-def run_knee_probe_leg(args, ds, dp, p, stream, world):
+def run_knee_probe_leg(args, ds, dp, p, stream, world, n_rank, n_total, idx_map):
     """SURVEY §8(f) item 3 measured: dstack_knee_probe (binary search from 30%) at b = 1 over every
     DNN, device-timed, with the fraction of DNNs whose probed knee equals Eq. 6's exact knee (dstack_knee)."""
     import torch
@@ -592,51 +712,54 @@ def run_knee_probe_leg(args, ds, dp, p, stream, world):
     if world == 1 and not args.no_cpu_baseline:
         import oracle
         orc = oracle_leg(args, sp_of(args), "oracle.knee_probe at b = 1",
-                         lambda pb, c: oracle.knee_probe(pb, p, 1), unit="DNNs/s", per_dnn=True, max_scen=65536)
+                         lambda pb, c: oracle.knee_probe(pb, p, 1), unit="DNNs/s", per_dnn=True, max_scen=65536,
+                         idx_map=idx_map)
     return {"cpu_oracle": orc, "api": "paper_2304_13541_b200.dstack.knee_probe (dstack_knee_probe)", "batch": 1, "ms_per_call": ms,
             "roofline": leg_roofline(args, "k_knee_probe", ms, dp.num_scen),
-            "dnns_per_s": dp.num_dnn * world / (ms / 1e3), "dnns_ok": n_ok,
+            "dnns_per_s": dp.num_dnn * n_total / max(n_rank, 1) / (ms / 1e3), "dnns_ok": n_ok,
             "exact_knee_match_frac": match / max(n_ok, 1),
             "mean_steps": float(pr[ok].float().mean().item()) if n_ok else 0.0,
             "max_steps": int(pr.max().item()) if dp.num_dnn else 0}
 
 
-def run_e2e(args, sp, p, dev, world, mode="w5"):
-    """End-to-end through the public API: per step, every chunk's inputs are copied host->device from
-    pinned memory (copy stream, double-buffered), evaluated with dstack_eval_batch, and its per-scenario
-    results copied back device->host.  Device-timed with CUDA events (max over ranks).
-    mode: how the rows travel -- "w5" 5 B/row (dstack_unpack_w5), "nr" 6 B/row (dstack_unpack_nr), "wide" 10 B/row;
-    the compact modes expand the rows on the device inside the timed region and fall back to the next wider mode
-    when some row does not fit them."""
+E2E_RES_SCEN = (("scen_status", "torch.uint8"), ("T_us", "torch.int32"), ("u_static", "torch.float64"),
+                ("u", "torch.float64"), ("thr", "torch.float64"), ("misses", "torch.int32"),
+                ("u_ideal", "torch.float64"), ("thr_ideal", "torch.float64"))
+E2E_RES_DNN = (("demand", "torch.int16"), ("batch", "torch.uint8"), ("knee", "torch.int16"), ("status", "torch.uint8"),
+               ("alloc_q16", "torch.int32"), ("level", "torch.int16"), ("runs", "torch.int16"), ("served", "torch.int32"))
+
+
+def run_e2e(args, n_rank, n_total, p, dev, world, chunk_fn, ref_out, mode="wide"):
+    """End-to-end through the public API: per step, every chunk's inputs are copied host->device from pinned
+    memory (copy stream, double-buffered), evaluated with dstack_eval_batch, and ALL its results -- per-scenario
+    (status, T, U_static, U, throughput, misses, U_ideal, throughput_ideal) and per-DNN (demand, batch, knee, status,
+    alloc, level, runs, served) -- plus the aggregate copied device->host.  Device-timed with CUDA events (max over
+    ranks).  mode "wide": the ABI's own row layout (n u32 + R u16 + d u32, 10 B/row) -- the headline e2e;
+    "w5": a compact 5 B/row transport expanded on the device by dstack_unpack_w5 inside the timed region (only when
+    every row fits it; the packing itself is done once, outside the timed region, so it is reported separately).
+    After timing, chunk 0's host results are compared with the device-resident run's (`check`)."""
     import torch
 
-    import synth
-
     nch = max(1, args.e2e_chunks)
-    per = (sp.num_scen + nch - 1) // nch
+    per = (n_rank + nch - 1) // nch
     hdr_fields = ("scen_dnn_off", "dnn_row_off", "t_p", "t_np", "mem_bw", "slo_us", "asm_us", "bmax")
     prob_fields = hdr_fields + ("n", "r", "d")
     host_chunks = []
     try:
         for c in range(nch):
             s0 = c * per
-            cnt = min(per, sp.num_scen - s0)
+            cnt = min(per, n_rank - s0)
             if cnt <= 0:
                 break
-            g = synth.generate_device(sp.replace(scen_base=sp.scen_base + s0, num_scen=cnt), dev)
-            R = int(g["dnn_row_off"][-1].item())
-            nn = g["n"][:R].to(torch.int64) & 0xFFFFFFFF
-            rr = g["r"][:R].to(torch.int64) & 0xFFFF
-            dd = g["d"][:R].to(torch.int64) & 0xFFFFFFFF
-            nmax, rmin, rmax, dmax = (int(nn.max()), int(rr.min()), int(rr.max()), int(dd.max())) if R else (0, 1, 1, 0)
-            fits = {"w5": nmax < 4096 and rmin >= 1 and rmax <= 4 and dmax < (1 << 26),
-                    "nr": nmax < 4096 and rmin >= 1 and rmax <= 15, "wide": True}
-            if not fits[mode]:
-                del g, nn, rr, dd
-                host_chunks.clear()
-                return run_e2e(args, sp, p, dev, world, "nr" if mode == "w5" else "wide")
+            g = chunk_fn(s0, cnt)
             fields = hdr_fields
             if mode == "w5":
+                R = int(g["dnn_row_off"][-1].item())
+                nn = g["n"][:R].to(torch.int64) & 0xFFFFFFFF
+                rr = g["r"][:R].to(torch.int64) & 0xFFFF
+                dd = g["d"][:R].to(torch.int64) & 0xFFFFFFFF
+                if R and not (int(nn.max()) < 4096 and int(rr.min()) >= 1 and int(rr.max()) <= 4 and int(dd.max()) < (1 << 26)):
+                    return None   # some row does not fit the compact transport
                 pad = g["d"].numel()
                 w = torch.zeros(pad, dtype=torch.int64, device=dev)
                 w[:R] = dd | ((rr - 1) << 26) | ((nn >> 8) << 28)
@@ -644,26 +767,20 @@ def run_e2e(args, sp, p, dev, world, mode="w5"):
                 lo = torch.zeros(pad, dtype=torch.uint8, device=dev)
                 lo[:R] = (nn & 255).to(torch.uint8)
                 g["lo"] = lo
-                del w
+                del w, nn, rr, dd
                 fields += ("w", "lo")
-            elif mode == "nr":
-                nr = torch.zeros(g["r"].numel(), dtype=torch.int16, device=dev)
-                nr[:R] = (nn | (rr << 12)).to(torch.int32).to(torch.int16)
-                g["nr"] = nr
-                fields += ("nr", "d")
             else:
                 fields += ("n", "r", "d")
-            del nn, rr, dd
             # straight into pinned host buffers (no pageable intermediate: 8 ranks x several GB of rows on one host)
             host_chunks.append({k: torch.empty(g[k].shape, dtype=g[k].dtype, pin_memory=True).copy_(g[k])
                                 for k in fields})
             del g
     except RuntimeError as e:
         return {"value": None, "unit": UNIT, "error": f"pinned host staging failed: {e}"[:200]}
-    return _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, mode)
+    return _e2e_timed(args, n_total, p, dev, world, host_chunks, prob_fields, mode, ref_out)
 
 
-def _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, mode):
+def _e2e_timed(args, n_total, p, dev, world, host_chunks, prob_fields, mode, ref_out):
     import torch
     import torch.distributed as dist
 
@@ -680,68 +797,62 @@ def _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, mode):
     def dev_max():
         b = {k: torch.empty(max(hc[k].numel() for hc in host_chunks), dtype=host_chunks[0][k].dtype, device=dev)
              for k in tfields}
-        if mode != "wide":
+        if mode == "w5":
             b["n"] = torch.empty(maxrows + 16, dtype=torch.int32, device=dev)
             b["r"] = torch.empty(maxrows + 16, dtype=torch.int16, device=dev)
-        if mode == "w5":
             b["d"] = torch.empty(maxrows + 16, dtype=torch.int32, device=dev)
         return b
     bufs = [dev_max(), dev_max()]
-    res_fields = ("scen_status", "u_static", "u", "thr", "misses")
+    dt = {k: getattr(torch, t.split(".")[1]) for k, t in E2E_RES_SCEN + E2E_RES_DNN}
     h2d = sum(v.numel() * v.element_size() for hc in host_chunks for v in hc.values())
-    d2h = 0
     host_res = []
     for hc in host_chunks:
-        S = hc["scen_dnn_off"].numel() - 1
-        host_res.append({k: torch.empty(S, dtype=t, pin_memory=True) for k, t in
-                         (("scen_status", torch.uint8), ("u_static", torch.float64), ("u", torch.float64),
-                          ("thr", torch.float64), ("misses", torch.int32))})
-        d2h += sum(v.numel() * v.element_size() for v in host_res[-1].values())
-    d2h += ds.AGG_WORDS * 8 * len(host_chunks)
+        S, D = hc["scen_dnn_off"].numel() - 1, hc["dnn_row_off"].numel() - 1
+        host_res.append({k: torch.empty(S if (k, t) in E2E_RES_SCEN else D, dtype=dt[k], pin_memory=True)
+                         for k, t in E2E_RES_SCEN + E2E_RES_DNN})
+    d2h = sum(v.numel() * v.element_size() for hr in host_res for v in hr.values()) + ds.AGG_WORDS * 8 * len(host_chunks)
     agg_host = torch.empty(ds.AGG_WORDS * len(host_chunks), dtype=torch.int64, pin_memory=True)
-    # one workspace for the largest chunk
-    ws_bytes = 0
+    ws_bytes = 0   # one workspace for the largest chunk
     for hc in host_chunks:
         dpc = ds.DeviceProblem(hc["scen_dnn_off"].numel() - 1, hc["dnn_row_off"].numel() - 1,
                                int(hc["dnn_row_off"][-1]), *[bufs[0][k] for k in prob_fields])
         ws_bytes = max(ws_bytes, ds.workspace_size(dpc, p))
     ws = ds.Workspace(ws_bytes, dev)
-    # two output sets for the largest chunk
     maxS = max(hc["scen_dnn_off"].numel() - 1 for hc in host_chunks)
     maxD = max(hc["dnn_row_off"].numel() - 1 for hc in host_chunks)
     dmax = ds.DeviceProblem(maxS, maxD, 0, *[bufs[0][k] for k in prob_fields])
     outs = [ds.alloc_outputs(dmax, agg=True), ds.alloc_outputs(dmax, agg=True)]
     launches = [0]
+    buf_free = [None, None]   # event: the last computation that read input buffer set i has finished
 
     def one_step():
-        copied = [torch.cuda.Event() for _ in host_chunks]
-        done = [torch.cuda.Event() for _ in host_chunks]
         for c, hc in enumerate(host_chunks):
-            b = bufs[c % 2]
+            i = c % 2
+            b = bufs[i]
             with torch.cuda.stream(copy_s):
-                if c >= 2:
-                    copy_s.wait_event(done[c - 2])
+                if buf_free[i] is not None:
+                    copy_s.wait_event(buf_free[i])   # across steps too: never overwrite inputs still being read
                 for k, v in hc.items():
                     b[k][: v.numel()].copy_(v, non_blocking=True)
-                copied[c].record(copy_s)
-            comp_s.wait_event(copied[c])
+                copied = torch.cuda.Event()
+                copied.record(copy_s)
+            comp_s.wait_event(copied)
             S = hc["scen_dnn_off"].numel() - 1
             D = hc["dnn_row_off"].numel() - 1
             R = int(hc["dnn_row_off"][-1])
             if mode == "w5":
                 ds.unpack_w5(b["w"], b["lo"], b["n"], b["r"], b["d"], R)
                 launches[0] += ds.last_launch_count()
-            elif mode == "nr":
-                ds.unpack_nr(b["nr"], b["n"], b["r"], R)
-                launches[0] += ds.last_launch_count()
             dpc = ds.DeviceProblem(S, D, R, *[b[k] for k in prob_fields])
-            o = outs[c % 2]
+            o = outs[i]
             ds.eval_batch(dpc, p, out=o, ws=ws)
             launches[0] += ds.last_launch_count()
-            for k in res_fields:
-                host_res[c][k].copy_(o[k][:S], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(comp_s)
+            buf_free[i] = done
+            for k, hr in host_res[c].items():   # every result back (same stream: before o is reused)
+                hr.copy_(o[k][: hr.numel()], non_blocking=True)
             agg_host[c * ds.AGG_WORDS:(c + 1) * ds.AGG_WORDS].copy_(o["agg"], non_blocking=True)
-            done[c].record(comp_s)
 
     one_step()
     torch.cuda.synchronize()
@@ -762,16 +873,20 @@ def _e2e_timed(args, sp, p, dev, world, host_chunks, prob_fields, mode):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    return {"value": sp.num_scen * world * args.e2e_steps / (ms / 1e3), "unit": UNIT,
+    # spot check: chunk 0 through the e2e path equals the device-resident run on the same scenarios
+    S0, D0 = host_res[0]["u"].numel(), host_res[0]["demand"].numel()
+    check = all(torch.equal(host_res[0][k], ref_out[k][: host_res[0][k].numel()].cpu())
+                for k, _ in E2E_RES_SCEN + E2E_RES_DNN)
+    return {"value": n_total * args.e2e_steps / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms / args.e2e_steps,
             "chunks": len(host_chunks), "gpu_launches_per_step": launches[0] // max(args.e2e_steps, 1),
+            "check": {"chunk0_equals_device_resident_run": bool(check), "scenarios": S0, "dnns": D0},
+            "results_copied": [k for k, _ in E2E_RES_SCEN + E2E_RES_DNN] + ["agg"],
             "transport": {"w5": "compact rows: w = d | (R-1) << 26 | (n >> 8) << 28 (u32) + n & 255 (u8), 5 B/row, "
-                                "expanded on the device by dstack_unpack_w5 inside the timed region",
-                          "nr": "compact rows: nr = n | R << 12 (u16) + d (u32), 6 B/row, expanded on the device by "
-                                "dstack_unpack_nr inside the timed region",
-                          "wide": "wide rows: n u32 + r u16 + d u32"}[mode],
+                                "expanded on the device by dstack_unpack_w5 inside the timed region; packed once on "
+                                "the device before timing (a caller holding the ABI's wide rows must pack them)",
+                          "wide": "the ABI's own rows: n u32 + r u16 + d u32, 10 B/row"}[mode],
             "api": {"w5": "paper_2304_13541_b200.dstack.unpack_w5 + eval_batch (dstack_unpack_w5, dstack_eval_batch)",
-                    "nr": "paper_2304_13541_b200.dstack.unpack_nr + eval_batch (dstack_unpack_nr, dstack_eval_batch)",
                     "wide": "paper_2304_13541_b200.dstack.eval_batch (dstack_eval_batch)"}[mode]}
 
 
@@ -788,8 +903,7 @@ def run_sim(args, rank, world, local):
     if world > 1:
         init_dist(dev)
     sp0, p = synth.config(5, num_scen=args.scen or None)
-    per_gpu = sp0.num_scen
-    sp = sp0.replace(scen_base=rank * per_gpu)
+    sp, n_total, per_gpu = shard_of(args, sp0, rank, world)
     dp = ds.from_device_dict(synth.generate_device(sp, dev))
     run = lambda: ds.simulate(dp, p, args.cycles, sp.seed, sp.cfg_tag, scen_base=sp.scen_base)
     for _ in range(args.warmup):
@@ -823,10 +937,11 @@ def run_sim(args, rank, world, local):
         arrived, in_slo, late, unserved, occ, runs = tot.tolist()
         nslots = (o["T_us"].to(torch.float64) / p.slot_us)
         line = {"metric": "scenario-cycles/sec (config 5 long-horizon simulation, a7)",
-                "value": per_gpu * world * args.cycles * args.steps / (ms / 1e3), "unit": "scenario-cycles/s",
+                "value": n_total * args.cycles * args.steps / (ms / 1e3), "unit": "scenario-cycles/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-                "data": "synthetic", "config": {"workload": f"config5: {per_gpu} scenarios/GPU x {args.cycles} cycles",
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
+                "data": "synthetic", "config": {"workload": f"config5: {n_total} scenarios ({args.scaling} scaling, "
+                                                            f"~{per_gpu} per GPU) x {args.cycles} cycles per step",
                                                  "l2": "flushed before every step (256 MB write, inside the timed region)"},
                 "gpu_launches": launches, "clocks": clocks,
                 "stats": {"arrived": arrived, "in_slo_frac": in_slo / max(arrived, 1),

@@ -33,9 +33,11 @@
  *                               scenario: > DSTACK_MAX_DNN_PER_SCEN DNNs, session > DSTACK_MAX_SLOTS
  *                               slots, or > DSTACK_MAX_JOBS static jobs
  *      DSTACK_ST_OVERSUBSCRIBED scenario: some static job could not be placed (counted in misses)
- *  - Results are deterministic: independent of GPU count, launch configuration and stream.
- *    Integer outputs equal the oracle's bit for bit; f64 outputs are the documented ratios of
- *    exact integers, evaluated in the documented order.
+ *  - Per-DNN and per-scenario results are deterministic: independent of GPU count, launch
+ *    configuration and stream.  Integer outputs equal the oracle's bit for bit; f64 outputs are the
+ *    documented ratios of exact integers, evaluated in the documented order.  The aggregate's integer
+ *    words (counts, histograms, checksum) are sums, so shards add up exactly; its f64 sums depend on
+ *    the summation order (fixed per call, but not across shardings: equal to ~1e-12 relative).
  *  - Row arrays n, r, d must be readable 16 bytes past their last element (vector loads).
  *  - There is no CPU fallback: without a CUDA device every compute call returns DSTACK_ELAUNCH.
  */
@@ -120,7 +122,8 @@ typedef struct {
   uint64_t misses, runs, served;
   uint64_t batch_hist[DSTACK_MAX_BATCH + 1];   /* b* histogram over OK DNNs */
   uint64_t demand_hist[256];                   /* demand-level histogram over OK DNNs */
-  uint64_t checksum;         /* sum over DNNs of a mix of (index, demand, batch, knee, alloc, runs, served) */
+  uint64_t checksum;         /* sum over DNNs of a mix of (demand, batch, knee, alloc, runs, served, status):
+                                position-free, so per-shard aggregates sum to the whole problem's */
 } dstack_agg_t;
 
 /* Outputs.  In dstack_eval_batch, demand/batch/knee/status/alloc_q16 are REQUIRED (the path reads
@@ -277,6 +280,14 @@ int dstack_profile_stop(double *ms_out, int32_t *calls);
 
 /* Number of kernel launches the previous call on this thread enqueued (bench accounting). */
 int dstack_last_launch_count(void);
+
+/* a6 work counters of the last dstack_eval_batch / dstack_schedule_cycle call with DSTACK_FLAG_IDEAL that used this
+ * workspace (§6.2 event-driven ideal scheduler, R15): out8[0] events (intervals between consecutive
+ * completions), [1] events whose subset selection was recomputed, [2] of those decided by "every live item fits",
+ * [3] by exhaustive subset enumeration, [4] by meet in the middle, [5] by the subset-sum DP, [6] scenarios
+ * simulated, [7] reserved (0).  Host pointer out8; synchronises `stream`.  EINVAL without the IDEAL flag. */
+int dstack_ideal_stats(const dstack_problem_t *pb, const dstack_params_t *p, const void *ws, size_t ws_bytes,
+                       uint64_t *out8, void *stream);
 
 /* Compact row transport (host -> device): a row whose n_i < 4096 and 1 <= R_i <= 15 travels as
  * nr = n_i | R_i << 12 (u16) beside its d_i (u32), 6 bytes instead of 10; this call expands nr[0..num_rows) into

@@ -157,6 +157,18 @@ int dstack_unpack_nr(int64_t num_rows, const uint16_t *nr, uint32_t *n_out, uint
 
 int dstack_last_launch_count(void) { return g_launches; }
 
+int dstack_ideal_stats(const dstack_problem_t *pb, const dstack_params_t *p, const void *ws, size_t ws_bytes,
+                       uint64_t *out8, void *stream) {
+  if (!problem_ok(pb) || !params_ok(p) || !out8 || !(p->flags & DSTACK_FLAG_IDEAL)) return DSTACK_EINVAL;
+  if (!ws || ws_bytes < dstack_workspace_size(pb, p)) return DSTACK_EWORKSPACE;
+  if (!have_device()) return DSTACK_ELAUNCH;
+  const char *src = (const char *)ws + ws_layout(pb, p).ideal + ideal_stats_offset(pb->num_rows, pb->num_scen);
+  if (cudaMemcpyAsync(out8, src, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost, (cudaStream_t)stream) != cudaSuccess ||
+      cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
+    return DSTACK_ELAUNCH;
+  return DSTACK_OK;
+}
+
 const char *dstack_status_str(int code) {
   switch (code) {
     case DSTACK_OK: return "OK";

@@ -92,7 +92,9 @@ __global__ void __launch_bounds__(AGG_THREADS) k_agg1(AggArgs a) {
       nok += ok;
       const uint32_t rn = a.runs ? a.runs[k] : 0, sv = a.served ? a.served[k] : 0;
       runs += rn; served += sv;
-      const uint64_t v = ((uint64_t)k << 40) ^ ((uint64_t)dm << 24) ^ ((uint64_t)bt << 16) ^
+      // no DNN index in the mix: the checksum is a sum over the multiset of per-DNN outputs, so shards of the
+      // problem (any GPU count, any chunking) add up to the whole problem's checksum
+      const uint64_t v = ((uint64_t)dm << 24) ^ ((uint64_t)bt << 16) ^
                          ((uint64_t)(a.knee ? a.knee[k] : 0)) ^ ((uint64_t)(a.alloc ? a.alloc[k] : 0) << 8) ^
                          ((uint64_t)rn << 44) ^ ((uint64_t)sv << 20) ^ ((uint64_t)st << 60);
       cks += mix64(v);

@@ -192,7 +192,9 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
       bool sel = false;
       uint64_t gsum = 0;
       uint64_t util = 0, t = 0;
+      uint32_t st_ev = 0, st_rs = 0, st_fit = 0, st_enum = 0, st_mitm = 0, st_dp = 0;   // a6 work counters
       while (n > 0 && t < T) {
+        ++st_ev;
         if (dirty) {   // priority rank among the live DNNs: (batch deadline, index)
           const uint64_t key = ((uint64_t)dl << 5) | (uint32_t)lane;
           rank = 0;
@@ -209,12 +211,15 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
         // optimum is all of them (g >= 1).
         uint32_t gtot = 0xFFFFFFFFu;
         if (DSTACK_IDEAL_SHORTCUTS && resel) gtot = __reduce_add_sync(FULL, live ? cur.g : 0u);
+        if (resel) ++st_rs;
         if (DSTACK_IDEAL_SHORTCUTS && !resel) {
           // keep sel, gsum
         } else if (DSTACK_IDEAL_SHORTCUTS && gtot <= (uint32_t)L) {
+          ++st_fit;
           sel = live;
           gsum = gtot;
         } else if (n <= DSTACK_IDEAL_ENUM_MAX) {
+          ++st_enum;
           sel = false;
           gsum = 0;
           // <= 1024 subsets: enumerate them all (8 per lane per round, 2^(n-8) rounds).  Subset index bit p <->
@@ -257,6 +262,7 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
           gsum = best >> NE;
           sel = live && ((best >> (n - 1 - rank)) & 1u);
         } else if (DSTACK_IDEAL_MITM && n <= 16) {
+          ++st_mitm;
           // meet in the middle: A = ranks 0..7 (A index bit p <-> rank 7 - p), B = ranks 8..n-1 (B index bit p <->
           // rank n - 1 - p), 256 subsets each, 8 per lane.  The lexicographically-first optimal subset has the
           // largest (A index, B index): first the largest A index among the A subsets that complete to the
@@ -320,6 +326,7 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
           gsum = best;
           sel = live && (rank < 8 ? ((ia >> (7 - rank)) & 1u) : ((ib >> (n - 1 - rank)) & 1u));
         } else {
+          ++st_dp;
           sel = false;
           gsum = 0;
           // suffix reachability: reach[q] = subset sums of the items of rank >= q; the items' weights by rank
@@ -383,6 +390,12 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
         resel = dirty || __any_sync(FULL, cur.g != g_before);
         __syncwarp();
       }
+      if (a.stats && lane == 0) {
+        atomicAdd(&a.stats[0], (unsigned long long)st_ev); atomicAdd(&a.stats[1], (unsigned long long)st_rs);
+        atomicAdd(&a.stats[2], (unsigned long long)st_fit); atomicAdd(&a.stats[3], (unsigned long long)st_enum);
+        atomicAdd(&a.stats[4], (unsigned long long)st_mitm); atomicAdd(&a.stats[5], (unsigned long long)st_dp);
+        atomicAdd(&a.stats[6], 1ull);
+      }
       const uint64_t bsum = warp_sum_u64(act ? (uint64_t)comp * a.batch[k] : 0ull);
       ui = (double)util / ((double)L * (double)T);
       ti = (double)bsum * 1e6 / (double)T;
@@ -393,6 +406,13 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
     }
     __syncwarp();
   }
+}
+
+// a6 work counters of the last launch (events, re-selections, all-fit / enumeration / meet-in-the-middle / DP
+// selections, scenarios simulated): 8 u64 at the end of the ideal workspace region
+size_t ideal_stats_offset(int64_t num_rows, int64_t num_scen) {
+  return (((size_t)(num_rows + 8) * 2 + 255) & ~(size_t)255) + (((size_t)(num_rows + 8) * 4 + 255) & ~(size_t)255) +
+         (((size_t)(num_scen + 8) * 4 + 255) & ~(size_t)255) + 48 * 4;
 }
 
 size_t ideal_ws_bytes(int64_t num_rows, int64_t num_scen) {
@@ -451,6 +471,8 @@ int launch_ideal(IdealArgs a, void *ws, cudaStream_t s, int *launches) {
   a.ex_tau = (uint32_t *)((char *)ws + (((size_t)(num_rows + 8) * 2 + 255) & ~(size_t)255));
   a.order = (uint32_t *)((char *)a.ex_tau + (((size_t)(num_rows + 8) * 4 + 255) & ~(size_t)255));
   a.bucket_cnt = (uint32_t *)((char *)a.order + (((size_t)(a.pb.num_scen + 8) * 4 + 255) & ~(size_t)255));
+  a.stats = (unsigned long long *)(a.bucket_cnt + 48);   // 8 u64 behind the 40 bucket counters (256 B slot)
+  if (cudaMemsetAsync(a.stats, 0, 8 * sizeof(unsigned long long), s) != cudaSuccess) return DSTACK_ELAUNCH;
   if (a.pb.num_dnn > 0) {
     int64_t blocks = ((int64_t)a.pb.num_dnn * 32 + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;

@@ -92,6 +92,7 @@ struct IdealArgs {
   const uint32_t *ws_RT;       // sum R per DNN (may be NULL)
   uint32_t *order;             // [num_scen] scenarios, heaviest estimate first (set by launch_ideal)
   uint32_t *bucket_cnt;        // [64] workspace
+  unsigned long long *stats;   // [8] workspace: work counters (ideal_stats_offset)
 };
 
 struct CmpArgs {
@@ -142,6 +143,7 @@ inline int64_t resident_wave(K kern, int threads, size_t smem, int64_t blocks) {
   return blocks < w ? blocks : w;
 }
 size_t ideal_ws_bytes(int64_t num_rows, int64_t num_scen);
+size_t ideal_stats_offset(int64_t num_rows, int64_t num_scen);
 size_t agg_ws_bytes();
 
 }  // namespace dstack

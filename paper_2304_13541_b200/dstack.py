@@ -96,6 +96,7 @@ def _load():
     lib.dstack_cluster.argtypes = [P(CProblem), P(CParams), C.c_int32] + [C.c_void_p] * 5 + [C.c_size_t, C.c_void_p]
     lib.dstack_unpack_nr.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.dstack_unpack_w5.argtypes = [C.c_int64] + [C.c_void_p] * 6
+    lib.dstack_ideal_stats.argtypes = [P(CProblem), P(CParams), C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
     lib.dstack_profile_start.argtypes = [C.c_int32]
     lib.dstack_profile_stop.argtypes = [C.c_void_p, C.c_void_p]
     lib.dstack_status_str.restype = C.c_char_p
@@ -385,6 +386,17 @@ def simulate(dp: DeviceProblem, p, cycles: int, seed: int, cfg_tag: int, scen_ba
                                 scen_base, C.byref(CSimOut(*[o[k].data_ptr() for k in _SIM_FIELDS])), ws.ptr(),
                                 ws.nbytes, _stream(dev)), "dstack_simulate")
     return {k: v[: dp.num_scen] for k, v in o.items()}
+
+
+IDEAL_STATS = ("events", "reselections", "sel_all_fit", "sel_enumeration", "sel_meet_in_middle", "sel_dp", "scenarios")
+
+
+def ideal_stats(dp: DeviceProblem, p, ws: "Workspace") -> dict:
+    """dstack_ideal_stats: a6 work counters of the last IDEAL call that used `ws`."""
+    out = (C.c_uint64 * 8)()
+    _check(_lib.dstack_ideal_stats(C.byref(dp.c()), C.byref(cparams(p)), ws.ptr(), ws.nbytes, out,
+                                   _stream(dp.device)), "dstack_ideal_stats")
+    return {k: int(out[i]) for i, k in enumerate(IDEAL_STATS)}
 
 
 def last_launch_count() -> int:

@@ -12,7 +12,7 @@ def mix64(x):
     return x
 
 
-def host_agg(o, global_dnn_base=0):
+def host_agg(o):
     """o: dict of numpy outputs (oracle.evaluate / dstack.to_numpy). Returns an int64 array of AGG_WORDS
     with the first 5 words holding f64 bit patterns (same layout as dstack_agg_t)."""
     T = o["T_us"].astype(np.int64)
@@ -32,7 +32,7 @@ def host_agg(o, global_dnn_base=0):
     cks = np.uint64(0)
     with np.errstate(over="ignore"):
         for k in range(D):
-            v = (np.uint64(k + global_dnn_base) << np.uint64(40)) ^ (np.uint64(o["demand"][k]) << np.uint64(24)) ^ \
+            v = (np.uint64(o["demand"][k]) << np.uint64(24)) ^ \
                 (np.uint64(o["batch"][k]) << np.uint64(16)) ^ np.uint64(o["knee"][k]) ^ \
                 (np.uint64(o["alloc_q16"][k]) << np.uint64(8)) ^ (np.uint64(o["runs"][k]) << np.uint64(44)) ^ \
                 (np.uint64(o["served"][k]) << np.uint64(20)) ^ (np.uint64(st[k]) << np.uint64(60))

@@ -278,6 +278,25 @@ def test_aggregate_matches_host_reference(ds):
     np.testing.assert_allclose(got[:5].view(np.float64), want[:5].view(np.float64), rtol=1e-12)
 
 
+def test_aggregate_of_shards_adds_up(ds):
+    """a8 across shards (the multi-GPU combine): the device aggregates of two uneven global-index shards, summed
+    word by word as the NCCL all-reduce does, equal the device aggregate of the whole problem -- integer words
+    (counts, histograms, position-free checksum) exactly, the f64 sums to 1e-12."""
+    n = 900
+    sp, p = synth.config(2, num_scen=n, rows_pct=20)
+    _, whole = run_gpu(ds, synth.generate_host(sp), p)
+    parts = []
+    for r in range(2):
+        b, e = (0, 337) if r == 0 else (337, n)
+        _, o = run_gpu(ds, synth.generate_host(sp.replace(scen_base=b, num_scen=e - b)), p)
+        parts.append(o["agg"].cpu().numpy())
+    want = whole["agg"].cpu().numpy()
+    ints = parts[0][5:].view(np.uint64) + parts[1][5:].view(np.uint64)
+    assert np.array_equal(ints, want[5:].view(np.uint64))
+    f = parts[0][:5].view(np.float64) + parts[1][:5].view(np.float64)
+    np.testing.assert_allclose(f, want[:5].view(np.float64), rtol=1e-12)
+
+
 def fast_path_problem(S_tot):
     """DNNs that drive every branch of k_prof_fast (prof.cu): certificate failure (t_np = 0, so the b >= 2
     bound has no gap), RT >= 2^24 (u32 prefix range exceeded), X(L, b_hi) within 1e-4 of 2^56 on either

@@ -22,12 +22,7 @@ def _worker(rank, world, port, q):
     sp, p = synth.config(2, num_scen=N_PER, rows_pct=20, scen_base=rank * N_PER)
     pb = synth.generate_host(sp)
     o = oracle.evaluate(pb, p)
-    # the checksum mixes the GLOBAL DNN index: offset by the DNNs of the lower ranks (all-gathered counts)
-    cnt = torch.tensor([pb.num_dnn], dtype=torch.int64)
-    allc = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
-    dist.all_gather(allc, cnt)
-    base = int(sum(c.item() for c in allc[:rank]))
-    agg = torch.from_numpy(host_agg(o, global_dnn_base=base))
+    agg = torch.from_numpy(host_agg(o))   # position-free checksum: shard aggregates add up
     allreduce_agg(agg)
     if rank == 0:
         q.put(agg.numpy().copy())
