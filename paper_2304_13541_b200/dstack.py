@@ -110,7 +110,7 @@ _lib = _load()
 EXPORTS = ("dstack_workspace_size", "dstack_knee", "dstack_knee_probe", "dstack_batch_opt", "dstack_wmaxmin", "dstack_schedule_cycle",
            "dstack_eval_batch", "dstack_aggregate", "dstack_sim_workspace_size", "dstack_simulate",
            "dstack_compare", "dstack_cluster", "dstack_unpack_nr", "dstack_unpack_w5", "dstack_profile_start", "dstack_profile_stop",
-           "dstack_last_launch_count", "dstack_status_str", "dstack_version")
+           "dstack_last_launch_count", "dstack_ideal_stats", "dstack_status_str", "dstack_version")
 
 
 def lib():
