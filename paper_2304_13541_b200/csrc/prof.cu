@@ -495,9 +495,371 @@ __global__ void __launch_bounds__(256, DSTACK_PROF_MINB) k_prof_fast(const __gri
   }
 }
 
+// ------------------------------------------------------------------------------------------------------
+// lane-per-DNN fast path (k_prof_lane): the same decisions as k_prof_fast, organised so that the per-DNN
+// scalar work runs one DNN per lane
+// ------------------------------------------------------------------------------------------------------
+//  * a warp takes groups of 32 consecutive DNNs; lane j loads and validates DNN kb+j's header;
+//  * a1 row pass, warp-cooperative and coalesced, one DNN after the other: per-lane partial sums (RT, min R,
+//    D = sum R d, W> = sum_{n > S_tot} R n, Wsm = sum_{n <= S_tot} R n) reduced to the owning lane, and the width
+//    histogram H[n] = sum_{n_i = n} R_i of n <= S_tot accumulated with shared-memory atomics into the owning
+//    lane's row of a [32][HSTRIDE] u32 table, two u16 bins per word (the fast path requires RT < 2^16, so no bin
+//    carries), HSTRIDE odd so that the lanes' rows start in distinct banks;
+//  * a2/a3 per lane: one sequential scan of the widths S = 1..S_tot forms PA[S], PW[S] and the exact
+//    X(S, 1) = S C1 + Mtp (S PA[S] + Wsm - PW[S]) + Mtp W> + mem (O1, b = 1) in u64, keeps the exact argmax of
+//    S / X^2 over the attained widths (ties -> smaller S; an f32 score filters, near-ties within 2^-19 are
+//    decided by the 128-bit comparison S' X^2 vs S X'^2), and the b >= 2 certificate G over the
+//    segments m <= S_tot / 2 from the same PA / Q values;
+//  * a DNN outside the fast ranges (RT >= 2^16, X near 2^56, certificate not won) is re-analysed by the generic
+//    warp path (prof_one_cold) after the group -- identical outputs, more work.
+#ifndef DSTACK_PROF_LANE
+#define DSTACK_PROF_LANE 1   // 1: the default-model fast path is k_prof_lane (0: k_prof_fast; A/B switch)
+#endif
+#ifndef DSTACK_PLANE_MINB
+#define DSTACK_PLANE_MINB 2
+#endif
+
+__host__ __device__ inline int plane_hstride(int S_tot) { return ((S_tot + 2) >> 1) | 1; }   // odd word stride
+__host__ __device__ inline size_t plane_warp_bytes(int S_tot) {
+  return (size_t)32 * plane_hstride(S_tot) * 4 + prof_warp_bytes(S_tot);   // H table + the cold path's scratch
+}
+
+// exact-with-filter update of the running argmax (Sb, Xb, fb) of S / X^2 by a later (larger) width S
+__device__ __forceinline__ void lane_best(uint32_t S, uint64_t X, float f, uint32_t &Sb, uint64_t &Xb, float &fb) {
+  bool take;
+  if (Sb == 0 || f > fb * 1.0000020f) take = true;          // 1 + 2^-19: certainly larger (score error < 2^-21)
+  else if (f < fb * 0.99999809f) take = false;              // 1 - 2^-19: certainly smaller
+  else take = (u128)S * ((u128)Xb * Xb) > (u128)Sb * ((u128)X * X);   // near tie: exact, strict (ties -> smaller S)
+  if (take) { Sb = S; Xb = X; fb = f; }
+}
+
+// Exact scan (cold within the fast path): the exact argmax (Sb, Xb) of S / X^2 over the attained widths, or over
+// those with 2X <= S F when feas_only (Eqs. 11-12 at b = 1); no_cert: skip the certificate terms.
+template <int SCAN_MEM>   // 0: memory term off / bw (in `base`), 2: verbatim (D S^2)
+static __device__ __noinline__ void lane_scan(const uint32_t *H, const uint16_t *lmin, int S_tot, int mh, uint64_t C1,
+                                              uint64_t Mtp, uint64_t base, uint64_t D, uint32_t Wsm, uint64_t F,
+                                              bool no_cert, float C1f2, float Mtpf, float Wbf, float membf, float half,
+                                              uint32_t &Sb, uint64_t &Xb, float &fb, float &G, bool feas_only) {
+  uint32_t ra = 0, rw = 0;
+  const int nw = (S_tot >> 1) + 1;
+  for (int w = 0; w < nw; ++w) {
+    const uint32_t hw = H[w];
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      const uint32_t S = (uint32_t)(2 * w + hi);
+      if (S > (uint32_t)S_tot) break;
+      const uint32_t h = S == 0 ? 0u : (hi ? (hw >> 16) : (hw & 0xFFFFu));   // n = 0 rows: in neither PA nor PW
+      ra += h; rw += h * S;
+      const uint32_t q = Wsm - rw;                                             // Q[S] - W>
+      if (!no_cert && (int)S <= mh) {   // certificate segment m = S: eta(S', b >= 2) <= s / (alpha s + beta)^2
+        const float af = fmaf(Mtpf, (float)ra, C1f2), bf = fmaf(Mtpf, (float)q + Wbf, membf);
+        const float lo = (float)S, hiS = fminf(lo + 1.f, half);
+        const float sx = fminf(fmaxf(bf * rcp_approx(af), lo), hiS);
+        const float x = fmaf(af, sx, bf);
+        G = fmaxf(G, bf == 0.f ? __int_as_float(0x7f800000) : sx * rcp_approx(x * x));
+      }
+      if (S == 0 || !lmin[S]) continue;
+      uint64_t X = (uint64_t)S * C1 + Mtp * ((uint64_t)S * ra + q) + base;
+      if (SCAN_MEM == 2) X += D * (uint64_t)(S * S);
+      if (feas_only && 2 * X > (uint64_t)S * F) continue;
+      lane_best(S, X, score_f(S, X), Sb, Xb, fb);
+    }
+  }
+}
+
+// X(S, 1) at one width from the lane's histogram (the demand level's width when a margin moves it off the argmax)
+__device__ __forceinline__ uint64_t lane_X_at(const uint32_t *H, uint32_t Sg, uint64_t C1, uint64_t Mtp, uint64_t base,
+                                             uint64_t D, uint32_t Wsm, int mem_mode) {
+  uint32_t ra = 0, rw = 0;
+  for (uint32_t S = 1; S <= Sg; ++S) {
+    const uint32_t hw = H[S >> 1];
+    const uint32_t h = (S & 1) ? (hw >> 16) : (hw & 0xFFFFu);
+    ra += h; rw += h * S;
+  }
+  uint64_t X = (uint64_t)Sg * C1 + Mtp * ((uint64_t)Sg * ra + (Wsm - rw)) + base;
+  if (mem_mode == 2) X += D * (uint64_t)(Sg * Sg);
+  return X;
+}
+
+// One f32 pass over the widths: per attained width S the score S / X(S, 1)^2 from an f32 evaluation of X
+// (all terms non-negative: relative error < 2^-20, so only scores within 2^-19 of each other can be misordered),
+// a top-3 tracker (t1 >= t2 >= t3, with the widths and PA / Q - W> values of the top 2), and the b >= 2
+// certificate G over the segments m <= S_tot / 2.  The caller takes s1 when t2 < t1 (1 - 2^-17), decides s1 vs s2
+// exactly when only t2 is that close (adjacent widths around a smooth maximum: ~4 % of DNNs), and rescans
+// exactly (lane_scan) when t3 is too.
+template <int SCAN_MEM>
+__device__ __forceinline__ void lane_scan_f(const uint32_t *H, const uint16_t *lmin, int S_tot, int mh, bool all_valid,
+                                            float C1f, float Mtpf, float basef, float Df, uint32_t Wsm, float C1f2,
+                                            float Wbf, float membf, float half, float &t1, float &t2, float &t3,
+                                            uint32_t &s1, uint32_t &ra1, uint32_t &q1, uint32_t &s2, float &G) {
+  uint32_t ra = 0, rw = 0;
+  const int nw = (S_tot + 2) >> 1;   // words holding bins 0..S_tot (bin S_tot + 1 of an even S_tot is 0)
+#pragma unroll 2
+  for (int w = 0; w < nw; ++w) {
+    const uint32_t hw = H[w];
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      const uint32_t S = (uint32_t)(2 * w + hi);   // S_tot + 1 (even S_tot): h = 0, lmin = 0 -> no candidate
+      const uint32_t h = S == 0 ? 0u : (hi ? (hw >> 16) : (hw & 0xFFFFu));
+      ra += h; rw += h * S;
+      const uint32_t q = Wsm - rw;
+      const float Sf = (float)S, raf = (float)ra, qf = (float)q;
+      if ((int)S <= mh) {
+        const float af = fmaf(Mtpf, raf, C1f2), bf = fmaf(Mtpf, qf + Wbf, membf);
+        const float hiS = fminf(Sf + 1.f, half);
+        const float sx = fminf(fmaxf(bf * rcp_approx(af), Sf), hiS);
+        const float x = fmaf(af, sx, bf);
+        G = fmaxf(G, bf == 0.f ? __int_as_float(0x7f800000) : sx * rcp_approx(x * x));
+      }
+      if (S == 0 || S > (uint32_t)S_tot || !(all_valid || lmin[S])) continue;
+      float xf = fmaf(Sf, C1f, fmaf(Mtpf, fmaf(Sf, raf, qf), basef));
+      if (SCAN_MEM == 2) xf = fmaf(Df, Sf * Sf, xf);
+      const float f = Sf * rcp_approx(xf * xf);
+      // top-3 of the scores (strict: the first width keeps a float tie), payloads of the top 2
+      const bool g1 = f > t1, g2 = f > t2;
+      t3 = fmaxf(t3, fminf(t2, f));
+      s2 = g1 ? s1 : (g2 ? S : s2);
+      t2 = fmaxf(t2, fminf(t1, f));
+      s1 = g1 ? S : s1; ra1 = g1 ? ra : ra1; q1 = g1 ? q : q1;
+      t1 = fmaxf(t1, f);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, DSTACK_PLANE_MINB) k_prof_lane(const __grid_constant__ ProfArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const dstack_problem_t &pb = a.pb;
+  const dstack_params_t &p = a.p;
+  const int L = p.L, S_tot = p.S_tot, mem_mode = p.mem_mode;
+  uint16_t *Stab = (uint16_t *)smem;
+  uint16_t *lmin = Stab + (L + 1);
+  const int tab_bytes = ((L + 1 + S_tot + 1) * 2 + 15) & ~15;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int HS = plane_hstride(S_tot);
+  unsigned char *wreg = smem + tab_bytes + (size_t)warp * plane_warp_bytes(S_tot);
+  uint32_t *Htab = (uint32_t *)wreg;                       // [32][HS]
+  uint64_t *cA = (uint64_t *)(wreg + (size_t)32 * HS * 4);  // cold path scratch
+  uint64_t *cU = cA + (S_tot + 1);
+  uint32_t *hist = (uint32_t *)(cU + (S_tot + 1));
+  fill_stab(Stab, L, S_tot);
+  for (int S = threadIdx.x; S <= S_tot; S += blockDim.x) {
+    const int l = S == 0 ? 0 : ((S - 1) * L) / S_tot + 1;
+    lmin[S] = (uint16_t)((S >= 1 && l <= L && s_of(l, S_tot, L) == S) ? l : 0);
+  }
+  for (int m = lane; m <= S_tot; m += 32) hist[m] = 0;
+  __syncthreads();
+  const int mh = S_tot >> 1;
+  const float half = 0.5f * (float)S_tot;
+  const int hwords = 32 * HS;
+  const bool all_valid = L == S_tot;   // every width is some level's S(l)
+  // groups of 32 DNNs from the work counter (one resident wave) or a grid stride over groups
+  const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp, nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = warp_next_item(a.work_ctr, -1, gwarp, nwarps, lane); g * 32 < pb.num_dnn;
+       g = warp_next_item(a.work_ctr, g, gwarp, nwarps, lane)) {
+    const int64_t kb = g * 32;
+    const int nj = pb.num_dnn - kb < 32 ? (int)(pb.num_dnn - kb) : 32;
+    const int64_t kl = kb + lane;
+    const bool have = lane < nj;
+    // ---- lane-parallel header: load + validate (DSTACK_ST_INVALID conditions, dstack.h) ----
+    int64_t r0 = 0;
+    int32_t K = 0, b_hi = 0;
+    uint32_t M = 1, t_np = 0;
+    uint64_t Mtp = 0, F = 0;
+    bool ok = false;
+    if (have) {
+      r0 = pb.dnn_row_off[kl];
+      const int64_t K64 = pb.dnn_row_off[kl + 1] - r0;
+      const int32_t t_p = pb.t_p[kl], tnp = pb.t_np[kl], slo = pb.slo_us[kl], asm_us = pb.asm_us[kl];
+      const int32_t bmax = pb.bmax[kl], mbw = pb.mem_bw[kl];
+      ok = !(K64 < 1 || K64 > DSTACK_MAX_ROWS_PER_DNN || t_p < 1 || tnp < 0 || slo < 1 || slo > (1 << 30) ||
+             (slo % p.slot_us) != 0 || asm_us < 0 || asm_us > (1 << 24) || bmax < 1 ||
+             (p.mem_mode != 0 && (mbw < 1 || mbw > (1 << 24))));
+      K = ok ? (int32_t)K64 : 0;
+      M = p.mem_mode == 0 ? 1u : (uint32_t)mbw;
+      t_np = (uint32_t)tnp;
+      Mtp = (uint64_t)M * (uint32_t)t_p;
+      // Eqs. 11-12 at b = 1 as one test 2X <= S F:  F = min(2 (SLO - a) M, SLO M)  (0 if a > SLO)
+      const uint64_t SLOM = (uint64_t)slo * M, aM = (uint64_t)asm_us * M;
+      F = SLOM < aM ? 0ull : (2 * (SLOM - aM) < SLOM ? 2 * (SLOM - aM) : SLOM);
+      b_hi = bmax < p.b_max ? bmax : p.b_max;
+    }
+    // ---- zero the 32 histogram rows (16-byte stores) ----
+    {
+      uint4 *hz = reinterpret_cast<uint4 *>(Htab);
+      for (int i = lane; i < (hwords >> 2); i += 32) hz[i] = make_uint4(0u, 0u, 0u, 0u);
+      for (int i = (hwords & ~3) + lane; i < hwords; i += 32) Htab[i] = 0u;
+    }
+    __syncwarp();
+    // ---- a1: row pass, one DNN after the other (coalesced), results to the owning lane; the first
+    //      32 * DSTACK_PROF_ROWS_U rows of the next DNN are loaded while the current one is reduced ----
+    constexpr int U = DSTACK_PROF_ROWS_U;
+    uint32_t myRT = 0, myRmin = 0, myWsm = 0, myDtop = 0, myWtop = 0;
+    uint64_t myD = 0, myWb = 0;
+    uint32_t cn[U], cd[U], cr[U], pn[U], pd[U], pr[U];
+    auto load_batch = [&](int64_t rb, int32_t Kb, int i0, uint32_t *bn, uint32_t *bd, uint32_t *br) {
+      const uint32_t *np = pb.n + rb + i0;
+      const uint32_t *dp = pb.d + rb + i0;
+      const uint16_t *rp = pb.r + rb + i0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        bn[u] = 0; bd[u] = 0; br[u] = 0;
+        if (i0 + 32 * u < Kb) { bn[u] = __ldg(np + 32 * u); bd[u] = __ldg(dp + 32 * u); br[u] = __ldg(rp + 32 * u); }
+      }
+    };
+    int32_t Kc = nj > 0 ? __shfl_sync(FULL, K, 0) : 0;
+    int64_t rc = nj > 0 ? (int64_t)shfl_u64((uint64_t)r0, 0) : 0;
+    load_batch(rc, Kc, lane, cn, cd, cr);
+    for (int jj = 0; jj < nj; ++jj) {
+      const int32_t Kn = jj + 1 < nj ? __shfl_sync(FULL, K, jj + 1) : 0;
+      const int64_t rn = jj + 1 < nj ? (int64_t)shfl_u64((uint64_t)r0, jj + 1) : 0;
+      load_batch(rn, Kn, lane, pn, pd, pr);   // prefetch (predicated off past the group / for invalid DNNs)
+      if (Kc > 0) {
+        uint32_t *Hj = Htab + jj * HS;
+        uint32_t RT = 0, Rmin = 0xFFFFFFFFu, Wsm = 0;
+        uint64_t D = 0, Wb = 0;
+        auto accum = [&](const uint32_t *bn, const uint32_t *bd, const uint32_t *br, int i0) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (i0 + 32 * u < Kc) {
+              RT += br[u]; D += (uint64_t)br[u] * bd[u]; Rmin = min(Rmin, br[u]);
+              if (bn[u] <= (uint32_t)S_tot) {
+                atomicAdd(&Hj[bn[u] >> 1], br[u] << ((bn[u] & 1u) << 4));
+                Wsm += br[u] * bn[u];
+              } else {
+                Wb += (uint64_t)br[u] * bn[u];
+              }
+            }
+          }
+        };
+        accum(cn, cd, cr, lane);
+        for (int i0 = lane + 32 * U; i0 - lane < Kc; i0 += 32 * U) {   // rows beyond the prefetched batch
+          uint32_t tn[U], td[U], tr[U];
+          load_batch(rc, Kc, i0, tn, td, tr);
+          accum(tn, td, tr, i0);
+        }
+        RT = __reduce_add_sync(FULL, RT);
+        Rmin = __reduce_min_sync(FULL, Rmin);
+        Wsm = __reduce_add_sync(FULL, Wsm);
+        uint32_t Dtop, Wtop;
+        D = warp_sum_limbs(D, &Dtop);
+        Wb = warp_sum_limbs(Wb, &Wtop);
+        if (lane == jj) { myRT = RT; myRmin = Rmin; myWsm = Wsm; myD = D; myWb = Wb; myDtop = Dtop; myWtop = Wtop; }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) { cn[u] = pn[u]; cd[u] = pd[u]; cr[u] = pr[u]; }
+      Kc = Kn; rc = rn;
+    }
+    __syncwarp();
+    // ---- a2/a3 for this lane's DNN ----
+    uint32_t st = ok ? DSTACK_ST_OK : DSTACK_ST_INVALID, knee = 0, demand = 0, dslots = 0;
+    bool cold = false;
+    if (have && ok) {
+      // status (same order as the generic path); the fast ranges (else the generic path decides)
+      if (myRmin == 0 || (t_np == 0 && myWb == 0 && myWtop == 0 && myWsm == 0 &&
+                          (mem_mode == 0 || (myD == 0 && myDtop == 0)))) {
+        st = DSTACK_ST_INVALID;
+      } else if (b_hi < 1) {
+        st = DSTACK_ST_INFEASIBLE;
+      } else if (myRT >= (1u << 16) || myWtop >= (1u << 19) || myDtop >= (1u << 19)) {
+        cold = true;
+      } else {
+        // overflow: X(L, b_hi) <= b_hi t_np RT S_tot M + Mtp (S_tot RT + b_hi (W> + Wsm)) + mem bounds every cell;
+        // within 1e-4 of 2^56 the generic path decides exactly
+        const double bd = (double)b_hi, Sd = (double)S_tot;
+        double xe = bd * (double)t_np * (double)M * (double)myRT * Sd +
+                    (double)Mtp * (Sd * (double)myRT + bd * ((double)myWb + (double)myWsm));
+        if (mem_mode == 1) xe += bd * (double)myD;
+        else if (mem_mode == 2) xe += bd * (double)myD * Sd * Sd;
+        if (xe >= 72057594037927936.0 * 0.9999) cold = true;
+      }
+      if (st == DSTACK_ST_OK && !cold) {
+        const uint64_t C1 = (uint64_t)t_np * M * myRT;
+        const uint64_t memb = mem_mode == 1 ? myD : 0ull;
+        const uint64_t base = Mtp * myWb + memb;
+        const float C1f2 = 2.f * (float)C1, Mtpf = (float)Mtp, Wbf = (float)myWb, membf = (float)memb;
+        const uint32_t *H = Htab + lane * HS;
+        uint32_t Sk = 0, ra1 = 0, q1 = 0, s2 = 0;
+        uint64_t Xk = 0;
+        float t1 = 0.f, t2 = 0.f, t3 = 0.f, G = 0.f;
+        const float C1f = (float)C1, basef = (float)base, Df = (float)myD;
+        if (mem_mode == 2) lane_scan_f<2>(H, lmin, S_tot, mh, all_valid, C1f, Mtpf, basef, Df, myWsm, C1f2, Wbf, membf, half, t1, t2, t3, Sk, ra1, q1, s2, G);
+        else lane_scan_f<0>(H, lmin, S_tot, mh, all_valid, C1f, Mtpf, basef, Df, myWsm, C1f2, Wbf, membf, half, t1, t2, t3, Sk, ra1, q1, s2, G);
+        const float band = t1 * 0.99999237f;   // 1 - 2^-17 (twice the worst f32 misordering)
+        auto x_at = [&](uint32_t S, uint32_t ra, uint32_t q) {
+          uint64_t X = (uint64_t)S * C1 + Mtp * ((uint64_t)S * ra + q) + base;
+          if (mem_mode == 2) X += myD * (uint64_t)(S * S);
+          return X;
+        };
+        if (t3 >= band) {   // three widths within the band (rare): exact rescan
+          float fk = 0.f, Gd = 0.f;
+          Sk = 0;
+          if (mem_mode == 2) lane_scan<2>(H, lmin, S_tot, mh, C1, Mtp, base, myD, myWsm, F, true, C1f2, Mtpf, Wbf, membf, half, Sk, Xk, fk, Gd, false);
+          else lane_scan<0>(H, lmin, S_tot, mh, C1, Mtp, base, myD, myWsm, F, true, C1f2, Mtpf, Wbf, membf, half, Sk, Xk, fk, Gd, false);
+        } else {
+          Xk = x_at(Sk, ra1, q1);
+          if (t2 >= band) {   // s1 vs s2 exactly: larger S / X^2, ties -> the smaller width
+            const uint64_t X2 = lane_X_at(H, s2, C1, Mtp, base, myD, myWsm, mem_mode);
+            const u128 l1 = (u128)Sk * ((u128)X2 * X2), l2 = (u128)s2 * ((u128)Xk * Xk);
+            if (l2 > l1 || (l2 == l1 && s2 < Sk)) { Sk = s2; Xk = X2; }
+          }
+        }
+        // knee = the exact argmax over every attained width; when it is feasible (Eqs. 11-12: 2X <= S F) it is
+        // also the feasible argmax, else the feasible widths are scanned again
+        uint32_t Se = 0;
+        uint64_t Xe = 0;
+        if (F != 0 && 2 * Xk <= (uint64_t)Sk * F) { Se = Sk; Xe = Xk; }
+        else {   // (F = 0: no width is feasible; scanned with F = 1 exactly as the generic fast path does)
+          const uint64_t F1 = F == 0 ? 1ull : F;
+          float fe = 0.f, Gd = 0.f;
+          if (mem_mode == 2) lane_scan<2>(H, lmin, S_tot, mh, C1, Mtp, base, myD, myWsm, F1, true, C1f2, Mtpf, Wbf, membf, half, Se, Xe, fe, Gd, true);
+          else lane_scan<0>(H, lmin, S_tot, mh, C1, Mtp, base, myD, myWsm, F1, true, C1f2, Mtpf, Wbf, membf, half, Se, Xe, fe, Gd, true);
+        }
+        if (Se == 0) {
+          st = DSTACK_ST_INFEASIBLE;   // b = 1 is feasible whenever any b is (O3)
+        } else if (b_hi >= 2 && !(score_f(Se, Xe) * 0.99975586f > G)) {
+          cold = true;   // b* = 1 not certified: the generic exact branch-and-bound decides
+        } else {
+          knee = lmin[Sk];
+          const uint32_t le = lmin[Se];
+          demand = le + (uint32_t)p.margin < (uint32_t)L ? le + (uint32_t)p.margin : (uint32_t)L;
+          if (a.dtab_rows) {   // d_j(1) = ceil(X(S(g), 1) / (S(g) M Delta)) at g = demand
+            const uint32_t Sg = Stab[demand];
+            const uint64_t Xg = Sg == Se ? Xe : lane_X_at(H, Sg, C1, Mtp, base, myD, myWsm, mem_mode);
+            dslots = ceil_div_clamp16_fast(Xg, (uint64_t)Sg * M * (uint64_t)p.slot_us);
+          }
+        }
+      }
+    }
+    // ---- outputs of the lanes' DNNs (coalesced: lane j writes DNN kb + j) ----
+    if (have && !cold) {
+      const bool okst = st == DSTACK_ST_OK;
+      if (a.ws_RT) { a.ws_RT[kl] = myRT; a.ws_D[kl] = myD; }
+      if (okst) {
+        if (a.dstar) a.dstar[kl] = (uint16_t)dslots;
+        else if (a.dtab_rows) a.dtab_rows[kl * DTAB_ROW] = (uint16_t)dslots;
+      }
+      if (a.knee) a.knee[kl] = okst ? (uint16_t)knee : 0;
+      if (a.status) a.status[kl] = (uint8_t)st;
+      if (a.demand) a.demand[kl] = okst ? (uint16_t)demand : 0;
+      if (a.batch) a.batch[kl] = okst ? 1 : 0;
+    }
+    // ---- the generic path for the DNNs outside the fast ranges ----
+    uint32_t colds = __ballot_sync(FULL, have && cold);
+    while (colds) {
+      const int j = __ffs(colds) - 1;
+      colds &= colds - 1;
+      prof_one_cold(&a, kb + j, Stab, hist, cA, cU, lane);
+    }
+    __syncwarp();
+  }
+}
+
 size_t prof_smem_bytes(const dstack_params_t *p, int warps) {
   return (size_t)(((p->L + 1 + p->S_tot + 1) * 2 + 15) & ~15) + (size_t)warps * prof_warp_bytes(p->S_tot) +
          (size_t)warps * FAST_STAGE_BYTES;
+}
+size_t plane_smem_bytes(const dstack_params_t *p, int warps) {
+  return (size_t)(((p->L + 1 + p->S_tot + 1) * 2 + 15) & ~15) + (size_t)warps * plane_warp_bytes(p->S_tot);
 }
 
 template <typename KernelT>
@@ -521,7 +883,16 @@ int launch_prof(const ProfArgs &a, cudaStream_t s, int *launches) {
     const int64_t wave = (int64_t)num_sms() * DSTACK_PROF_MINB;
     if (blocks > wave) blocks = wave;
   }
-  if (fast && a.p.S_tot < 5 * 32) launch_k(k_prof_fast<5>, b, blocks, threads, smem, s);
+  if (fast && DSTACK_PROF_LANE) {
+    // k_prof_lane: one resident wave of warps pulling groups of 32 DNNs (grid stride over groups without a counter)
+    const size_t sm2 = plane_smem_bytes(&a.p, warps);
+    cudaFuncSetAttribute(k_prof_lane, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    const int64_t groups = (a.pb.num_dnn + 31) / 32;
+    int64_t nb = (groups + warps - 1) / warps;
+    const int64_t wave = resident_wave(k_prof_lane, threads, sm2, nb);
+    if (b.work_ctr || nb > wave) nb = wave;
+    k_prof_lane<<<(unsigned)nb, threads, sm2, s>>>(b);
+  } else if (fast && a.p.S_tot < 5 * 32) launch_k(k_prof_fast<5>, b, blocks, threads, smem, s);
   else if (fast) launch_k(k_prof_fast<9>, b, blocks, threads, smem, s);
   else if (a.p.par_mode == 0) launch_k(k_prof<0>, b, blocks, threads, smem, s);
   else launch_k(k_prof<1>, b, blocks, threads, smem, s);
