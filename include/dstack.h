@@ -246,6 +246,22 @@ int dstack_compare(const dstack_problem_t *pb, const dstack_params_t *p, const u
                    const uint32_t *alloc_q16, double *u, double *thr, double *jain, void *ws, size_t ws_bytes,
                    void *stream);
 
+/* O9b max-throughput, the §6.3 comparison "a schedule that maximizes the sum of the throughput across all the
+ * models" (reading R24; the paper's ">80%" comparison at P:2582).  Per scenario, on the
+ * a3/a4 outputs (demand, batch = b*, alloc_q16, e.g. from dstack_eval_batch): the session T = max SLO over the active
+ * DNNs (demand > 0) and their levels g_j = max(demand_j, floor(alloc_j)) as in D-STACK's session; every schedule of
+ * non-overlapping runs of a batch b in [b_min, b*_j] lasting d_j(b) = ceil(X(S(g_j), b) / (S(g_j) M Delta)) slots per
+ * DNN, starting at slot boundaries, ending by the session end, with the summed level of the runs in progress <= L at
+ * every slot, is searched exactly (dynamic programming over the slots left of every DNN's run in progress).
+ *   served_out[s] = the largest number of requests such a schedule serves (throughput = served * 1e6 / T_us);
+ *   st_out[s] = DSTACK_ST_OK, DSTACK_ST_INFEASIBLE (no active DNN), or DSTACK_ST_INVALID (more than 8 active DNNs,
+ *   more than DSTACK_MAX_SLOTS slots, or a state space prod_j (max_b d_j(b) + 1) above 8192): exact search is for
+ *   small instances only.  Device u32 / u8 arrays [num_scen].  Workspace: dstack_workspace_size();
+ *   DSTACK_FLAG_BELOW_KNEE is rejected (DSTACK_EINVAL). */
+int dstack_max_throughput(const dstack_problem_t *pb, const dstack_params_t *p, const uint16_t *demand,
+                          const uint8_t *batch, const uint32_t *alloc_q16, uint32_t *served_out, uint8_t *st_out,
+                          void *ws, size_t ws_bytes, void *stream);
+
 /* F4 multi-GPU cluster of §7.1 ("one T4 GPU for each DNN model exclusively",
  * "all 4 models in each GPU, temporally sharing the GPU", "D-STACK with the 4 DNN models"; reading R23,
  * DESIGN.md §3.5): `gpus` = G modelled GPUs of L levels (1 <= G <= 32) serve each scenario's active models

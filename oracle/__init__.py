@@ -82,6 +82,8 @@ def lib():
         L.oracle_gslice_direct.argtypes = ([C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]
                                            + [C.c_void_p] * 5)
         L.oracle_compare.argtypes = [P(OrProblem), P(OrParams)] + [C.c_void_p] * 4 + [C.c_int64, C.c_int32]
+        L.oracle_maxthr_direct.argtypes = ([C.c_int32] + [C.c_void_p] * 3 + [C.c_int32] * 3 + [C.c_int64, C.c_void_p])
+        L.oracle_maxthr.argtypes = ([P(OrProblem), P(OrParams), C.c_int64] + [C.c_void_p] * 4 + [C.c_int64, C.c_int32])
         L.oracle_cluster.argtypes = [P(OrProblem), P(OrParams), C.c_int32] + [C.c_void_p] * 3 + [C.c_int64, C.c_int32]
         L.oracle_simulate.argtypes = [P(OrProblem), P(OrParams), C.c_void_p, C.c_int32, C.c_uint64, C.c_int32,
                                       C.c_int64, P(OrSimOut), C.c_void_p, C.c_int64, C.c_int32]
@@ -240,6 +242,36 @@ def compare(pb: Problem, p: Params, nthreads: int = 0, subset=None):
                               0 if idx is None else idx.shape[0], nthreads)
     assert rc == 0
     return dict(u=u, thr=thr, jain=jain)
+
+
+MAXTHR_STATES = 8192   # state-space cap shared with the CUDA path (R24)
+
+
+def maxthr_direct(g, bstar, dtab, b_lo: int, L: int, nslots: int, max_states: int = 1 << 22):
+    """O9b max-throughput with direct inputs: the largest number of requests any session schedule serves (runs of
+    batch b <= b*_j lasting dtab[j, b-1] slots at level g_j, capacity L); None if the state space exceeds
+    max_states."""
+    g = np.ascontiguousarray(g, np.int32); bs = np.ascontiguousarray(bstar, np.int32)
+    n = g.shape[0]
+    dt = np.zeros((n, 64), np.int64)
+    dtab = np.asarray(dtab, np.int64)
+    if n:
+        dt[:, : dtab.shape[1]] = dtab
+    best = C.c_int64()
+    rc = lib().oracle_maxthr_direct(n, _p(g), _p(bs), _p(dt), b_lo, L, nslots, max_states, C.byref(best))
+    return None if rc != 0 else int(best.value)
+
+
+def maxthr(pb: Problem, p: Params, max_states: int = MAXTHR_STATES, nthreads: int = 0, subset=None):
+    """O9b per scenario on the eval path's quantities: dict(served int64, status u8, T_us int64) [scenarios of
+    `subset` in order, or all]."""
+    idx = None if subset is None else np.ascontiguousarray(np.asarray(list(subset)), np.int64)
+    n = pb.num_scen if idx is None else idx.shape[0]
+    served = np.zeros(n, np.int64); st = np.zeros(n, np.uint8); T = np.zeros(n, np.int64)
+    rc = lib().oracle_maxthr(C.byref(_problem(pb)), C.byref(_params(p)), max_states, _p(served), _p(st), _p(T),
+                             _p(idx), 0 if idx is None else n, nthreads)
+    assert rc == 0
+    return dict(served=served, status=st, T_us=T)
 
 
 CLUSTER_NAMES = ("exclusive", "temporal", "dstack", "dstack_ffd")

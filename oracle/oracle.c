@@ -916,6 +916,132 @@ int oracle_compare(const or_problem_t *pb, const or_params_t *p, double *u, doub
   return 0;
 }
 
+/* ------------------------------------------------------------ O9b ---
+ * Max-throughput (§6.3): "a schedule that maximizes the sum of the throughput across all the models".
+ * Reading R24: over one session of nslots slots, every active model j runs at its session level
+ * g_j (the level D-STACK's session uses), as any sequence of non-overlapping runs of a batch b in [b_lo, b*_j]
+ * lasting d_j(b) slots, starting at slot boundaries and ending by the session end, with the summed level of the
+ * runs in progress <= L at every slot (Eq. 14); the value is the number of requests served, sum of b over all runs
+ * (throughput = served / T).  No SLO window: it is the throughput ceiling D-STACK is compared with (any D-STACK
+ * session is one such schedule, so D-STACK <= max-throughput).
+ * Exhaustive search over the schedules, memoised on the state: r_j = slots left of model j's run in progress
+ * (0 = idle).  V_t(r) = max over the starts at t (each idle model: none, or one batch b with t + d_j(b) <= nslots)
+ * whose occupancy at t stays <= L, of (sum b of the starts) + V_{t+1}(r - 1); V_nslots = 0; the answer is V_0(0).
+ * Returns -1 when the state space prod_j (max_b d_j(b) + 1) exceeds max_states (the instance is too large). */
+int oracle_maxthr_direct(int32_t n, const int32_t *g, const int32_t *bstar, const int64_t *dtab, int32_t b_lo,
+                         int32_t L, int32_t nslots, int64_t max_states, int64_t *best) {
+  if (n < 0 || n > 16 || nslots < 0) return -1;
+  int64_t D[16], radix[16], nst = 1;
+  for (int32_t j = 0; j < n; ++j) {
+    D[j] = 0;
+    if (g[j] > 0)
+      for (int32_t b = b_lo; b <= bstar[j]; ++b) if (dtab[(int64_t)j * 64 + b - 1] > D[j]) D[j] = dtab[(int64_t)j * 64 + b - 1];
+    radix[j] = nst;
+    if (D[j] + 1 > max_states) return -1;
+    nst *= D[j] + 1;
+    if (nst > max_states) return -1;
+  }
+  int64_t *V = (int64_t *)calloc((size_t)nst, sizeof(int64_t));      /* V_{t+1} */
+  int64_t *W = (int64_t *)calloc((size_t)nst, sizeof(int64_t));      /* V_t */
+  int64_t r[16], c[16];
+  for (int32_t t = nslots - 1; t >= 0; --t) {
+    for (int64_t st = 0; st < nst; ++st) {
+      for (int32_t j = 0; j < n; ++j) r[j] = (st / radix[j]) % (D[j] + 1);
+      /* every combination of choices: c[j] = 0 (keep / idle) or a batch b (an idle active model starts b) */
+      for (int32_t j = 0; j < n; ++j) c[j] = 0;
+      int64_t bestv = -1;
+      while (1) {
+        int64_t occ = 0, gain = 0, nxt = 0;
+        int ok = 1;
+        for (int32_t j = 0; j < n && ok; ++j) {
+          int64_t rr = r[j];
+          if (c[j] > 0) {                                   /* start a run of batch c[j] */
+            const int64_t d = dtab[(int64_t)j * 64 + c[j] - 1];
+            if (d < 1 || t + d > nslots) ok = 0;
+            rr = d; gain += c[j];
+          }
+          if (rr > 0) occ += g[j];
+          nxt += (rr > 0 ? rr - 1 : 0) * radix[j];
+        }
+        if (ok && occ <= L) {
+          const int64_t v = gain + V[nxt];
+          if (v > bestv) bestv = v;
+        }
+        /* next combination (odometer over the idle active models' choices 0, b_lo..b*) */
+        int32_t j = 0;
+        for (; j < n; ++j) {
+          if (r[j] > 0 || g[j] <= 0) continue;
+          if (c[j] == 0) { c[j] = b_lo; break; }
+          if (c[j] < bstar[j]) { ++c[j]; break; }
+          c[j] = 0;
+        }
+        if (j == n) break;
+      }
+      W[st] = bestv < 0 ? 0 : bestv;   /* a state whose running models alone exceed L is unreachable */
+    }
+    int64_t *tmp = V; V = W; W = tmp;
+  }
+  *best = nslots > 0 ? V[0] : 0;
+  free(V); free(W);
+  return 0;
+}
+
+/* O9b per scenario on the eval path's quantities (O3 demand / b*, O4 levels g_j, session T = max SLO, d_j(b) at g_j
+ * from O1): served_out[q] = the max-throughput served count, st_out[q] = OR_OK, OR_INFEASIBLE (nothing servable)
+ * or OR_INVALID (more than 8 active models, a session over OR_MAX_SLOTS, or a state space over max_states). */
+int oracle_maxthr(const or_problem_t *pb, const or_params_t *p, int64_t max_states, int64_t *served_out,
+                  uint8_t *st_out, int64_t *T_out, const int64_t *idx, int64_t count, int32_t nthreads) {
+  if (!pb || !p || !served_out || !st_out || check_params(p)) return -1;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+  const int64_t nq = idx ? count : pb->num_scen;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t q = 0; q < nq; ++q) {
+    const int64_t s = idx ? idx[q] : q;
+    served_out[q] = 0; st_out[q] = OR_INVALID; if (T_out) T_out[q] = 0;
+    const int32_t k0 = pb->scen_dnn_off[s], nd = pb->scen_dnn_off[s + 1] - k0;
+    if (nd > OR_MAX_DNN_PER_SCEN) continue;
+    uint16_t dem[OR_MAX_DNN_PER_SCEN], knee[OR_MAX_DNN_PER_SCEN];
+    uint8_t bt[OR_MAX_DNN_PER_SCEN], st[OR_MAX_DNN_PER_SCEN];
+    uint32_t alloc[OR_MAX_DNN_PER_SCEN];
+    for (int32_t j = 0; j < nd; ++j) {
+      dnn_t m = get_dnn(pb, p, k0 + j);
+      batch_opt_one(&m, p, dem + j, bt + j, knee + j, st + j);
+      if (st[j] != OR_OK) dem[j] = 0;
+    }
+    oracle_wmaxmin(nd, dem, p->L, alloc);
+    int64_t T = 0;
+    int32_t nact = 0;
+    for (int32_t j = 0; j < nd; ++j) if (dem[j] > 0) { ++nact; if (pb->slo_us[k0 + j] > T) T = pb->slo_us[k0 + j]; }
+    if (T == 0) { st_out[q] = OR_INFEASIBLE; continue; }
+    const int64_t nslots = T / p->slot_us;
+    if (nact > 8 || nslots > OR_MAX_SLOTS) continue;
+    int32_t g[8], bst[8];
+    int64_t dtab[8 * 64];
+    int32_t n = 0;
+    for (int32_t j = 0; j < nd; ++j) {
+      if (dem[j] == 0) continue;
+      const int32_t al = (int32_t)(alloc[j] >> 16);
+      g[n] = dem[j] > al ? dem[j] : al;
+      bst[n] = bt[j];
+      dnn_t m = get_dnn(pb, p, k0 + j);
+      const int64_t S = S_of(p, g[n]);
+      const u128 den = (u128)S * (u128)m.M * (u128)p->slot_us;
+      for (int32_t b = p->b_min; b <= bst[n]; ++b) {
+        const u128 dd = (X_of(&m, p, S, b) + den - 1) / den;
+        dtab[n * 64 + b - 1] = dd > (u128)0x7FFFFFFF ? 0x7FFFFFFF : (int64_t)dd;
+      }
+      ++n;
+    }
+    int64_t best = 0;
+    if (oracle_maxthr_direct(n, g, bst, dtab, p->b_min, p->L, (int32_t)nslots, max_states, &best) != 0) continue;
+    served_out[q] = best; st_out[q] = OR_OK;
+    if (T_out) T_out[q] = T;
+  }
+  return 0;
+}
+
 /* ---------------------------------------------------------------- F4 ---
  * Multi-GPU cluster of §7.1 (reading R23): G modelled GPUs
  * of L levels each serve the scenario's active models (status OK).  out[s*4 + c]:

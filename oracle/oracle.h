@@ -122,6 +122,10 @@ int oracle_compare(const or_problem_t *pb, const or_params_t *p, double *u, doub
 /* F4 multi-GPU cluster of §7.1: G modelled GPUs; out[s*4 + c], c = 0 exclusive (round robin,
  * temporal within a GPU), 1 temporal on every GPU, 2 D-STACK on every GPU, 3 D-STACK with first-fit-decreasing
  * placement; U = mean over the G GPUs, throughput = sum (req/s). */
+int oracle_maxthr_direct(int32_t n, const int32_t *g, const int32_t *bstar, const int64_t *dtab, int32_t b_lo,
+                         int32_t L, int32_t nslots, int64_t max_states, int64_t *best);
+int oracle_maxthr(const or_problem_t *pb, const or_params_t *p, int64_t max_states, int64_t *served_out,
+                  uint8_t *st_out, int64_t *T_out, const int64_t *idx, int64_t count, int32_t nthreads);
 int oracle_cluster(const or_problem_t *pb, const or_params_t *p, int32_t G, double *u, double *thr,
                    const int64_t *idx, int64_t count, int32_t nthreads);
 

@@ -417,6 +417,25 @@ int dstack_compare(const dstack_problem_t *pb, const dstack_params_t *p, const u
   return finish(launch_compare(c, (cudaStream_t)stream, &g_launches));
 }
 
+int dstack_max_throughput(const dstack_problem_t *pb, const dstack_params_t *p, const uint16_t *demand,
+                          const uint8_t *batch, const uint32_t *alloc_q16, uint32_t *served_out, uint8_t *st_out,
+                          void *ws, size_t ws_bytes, void *stream) {
+  g_launches = 0;
+  if (!problem_ok(pb) || !params_ok(p) || (p->flags & DSTACK_FLAG_BELOW_KNEE)) return DSTACK_EINVAL;
+  if (pb->num_dnn > 0 && (!demand || !batch || !alloc_q16)) return DSTACK_EINVAL;
+  if (pb->num_scen > 0 && (!served_out || !st_out)) return DSTACK_EINVAL;
+  if (!disjoint(pb, served_out) || !disjoint(pb, st_out) || (const void *)served_out == (const void *)st_out)
+    return DSTACK_EINVAL;
+  const size_t need = dstack_workspace_size(pb, p);
+  if (ws_bytes < need || (need > 0 && !ws)) return DSTACK_EWORKSPACE;
+  if (!have_device()) return DSTACK_ELAUNCH;
+  MtArgs m;
+  std::memset(&m, 0, sizeof(m));
+  m.pb = *pb; m.p = *p; m.demand = demand; m.batch = batch; m.alloc = alloc_q16; m.served = served_out; m.st = st_out;
+  m.work_ctr = (uint32_t *)((char *)ws + ws_layout(pb, p).ctr) + 10;
+  return finish(launch_maxthr(m, (cudaStream_t)stream, &g_launches));
+}
+
 int dstack_cluster(const dstack_problem_t *pb, const dstack_params_t *p, int32_t gpus, const uint16_t *demand,
                    const uint8_t *batch, double *u, double *thr, void *ws, size_t ws_bytes, void *stream) {
   g_launches = 0;

@@ -106,6 +106,17 @@ struct CmpArgs {
   uint32_t *work_ctr;       // workspace word: scenario counter (NULL: grid stride)
 };
 
+struct MtArgs {   // O9b max-throughput (maxthr.cu)
+  dstack_problem_t pb;
+  dstack_params_t p;
+  const uint16_t *demand;
+  const uint8_t *batch;
+  const uint32_t *alloc;
+  uint32_t *served;
+  uint8_t *st;
+  uint32_t *work_ctr;
+};
+
 struct AggArgs {
   int32_t num_scen;
   const int32_t *off;
@@ -127,6 +138,7 @@ int launch_sim(const SimArgs &a, cudaStream_t s, int *launches);
 size_t sim_fill_log_bytes();
 int launch_agg(const AggArgs &a, cudaStream_t s, int *launches);
 int launch_compare(const CmpArgs &a, cudaStream_t s, int *launches);
+int launch_maxthr(const MtArgs &a, cudaStream_t s, int *launches);
 int launch_unpack_nr(int64_t num_rows, const uint16_t *nr, uint32_t *n, uint16_t *r, cudaStream_t s, int *launches);
 int launch_unpack_w5(int64_t num_rows, const uint32_t *w, const uint8_t *lo, uint32_t *n, uint16_t *r, uint32_t *d,
                      cudaStream_t s, int *launches);

@@ -96,6 +96,7 @@ def _load():
     lib.dstack_cluster.argtypes = [P(CProblem), P(CParams), C.c_int32] + [C.c_void_p] * 5 + [C.c_size_t, C.c_void_p]
     lib.dstack_unpack_nr.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.dstack_unpack_w5.argtypes = [C.c_int64] + [C.c_void_p] * 6
+    lib.dstack_max_throughput.argtypes = [P(CProblem), P(CParams)] + [C.c_void_p] * 6 + [C.c_size_t, C.c_void_p]
     lib.dstack_ideal_stats.argtypes = [P(CProblem), P(CParams), C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
     lib.dstack_profile_start.argtypes = [C.c_int32]
     lib.dstack_profile_stop.argtypes = [C.c_void_p, C.c_void_p]
@@ -109,7 +110,7 @@ _lib = _load()
 # every symbol include/dstack.h declares (checked by tests/test_abi.py)
 EXPORTS = ("dstack_workspace_size", "dstack_knee", "dstack_knee_probe", "dstack_batch_opt", "dstack_wmaxmin", "dstack_schedule_cycle",
            "dstack_eval_batch", "dstack_aggregate", "dstack_sim_workspace_size", "dstack_simulate",
-           "dstack_compare", "dstack_cluster", "dstack_unpack_nr", "dstack_unpack_w5", "dstack_profile_start", "dstack_profile_stop",
+           "dstack_compare", "dstack_cluster", "dstack_max_throughput", "dstack_unpack_nr", "dstack_unpack_w5", "dstack_profile_start", "dstack_profile_stop",
            "dstack_last_launch_count", "dstack_ideal_stats", "dstack_status_str", "dstack_version")
 
 
@@ -356,6 +357,20 @@ def compare(dp: DeviceProblem, p, demand, batch, alloc_q16, out=None, ws: Worksp
                                _ptr(out["u"]), _ptr(out["thr"]), _ptr(out["jain"]), ws.ptr(), ws.nbytes,
                                _stream(dev)), "dstack_compare")
     return out
+
+
+def max_throughput(dp: DeviceProblem, p, demand, batch, alloc_q16, ws: "Workspace | None" = None):
+    """dstack_max_throughput (O9b): (served u32-in-int32 [num_scen], status u8 [num_scen]) device tensors."""
+    dev = dp.device
+    S = max(dp.num_scen, 1)
+    served = torch.zeros(S, dtype=torch.int32, device=dev)
+    st = torch.zeros(S, dtype=torch.uint8, device=dev)
+    if ws is None:
+        ws = Workspace(workspace_size(dp, p), dev)
+    _check(_lib.dstack_max_throughput(C.byref(dp.c()), C.byref(cparams(p)), _ptr(demand), _ptr(batch), _ptr(alloc_q16),
+                                      _ptr(served), _ptr(st), ws.ptr(), ws.nbytes, _stream(dev)),
+           "dstack_max_throughput")
+    return served[: dp.num_scen], st[: dp.num_scen]
 
 
 PROF_SLOTS = ("k_prof", "k_wmaxmin", "k_cycle", "k_ideal", "k_agg")

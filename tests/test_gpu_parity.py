@@ -628,3 +628,50 @@ def test_unpack_w5_round_trip(ds):
     torch.cuda.synchronize()
     assert torch.equal(n2[:R], g["n"][:R]) and torch.equal(r2[:R], g["r"][:R]) and torch.equal(d2[:R], g["d"][:R])
     assert int((n2[R:] != -1).sum()) == 0 and int((r2[R:] != -1).sum()) == 0 and int((d2[R:] != -1).sum()) == 0
+
+
+def maxthr_workload(n, variant="default", rows_pct=20):
+    """Config-2 mixes (<= 5 DNNs) with 2.5 ms slots: sessions of 10-40 slots, run lengths of a few slots -- the
+    small instances the exact max-throughput search (O9b) is for."""
+    sp, p = synth.config(2, num_scen=n, rows_pct=rows_pct, variant=variant)
+    sp = sp.replace(slot_us=2500, slo_min_slots=10, slo_max_slots=40, ndnn_max=5)
+    return sp, p.replace(slot_us=2500, ideal=0)
+
+
+@pytest.mark.parametrize("variant", ["default", "batching"])
+def test_max_throughput_parity(ds, variant):
+    """O9b (dstack_max_throughput) against the oracle's exhaustive search: served count and status bit-exact per
+    scenario; every OK scenario serves at least D-STACK's own session count."""
+    sp, p = maxthr_workload(300 if variant == "default" else 120, variant)
+    pb = synth.generate_host(sp)
+    dp = ds.from_host(pb, "cuda")
+    o = ds.eval_batch(dp, p)
+    served, st = ds.max_throughput(dp, p, o["demand"], o["batch"], o["alloc_q16"])
+    torch.cuda.synchronize()
+    want = oracle.maxthr(pb, p)
+    assert np.array_equal(st.cpu().numpy(), want["status"])
+    assert np.array_equal(served.cpu().numpy().astype(np.int64), want["served"])
+    ok = want["status"] == oracle.OK
+    assert ok.sum() > 0.5 * pb.num_scen
+    g = ds.to_numpy(o, pb.num_scen, pb.num_dnn)
+    dst = np.rint(g["thr"] * g["T_us"] / 1e6).astype(np.int64)
+    assert (want["served"][ok] >= dst[ok]).all()
+    if variant == "batching":
+        assert (want["served"][ok] > dst[ok]).any()
+
+
+def test_max_throughput_caps(ds):
+    """O9b beyond its exact-search caps (100 us slots: run lengths of ~60 slots, so 3+ DNNs exceed 8192 states; and
+    9-12 DNN mixes exceed 8 active DNNs): the same INVALID / OK split and counts as the oracle."""
+    sp, p = synth.config(2, num_scen=60, rows_pct=20)
+    sp = sp.replace(ndnn_min=2, ndnn_max=12)
+    p = p.replace(ideal=0)
+    pb = synth.generate_host(sp)
+    dp = ds.from_host(pb, "cuda")
+    o = ds.eval_batch(dp, p)
+    served, st = ds.max_throughput(dp, p, o["demand"], o["batch"], o["alloc_q16"])
+    torch.cuda.synchronize()
+    want = oracle.maxthr(pb, p)
+    assert np.array_equal(st.cpu().numpy(), want["status"])
+    assert np.array_equal(served.cpu().numpy().astype(np.int64), want["served"])
+    assert (want["status"] == oracle.INVALID).any() and (want["status"] == oracle.OK).any()
