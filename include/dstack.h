@@ -231,14 +231,16 @@ int dstack_simulate(const dstack_problem_t *pb, const dstack_params_t *p, const 
  *   jain[s*DSTACK_NCMP + c] Jain's index (sum x)^2 / (n sum x^2) of the per-model GPU time x_j (slots)
  * c = DSTACK_CMP_DSTACK: the D-STACK session (identical to dstack_schedule_cycle's u / thr);
  *     DSTACK_CMP_MAXMIN: same session, fill in ascending (GPU%, index) order (Max-Min fair);
- *     DSTACK_CMP_MAXTHR: same session, fill in ascending (run time of b*, index) order (max-throughput);
+ *     DSTACK_CMP_SRF_STRUCK: same session, fill in ascending (run time of b*, index) order -- "shortest run first",
+ *     the procedure of the STRUCK text at P:2540 ("by prioritizing scheduling the model with the least runtime");
+ *     the live definition of max-throughput is dstack_max_throughput (O9b);
  *     DSTACK_CMP_TEMPORAL: slices proportional to SLO at 100% GPU, knee% accounting;
  *     DSTACK_CMP_GSLICE: static spatial sharing at the knees, residents + first-fit decreasing time slots.
  * Scenarios that are INVALID / INFEASIBLE for the D-STACK session get zeros.  All pointers are device
  * pointers; u/thr/jain are [num_scen * DSTACK_NCMP] f64.  Workspace: dstack_workspace_size() (d_j(b) rows). */
 #define DSTACK_CMP_DSTACK 0
 #define DSTACK_CMP_MAXMIN 1
-#define DSTACK_CMP_MAXTHR 2
+#define DSTACK_CMP_SRF_STRUCK 2
 #define DSTACK_CMP_TEMPORAL 3
 #define DSTACK_CMP_GSLICE 4
 #define DSTACK_NCMP 5

@@ -229,7 +229,7 @@ def gslice_direct(lvl, dk, nslots: int, L: int):
     return dict(home=home, nbins=K.value, runs=runs, busy=busy, occ_num=occ.value)
 
 
-CMP_NAMES = ("dstack", "maxmin", "maxthr", "temporal", "gslice")
+CMP_NAMES = ("dstack", "maxmin", "srf_struck", "temporal", "gslice")
 
 
 def compare(pb: Problem, p: Params, nthreads: int = 0, subset=None):

@@ -304,7 +304,7 @@ def eval_batch(dp: DeviceProblem, p, out=None, ws: Workspace | None = None, agg=
     return o
 
 
-CMP_NAMES = ("dstack", "maxmin", "maxthr", "temporal", "gslice")   # DSTACK_CMP_* order
+CMP_NAMES = ("dstack", "maxmin", "srf_struck", "temporal", "gslice")   # DSTACK_CMP_* order
 CLU_NAMES = ("exclusive", "temporal", "dstack", "dstack_ffd")         # DSTACK_CLU_* order
 
 
