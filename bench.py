@@ -65,6 +65,11 @@ def parse():
 L2_BYTES = 126 * 2 ** 20   # B200 L2 (B200_PROFILING.md)
 
 
+def shard_bounds(n, rank, world):
+    from paper_2304_13541_b200.dist import shard
+    return shard(n, rank, world)
+
+
 def shard_of(args, sp0, rank, world):
     """(spec of this rank's shard, scenarios over all ranks, this rank's scenarios).  Strong scaling: the
     contiguous global-index shard [g n / G, (g + 1) n / G) (dist.shard); weak: rank g evaluates
@@ -533,6 +538,8 @@ def run_native(args, rank, world, local):
         "cluster": clu_line,
         "max_throughput": mt_line,
         "selection": sel_stats,
+        "shards": ([list(shard_bounds(n_total, r, world)) for r in range(world)] if args.scaling == "strong" else
+                   [[r * n_rank, (r + 1) * n_rank] for r in range(world)]),
         "stats": {"mean_u": agg["sum_u"] / max(agg["n_scen_scheduled"], 1),
                   "mean_u_static": agg["sum_u_static"] / max(agg["n_scen_scheduled"], 1),
                   "mean_u_ideal": agg["sum_u_ideal"] / max(agg["n_scen_scheduled"], 1) if p.ideal else None,
