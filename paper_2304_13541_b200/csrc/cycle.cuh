@@ -46,7 +46,7 @@ struct BelowKnee {
 
 
 struct CycSmem {
-  uint8_t occ[DSTACK_MAX_SLOTS];
+  uint8_t occ[DSTACK_MAX_SLOTS + 128];   // + one register window of padding (never read as session slots)
   uint32_t dmask[DSTACK_MAX_SLOTS / 32];   // decision times (bit u of word w <=> slot 32 w + u)
   uint32_t sr[DSTACK_MAX_JOBS];   // static job (j, r): start | run slots << 16, or NONE32 (miss)
 };
@@ -122,7 +122,7 @@ __device__ __forceinline__ int find_early_packed(const uint8_t *occ, int rel, in
   int s = rel;
   while (s + d <= dl) {
     const int bt = s & ~3, wi = (bt >> 2) + lane, mybase = bt + 4 * lane;
-    const uint32_t word = wi < DSTACK_MAX_SLOTS / 4 ? w32[wi] : 0u;
+    const uint32_t word = w32[wi];   // padded array
     const uint32_t bb = __vcmpgtu4(word, th) & bytes_mask(s, s + d, mybase);   // blocking slots in the run
     const uint32_t lb = bb ? (uint32_t)(mybase + ((31 - __clz(bb)) >> 3) + 1) : 0u;
     const uint32_t last = __reduce_max_sync(FULL, lb);   // (last blocking slot) + 1, or 0
@@ -138,7 +138,7 @@ __device__ __forceinline__ int find_late_packed(const uint8_t *occ, int rel, int
   int s = dl - d;
   while (s >= rel) {
     const int bt = s & ~3, wi = (bt >> 2) + lane, mybase = bt + 4 * lane;
-    const uint32_t word = wi < DSTACK_MAX_SLOTS / 4 ? w32[wi] : 0u;
+    const uint32_t word = w32[wi];   // padded array
     const uint32_t bb = __vcmpgtu4(word, th) & bytes_mask(s, s + d, mybase);
     const uint32_t fb = bb ? (uint32_t)(mybase + ((__ffs(bb) - 1) >> 3)) : 0xFFFFFFFFu;
     const uint32_t first = __reduce_min_sync(FULL, fb);   // first blocking slot, or none
@@ -150,7 +150,7 @@ __device__ __forceinline__ int find_late_packed(const uint8_t *occ, int rel, int
 
 __device__ __forceinline__ uint32_t bytes_mask(int s, int e, int base) {
   const int lo = min(max(s - base, 0), 4), hi = min(max(e - base, 0), 4);
-  return (uint32_t)((0xFFFFFFFFull << (8 * lo)) & (0xFFFFFFFFull >> (32 - 8 * hi)));
+  return __funnelshift_lc(0u, 0xFFFFFFFFu, (uint32_t)(8 * lo)) & __funnelshift_rc(0xFFFFFFFFu, 0u, (uint32_t)(32 - 8 * hi));
 }
 
 // occ[u] += g for u in [s, s+d): 4 slots per lane per step (packed u32; callers guarantee occ + g <= L <= 255,
@@ -339,27 +339,28 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   }
   res.occ_static = occ_sum(sm.occ, nslots, lane);
   // ---- opportunistic fill at decision times {0} u {run ends} (Dynamic-schedule) ----
-  // Per decision time t the warp holds the occupancy of slots [t & ~3, (t & ~3) + 128) in registers (one packed
-  // word per lane); slice queries and placements inside that window touch no shared memory except the
-  // write-through of placed runs.  Longer runs fall back to the shared-memory scans.
+  // Decision times are visited in increasing order.  With nslots <= 1024 they live in one register word per
+  // lane and are consumed (bit t cleared when t is visited; every time set later is > t).  Per decision time t
+  // the warp holds the occupancy of slots [t & ~3, (t & ~3) + 128) in registers (one packed word per lane);
+  // slice queries and placements inside that window touch no shared memory except the write-through of placed
+  // runs.  Longer runs fall back to the shared-memory scans.
+  // Per lane (DNN): free_at = end of its current run (static or fill); [ns, ne) = its next placed static run not
+  // yet begun (ns = nslots when none).  Static runs that began by t are folded into free_at, so the DNN is
+  // running at t <=> t < free_at, and ns is its next own static start after t (a fill run's slice stops there).
   dset(0);
   __syncwarp();
   uint32_t count = runs + count0;
-  int fs = -1, fe = -1;       // last fill run of this lane's DNN
   uint32_t nfill = 0;
-  // this lane's next placed static run not yet over: index p into its windows, start sp, end se
-  int p = 0, sp = -1, se = 0;
-  auto adv = [&](int tt) {
-    while (p < (int)rep) {
-      if (sp < 0) {
-        const uint32_t v = sm.sr[joff + p];
-        sp = v == NONE32 ? -2 : (int)(v & 0xFFFFu);
-        se = sp + (int)(v >> 16);
-      }
-      if (sp == -2 || se <= tt) { ++p; sp = -1; continue; }
-      break;
+  int pnext = 0, ns = nslots, ne = 0, free_at = 0;
+  auto next_static = [&]() {
+    ns = nslots;
+    while (pnext < (int)rep) {
+      const uint32_t v = sm.sr[joff + pnext];
+      ++pnext;
+      if (v != NONE32) { ns = (int)(v & 0xFFFFu); ne = ns + (int)(v >> 16); break; }
     }
   };
+  if (active) next_static();
   const uint32_t pk = (g & 0xFFu) | ((bs & 0xFFu) << 8) | (dstar << 16);   // dstar <= 0xFFFF (u16 rows)
   const int nwords = (nslots + 31) >> 5;
   uint32_t *w32 = reinterpret_cast<uint32_t *>(sm.occ);
@@ -368,18 +369,15 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   int blk = 0;
   int t = -1;
   while (true) {
-    const int start = t + 1;
-    int nt = -1;
     if (dreg) {
-      const int sw = start >> 5;
-      uint32_t v = lane < sw ? 0u : dmw;
-      if (lane == sw) v &= ~((1u << (start & 31)) - 1u);
-      const uint32_t bal = __ballot_sync(FULL, v != 0);
-      if (bal) {
-        const int pl = __ffs(bal) - 1;
-        nt = pl * 32 + __ffs(__shfl_sync(FULL, v, pl)) - 1;
-      }
+      const uint32_t bal = __ballot_sync(FULL, dmw != 0u);
+      if (bal == 0u) break;
+      const int pl = __ffs(bal) - 1;
+      t = pl * 32 + __ffs(__shfl_sync(FULL, dmw, pl)) - 1;
+      if (lane == pl) dmw &= dmw - 1u;
     } else {
+      const int start = t + 1;
+      int nt = -1;
       for (int wb = start >> 5; wb < nwords; wb += 32) {
         const int w = wb + lane;
         uint32_t v = w < nwords ? sm.dmask[w] : 0u;
@@ -391,21 +389,20 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
           break;
         }
       }
+      if (nt < 0) break;
+      t = nt;
     }
-    if (nt < 0 || nt >= nslots) break;
-    t = nt;
+    if (t >= nslots) break;
     if (lane == 0) CSTAT(3, 1);
     const int bt = t & ~3, mybase = bt + 4 * lane, wi = (t >> 2) + lane;
-    uint32_t wv = wi < DSTACK_MAX_SLOTS / 4 ? w32[wi] : 0u;
+    uint32_t wv = w32[wi];   // occ is padded by 128 slots: the window never leaves the array
     const uint32_t lo_mask = lane == 0 ? (0xFFFFFFFFu << (8 * (t & 3))) : 0xFFFFFFFFu;
-    int occ_t = (int)sm.occ[t];   // broadcast byte load
+    uint32_t wvm = wv & lo_mask;   // the window's slots >= t
+    int occ_t = (int)sm.occ[t];    // broadcast byte load
     bool elig = false;
-    int ns = nslots;
-    if (active) {   // eligible: not running at t (static or last fill run), fits at t
-      adv(t);
-      const bool cov_static = p < (int)rep && sp <= t;
-      if (p < (int)rep && sp > t) ns = sp;
-      elig = t >= blk && !cov_static && !(fs <= t && t < fe) && occ_t + (int)g <= L;
+    if (active) {   // eligible: not running at t (static or fill run), fits at t
+      while (t >= ns) { free_at = max(free_at, ne); next_static(); }
+      elig = t >= free_at && t >= blk && occ_t + (int)g <= L;
     }
     // candidates in (runs so far, index) order; a placement raises occ[t], so re-test the rest in parallel
     const uint32_t prio = fill_order == 0 ? count : (fill_order == 1 ? g : dstar);
@@ -419,16 +416,16 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       const uint32_t pj = __shfl_sync(FULL, pk, j);
       const int gj = (int)(pj & 0xFFu), bsj = (int)((pj >> 8) & 0xFFu), dsj = (int)(pj >> 16);
       const int limit = __shfl_sync(FULL, ns, j);
-      // slice: first u in [t, stop) with occ[u] + g > L (stop = min(t + d(b*), next own static start))
-      const int stop = t + dsj < limit ? t + dsj : limit;
+      // slice: first u in [t, stop) with occ[u] + g > L, else stop (stop = min(t + d(b*), next own static start))
+      const int stop = min(t + dsj, limit);
       int kend;
-      if (stop <= bt + 128) {
-        const uint32_t bb = __vcmpgtu4(wv, (uint32_t)(L - gj) * 0x01010101u) & lo_mask & bytes_below(stop, mybase);
-        const uint32_t bal = __ballot_sync(FULL, bb != 0);
+      if (stop <= bt + 128) {   // first blocking slot of the window at or after t, capped at stop
+        const uint32_t bb = __vcmpgtu4(wvm, (uint32_t)(L - gj) * 0x01010101u);
+        const uint32_t bal = __ballot_sync(FULL, bb != 0u);
         kend = stop;
         if (bal) {
           const int pl = __ffs(bal) - 1;
-          kend = bt + 4 * pl + ((__ffs(__shfl_sync(FULL, bb, pl)) - 1) >> 3);
+          kend = min(stop, bt + 4 * pl + ((__ffs(__shfl_sync(FULL, bb, pl)) - 1) >> 3));
         }
       } else {
         kend = first_above(sm.occ, t, stop, L - gj, lane);
@@ -456,17 +453,19 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       if (e <= bt + 128) {   // place inside the window: register word + write-through
         const uint32_t add = ((uint32_t)gj * 0x01010101u) & lo_mask & bytes_below(e, mybase);
         if (add) { wv += add; w32[wi] = wv; }
+        wvm += add;
       } else {
         occ_add(sm.occ, t, dsel, gj, lane);
-        wv = wi < DSTACK_MAX_SLOTS / 4 ? w32[wi] : 0u;
+        wv = w32[wi];
+        wvm = wv & lo_mask;
       }
       occ_t += gj;
-      if (e < nslots) dset(e);
+      if (e < nslots && e > t) dset(e);
       if (lane == 0 && fill_log && nfill < fill_cap) fill_log[nfill] = pack_run((uint32_t)j, (uint32_t)t, (uint32_t)dsel, (uint32_t)bsel);
       nfill++;
       __syncwarp();
       if (lane == j) {
-        count++; runs++; served += (uint32_t)bsel; fs = t; fe = e;
+        count++; runs++; served += (uint32_t)bsel; free_at = e;
         if (busy) *busy += (uint32_t)dsel;
       }
       if (occ_t + (int)g > L) key = 0xFFFFFFFFu;
