@@ -326,6 +326,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     }
     if (st >= 0) {
       occ_add(sm.occ, st, dd, lv, lane);
+      res.occ_static += (uint32_t)dd * (uint32_t)lv;   // sum of occ over the session = sum of d g over its runs
       if (lane == 0) sm.sr[offj + rj] = (uint32_t)st | ((uint32_t)dd << 16);
       if (st + dd < nslots) dset(st + dd);
       if (lane == j) { runs++; served += bs; if (busy) *busy += (uint32_t)dd; }
@@ -337,7 +338,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     if (lane == j) nextr++;
     __syncwarp();
   }
-  res.occ_static = occ_sum(sm.occ, nslots, lane);
+  uint32_t occ_fill = 0;
   // ---- opportunistic fill at decision times {0} u {run ends} (Dynamic-schedule) ----
   // Decision times are visited in increasing order.  With nslots <= 1024 they live in one register word per
   // lane and are consumed (bit t cleared when t is visited; every time set later is > t).  Per decision time t
@@ -460,6 +461,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
         wvm = wv & lo_mask;
       }
       occ_t += gj;
+      occ_fill += (uint32_t)dsel * (uint32_t)gj;
       if (e < nslots && e > t) dset(e);
       if (lane == 0 && fill_log && nfill < fill_cap) fill_log[nfill] = pack_run((uint32_t)j, (uint32_t)t, (uint32_t)dsel, (uint32_t)bsel);
       nfill++;
@@ -471,7 +473,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       if (occ_t + (int)g > L) key = 0xFFFFFFFFu;
     }
   }
-  res.occ_all = occ_sum(sm.occ, nslots, lane);
+  res.occ_all = res.occ_static + occ_fill;   // every run lies inside [0, nslots)
   if (lane == 0) CSTAT(0, 1);
   if (fill_n) *fill_n = nfill;
   res.served_tot = __reduce_add_sync(FULL, served);
