@@ -110,6 +110,9 @@ constexpr int IDEAL_WARPS = 8;
 #ifndef DSTACK_IDEAL_ORDER
 #define DSTACK_IDEAL_ORDER 1   // heavy-first scenario order for k_ideal_sim (A/B switch)
 #endif
+#ifndef DSTACK_IDEAL_SMALL_MITM
+#define DSTACK_IDEAL_SMALL_MITM 1   // 9-10 live items: 5 + 5 meet in the middle, one subset per lane (else enumeration)
+#endif
 #ifndef DSTACK_IDEAL_SHORTCUTS
 #define DSTACK_IDEAL_SHORTCUTS 1   // reuse the selection when no (rank, g) changed; all-fit shortcut (A/B switch)
 #endif
@@ -218,6 +221,65 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
           ++st_fit;
           sel = live;
           gsum = gtot;
+        } else if (n <= 5) {
+          ++st_enum;
+          // <= 32 subsets: one per lane (index bit p <-> rank n-1-p; the largest index among the max-sum subsets is
+          // the lexicographically-first optimum)
+          if (live) grank[rank] = (uint8_t)cur.g;
+          __syncwarp();
+          uint32_t sum = 0;
+#pragma unroll
+          for (int p = 0; p < 5; ++p)
+            if (p < (int)n && ((lane >> p) & 1)) sum += grank[n - 1 - p];
+          const uint32_t best = __reduce_max_sync(FULL, ((uint32_t)lane < (1u << n) && sum <= (uint32_t)L)
+                                                            ? ((sum << 5) | (uint32_t)lane) : 0u);
+          gsum = best >> 5;
+          sel = live && (((best & 31u) >> (n - 1 - rank)) & 1u);
+        } else if (DSTACK_IDEAL_SMALL_MITM && n >= 9 && n <= 10) {
+          ++st_enum;
+          // 9-10 live items: meet in the middle with one subset per lane on each side.  A = the nA = min(n, 5)
+          // highest-priority items (A index bit p <-> rank nA-1-p), B = ranks nA..n-1 (nB <= 5; B index bit p <->
+          // rank n-1-p); lane = subset index on both sides.  The lexicographically-first optimal subset has the
+          // largest (A index, B index), exactly as in the 8 + 8 split below.
+          if (live) grank[rank] = (uint8_t)cur.g;
+          if (lane < 8) mb_bits[lane] = 0u;
+          __syncwarp();
+          const uint32_t nA = n < 5u ? n : 5u, nB = n - nA;
+          uint32_t sA = 0, sB = 0;
+#pragma unroll
+          for (int p = 0; p < 5; ++p) {
+            if (p < (int)nA && ((lane >> p) & 1)) sA += grank[nA - 1 - p];
+            if (p < (int)nB && ((lane >> p) & 1)) sB += grank[n - 1 - p];
+          }
+          const bool bvalid_lane = (uint32_t)lane < (1u << nB);
+          if (bvalid_lane && sB <= (uint32_t)L) atomicOr(&mb_bits[sB >> 5], 1u << (sB & 31));
+          __syncwarp();
+          {   // highest achievable B sum in the words below w (the empty B subset makes sum 0 achievable)
+            const uint32_t wd = lane < 8 ? mb_bits[lane] : 0u;
+            const int h = wd ? 32 * lane + 31 - __clz(wd) : -1;
+            int ex = __shfl_up_sync(FULL, h, 1);
+            if (lane == 0) ex = -1;
+#pragma unroll
+            for (int dd = 1; dd < 8; dd <<= 1) {
+              const int o = __shfl_up_sync(FULL, ex, dd);
+              if (lane >= dd) ex = max(ex, o);
+            }
+            if (lane < 8) mb_below[lane] = ex;
+          }
+          __syncwarp();
+          uint32_t keyA = 0;   // (a + max{B sum <= L - a}, A index); the empty A subset always qualifies
+          if ((uint32_t)lane < (1u << nA) && sA <= (uint32_t)L) {
+            const uint32_t c = (uint32_t)L - sA, w = c >> 5;
+            const uint32_t m = mb_bits[w] & (0xFFFFFFFFu >> (31u - (c & 31u)));
+            const uint32_t mbs = m ? 32u * w + 31u - __clz(m) : (uint32_t)mb_below[w];
+            keyA = ((sA + mbs) << 5) | (uint32_t)lane;
+          }
+          const uint32_t bestA = __reduce_max_sync(FULL, keyA);
+          const uint32_t best = bestA >> 5, ia = bestA & 31u;
+          const uint32_t tb = best - __shfl_sync(FULL, sA, (int)ia);
+          const uint32_t ib = __reduce_max_sync(FULL, (bvalid_lane && sB == tb) ? (uint32_t)lane + 1u : 0u) - 1u;
+          gsum = best;
+          sel = live && (rank < nA ? ((ia >> (nA - 1 - rank)) & 1u) : ((ib >> (n - 1 - rank)) & 1u));
         } else if (n <= DSTACK_IDEAL_ENUM_MAX) {
           ++st_enum;
           sel = false;
