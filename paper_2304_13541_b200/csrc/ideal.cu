@@ -88,8 +88,8 @@ __global__ void __launch_bounds__(256) k_ideal_rows(IdealArgs a) {
 #endif
       const uint64_t den = (uint64_t)bestS * M;
       const uint64_t tau = (bestX + den - 1) / den;
-      a.ex_g[i] = (uint16_t)bestl;
-      a.ex_tau[i] = (uint32_t)(tau > 0xFFFFFFFFull ? 0xFFFFFFFFull : tau);
+      // one 8-byte record per execution for k_ideal_sim: tau | g << 32 | R << 48
+      a.ex_pk[i] = (tau > 0xFFFFFFFFull ? 0xFFFFFFFFull : tau) | ((uint64_t)bestl << 32) | ((uint64_t)a.pb.r[i] << 48);
     }
   }
 }
@@ -128,16 +128,22 @@ __device__ __forceinline__ IdealRow ideal_row_raw(const IdealArgs &a, int64_t i,
   IdealRow w;
   w.i = i;
   w.R = 0; w.tau = 0; w.g = 0;
-  if (i < r1) { w.R = a.pb.r[i]; w.tau = a.ex_tau[i]; w.g = a.ex_g[i]; }
+  if (i < r1) {
+    const uint64_t v = a.ex_pk[i];
+    w.R = (uint32_t)(v >> 48); w.tau = (uint32_t)v; w.g = (uint32_t)(v >> 32) & 0xFFFFu;
+  }
   return w;
 }
 
 __device__ __forceinline__ IdealRow ideal_row_at(const IdealArgs &a, int64_t i, int64_t r1) {
   IdealRow w;
-  while (i < r1 && a.ex_tau[i] == 0) ++i;    // zero-duration rows complete instantly
+  while (i < r1 && (uint32_t)a.ex_pk[i] == 0u) ++i;    // zero-duration rows complete instantly
   w.i = i;
   w.R = 0; w.tau = 0; w.g = 0;
-  if (i < r1) { w.R = a.pb.r[i]; w.tau = a.ex_tau[i]; w.g = a.ex_g[i]; }
+  if (i < r1) {
+    const uint64_t v = a.ex_pk[i];
+    w.R = (uint32_t)(v >> 48); w.tau = (uint32_t)v; w.g = (uint32_t)(v >> 32) & 0xFFFFu;
+  }
   return w;
 }
 
@@ -193,8 +199,9 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
       bool dirty = true;
       bool resel = true;   // the selection must be recomputed (first event, a rank or a live item's g changed)
       bool sel = false;
-      uint64_t gsum = 0;
-      uint64_t util = 0, t = 0;
+      uint32_t gsum = 0;
+      uint64_t util = 0;
+      uint32_t t = 0;   // < T <= 2^30 us
       uint32_t st_ev = 0, st_rs = 0, st_fit = 0, st_enum = 0, st_mitm = 0, st_dp = 0;   // a6 work counters
       while (n > 0 && t < T) {
         ++st_ev;
@@ -424,8 +431,8 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
         }
         uint32_t dt = __reduce_min_sync(FULL, sel ? rem : 0xFFFFFFFFu);
         if (!__any_sync(FULL, sel) || dt == 0) break;
-        if ((uint64_t)dt > (uint64_t)T - t) dt = (uint32_t)((uint64_t)T - t);
-        util += gsum * dt;
+        if (dt > T - t) dt = T - t;
+        util += (uint64_t)gsum * dt;
         t += dt;
         bool done_batch = false;
         const uint32_t g_before = cur.g;
@@ -473,15 +480,14 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_s
 // a6 work counters of the last launch (events, re-selections, all-fit / enumeration / meet-in-the-middle / DP
 // selections, scenarios simulated): 8 u64 at the end of the ideal workspace region
 size_t ideal_stats_offset(int64_t num_rows, int64_t num_scen) {
-  return (((size_t)(num_rows + 8) * 2 + 255) & ~(size_t)255) + (((size_t)(num_rows + 8) * 4 + 255) & ~(size_t)255) +
-         (((size_t)(num_scen + 8) * 4 + 255) & ~(size_t)255) + 48 * 4;
+  return (((size_t)(num_rows + 8) * 8 + 255) & ~(size_t)255) + (((size_t)(num_scen + 8) * 4 + 255) & ~(size_t)255) +
+         48 * 4;
 }
 
 size_t ideal_ws_bytes(int64_t num_rows, int64_t num_scen) {
-  size_t g = ((size_t)(num_rows + 8) * 2 + 255) & ~(size_t)255;
-  size_t t = ((size_t)(num_rows + 8) * 4 + 255) & ~(size_t)255;
+  size_t pk = ((size_t)(num_rows + 8) * 8 + 255) & ~(size_t)255;
   size_t o = ((size_t)(num_scen + 8) * 4 + 255) & ~(size_t)255;
-  return g + t + o + 256;
+  return pk + o + 256;
 }
 
 // Heavy-first scenario order for k_ideal_sim: its cost is the number of events, roughly sum over active DNNs of
@@ -529,9 +535,8 @@ __global__ void __launch_bounds__(256) k_ideal_order_scatter(IdealArgs a) {
 int launch_ideal(IdealArgs a, void *ws, cudaStream_t s, int *launches) {
   if (a.pb.num_scen <= 0) return 0;
   const int64_t num_rows = a.pb.num_rows;
-  a.ex_g = (uint16_t *)ws;
-  a.ex_tau = (uint32_t *)((char *)ws + (((size_t)(num_rows + 8) * 2 + 255) & ~(size_t)255));
-  a.order = (uint32_t *)((char *)a.ex_tau + (((size_t)(num_rows + 8) * 4 + 255) & ~(size_t)255));
+  a.ex_pk = (uint64_t *)ws;
+  a.order = (uint32_t *)((char *)ws + (((size_t)(num_rows + 8) * 8 + 255) & ~(size_t)255));
   a.bucket_cnt = (uint32_t *)((char *)a.order + (((size_t)(a.pb.num_scen + 8) * 4 + 255) & ~(size_t)255));
   a.stats = (unsigned long long *)(a.bucket_cnt + 48);   // 8 u64 behind the 40 bucket counters (256 B slot)
   if (cudaMemsetAsync(a.stats, 0, 8 * sizeof(unsigned long long), s) != cudaSuccess) return DSTACK_ELAUNCH;

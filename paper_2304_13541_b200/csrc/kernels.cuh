@@ -84,8 +84,7 @@ struct IdealArgs {
   dstack_params_t p;
   const uint16_t *demand;
   const uint8_t *batch;
-  uint16_t *ex_g;     // [num_rows] workspace
-  uint32_t *ex_tau;   // [num_rows] workspace
+  uint64_t *ex_pk;    // [num_rows] workspace: tau | g << 32 | R << 48 per execution (k_ideal_rows -> k_ideal_sim)
   double *u_ideal, *thr_ideal;
   uint32_t *work_ctr;   // workspace word: k_ideal_sim's scenario counter (NULL: grid stride)
   const uint16_t *dstar;       // d_j(b*) of the session just computed, per DNN (cost estimate for the order; may be NULL)
