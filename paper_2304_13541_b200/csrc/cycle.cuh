@@ -47,7 +47,6 @@ struct BelowKnee {
 
 struct CycSmem {
   uint8_t occ[DSTACK_MAX_SLOTS + 128];   // + one register window of padding (never read as session slots)
-  uint32_t dmask[DSTACK_MAX_SLOTS / 32];   // decision times (bit u of word w <=> slot 32 w + u)
   uint32_t sr[DSTACK_MAX_JOBS];   // static job (j, r): start | run slots << 16, or NONE32 (miss)
 };
 
@@ -278,16 +277,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   // first), 2 max-throughput (shortest d(b*) first); ties by index.  busy (nullable): this lane's run slots.
   CycRes res; res.occ_static = 0; res.occ_all = 0; res.served_tot = 0; res.misses = 0; res.below = 0; res.oversub = false;
   for (int w = lane; (w << 2) < nslots; w += 32) reinterpret_cast<uint32_t *>(sm.occ)[w] = 0u;
-  // decision-time bits: one register word per lane (word = lane) when nslots <= 1024, else shared memory
-  const bool dreg = nslots <= 1024;
-  uint32_t dmw = 0;
-  if (!dreg)
-    for (int w = lane; w < DSTACK_MAX_SLOTS / 32; w += 32) sm.dmask[w] = 0;
   __syncwarp();
-  auto dset = [&](int e) {   // warp-uniform e < nslots
-    if (dreg) dmw |= (uint32_t)(lane == (e >> 5)) << (e & 31);
-    else if (lane == 0) sm.dmask[e >> 5] |= 1u << (e & 31);
-  };
   uint32_t joff = rep;   // exclusive prefix of rep over lanes
 #pragma unroll
   for (int dlt = 1; dlt < 32; dlt <<= 1) {
@@ -328,7 +318,6 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       occ_add(sm.occ, st, dd, lv, lane);
       res.occ_static += (uint32_t)dd * (uint32_t)lv;   // sum of occ over the session = sum of d g over its runs
       if (lane == 0) sm.sr[offj + rj] = (uint32_t)st | ((uint32_t)dd << 16);
-      if (st + dd < nslots) dset(st + dd);
       if (lane == j) { runs++; served += bs; if (busy) *busy += (uint32_t)dd; }
     } else {
       if (lane == 0) sm.sr[offj + rj] = NONE32;
@@ -340,15 +329,14 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   }
   uint32_t occ_fill = 0;
   // ---- opportunistic fill at decision times {0} u {run ends} (Dynamic-schedule) ----
-  // Decision times are visited in increasing order.  With nslots <= 1024 they live in one register word per
-  // lane and are consumed (bit t cleared when t is visited; every time set later is > t).  Per decision time t
-  // the warp holds the occupancy of slots [t & ~3, (t & ~3) + 128) in registers (one packed word per lane);
-  // slice queries and placements inside that window touch no shared memory except the write-through of placed
-  // runs.  Longer runs fall back to the shared-memory scans.
   // Per lane (DNN): free_at = end of its current run (static or fill); [ns, ne) = its next placed static run not
   // yet begun (ns = nslots when none).  Static runs that began by t are folded into free_at, so the DNN is
   // running at t <=> t < free_at, and ns is its next own static start after t (a fill run's slice stops there).
-  dset(0);
+  // A DNN's runs are disjoint, so its first run end after t is free_at when it is running, else the end of its
+  // next static run: the next decision time is the minimum of these over the DNNs (run ends >= nslots are none).
+  // Per decision time t the warp holds the occupancy of slots [t & ~3, (t & ~3) + 128) in registers (one packed
+  // word per lane); slice queries and placements inside that window touch no shared memory except the
+  // write-through of placed runs.  Longer runs fall back to the shared-memory scans.
   __syncwarp();
   uint32_t count = runs + count0;
   uint32_t nfill = 0;
@@ -363,37 +351,11 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   };
   if (active) next_static();
   const uint32_t pk = (g & 0xFFu) | ((bs & 0xFFu) << 8) | (dstar << 16);   // dstar <= 0xFFFF (u16 rows)
-  const int nwords = (nslots + 31) >> 5;
   uint32_t *w32 = reinterpret_cast<uint32_t *>(sm.occ);
   // a candidate whose slice at t is too short for d(b_lo) stays too short at every later decision time
   // t' < blk: the slot that ended its slice never loses occupancy (or it was its own next static start)
   int blk = 0;
-  int t = -1;
-  while (true) {
-    if (dreg) {
-      const uint32_t bal = __ballot_sync(FULL, dmw != 0u);
-      if (bal == 0u) break;
-      const int pl = __ffs(bal) - 1;
-      t = pl * 32 + __ffs(__shfl_sync(FULL, dmw, pl)) - 1;
-      if (lane == pl) dmw &= dmw - 1u;
-    } else {
-      const int start = t + 1;
-      int nt = -1;
-      for (int wb = start >> 5; wb < nwords; wb += 32) {
-        const int w = wb + lane;
-        uint32_t v = w < nwords ? sm.dmask[w] : 0u;
-        if (w == (start >> 5)) v &= ~((1u << (start & 31)) - 1u);
-        const uint32_t bal = __ballot_sync(FULL, v != 0);
-        if (bal) {
-          const int pl = __ffs(bal) - 1;
-          nt = (wb + pl) * 32 + __ffs(__shfl_sync(FULL, v, pl)) - 1;
-          break;
-        }
-      }
-      if (nt < 0) break;
-      t = nt;
-    }
-    if (t >= nslots) break;
+  for (int t = 0; t < nslots;) {
     if (lane == 0) CSTAT(3, 1);
     const int bt = t & ~3, mybase = bt + 4 * lane, wi = (t >> 2) + lane;
     uint32_t wv = w32[wi];   // occ is padded by 128 slots: the window never leaves the array
@@ -462,7 +424,6 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       }
       occ_t += gj;
       occ_fill += (uint32_t)dsel * (uint32_t)gj;
-      if (e < nslots && e > t) dset(e);
       if (lane == 0 && fill_log && nfill < fill_cap) fill_log[nfill] = pack_run((uint32_t)j, (uint32_t)t, (uint32_t)dsel, (uint32_t)bsel);
       nfill++;
       __syncwarp();
@@ -472,6 +433,8 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       }
       if (occ_t + (int)g > L) key = 0xFFFFFFFFu;
     }
+    const uint32_t nend = !active ? 0xFFFFFFFFu : (free_at > t ? (uint32_t)free_at : (ns < nslots ? (uint32_t)ne : 0xFFFFFFFFu));
+    t = (int)min(__reduce_min_sync(FULL, nend), (uint32_t)nslots);
   }
   res.occ_all = res.occ_static + occ_fill;   // every run lies inside [0, nslots)
   if (lane == 0) CSTAT(0, 1);
