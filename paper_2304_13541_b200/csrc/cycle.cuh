@@ -122,7 +122,8 @@ __device__ __forceinline__ int find_early_packed(const uint8_t *occ, int rel, in
   while (s + d <= dl) {
     const int bt = s & ~3, wi = (bt >> 2) + lane, mybase = bt + 4 * lane;
     const uint32_t word = w32[wi];   // padded array
-    const uint32_t bb = __vcmpgtu4(word, th) & bytes_mask(s, s + d, mybase);   // blocking slots in the run
+    uint32_t bb = __vcmpgtu4(word, th) & bytes_below(s + d, mybase);   // blocking slots in the run
+    if (lane == 0) bb &= 0xFFFFFFFFu << (8 * (s & 3));
     const uint32_t lb = bb ? (uint32_t)(mybase + ((31 - __clz(bb)) >> 3) + 1) : 0u;
     const uint32_t last = __reduce_max_sync(FULL, lb);   // (last blocking slot) + 1, or 0
     if (last == 0) return s;
@@ -138,7 +139,8 @@ __device__ __forceinline__ int find_late_packed(const uint8_t *occ, int rel, int
   while (s >= rel) {
     const int bt = s & ~3, wi = (bt >> 2) + lane, mybase = bt + 4 * lane;
     const uint32_t word = w32[wi];   // padded array
-    const uint32_t bb = __vcmpgtu4(word, th) & bytes_mask(s, s + d, mybase);
+    uint32_t bb = __vcmpgtu4(word, th) & bytes_below(s + d, mybase);
+    if (lane == 0) bb &= 0xFFFFFFFFu << (8 * (s & 3));
     const uint32_t fb = bb ? (uint32_t)(mybase + ((__ffs(bb) - 1) >> 3)) : 0xFFFFFFFFu;
     const uint32_t first = __reduce_min_sync(FULL, fb);   // first blocking slot, or none
     if (first == 0xFFFFFFFFu) return s;
@@ -292,15 +294,15 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   // ---- static placement in EDF order (Alg. 1 l.5; even repeats Start-Early, odd Start-Late) ----
   for (uint32_t q = 0; q < njobs; ++q) {
     const bool has = active && nextr < rep;
-    const uint32_t dl = has ? (nextr + 1) * sl : 0xFFFFFFFFu;
-    const uint32_t mindl = __reduce_min_sync(FULL, dl);
-    const uint32_t key2 = (has && dl == mindl) ? ((dstar << 5) | (uint32_t)lane) : 0xFFFFFFFFu;
-    const uint32_t mk = __reduce_min_sync(FULL, key2);
+    // EDF key (deadline, d(b*), index) in one word: deadline <= nslots <= 4096 (13 bits), d(b*) clamped to 8191
+    // (13 bits; every d >= 8191 > nslots misses its window, so their order among themselves changes nothing)
+    const uint32_t key = has ? (((nextr + 1) * sl) << 18) | (min(dstar, 8191u) << 5) | (uint32_t)lane : 0xFFFFFFFFu;
+    const uint32_t mk = __reduce_min_sync(FULL, key);
     const int j = (int)(mk & 31u);
     const int rj = (int)__shfl_sync(FULL, nextr, j);
     const int slj = (int)__shfl_sync(FULL, sl, j);
     const int gj = (int)__shfl_sync(FULL, g, j);
-    const int dj = (int)(mk >> 5);
+    const int dj = (int)__shfl_sync(FULL, dstar, j);
     const int offj = (int)__shfl_sync(FULL, joff, j);
     const int rel = rj * slj, dlv = rel + slj;
     int st;
@@ -340,9 +342,10 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   __syncwarp();
   uint32_t count = runs + count0;
   uint32_t nfill = 0;
-  int pnext = 0, ns = nslots, ne = 0, free_at = 0;
+  int pnext = 0, ns = nslots, ne = 0x7FFFFFFF, free_at = 0;   // ne: no next static run -> never a run end
   auto next_static = [&]() {
     ns = nslots;
+    ne = 0x7FFFFFFF;
     while (pnext < (int)rep) {
       const uint32_t v = sm.sr[joff + pnext];
       ++pnext;
@@ -433,7 +436,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
       }
       if (occ_t + (int)g > L) key = 0xFFFFFFFFu;
     }
-    const uint32_t nend = !active ? 0xFFFFFFFFu : (free_at > t ? (uint32_t)free_at : (ns < nslots ? (uint32_t)ne : 0xFFFFFFFFu));
+    const uint32_t nend = (uint32_t)(free_at > t ? free_at : ne);   // inactive lanes: free_at = 0, no static run
     t = (int)min(__reduce_min_sync(FULL, nend), (uint32_t)nslots);
   }
   res.occ_all = res.occ_static + occ_fill;   // every run lies inside [0, nslots)

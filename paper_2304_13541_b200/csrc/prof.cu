@@ -516,12 +516,17 @@ __global__ void __launch_bounds__(256, DSTACK_PROF_MINB) k_prof_fast(const __gri
 #define DSTACK_PROF_LANE 1   // 1: the default-model fast path is k_prof_lane (0: k_prof_fast; A/B switch)
 #endif
 #ifndef DSTACK_PLANE_MINB
-#define DSTACK_PLANE_MINB 2
+#define DSTACK_PLANE_MINB 2   // resident blocks per SM
+#endif
+#ifndef DSTACK_PLANE_WARPS
+#define DSTACK_PLANE_WARPS 8   // warps per block
 #endif
 
 __host__ __device__ inline int plane_hstride(int S_tot) { return ((S_tot + 2) >> 1) | 1; }   // odd word stride
 __host__ __device__ inline size_t plane_warp_bytes(int S_tot) {
-  return (size_t)32 * plane_hstride(S_tot) * 4 + prof_warp_bytes(S_tot);   // H table + the cold path's scratch
+  // the H table; the cold path's scratch (cA, cU, hist) reuses it once the group's lane scans are done
+  const size_t h = (size_t)32 * plane_hstride(S_tot) * 4, c = prof_warp_bytes(S_tot);
+  return h > c ? h : c;
 }
 
 // exact-with-filter update of the running argmax (Sb, Xb, fb) of S / X^2 by a later (larger) width S
@@ -626,7 +631,7 @@ __device__ __forceinline__ void lane_scan_f(const uint32_t *H, const uint16_t *l
   }
 }
 
-__global__ void __launch_bounds__(256, DSTACK_PLANE_MINB) k_prof_lane(const __grid_constant__ ProfArgs a) {
+__global__ void __launch_bounds__(DSTACK_PLANE_WARPS * 32, DSTACK_PLANE_MINB) k_prof_lane(const __grid_constant__ ProfArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const dstack_problem_t &pb = a.pb;
   const dstack_params_t &p = a.p;
@@ -638,7 +643,7 @@ __global__ void __launch_bounds__(256, DSTACK_PLANE_MINB) k_prof_lane(const __gr
   const int HS = plane_hstride(S_tot);
   unsigned char *wreg = smem + tab_bytes + (size_t)warp * plane_warp_bytes(S_tot);
   uint32_t *Htab = (uint32_t *)wreg;                       // [32][HS]
-  uint64_t *cA = (uint64_t *)(wreg + (size_t)32 * HS * 4);  // cold path scratch
+  uint64_t *cA = (uint64_t *)wreg;                          // cold path scratch (aliases Htab, used after the scans)
   uint64_t *cU = cA + (S_tot + 1);
   uint32_t *hist = (uint32_t *)(cU + (S_tot + 1));
   fill_stab(Stab, L, S_tot);
@@ -646,7 +651,6 @@ __global__ void __launch_bounds__(256, DSTACK_PLANE_MINB) k_prof_lane(const __gr
     const int l = S == 0 ? 0 : ((S - 1) * L) / S_tot + 1;
     lmin[S] = (uint16_t)((S >= 1 && l <= L && s_of(l, S_tot, L) == S) ? l : 0);
   }
-  for (int m = lane; m <= S_tot; m += 32) hist[m] = 0;
   __syncthreads();
   const int mh = S_tot >> 1;
   const float half = 0.5f * (float)S_tot;
@@ -845,6 +849,11 @@ __global__ void __launch_bounds__(256, DSTACK_PLANE_MINB) k_prof_lane(const __gr
     }
     // ---- the generic path for the DNNs outside the fast ranges ----
     uint32_t colds = __ballot_sync(FULL, have && cold);
+    if (colds) {   // the cold path expects a zeroed hist (its scratch overlays the H table)
+      __syncwarp();
+      for (int m = lane; m <= S_tot; m += 32) hist[m] = 0;
+      __syncwarp();
+    }
     while (colds) {
       const int j = __ffs(colds) - 1;
       colds &= colds - 1;
@@ -885,13 +894,14 @@ int launch_prof(const ProfArgs &a, cudaStream_t s, int *launches) {
   }
   if (fast && DSTACK_PROF_LANE) {
     // k_prof_lane: one resident wave of warps pulling groups of 32 DNNs (grid stride over groups without a counter)
-    const size_t sm2 = plane_smem_bytes(&a.p, warps);
+    const int pw = DSTACK_PLANE_WARPS;
+    const size_t sm2 = plane_smem_bytes(&a.p, pw);
     cudaFuncSetAttribute(k_prof_lane, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     const int64_t groups = (a.pb.num_dnn + 31) / 32;
-    int64_t nb = (groups + warps - 1) / warps;
-    const int64_t wave = resident_wave(k_prof_lane, threads, sm2, nb);
+    int64_t nb = (groups + pw - 1) / pw;
+    const int64_t wave = resident_wave(k_prof_lane, pw * 32, sm2, nb);
     if (b.work_ctr || nb > wave) nb = wave;
-    k_prof_lane<<<(unsigned)nb, threads, sm2, s>>>(b);
+    k_prof_lane<<<(unsigned)nb, pw * 32, sm2, s>>>(b);
   } else if (fast && a.p.S_tot < 5 * 32) launch_k(k_prof_fast<5>, b, blocks, threads, smem, s);
   else if (fast) launch_k(k_prof_fast<9>, b, blocks, threads, smem, s);
   else if (a.p.par_mode == 0) launch_k(k_prof<0>, b, blocks, threads, smem, s);
