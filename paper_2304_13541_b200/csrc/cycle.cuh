@@ -29,6 +29,11 @@ static __device__ unsigned long long g_cstats[16];   // per TU (instrumentation 
 #endif
 
 
+#ifndef DSTACK_CYC_PACKED_MAX
+#define DSTACK_CYC_PACKED_MAX 124   // static runs up to this length use the packed-word searches (A/B switch; <= 124;
+                                    // 0 -> 32-slot ballot chunks: k_cycle 11.87 -> 12.59 ms at config 3)
+#endif
+
 constexpr uint16_t NONE16 = 0xFFFF;
 constexpr uint32_t NONE32 = 0xFFFFFFFFu;
 
@@ -307,7 +312,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     const int rel = rj * slj, dlv = rel + slj;
     int st;
     if (dj > dlv - rel) st = -1;
-    else if (dj <= 124) st = (rj & 1) ? find_late_packed(sm.occ, rel, dlv, dj, gj, L, lane)
+    else if (dj <= DSTACK_CYC_PACKED_MAX) st = (rj & 1) ? find_late_packed(sm.occ, rel, dlv, dj, gj, L, lane)
                                       : find_early_packed(sm.occ, rel, dlv, dj, gj, L, lane);
     else st = (rj & 1) ? find_late(sm.occ, rel, dlv, dj, gj, L, lane) : find_early(sm.occ, rel, dlv, dj, gj, L, lane);
     if (lane == 0) CSTAT(1, 1);

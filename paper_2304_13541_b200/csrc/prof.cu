@@ -598,17 +598,23 @@ __device__ __forceinline__ void lane_scan_f(const uint32_t *H, const uint16_t *l
                                             float Wbf, float membf, float half, float &t1, float &t2, float &t3,
                                             uint32_t &s1, uint32_t &ra1, uint32_t &q1, uint32_t &s2, float &G) {
   uint32_t ra = 0, rw = 0;
+  // the same integers as floats, carried (all < 2^24, so every value is exact and equals (float) of the integer)
+  float raf = 0.f, rwf = 0.f;
+  const float Wsmf = (float)Wsm;
+  float Sw = 0.f;   // 2 w
   const int nw = (S_tot + 2) >> 1;   // words holding bins 0..S_tot (bin S_tot + 1 of an even S_tot is 0)
 #pragma unroll 2
-  for (int w = 0; w < nw; ++w) {
+  for (int w = 0; w < nw; ++w, Sw += 2.f) {
     const uint32_t hw = H[w];
 #pragma unroll
     for (int hi = 0; hi < 2; ++hi) {
       const uint32_t S = (uint32_t)(2 * w + hi);   // S_tot + 1 (even S_tot): h = 0, lmin = 0 -> no candidate
       const uint32_t h = S == 0 ? 0u : (hi ? (hw >> 16) : (hw & 0xFFFFu));
+      const float Sf = hi ? Sw + 1.f : Sw, hf = (float)h;
       ra += h; rw += h * S;
+      raf += hf; rwf = fmaf(hf, Sf, rwf);
       const uint32_t q = Wsm - rw;
-      const float Sf = (float)S, raf = (float)ra, qf = (float)q;
+      const float qf = Wsmf - rwf;
       if ((int)S <= mh) {
         const float af = fmaf(Mtpf, raf, C1f2), bf = fmaf(Mtpf, qf + Wbf, membf);
         const float hiS = fminf(Sf + 1.f, half);
@@ -620,12 +626,13 @@ __device__ __forceinline__ void lane_scan_f(const uint32_t *H, const uint16_t *l
       float xf = fmaf(Sf, C1f, fmaf(Mtpf, fmaf(Sf, raf, qf), basef));
       if (SCAN_MEM == 2) xf = fmaf(Df, Sf * Sf, xf);
       const float f = Sf * rcp_approx(xf * xf);
-      // top-3 of the scores (strict: the first width keeps a float tie), payloads of the top 2
-      const bool g1 = f > t1, g2 = f > t2;
+      // top-3 of the scores (strict: the first width keeps a float tie), payloads of the top 2; branch-free
+      // (lanes hold different DNNs, so a branch on f > t1 diverges)
+      const uint32_t m1 = 0u - (uint32_t)(f > t1), m2 = 0u - (uint32_t)(f > t2);
       t3 = fmaxf(t3, fminf(t2, f));
-      s2 = g1 ? s1 : (g2 ? S : s2);
+      s2 = (s1 & m1) | (((S & m2) | (s2 & ~m2)) & ~m1);
       t2 = fmaxf(t2, fminf(t1, f));
-      s1 = g1 ? S : s1; ra1 = g1 ? ra : ra1; q1 = g1 ? q : q1;
+      s1 = (S & m1) | (s1 & ~m1); ra1 = (ra & m1) | (ra1 & ~m1); q1 = (q & m1) | (q1 & ~m1);
       t1 = fmaxf(t1, f);
     }
   }
