@@ -2,7 +2,7 @@
 //
 // Stage 1: a FIXED grid of AGG_BLOCKS blocks (independent of the device) each owns a contiguous
 // scenario range; f64 sums are reduced in a fixed tree order, integer counts / histograms with
-// shared-memory atomics (order-free).  Stage 2: one block folds the partials in index order.
+// shared-memory atomics (order-free).  Stage 2: one warp per struct word folds the partials in a fixed order.
 // The multi-GPU combine is one NCCL all-reduce of this struct (python side).
 #include "kernels.cuh"
 
@@ -124,19 +124,26 @@ __global__ void __launch_bounds__(AGG_THREADS) k_agg1(AggArgs a) {
   for (int i = threadIdx.x; i < 256; i += blockDim.x) dst->demand_hist[i] = hs.demand[i];
 }
 
+// Stage 2: one warp per word of the struct; lane i folds partials i, i + 32, ... in index order, then a fixed
+// butterfly combines the lanes (a fixed order: deterministic)
 __global__ void __launch_bounds__(AGG_THREADS) k_agg2(AggArgs a) {
-  // field-wise fold of the partials in index order: doubles first (5), then u64 words
   const int nwords = (int)(sizeof(dstack_agg_t) / 8);
-  for (int w = threadIdx.x; w < nwords; w += blockDim.x) {
-    if (w < 5) {
-      double t = 0.0;
-      for (int b = 0; b < AGG_BLOCKS; ++b) t += reinterpret_cast<const double *>(&a.partials[b])[w];
-      reinterpret_cast<double *>(a.out)[w] = t;
-    } else {
-      uint64_t t = 0;
-      for (int b = 0; b < AGG_BLOCKS; ++b) t += reinterpret_cast<const uint64_t *>(&a.partials[b])[w];
-      reinterpret_cast<uint64_t *>(a.out)[w] = t;
-    }
+  const int w = (int)(blockIdx.x * (AGG_THREADS / 32) + (threadIdx.x >> 5)), lane = threadIdx.x & 31;
+  if (w >= nwords) return;
+  if (w < 5) {   // the doubles
+    double t = 0.0;
+#pragma unroll 8
+    for (int b = lane; b < AGG_BLOCKS; b += 32) t += reinterpret_cast<const double *>(&a.partials[b])[w];
+#pragma unroll
+    for (int m = 16; m; m >>= 1) t += __shfl_xor_sync(FULL, t, m);
+    if (lane == 0) reinterpret_cast<double *>(a.out)[w] = t;
+  } else {
+    uint64_t t = 0;
+#pragma unroll 8
+    for (int b = lane; b < AGG_BLOCKS; b += 32) t += reinterpret_cast<const uint64_t *>(&a.partials[b])[w];
+#pragma unroll
+    for (int m = 16; m; m >>= 1) t += __shfl_xor_sync(FULL, t, m);
+    if (lane == 0) reinterpret_cast<uint64_t *>(a.out)[w] = t;
   }
 }
 
@@ -144,7 +151,8 @@ size_t agg_ws_bytes() { return sizeof(dstack_agg_t) * AGG_BLOCKS; }
 
 int launch_agg(const AggArgs &a, cudaStream_t s, int *launches) {
   k_agg1<<<AGG_BLOCKS, AGG_THREADS, 0, s>>>(a);
-  k_agg2<<<1, AGG_THREADS, 0, s>>>(a);
+  const int nwords = (int)(sizeof(dstack_agg_t) / 8), wpb = AGG_THREADS / 32;
+  k_agg2<<<(nwords + wpb - 1) / wpb, AGG_THREADS, 0, s>>>(a);
   *launches += 2;
   return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;
 }
