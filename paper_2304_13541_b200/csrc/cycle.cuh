@@ -430,7 +430,7 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
         wv = w32[wi];
         wvm = wv & lo_mask;
       }
-      occ_t += gj;
+      if (dsel > 0) occ_t += gj;   // a zero-length run (d = 0, reachable through the test hook) occupies no slot
       occ_fill += (uint32_t)dsel * (uint32_t)gj;
       if (lane == 0 && fill_log && nfill < fill_cap) fill_log[nfill] = pack_run((uint32_t)j, (uint32_t)t, (uint32_t)dsel, (uint32_t)bsel);
       nfill++;
