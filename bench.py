@@ -971,6 +971,28 @@ def _e2e_timed(args, n_total, p, dev, world, host_chunks, prob_fields, mode, ref
                     "wide": "paper_2304_13541_b200.dstack.eval_batch (dstack_eval_batch)"}[mode]}
 
 
+def sim_cpu_baseline(args, sp, p):
+    """The oracle's O7 (config 5) on the host cores (OpenMP over scenarios): contiguous blocks of 64 scenarios spread
+    evenly over the workload, each drawn and simulated at its global indices, the same cycles per scenario; unit
+    scenario-cycles/s."""
+    import oracle
+    import synth
+    cores = host_cores()
+    total, done, el, k, chunk = sp.num_scen, 0, 0.0, 0, 64
+    nblk = max(1, total // chunk)
+    stride = max(1, nblk // 64)
+    while el < args.cpu_seconds and done < 4096:
+        base = sp.scen_base + ((k * stride) % nblk) * chunk
+        pb = synth.generate_host(sp.replace(scen_base=base, num_scen=min(chunk, total)))
+        t0 = time.perf_counter()
+        oracle.simulate(pb, p, args.cycles, sp.seed, sp.cfg_tag, scen_base=base, nthreads=cores)
+        el += time.perf_counter() - t0
+        done += pb.num_scen; k += 1
+    return {"value": done * args.cycles / el, "unit": "scenario-cycles/s", "cores": cores, "kind": "oracle",
+            "sample": f"{done} scenarios (blocks of {chunk} spread over the config-5 workload) x {args.cycles} "
+                      f"cycles, {el:.1f} s wall on {cores} host threads (OpenMP over scenarios)"}
+
+
 def run_sim(args, rank, world, local):
     """Config 5 (a7): dstack_simulate over the shard; unit scenario-cycles/s."""
     import torch
@@ -1009,13 +1031,14 @@ def run_sim(args, rank, world, local):
         dist.barrier()
     clocks = sampler.stop() if sampler else None
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    tot = torch.stack([o[k].sum() for k in ("arrived", "in_slo", "late", "unserved", "occ_sum", "runs")]).to(torch.float64)
+    tot = torch.stack([o[k].sum() for k in ("arrived", "in_slo", "late", "unserved", "occ_sum", "runs",
+                                             "realloc")]).to(torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
     ms = float(t.item())
     if rank == 0:
-        arrived, in_slo, late, unserved, occ, runs = tot.tolist()
+        arrived, in_slo, late, unserved, occ, runs, realloc = tot.tolist()
         nslots = (o["T_us"].to(torch.float64) / p.slot_us)
         line = {"metric": "scenario-cycles/sec (config 5 long-horizon simulation, a7)",
                 "value": n_total * args.cycles * args.steps / (ms / 1e3), "unit": "scenario-cycles/s",
@@ -1029,7 +1052,12 @@ def run_sim(args, rank, world, local):
                           "late_frac": late / max(arrived, 1), "unserved_frac": unserved / max(arrived, 1),
                           "mean_u_rank0": float((o["occ_sum"].to(torch.float64) /
                                                  (nslots * p.L * args.cycles).clamp(min=1)).mean().item()),
-                          "runs": runs}}
+                          "runs": runs,
+                          # sessions 2..cycles whose active DNN set changed: each one is a per-cycle WMAX-MIN
+                          # re-allocation over a new set (the "dynamic re-allocation" of BASELINE config 5)
+                          "realloc_frac": realloc / max(n_total * max(args.cycles - 1, 1) * args.steps, 1)}}
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = sim_cpu_baseline(args, sp0, p)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

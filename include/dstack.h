@@ -212,11 +212,12 @@ int dstack_aggregate(const dstack_problem_t *pb, const dstack_params_t *p, dstac
  * every run serves FIFO min(batch, queue at its start) requests (void if the queue is empty).
  * Outputs per scenario (all device arrays [num_scen]): status, T_us, arrived, in_slo, late (completed
  * after arrival + SLO), unserved (queued at the horizon), occ_sum (sum over non-void runs of level x
- * slots; mean utilisation = occ_sum / (nslots L cycles)), runs (non-void), misses (unplaced static jobs).
- * Workspace: dstack_sim_workspace_size(). */
+ * slots; mean utilisation = occ_sum / (nslots L cycles)), runs (non-void), misses (unplaced static jobs),
+ * realloc (sessions 2..cycles whose active DNN set differs from the previous session's: each is a per-cycle
+ * WMAX-MIN re-allocation over a changed set).  Workspace: dstack_sim_workspace_size(). */
 typedef struct {
   uint8_t *status; uint32_t *T_us;
-  uint64_t *arrived, *in_slo, *late, *unserved, *occ_sum, *runs, *misses;
+  uint64_t *arrived, *in_slo, *late, *unserved, *occ_sum, *runs, *misses, *realloc;
 } dstack_sim_out_t;
 size_t dstack_sim_workspace_size(const dstack_problem_t *pb, const dstack_params_t *p);
 int dstack_simulate(const dstack_problem_t *pb, const dstack_params_t *p, const int32_t *lam_pct, int32_t cycles,

@@ -52,7 +52,7 @@ class OrCycSum(C.Structure):
 
 class OrSimOut(C.Structure):
     _fields_ = [(k, C.c_void_p) for k in ("status", "T_us", "arrived", "in_slo", "late", "unserved", "occ_sum", "runs",
-                                          "misses")]
+                                          "misses", "realloc")]
 
 
 _lib = None
@@ -348,7 +348,7 @@ def simulate(pb: Problem, p: Params, cycles: int, seed: int, cfg_tag: int, scen_
     S = pb.num_scen
     o = dict(status=np.zeros(S, np.uint8), T_us=np.zeros(S, np.uint32),
              **{k: np.zeros(S, np.uint64) for k in ("arrived", "in_slo", "late", "unserved", "occ_sum", "runs",
-                                                     "misses")})
+                                                     "misses", "realloc")})
     oo = OrSimOut(*[_p(o[k]) for k, _ in OrSimOut._fields_])
     lam = np.ascontiguousarray(pb.lam_pct, np.int32)
     idx = None if subset is None else np.ascontiguousarray(np.asarray(list(subset)), np.int64)

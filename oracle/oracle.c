@@ -1221,7 +1221,7 @@ static void simulate_scenario(const or_problem_t *pb, const or_params_t *p, cons
   const int32_t k0 = pb->scen_dnn_off[s], k1 = pb->scen_dnn_off[s + 1];
   const int32_t nd = k1 - k0;
   o->status[s] = OR_OK; o->T_us[s] = 0; o->arrived[s] = 0; o->in_slo[s] = 0; o->late[s] = 0;
-  o->unserved[s] = 0; o->occ_sum[s] = 0; o->runs[s] = 0; o->misses[s] = 0;
+  o->unserved[s] = 0; o->occ_sum[s] = 0; o->runs[s] = 0; o->misses[s] = 0; o->realloc[s] = 0;
   if (nd > OR_MAX_DNN_PER_SCEN) { o->status[s] = OR_INVALID; return; }
   if (nd <= 0) { o->status[s] = OR_INFEASIBLE; return; }
   uint16_t dem[OR_MAX_DNN_PER_SCEN], knee[OR_MAX_DNN_PER_SCEN];
@@ -1260,6 +1260,8 @@ static void simulate_scenario(const or_problem_t *pb, const or_params_t *p, cons
   int64_t dtab[OR_MAX_DNN_PER_SCEN * 64];
   uint16_t dm[OR_MAX_DNN_PER_SCEN];
   uint32_t alloc[OR_MAX_DNN_PER_SCEN];
+  uint8_t prev_act[OR_MAX_DNN_PER_SCEN];
+  memset(prev_act, 0, sizeof(prev_act));
   for (int32_t c = 0; c < cycles; ++c) {
     const uint64_t t0 = (uint64_t)c * (uint64_t)T;
     for (int32_t j = 0; j < nd; ++j) {
@@ -1268,6 +1270,9 @@ static void simulate_scenario(const or_problem_t *pb, const or_params_t *p, cons
       const uint64_t A = arr_count(arr + j, t0);
       if (A > served[j]) dm[j] = dem[j];                 /* active: requests queued at the cycle start */
     }
+    int changed = 0;                                       /* the active set moved: WMAX-MIN re-allocates */
+    for (int32_t j = 0; j < nd; ++j) { changed |= (dm[j] > 0) != prev_act[j]; prev_act[j] = dm[j] > 0; }
+    if (c > 0) o->realloc[s] += (uint64_t)changed;
     oracle_wmaxmin(nd, dm, p->L, alloc);
     for (int32_t j = 0; j < nd; ++j) {
       g[j] = 0; sl[j] = pb->slo_us[k0 + j] / p->slot_us; bst[j] = bst8[j];
@@ -1296,7 +1301,7 @@ static void simulate_scenario(const or_problem_t *pb, const or_params_t *p, cons
     if (nfill > OR_MAX_FILL_RUNS) {                       /* ABI capacity limit: scenario INVALID */
       free(rl);
       o->status[s] = OR_INVALID; o->T_us[s] = 0; o->in_slo[s] = o->late[s] = o->occ_sum[s] = o->runs[s] = 0;
-      o->misses[s] = 0;
+      o->misses[s] = 0; o->realloc[s] = 0;
       return;
     }
     qsort(rl, (size_t)nrun, sizeof(run_t), run_cmp);     /* per DNN, in start order */

@@ -144,6 +144,7 @@ int oracle_ideal_rows(const or_problem_t *pb, const or_params_t *p, int64_t dnn,
 typedef struct {
   uint8_t *status; uint32_t *T_us;
   uint64_t *arrived, *in_slo, *late, *unserved, *occ_sum, *runs, *misses;
+  uint64_t *realloc;   /* sessions 2..cycles whose active set differs from the previous session's */
 } or_sim_out_t;
 int oracle_simulate(const or_problem_t *pb, const or_params_t *p, const int32_t *lam_pct, int32_t cycles,
                     uint64_t seed, int32_t cfg_tag, int64_t scen_base, or_sim_out_t *out, const int64_t *scen_idx,

@@ -365,7 +365,7 @@ int dstack_simulate(const dstack_problem_t *pb, const dstack_params_t *p, const 
   if (!problem_ok(pb) || !params_ok(p) || !out || cycles < 0 || (pb->num_dnn > 0 && !lam_pct)) return DSTACK_EINVAL;
   if (p->flags & DSTACK_FLAG_BELOW_KNEE) return DSTACK_EINVAL;
   if (pb->num_scen > 0 && (!out->status || !out->T_us || !out->arrived || !out->in_slo || !out->late ||
-                           !out->unserved || !out->occ_sum || !out->runs || !out->misses))
+                           !out->unserved || !out->occ_sum || !out->runs || !out->misses || !out->realloc))
     return DSTACK_EINVAL;
   const size_t need = dstack_sim_workspace_size(pb, p);
   if (ws_bytes < need || !ws) return DSTACK_EWORKSPACE;

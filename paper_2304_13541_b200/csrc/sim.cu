@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(SIM_WARPS * 32, DSTACK_SIM_MINB) k_sim(SimArgs
     const int64_t gs = a.scen_base + s;
     uint8_t sst = DSTACK_ST_OK;
     uint32_t T = 0;
-    uint64_t arrived = 0, in_slo = 0, late = 0, unserved = 0, occ_tot = 0, nruns = 0, misses = 0;
+    uint64_t arrived = 0, in_slo = 0, late = 0, unserved = 0, occ_tot = 0, nruns = 0, misses = 0, realloc = 0;
     const bool mine = lane < nd && nd <= DSTACK_MAX_DNN_PER_SCEN;
     const int k = k0 + lane;
     uint32_t dem = 0, bs = 0, slo = 0, sl = 1, rep = 0;
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(SIM_WARPS * 32, DSTACK_SIM_MINB) k_sim(SimArgs
         head = arr;
       }
       uint64_t served = 0;
-      uint32_t sb = 0, gcache = 0;
+      uint32_t sb = 0, gcache = 0, prev_act = 0;
       for (int i = 0; i < 10; ++i) ring[i * 32 + lane] = 0;
       uint16_t *dtab = a.dtab_rows + (int64_t)k0 * DTAB_ROW;
       const uint32_t dstar_slo = slo;
@@ -94,6 +94,9 @@ __global__ void __launch_bounds__(SIM_WARPS * 32, DSTACK_SIM_MINB) k_sim(SimArgs
         const uint64_t t0 = (uint64_t)c * T;
         if (ok) while (arr.time <= t0) arr_next(arr, a, gs, (uint32_t)lane, mq);
         const bool active = ok && arr.idx > served;
+        const uint32_t act_mask = __ballot_sync(FULL, active);   // a changed set: WMAX-MIN re-allocates
+        if (c > 0 && act_mask != prev_act) ++realloc;
+        prev_act = act_mask;
         const uint32_t dm = active ? dem : 0u;
         const uint32_t al = wmaxmin_lane(dm, lane, nd, L);
         const uint32_t g = active ? (dm > (al >> 16) ? dm : (al >> 16)) : 0u;
@@ -170,13 +173,13 @@ __global__ void __launch_bounds__(SIM_WARPS * 32, DSTACK_SIM_MINB) k_sim(SimArgs
         }
       }
     }
-    if (sst == DSTACK_ST_INVALID) { arrived = in_slo = late = unserved = occ_tot = nruns = misses = 0; T = 0; }
+    if (sst == DSTACK_ST_INVALID) { arrived = in_slo = late = unserved = occ_tot = nruns = misses = realloc = 0; T = 0; }
     arrived = warp_sum_u64(arrived); in_slo = warp_sum_u64(in_slo); late = warp_sum_u64(late);
     unserved = warp_sum_u64(unserved); occ_tot = warp_sum_u64(occ_tot); nruns = warp_sum_u64(nruns);
     if (lane == 0) {
       a.out.status[s] = sst; a.out.T_us[s] = T; a.out.arrived[s] = arrived; a.out.in_slo[s] = in_slo;
       a.out.late[s] = late; a.out.unserved[s] = unserved; a.out.occ_sum[s] = occ_tot; a.out.runs[s] = nruns;
-      a.out.misses[s] = misses;
+      a.out.misses[s] = misses; a.out.realloc[s] = realloc;
     }
     __syncwarp();
   }

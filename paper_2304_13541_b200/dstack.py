@@ -60,7 +60,7 @@ class COut(C.Structure):
     _fields_ = [(k, C.c_void_p) for k in _OUT_FIELDS]
 
 
-_SIM_FIELDS = ("status", "T_us", "arrived", "in_slo", "late", "unserved", "occ_sum", "runs", "misses")
+_SIM_FIELDS = ("status", "T_us", "arrived", "in_slo", "late", "unserved", "occ_sum", "runs", "misses", "realloc")
 
 
 class CSimOut(C.Structure):

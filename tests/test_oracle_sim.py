@@ -60,13 +60,18 @@ def reference_sim(pb, p, s, cycles, seed, cfg_tag):
         streams[j] = Stream(j, min(mq, 1 << 62))
     served = [0] * nd
     ring = np.zeros((10, nd), np.int64)
-    res = dict(in_slo=0, late=0, occ_sum=0, runs=0, misses=0)
+    res = dict(in_slo=0, late=0, occ_sum=0, runs=0, misses=0, realloc=0)
+    prev = None
     for c in range(cycles):
         t0 = c * T
         dm = np.zeros(nd, np.uint16)
         for j in streams:
             if streams[j].count(t0) > served[j]:
                 dm[j] = bo["demand"][j]
+        act = tuple(int(x > 0) for x in dm)   # the active set; a change means a WMAX-MIN re-allocation
+        if prev is not None and act != prev:
+            res["realloc"] += 1
+        prev = act
         al = oracle.wmaxmin(dm, p.L)
         g = np.zeros(nd, np.int32); dtab = np.zeros((nd, 64), np.int64)
         for j in range(nd):
@@ -114,7 +119,7 @@ def test_sim_matches_independent_reimplementation():
         want = reference_sim(pb, p, s, cycles, sp.seed, sp.cfg_tag)
         if want is None:
             continue
-        for k in ("arrived", "in_slo", "late", "unserved", "occ_sum", "runs", "misses"):
+        for k in ("arrived", "in_slo", "late", "unserved", "occ_sum", "runs", "misses", "realloc"):
             assert int(o[k][s]) == want[k], (s, k, int(o[k][s]), want[k])
 
 
