@@ -1056,6 +1056,18 @@ def run_sim(args, rank, world, local):
                           # sessions 2..cycles whose active DNN set changed: each one is a per-cycle WMAX-MIN
                           # re-allocation over a new set (the "dynamic re-allocation" of BASELINE config 5)
                           "realloc_frac": realloc / max(n_total * max(args.cycles - 1, 1) * args.steps, 1)}}
+        # the same scenarios at a quarter of the offered load (lam_pct // 4, i.e. 7-30 % of each DNN's standalone
+        # capacity; a harness-side input change): queues empty more often, so the active set and WMAX-MIN's
+        # re-allocation move more (context beside the headline workload, one untimed call)
+        import dataclasses
+        dq = dataclasses.replace(dp, lam_pct=torch.clamp(dp.lam_pct // 4, min=1))
+        oq = ds.simulate(dq, p, args.cycles, sp.seed, sp.cfg_tag, scen_base=sp.scen_base)
+        q = {k: float(oq[k].sum().item()) for k in ("arrived", "in_slo", "late", "unserved", "realloc")}
+        line["quarter_load"] = {"lam_pct": "generator's U{30..120} // 4", "in_slo_frac": q["in_slo"] / max(q["arrived"], 1),
+                                "late_frac": q["late"] / max(q["arrived"], 1),
+                                "unserved_frac": q["unserved"] / max(q["arrived"], 1),
+                                "realloc_frac": q["realloc"] / max(dp.num_scen * max(args.cycles - 1, 1), 1),
+                                "scenarios": dp.num_scen, "note": "rank 0's shard"}
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = sim_cpu_baseline(args, sp0, p)
         print(json.dumps(line), flush=True)
