@@ -343,11 +343,12 @@ def algorithmic_bytes(dp, args, out=None):
     rows = 10 * R                                   # n u32 + R u16 + d u32
     hdr = D * (8 + 6 * 4)                           # dnn_row_off + t_p, t_np, M, SLO, a, bmax
     prof = rows + hdr + D * (2 + 1 + 2 + 1)         # -> demand, batch, knee, status
-    wmm = S * 4 + D * (2 + 4)                       # offsets, demand -> alloc
-    cyc = S * 4 + D * (2 + 1 + 4 + 4) + D * (2 + 2 + 4) + S * (1 + 4 + 3 * 8 + 4) + 10 * rr + nr * (8 + 4 + 8)
+    # k_cycle runs a4 too on the eval path (WMAX-MIN fused): offsets + demand, batch, d_j(b*), SLO in; alloc, level,
+    # runs, served, per-scenario results out
+    cyc = S * 4 + D * (2 + 1 + 2 + 4) + D * (4 + 2 + 2 + 4) + S * (1 + 4 + 3 * 8 + 4) + 10 * rr + nr * (8 + 4 + 8)
     agg = S * (4 + 1 + 4 + 3 * 8 + 4) + D * (2 + 1 + 2 + 1 + 4 + 2 + 2 + 4)
     path = rows + hdr + S * 4 + D * (2 + 1 + 2 + 1 + 4 + 2 + 2 + 4) + S * (1 + 4 + 3 * 8 + 4)
-    return {"k_prof": prof, "k_wmaxmin": wmm, "k_cycle": cyc, "k_ideal": rows, "k_agg": agg, "path": path}
+    return {"k_prof": prof, "k_cycle": cyc, "k_ideal": rows, "k_agg": agg, "path": path}
 
 
 def prepare_workload(args, p, dev, rank, world, ds):
@@ -495,10 +496,10 @@ def run_native(args, rank, world, local):
         return r
 
     dom_name = max(kern, key=kern.get)          # the kernel with the largest share of the step
-    path_kernels = [k for k in ("k_prof", "k_wmaxmin", "k_cycle", "k_agg") if k in cnt]
-    path_traffic = sum(cnt[k]["dram_bytes"] for k in path_kernels) * n_rank if len(path_kernels) == 4 else None
+    path_kernels = [k for k in ("k_prof", "k_cycle", "k_agg") if k in cnt]
+    path_traffic = sum(cnt[k]["dram_bytes"] for k in path_kernels) * n_rank if len(path_kernels) == 3 else None
     path_ach = ab["path"] / step_s / 1e9
-    roofline = {"bound": "hbm", "kernel": "whole path per step (k_prof + k_wmaxmin + k_cycle + k_agg)",
+    roofline = {"bound": "hbm", "kernel": "whole path per step (k_prof: a1-a3; k_cycle: a4 + a5; k_agg: a8)",
                 "achieved": path_ach, "peak": peak, "unit": "GB/s", "frac": path_ach / peak, "traffic": path_traffic,
                 "algorithmic_bytes_per_step": ab["path"], "peak_source": peak_src,
                 "bytes_rule": "every row once (10 B) + DNN headers + per-DNN / per-scenario outputs once (DESIGN.md §6)",
@@ -520,13 +521,12 @@ def run_native(args, rank, world, local):
         "config": workload_config(args, sp0, p, world, input_bytes, flush),
         "roofline": roofline,
         "budget": budget,
-        "roofline_by_kernel": {k: kernel_roofline(k) for k in kern},
-        # a1-a4 alone (k_prof + k_wmaxmin) as the HBM-bound sub-path, algorithmic bytes / their time
-        "a1_a4_subpath": ({"ms": kern["k_prof"] + kern["k_wmaxmin"],
-                           "algorithmic_bytes": ab["k_prof"] + ab["k_wmaxmin"],
-                           "achieved_GBps": (ab["k_prof"] + ab["k_wmaxmin"]) / ((kern["k_prof"] + kern["k_wmaxmin"]) / 1e3) / 1e9,
-                           "frac": (ab["k_prof"] + ab["k_wmaxmin"]) / ((kern["k_prof"] + kern["k_wmaxmin"]) / 1e3) / 1e9 / peak}
-                          if "k_prof" in kern and "k_wmaxmin" in kern else None),
+        "roofline_by_kernel": {k: kernel_roofline(k) for k in kern if k in ab},
+        # the row-streaming sub-path a1-a3 alone (k_prof; a4 is fused into k_cycle), algorithmic
+        # bytes / its time
+        "a1_a3_subpath": ({"ms": kern["k_prof"], "algorithmic_bytes": ab["k_prof"],
+                           "achieved_GBps": ab["k_prof"] / (kern["k_prof"] / 1e3) / 1e9,
+                           "frac": ab["k_prof"] / (kern["k_prof"] / 1e3) / 1e9 / peak} if "k_prof" in kern else None),
         "kernels_ms": kern, "kernels_share": {k: v / (ms_max / args.steps) for k, v in kern.items()},
         "gpu_launches": launches[0],
         "clocks": clocks,

@@ -252,6 +252,7 @@ static int schedule_impl(const dstack_problem_t *pb, const dstack_params_t *p, c
   CycArgs c;
   std::memset(&c, 0, sizeof(c));
   c.pb = *pb; c.p = *p; c.demand = demand; c.batch = batch; c.alloc = alloc_q16;
+  if (pre_ws && !hook) c.alloc_out = out->alloc_q16;   // eval path: a4 fused into k_cycle
   if (hook) { c.hook_level = hook->level; c.hook_d = hook->d_slots; }
   c.level = out->level; c.runs = out->runs; c.served = out->served; c.scen_status = out->scen_status;
   c.T_us = out->T_us; c.u_static = out->u_static; c.u = out->u; c.thr = out->thr; c.misses = out->misses;
@@ -323,11 +324,12 @@ int dstack_eval_batch(const dstack_problem_t *pb, const dstack_params_t *p, dsta
   a.work_ctr = (uint32_t *)((char *)ws + w.ctr) + 1;   // word 0: k_cycle's counter
   const bool prof = g_prof.on && g_prof.calls < g_prof.max_calls;
   uint8_t *used = prof ? g_prof.used + g_prof.calls * DSTACK_PROF_SLOTS : nullptr;
-  if (prof) { used[0] = used[1] = used[2] = 1; used[3] = (p->flags & DSTACK_FLAG_IDEAL) ? 1 : 0; used[4] = out->agg ? 1 : 0; }
+  // slots: k_prof, (k_wmaxmin: a4 runs inside k_cycle on this path, slot unused), k_cycle, k_ideal, k_agg
+  if (prof) { used[0] = used[2] = 1; used[1] = 0; used[3] = (p->flags & DSTACK_FLAG_IDEAL) ? 1 : 0; used[4] = out->agg ? 1 : 0; }
   prof_mark(s, 0);
   int rc = launch_prof(a, s, &g_launches);                                            // a1-a3
   prof_mark(s, 1);
-  if (!rc) rc = launch_wmaxmin(pb->num_scen, pb->scen_dnn_off, p->L, out->demand, out->alloc_q16, s, &g_launches);
+  // a4 (WMAX-MIN) runs inside k_cycle on this path (CycArgs::alloc_out): the profile slot stays empty
   prof_mark(s, 2);
   if (!rc) rc = schedule_impl(pb, p, out->demand, out->batch, out->alloc_q16, nullptr, out, ws, ws_bytes, s, true);
   if (!rc && out->agg) { prof_mark(s, 4); rc = aggregate_impl(pb, out, ws, s); }

@@ -74,9 +74,22 @@ __global__ void __launch_bounds__(CYC_WARPS * 32, BK ? DSTACK_CYC_BK_MINB : DSTA
         dem = g;
       } else {
         dem = a.demand[k];
-        const uint32_t al = a.alloc[k] >> 16;
-        g = dem == 0 ? 0u : (dem > al ? dem : al);
       }
+    }
+    if (!a.hook_level) {
+      uint32_t al = 0;
+      if (a.alloc_out) {   // a4 fused (the eval path): WMAX-MIN over this scenario's demands, written out
+        if (nd <= DSTACK_MAX_DNN_PER_SCEN) {
+          al = wmaxmin_lane(dem, lane, nd, L);
+          if (mine) a.alloc_out[k] = al;
+        } else {
+          for (int j = lane; j < nd; j += 32) a.alloc_out[k0 + j] = 0;
+        }
+      } else if (mine) {
+        al = a.alloc[k];
+      }
+      al >>= 16;
+      g = dem == 0 ? 0u : (dem > al ? dem : al);
     }
     const bool active = mine && dem > 0;
     if (nd > DSTACK_MAX_DNN_PER_SCEN) {

@@ -41,6 +41,7 @@ struct CycArgs {
   const uint16_t *demand;
   const uint8_t *batch;
   const uint32_t *alloc;
+  uint32_t *alloc_out;     // non-NULL (eval path): a4 fused -- WMAX-MIN computed here and written out; alloc unused
   const int32_t *hook_level;
   const int32_t *hook_d;
   uint16_t *level;
