@@ -150,7 +150,13 @@ __device__ __forceinline__ IdealRow ideal_row_at(const IdealArgs &a, int64_t i, 
 #ifndef DSTACK_IDEAL_MINB
 #define DSTACK_IDEAL_MINB 4   // 64 registers (the meet-in-the-middle branch would take 109)
 #endif
-__global__ void __launch_bounds__(IDEAL_WARPS * 32, DSTACK_IDEAL_MINB) k_ideal_sim(IdealArgs a) {
+#ifndef DSTACK_IDEAL_FEW
+#define DSTACK_IDEAL_FEW 32768   // below this many scenarios the 3-blocks-per-SM build (79 registers, shorter event
+                                 // latency) runs: few scenarios per warp, the longest event chains set the time
+                                 // (A/B: config 2 (10k) 14.7 -> 13.1 ms; config 4 (100k) 109.1 -> 114.8 ms)
+#endif
+template <int MINB>
+__global__ void __launch_bounds__(IDEAL_WARPS * 32, MINB) k_ideal_sim(IdealArgs a) {
   __shared__ uint8_t reach_all[IDEAL_WARPS][DSTACK_MAX_DNN_PER_SCEN + 1][32];
   __shared__ uint8_t grank_all[IDEAL_WARPS][32];   // g of the live item of each priority rank
   __shared__ uint32_t mbb_all[IDEAL_WARPS][8];     // meet in the middle: achievable B sums (256-bit set)
@@ -548,10 +554,12 @@ int launch_ideal(IdealArgs a, void *ws, cudaStream_t s, int *launches) {
   }
   int64_t blocks = (a.pb.num_scen + IDEAL_WARPS - 1) / IDEAL_WARPS;
   if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  const bool few = a.pb.num_scen < DSTACK_IDEAL_FEW;
   if (!DSTACK_DYN_SCEN) a.work_ctr = nullptr;
   if (a.work_ctr) {   // one resident wave pulling scenarios (their event counts differ by orders of magnitude)
     if (cudaMemsetAsync(a.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
-    blocks = resident_wave(k_ideal_sim, IDEAL_WARPS * 32, 0, blocks);
+    blocks = few ? resident_wave(k_ideal_sim<3>, IDEAL_WARPS * 32, 0, blocks)
+                 : resident_wave(k_ideal_sim<DSTACK_IDEAL_MINB>, IDEAL_WARPS * 32, 0, blocks);
     if (DSTACK_IDEAL_ORDER) {   // heaviest estimated scenarios first
       if (cudaMemsetAsync(a.bucket_cnt, 0, sizeof(uint32_t) * IDEAL_BUCKETS, s) != cudaSuccess) return DSTACK_ELAUNCH;
       int64_t ob = (a.pb.num_scen + 255) / 256;
@@ -566,7 +574,8 @@ int launch_ideal(IdealArgs a, void *ws, cudaStream_t s, int *launches) {
   } else {
     a.order = nullptr;
   }
-  k_ideal_sim<<<(unsigned)blocks, IDEAL_WARPS * 32, 0, s>>>(a);
+  if (few) k_ideal_sim<3><<<(unsigned)blocks, IDEAL_WARPS * 32, 0, s>>>(a);
+  else k_ideal_sim<DSTACK_IDEAL_MINB><<<(unsigned)blocks, IDEAL_WARPS * 32, 0, s>>>(a);
   ++*launches;
   return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;
 }
