@@ -1068,6 +1068,11 @@ def run_sim(args, rank, world, local):
                                 "unserved_frac": q["unserved"] / max(q["arrived"], 1),
                                 "realloc_frac": q["realloc"] / max(dp.num_scen * max(args.cycles - 1, 1), 1),
                                 "scenarios": dp.num_scen, "note": "rank 0's shard"}
+        # the per-cycle aggregate series (dstack_sim_out_t.series) of rank 0's shard, one untimed call
+        rs = ds.simulate(dp, p, args.cycles, sp.seed, sp.cfg_tag, scen_base=sp.scen_base, series=True)["series"]
+        rs = rs.cpu().tolist()
+        line["series"] = {"columns": list(ds.SIM_SERIES), "rows": {str(c): rs[c] for c in sorted({0, 1, 2, len(rs) - 1})},
+                          "note": "rank 0's shard; row c sums session c over the scenarios (dstack.h DSTACK_SIM_*)"}
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = sim_cpu_baseline(args, sp0, p)
         print(json.dumps(line), flush=True)

@@ -214,10 +214,27 @@ int dstack_aggregate(const dstack_problem_t *pb, const dstack_params_t *p, dstac
  * after arrival + SLO), unserved (queued at the horizon), occ_sum (sum over non-void runs of level x
  * slots; mean utilisation = occ_sum / (nslots L cycles)), runs (non-void), misses (unplaced static jobs),
  * realloc (sessions 2..cycles whose active DNN set differs from the previous session's: each is a per-cycle
- * WMAX-MIN re-allocation over a changed set).  Workspace: dstack_sim_workspace_size(). */
+ * WMAX-MIN re-allocation over a changed set).
+ * series (optional, may be NULL): the per-cycle aggregate series, u64 [cycles][DSTACK_SIM_SERIES], zeroed by the
+ * call; row c sums over the scenarios' session c: DSTACK_SIM_ACTIVE DNNs with requests queued at its start,
+ * DSTACK_SIM_REALLOC scenarios whose active set changed at c (c >= 1), DSTACK_SIM_RUNS non-void runs,
+ * DSTACK_SIM_SERVED requests served, DSTACK_SIM_IN_SLO / DSTACK_SIM_LATE of them in / after SLO,
+ * DSTACK_SIM_OCC level-slots of the non-void runs, DSTACK_SIM_MISSES unplaced static jobs.  A scenario that turns
+ * INVALID at session c (fill-run capacity) contributes its sessions before c.  Sums of integers: exact and
+ * independent of the launch.  Workspace: dstack_sim_workspace_size(). */
+#define DSTACK_SIM_ACTIVE 0
+#define DSTACK_SIM_REALLOC 1
+#define DSTACK_SIM_RUNS 2
+#define DSTACK_SIM_SERVED 3
+#define DSTACK_SIM_IN_SLO 4
+#define DSTACK_SIM_LATE 5
+#define DSTACK_SIM_OCC 6
+#define DSTACK_SIM_MISSES 7
+#define DSTACK_SIM_SERIES 8
 typedef struct {
   uint8_t *status; uint32_t *T_us;
   uint64_t *arrived, *in_slo, *late, *unserved, *occ_sum, *runs, *misses, *realloc;
+  uint64_t *series;
 } dstack_sim_out_t;
 size_t dstack_sim_workspace_size(const dstack_problem_t *pb, const dstack_params_t *p);
 int dstack_simulate(const dstack_problem_t *pb, const dstack_params_t *p, const int32_t *lam_pct, int32_t cycles,

@@ -52,7 +52,7 @@ class OrCycSum(C.Structure):
 
 class OrSimOut(C.Structure):
     _fields_ = [(k, C.c_void_p) for k in ("status", "T_us", "arrived", "in_slo", "late", "unserved", "occ_sum", "runs",
-                                          "misses", "realloc")]
+                                          "misses", "realloc", "series")]
 
 
 _lib = None
@@ -343,13 +343,16 @@ def evaluate(pb: Problem, p: Params, nthreads: int = 0, subset=None):
 
 
 def simulate(pb: Problem, p: Params, cycles: int, seed: int, cfg_tag: int, scen_base: int = 0, subset=None,
-             nthreads: int = 0):
-    """O7 long-horizon simulation; per-scenario dict (subset: scenario indices, others left zero)."""
+             nthreads: int = 0, series: bool = False):
+    """O7 long-horizon simulation; per-scenario dict (subset: scenario indices, others left zero).  series: also
+    the per-cycle aggregate series, uint64 [cycles, 8] (dstack.h DSTACK_SIM_* order)."""
     S = pb.num_scen
     o = dict(status=np.zeros(S, np.uint8), T_us=np.zeros(S, np.uint32),
              **{k: np.zeros(S, np.uint64) for k in ("arrived", "in_slo", "late", "unserved", "occ_sum", "runs",
                                                      "misses", "realloc")})
-    oo = OrSimOut(*[_p(o[k]) for k, _ in OrSimOut._fields_])
+    if series:
+        o["series"] = np.zeros((max(cycles, 1), 8), np.uint64)
+    oo = OrSimOut(*[(_p(o[k]) if k in o else None) for k, _ in OrSimOut._fields_])
     lam = np.ascontiguousarray(pb.lam_pct, np.int32)
     idx = None if subset is None else np.ascontiguousarray(np.asarray(list(subset)), np.int64)
     rc = lib().oracle_simulate(C.byref(_problem(pb)), C.byref(_params(p)), _p(lam), cycles, seed, cfg_tag, scen_base,

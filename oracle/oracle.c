@@ -1271,8 +1271,15 @@ static void simulate_scenario(const or_problem_t *pb, const or_params_t *p, cons
       if (A > served[j]) dm[j] = dem[j];                 /* active: requests queued at the cycle start */
     }
     int changed = 0;                                       /* the active set moved: WMAX-MIN re-allocates */
-    for (int32_t j = 0; j < nd; ++j) { changed |= (dm[j] > 0) != prev_act[j]; prev_act[j] = dm[j] > 0; }
+    uint64_t nact = 0;
+    for (int32_t j = 0; j < nd; ++j) {
+      changed |= (dm[j] > 0) != prev_act[j]; prev_act[j] = dm[j] > 0;
+      nact += dm[j] > 0;
+    }
     if (c > 0) o->realloc[s] += (uint64_t)changed;
+    const uint64_t in0 = o->in_slo[s], late0 = o->late[s], occ0 = o->occ_sum[s], runs0 = o->runs[s];
+    uint64_t srv0 = 0;
+    for (int32_t j = 0; j < nd; ++j) srv0 += served[j];
     oracle_wmaxmin(nd, dm, p->L, alloc);
     for (int32_t j = 0; j < nd; ++j) {
       g[j] = 0; sl[j] = pb->slo_us[k0 + j] / p->slot_us; bst[j] = bst8[j];
@@ -1326,6 +1333,16 @@ static void simulate_scenario(const or_problem_t *pb, const or_params_t *p, cons
     }
     free(rl);
     for (int32_t j = 0; j < nd; ++j) { sb[j] += cnt[j] - ring[c % 10][j]; ring[c % 10][j] = cnt[j]; }
+    if (o->series) {   /* this session's row of the per-cycle series (a completed session only) */
+      uint64_t srv = 0;
+      for (int32_t j = 0; j < nd; ++j) srv += served[j];
+      const uint64_t v[8] = {nact, (uint64_t)(c > 0 && changed), o->runs[s] - runs0, srv - srv0,
+                             o->in_slo[s] - in0, o->late[s] - late0, o->occ_sum[s] - occ0, (uint64_t)cs.misses};
+      for (int f = 0; f < 8; ++f) {
+#pragma omp atomic
+        o->series[(int64_t)c * 8 + f] += v[f];
+      }
+    }
   }
   const uint64_t tend = (uint64_t)cycles * (uint64_t)T;
   for (int32_t j = 0; j < nd; ++j) {

@@ -145,6 +145,8 @@ typedef struct {
   uint8_t *status; uint32_t *T_us;
   uint64_t *arrived, *in_slo, *late, *unserved, *occ_sum, *runs, *misses;
   uint64_t *realloc;   /* sessions 2..cycles whose active set differs from the previous session's */
+  uint64_t *series;    /* optional [cycles][8] per-cycle sums over the scenarios (dstack_sim_out_t.series order):
+                          active DNNs, realloc, runs, served, in SLO, late, occupied level-slots, misses */
 } or_sim_out_t;
 int oracle_simulate(const or_problem_t *pb, const or_params_t *p, const int32_t *lam_pct, int32_t cycles,
                     uint64_t seed, int32_t cfg_tag, int64_t scen_base, or_sim_out_t *out, const int64_t *scen_idx,

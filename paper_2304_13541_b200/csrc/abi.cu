@@ -393,6 +393,9 @@ int dstack_simulate(const dstack_problem_t *pb, const dstack_params_t *p, const 
   m.ws_D = a.ws_D; m.dtab_rows = (uint16_t *)(base + w.dtab); m.fill_log = (uint64_t *)(base + sl.log);
   m.out = *out;
   m.work_ctr = (uint32_t *)(base + w.ctr) + 5;
+  if (out->series && cycles > 0 &&
+      cudaMemsetAsync(out->series, 0, (size_t)cycles * DSTACK_SIM_SERIES * sizeof(uint64_t), s) != cudaSuccess)
+    return DSTACK_ELAUNCH;
   return finish(launch_sim(m, s, &g_launches));
 }
 

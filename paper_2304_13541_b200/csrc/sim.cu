@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(SIM_WARPS * 32, DSTACK_SIM_MINB) k_sim(SimArgs
         if (ok) while (arr.time <= t0) arr_next(arr, a, gs, (uint32_t)lane, mq);
         const bool active = ok && arr.idx > served;
         const uint32_t act_mask = __ballot_sync(FULL, active);   // a changed set: WMAX-MIN re-allocates
+        const uint32_t prev_mask = prev_act;
         if (c > 0 && act_mask != prev_act) ++realloc;
         prev_act = act_mask;
         const uint32_t dm = active ? dem : 0u;
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(SIM_WARPS * 32, DSTACK_SIM_MINB) k_sim(SimArgs
                                      srv, sb, fill_log, DSTACK_MAX_FILL_RUNS, &nfill);
         misses += cr.misses;
         if (nfill > DSTACK_MAX_FILL_RUNS) { sst = DSTACK_ST_INVALID; break; }
+        const uint64_t in0 = in_slo, late0 = late, sv0 = served, occ0 = occ_tot, nr0 = nruns;   // per-cycle series
         // ---- execute this lane's runs in start order: static windows merged with its fill runs ----
         uint32_t cnt = 0;
         uint32_t jo = active ? rep : 0u;   // this lane's static-run offset (as in cycle_core)
@@ -158,6 +160,22 @@ __global__ void __launch_bounds__(SIM_WARPS * 32, DSTACK_SIM_MINB) k_sim(SimArgs
             cnt++;
             occ_tot += (uint64_t)g * d;
             nruns++;
+          }
+        }
+        if (a.out.series) {   // this session's row of the per-cycle aggregate series
+          const uint64_t v_in = warp_sum_u64(in_slo - in0), v_late = warp_sum_u64(late - late0);
+          const uint64_t v_sv = warp_sum_u64(served - sv0), v_occ = warp_sum_u64(occ_tot - occ0);
+          const uint64_t v_runs = warp_sum_u64(nruns - nr0);
+          if (lane == 0) {
+            unsigned long long *row = reinterpret_cast<unsigned long long *>(a.out.series) + (int64_t)c * DSTACK_SIM_SERIES;
+            atomicAdd(row + DSTACK_SIM_ACTIVE, (unsigned long long)__popc(act_mask));
+            if (c > 0 && act_mask != prev_mask) atomicAdd(row + DSTACK_SIM_REALLOC, 1ull);
+            if (v_runs) atomicAdd(row + DSTACK_SIM_RUNS, (unsigned long long)v_runs);
+            if (v_sv) atomicAdd(row + DSTACK_SIM_SERVED, (unsigned long long)v_sv);
+            if (v_in) atomicAdd(row + DSTACK_SIM_IN_SLO, (unsigned long long)v_in);
+            if (v_late) atomicAdd(row + DSTACK_SIM_LATE, (unsigned long long)v_late);
+            if (v_occ) atomicAdd(row + DSTACK_SIM_OCC, (unsigned long long)v_occ);
+            if (cr.misses) atomicAdd(row + DSTACK_SIM_MISSES, (unsigned long long)cr.misses);
           }
         }
         sb += cnt - ring[(c % 10) * 32 + lane];

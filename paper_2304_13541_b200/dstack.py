@@ -63,8 +63,11 @@ class COut(C.Structure):
 _SIM_FIELDS = ("status", "T_us", "arrived", "in_slo", "late", "unserved", "occ_sum", "runs", "misses", "realloc")
 
 
+SIM_SERIES = ("active", "realloc", "runs", "served", "in_slo", "late", "occ", "misses")   # DSTACK_SIM_* columns
+
+
 class CSimOut(C.Structure):
-    _fields_ = [(k, C.c_void_p) for k in _SIM_FIELDS]
+    _fields_ = [(k, C.c_void_p) for k in _SIM_FIELDS] + [("series", C.c_void_p)]
 
 
 class CHook(C.Structure):
@@ -389,18 +392,23 @@ def profile_stop() -> tuple[dict, int]:
     return {k: ms[i] for i, k in enumerate(PROF_SLOTS)}, calls.value
 
 
-def simulate(dp: DeviceProblem, p, cycles: int, seed: int, cfg_tag: int, scen_base: int = 0):
-    """dstack_simulate (a7, config 5): per-scenario counters as device tensors (uint64 stored as int64)."""
+def simulate(dp: DeviceProblem, p, cycles: int, seed: int, cfg_tag: int, scen_base: int = 0, series: bool = False):
+    """dstack_simulate (a7, config 5): per-scenario counters as device tensors (uint64 stored as int64); series:
+    also the per-cycle aggregate series [cycles, 8] (columns SIM_SERIES)."""
     dev = dp.device
     S = max(dp.num_scen, 1)
     o = dict(status=torch.zeros(S, dtype=torch.uint8, device=dev), T_us=torch.zeros(S, dtype=torch.int32, device=dev),
              **{k: torch.zeros(S, dtype=torch.int64, device=dev) for k in _SIM_FIELDS[2:]})
+    ser = torch.zeros((max(cycles, 1), len(SIM_SERIES)), dtype=torch.int64, device=dev) if series else None
     wsz = int(_lib.dstack_sim_workspace_size(C.byref(dp.c()), C.byref(cparams(p))))
     ws = Workspace(wsz, dev)
+    cout = CSimOut(*[o[k].data_ptr() for k in _SIM_FIELDS], ser.data_ptr() if ser is not None else None)
     _check(_lib.dstack_simulate(C.byref(dp.c()), C.byref(cparams(p)), _ptr(dp.lam_pct), cycles, seed, cfg_tag,
-                                scen_base, C.byref(CSimOut(*[o[k].data_ptr() for k in _SIM_FIELDS])), ws.ptr(),
-                                ws.nbytes, _stream(dev)), "dstack_simulate")
-    return {k: v[: dp.num_scen] for k, v in o.items()}
+                                scen_base, C.byref(cout), ws.ptr(), ws.nbytes, _stream(dev)), "dstack_simulate")
+    r = {k: v[: dp.num_scen] for k, v in o.items()}
+    if ser is not None:
+        r["series"] = ser[:cycles]
+    return r
 
 
 IDEAL_STATS = ("events", "reselections", "sel_all_fit", "sel_enumeration", "sel_meet_in_middle", "sel_dp", "scenarios")

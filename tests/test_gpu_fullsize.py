@@ -93,7 +93,7 @@ def test_config5_fullsize_sampled_parity(ds):
     cycles = 1000
     g = synth.generate_device(sp, "cuda")
     dp = ds.from_device_dict(g)
-    r = ds.simulate(dp, p, cycles, sp.seed, sp.cfg_tag)
+    r = ds.simulate(dp, p, cycles, sp.seed, sp.cfg_tag, series=True)
     torch.cuda.synchronize()
     idx = np.arange(0, sp.num_scen, 2500)
     for s in idx:
@@ -105,6 +105,12 @@ def test_config5_fullsize_sampled_parity(ds):
     arrived = r["arrived"].cpu().numpy()
     kept = (r["in_slo"] + r["late"] + r["unserved"]).cpu().numpy()
     assert np.array_equal(arrived, kept)   # conservation over all 100k scenarios
+    # the per-cycle series adds up to the per-scenario totals (every scenario OK: no partial contributions)
+    ser = r["series"].cpu().numpy().sum(axis=0)
+    if bool((r["status"] != 3).all()):   # no INVALID scenario (whose sessions before it turned INVALID would count)
+        for col, k in ((1, "realloc"), (2, "runs"), (4, "in_slo"), (5, "late"), (6, "occ_sum"), (7, "misses")):
+            assert int(ser[col]) == int(r[k].sum().item()), k
+        assert int(ser[3]) == int((r["in_slo"] + r["late"]).sum().item())   # served = in SLO + late
 
 
 def test_knee_probe_config3_fullsize_sampled(ds):

@@ -61,6 +61,8 @@ def reference_sim(pb, p, s, cycles, seed, cfg_tag):
     served = [0] * nd
     ring = np.zeros((10, nd), np.int64)
     res = dict(in_slo=0, late=0, occ_sum=0, runs=0, misses=0, realloc=0)
+    # per-cycle rows in dstack.h's DSTACK_SIM_* order: active, realloc, runs, served, in SLO, late, occ, misses
+    res["series"] = np.zeros((cycles, 8), np.int64)
     prev = None
     for c in range(cycles):
         t0 = c * T
@@ -69,8 +71,11 @@ def reference_sim(pb, p, s, cycles, seed, cfg_tag):
             if streams[j].count(t0) > served[j]:
                 dm[j] = bo["demand"][j]
         act = tuple(int(x > 0) for x in dm)   # the active set; a change means a WMAX-MIN re-allocation
+        row = res["series"][c]
+        row[0] = sum(act)
         if prev is not None and act != prev:
             res["realloc"] += 1
+            row[1] = 1
         prev = act
         al = oracle.wmaxmin(dm, p.L)
         g = np.zeros(nd, np.int32); dtab = np.zeros((nd, 64), np.int64)
@@ -87,6 +92,7 @@ def reference_sim(pb, p, s, cycles, seed, cfg_tag):
         cyc = oracle.cycle_direct(g, sl, bo["batch"].astype(np.int32), dtab, p.b_min, p.L, nslots,
                                   count0=ring.sum(axis=0))
         res["misses"] += cyc["misses"]
+        row[7] = cyc["misses"]
         tr = cyc["trace"]
         order = sorted(range(len(tr["dnn"])), key=lambda q: (tr["dnn"][q], tr["start"][q]))
         cnt = np.zeros(nd, np.int64)
@@ -99,12 +105,17 @@ def reference_sim(pb, p, s, cycles, seed, cfg_tag):
             for i in range(served[j], served[j] + k):
                 if te - streams[j].time(i) > int(one.slo_us[j]):
                     res["late"] += 1
+                    row[5] += 1
                 else:
                     res["in_slo"] += 1
+                    row[4] += 1
             served[j] += k
+            row[3] += k
             cnt[j] += 1
             res["occ_sum"] += int(g[j]) * (en - st)
+            row[6] += int(g[j]) * (en - st)
             res["runs"] += 1
+            row[2] += 1
         ring[c % 10] = cnt
     res["arrived"] = sum(streams[j].count(cycles * T) for j in streams)
     res["unserved"] = res["arrived"] - sum(served)
@@ -114,13 +125,17 @@ def reference_sim(pb, p, s, cycles, seed, cfg_tag):
 def test_sim_matches_independent_reimplementation():
     sp, p, pb = small_sim_problem(num_scen=4, rows_pct=10)
     cycles = 12
-    o = oracle.simulate(pb, p, cycles, sp.seed, sp.cfg_tag)
+    o = oracle.simulate(pb, p, cycles, sp.seed, sp.cfg_tag, series=True)
+    series = np.zeros((cycles, 8), np.int64)
     for s in range(pb.num_scen):
         want = reference_sim(pb, p, s, cycles, sp.seed, sp.cfg_tag)
         if want is None:
             continue
         for k in ("arrived", "in_slo", "late", "unserved", "occ_sum", "runs", "misses", "realloc"):
             assert int(o[k][s]) == want[k], (s, k, int(o[k][s]), want[k])
+        series += want["series"]
+    # the per-cycle aggregate series (dstack.h DSTACK_SIM_*), summed over the scenarios
+    assert np.array_equal(o["series"].astype(np.int64), series)
 
 
 def test_sim_conservation_and_determinism():
