@@ -51,15 +51,19 @@ __device__ __forceinline__ uint32_t warp_or(uint32_t v) { return __reduce_or_syn
 #endif
 
 // Work distribution of warp-per-item kernels: with a counter (a resident wave of warps, each taking the next item
-// when it finishes one -- items of very different cost balance themselves) or else a grid stride.
+// when it finishes one -- items of very different cost balance themselves) or else a grid stride.  The item index
+// is delivered by a reduction, not a shuffle: it lands in a uniform register, so the compiler can prove that every
+// loop and branch derived from it is warp-uniform and emits no divergence check (BRA.DIV) at the collectives of
+// the item's body (items < 2^31, so the index fits the u32 reduction).
 __device__ __forceinline__ int64_t warp_next_item(uint32_t *ctr, int64_t prev, int64_t gwarp, int64_t nwarps,
                                                   int lane) {
+  uint32_t v = 0;
   if (ctr) {
-    uint32_t v = 0;
     if (lane == 0) v = atomicAdd(ctr, 1u);
-    return (int64_t)__shfl_sync(FULL, v, 0);
+  } else {
+    v = (uint32_t)(prev < 0 ? gwarp : prev + nwarps);
   }
-  return prev < 0 ? gwarp : prev + nwarps;
+  return (int64_t)__reduce_max_sync(FULL, v);
 }
 
 // bulk L2 prefetch of [ptr, ptr+bytes) (TMA engine, no registers / no wait): 16-byte aligned chunks

@@ -50,14 +50,7 @@ __global__ void __launch_bounds__(CYC_WARPS * 32, BK ? DSTACK_CYC_BK_MINB : DSTA
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   // scenario order: a work counter (one resident wave of warps, each takes the next scenario when it finishes one)
   // or a grid stride
-  auto fetch = [&](int64_t prev) -> int64_t {
-    if (a.work_ctr) {
-      uint32_t v = 0;
-      if (lane == 0) v = atomicAdd(a.work_ctr, 1u);
-      return (int64_t)__shfl_sync(FULL, v, 0);
-    }
-    return prev < 0 ? gwarp : prev + nwarps;
-  };
+  auto fetch = [&](int64_t prev) -> int64_t { return warp_next_item(a.work_ctr, prev, gwarp, nwarps, lane); };
   for (int64_t s = fetch(-1); s < a.pb.num_scen; s = fetch(s)) {
     const int32_t k0 = a.pb.scen_dnn_off[s], nd = a.pb.scen_dnn_off[s + 1] - k0;
     uint8_t sst = DSTACK_ST_OK;

@@ -426,13 +426,14 @@ __global__ void __launch_bounds__(256, DSTACK_PROF_MINB) k_prof_fast(const __gri
   // groups of 32 DNNs: taken from the work counter (one resident wave of warps) or the warp's contiguous range
   const bool dyn = a.work_ctr != nullptr;
   const int64_t kend = dyn ? pb.num_dnn : (kbeg + per < pb.num_dnn ? kbeg + per : pb.num_dnn);
-  auto fetch = [&](int64_t prev) -> int64_t {
+  auto fetch = [&](int64_t prev) -> int64_t {   // a reduction: the index is provably warp-uniform (common.cuh)
+    uint32_t v = 0;
     if (dyn) {
-      uint32_t v = 0;
       if (lane == 0) v = atomicAdd(a.work_ctr, 32u);
-      return (int64_t)__shfl_sync(FULL, v, 0);
+    } else {
+      v = (uint32_t)(prev < 0 ? kbeg : prev + 32);
     }
-    return prev < 0 ? kbeg : prev + 32;
+    return (int64_t)__reduce_max_sync(FULL, v);
   };
   for (int64_t kb = fetch(-1); kb < kend; kb = fetch(kb)) {
     const int nj = kend - kb < 32 ? (int)(kend - kb) : 32;
