@@ -57,9 +57,9 @@ bool disjoint(const dstack_problem_t *pb, const void *o) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // workspace layout: [agg partials | counters | d_j(b) rows u16[num_dnn][64] | RT u32[num_dnn] | D u64[num_dnn] |
-//                    d_j(b*) u16[num_dnn] | ideal]
+//                    d_j(b*) u16[num_dnn] | cold-DNN queue u32[num_dnn + 2] | ideal]
 struct WsLayout {
-  size_t ctr, dtab, rt, d, dst, ideal, end;
+  size_t ctr, dtab, rt, d, dst, cold, ideal, end;
 };
 WsLayout ws_layout(const dstack_problem_t *pb, const dstack_params_t *p) {
   WsLayout w;
@@ -69,7 +69,8 @@ WsLayout ws_layout(const dstack_problem_t *pb, const dstack_params_t *p) {
   w.rt = w.dtab + align256(nd * DTAB_ROW * 2);
   w.d = w.rt + align256(nd * 4);
   w.dst = w.d + align256(nd * 8);
-  w.ideal = w.dst + align256(nd * 2);
+  w.cold = w.dst + align256(nd * 2);
+  w.ideal = w.cold + align256((nd + 2) * 4);
   w.end = w.ideal + ((p->flags & DSTACK_FLAG_IDEAL) ? align256(ideal_ws_bytes(pb->num_rows, pb->num_scen)) : 0);
   return w;
 }
@@ -322,6 +323,7 @@ int dstack_eval_batch(const dstack_problem_t *pb, const dstack_params_t *p, dsta
   a.ws_RT = (uint32_t *)((char *)ws + w.rt);
   a.ws_D = (uint64_t *)((char *)ws + w.d);
   a.work_ctr = (uint32_t *)((char *)ws + w.ctr) + 1;   // word 0: k_cycle's counter
+  a.cold_q = (uint32_t *)((char *)ws + w.cold);
   const bool prof = g_prof.on && g_prof.calls < g_prof.max_calls;
   uint8_t *used = prof ? g_prof.used + g_prof.calls * DSTACK_PROF_SLOTS : nullptr;
   // slots: k_prof, (k_wmaxmin: a4 runs inside k_cycle on this path, slot unused), k_cycle, k_ideal, k_agg
@@ -384,6 +386,7 @@ int dstack_simulate(const dstack_problem_t *pb, const dstack_params_t *p, const 
   a.demand = (uint16_t *)(base + sl.dem); a.knee = (uint16_t *)(base + sl.knee);
   a.batch = (uint8_t *)(base + sl.bat); a.status = (uint8_t *)(base + sl.st);
   a.ws_RT = (uint32_t *)(base + w.rt); a.ws_D = (uint64_t *)(base + w.d);
+  a.cold_q = (uint32_t *)(base + w.cold);
   int rc = launch_prof(a, s, &g_launches);   // a1-a3 (RT, D for the arrival rates and d_j(b))
   if (rc) return finish(rc);
   SimArgs m;

@@ -33,6 +33,8 @@ struct ProfArgs {
   uint32_t *ws_RT;
   uint64_t *ws_D;
   uint32_t *work_ctr;   // workspace word: k_prof_fast's DNN-group counter (NULL: contiguous ranges)
+  uint32_t *cold_q;     // workspace [num_dnn + 2] (eval path): [0] count, [1] pull counter, then the DNNs k_prof_lane
+                        // leaves to the generic path, which k_prof_cold then analyses (NULL: analysed in place)
 };
 
 struct CycArgs {

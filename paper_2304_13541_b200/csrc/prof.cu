@@ -639,6 +639,10 @@ __device__ __forceinline__ void lane_scan_f(const uint32_t *H, const uint16_t *l
   }
 }
 
+// QUEUE: DNNs outside the fast ranges are queued for k_prof_cold instead of analysed in place: a call inside the
+// group loop would make the compiler distrust the warp's convergence everywhere in it (a divergence check at every
+// collective); with the queue the loop has none.
+template <bool QUEUE>
 __global__ void __launch_bounds__(DSTACK_PLANE_WARPS * 32, DSTACK_PLANE_MINB) k_prof_lane(const __grid_constant__ ProfArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const dstack_problem_t &pb = a.pb;
@@ -698,8 +702,10 @@ __global__ void __launch_bounds__(DSTACK_PLANE_WARPS * 32, DSTACK_PLANE_MINB) k_
     // ---- zero the 32 histogram rows (16-byte stores) ----
     {
       uint4 *hz = reinterpret_cast<uint4 *>(Htab);
-      for (int i = lane; i < (hwords >> 2); i += 32) hz[i] = make_uint4(0u, 0u, 0u, 0u);
-      for (int i = (hwords & ~3) + lane; i < hwords; i += 32) Htab[i] = 0u;
+      // warp-uniform loops (lane-dependent trip counts would make the compiler distrust convergence afterwards)
+      for (int i0 = 0; i0 < (hwords >> 2); i0 += 32)
+        if (i0 + lane < (hwords >> 2)) hz[i0 + lane] = make_uint4(0u, 0u, 0u, 0u);
+      if ((hwords & ~3) + lane < hwords) Htab[(hwords & ~3) + lane] = 0u;
     }
     __syncwarp();
     // ---- a1: row pass, one DNN after the other (coalesced), results to the owning lane; the first
@@ -718,11 +724,13 @@ __global__ void __launch_bounds__(DSTACK_PLANE_WARPS * 32, DSTACK_PLANE_MINB) k_
         if (i0 + 32 * u < Kb) { bn[u] = __ldg(np + 32 * u); bd[u] = __ldg(dp + 32 * u); br[u] = __ldg(rp + 32 * u); }
       }
     };
-    int32_t Kc = nj > 0 ? __shfl_sync(FULL, K, 0) : 0;
+    // row counts broadcast by a reduction (not a shuffle): warp-uniform to the compiler, so the row loops bounded by
+    // them carry no divergence checks (K >= 0)
+    int32_t Kc = (int32_t)__reduce_max_sync(FULL, lane == 0 ? (uint32_t)K : 0u);
     int64_t rc = nj > 0 ? (int64_t)shfl_u64((uint64_t)r0, 0) : 0;
     load_batch(rc, Kc, lane, cn, cd, cr);
     for (int jj = 0; jj < nj; ++jj) {
-      const int32_t Kn = jj + 1 < nj ? __shfl_sync(FULL, K, jj + 1) : 0;
+      const int32_t Kn = (int32_t)__reduce_max_sync(FULL, lane == jj + 1 ? (uint32_t)K : 0u);   // 0 past the group
       const int64_t rn = jj + 1 < nj ? (int64_t)shfl_u64((uint64_t)r0, jj + 1) : 0;
       load_batch(rn, Kn, lane, pn, pd, pr);   // prefetch (predicated off past the group / for invalid DNNs)
       if (Kc > 0) {
@@ -744,10 +752,10 @@ __global__ void __launch_bounds__(DSTACK_PLANE_WARPS * 32, DSTACK_PLANE_MINB) k_
           }
         };
         accum(cn, cd, cr, lane);
-        for (int i0 = lane + 32 * U; i0 - lane < Kc; i0 += 32 * U) {   // rows beyond the prefetched batch
+        for (int b0 = 32 * U; b0 < Kc; b0 += 32 * U) {   // rows beyond the prefetched batch (a warp-uniform loop)
           uint32_t tn[U], td[U], tr[U];
-          load_batch(rc, Kc, i0, tn, td, tr);
-          accum(tn, td, tr, i0);
+          load_batch(rc, Kc, b0 + lane, tn, td, tr);
+          accum(tn, td, tr, b0 + lane);
         }
         RT = __reduce_add_sync(FULL, RT);
         Rmin = __reduce_min_sync(FULL, Rmin);
@@ -856,18 +864,48 @@ __global__ void __launch_bounds__(DSTACK_PLANE_WARPS * 32, DSTACK_PLANE_MINB) k_
       if (a.batch) a.batch[kl] = okst ? 1 : 0;
     }
     // ---- the generic path for the DNNs outside the fast ranges ----
-    uint32_t colds = __ballot_sync(FULL, have && cold);
-    if (colds) {   // the cold path expects a zeroed hist (its scratch overlays the H table)
-      __syncwarp();
-      for (int m = lane; m <= S_tot; m += 32) hist[m] = 0;
-      __syncwarp();
-    }
-    while (colds) {
-      const int j = __ffs(colds) - 1;
-      colds &= colds - 1;
-      prof_one_cold(&a, kb + j, Stab, hist, cA, cU, lane);
+    if (QUEUE) {
+      if (have && cold) a.cold_q[2 + atomicAdd(a.cold_q, 1u)] = (uint32_t)kl;
+    } else {
+      uint32_t colds = __ballot_sync(FULL, have && cold);
+      if (colds) {   // the cold path expects a zeroed hist (its scratch overlays the H table)
+        __syncwarp();
+        for (int m = lane; m <= S_tot; m += 32) hist[m] = 0;
+        __syncwarp();
+      }
+      while (colds) {
+        const int j = __ffs(colds) - 1;
+        colds &= colds - 1;
+        prof_one_cold(&a, kb + j, Stab, hist, cA, cU, lane);
+      }
     }
     __syncwarp();
+  }
+}
+
+// The DNNs k_prof_lane<true> queued (outside its fast ranges, or b* = 1 not certified): the generic exact analysis,
+// one warp per DNN pulled from the queue (usually none: the warps read the count and exit).
+__global__ void __launch_bounds__(256) k_prof_cold(const __grid_constant__ ProfArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int L = a.p.L, S_tot = a.p.S_tot;
+  uint16_t *Stab = (uint16_t *)smem;
+  const int tab_bytes = ((L + 1 + S_tot + 1) * 2 + 15) & ~15;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t n = a.cold_q[0];
+  if (n == 0) return;
+  unsigned char *wreg = smem + tab_bytes + (size_t)warp * prof_warp_bytes(S_tot);
+  uint64_t *cA = (uint64_t *)wreg;
+  uint64_t *cU = cA + (S_tot + 1);
+  uint32_t *hist = (uint32_t *)(cU + (S_tot + 1));
+  fill_stab(Stab, L, S_tot);
+  for (int m = lane; m <= S_tot; m += 32) hist[m] = 0;
+  __syncthreads();
+  for (;;) {
+    uint32_t i = 0;
+    if (lane == 0) i = atomicAdd(a.cold_q + 1, 1u);
+    i = __shfl_sync(FULL, i, 0);
+    if (i >= n) break;
+    prof_one_cold(&a, (int64_t)a.cold_q[2 + i], Stab, hist, cA, cU, lane);
   }
 }
 
@@ -904,12 +942,24 @@ int launch_prof(const ProfArgs &a, cudaStream_t s, int *launches) {
     // k_prof_lane: one resident wave of warps pulling groups of 32 DNNs (grid stride over groups without a counter)
     const int pw = DSTACK_PLANE_WARPS;
     const size_t sm2 = plane_smem_bytes(&a.p, pw);
-    cudaFuncSetAttribute(k_prof_lane, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     const int64_t groups = (a.pb.num_dnn + 31) / 32;
     int64_t nb = (groups + pw - 1) / pw;
-    const int64_t wave = resident_wave(k_prof_lane, pw * 32, sm2, nb);
-    if (b.work_ctr || nb > wave) nb = wave;
-    k_prof_lane<<<(unsigned)nb, pw * 32, sm2, s>>>(b);
+    if (b.cold_q) {
+      cudaFuncSetAttribute(k_prof_lane<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      const int64_t wave = resident_wave(k_prof_lane<true>, pw * 32, sm2, nb);
+      if (b.work_ctr || nb > wave) nb = wave;
+      if (cudaMemsetAsync(b.cold_q, 0, 2 * sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
+      k_prof_lane<true><<<(unsigned)nb, pw * 32, sm2, s>>>(b);
+      const size_t smc = (size_t)(((a.p.L + 1 + a.p.S_tot + 1) * 2 + 15) & ~15) + 8 * prof_warp_bytes(a.p.S_tot);
+      cudaFuncSetAttribute(k_prof_cold, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+      k_prof_cold<<<(unsigned)num_sms(), 256, smc, s>>>(b);
+      ++*launches;
+    } else {
+      cudaFuncSetAttribute(k_prof_lane<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      const int64_t wave = resident_wave(k_prof_lane<false>, pw * 32, sm2, nb);
+      if (b.work_ctr || nb > wave) nb = wave;
+      k_prof_lane<false><<<(unsigned)nb, pw * 32, sm2, s>>>(b);
+    }
   } else if (fast && a.p.S_tot < 5 * 32) launch_k(k_prof_fast<5>, b, blocks, threads, smem, s);
   else if (fast) launch_k(k_prof_fast<9>, b, blocks, threads, smem, s);
   else if (a.p.par_mode == 0) launch_k(k_prof<0>, b, blocks, threads, smem, s);
