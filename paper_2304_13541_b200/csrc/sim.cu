@@ -54,8 +54,9 @@ __global__ void __launch_bounds__(SIM_WARPS * 32, DSTACK_SIM_MINB) k_sim(SimArgs
       ok = a.status[k] == DSTACK_ST_OK;
       dem = ok ? a.demand[k] : 0u; bs = ok ? a.batch[k] : 0u; slo = (uint32_t)a.pb.slo_us[k];
     }
-    if (nd > DSTACK_MAX_DNN_PER_SCEN) sst = DSTACK_ST_INVALID;
-    else if (nd <= 0 || (T = __reduce_max_sync(FULL, ok ? slo : 0u)) == 0) sst = DSTACK_ST_INFEASIBLE;
+    T = __reduce_max_sync(FULL, ok ? slo : 0u);   // 0 when nd <= 0 (no lane owns a DNN)
+    if (nd > DSTACK_MAX_DNN_PER_SCEN) { sst = DSTACK_ST_INVALID; T = 0; }
+    else if (T == 0) sst = DSTACK_ST_INFEASIBLE;
     int32_t nslots = 0;
     if (sst == DSTACK_ST_OK) {
       nslots = (int32_t)(T / (uint32_t)slot);
