@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(CLU_WARPS * 32, DSTACK_CLU_MINB) k_cluster(con
     uint32_t dem = 0, bs = 0, slo = 0, sl = 1;
     if (mine) { dem = a.demand[k]; bs = a.batch[k]; slo = (uint32_t)a.pb.slo_us[k]; sl = slo / (uint32_t)slot; }
     const bool active = mine && dem > 0;
-    uint32_t T = nd > DSTACK_MAX_DNN_PER_SCEN ? 0u : __reduce_max_sync(FULL, active ? slo : 0u);
+    uint32_t T = __reduce_max_sync(FULL, active ? slo : 0u);   // 0 when nd > DSTACK_MAX_DNN_PER_SCEN (no lane active); unconditional: see sim.cu
     int32_t nslots = 0;
     if (T > 0) {
       nslots = (int32_t)(T / (uint32_t)slot);

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(CMP_WARPS * 32, DSTACK_CMP_MINB) k_compare(Cmp
       g = dem == 0 ? 0u : (dem > al ? dem : al);
     }
     const bool active = mine && dem > 0;
-    uint32_t T = nd > DSTACK_MAX_DNN_PER_SCEN ? 0u : __reduce_max_sync(FULL, active ? slo : 0u);
+    uint32_t T = __reduce_max_sync(FULL, active ? slo : 0u);   // 0 when nd > DSTACK_MAX_DNN_PER_SCEN (no lane active); unconditional: see sim.cu
     int32_t nslots = 0;
     if (T > 0) {
       nslots = (int32_t)(T / (uint32_t)slot);
@@ -64,15 +64,18 @@ __global__ void __launch_bounds__(CMP_WARPS * 32, DSTACK_CMP_MINB) k_compare(Cmp
         const int j = __ffs(todo) - 1;
         todo &= todo - 1;
         const int64_t kj = k0 + j;
-        const int32_t gj = (int32_t)__shfl_sync(FULL, g, j), bj = (int32_t)__shfl_sync(FULL, bs, j);
-        const int32_t dj = (int32_t)__shfl_sync(FULL, dem, j);
+        // broadcast by reductions (uniform registers): the conditional out-of-line call below then needs no
+        // divergence checks at the collectives that follow it
+        const int32_t gj = (int32_t)__reduce_max_sync(FULL, lane == j ? g : 0u);
+        const int32_t bj = (int32_t)__reduce_max_sync(FULL, lane == j ? bs : 0u);
+        const int32_t dj = (int32_t)__reduce_max_sync(FULL, lane == j ? dem : 0u);
         const uint64_t M = a.p.mem_mode == 0 ? 1ull : (uint64_t)a.pb.mem_bw[kj];
         const uint64_t SL = (uint64_t)a.p.S_tot, Sk = (uint64_t)s_of(dj, a.p.S_tot, L);
         const uint64_t Sg = (uint64_t)s_of(gj, a.p.S_tot, L);
         // one row pass: the sums, X(g, b*), X(L, b*), X(knee, b*); d_j(b) for b < b* (rare) one pass each
         uint64_t RT, D, Vg, VL, Vk;
         rows_pass3(a.pb, a.p, kj, bj, Sg, SL, Sk, RT, D, Vg, VL, Vk, lane);
-        if (bj > b_lo) dtab_lower(a.pb, a.p, kj, RT, D, gj, b_lo, bj - 1, dtab + j * DTAB_ROW, lane);
+        if (bj > b_lo) dtab_from_rows(a.pb, a.p, kj, RT, D, gj, b_lo, bj - 1, dtab + j * DTAB_ROW, lane);
         if (lane == 0)
           dtab[j * DTAB_ROW + bj - 1] = ceil_div_clamp16(x_of_v(a.pb, a.p, kj, RT, D, Sg, bj, Vg), Sg * M * (uint64_t)slot);
         const uint64_t XL = x_of_v(a.pb, a.p, kj, RT, D, SL, bj, VL);

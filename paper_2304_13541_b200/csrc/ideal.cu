@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, MINB) k_ideal_sim(IdealArgs 
     const int k = k0 + lane;
     const bool act = mine && a.demand[k] > 0;
     const uint32_t slo = mine ? (uint32_t)a.pb.slo_us[k] : 0u;
-    uint32_t T = nd > DSTACK_MAX_DNN_PER_SCEN ? 0u : __reduce_max_sync(FULL, act ? slo : 0u);
+    uint32_t T = __reduce_max_sync(FULL, act ? slo : 0u);   // 0 when nd > DSTACK_MAX_DNN_PER_SCEN (no lane active)
     if (T > 0) {
       const uint32_t nslots = T / (uint32_t)slot;
       const uint32_t njobs = __reduce_add_sync(FULL, act ? nslots / (slo / (uint32_t)slot) : 0u);
