@@ -243,6 +243,57 @@ def test_edge_cases_parity(ds):
     assert oracle.INVALID in want["scen_status"].tolist()
 
 
+def random_profile_problem(seed, S=260, S_tot=148):
+    """Adversarial random DNN profiles for the a1-a3 kernels (fast path, its exactness bands and the generic path):
+    1-400 rows of widths from 0 to far beyond S_tot, R up to 3 (and whole DNNs whose R sum reaches 2^16), memory
+    bytes from 0 to 2^31, t_np = 0 (ties, the certificate's blind spot) or small, t_p, M, SLO, a and MaxBatch across
+    their ranges; 1-6 DNNs per scenario."""
+    rng = np.random.default_rng(seed)
+    sizes = rng.integers(1, 7, S)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    D = int(off[-1])
+    K = rng.integers(1, 401, D)
+    K[rng.random(D) < 0.05] = 1
+    roff = np.concatenate([[0], np.cumsum(K)]).astype(np.int64)
+    R = int(roff[-1])
+    kind = rng.choice(4, R, p=[0.3, 0.4, 0.297, 0.003])
+    n = np.where(kind == 0, rng.integers(0, 16, R), np.where(kind == 1, rng.integers(1, S_tot + 1, R),
+                 np.where(kind == 2, rng.integers(S_tot, 4 * S_tot, R), rng.integers(1, 1 << 16, R)))).astype(np.uint32)
+    r = rng.integers(1, 4, R).astype(np.uint16)
+    dk = rng.random(R)
+    d = np.where(dk < 0.1, 0, np.where(dk < 0.8, rng.integers(0, 10 ** 6, R), np.where(
+        dk < 0.97, rng.integers(0, 10 ** 8, R), rng.integers(0, 1 << 31, R, dtype=np.int64)))).astype(np.uint32)
+    big = rng.random(D) < 0.03                        # R sums >= 2^16: outside the fast path
+    for k in np.flatnonzero(big):
+        r[roff[k]:roff[k + 1]] = min(65535, 65535 // max(1, int(K[k])) + 200)
+    t_p = rng.integers(1, 41, D).astype(np.int32)
+    t_np = np.where(rng.random(D) < 0.25, 0, rng.integers(1, 21, D)).astype(np.int32)
+    mbw = rng.integers(1000, 1 << 20, D).astype(np.int32)
+    slo = (rng.integers(20, 2001, D) * 100).astype(np.int32)
+    asm = rng.integers(0, 3000, D).astype(np.int32)
+    bmax = rng.integers(1, 65, D).astype(np.int32)
+    return synth.make_problem(off, roff, t_p, t_np, mbw, slo, asm, bmax, n, r, d)
+
+
+@pytest.mark.parametrize("mode", ["default", "mem_off", "verbatim", "per_launch", "b_min3", "threads", "ideal",
+                                  "L_eq_S"])
+def test_random_profiles_parity(ds, mode):
+    """Whole path (a1-a6 + a8, eval path) on adversarial random profiles vs the oracle: every integer output
+    bit-exact, f64 bit-identical."""
+    seeds = {"default": 1, "mem_off": 2, "verbatim": 3, "per_launch": 4, "b_min3": 5, "threads": 6, "ideal": 7,
+             "L_eq_S": 8}
+    pb = random_profile_problem(seeds[mode], S=120 if mode == "ideal" else 260)
+    p = Params(L=100, S_tot=148, ideal=0)
+    p = {"default": p, "mem_off": p.replace(mem_mode=0), "verbatim": p.replace(mem_mode=2),
+         "per_launch": p.replace(wse_mode=1), "b_min3": p.replace(b_min=3), "threads": p.replace(par_mode=1),
+         "ideal": p.replace(ideal=1), "L_eq_S": p.replace(L=148)}[mode]
+    g, _ = run_gpu(ds, pb, p)
+    want = oracle.evaluate(pb, p, nthreads=8)
+    assert_parity(g, want, ideal=(mode == "ideal"), where=mode)
+    st = want["status"]
+    assert (st == 0).sum() > 50   # most DNNs are schedulable, the rest exercise the statuses
+
+
 def test_ideal_parity_config2(ds):
     sp, p = synth.config(2, num_scen=40, rows_pct=20)
     pb = synth.generate_host(sp)
