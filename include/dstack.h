@@ -206,7 +206,8 @@ int dstack_aggregate(const dstack_problem_t *pb, const dstack_params_t *p, dstac
 
 /* a7: long-horizon simulation (config 5, readings in DESIGN.md §3).  Per scenario:
  * cycles sessions of T = max SLO over its servable DNNs; Poisson request arrivals per DNN with mean gap
- * f_L(l*, b*) * 100 / (lam_pct * b*) us drawn by the counter-based sampler of synth/synth_core.h keyed by
+ * f_L(l*, b*) * 100 / (lam_pct * b*) us (lam_pct <= 0: no requests, the gap takes its 2^30 us cap; reading R25)
+ * drawn by the counter-based sampler of synth/synth_core.h keyed by
  * (seed, cfg_tag, scen_base + s, dnn, k); each session: active = queued requests at its start, WMAX-MIN
  * over their demands, one D-STACK session with the fill ordered by the runs of the last 10 sessions, then
  * every run serves FIFO min(batch, queue at its start) requests (void if the queue is empty).

@@ -1250,8 +1250,10 @@ static void simulate_scenario(const or_problem_t *pb, const or_params_t *p, cons
     const int64_t ls = dem[j] - p->margin > 0 ? dem[j] - p->margin : 1;   /* l* (demand = l* + margin) */
     const int64_t S = S_of(p, ls);
     const u128 X = X_of(&m, p, S, bst8[j]);
-    const u128 den = (u128)S * (u128)m.M * (u128)lam_pct[k0 + j] * (u128)bst8[j];
-    u128 mq = ((X * 100) << 32) / den;
+    /* lam_pct <= 0: no offered load, the gap is infinite and takes the 2^30 us cap (R25) */
+    const int32_t lam = lam_pct[k0 + j];
+    const u128 den = lam > 0 ? (u128)S * (u128)m.M * (u128)lam * (u128)bst8[j] : 0;
+    u128 mq = den ? ((X * 100) << 32) / den : (u128)1 << 62;
     if (mq > ((u128)1 << 62)) mq = (u128)1 << 62;
     arr_init(arr + j, seed, cfg_tag, scen_base + s, (uint32_t)j, (uint64_t)mq);
     arr_init(head + j, seed, cfg_tag, scen_base + s, (uint32_t)j, (uint64_t)mq);

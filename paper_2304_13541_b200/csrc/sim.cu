@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(SIM_WARPS * 32, DSTACK_SIM_MINB) k_sim(SimArgs
         const uint64_t M = a.p.mem_mode == 0 ? 1ull : (uint64_t)a.pb.mem_bw[kj];
         const uint64_t X = x_from_rows(a.pb, a.p, kj, a.ws_RT[kj], a.ws_D[kj], S, bj, lane);
         if (lane == j) {
-          const u128 den = (u128)S * M * (u128)a.lam_pct[kj] * (u128)bj;
+          const int32_t lam = a.lam_pct[kj];                      // <= 0: no requests (R25)
+          const u128 den = lam > 0 ? (u128)S * M * (u128)lam * (u128)bj : (u128)0;
           u128 q = den ? ((((u128)X * 100u) << 32) / den) : ((u128)1 << 62);
           mq = q > ((u128)1 << 62) ? (1ull << 62) : (uint64_t)q;
         }

@@ -3,6 +3,8 @@
 Bar (BASELINE.json north_star): integer outputs bit-exact; f64 outputs within 1e-6 relative (they are
 ratios of exact integers evaluated in the same order, so equality is expected and also asserted).
 """
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -781,3 +783,58 @@ def test_max_throughput_caps(ds):
     assert np.array_equal(st.cpu().numpy(), want["status"])
     assert np.array_equal(served.cpu().numpy().astype(np.int64), want["served"])
     assert (want["status"] == oracle.INVALID).any() and (want["status"] == oracle.OK).any()
+
+
+@pytest.mark.parametrize("leg", ["compare", "cluster", "knee_probe", "below_knee", "max_throughput", "simulate"])
+def test_random_profiles_legs_parity(ds, leg):
+    """The §8 "next" rows (O9, F4, F3, F1, O9b) and a7 on the adversarial random profiles of
+    test_random_profiles_parity: every output bit-exact against the oracle."""
+    seed = {"compare": 11, "cluster": 12, "knee_probe": 13, "below_knee": 14, "max_throughput": 15,
+            "simulate": 16}[leg]
+    pb = random_profile_problem(seed, S=80 if leg == "max_throughput" else 200)
+    p = Params(L=100, S_tot=148, ideal=0)
+    dp = ds.from_host(pb, "cuda")
+    if leg == "knee_probe":
+        for pp in (p, p.replace(mem_mode=2), p.replace(wse_mode=1, L=148)):
+            for b in (1, 7, 64):
+                k, pr, st = ds.knee_probe(dp, pp, b)
+                ko, pro, sto = oracle.knee_probe(pb, pp, b)
+                assert np.array_equal(st.cpu().numpy(), sto), (b, pp)
+                assert np.array_equal(k.cpu().numpy().view(np.uint16), ko), (b, pp)
+                assert np.array_equal(pr.cpu().numpy(), pro), (b, pp)
+        return
+    if leg == "below_knee":
+        p = p.replace(below_knee=1)
+        g, _ = run_gpu(ds, pb, p)
+        assert_parity(g, oracle.evaluate(pb, p, nthreads=8), ideal=False, where="random below-knee")
+        return
+    if leg == "simulate":
+        lam = np.random.default_rng(seed).integers(0, 201, pb.num_dnn).astype(np.int32)   # 0-200 % offered load
+        pb = dataclasses.replace(pb, lam_pct=lam)
+        dp = ds.from_host(pb, "cuda")
+        g = ds.simulate(dp, p, 12, 99, 5, series=True)
+        torch.cuda.synchronize()
+        want = oracle.simulate(pb, p, 12, 99, 5, series=True)
+        for k in want:
+            a = g[k].cpu().numpy().astype(np.int64)
+            assert np.array_equal(a, want[k].astype(np.int64)), (k, np.flatnonzero(a != want[k].astype(np.int64))[:5])
+        return
+    o = ds.eval_batch(dp, p)
+    if leg == "compare":
+        c = ds.compare(dp, p, o["demand"], o["batch"], o["alloc_q16"])
+        torch.cuda.synchronize()
+        assert_compare_parity({k: v.cpu().numpy() for k, v in c.items()}, oracle.compare(pb, p, nthreads=8),
+                              where="random compare")
+    elif leg == "cluster":
+        for G in (1, 3, 8):
+            c = ds.cluster(dp, p, G, o["demand"], o["batch"])
+            torch.cuda.synchronize()
+            want = oracle.cluster(pb, p, G, nthreads=8)
+            for k in ("u", "thr"):
+                assert np.array_equal(c[k].cpu().numpy(), want[k]), (G, k)
+    else:
+        served, st = ds.max_throughput(dp, p, o["demand"], o["batch"], o["alloc_q16"])
+        torch.cuda.synchronize()
+        want = oracle.maxthr(pb, p, nthreads=8)
+        assert np.array_equal(st.cpu().numpy(), want["status"])
+        assert np.array_equal(served.cpu().numpy().astype(np.int64), want["served"])

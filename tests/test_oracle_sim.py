@@ -56,7 +56,8 @@ def reference_sim(pb, p, s, cycles, seed, cfg_tag):
         S = -(-ls * p.S_tot // p.L)
         X = oracle.X(one, p, j, ls, int(bo["batch"][j]))
         M = int(one.mem_bw[j]) if p.mem_mode else 1
-        mq = ((X * 100) << 32) // (S * M * int(one.lam_pct[j]) * int(bo["batch"][j]))
+        lam = int(one.lam_pct[j])            # R25: no offered load -> infinite gap, capped below
+        mq = ((X * 100) << 32) // (S * M * lam * int(bo["batch"][j])) if lam > 0 else 1 << 62
         streams[j] = Stream(j, min(mq, 1 << 62))
     served = [0] * nd
     ring = np.zeros((10, nd), np.int64)
@@ -136,6 +137,28 @@ def test_sim_matches_independent_reimplementation():
         series += want["series"]
     # the per-cycle aggregate series (dstack.h DSTACK_SIM_*), summed over the scenarios
     assert np.array_equal(o["series"].astype(np.int64), series)
+
+
+def test_sim_zero_load():
+    """R25: lam_pct <= 0 offers no requests. All-zero load: nothing arrives, runs or occupies a slot (every
+    session is empty); a mix of zero and positive loads matches the independent re-implementation."""
+    sp, p, pb = small_sim_problem(num_scen=6, rows_pct=10, lam=0)
+    o = oracle.simulate(pb, p, 10, sp.seed, sp.cfg_tag, series=True)
+    ok = o["status"] == oracle.OK
+    assert ok.any()
+    for k in ("arrived", "in_slo", "late", "unserved", "occ_sum", "runs", "realloc"):
+        assert (o[k] == 0).all(), k
+    pb.lam_pct[::2] = 0
+    pb.lam_pct[1::2] = 90
+    pb.lam_pct[3::4] = -5
+    o = oracle.simulate(pb, p, 10, sp.seed, sp.cfg_tag)
+    for s in range(pb.num_scen):
+        want = reference_sim(pb, p, s, 10, sp.seed, sp.cfg_tag)
+        if want is None:
+            continue
+        for k in ("arrived", "in_slo", "late", "unserved", "occ_sum", "runs", "misses", "realloc"):
+            assert int(o[k][s]) == want[k], (s, k)
+    assert o["arrived"].sum() > 0
 
 
 def test_sim_conservation_and_determinism():
