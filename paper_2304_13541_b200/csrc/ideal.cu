@@ -114,35 +114,53 @@ constexpr int IDEAL_WARPS = 8;
 #define DSTACK_IDEAL_SMALL_MITM 1   // 9-10 live items: 5 + 5 meet in the middle, one subset per lane (else enumeration)
 #endif
 #ifndef DSTACK_IDEAL_SHORTCUTS
-#define DSTACK_IDEAL_SHORTCUTS 1   // reuse the selection when no (rank, g) changed; all-fit shortcut (A/B switch)
+#define DSTACK_IDEAL_SHORTCUTS 1   // all-fit shortcut: sum g <= L selects every live item (A/B switch)
 #endif
 
-struct IdealRow {
-  int64_t i;      // absolute row index (r1 = end of chain)
-  uint32_t R, tau, g;
-};
-
-// row i as stored (no skipping): the prefetch of a chain's next row, whose loads are only consumed at the next
-// advance, so their latency overlaps the events in between
-__device__ __forceinline__ IdealRow ideal_row_raw(const IdealArgs &a, int64_t i, int64_t r1) {
-  IdealRow w;
-  w.i = i;
-  w.R = 0; w.tau = 0; w.g = 0;
-  if (i < r1) {
-    const uint64_t v = a.ex_pk[i];
-    w.R = (uint32_t)(v >> 48); w.tau = (uint32_t)v; w.g = (uint32_t)(v >> 32) & 0xFFFFu;
+// Execution runs (k_ideal_runs): the subset selection sees a chain only through its current item's demand g, so
+// consecutive executions of equal g (the R repeats of a kernel, and successive kernels of the same knee) form one
+// item whose duration is their sum; zero-duration rows complete instantly and are skipped.  Each run's record
+// (at its first non-zero row; the chain's first run at the chain's first row) is tau | g << 32 | next << 48, next =
+// rows to the following run's record (r1 - i: none); an all-zero chain has tau = 0 at its first row.  Merging
+// removes exactly the events at which no item's (rank, g) changes: the selection, its sum and every item's
+// progress are the same on both sides of such an event, so the schedule and util are unchanged.
+__global__ void __launch_bounds__(256) k_ideal_runs(IdealArgs a) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.pb.num_dnn;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    if (a.demand[k] == 0) continue;
+    const int64_t r0 = a.pb.dnn_row_off[k], r1 = a.pb.dnn_row_off[k + 1];
+    auto put = [&](int64_t i, uint64_t tau, uint32_t g, int64_t nx) {
+      a.ex_pk[i] = (tau > 0xFFFFFFFFull ? 0xFFFFFFFFull : tau) | ((uint64_t)g << 32) | ((uint64_t)(nx - i) << 48);
+    };
+    int64_t nx = r1, first_nz = -1;   // the run being built backwards starts at first_nz; the following one at nx
+    uint64_t acc = 0;
+    uint32_t gcur = 0;
+    for (int64_t i = r1 - 1; i >= r0; --i) {
+      const uint64_t v = a.ex_pk[i];
+      const uint64_t tz = (v & 0xFFFFFFFFull) * (v >> 48);   // tau x R (< 2^48)
+      if (tz == 0) continue;
+      const uint32_t g = (uint32_t)(v >> 32) & 0xFFFFu;
+      if (first_nz >= 0 && g != gcur) { put(first_nz, acc, gcur, nx); nx = first_nz; acc = 0; }
+      gcur = g; acc += tz; first_nz = i;
+    }
+    put(r0, acc, gcur, nx);   // the first run (or tau = 0: the chain never runs)
   }
-  return w;
 }
 
-__device__ __forceinline__ IdealRow ideal_row_at(const IdealArgs &a, int64_t i, int64_t r1) {
+struct IdealRow {
+  int64_t i;      // row of the run's record (r1 = end of chain)
+  uint32_t tau, g, nx;
+};
+
+// the run record at row i (tau = 0 past the chain's end): the prefetch of a chain's next run, whose load is only
+// consumed at the next advance, so its latency overlaps the events in between
+__device__ __forceinline__ IdealRow ideal_run_at(const IdealArgs &a, int64_t i, int64_t r1) {
   IdealRow w;
-  while (i < r1 && (uint32_t)a.ex_pk[i] == 0u) ++i;    // zero-duration rows complete instantly
   w.i = i;
-  w.R = 0; w.tau = 0; w.g = 0;
+  w.tau = 0; w.g = 0; w.nx = 0;
   if (i < r1) {
     const uint64_t v = a.ex_pk[i];
-    w.R = (uint32_t)(v >> 48); w.tau = (uint32_t)v; w.g = (uint32_t)(v >> 32) & 0xFFFFu;
+    w.tau = (uint32_t)v; w.g = (uint32_t)(v >> 32) & 0xFFFFu; w.nx = (uint32_t)(v >> 48);
   }
   return w;
 }
@@ -190,20 +208,19 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, MINB) k_ideal_sim(IdealArgs 
     if (T > 0) {
       int64_t r0 = 0, r1 = 0;
       IdealRow first, cur, nxt;
-      first.i = cur.i = nxt.i = 0; first.R = cur.R = nxt.R = 0; first.tau = cur.tau = nxt.tau = 0;
+      first.i = cur.i = nxt.i = 0; first.nx = cur.nx = nxt.nx = 0; first.tau = cur.tau = nxt.tau = 0;
       first.g = cur.g = nxt.g = 0;
       bool live = false;
       if (act) {
         r0 = a.pb.dnn_row_off[k]; r1 = a.pb.dnn_row_off[k + 1];
-        first = ideal_row_at(a, r0, r1);
-        live = first.i < r1;                  // an all-zero chain never runs
+        first = ideal_run_at(a, r0, r1);
+        live = first.tau > 0;                 // an all-zero chain never runs
         cur = first;
-        if (live) nxt = ideal_row_raw(a, cur.i + 1, r1);
+        if (live) nxt = ideal_run_at(a, cur.i + cur.nx, r1);
       }
-      uint32_t rp = 0, rem = cur.tau, dl = slo, comp = 0, rank = 0;
+      uint32_t rem = cur.tau, dl = slo, comp = 0, rank = 0;
       const uint32_t n = (uint32_t)__popc(__ballot_sync(FULL, live));
       bool dirty = true;
-      bool resel = true;   // the selection must be recomputed (first event, a rank or a live item's g changed)
       bool sel = false;
       uint32_t gsum = 0;
       uint64_t util = 0;
@@ -221,16 +238,12 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, MINB) k_ideal_sim(IdealArgs 
           }
           dirty = false;
         }
-        // The max-sum subset depends only on the live items' (rank, g): when no rank and no g changed since the
-        // last event (a repeated execution R_i > 1, or a next kernel of the same demand), the previous selection
-        // is still the lexicographically-first optimum.  When every live item fits (sum g <= L) the unique
-        // optimum is all of them (g >= 1).
-        uint32_t gtot = 0xFFFFFFFFu;
-        if (DSTACK_IDEAL_SHORTCUTS && resel) gtot = __reduce_add_sync(FULL, live ? cur.g : 0u);
-        if (resel) ++st_rs;
-        if (DSTACK_IDEAL_SHORTCUTS && !resel) {
-          // keep sel, gsum
-        } else if (DSTACK_IDEAL_SHORTCUTS && gtot <= (uint32_t)L) {
+        // Every event changes some live item's g (consecutive runs of a chain differ in g) or a rank, so the
+        // selection is recomputed.  When every live item fits (sum g <= L) the unique optimum is all of them
+        // (g >= 1).
+        const uint32_t gtot = __reduce_add_sync(FULL, live ? cur.g : 0u);
+        ++st_rs;
+        if (DSTACK_IDEAL_SHORTCUTS && gtot <= (uint32_t)L) {
           ++st_fit;
           sel = live;
           gsum = gtot;
@@ -441,28 +454,22 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, MINB) k_ideal_sim(IdealArgs 
         util += (uint64_t)gsum * dt;
         t += dt;
         bool done_batch = false;
-        const uint32_t g_before = cur.g;
         if (sel) {
           rem -= dt;
-          if (rem == 0) {   // next execution of the chain
-            if (++rp >= cur.R) {
-              rp = 0;
-              while (nxt.i < r1 && nxt.tau == 0) nxt = ideal_row_raw(a, nxt.i + 1, r1);   // zero-duration rows (rare)
-              if (nxt.i >= r1) {              // batch complete: next batch back-to-back
-                comp++;
-                dl = (uint32_t)t + slo;
-                done_batch = true;
-                cur = first;
-              } else {
-                cur = nxt;
-              }
-              nxt = ideal_row_raw(a, cur.i + 1, r1);
+          if (rem == 0) {   // next run of the chain
+            if (nxt.i >= r1) {              // batch complete: next batch back-to-back
+              comp++;
+              dl = (uint32_t)t + slo;
+              done_batch = true;
+              cur = first;
+            } else {
+              cur = nxt;
             }
+            nxt = ideal_run_at(a, cur.i + cur.nx, r1);
             rem = cur.tau;
           }
         }
         dirty = __any_sync(FULL, done_batch);
-        resel = dirty || __any_sync(FULL, cur.g != g_before);
         __syncwarp();
       }
       if (a.stats && lane == 0) {
@@ -550,7 +557,10 @@ int launch_ideal(IdealArgs a, void *ws, cudaStream_t s, int *launches) {
     int64_t blocks = ((int64_t)a.pb.num_dnn * 32 + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     k_ideal_rows<<<(unsigned)blocks, 256, 0, s>>>(a);
-    ++*launches;
+    int64_t rb = (a.pb.num_dnn + 255) / 256;
+    if (rb > (int64_t)num_sms() * 8) rb = (int64_t)num_sms() * 8;
+    k_ideal_runs<<<(unsigned)rb, 256, 0, s>>>(a);
+    *launches += 2;
   }
   int64_t blocks = (a.pb.num_scen + IDEAL_WARPS - 1) / IDEAL_WARPS;
   if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
