@@ -176,7 +176,7 @@ __device__ __forceinline__ IdealRow ideal_run_at(const IdealArgs &a, int64_t i, 
 template <int MINB>
 __global__ void __launch_bounds__(IDEAL_WARPS * 32, MINB) k_ideal_sim(IdealArgs a) {
   __shared__ uint8_t reach_all[IDEAL_WARPS][DSTACK_MAX_DNN_PER_SCEN + 1][32];
-  __shared__ uint8_t grank_all[IDEAL_WARPS][32];   // g of the live item of each priority rank
+  __shared__ __align__(16) uint8_t grank_all[IDEAL_WARPS][32];   // g of the live item of each priority rank
   __shared__ uint32_t mbb_all[IDEAL_WARPS][8];     // meet in the middle: achievable B sums (256-bit set)
   __shared__ int32_t mbl_all[IDEAL_WARPS][8];      // ... highest achievable B sum below each word
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -314,25 +314,33 @@ __global__ void __launch_bounds__(IDEAL_WARPS * 32, MINB) k_ideal_sim(IdealArgs 
           // the item of rank n-1-p, so the largest index among the max-sum subsets is the lexicographically-
           // first (priority order) optimal subset -- the one the read-back below selects -- and one
           // max-reduction over (sum, index) decides.
-          if (live) grank[rank] = (uint8_t)cur.g;
+          // grank reversed here: gp[p] = grank[p] (subset bit p <-> rank n-1-p); entries >= n are stale, but only
+          // subsets of the first 2^n indices are ever kept
+          if (live) grank[n - 1 - rank] = (uint8_t)cur.g;
           __syncwarp();
           constexpr int NE = DSTACK_IDEAL_ENUM_MAX > 8 ? DSTACK_IDEAL_ENUM_MAX : 8;   // items enumerable
+          const uint32_t *gw = reinterpret_cast<const uint32_t *>(grank);
           uint32_t gp[NE];
 #pragma unroll
-          for (int p = 0; p < NE; ++p) gp[p] = p < (int)n ? grank[n - 1 - p] : 0u;
+          for (int p = 0; p < NE; ++p) gp[p] = (gw[p >> 2] >> (8 * (p & 3))) & 0xFFu;
+          // key = (sum << NE) | index, built as (subset sum of bits 3..7 << NE | lane << 3) + (the low 3 bits' sum
+          // << NE | lo): the fields never carry into each other, and sum <= L <=> key <= lim
           uint32_t lbase = 0;
 #pragma unroll
           for (int p = 3; p < 8; ++p)
             if ((lane >> (p - 3)) & 1) lbase += gp[p];
-          uint32_t best = 0;
+          const uint32_t k1 = (gp[0] << NE) | 1u, k2 = (gp[1] << NE) | 2u, k4 = (gp[2] << NE) | 4u;
+          const uint32_t kB[8] = {0u, k1, k2, k1 + k2, k4, k1 + k4, k2 + k4, k1 + k2 + k4};
+          const uint32_t lim = (((uint32_t)L + 1u) << NE) - 1u;
           const uint32_t nsub = 1u << n;
+          uint32_t best = 0;
           auto scan8 = [&](uint32_t base, uint32_t r) {
+            const uint32_t kb = (base << NE) | (r << 8) | ((uint32_t)lane << 3);
+            const uint32_t lm = (r << 8) + ((uint32_t)lane << 3) < nsub ? lim : 0u;   // this lane's indices exist
 #pragma unroll
             for (int lo = 0; lo < 8; ++lo) {
-              const uint32_t idx = (r << 8) | ((uint32_t)lane << 3) | (uint32_t)lo;
-              const uint32_t sum = base + ((lo & 1) ? gp[0] : 0u) + ((lo & 2) ? gp[1] : 0u) + ((lo & 4) ? gp[2] : 0u);
-              const uint32_t key = (sum << NE) | idx;
-              if (idx < nsub && sum <= (uint32_t)L && key > best) best = key;
+              const uint32_t key = kb + kB[lo];
+              if (key <= lm) best = max(best, key);
             }
           };
           if (n <= 8) {
