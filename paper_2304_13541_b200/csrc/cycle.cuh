@@ -57,7 +57,7 @@ struct CycSmem {
 
 // bytes of a lane's 4-slot word (first slot `base`) below slot x
 __device__ __forceinline__ uint32_t bytes_below(int x, int base) {
-  const int hb = min(max(x - base, 0), 4);
+  const int hb = min(x - base, 4);   // hb <= 0: shift >= 32, which the funnel shift clamps to 32 (no bytes)
   return __funnelshift_rc(0xFFFFFFFFu, 0u, (uint32_t)(32 - 8 * hb));
 }
 
@@ -127,11 +127,11 @@ __device__ __forceinline__ int find_early_packed(const uint8_t *occ, int rel, in
   while (s + d <= dl) {
     const int bt = s & ~3, wi = (bt >> 2) + lane, mybase = bt + 4 * lane;
     const uint32_t word = w32[wi];   // padded array
-    uint32_t bb = __vcmpgtu4(word, th) & bytes_below(s + d, mybase);   // blocking slots in the run
-    if (lane == 0) bb &= 0xFFFFFFFFu << (8 * (s & 3));
+    // blocking slots of [s & ~3, s + d): the last one + 1 is <= s iff none lies in the run [s, s + d)
+    const uint32_t bb = __vcmpgtu4(word, th) & bytes_below(s + d, mybase);
     const uint32_t lb = bb ? (uint32_t)(mybase + ((31 - __clz(bb)) >> 3) + 1) : 0u;
     const uint32_t last = __reduce_max_sync(FULL, lb);   // (last blocking slot) + 1, or 0
-    if (last == 0) return s;
+    if ((int)last <= s) return s;
     s = (int)last;
   }
   return -1;
