@@ -370,11 +370,10 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     const uint32_t lo_mask = lane == 0 ? (0xFFFFFFFFu << (8 * (t & 3))) : 0xFFFFFFFFu;
     uint32_t wvm = wv & lo_mask;   // the window's slots >= t
     int occ_t = (int)sm.occ[t];    // broadcast byte load
-    bool elig = false;
-    if (active) {   // eligible: not running at t (static or fill run), fits at t
-      while (t >= ns) { free_at = max(free_at, ne); next_static(); }
-      elig = t >= free_at && t >= blk && occ_t + (int)g <= L;
-    }
+    // static runs begun by t folded into free_at (inactive lanes: ns = nslots > t, no iteration)
+    while (t >= ns) { free_at = max(free_at, ne); next_static(); }
+    // eligible: not running at t (static or fill run), not blocked, fits at t
+    const bool elig = active && t >= max(free_at, blk) && occ_t + (int)g <= L;
     // candidates in (runs so far, index) order; a placement raises occ[t], so re-test the rest in parallel
     const uint32_t prio = fill_order == 0 ? count : (fill_order == 1 ? g : dstar);
     uint32_t key = elig ? ((prio << 5) | (uint32_t)lane) : 0xFFFFFFFFu;
