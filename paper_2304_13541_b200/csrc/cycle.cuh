@@ -131,6 +131,7 @@ __device__ __forceinline__ int find_early_packed(const uint8_t *occ, int rel, in
     const uint32_t bb = __vcmpgtu4(word, th) & bytes_below(s + d, mybase);
     const uint32_t lb = bb ? (uint32_t)(mybase + ((31 - __clz(bb)) >> 3) + 1) : 0u;
     const uint32_t last = __reduce_max_sync(FULL, lb);   // (last blocking slot) + 1, or 0
+    if (lane == 0) CSTAT(9, 1);
     if ((int)last <= s) return s;
     s = (int)last;
   }
@@ -148,6 +149,7 @@ __device__ __forceinline__ int find_late_packed(const uint8_t *occ, int rel, int
     if (lane == 0) bb &= 0xFFFFFFFFu << (8 * (s & 3));
     const uint32_t fb = bb ? (uint32_t)(mybase + ((__ffs(bb) - 1) >> 3)) : 0xFFFFFFFFu;
     const uint32_t first = __reduce_min_sync(FULL, fb);   // first blocking slot, or none
+    if (lane == 0) CSTAT(10, 1);
     if (first == 0xFFFFFFFFu) return s;
     s = (int)first - d;
   }
@@ -377,11 +379,18 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     // candidates in (runs so far, index) order; a placement raises occ[t], so re-test the rest in parallel
     const uint32_t prio = fill_order == 0 ? count : (fill_order == 1 ? g : dstar);
     uint32_t key = elig ? ((prio << 5) | (uint32_t)lane) : 0xFFFFFFFFu;
+#if DSTACK_PROF_STATS
+    bool st_first = true;
+#endif
     while (true) {
       const uint32_t mk = __reduce_min_sync(FULL, key);
       if (mk == 0xFFFFFFFFu) break;
       const int j = (int)(mk & 31u);
       if (lane == 0) CSTAT(4, 1);
+#if DSTACK_PROF_STATS
+      if (lane == 0 && st_first) CSTAT(8, 1);   // decision times with at least one candidate
+      st_first = false;
+#endif
       if (lane == j) key = 0xFFFFFFFFu;
       const uint32_t pj = __shfl_sync(FULL, pk, j);
       const int gj = (int)(pj & 0xFFu), bsj = (int)((pj >> 8) & 0xFFu), dsj = (int)(pj >> 16);

@@ -623,10 +623,12 @@ __device__ __forceinline__ void lane_scan_f(const uint32_t *H, const uint16_t *l
         const float x = fmaf(af, sx, bf);
         G = fmaxf(G, bf == 0.f ? __int_as_float(0x7f800000) : sx * rcp_approx(x * x));
       }
-      if (S == 0 || S > (uint32_t)S_tot || !(all_valid || lmin[S])) continue;
+      // widths that are no level's S(l) (and S = 0, S_tot + 1) score 0: a no-op for the tracker (f > t strict,
+      // t1 >= t2 >= t3 >= 0), so the loop body has no data-dependent branch
+      const bool cand = S != 0 && S <= (uint32_t)S_tot && (all_valid || lmin[S] != 0);
       float xf = fmaf(Sf, C1f, fmaf(Mtpf, fmaf(Sf, raf, qf), basef));
       if (SCAN_MEM == 2) xf = fmaf(Df, Sf * Sf, xf);
-      const float f = Sf * rcp_approx(xf * xf);
+      const float f = cand ? Sf * rcp_approx(xf * xf) : 0.f;
       // top-3 of the scores (strict: the first width keeps a float tie), payloads of the top 2; branch-free
       // (lanes hold different DNNs, so a branch on f > t1 diverges)
       const uint32_t m1 = 0u - (uint32_t)(f > t1), m2 = 0u - (uint32_t)(f > t2);
@@ -792,18 +794,25 @@ __global__ void __launch_bounds__(DSTACK_PLANE_WARPS * 32, DSTACK_PLANE_MINB) k_
         else if (mem_mode == 2) xe += bd * (double)myD * Sd * Sd;
         if (xe >= 72057594037927936.0 * 0.9999) cold = true;
       }
+    }
+    // The f32 width scan runs on every lane, outside any lane-dependent branch: its branches on the width are then
+    // provably warp-uniform (no reconvergence regions in the loop).  Lanes without a fast-path DNN scan their
+    // (zero or partial) histogram row with their own parameters and drop the result.
+    const uint64_t C1 = (uint64_t)t_np * M * myRT;
+    const uint64_t memb = mem_mode == 1 ? myD : 0ull;
+    const uint64_t base = Mtp * myWb + memb;
+    const float C1f2 = 2.f * (float)C1, Mtpf = (float)Mtp, Wbf = (float)myWb, membf = (float)memb;
+    const uint32_t *H = Htab + lane * HS;
+    uint32_t Sk = 0, ra1 = 0, q1 = 0, s2 = 0;
+    float t1 = 0.f, t2 = 0.f, t3 = 0.f, G = 0.f;
+    {
+      const float C1f = (float)C1, basef = (float)base, Df = (float)myD;
+      if (mem_mode == 2) lane_scan_f<2>(H, lmin, S_tot, mh, all_valid, C1f, Mtpf, basef, Df, myWsm, C1f2, Wbf, membf, half, t1, t2, t3, Sk, ra1, q1, s2, G);
+      else lane_scan_f<0>(H, lmin, S_tot, mh, all_valid, C1f, Mtpf, basef, Df, myWsm, C1f2, Wbf, membf, half, t1, t2, t3, Sk, ra1, q1, s2, G);
+    }
+    if (have && ok) {
       if (st == DSTACK_ST_OK && !cold) {
-        const uint64_t C1 = (uint64_t)t_np * M * myRT;
-        const uint64_t memb = mem_mode == 1 ? myD : 0ull;
-        const uint64_t base = Mtp * myWb + memb;
-        const float C1f2 = 2.f * (float)C1, Mtpf = (float)Mtp, Wbf = (float)myWb, membf = (float)memb;
-        const uint32_t *H = Htab + lane * HS;
-        uint32_t Sk = 0, ra1 = 0, q1 = 0, s2 = 0;
         uint64_t Xk = 0;
-        float t1 = 0.f, t2 = 0.f, t3 = 0.f, G = 0.f;
-        const float C1f = (float)C1, basef = (float)base, Df = (float)myD;
-        if (mem_mode == 2) lane_scan_f<2>(H, lmin, S_tot, mh, all_valid, C1f, Mtpf, basef, Df, myWsm, C1f2, Wbf, membf, half, t1, t2, t3, Sk, ra1, q1, s2, G);
-        else lane_scan_f<0>(H, lmin, S_tot, mh, all_valid, C1f, Mtpf, basef, Df, myWsm, C1f2, Wbf, membf, half, t1, t2, t3, Sk, ra1, q1, s2, G);
         const float band = t1 * 0.99999237f;   // 1 - 2^-17 (twice the worst f32 misordering)
         auto x_at = [&](uint32_t S, uint32_t ra, uint32_t q) {
           uint64_t X = (uint64_t)S * C1 + Mtp * ((uint64_t)S * ra + q) + base;

@@ -28,7 +28,7 @@ for i, nm in enumerate(names):
 lib.dstack_debug_stats_cycle(cbuf, 1)
 c = list(cbuf)
 cn = ["sessions", "static_jobs", "static_scan_chunks", "decision_times", "fill_candidates", "fill_placed",
-      "fill_smaller_b", "fill_slice_short"]
+      "fill_smaller_b", "fill_slice_short", "dec_with_cand", "early_tries", "late_tries"]
 ns = max(c[0], 1)
 for i, nm in enumerate(cn):
     print(f"{nm:18s} {c[i]:14d}  per session {c[i]/ns:8.3f}")
