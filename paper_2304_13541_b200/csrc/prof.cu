@@ -523,7 +523,20 @@ __global__ void __launch_bounds__(256, DSTACK_PROF_MINB) k_prof_fast(const __gri
 #define DSTACK_PLANE_WARPS 8   // warps per block
 #endif
 
-__host__ __device__ inline int plane_hstride(int S_tot) { return ((S_tot + 2) >> 1) | 1; }   // odd word stride
+#ifndef DSTACK_PLANE_SEARCH
+#define DSTACK_PLANE_SEARCH 1   // 1: a2/a3 by exact searches over the unimodal b = 1 curve (0: the f32 width scan; A/B)
+#endif
+__host__ __device__ inline int plane_nw(int S_tot) { return (S_tot + 2) >> 1; }         // bin words (bins 0..S_tot)
+__host__ __device__ inline int plane_nck(int S_tot) { return ((plane_nw(S_tot) - 1) >> 2) + 1; }   // PPA checkpoints
+__host__ __device__ inline int plane_hstride(int S_tot) {   // odd word stride
+#if DSTACK_PLANE_SEARCH
+  // a lane's row: the bins (then PA, in place), the PPA checkpoints, and room for a 4-word read at any checkpoint
+  const int a = plane_nw(S_tot) + plane_nck(S_tot), b = 4 * plane_nck(S_tot);
+  return (a > b ? a : b) | 1;
+#else
+  return plane_nw(S_tot) | 1;
+#endif
+}
 __host__ __device__ inline size_t plane_warp_bytes(int S_tot) {
   // the H table; the cold path's scratch (cA, cU, hist) reuses it once the group's lane scans are done
   const size_t h = (size_t)32 * plane_hstride(S_tot) * 4, c = prof_warp_bytes(S_tot);
@@ -585,6 +598,86 @@ __device__ __forceinline__ uint64_t lane_X_at(const uint32_t *H, uint32_t Sg, ui
   uint64_t X = (uint64_t)Sg * C1 + Mtp * ((uint64_t)Sg * ra + (Wsm - rw)) + base;
   if (mem_mode == 2) X += D * (uint64_t)(Sg * Sg);
   return X;
+}
+
+// ---- a2/a3 by search (DSTACK_PLANE_SEARCH) -------------------------------------------------------------------
+// O1 at b = 1 over the rows with n_i <= S_tot:  S PA[S] + Q[S] = sum_i R_i max(n_i, S) = Wsm + PPA(S), with
+// PA[S] = sum_{1 <= n_i <= S} R_i and PPA(S) = sum_{k < S} PA[k] (summation by parts: PW[S] = S PA[S] - PPA(S)), so
+//   X(S, 1) = S C1 + Mtp (Wsm + PPA(S)) + base  (+ D S^2 verbatim).
+// sum_i R_i max(n_i, s) is convex in s, so X is convex and positive and S / X^2 is unimodal in S: d/ds log(s / X^2)
+// has the sign of X - 2 s X', and (2 s X' - X)' = X' + 2 s X'' >= 0.  Both argmaxes are then binary searches:
+//  * the knee (Eq. 6 at b = 1, ties -> smaller S) over the attained widths: compare adjacent candidates, keep the
+//    left one on >=.  Strictly increasing before the real peak, so the first i with f(i) >= f(i + 1) is the
+//    leftmost maximum (at most two maxima, adjacent);
+//  * the b >= 2 certificate G: on segment m, s / (alpha_m s + beta_m)^2 rises while beta_m > alpha_m s,
+//    and K(s) = alpha(s) s - beta(s) is nondecreasing (it jumps by 2 Mtp h(m+1) (m+1) >= 0 at each breakpoint), so
+//    the supremum over (0, S_tot / 2] lies in the first segment m with alpha_m (m + 1) >= beta_m (exact u64), else
+//    in the last; the closed form is evaluated there (the maximum over all segments of the scan version).
+// The lane's histogram row becomes PA in place (u16, exact: RT < 2^16 on the fast path) with PPA checkpoints every
+// 8 widths after the bins; PPA(S) = checkpoint + at most 7 PA terms.
+
+// Row conversion: bins -> PA (bin 0, n = 0 rows, is in no prefix sum), PPA(8c) -> CK[c].  Returns PA[S_tot + 1].
+__device__ __forceinline__ uint32_t lane_prefix(uint32_t *H, int nw, int nck) {
+  uint32_t *CK = H + nw;
+  uint32_t pa = 0, ppa = 0;
+  for (int c = 0; c < nck; ++c) {   // warp-uniform bounds
+    CK[c] = ppa;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int w = 4 * c + q;
+      if (w < nw) {
+        const uint32_t hw = H[w];
+        const uint32_t p0 = pa + (w == 0 ? 0u : (hw & 0xFFFFu)), p1 = p0 + (hw >> 16);
+        H[w] = (p0 & 0xFFFFu) | (p1 << 16);
+        ppa += p0 + p1;
+        pa = p1;
+      }
+    }
+  }
+  return pa;
+}
+
+// PPA(S) and PA[S] from the converted row (S <= S_tot)
+__device__ __forceinline__ uint32_t lane_ppa(const uint32_t *H, int nw, uint32_t S, uint32_t &paS) {
+  const uint32_t c = S >> 3, jj = (S & 7u) >> 1;
+  const uint32_t *wp = H + 4 * c;
+  uint32_t s = H[nw + c];
+#pragma unroll
+  for (uint32_t q = 0; q < 3; ++q) {   // whole words below S's word
+    const uint32_t w = wp[q];
+    s += q < jj ? (w & 0xFFFFu) + (w >> 16) : 0u;
+  }
+  const uint32_t wj = wp[jj];
+  if (S & 1u) { s += wj & 0xFFFFu; paS = wj >> 16; }
+  else paS = wj & 0xFFFFu;
+  return s;
+}
+
+// f(a) >= f(b) for f = S / X^2: S_a X_b^2 >= S_b X_a^2, an f32 filter (each side within 2^-22) and u128 when close
+__device__ __forceinline__ bool score_ge(uint32_t Sa, uint64_t Xa, uint32_t Sb, uint64_t Xb) {
+  const float xa = (float)Xa, xb = (float)Xb;
+  const float pa = (float)Sa * (xb * xb), pb = (float)Sb * (xa * xa);
+  if (pa > pb * 1.00000095f) return true;    // 1 + 2^-20
+  if (pa < pb * 0.99999905f) return false;   // 1 - 2^-20
+  return (u128)Sa * ((u128)Xb * Xb) >= (u128)Sb * ((u128)Xa * Xa);
+}
+
+// Exact scan of the feasible widths (2X <= S F) from the converted row: the knee was infeasible (rare)
+template <int SCAN_MEM>
+static __device__ __noinline__ void lane_scan_pa(const uint32_t *H, const uint16_t *lmin, int S_tot, uint64_t C1,
+                                                 uint64_t Mtp, uint64_t base, uint64_t D, uint32_t Wsm, uint64_t F,
+                                                 uint32_t &Sb, uint64_t &Xb) {
+  uint32_t ppa = 0;   // PPA(S) at the top of iteration S (PPA(1) = PA[0] = 0)
+  float fb = 0.f;
+  for (int S = 1; S <= S_tot; ++S) {
+    const uint32_t hw = H[S >> 1];
+    const uint32_t pa = (S & 1) ? (hw >> 16) : (hw & 0xFFFFu);
+    uint64_t X = (uint64_t)S * C1 + Mtp * ((uint64_t)Wsm + ppa) + base;
+    if (SCAN_MEM == 2) X += D * (uint64_t)(S * S);
+    ppa += pa;
+    if (!lmin[S] || 2 * X > (uint64_t)S * F) continue;
+    lane_best((uint32_t)S, X, score_f((uint32_t)S, X), Sb, Xb, fb);
+  }
 }
 
 // One f32 pass over the widths: per attained width S the score S / X(S, 1)^2 from an f32 evaluation of X
@@ -795,6 +888,95 @@ __global__ void __launch_bounds__(DSTACK_PLANE_WARPS * 32, DSTACK_PLANE_MINB) k_
         if (xe >= 72057594037927936.0 * 0.9999) cold = true;
       }
     }
+#if DSTACK_PLANE_SEARCH
+    // a2/a3 by search on every lane (uniform trip counts; lanes without a fast-path DNN search their own zero or
+    // partial row and drop the result)
+    const uint64_t C1 = (uint64_t)t_np * M * myRT;
+    const uint64_t memb = mem_mode == 1 ? myD : 0ull;
+    const uint64_t base = Mtp * myWb + memb;
+    const float C1f2 = 2.f * (float)C1, Mtpf = (float)Mtp, Wbf = (float)myWb, membf = (float)memb;
+    const int nw = plane_nw(S_tot);
+    lane_prefix(Htab + lane * HS, nw, plane_nck(S_tot));
+    const uint32_t *H = Htab + lane * HS;
+    auto x_of = [&](uint32_t S, uint32_t ppa) {   // X(S, 1) from PPA(S)
+      uint64_t X = (uint64_t)S * C1 + Mtp * ((uint64_t)myWsm + ppa) + base;
+      if (mem_mode == 2) X += myD * (uint64_t)(S * S);
+      return X;
+    };
+    // knee: the leftmost maximum of S / X^2 over the candidates i = 1..N (widths i when every width is some level's
+    // S(l), i.e. L >= S_tot; else S(i) = Stab[i], strictly increasing)
+    const bool dense = L >= S_tot;
+    const int N = dense ? S_tot : L;
+    int ilo = 1, ihi = N;
+    const int ksteps = N > 1 ? 32 - __clz(N - 1) : 0;
+    for (int it = 0; it < ksteps; ++it) {
+      const int mid = (ilo + ihi) >> 1;
+      const uint32_t Sa = dense ? (uint32_t)mid : Stab[mid];
+      uint32_t paA, ppaB;
+      const uint32_t ppaA = lane_ppa(H, nw, Sa, paA);
+      uint32_t Sb2;
+      if (dense) { Sb2 = Sa + 1; ppaB = ppaA + paA; }
+      else { Sb2 = Stab[mid + 1 <= N ? mid + 1 : N]; uint32_t t; ppaB = lane_ppa(H, nw, Sb2, t); }
+      const bool left = score_ge(Sa, x_of(Sa, ppaA), Sb2, x_of(Sb2, ppaB));
+      if (ilo < ihi) { if (left) ihi = mid; else ilo = mid + 1; }
+    }
+    uint32_t Sk = dense ? (uint32_t)ilo : Stab[ilo];
+    uint64_t Xk;
+    { uint32_t t; Xk = x_of(Sk, lane_ppa(H, nw, Sk, t)); }
+    // certificate G: the closed-form supremum on the first segment m <= S_tot / 2 with alpha_m (m + 1) >= beta_m
+    float G;
+    {
+      int mlo = 0, mhi = mh;
+      const int csteps = mh > 0 ? 32 - __clz(mh) : 0;
+      const uint64_t C12 = 2 * C1;
+      for (int it = 0; it < csteps; ++it) {
+        const int mid = (mlo + mhi) >> 1;
+        uint32_t pam;
+        const uint32_t ppam = lane_ppa(H, nw, (uint32_t)mid, pam);
+        const uint32_t Qm = myWsm - (uint32_t)mid * pam + ppam;   // Q[m] = Wsm - PW[m]
+        const uint64_t alpha = C12 + Mtp * pam, beta = Mtp * ((uint64_t)Qm + myWb) + memb;
+        const bool peak_by = alpha * (uint64_t)(mid + 1) >= beta;
+        if (mlo < mhi) { if (peak_by) mhi = mid; else mlo = mid + 1; }
+      }
+      uint32_t pam;
+      const uint32_t ppam = lane_ppa(H, nw, (uint32_t)mlo, pam);
+      const uint32_t Qm = myWsm - (uint32_t)mlo * pam + ppam;
+      const float af = fmaf(Mtpf, (float)pam, C1f2), bf = fmaf(Mtpf, (float)Qm + Wbf, membf);
+      const float Sf = (float)mlo, hiS = fminf(Sf + 1.f, half);
+      const float sx = fminf(fmaxf(bf * rcp_approx(af), Sf), hiS);
+      const float x = fmaf(af, sx, bf);
+      G = bf == 0.f ? __int_as_float(0x7f800000) : sx * rcp_approx(x * x);
+    }
+    if (have && ok) {
+      if (st == DSTACK_ST_OK && !cold) {
+        // knee = the exact argmax over every attained width; when it is feasible (Eqs. 11-12: 2X <= S F) it is
+        // also the feasible argmax, else the feasible widths are scanned exactly
+        uint32_t Se = 0;
+        uint64_t Xe = 0;
+        if (F != 0 && 2 * Xk <= (uint64_t)Sk * F) { Se = Sk; Xe = Xk; }
+        else {   // (F = 0: no width is feasible; scanned with F = 1 exactly as the generic fast path does)
+          const uint64_t F1 = F == 0 ? 1ull : F;
+          if (mem_mode == 2) lane_scan_pa<2>(H, lmin, S_tot, C1, Mtp, base, myD, myWsm, F1, Se, Xe);
+          else lane_scan_pa<0>(H, lmin, S_tot, C1, Mtp, base, myD, myWsm, F1, Se, Xe);
+        }
+        if (Se == 0) {
+          st = DSTACK_ST_INFEASIBLE;   // b = 1 is feasible whenever any b is (O3)
+        } else if (b_hi >= 2 && !(score_f(Se, Xe) * 0.99975586f > G)) {
+          cold = true;   // b* = 1 not certified: the generic exact branch-and-bound decides
+        } else {
+          knee = lmin[Sk];
+          const uint32_t le = lmin[Se];
+          demand = le + (uint32_t)p.margin < (uint32_t)L ? le + (uint32_t)p.margin : (uint32_t)L;
+          if (a.dtab_rows) {   // d_j(1) = ceil(X(S(g), 1) / (S(g) M Delta)) at g = demand
+            const uint32_t Sg = Stab[demand];
+            uint32_t t;
+            const uint64_t Xg = Sg == Se ? Xe : x_of(Sg, lane_ppa(H, nw, Sg, t));
+            dslots = ceil_div_clamp16_fast(Xg, (uint64_t)Sg * M * (uint64_t)p.slot_us);
+          }
+        }
+      }
+    }
+#else
     // The f32 width scan runs on every lane, outside any lane-dependent branch: its branches on the width are then
     // provably warp-uniform (no reconvergence regions in the loop).  Lanes without a fast-path DNN scan their
     // (zero or partial) histogram row with their own parameters and drop the result.
@@ -859,6 +1041,7 @@ __global__ void __launch_bounds__(DSTACK_PLANE_WARPS * 32, DSTACK_PLANE_MINB) k_
         }
       }
     }
+#endif
     // ---- outputs of the lanes' DNNs (coalesced: lane j writes DNN kb + j) ----
     if (have && !cold) {
       const bool okst = st == DSTACK_ST_OK;

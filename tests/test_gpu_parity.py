@@ -838,3 +838,15 @@ def test_random_profiles_legs_parity(ds, leg):
         want = oracle.maxthr(pb, p, nthreads=8)
         assert np.array_equal(st.cpu().numpy(), want["status"])
         assert np.array_equal(served.cpu().numpy().astype(np.int64), want["served"])
+
+
+@pytest.mark.parametrize("S_tot", [1, 2, 7, 8, 9, 16, 17, 63, 149, 255])
+def test_knee_search_sm_counts_parity(ds, S_tot):
+    """k_prof_lane's a2/a3 searches (PA rows with PPA checkpoints every 8 widths, binary searches over the levels and
+    the certificate's segments) at SM counts around the checkpoint and word boundaries, with every width a level
+    (L = S_tot), coarse levels (L < S_tot) and repeated widths (L > S_tot), on adversarial random profiles."""
+    pb = random_profile_problem(40 + S_tot, S=60, S_tot=S_tot)
+    for L in sorted({S_tot, max(1, S_tot // 3), min(255, 2 * S_tot)}):
+        p = Params(L=L, S_tot=S_tot, ideal=0)
+        g, _ = run_gpu(ds, pb, p)
+        assert_parity(g, oracle.evaluate(pb, p, nthreads=8), ideal=False, where=f"L={L} S_tot={S_tot}")
