@@ -361,6 +361,10 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
   };
   if (active) next_static();
   const uint32_t pk = (g & 0xFFu) | ((bs & 0xFFu) << 8) | (dstar << 16);   // dstar <= 0xFFFF (u16 rows)
+  // the shortest run the fill may place for this DNN: d(b_lo) when a batch below b* is allowed, else d(b*)
+  // (d nondecreasing in b)
+  const int dlo = !active ? 0 : ((!hook_b_only && (int)bs - 1 >= b_lo) ? (int)dtab[lane * DSTACK_MAX_BATCH + b_lo - 1]
+                                                                        : (int)dstar);
   uint32_t *w32 = reinterpret_cast<uint32_t *>(sm.occ);
   // a candidate whose slice at t is too short for d(b_lo) stays too short at every later decision time
   // t' < blk: the slot that ended its slice never loses occupancy (or it was its own next static start)
@@ -375,7 +379,14 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     // static runs begun by t folded into free_at (inactive lanes: ns = nslots > t, no iteration)
     while (t >= ns) { free_at = max(free_at, ne); next_static(); }
     // eligible: not running at t (static or fill run), not blocked, fits at t
-    const bool elig = active && t >= max(free_at, blk) && occ_t + (int)g <= L;
+    bool elig = active && t >= max(free_at, blk) && occ_t + (int)g <= L;
+    // necessary for a placement (checked lane-parallel, so that most candidates that would be rejected never enter
+    // the serial loop): its shortest run [t, t + dlo) ends by its next own static start and fits at its last slot.
+    // Placements at t only raise occupancy, so a candidate failing here fails its serial test too.
+    {
+      const int xe = t + dlo;
+      elig = elig && xe <= ns && (dlo == 0 || (int)sm.occ[xe - 1] + (int)g <= L);
+    }
     // candidates in (runs so far, index) order; a placement raises occ[t], so re-test the rest in parallel
     const uint32_t prio = fill_order == 0 ? count : (fill_order == 1 ? g : dstar);
     uint32_t key = elig ? ((prio << 5) | (uint32_t)lane) : 0xFFFFFFFFu;
