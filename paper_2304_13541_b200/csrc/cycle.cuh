@@ -5,13 +5,13 @@
 // grant_j = min(k_j, max(0, L - sum_before)); the surplus split is Q16.16, floored.
 //
 // a5, Alg. 1 / Alg. 3 / Dynamic-schedule (§6.1): the session of
-// nslots = T/Delta slots is a shared-memory u8 occupancy array (levels <= 255).  Static jobs come in
-// EDF order from two warp min-reductions over the lanes' next repeats (deadline; then d(b*), index).
-// A window query is a ballot scan over 32-slot chunks: each lane derives the length of the run of
-// fitting slots ending (Start-Early) or starting (Start-Late) at its slot from the chunk's ballot
-// and the carried run, so one chunk costs two ballots.  The opportunistic fill walks decision times
-// kept in a bitmask, tests every DNN's eligibility in parallel (lane = DNN) and serves the eligible
-// ones in (runs so far, index) order by repeated min-reductions.
+// nslots = T/Delta slots is a shared-memory u8 occupancy array (levels <= 255), read as packed u32 words of 4 slots
+// (one word per lane: a 128-slot window per warp instruction).  Static jobs come in EDF order from one warp
+// min-reduction over a packed (deadline, d(b*), lane) key; Start-Early searches one window per step
+// (find_early_win), Start-Late jumps over the first blocking slot of the candidate run (find_late_packed).  The
+// opportunistic fill visits the decision times {0} u {run ends} (the next one is a min-reduction over the lanes' first
+// run end after t), tests every DNN's eligibility in parallel (lane = DNN; including a necessary fit test of its
+// shortest run) and serves the eligible ones in (runs so far, index) order by repeated min-reductions.
 #pragma once
 #include "common.cuh"
 #include "prof.cuh"
@@ -32,6 +32,13 @@ static __device__ unsigned long long g_cstats[16];   // per TU (instrumentation 
 #ifndef DSTACK_CYC_PACKED_MAX
 #define DSTACK_CYC_PACKED_MAX 124   // static runs up to this length use the packed-word searches (A/B switch; <= 124;
                                     // 0 -> 32-slot ballot chunks: k_cycle 11.87 -> 12.59 ms at config 3)
+#endif
+
+#ifndef DSTACK_CYC_EARLY_WIN
+#define DSTACK_CYC_EARLY_WIN 1   // 1: static Start-Early searches one 128-slot window per step (find_early_win)
+#endif
+#ifndef DSTACK_CYC_PRE_PTS
+#define DSTACK_CYC_PRE_PTS 1   // slots of the shortest run tested lane-parallel before the serial fill loop (1, 2 or 4)
 #endif
 
 constexpr uint16_t NONE16 = 0xFFFF;
@@ -137,6 +144,36 @@ __device__ __forceinline__ int find_early_packed(const uint8_t *occ, int rel, in
   }
   return -1;
 }
+// Start-Early over 128-slot windows for 4 <= d <= 124: the smallest feasible start s* >= s is s itself or x + 1 for a
+// blocking slot x (s* - 1 >= s infeasible while [s*, s* + d) is free forces s* - 1 to block).  With d >= 4 only
+// the last blocking slot of a lane's 4-slot word can open a gap of d, so one window costs a min-reduction for s,
+// then per lane that slot, the next blocking slot after its word (ballot + one shuffle), and a min-reduction over
+// the starts whose gap is known to reach d.  Otherwise the next window starts after the window's last blocking
+// slot (every start before it is infeasible).  Slots >= dl may hold stale bytes: every accepted start has s + d <= dl,
+// and a stale blocking slot >= dl only caps a gap at >= dl.
+__device__ __forceinline__ int find_early_win(const uint8_t *occ, int rel, int dl, int d, int g, int L, int lane) {
+  const uint32_t *w32 = reinterpret_cast<const uint32_t *>(occ);
+  const uint32_t th = (uint32_t)(L - g) * 0x01010101u;
+  int s = rel;
+  while (s + d <= dl) {
+    const int bt = s & ~3, mybase = bt + 4 * lane;
+    const uint32_t word = w32[(bt >> 2) + lane];   // padded array
+    const uint32_t bb = __vcmpgtu4(word, th) & ~bytes_below(s, mybase);   // blocking slots >= s
+    const uint32_t fbl = bb ? (uint32_t)(mybase + ((__ffs(bb) - 1) >> 3)) : 0xFFFFFFFFu;
+    const uint32_t first = __reduce_min_sync(FULL, fbl);
+    if (lane == 0) CSTAT(9, 1);
+    if (first >= (uint32_t)(s + d)) return s;   // none in the window: the gap is >= 125 > d
+    const uint32_t later = __ballot_sync(FULL, bb != 0u) & ~((2u << lane) - 1u);   // lanes above with a blocking slot
+    const uint32_t nbx = __shfl_sync(FULL, fbl, later ? __ffs(later) - 1 : 0);
+    const int c = bb ? mybase + ((31 - __clz(bb)) >> 3) + 1 : 0;   // after this word's last blocking slot
+    const bool feas = bb != 0u && c + d <= dl && (later ? (int)nbx >= c + d : c + d <= bt + 128);
+    const uint32_t best = __reduce_min_sync(FULL, feas ? (uint32_t)c : 0xFFFFFFFFu);
+    if (best != 0xFFFFFFFFu) return (int)best;
+    s = (int)__reduce_max_sync(FULL, (uint32_t)c);
+  }
+  return -1;
+}
+
 // Start-Late: largest feasible s in [rel, dl-d]; -1 if none.
 __device__ __forceinline__ int find_late_packed(const uint8_t *occ, int rel, int dl, int d, int g, int L, int lane) {
   const uint32_t *w32 = reinterpret_cast<const uint32_t *>(occ);
@@ -315,7 +352,8 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     int st;
     if (dj > dlv - rel) st = -1;
     else if (dj <= DSTACK_CYC_PACKED_MAX) st = (rj & 1) ? find_late_packed(sm.occ, rel, dlv, dj, gj, L, lane)
-                                      : find_early_packed(sm.occ, rel, dlv, dj, gj, L, lane);
+                                      : ((DSTACK_CYC_EARLY_WIN && dj >= 4) ? find_early_win(sm.occ, rel, dlv, dj, gj, L, lane)
+                                                                           : find_early_packed(sm.occ, rel, dlv, dj, gj, L, lane));
     else st = (rj & 1) ? find_late(sm.occ, rel, dlv, dj, gj, L, lane) : find_early(sm.occ, rel, dlv, dj, gj, L, lane);
     if (lane == 0) CSTAT(1, 1);
     int lv = gj, dd = dj;
@@ -386,6 +424,12 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
     {
       const int xe = t + dlo;
       elig = elig && xe <= ns && (dlo == 0 || (int)sm.occ[xe - 1] + (int)g <= L);
+#if DSTACK_CYC_PRE_PTS >= 2
+      elig = elig && (int)sm.occ[t + (dlo >> 1)] + (int)g <= L;   // dlo >= 1 here (xe - 1 >= t)
+#endif
+#if DSTACK_CYC_PRE_PTS >= 3
+      elig = elig && (int)sm.occ[t + (dlo >> 2)] + (int)g <= L && (int)sm.occ[t + ((3 * dlo) >> 2)] + (int)g <= L;
+#endif
     }
     // candidates in (runs so far, index) order; a placement raises occ[t], so re-test the rest in parallel
     const uint32_t prio = fill_order == 0 ? count : (fill_order == 1 ? g : dstar);
