@@ -465,16 +465,20 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
         kend = first_above(sm.occ, t, stop, L - gj, lane);
       }
       const int kslice = kend - t;
-      int bsel = 0;   // largest b in [b_lo, b*] with d(b) <= slice (d nondecreasing in b)
+      int bsel = 0, dsel = 0;   // largest b in [b_lo, b*] with d(b) <= slice (d nondecreasing in b), and d(b)
       const uint16_t *dj = dtab + j * DSTACK_MAX_BATCH;
       if (kslice >= dsj) {
-        bsel = bsj;
+        bsel = bsj; dsel = dsj;
       } else if (!hook_b_only && bsj - 1 >= b_lo) {
         for (int b0 = b_lo + 32 * ((bsj - 1 - b_lo) >> 5); b0 >= b_lo; b0 -= 32) {
           const int b = b0 + lane;
-          const bool ok = b < bsj && (int)dj[b - 1] <= kslice;
-          const uint32_t bal = __ballot_sync(FULL, ok);
-          if (bal) { bsel = b0 + 31 - __clz(bal); break; }
+          const int dv = b < bsj ? (int)dj[b - 1] : 0x7FFFFFFF;
+          const uint32_t bal = __ballot_sync(FULL, dv <= kslice);
+          if (bal) {
+            const int src = 31 - __clz(bal);
+            bsel = b0 + src; dsel = __shfl_sync(FULL, dv, src);
+            break;
+          }
         }
       }
       if (bsel == 0) {
@@ -482,10 +486,9 @@ __device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, 
         continue;
       }
       if (lane == 0) { CSTAT(5, 1); CSTAT(6, bsel != bsj); CSTAT(7, kslice < dsj); }
-      const int dsel = bsel == bsj ? dsj : (int)dj[bsel - 1];
       const int e = t + dsel;
       if (e <= bt + 128) {   // place inside the window: register word + write-through
-        const uint32_t add = ((uint32_t)gj * 0x01010101u) & lo_mask & bytes_below(e, mybase);
+        const uint32_t add = ((uint32_t)gj * 0x01010101u) & bytes_mask(t, e, mybase);
         if (add) { wv += add; w32[wi] = wv; }
         wvm += add;
       } else {

@@ -762,7 +762,9 @@ __global__ void __launch_bounds__(DSTACK_PLANE_WARPS * 32, DSTACK_PLANE_MINB) k_
   const int mh = S_tot >> 1;
   const float half = 0.5f * (float)S_tot;
   const int hwords = 32 * HS;
+#if !DSTACK_PLANE_SEARCH
   const bool all_valid = L == S_tot;   // every width is some level's S(l)
+#endif
   // groups of 32 DNNs from the work counter (one resident wave) or a grid stride over groups
   const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp, nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t g = warp_next_item(a.work_ctr, -1, gwarp, nwarps, lane); g * 32 < pb.num_dnn;
