@@ -135,6 +135,15 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.rows.append([x.strip() for x in line.split(",")])
 
+    def wait_first(self, timeout=10.0):
+        """Block until nvidia-smi has printed its first sample (its NVML start-up, which can take a second on a
+        fresh box and was seen to stall the GPU, then lies outside the timed region), at least 0.3 s."""
+        t0 = time.time()
+        time.sleep(0.3)
+        while self.proc is not None and not self.rows and time.time() - t0 < timeout:
+            time.sleep(0.05)
+        time.sleep(0.2)
+
     def stop(self):
         if self.proc is None:
             return None
@@ -415,7 +424,7 @@ def run_native(args, rank, world, local):
         dist.barrier()
     torch.cuda.synchronize()
     if sampler:
-        sampler.start(); time.sleep(0.3)
+        sampler.start(); sampler.wait_first()
     t_start = torch.cuda.Event(enable_timing=True); t_end = torch.cuda.Event(enable_timing=True)
     ds.profile_start(args.steps)
     t_start.record(stream)
@@ -1016,7 +1025,7 @@ def run_sim(args, rank, world, local):
         dist.barrier()
     sampler = ClockSampler(range(world)) if rank == 0 else None
     if sampler:
-        sampler.start(); time.sleep(0.3)
+        sampler.start(); sampler.wait_first()
     launches = 0
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > L2 (126 MB)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -10,7 +10,7 @@ python tools/ncu_counters.py gpurun_out/m3_counters_legs.csv 1000000 gpurun_out/
 cp gpurun_out/m3_counters.json profiles/counters.json
 python bench.py > gpurun_out/m3_bench_c3.json 2> gpurun_out/m3_bench_c3.err; echo c3 rc=$?
 for c in 2 4 1; do python bench.py --config $c > gpurun_out/m3_bench_c$c.json 2> gpurun_out/m3_bench_c$c.err; echo c$c rc=$?; done
-python bench.py --config 5 --steps 3 --warmup 3 > gpurun_out/m3_bench_c5.json 2> gpurun_out/m3_bench_c5.err; echo c5 rc=$?
+python bench.py --config 5 --steps 3 --warmup 3 > gpurun_out/m3_bench_c5.json 2> gpurun_out/m3_bench_c5.err; echo c5 rc=$?; python bench.py --config 5 --steps 3 --warmup 3 > gpurun_out/m3_bench_c5b.json 2>> gpurun_out/m3_bench_c5.err
 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/m3_ref.json 2> gpurun_out/m3_ref.err; echo ref rc=$?
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/m3_launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-compare --no-below-knee --no-knee-probe --no-cluster --no-maxthr > gpurun_out/m3_launches_bench.log 2>&1
 ncu --set full --import-source on --clock-control none -k 'regex:k_prof_lane|k_cycle' -c 2 -o gpurun_out/m3_full python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-compare --no-below-knee --no-knee-probe --no-cluster --no-maxthr > gpurun_out/m3_full_bench.log 2>&1
