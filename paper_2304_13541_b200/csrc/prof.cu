@@ -27,7 +27,7 @@ __host__ __device__ inline size_t prof_warp_bytes(int S_tot) {
 #define DSTACK_PROF_DYN 1   // 1: k_prof_fast takes groups of 32 DNNs from a work counter (A/B switch)
 #endif
 #ifndef DSTACK_PROF_ROWS_U
-#define DSTACK_PROF_ROWS_U 6   // rows per lane in flight in the row pass (A/B at config 3: 2 -> 10.86, 4 -> 11.41, 6 -> 10.44, 8 -> 10.71 ms)
+#define DSTACK_PROF_ROWS_U 7   // rows per lane in flight in the row pass (A/B at config 3, k_prof_lane ms: 4 -> 5.35, 5 -> 4.87, 6 -> 4.70, 7 -> 4.66, 8 -> 4.76)
 #endif
 #ifndef DSTACK_PROF_FAST
 #define DSTACK_PROF_FAST 1   // 0: every launch takes the generic kernel (A/B switch)
