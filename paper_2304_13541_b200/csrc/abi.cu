@@ -59,7 +59,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 // workspace layout: [agg partials | counters | d_j(b) rows u16[num_dnn][64] | RT u32[num_dnn] | D u64[num_dnn] |
 //                    d_j(b*) u16[num_dnn] | cold-DNN queue u32[num_dnn + 2] | ideal]
 struct WsLayout {
-  size_t ctr, dtab, rt, d, dst, cold, ideal, end;
+  size_t ctr, dtab, rt, d, dst, cold, bigq, ideal, end;
 };
 WsLayout ws_layout(const dstack_problem_t *pb, const dstack_params_t *p) {
   WsLayout w;
@@ -70,7 +70,8 @@ WsLayout ws_layout(const dstack_problem_t *pb, const dstack_params_t *p) {
   w.d = w.rt + align256(nd * 4);
   w.dst = w.d + align256(nd * 8);
   w.cold = w.dst + align256(nd * 2);
-  w.ideal = w.cold + align256((nd + 2) * 4);
+  w.bigq = w.cold + align256((nd + 2) * 4);   // k_cycle's queue of long sessions (count, unused, scenarios)
+  w.ideal = w.bigq + align256(((size_t)(pb->num_scen > 0 ? pb->num_scen : 0) + 2) * 4);
   w.end = w.ideal + ((p->flags & DSTACK_FLAG_IDEAL) ? align256(ideal_ws_bytes(pb->num_rows, pb->num_scen)) : 0);
   return w;
 }
@@ -261,6 +262,7 @@ static int schedule_impl(const dstack_problem_t *pb, const dstack_params_t *p, c
   c.dtab_rows = (uint16_t *)((char *)ws + ws_layout(pb, p).dtab);
   c.dstar = (uint16_t *)((char *)ws + ws_layout(pb, p).dst);
   c.work_ctr = (uint32_t *)((char *)ws + ws_layout(pb, p).ctr);
+  c.big_q = (uint32_t *)((char *)ws + ws_layout(pb, p).bigq);
   if (pre_ws) { c.ws_RT = (const uint32_t *)((char *)ws + ws_layout(pb, p).rt); c.ws_D = (const uint64_t *)((char *)ws + ws_layout(pb, p).d); }
   int rc = launch_cycle(c, s, &g_launches);
   if (rc) return rc;

@@ -1,5 +1,7 @@
 // cycle.cu -- standalone a4 (dstack_wmaxmin) and a5 (dstack_schedule_cycle) kernels, warp per scenario.
 // Device code in cycle.cuh; the fused path (a1-a5 in one kernel) is fused.cu.
+#include <type_traits>
+
 #include "cycle.cuh"
 #include "kernels.cuh"
 #include "prof.cuh"
@@ -39,19 +41,37 @@ __global__ void __launch_bounds__(256) k_wmaxmin(int32_t num_scen, const int32_t
 #ifndef DSTACK_CYC_MINB
 #define DSTACK_CYC_MINB 4
 #endif
+#ifndef DSTACK_CYC_SMALL
+#define DSTACK_CYC_SMALL 1   // 1: the eval / schedule path runs the small-buffer pass first (A/B switch)
+#endif
+#ifndef DSTACK_CYC_SMALL_MINB
+#define DSTACK_CYC_SMALL_MINB 5   // small-buffer pass: resident blocks per SM (40 warps, 48 registers)
+#endif
+// Small-buffer pass: 1.6 KB of session buffers per warp instead of 6.3 KB, so 40 warps fit an SM (A/B at config 3,
+// where every session qualifies: 9.38 -> 9.23 ms); a longer session is queued for the full-buffer pass.
+constexpr int CYC_SMALL_SLOTS = 1024, CYC_SMALL_JOBS = 128;
+using CycSmemSmall = CycSmemT<CYC_SMALL_SLOTS, CYC_SMALL_JOBS>;
+
 // BK: F1 below-knee fallback compiled in (DSTACK_FLAG_BELOW_KNEE); the default instantiation has no trace of it.
-template <bool BK>
-__global__ void __launch_bounds__(CYC_WARPS * 32, BK ? DSTACK_CYC_BK_MINB : DSTACK_CYC_MINB) k_cycle(const __grid_constant__ CycArgs a) {
+// SMALL: the small-buffer pass (sessions over CYC_SMALL_SLOTS slots or CYC_SMALL_JOBS static jobs go to a.big_q);
+// !SMALL with a.big_q set: the full-buffer pass over the queued scenarios only.
+template <bool BK, bool SMALL>
+__global__ void __launch_bounds__(CYC_WARPS * 32, BK ? DSTACK_CYC_BK_MINB : (SMALL ? DSTACK_CYC_SMALL_MINB : DSTACK_CYC_MINB))
+k_cycle(const __grid_constant__ CycArgs a) {
+  using SM = typename std::conditional<SMALL, CycSmemSmall, CycSmem>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  CycSmem &sm = reinterpret_cast<CycSmem *>(smem_raw)[warp];
+  SM &sm = reinterpret_cast<SM *>(smem_raw)[warp];
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int32_t L = a.p.L, slot = a.p.slot_us, b_lo = a.p.b_min;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   // scenario order: a work counter (one resident wave of warps, each takes the next scenario when it finishes one)
-  // or a grid stride
+  // or a grid stride; the queued pass walks the queue instead
+  const bool queued = !SMALL && a.big_q != nullptr;
+  const int64_t nitems = queued ? (int64_t)__ldcg(a.big_q) : (int64_t)a.pb.num_scen;
   auto fetch = [&](int64_t prev) -> int64_t { return warp_next_item(a.work_ctr, prev, gwarp, nwarps, lane); };
-  for (int64_t s = fetch(-1); s < a.pb.num_scen; s = fetch(s)) {
+  for (int64_t item = fetch(-1); item < nitems; item = fetch(item)) {
+    const int64_t s = queued ? (int64_t)__ldcg(a.big_q + 2 + item) : item;
     const int32_t k0 = a.pb.scen_dnn_off[s], nd = a.pb.scen_dnn_off[s + 1] - k0;
     uint8_t sst = DSTACK_ST_OK;
     uint32_t T = 0;
@@ -97,6 +117,11 @@ __global__ void __launch_bounds__(CYC_WARPS * 32, BK ? DSTACK_CYC_BK_MINB : DSTA
       if (active) { sl = slo / (uint32_t)slot; rep = (uint32_t)nslots / sl; }
       const uint32_t njobs = __reduce_add_sync(FULL, rep);
       if (nslots > DSTACK_MAX_SLOTS || njobs > DSTACK_MAX_JOBS) { sst = DSTACK_ST_INVALID; T = 0; }
+      else if (SMALL && (nslots > CYC_SMALL_SLOTS || njobs > CYC_SMALL_JOBS)) {   // to the full-buffer pass
+        if (lane == 0) a.big_q[2 + atomicAdd(a.big_q, 1u)] = (uint32_t)s;
+        __syncwarp();
+        continue;
+      }
     }
     if (sst == DSTACK_ST_OK) {
       // runtimes d_j(b) = ceil(X(g_j, b) / (S(g_j) M Delta)), b in [b_lo, b*_j], one u16 row per DNN.
@@ -187,31 +212,54 @@ int launch_wmaxmin(int32_t num_scen, const int32_t *off, int32_t L, const uint16
 int launch_cycle(const CycArgs &a, cudaStream_t s, int *launches) {
   if (a.pb.num_scen <= 0) return 0;
   const size_t smem = sizeof(CycSmem) * CYC_WARPS;
+  if (DSTACK_CYC_SMALL && DSTACK_CYC_DYN && a.work_ctr && a.big_q && !(a.p.flags & DSTACK_FLAG_BELOW_KNEE)) {
+    // small-buffer pass over every scenario, then the full-buffer pass over the queued long sessions (usually none:
+    // its warps read an empty queue and exit)
+    CycArgs b = a;
+    b.big_q = a.big_q;
+    if (cudaMemsetAsync(a.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess ||
+        cudaMemsetAsync(a.big_q, 0, 2 * sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
+    const size_t smem_s = sizeof(CycSmemSmall) * CYC_WARPS;
+    const int64_t blocks = (a.pb.num_scen + CYC_WARPS - 1) / CYC_WARPS;
+    const int64_t wave_s = (int64_t)num_sms() * DSTACK_CYC_SMALL_MINB;
+    cudaFuncSetAttribute(k_cycle<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s);
+    k_cycle<false, true><<<(unsigned)(blocks < wave_s ? blocks : wave_s), CYC_WARPS * 32, smem_s, s>>>(b);
+    if (cudaMemsetAsync(a.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
+    const int64_t wave = (int64_t)num_sms() * DSTACK_CYC_MINB;
+    cudaFuncSetAttribute(k_cycle<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_cycle<false, false><<<(unsigned)(blocks < wave ? blocks : wave), CYC_WARPS * 32, smem, s>>>(b);
+    *launches += 2;
+    return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;
+  }
   int64_t blocks = (a.pb.num_scen + CYC_WARPS - 1) / CYC_WARPS;
   const int64_t cap = (int64_t)num_sms() * DSTACK_CYC_GRID;
   if (blocks > cap) blocks = cap;
   if (a.p.flags & DSTACK_FLAG_BELOW_KNEE) {
     CycArgs b = a;
+    b.big_q = nullptr;
     int64_t bk_blocks = blocks < (int64_t)num_sms() * DSTACK_CYC_BK_GRID ? blocks : (int64_t)num_sms() * DSTACK_CYC_BK_GRID;
-    cudaFuncSetAttribute(k_cycle<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_cycle<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (DSTACK_CYC_DYN && b.work_ctr) {   // retries make F1 sessions very uneven: one resident wave pulling scenarios
       if (cudaMemsetAsync(b.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
-      bk_blocks = resident_wave(k_cycle<true>, CYC_WARPS * 32, smem, blocks);
+      bk_blocks = resident_wave(k_cycle<true, false>, CYC_WARPS * 32, smem, blocks);
     } else {
       b.work_ctr = nullptr;
     }
-    k_cycle<true><<<(unsigned)bk_blocks, CYC_WARPS * 32, smem, s>>>(b);
+    k_cycle<true, false><<<(unsigned)bk_blocks, CYC_WARPS * 32, smem, s>>>(b);
   } else if (DSTACK_CYC_DYN && a.work_ctr) {
     // one resident wave (DSTACK_CYC_MINB blocks per SM) pulling scenarios from the work counter
     if (cudaMemsetAsync(a.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
     const int64_t wave = (int64_t)num_sms() * DSTACK_CYC_MINB;
-    cudaFuncSetAttribute(k_cycle<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_cycle<false><<<(unsigned)(blocks < wave ? blocks : wave), CYC_WARPS * 32, smem, s>>>(a);
+    CycArgs b = a;
+    b.big_q = nullptr;
+    cudaFuncSetAttribute(k_cycle<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_cycle<false, false><<<(unsigned)(blocks < wave ? blocks : wave), CYC_WARPS * 32, smem, s>>>(b);
   } else {
     CycArgs b = a;
     b.work_ctr = nullptr;
-    cudaFuncSetAttribute(k_cycle<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_cycle<false><<<(unsigned)blocks, CYC_WARPS * 32, smem, s>>>(b);
+    b.big_q = nullptr;
+    cudaFuncSetAttribute(k_cycle<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_cycle<false, false><<<(unsigned)blocks, CYC_WARPS * 32, smem, s>>>(b);
   }
   ++*launches;
   return cudaGetLastError() == cudaSuccess ? 0 : DSTACK_ELAUNCH;

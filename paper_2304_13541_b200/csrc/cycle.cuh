@@ -57,10 +57,13 @@ struct BelowKnee {
 };
 
 
-struct CycSmem {
-  uint8_t occ[DSTACK_MAX_SLOTS + 128];   // + one register window of padding (never read as session slots)
-  uint32_t sr[DSTACK_MAX_JOBS];   // static job (j, r): start | run slots << 16, or NONE32 (miss)
+// one warp's session buffers: SLOTS >= nslots and JOBS >= the session's static jobs
+template <int SLOTS, int JOBS>
+struct CycSmemT {
+  uint8_t occ[SLOTS + 128];   // + one register window of padding (never read as session slots)
+  uint32_t sr[JOBS];          // static job (j, r): start | run slots << 16, or NONE32 (miss)
 };
+using CycSmem = CycSmemT<DSTACK_MAX_SLOTS, DSTACK_MAX_JOBS>;
 
 // bytes of a lane's 4-slot word (first slot `base`) below slot x
 __device__ __forceinline__ uint32_t bytes_below(int x, int base) {
@@ -313,7 +316,8 @@ __device__ __forceinline__ uint64_t pack_run(uint32_t j, uint32_t t, uint32_t d,
   return ((uint64_t)j << 56) | ((uint64_t)t << 32) | ((uint64_t)d << 8) | b;
 }
 
-__device__ __forceinline__ CycRes cycle_core(CycSmem &sm, const uint16_t *dtab, int lane, bool active, uint32_t g,
+template <class SM>
+__device__ __forceinline__ CycRes cycle_core(SM &sm, const uint16_t *dtab, int lane, bool active, uint32_t g,
                                             uint32_t bs, uint32_t sl, uint32_t rep, int32_t nslots, int32_t L,
                                             int32_t b_lo, bool hook_b_only, uint32_t &runs, uint32_t &served,
                                             uint32_t count0 = 0, uint64_t *fill_log = nullptr, uint32_t fill_cap = 0,

@@ -59,6 +59,8 @@ struct CycArgs {
   const uint32_t *ws_RT;   // non-NULL => dtab_rows / dstar already hold d_j(b) at g = demand (from k_prof)
   const uint64_t *ws_D;
   uint32_t *work_ctr;      // workspace word: k_cycle's scenario counter (NULL: grid stride)
+  uint32_t *big_q;         // workspace: [count, unused, scenario...] of the sessions too long for the small-buffer
+                           // pass (NULL: one full-buffer pass)
 };
 
 constexpr int64_t SIM_MAX_WARPS = 148 * 32;   // persistent-grid cap (sizes the fill-run logs)

@@ -14,8 +14,8 @@ from collections import defaultdict
 SLOTS = (("k_prof", "k_prof"), ("k_wmaxmin", "k_wmaxmin"), ("k_cycle", "k_cycle"), ("k_agg", "k_agg"),
          ("k_ideal", "k_ideal"))
 # the next-row legs' kernels (bench.py compare / below_knee / knee_probe / cluster legs), counted in a separate run
-LEG_SLOTS = (("k_compare", "k_compare"), ("k_cluster", "k_cluster"), ("k_cycle<1>", "k_cycle_bk"),
-             ("k_cycle<true>", "k_cycle_bk"), ("k_prof<0>", "k_knee_probe"))
+LEG_SLOTS = (("k_compare", "k_compare"), ("k_cluster", "k_cluster"), ("k_cycle<1,", "k_cycle_bk"), ("k_cycle<1>", "k_cycle_bk"),
+             ("k_cycle<true,", "k_cycle_bk"), ("k_cycle<true>", "k_cycle_bk"), ("k_prof<0>", "k_knee_probe"))
 
 
 def slot_of(name, legs=False):
