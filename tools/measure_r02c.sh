@@ -4,7 +4,7 @@
 set -x
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/m3_smoke.log 2>&1; echo smoke rc=$?
 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/m3_counters.csv -k regex:k_ python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-compare --no-below-knee --no-knee-probe --no-cluster --no-maxthr > gpurun_out/m3_counters_bench.log 2>&1
-python tools/ncu_counters.py gpurun_out/m3_counters.csv 1000000 gpurun_out/m3_counters.json "r02 final (search a2/a3, fill prefilter, window Start-Early)"
+python tools/ncu_counters.py gpurun_out/m3_counters.csv 1000000 gpurun_out/m3_counters.json "r02 final (search a2/a3, fill prefilter, window Start-Early, two-pass k_cycle)"
 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/m3_counters_legs.csv -k 'regex:k_compare|k_cluster|k_cycle|k_prof' python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-maxthr > gpurun_out/m3_counters_legs_bench.log 2>&1
 python tools/ncu_counters.py gpurun_out/m3_counters_legs.csv 1000000 gpurun_out/m3_counters.json "r02 final, next-row legs" --legs
 cp gpurun_out/m3_counters.json profiles/counters.json
