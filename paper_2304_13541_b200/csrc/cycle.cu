@@ -44,6 +44,9 @@ __global__ void __launch_bounds__(256) k_wmaxmin(int32_t num_scen, const int32_t
 #ifndef DSTACK_CYC_SMALL
 #define DSTACK_CYC_SMALL 1   // 1: the eval / schedule path runs the small-buffer pass first (A/B switch)
 #endif
+#ifndef DSTACK_CYC_SMALL_WARPS
+#define DSTACK_CYC_SMALL_WARPS 8   // small-buffer pass: warps per block
+#endif
 #ifndef DSTACK_CYC_SMALL_MINB
 #define DSTACK_CYC_SMALL_MINB 5   // small-buffer pass: resident blocks per SM (40 warps, 48 registers)
 #endif
@@ -56,7 +59,8 @@ using CycSmemSmall = CycSmemT<CYC_SMALL_SLOTS, CYC_SMALL_JOBS>;
 // SMALL: the small-buffer pass (sessions over CYC_SMALL_SLOTS slots or CYC_SMALL_JOBS static jobs go to a.big_q);
 // !SMALL with a.big_q set: the full-buffer pass over the queued scenarios only.
 template <bool BK, bool SMALL>
-__global__ void __launch_bounds__(CYC_WARPS * 32, BK ? DSTACK_CYC_BK_MINB : (SMALL ? DSTACK_CYC_SMALL_MINB : DSTACK_CYC_MINB))
+__global__ void __launch_bounds__((SMALL ? DSTACK_CYC_SMALL_WARPS : CYC_WARPS) * 32,
+                                  BK ? DSTACK_CYC_BK_MINB : (SMALL ? DSTACK_CYC_SMALL_MINB : DSTACK_CYC_MINB))
 k_cycle(const __grid_constant__ CycArgs a) {
   using SM = typename std::conditional<SMALL, CycSmemSmall, CycSmem>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -219,11 +223,12 @@ int launch_cycle(const CycArgs &a, cudaStream_t s, int *launches) {
     b.big_q = a.big_q;
     if (cudaMemsetAsync(a.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess ||
         cudaMemsetAsync(a.big_q, 0, 2 * sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
-    const size_t smem_s = sizeof(CycSmemSmall) * CYC_WARPS;
+    const size_t smem_s = sizeof(CycSmemSmall) * DSTACK_CYC_SMALL_WARPS;
+    const int64_t blocks_s = (a.pb.num_scen + DSTACK_CYC_SMALL_WARPS - 1) / DSTACK_CYC_SMALL_WARPS;
     const int64_t blocks = (a.pb.num_scen + CYC_WARPS - 1) / CYC_WARPS;
     const int64_t wave_s = (int64_t)num_sms() * DSTACK_CYC_SMALL_MINB;
     cudaFuncSetAttribute(k_cycle<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s);
-    k_cycle<false, true><<<(unsigned)(blocks < wave_s ? blocks : wave_s), CYC_WARPS * 32, smem_s, s>>>(b);
+    k_cycle<false, true><<<(unsigned)(blocks_s < wave_s ? blocks_s : wave_s), DSTACK_CYC_SMALL_WARPS * 32, smem_s, s>>>(b);
     if (cudaMemsetAsync(a.work_ctr, 0, sizeof(uint32_t), s) != cudaSuccess) return DSTACK_ELAUNCH;
     const int64_t wave = (int64_t)num_sms() * DSTACK_CYC_MINB;
     cudaFuncSetAttribute(k_cycle<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
